@@ -1,0 +1,398 @@
+#!/usr/bin/env python
+"""Benchmark of the Meerkat hot path on B200 (BASELINE.json metric:
+"edge updates/sec (insert+delete) and dynamic-SSSP ms/batch").
+
+Workload (BASELINE config 3): R-MAT scale 24, edge factor 16,
+Graph500 initiator, scrambled ids, w ~ U{1..64}; the base graph is E minus the
+held-out insert batches; the source is R-MAT's hub.  One STEP = the whole hot
+path over one batch pair:
+
+    insert_batch(100K held-out edges) -> sssp_incremental -> bfs_incremental
+    delete_batch(100K present edges)  -> sssp_decremental -> bfs_decremental
+
+value = 200K edge updates / device time of the step (inputs resident in HBM),
+with per-call times reported beside it.  L2 is flushed (256 MiB write) between
+timed steps, outside the timed intervals.  `e2e` repeats the step through the
+C ABI with pinned HOST batch arrays (staged by the library inside each call)
+and reads the insert/delete counts back to the host.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "edge updates/sec (insert+delete) and dynamic-SSSP ms/batch at 1/2/4/8 B200"
+BATCH_SEED_BASE = 3
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--scale", type=int, default=24)
+    p.add_argument("--ef", type=int, default=16)
+    p.add_argument("--batch", type=int, default=100_000)
+    p.add_argument("--lf", type=float, default=0.7)
+    p.add_argument("--no-hashing", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-scale", type=int, default=20, help="R-MAT scale of the oracle's bounded sample")
+    p.add_argument("--cpu-steps", type=int, default=2)
+    p.add_argument("--json-out", default=None)
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------ distributed plumbing
+
+def dist_init(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allreduce_max(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """SM clock and clock-event (throttle) reasons sampled every 5 ms via NVML during the timed region."""
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap",
+               0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.stop_flag = threading.Event()
+        self.h = None
+
+    def start(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            idx = self.device
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            if vis:
+                try:
+                    idx = int(vis.split(",")[self.device])
+                except ValueError:
+                    pass
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.nv = pynvml
+            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+            self.h = None
+            return
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def _run(self):
+        nv = self.nv
+        while not self.stop_flag.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.rows.append((sm, rs))
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def stop(self):
+        if self.h is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        self.stop_flag.set()
+        self.t.join(timeout=2)
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({name for _, rs in self.rows for bit, name in self.REASONS.items() if rs & bit})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": self.max_sm, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ workload
+
+def make_workload(args, n_batches, rank=0):
+    import synth
+    t0 = time.time()
+    W = synth.rmat_dynamic(args.scale, args.ef, batch=args.batch, n_ins=n_batches, n_del=n_batches,
+                           seed_batch=BATCH_SEED_BASE + 1000 * rank)
+    return W, time.time() - t0
+
+
+def cpu_baseline(args, steps):
+    """The oracle as it stands, on a bounded sample of the same workload recipe (R-MAT at
+    --cpu-scale, same generator, same batch size): per step it applies an insert batch and a
+    delete batch and recomputes SSSP + BFS from scratch after each (the oracle has no dynamic
+    algorithm)."""
+    import oracle
+    import synth
+    W = synth.rmat_dynamic(args.cpu_scale, args.ef, batch=args.batch, n_ins=steps, n_del=steps,
+                           seed_batch=BATCH_SEED_BASE)
+    o = oracle.OracleGraph(W.vertex_n)
+    o.insert(*W.base)
+    t0 = time.perf_counter()
+    for i in range(steps):
+        o.insert(*W.inserts[i]); o.sssp(W.source); o.bfs(W.source)
+        o.delete(W.deletes[i][0], W.deletes[i][1]); o.sssp(W.source); o.bfs(W.source)
+    dt = time.perf_counter() - t0
+    return {"value": 2 * args.batch * steps / dt, "unit": "edges/s", "cores": 1, "kind": "oracle",
+            "sample": (f"oracle (single-threaded C) on R-MAT scale {args.cpu_scale} ef {args.ef} "
+                       f"(same recipe as the workload, 1/{2 ** (args.scale - args.cpu_scale)} of its vertices), "
+                       f"{steps} step(s) of insert {args.batch} + delete {args.batch} edges, each followed by "
+                       f"from-scratch SSSP + BFS; {dt:.1f} s"),
+            "seconds": dt}
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    t_all = time.time()
+    for _ in range(args.warmup):
+        pass   # the oracle has no warm state worth warming; bounded sample only
+    cb = cpu_baseline(args, max(1, min(args.steps, args.cpu_steps)))
+    line = {"metric": METRIC, "value": cb["value"], "unit": "edges/s", "n_gpus": 0, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * cb["seconds"] / max(1, min(args.steps, args.cpu_steps)),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"rmat-s{args.cpu_scale}-ef{args.ef} sample of rmat-s{args.scale}-ef{args.ef}",
+                       "batch": args.batch},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": cb["value"], "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": time.time() - t_all}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+
+def run_ours(args, ws, rank, local):
+    import torch
+    from paper_2305_17813_b200 import Graph
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    K, Wm = args.steps, args.warmup
+    W, gen_s = make_workload(args, K + Wm, rank)
+    V = W.vertex_n
+    stream = torch.cuda.current_stream(dev)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.uint32).view(np.int32)).to(dev)
+    bs, bd, bw = W.base
+    hints = np.bincount(bs, minlength=V).astype(np.uint32)
+    g = Graph(V, weighted=True, hashing=not args.no_hashing, load_factor=args.lf, degree_hints=T(hints),
+              device=local, stream=stream)
+    base_t = (T(bs), T(bd), T(bw))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    n_base = g.insert(*base_t)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    bulk_ms = e0.elapsed_time(e1)
+    del base_t
+    t_create0 = time.time()
+    sp = g.sssp(W.source)
+    bf = g.bfs(W.source)
+    torch.cuda.synchronize()
+    ins = [tuple(T(x) for x in b) for b in W.inserts]
+    dels = [tuple(T(x) for x in b[:2]) for b in W.deletes]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    names = ["insert", "sssp_inc", "bfs_inc", "delete", "sssp_dec", "bfs_dec"]
+
+    def step(i, evs):
+        s, d, w = ins[i]
+        evs[0].record(stream)
+        g.insert(s, d, w, count=False)
+        evs[1].record(stream)
+        sp.incremental(s, d, w)
+        evs[2].record(stream)
+        bf.incremental(s, d)
+        evs[3].record(stream)
+        s, d = dels[i]
+        g.delete(s, d, count=False)
+        evs[4].record(stream)
+        sp.decremental(s, d)
+        evs[5].record(stream)
+        bf.decremental(s, d)
+        evs[6].record(stream)
+
+    for i in range(Wm):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
+        step(i, evs)
+        flush.zero_()
+    torch.cuda.synchronize()
+    g.sync()
+    st0 = g.stats()
+    per_call = {n: [] for n in names}
+    tstats = {"sssp_dec": [], "bfs_dec": [], "sssp_inc": [], "bfs_inc": []}
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier(ws)
+    torch.cuda.synchronize()
+    total_ms = 0.0
+    for k in range(K):
+        i = Wm + k
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
+        step(i, evs)
+        evs[6].synchronize()
+        for j, n in enumerate(names):
+            per_call[n].append(evs[j].elapsed_time(evs[j + 1]))
+        total_ms += evs[0].elapsed_time(evs[6])
+        # per-call algorithmic bytes of the tree kernels (device counters, read outside the intervals)
+        tstats["sssp_dec"].append(sp.stats())
+        tstats["bfs_dec"].append(bf.stats())
+        flush.zero_()
+    torch.cuda.synchronize()
+    barrier(ws)
+    clk = clocks.stop()
+    g.sync()
+    st1 = g.stats()
+    total_ms = allreduce_max(total_ms, ws)
+    ms_per_step = total_ms / K
+    edges = 2 * args.batch * K * ws
+    value = edges / (total_ms / 1e3)
+
+    # the dominant call and its roofline (HBM-bound: slab streaming / pointer chasing)
+    mean = {n: float(np.mean(v)) for n, v in per_call.items()}
+    dom = max(mean, key=mean.get)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = peaks.get("hbm_gbs") or 6650.0
+    peak_src = "measured" if peaks.get("hbm_gbs") else "fallback"
+    roof = None
+    if dom in tstats and tstats[dom]:
+        ab = float(np.mean([s["alg_bytes"] for s in tstats[dom]]))
+        ach = ab / (mean[dom] * 1e-3) / 1e9
+        traffic = None
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+            traffic = tr.get(dom)
+        except Exception:
+            pass
+        roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                "traffic": traffic, "alg_bytes_per_launch": ab, "peak_source": peak_src}
+    tree_detail = {n: {k: float(np.mean([s[k] for s in v])) for k in
+                       ("rounds", "propagate_rounds", "invalidated", "frontier_edges", "scan_slabs", "slabs_read",
+                        "alg_bytes")} for n, v in tstats.items() if v}
+
+    # ---------------- e2e through the C ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.uint32).view(np.int32)).pin_memory()
+        hi = [tuple(pin(x) for x in b) for b in W.inserts[Wm:Wm + K]]
+        hd = [tuple(pin(x) for x in b[:2]) for b in W.deletes[Wm:Wm + K]]
+        # the timed steps above already applied these batches: undo them first (not timed)
+        for k in reversed(range(K)):
+            g.insert(*[T(x) for x in W.deletes[Wm + k]], count=False)
+            g.delete(*[T(x) for x in W.inserts[Wm + k][:2]], count=False)
+        sp.recompute(); bf.recompute()
+        g.sync()
+        e_ms = 0.0
+        barrier(ws)
+        for k in range(K):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            s, d, w = hi[k]
+            n_i = g.insert(s, d, w, count=True)          # H2D staged inside the call, count read back (D2H)
+            sp.incremental(s, d, w)
+            bf.incremental(s, d)
+            s, d = hd[k]
+            n_d = g.delete(s, d, count=True)
+            sp.decremental(s, d)
+            bf.decremental(s, d)
+            b.record(stream)
+            b.synchronize()
+            e_ms += a.elapsed_time(b)
+            flush.zero_()
+        e_ms = allreduce_max(e_ms, ws)
+        n = args.batch
+        e2e = {"value": edges / (e_ms / 1e3), "unit": "edges/s",
+               "h2d_bytes_per_step": n * 4 * (3 + 3 + 2 + 2 + 2 + 2), "d2h_bytes_per_step": 2 * 64,
+               "ms_per_step": e_ms / K}
+
+    cb = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cb = cpu_baseline(args, args.cpu_steps)
+        cb = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    gs = g.stats()
+    line = {
+        "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": ws, "steps": K, "warmup": Wm,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u64", "data": "synthetic",
+        "config": {"workload": f"rmat-s{args.scale}-ef{args.ef} dynamic SSSP+BFS, {args.batch}-edge insert+delete "
+                               f"batches (BASELINE config 3)",
+                   "vertices": V, "edges": int(n_base), "batch": args.batch, "source": W.source,
+                   "hashing": not args.no_hashing, "load_factor": args.lf,
+                   "parallelism": "single GPU" if ws == 1 else f"{ws} independent replicas",
+                   "l2": "flushed between timed steps (256 MiB write, outside the intervals); store > L2"},
+        "update_edges_per_s": 2 * args.batch / ((mean["insert"] + mean["delete"]) / 1e3),
+        "insert_edges_per_s": args.batch / (mean["insert"] / 1e3),
+        "delete_edges_per_s": args.batch / (mean["delete"] / 1e3),
+        "sssp_ms_per_batch": {"incremental": mean["sssp_inc"], "decremental": mean["sssp_dec"]},
+        "bfs_ms_per_batch": {"incremental": mean["bfs_inc"], "decremental": mean["bfs_dec"]},
+        "per_call_ms": mean,
+        "bulk_build": {"edges": int(n_base), "ms": bulk_ms, "edges_per_s": n_base / (bulk_ms / 1e3)},
+        "tree_calls": tree_detail,
+        "roofline": roof,
+        "cpu_baseline": cb,
+        "e2e": e2e,
+        "gpu_launches": int(st1["kernel_launches"] - st0["kernel_launches"]),
+        "clocks": clk,
+        "store": {k: gs[k] for k in ("head_slabs", "buckets", "pool_used", "bytes_device")},
+        "generate_s": gen_s,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+        if args.json_out:
+            with open(args.json_out, "w") as f:
+                json.dump(line, f, indent=1)
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_init(args)
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+    else:
+        run_ours(args, ws, rank, local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,172 @@
+/*
+ * meerkat.h — C ABI of the B200-native Meerkat hot path (arXiv 2305.17813).
+ *
+ * Plain C: opaque handles, fixed-width integers, plain pointers.  No C++ or
+ * torch types cross this boundary.  One graph handle lives on one CUDA device
+ * and orders all its work on one CUDA stream (cfg.stream, or the legacy
+ * default stream when NULL).
+ *
+ * What the calls compute (citations: PAPER.md line numbers "P:n"):
+ *   - the dynamic graph object G of the problem statement: a
+ *     per-vertex SlabHash adjacency store with a single head-slab
+ *     arena sized from degree hints, batched warp-
+ *     cooperative InsertEdge / DeleteEdge / SearchEdge (WCWS
+ *     P:552-593, host COO batches P:2126-2140);
+ *   - a dependence tree T_G of packed <distance, parent> words, one 64-bit
+ *     atomicMin per relaxation (footnote P:28-30), maintained by
+ *     static, incremental and decremental (P:49-64,
+ *     P:138-165) SSSP, and BFS.
+ *
+ * Pointer arguments.  Batch inputs (src, dst, w) may be HOST or DEVICE
+ * pointers: the library inspects each pointer; host arrays are staged to the
+ * device on the graph's stream inside the call (pinned host memory makes the
+ * copy asynchronous).  Output arrays of query_batch / export_edges /
+ * tree_nodes / tree_invalidated may likewise be host or device; host outputs
+ * make the call synchronous.  The caller owns every batch and output buffer;
+ * the library owns the slab store, trees and scratch (released by destroy).
+ *
+ * Synchronisation and errors.  Calls are stream-ordered and return after
+ * enqueueing, unless they return a host count or write a host output, in
+ * which case they synchronise the stream.  Invalid edges (an id >= vertex_n;
+ * a weight of 0 or >= 2^31 on a weighted graph) are SKIPPED, never applied or
+ * counted; the condition is recorded on the device and reported (with
+ * VERTEX_RANGE taking precedence over WEIGHT) by the next synchronising call
+ * on that graph, then cleared.  Any non-OK status leaves the graph valid.
+ *
+ * Ordering contract ("G undergoes modifications through the
+ * application of an insertion/deletion edge batch; the incremental/decremental
+ * SSSP algorithm re-computes"): mutate first, then call the matching tree
+ * update with the SAME batch, for every tree of the graph, before the next
+ * mutation.  A tree update against any other graph version returns
+ * MEERKAT_E_STATE without touching the tree.
+ *
+ * Thread safety: a graph handle (and its trees) must not be used from two
+ * host threads at once.
+ */
+#ifndef MEERKAT_H_
+#define MEERKAT_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct meerkat_graph meerkat_graph; /* opaque: slab store + metadata on one device */
+typedef struct meerkat_tree meerkat_tree;   /* opaque: one SSSP or BFS tree for one source */
+
+typedef enum {
+  MEERKAT_OK = 0,
+  MEERKAT_E_INVALID_ARG = 1,  /* null handle/pointer, vertex_n 0 or >= 2^32-4, lf not in (0,1], missing weights */
+  MEERKAT_E_VERTEX_RANGE = 2, /* some id >= vertex_n (edge skipped) */
+  MEERKAT_E_WEIGHT = 3,       /* some weight 0 or >= 2^31 (edge skipped) */
+  MEERKAT_E_CAPACITY = 4,     /* slab pool or frontier exhausted; placed edges are kept and counted */
+  MEERKAT_E_OVERFLOW = 5,     /* a distance would reach 2^32-1; that relaxation is not applied (C5) */
+  MEERKAT_E_STATE = 6,        /* tree/graph version mismatch; SSSP on an unweighted graph */
+  MEERKAT_E_CUDA = 7,         /* CUDA runtime error (out of memory, launch failure, no device) */
+  MEERKAT_E_NCCL = 8          /* reserved for the multi-GPU router */
+} meerkat_status;
+
+typedef struct {
+  uint32_t vertex_n;            /* |V|, fixed for the graph's lifetime; ids are 0..vertex_n-1 */
+  uint32_t weighted;            /* 1: ConcurrentMap slabs, 15 <dst,w> pairs; 0: ConcurrentSet, 31 keys */
+  uint32_t hashing;             /* 0: one slab list per vertex ("hashing disabled") */
+  float load_factor;            /* lf in (0,1]; bucket_count[v] = ceil(hint[v]/(lf*capacity)); 0 => 0.7 */
+  const uint32_t* degree_hints; /* host or device [vertex_n], or NULL (every vertex one bucket) */
+  uint64_t pool_slabs;          /* growth-pool capacity in 128-B slabs; 0 => automatic */
+  uint64_t hash_seed;           /* bucket hash seed (storage only; results do not depend on it) */
+  int device;                   /* CUDA device ordinal */
+  void* stream;                 /* cudaStream_t for every call on this graph; NULL = default stream */
+} meerkat_config;
+
+typedef struct {
+  uint64_t vertex_n;
+  uint64_t edges;           /* live edges (inserted - deleted, as counted by the kernels) */
+  uint64_t head_slabs;      /* slabs in the head arena, = sum over v with hint > 0 of bucket_count[v] */
+  uint64_t buckets;         /* total slab lists (arena heads + one lazily allocated head per hint-0 vertex) */
+  uint64_t pool_capacity;   /* growth-pool capacity (slabs) */
+  uint64_t pool_used;       /* pool slabs handed out (chained slabs + lazily allocated heads) */
+  uint64_t bytes_device;    /* device bytes owned by the graph (excluding trees) */
+  uint64_t kernel_launches; /* kernels this graph and its trees have launched since creation */
+  uint64_t version;         /* mutation counter */
+} meerkat_stats;
+
+typedef struct {
+  uint64_t rounds;           /* relax rounds of the last tree call (frontier iterations) */
+  uint64_t propagate_rounds; /* invalidation-propagation rounds of the last decremental call */
+  uint64_t direct_invalid;   /* vertices invalidated directly by deleted tree edges */
+  uint64_t invalidated;      /* direct + propagated (|V_invalid|) */
+  uint64_t frontier_edges;   /* valid->invalid edges found by the decremental scan */
+  uint64_t items;            /* (vertex, bucket) work items expanded over all rounds */
+  uint64_t slabs_read;       /* slabs read by the last call */
+  uint64_t scan_slabs;       /* slabs streamed by the decremental scan */
+  uint64_t improved;         /* successful atomicMin relaxations */
+  uint64_t alg_bytes;        /* algorithmic bytes of the last call (DESIGN.md accounting) */
+  uint64_t version;          /* graph version this tree reflects */
+  uint32_t source;
+  uint32_t unit_weights;     /* 1 for BFS trees */
+} meerkat_tree_stats;
+
+const char* meerkat_status_string(meerkat_status s);
+
+/* Store construction: bucket counts from the hints,
+ * exclusive scan into one head arena, slab pool.  *out receives the handle. */
+meerkat_status meerkat_create(const meerkat_config* cfg, meerkat_graph** out);
+meerkat_status meerkat_destroy(meerkat_graph* g);
+/* Rebind the graph (and its trees) to another stream. */
+meerkat_status meerkat_set_stream(meerkat_graph* g, void* stream);
+/* Wait for the graph's stream; returns (and clears) any recorded batch error. */
+meerkat_status meerkat_sync(meerkat_graph* g);
+
+/* InsertEdges (device InsertEdge P:634-641).  Inserting a present
+ * edge keeps the smaller weight (C8).  w must be NULL iff the graph is
+ * unweighted.  n_inserted (host, nullable) receives the number of edges that
+ * were absent; passing it synchronises. */
+meerkat_status meerkat_insert_batch(meerkat_graph* g, const uint32_t* src, const uint32_t* dst,
+                                    const uint32_t* w, uint64_t n, uint64_t* n_inserted);
+/* DeleteEdges (DeleteEdge P:637, TOMBSTONE P:1506-1507).  Absent
+ * edges are no-ops (C11).  n_deleted (host, nullable) receives the number removed. */
+meerkat_status meerkat_delete_batch(meerkat_graph* g, const uint32_t* src, const uint32_t* dst, uint64_t n,
+                                    uint64_t* n_deleted);
+/* SearchEdge: found[i] = 1 iff (src[i], dst[i]) is present; w_out[i] =
+ * its weight (0 when absent or unweighted).  w_out may be NULL. */
+meerkat_status meerkat_query_batch(meerkat_graph* g, const uint32_t* src, const uint32_t* dst, uint64_t n,
+                                   uint8_t* found, uint32_t* w_out);
+/* Every live edge, in unspecified order (w = 0 when unweighted).  Writes at
+ * most `capacity` edges, sets *n_out to the live count, synchronises;
+ * MEERKAT_E_CAPACITY if capacity < live count. */
+meerkat_status meerkat_export_edges(meerkat_graph* g, uint32_t* src, uint32_t* dst, uint32_t* w,
+                                    uint64_t capacity, uint64_t* n_out);
+meerkat_status meerkat_stats_get(meerkat_graph* g, meerkat_stats* out); /* synchronises */
+
+/* Static SSSP (weighted graphs only) / level-based static BFS
+ * (hop counts, weights ignored).  The new tree reflects the current
+ * graph version. */
+meerkat_status meerkat_sssp_create(meerkat_graph* g, uint32_t source, meerkat_tree** out);
+meerkat_status meerkat_bfs_create(meerkat_graph* g, uint32_t source, meerkat_tree** out);
+/* Incremental update: the batch just applied by insert_batch is the
+ * initial frontier.  w: the batch's weights (NULL for BFS trees). */
+meerkat_status meerkat_sssp_incremental(meerkat_graph* g, meerkat_tree* t, const uint32_t* src,
+                                        const uint32_t* dst, const uint32_t* w, uint64_t n);
+meerkat_status meerkat_bfs_incremental(meerkat_graph* g, meerkat_tree* t, const uint32_t* src,
+                                       const uint32_t* dst, uint64_t n);
+/* Decremental update: invalidate deleted tree edges,
+ * propagate down T_v, re-seed from valid->invalid edges, relax to fixpoint. */
+meerkat_status meerkat_sssp_decremental(meerkat_graph* g, meerkat_tree* t, const uint32_t* src,
+                                        const uint32_t* dst, uint64_t n);
+meerkat_status meerkat_bfs_decremental(meerkat_graph* g, meerkat_tree* t, const uint32_t* src,
+                                       const uint32_t* dst, uint64_t n);
+/* Static re-run on the current graph (the s_b^n baseline). */
+meerkat_status meerkat_tree_recompute(meerkat_graph* g, meerkat_tree* t);
+/* node[v] = dist << 32 | parent for every v, UINT64_MAX when unreached (C3). */
+meerkat_status meerkat_tree_nodes(meerkat_tree* t, uint64_t* out);
+/* The vertices invalidated by the last decremental call (unordered). */
+meerkat_status meerkat_tree_invalidated(meerkat_tree* t, uint32_t* out, uint64_t capacity, uint64_t* n_out);
+meerkat_status meerkat_tree_stats_get(meerkat_tree* t, meerkat_tree_stats* out); /* synchronises */
+meerkat_status meerkat_tree_destroy(meerkat_tree* t);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MEERKAT_H_ */

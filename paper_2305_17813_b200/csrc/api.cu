@@ -1,0 +1,465 @@
+// api.cu — the C ABI declared in include/meerkat.h: argument checking, pointer
+// staging, stream ordering, version checks and status translation around the
+// launchers in store.cu and tree.cu.  No compute happens here.
+#include <algorithm>
+#include <cstring>
+#include <new>
+
+#include "graph.h"
+
+using namespace mk;
+
+namespace {
+
+meerkat_status from_cuda(cudaError_t e) { return e == cudaSuccess ? MEERKAT_OK : MEERKAT_E_CUDA; }
+
+meerkat_status from_err(uint32_t err) {
+  if (err & ERR_RANGE) return MEERKAT_E_VERTEX_RANGE;
+  if (err & ERR_WEIGHT) return MEERKAT_E_WEIGHT;
+  if (err & ERR_CAPACITY) return MEERKAT_E_CAPACITY;
+  if (err & ERR_OVERFLOW) return MEERKAT_E_OVERFLOW;
+  if (err & ERR_STATE) return MEERKAT_E_STATE;
+  return MEERKAT_OK;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int d) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+cudaError_t ensure_stage(meerkat_graph* g, int slot, size_t bytes) {
+  if (g->stage_bytes[slot] >= bytes) return cudaSuccess;
+  cudaError_t e = cudaStreamSynchronize(g->stream);
+  if (e != cudaSuccess) return e;
+  cudaFree(g->stage[slot]);
+  g->stage[slot] = nullptr;
+  g->stage_bytes[slot] = 0;
+  size_t cap = std::max<size_t>(bytes, 1 << 16);
+  e = cudaMalloc(&g->stage[slot], cap);
+  if (e == cudaSuccess) g->stage_bytes[slot] = cap;
+  return e;
+}
+
+// Device view of a caller array: device pointers pass through, host arrays are
+// copied into the graph's staging slot on its stream.
+cudaError_t stage_in(meerkat_graph* g, int slot, const void* p, size_t bytes, const void** out) {
+  *out = p;
+  if (!p || !bytes || is_device_ptr(p)) return cudaSuccess;
+  cudaError_t e = ensure_stage(g, slot, bytes);
+  if (e != cudaSuccess) return e;
+  *out = g->stage[slot];
+  return cudaMemcpyAsync(g->stage[slot], p, bytes, cudaMemcpyHostToDevice, g->stream);
+}
+
+// Read the control block back (synchronises); returns and clears the sticky error.
+meerkat_status collect(meerkat_graph* g) {
+  cudaError_t e = cudaMemcpyAsync(g->hctrl, g->dev.ctrl, sizeof(GraphCtrl), cudaMemcpyDeviceToHost, g->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  const uint32_t err = g->hctrl->err;
+  if (err) {
+    if (cudaMemsetAsync(&g->dev.ctrl->err, 0, 4, g->stream) != cudaSuccess) return MEERKAT_E_CUDA;
+  }
+  return from_err(err);
+}
+
+meerkat_status check_batch(meerkat_graph* g, const uint32_t* s, const uint32_t* d, uint64_t n) {
+  if (!g) return MEERKAT_E_INVALID_ARG;
+  if (n && (!s || !d)) return MEERKAT_E_INVALID_ARG;
+  return MEERKAT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* meerkat_status_string(meerkat_status s) {
+  switch (s) {
+    case MEERKAT_OK: return "MEERKAT_OK";
+    case MEERKAT_E_INVALID_ARG: return "MEERKAT_E_INVALID_ARG";
+    case MEERKAT_E_VERTEX_RANGE: return "MEERKAT_E_VERTEX_RANGE";
+    case MEERKAT_E_WEIGHT: return "MEERKAT_E_WEIGHT";
+    case MEERKAT_E_CAPACITY: return "MEERKAT_E_CAPACITY";
+    case MEERKAT_E_OVERFLOW: return "MEERKAT_E_OVERFLOW";
+    case MEERKAT_E_STATE: return "MEERKAT_E_STATE";
+    case MEERKAT_E_CUDA: return "MEERKAT_E_CUDA";
+    case MEERKAT_E_NCCL: return "MEERKAT_E_NCCL";
+  }
+  return "MEERKAT_E_UNKNOWN";
+}
+
+meerkat_status meerkat_create(const meerkat_config* cfg, meerkat_graph** out) {
+  if (!cfg || !out) return MEERKAT_E_INVALID_ARG;
+  *out = nullptr;
+  const float lf = cfg->load_factor == 0.0f ? 0.7f : cfg->load_factor;
+  if (cfg->vertex_n == 0 || cfg->vertex_n >= 0xFFFFFFFCu || !(lf > 0.0f && lf <= 1.0f))
+    return MEERKAT_E_INVALID_ARG;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || cfg->device < 0 || cfg->device >= ndev) {
+    cudaGetLastError();
+    return MEERKAT_E_CUDA;
+  }
+  DeviceGuard dg(cfg->device);
+  meerkat_graph* g = new (std::nothrow) meerkat_graph();
+  if (!g) return MEERKAT_E_CUDA;
+  g->device = cfg->device;
+  g->stream = static_cast<cudaStream_t>(cfg->stream);
+  g->V = cfg->vertex_n;
+  g->weighted = cfg->weighted != 0;
+  g->hashing = cfg->hashing != 0;
+  g->lf = lf;
+  g->P = cfg->pool_slabs;
+  g->dev.seed = (uint32_t)(cfg->hash_seed ^ (cfg->hash_seed >> 32)) ^ 0x5bd1e995u;
+  cudaError_t e = cudaDeviceGetAttribute(&g->sm_count, cudaDevAttrMultiProcessorCount, g->device);
+  const void* hints = nullptr;
+  if (e == cudaSuccess) e = cudaMallocHost(&g->hctrl, sizeof(GraphCtrl));
+  if (e == cudaSuccess) e = stage_in(g, 0, cfg->degree_hints, (size_t)g->V * 4, &hints);
+  if (e == cudaSuccess) e = launch_build(g, static_cast<const uint32_t*>(hints));
+  if (e == cudaSuccess) e = tree_occupancy(g);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    meerkat_destroy(g);
+    return MEERKAT_E_CUDA;
+  }
+  std::memset(g->hctrl, 0, sizeof(GraphCtrl));
+  *out = g;
+  return MEERKAT_OK;
+}
+
+meerkat_status meerkat_destroy(meerkat_graph* g) {
+  if (!g) return MEERKAT_E_INVALID_ARG;
+  DeviceGuard dg(g->device);
+  cudaStreamSynchronize(g->stream);
+  cudaFree(g->dev.slabs);
+  cudaFree(g->dev.owner);
+  cudaFree(g->dev.vmeta);
+  cudaFree(g->dev.ctrl);
+  for (int i = 0; i < 4; i++) cudaFree(g->stage[i]);
+  if (g->hctrl) cudaFreeHost(g->hctrl);
+  delete g;
+  return MEERKAT_OK;
+}
+
+meerkat_status meerkat_set_stream(meerkat_graph* g, void* stream) {
+  if (!g) return MEERKAT_E_INVALID_ARG;
+  DeviceGuard dg(g->device);
+  cudaError_t e = cudaStreamSynchronize(g->stream);
+  g->stream = static_cast<cudaStream_t>(stream);
+  return from_cuda(e);
+}
+
+meerkat_status meerkat_sync(meerkat_graph* g) {
+  if (!g) return MEERKAT_E_INVALID_ARG;
+  DeviceGuard dg(g->device);
+  return collect(g);
+}
+
+meerkat_status meerkat_insert_batch(meerkat_graph* g, const uint32_t* src, const uint32_t* dst, const uint32_t* w,
+                                    uint64_t n, uint64_t* n_inserted) {
+  meerkat_status st = check_batch(g, src, dst, n);
+  if (st != MEERKAT_OK) return st;
+  if (n && (g->weighted != (w != nullptr))) return MEERKAT_E_INVALID_ARG;
+  DeviceGuard dg(g->device);
+  const void *s, *d, *ww = nullptr;
+  cudaError_t e = stage_in(g, 0, src, n * 4, &s);
+  if (e == cudaSuccess) e = stage_in(g, 1, dst, n * 4, &d);
+  if (e == cudaSuccess && w) e = stage_in(g, 2, w, n * 4, &ww);
+  if (e == cudaSuccess && n_inserted) e = cudaMemsetAsync(&g->dev.ctrl->n_inserted, 0, 8, g->stream);
+  if (e == cudaSuccess)
+    e = launch_insert(g, (const uint32_t*)s, (const uint32_t*)d, (const uint32_t*)ww, n);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  g->version++;
+  g->last_kind = 1;
+  if (!n_inserted) return MEERKAT_OK;
+  st = collect(g);
+  *n_inserted = g->hctrl->n_inserted;
+  return st;
+}
+
+meerkat_status meerkat_delete_batch(meerkat_graph* g, const uint32_t* src, const uint32_t* dst, uint64_t n,
+                                    uint64_t* n_deleted) {
+  meerkat_status st = check_batch(g, src, dst, n);
+  if (st != MEERKAT_OK) return st;
+  DeviceGuard dg(g->device);
+  const void *s, *d;
+  cudaError_t e = stage_in(g, 0, src, n * 4, &s);
+  if (e == cudaSuccess) e = stage_in(g, 1, dst, n * 4, &d);
+  if (e == cudaSuccess && n_deleted) e = cudaMemsetAsync(&g->dev.ctrl->n_deleted, 0, 8, g->stream);
+  if (e == cudaSuccess) e = launch_delete(g, (const uint32_t*)s, (const uint32_t*)d, n);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  g->version++;
+  g->last_kind = 2;
+  if (!n_deleted) return MEERKAT_OK;
+  st = collect(g);
+  *n_deleted = g->hctrl->n_deleted;
+  return st;
+}
+
+meerkat_status meerkat_query_batch(meerkat_graph* g, const uint32_t* src, const uint32_t* dst, uint64_t n,
+                                   uint8_t* found, uint32_t* w_out) {
+  meerkat_status st = check_batch(g, src, dst, n);
+  if (st != MEERKAT_OK) return st;
+  if (n && !found) return MEERKAT_E_INVALID_ARG;
+  DeviceGuard dg(g->device);
+  const void *s, *d;
+  cudaError_t e = stage_in(g, 0, src, n * 4, &s);
+  if (e == cudaSuccess) e = stage_in(g, 1, dst, n * 4, &d);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  const bool host_f = n && !is_device_ptr(found);
+  const bool host_w = n && w_out && !is_device_ptr(w_out);
+  uint8_t* df = found;
+  uint32_t* dw = w_out;
+  if (host_f) { e = ensure_stage(g, 2, n); df = (uint8_t*)g->stage[2]; }
+  if (e == cudaSuccess && host_w) { e = ensure_stage(g, 3, n * 4); dw = (uint32_t*)g->stage[3]; }
+  if (e == cudaSuccess) e = launch_query(g, (const uint32_t*)s, (const uint32_t*)d, n, df, dw);
+  if (e == cudaSuccess && host_f) e = cudaMemcpyAsync(found, df, n, cudaMemcpyDeviceToHost, g->stream);
+  if (e == cudaSuccess && host_w) e = cudaMemcpyAsync(w_out, dw, n * 4, cudaMemcpyDeviceToHost, g->stream);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  if (host_f || host_w) return collect(g);
+  return MEERKAT_OK;
+}
+
+meerkat_status meerkat_export_edges(meerkat_graph* g, uint32_t* src, uint32_t* dst, uint32_t* w, uint64_t capacity,
+                                    uint64_t* n_out) {
+  if (!g || !n_out || (capacity && (!src || !dst))) return MEERKAT_E_INVALID_ARG;
+  DeviceGuard dg(g->device);
+  const bool host = capacity && !is_device_ptr(src);
+  uint32_t *ds = src, *dd = dst, *dw = w;
+  cudaError_t e = cudaSuccess;
+  if (host) {
+    e = ensure_stage(g, 0, capacity * 4);
+    if (e == cudaSuccess) e = ensure_stage(g, 1, capacity * 4);
+    if (e == cudaSuccess && w) e = ensure_stage(g, 2, capacity * 4);
+    ds = (uint32_t*)g->stage[0]; dd = (uint32_t*)g->stage[1]; dw = w ? (uint32_t*)g->stage[2] : nullptr;
+  }
+  if (e == cudaSuccess) e = launch_export(g, ds, dd, dw, capacity);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  meerkat_status st = collect(g);
+  const uint64_t n = g->hctrl->export_n;
+  *n_out = n;
+  if (host) {
+    const uint64_t m = std::min(n, capacity);
+    e = cudaMemcpyAsync(src, ds, m * 4, cudaMemcpyDeviceToHost, g->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dst, dd, m * 4, cudaMemcpyDeviceToHost, g->stream);
+    if (e == cudaSuccess && w) e = cudaMemcpyAsync(w, dw, m * 4, cudaMemcpyDeviceToHost, g->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+    if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  }
+  if (st != MEERKAT_OK) return st;
+  return n > capacity ? MEERKAT_E_CAPACITY : MEERKAT_OK;
+}
+
+meerkat_status meerkat_stats_get(meerkat_graph* g, meerkat_stats* out) {
+  if (!g || !out) return MEERKAT_E_INVALID_ARG;
+  DeviceGuard dg(g->device);
+  cudaError_t e = cudaMemcpyAsync(g->hctrl, g->dev.ctrl, sizeof(GraphCtrl), cudaMemcpyDeviceToHost, g->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  std::memset(out, 0, sizeof(*out));
+  out->vertex_n = g->V;
+  out->edges = g->hctrl->ins_total - g->hctrl->del_total;
+  out->head_slabs = g->H;
+  out->buckets = g->buckets;
+  out->pool_capacity = g->P;
+  out->pool_used = std::min<uint64_t>(g->hctrl->pool_top, g->P);
+  out->bytes_device = g->bytes;
+  out->kernel_launches = g->launches;
+  out->version = g->version;
+  return MEERKAT_OK;
+}
+
+// ------------------------------------------------------------------ trees
+
+static meerkat_status tree_create(meerkat_graph* g, uint32_t source, bool unit, meerkat_tree** out) {
+  if (!g || !out) return MEERKAT_E_INVALID_ARG;
+  *out = nullptr;
+  if (source >= g->V) return MEERKAT_E_VERTEX_RANGE;
+  if (!unit && !g->weighted) return MEERKAT_E_STATE;   // SSSP needs weights
+  DeviceGuard dg(g->device);
+  meerkat_tree* t = new (std::nothrow) meerkat_tree();
+  if (!t) return MEERKAT_E_CUDA;
+  t->g = g;
+  t->unit = unit;
+  TreeDev& T = t->dev;
+  T.source = source;
+  T.fr_cap = std::max<uint64_t>(g->buckets, 1);
+  const size_t V = g->V, words = (V + 31) / 32;
+  cudaError_t e = cudaMalloc(&T.node, V * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&T.stamp, V * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&T.inval_bits, words * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&T.inval_list, V * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&T.fr[0], T.fr_cap * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&T.fr[1], T.fr_cap * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&T.ctrl, sizeof(TreeCtrl));
+  if (e == cudaSuccess) e = cudaMalloc(&T.epoch_ptr, 4);
+  if (e == cudaSuccess) e = cudaMallocHost(&t->hctrl, sizeof(TreeCtrl));
+  if (e == cudaSuccess) e = cudaMemsetAsync(T.stamp, 0, V * 4, g->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(T.inval_bits, 0, words * 4, g->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(T.epoch_ptr, 0, 4, g->stream);
+  if (e == cudaSuccess) {
+    const uint32_t one = 1;
+    e = cudaMemcpyAsync(T.epoch_ptr, &one, 4, cudaMemcpyHostToDevice, g->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  }
+  t->bytes = V * 8 + V * 4 + words * 4 + V * 4 + 2 * T.fr_cap * 8 + sizeof(TreeCtrl) + 4;
+  if (e == cudaSuccess) e = launch_tree(g, t, MODE_STATIC, nullptr, nullptr, nullptr, 0);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    meerkat_tree_destroy(t);
+    return MEERKAT_E_CUDA;
+  }
+  t->version = g->version;
+  *out = t;
+  return MEERKAT_OK;
+}
+
+meerkat_status meerkat_sssp_create(meerkat_graph* g, uint32_t source, meerkat_tree** out) {
+  return tree_create(g, source, false, out);
+}
+
+meerkat_status meerkat_bfs_create(meerkat_graph* g, uint32_t source, meerkat_tree** out) {
+  return tree_create(g, source, true, out);
+}
+
+static meerkat_status tree_update(meerkat_graph* g, meerkat_tree* t, bool unit, int kind, const uint32_t* src,
+                                  const uint32_t* dst, const uint32_t* w, uint64_t n) {
+  meerkat_status st = check_batch(g, src, dst, n);
+  if (st != MEERKAT_OK) return st;
+  if (!t || t->g != g || t->unit != unit) return MEERKAT_E_INVALID_ARG;
+  // ordering contract: the batch must be the mutation just applied
+  if (g->last_kind != kind || t->version + 1 != g->version) return MEERKAT_E_STATE;
+  if (kind == 1 && !unit && n && !w) return MEERKAT_E_INVALID_ARG;
+  DeviceGuard dg(g->device);
+  const void *s, *d, *ww = nullptr;
+  cudaError_t e = stage_in(g, 0, src, n * 4, &s);
+  if (e == cudaSuccess) e = stage_in(g, 1, dst, n * 4, &d);
+  if (e == cudaSuccess && kind == 1 && !unit) e = stage_in(g, 2, w, n * 4, &ww);
+  if (e == cudaSuccess)
+    e = launch_tree(g, t, kind == 1 ? MODE_INCREMENTAL : MODE_DECREMENTAL, (const uint32_t*)s, (const uint32_t*)d,
+                    (const uint32_t*)ww, n);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  t->version = g->version;
+  return MEERKAT_OK;
+}
+
+meerkat_status meerkat_sssp_incremental(meerkat_graph* g, meerkat_tree* t, const uint32_t* src, const uint32_t* dst,
+                                        const uint32_t* w, uint64_t n) {
+  return tree_update(g, t, false, 1, src, dst, w, n);
+}
+
+meerkat_status meerkat_bfs_incremental(meerkat_graph* g, meerkat_tree* t, const uint32_t* src, const uint32_t* dst,
+                                       uint64_t n) {
+  return tree_update(g, t, true, 1, src, dst, nullptr, n);
+}
+
+meerkat_status meerkat_sssp_decremental(meerkat_graph* g, meerkat_tree* t, const uint32_t* src, const uint32_t* dst,
+                                        uint64_t n) {
+  return tree_update(g, t, false, 2, src, dst, nullptr, n);
+}
+
+meerkat_status meerkat_bfs_decremental(meerkat_graph* g, meerkat_tree* t, const uint32_t* src, const uint32_t* dst,
+                                       uint64_t n) {
+  return tree_update(g, t, true, 2, src, dst, nullptr, n);
+}
+
+meerkat_status meerkat_tree_recompute(meerkat_graph* g, meerkat_tree* t) {
+  if (!g || !t || t->g != g) return MEERKAT_E_INVALID_ARG;
+  DeviceGuard dg(g->device);
+  cudaError_t e = launch_tree(g, t, MODE_STATIC, nullptr, nullptr, nullptr, 0);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  t->version = g->version;
+  return MEERKAT_OK;
+}
+
+meerkat_status meerkat_tree_nodes(meerkat_tree* t, uint64_t* out) {
+  if (!t || !out) return MEERKAT_E_INVALID_ARG;
+  meerkat_graph* g = t->g;
+  DeviceGuard dg(g->device);
+  const bool host = !is_device_ptr(out);
+  cudaError_t e = cudaMemcpyAsync(out, t->dev.node, (size_t)g->V * 8,
+                                  host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, g->stream);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  if (host) return collect(g);
+  return MEERKAT_OK;
+}
+
+meerkat_status meerkat_tree_invalidated(meerkat_tree* t, uint32_t* out, uint64_t capacity, uint64_t* n_out) {
+  if (!t || !n_out || (capacity && !out)) return MEERKAT_E_INVALID_ARG;
+  meerkat_graph* g = t->g;
+  DeviceGuard dg(g->device);
+  cudaError_t e = cudaMemcpyAsync(t->hctrl, t->dev.ctrl, sizeof(TreeCtrl), cudaMemcpyDeviceToHost, g->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  const uint64_t n = t->hctrl->inval_n;
+  *n_out = n;
+  const uint64_t m = std::min(n, capacity);
+  if (m) {
+    const bool host = !is_device_ptr(out);
+    e = cudaMemcpyAsync(out, t->dev.inval_list, m * 4, host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                        g->stream);
+    if (e == cudaSuccess && host) e = cudaStreamSynchronize(g->stream);
+    if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  }
+  return n > capacity ? MEERKAT_E_CAPACITY : MEERKAT_OK;
+}
+
+meerkat_status meerkat_tree_stats_get(meerkat_tree* t, meerkat_tree_stats* out) {
+  if (!t || !out) return MEERKAT_E_INVALID_ARG;
+  meerkat_graph* g = t->g;
+  DeviceGuard dg(g->device);
+  cudaError_t e = cudaMemcpyAsync(t->hctrl, t->dev.ctrl, sizeof(TreeCtrl), cudaMemcpyDeviceToHost, g->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  const TreeCtrl& c = *t->hctrl;
+  std::memset(out, 0, sizeof(*out));
+  out->rounds = c.rounds;
+  out->propagate_rounds = c.prop_rounds;
+  out->direct_invalid = c.direct_n;
+  out->invalidated = c.inval_n;
+  out->frontier_edges = c.scan_hits;
+  out->items = c.items;
+  out->slabs_read = c.slabs_read;
+  out->scan_slabs = c.scan_slabs;
+  out->improved = c.improved;
+  // algorithmic bytes: item read + vmeta + node[v] + item write (32 B),
+  // 128 B per slab walked or streamed, 8 B node[x] probe per visited edge, 12 B (atomicMin + stamp) per
+  // improvement, 16 B (owner + node[u] + bit) per scan hit, 20 B per batch edge (src, dst, w, node[u]).
+  out->alg_bytes = c.items * 32 + (c.slabs_read + c.scan_slabs) * 128 + c.visited * 8 + c.improved * 12 +
+                   c.scan_hits * 16 + c.batch_edges * 20;
+  out->version = t->version;
+  out->source = t->dev.source;
+  out->unit_weights = t->unit ? 1 : 0;
+  return MEERKAT_OK;
+}
+
+meerkat_status meerkat_tree_destroy(meerkat_tree* t) {
+  if (!t) return MEERKAT_E_INVALID_ARG;
+  DeviceGuard dg(t->g->device);
+  cudaStreamSynchronize(t->g->stream);
+  TreeDev& T = t->dev;
+  cudaFree(T.node); cudaFree(T.stamp); cudaFree(T.inval_bits); cudaFree(T.inval_list);
+  cudaFree(T.fr[0]); cudaFree(T.fr[1]); cudaFree(T.ctrl); cudaFree(T.epoch_ptr);
+  if (t->hctrl) cudaFreeHost(t->hctrl);
+  delete t;
+  return MEERKAT_OK;
+}
+
+}  // extern "C"

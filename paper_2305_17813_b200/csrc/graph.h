@@ -1,0 +1,83 @@
+// graph.h — host-side handle layouts and the launchers each .cu file exports.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/meerkat.h"
+#include "internal.cuh"
+
+namespace mk {
+
+struct TreeCtrl {
+  unsigned long long size[3];       // rotating frontier sizes (see tree.cu, "round protocol")
+  unsigned long long inval_n;       // |V_invalid| of this call
+  unsigned long long direct_n;      // directly invalidated vertices
+  unsigned long long rounds;        // relax rounds
+  unsigned long long prop_rounds;   // propagation rounds
+  unsigned long long items;         // (vertex, bucket) items expanded
+  unsigned long long slabs_read;    // slabs walked by expansion
+  unsigned long long scan_slabs;    // slabs streamed by the decremental scan
+  unsigned long long scan_hits;     // valid->invalid edges found by the scan
+  unsigned long long improved;      // successful atomicMin
+  unsigned long long visited;       // live edges visited by expansion (one node[x] probe each)
+  unsigned long long batch_edges;   // batch edges examined by the prologue
+};
+
+struct TreeDev {
+  uint64_t* node;        // packed <dist, parent> per vertex
+  uint32_t* stamp;       // last epoch a vertex was enqueued (frontier de-duplication)
+  uint32_t* inval_bits;  // V-bit set of invalidated vertices (decremental only)
+  uint32_t* inval_list;  // invalidated vertex ids
+  uint64_t* fr[2];       // frontier item buffers: (bucket << 32) | vertex
+  TreeCtrl* ctrl;
+  uint32_t* epoch_ptr;   // device-resident stamp epoch base, advanced by each call
+  uint64_t fr_cap;       // items per frontier buffer (= number of slab lists)
+  uint32_t source;
+};
+
+}  // namespace mk
+
+struct meerkat_graph {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  uint32_t V = 0;
+  bool weighted = false, hashing = true;
+  float lf = 0.7f;
+  uint64_t H = 0, P = 0, buckets = 0;
+  mk::GraphDev dev{};
+  mk::GraphCtrl* hctrl = nullptr;   // pinned mirror of dev.ctrl
+  uint64_t version = 0;
+  int last_kind = 0;                // 0 none, 1 insert, 2 delete
+  uint64_t launches = 0;
+  int sm_count = 0;
+  size_t bytes = 0;
+  void* stage[4] = {nullptr, nullptr, nullptr, nullptr};   // staging for host inputs / outputs
+  size_t stage_bytes[4] = {0, 0, 0, 0};
+  int tree_blocks_per_sm[3] = {0, 0, 0};   // cooperative occupancy: static/incremental, decremental (set, map)
+};
+
+struct meerkat_tree {
+  meerkat_graph* g = nullptr;
+  mk::TreeDev dev{};
+  mk::TreeCtrl* hctrl = nullptr;
+  bool unit = false;     // BFS
+  uint64_t version = 0;
+  uint32_t last_inval_n = 0;
+  size_t bytes = 0;
+};
+
+namespace mk {
+// store.cu
+cudaError_t launch_build(meerkat_graph* g, const uint32_t* d_hints);
+cudaError_t launch_insert(meerkat_graph* g, const uint32_t* s, const uint32_t* d, const uint32_t* w, uint64_t n);
+cudaError_t launch_delete(meerkat_graph* g, const uint32_t* s, const uint32_t* d, uint64_t n);
+cudaError_t launch_query(meerkat_graph* g, const uint32_t* s, const uint32_t* d, uint64_t n, uint8_t* found,
+                         uint32_t* w_out);
+cudaError_t launch_export(meerkat_graph* g, uint32_t* s, uint32_t* d, uint32_t* w, uint64_t cap);
+// tree.cu
+cudaError_t tree_occupancy(meerkat_graph* g);
+enum TreeMode { MODE_STATIC = 0, MODE_INCREMENTAL = 1, MODE_DECREMENTAL = 2 };
+cudaError_t launch_tree(meerkat_graph* g, meerkat_tree* t, int mode, const uint32_t* s, const uint32_t* d,
+                        const uint32_t* w, uint64_t n);
+}  // namespace mk

@@ -1,0 +1,112 @@
+// internal.cuh — device-side layout, sentinels and warp-group primitives shared
+// by the store kernels (store.cu) and the traversal kernels (tree.cu).
+//
+// Slab layout: a slab is 128 B = 32 lanes x 4 B,
+// one L1/L2 line.  Lane 31 holds the next slab's index (INVALID_SLAB ends the
+// chain).  ConcurrentSet (unweighted) slabs keep 31 keys in lanes 0..30;
+// ConcurrentMap (weighted) slabs keep 15 <key, weight> pairs in lanes (2k, 2k+1),
+// k < 15, lane 30 permanently EMPTY.  A pair is one aligned 64-bit word whose
+// low half is the key, so one 64-bit CAS / atomicMin updates it.
+//
+// B200 mapping: a slab is read by a GROUP of 8 lanes, each loading 16 B
+// (one LDG.128), so one warp instruction reads four independent slabs
+// (4 memory requests in flight per warp instead of the paper's one,
+// SURVEY §7 H2).  Every group-level collective uses the group's 8-lane mask.
+#pragma once
+#include <cooperative_groups.h>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mk {
+
+constexpr uint32_t EMPTY_KEY = 0xFFFFFFFEu;              // UINT32_MAX-1 (P:1504 footnote)
+constexpr uint32_t TOMBSTONE_KEY = 0xFFFFFFFDu;          // UINT32_MAX-2 (P:1506 footnote)
+constexpr uint32_t INVALID_SLAB = 0xFFFFFFFFu;           // end of chain / no head slab yet
+constexpr uint32_t LINKING = 0xFFFFFFFEu;                // link word locked while one group links a slab
+constexpr uint32_t NO_OWNER = 0xFFFFFFFFu;               // owner[] of a slab outside any list
+constexpr uint64_t EMPTY_PAIR = 0xFFFFFFFFFFFFFFFEull;   // UINT64_MAX-1 (P:1504 footnote)
+constexpr uint64_t TOMB_PAIR = 0xFFFFFFFDFFFFFFFDull;    // <UINT32_MAX-2, UINT32_MAX-2> (P:1506 footnote)
+constexpr uint64_t UNREACHED = ~0ull;                    // <INF, INVALID> packed (C3)
+constexpr uint32_t INF_DIST = 0xFFFFFFFFu;
+constexpr uint32_t W_LIMIT = 0x80000000u;                // weights in [1, 2^31) (C6)
+constexpr int SLAB_WORDS = 32;
+constexpr int GROUP = 8;                                 // lanes per slab
+constexpr int SET_CAP = 31, MAP_CAP = 15;
+
+enum ErrBits : uint32_t { ERR_RANGE = 1, ERR_WEIGHT = 2, ERR_CAPACITY = 4, ERR_OVERFLOW = 8, ERR_STATE = 16 };
+
+struct GraphCtrl {
+  unsigned long long pool_top;    // bump pointer of the growth pool
+  unsigned long long n_inserted;  // per-call counters (reset by the host when a count is requested)
+  unsigned long long n_deleted;
+  unsigned long long ins_total;   // cumulative: live edges = ins_total - del_total
+  unsigned long long del_total;
+  unsigned long long export_n;
+  unsigned int err;               // sticky ErrBits
+  unsigned int pad;
+};
+
+struct GraphDev {
+  uint32_t* slabs;   // (H + P) slabs x 32 words: head arena [0, H) then pool [H, H + P)
+  uint32_t* owner;   // source vertex of every slab (the paper's bucket_vertex[])
+  uint2* vmeta;      // per vertex {first head slab | INVALID_SLAB, bucket_count}
+  GraphCtrl* ctrl;
+  uint32_t V, H, P, seed;
+};
+
+__device__ __forceinline__ uint32_t* slab_ptr(const GraphDev& G, uint32_t s) {
+  return G.slabs + (size_t)s * SLAB_WORDS;
+}
+
+// Bucket hash ("determined by a hashing function", unnamed; reading C21):
+// a murmur3 finaliser of the key, range-reduced by a multiply-high.  Storage only.
+__device__ __forceinline__ uint32_t mix32(uint32_t x) {
+  x ^= x >> 16; x *= 0x7feb352du; x ^= x >> 15; x *= 0x846ca68bu; x ^= x >> 16;
+  return x;
+}
+__device__ __forceinline__ uint32_t bucket_of(uint32_t key, uint32_t count, uint32_t seed) {
+  return count <= 1 ? 0u : __umulhi(mix32(key ^ seed), count);
+}
+
+// Coherent 16-B slab fragment load for kernels that race with writers (update kernels).
+__device__ __forceinline__ uint4 ld_slab_cg(const uint32_t* slab, int l8) {
+  return __ldcg(reinterpret_cast<const uint4*>(slab) + l8);
+}
+// Read-only streaming load for traversal kernels (the store is immutable while a tree kernel runs).
+__device__ __forceinline__ uint4 ld_slab_ro(const uint32_t* slab, int l8) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(reinterpret_cast<const uint4*>(slab) + l8));
+  return r;
+}
+__device__ __forceinline__ uint64_t ld_cg_u64(const uint64_t* p) {
+  return __ldcg(reinterpret_cast<const unsigned long long*>(p));
+}
+
+// Keys held by one lane's 16-B fragment: MAP -> 2 pairs (x,y),(z,w); SET -> 4 keys.
+// Cell index c = l8 * NK + k.  The last cell of lane 7 is not a key cell
+// (MAP: pair 15 = lanes 30/31; SET: lane 31 = next pointer).
+template <bool MAP> struct Frag {
+  static constexpr int NK = MAP ? 2 : 4;
+  __device__ __forceinline__ static uint32_t key(const uint4& d, int k) {
+    if (MAP) return k == 0 ? d.x : d.z;
+    return k == 0 ? d.x : (k == 1 ? d.y : (k == 2 ? d.z : d.w));
+  }
+  __device__ __forceinline__ static uint32_t weight(const uint4& d, int k) { return k == 0 ? d.y : d.w; }
+  __device__ __forceinline__ static bool valid_cell(int l8, int k) { return !(l8 == GROUP - 1 && k == NK - 1); }
+};
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// First cell (in chain order) whose per-lane predicate bits are set.
+// bits: NK-bit mask of this lane's cells.  Returns cell index or -1 (group-uniform).
+template <int NK>
+__device__ __forceinline__ int group_first_cell(uint32_t bits, uint32_t gmask, int gbase) {
+  uint32_t any = (__ballot_sync(gmask, bits != 0) >> gbase) & 0xFFu;
+  if (!any) return -1;
+  int l = __ffs(any) - 1;
+  uint32_t lb = __shfl_sync(gmask, bits, l, GROUP);
+  return l * NK + (__ffs(lb) - 1);
+}
+
+}  // namespace mk

@@ -1,0 +1,503 @@
+// store.cu — the per-vertex SlabHash adjacency store on sm_100a.
+//
+//  * construction: bucket_count[v] = ceil(hint/(lf*cap)),
+//    exclusive scan into ONE head-slab arena, owner[] (the paper's
+//    bucket_vertex[]) and a growth pool in the same allocation;
+//  * batched insert / delete / query with the warp-cooperative work strategy
+//    (WCWS; InsertEdge/DeleteEdge/SearchEdge P:634-641) re-cut for
+//    B200 as 8-lane groups, one LDG.128 per lane per slab step;
+//  * insert uses the search-then-claim protocol: pass 1
+//    walks the slab list up to the first slab holding an EMPTY cell, looking
+//    for the key and remembering the first writable (EMPTY or TOMBSTONE) cell;
+//    pass 2 claims that cell with one CAS (64-bit for map pairs) and rescans
+//    from it on failure; a full list gets a pool slab linked into lane 31 by
+//    CAS ("chained at the end of the last filled slab").  A present key
+//    keeps the minimum weight via a 64-bit atomicMin on the <key, w> pair (C8).
+#include <cub/cub.cuh>
+
+#include "graph.h"
+
+namespace mk {
+
+// ------------------------------------------------------------------ helpers
+
+__device__ __forceinline__ uint32_t fill_word(bool map, int word) {
+  if (word == SLAB_WORDS - 1) return INVALID_SLAB;
+  if (map) return (word & 1) ? 0xFFFFFFFFu : EMPTY_KEY;   // pair = UINT64_MAX-1 (P:1504 footnote)
+  return EMPTY_KEY;
+}
+
+// Group-cooperative: take one slab from the pool, write the EMPTY pattern with
+// `first` in cell 0, record its owner, and fence it before it can be published.
+template <bool MAP>
+__device__ uint32_t group_alloc(const GraphDev& G, uint32_t u, uint64_t first, int l8, uint32_t gmask) {
+  unsigned long long idx = 0;
+  if (l8 == 0) idx = atomicAdd(&G.ctrl->pool_top, 1ull);
+  idx = __shfl_sync(gmask, idx, 0, GROUP);
+  if (idx >= G.P) return INVALID_SLAB;
+  uint32_t s = G.H + (uint32_t)idx;
+  uint4 f;
+  f.x = fill_word(MAP, 4 * l8 + 0); f.y = fill_word(MAP, 4 * l8 + 1);
+  f.z = fill_word(MAP, 4 * l8 + 2); f.w = fill_word(MAP, 4 * l8 + 3);
+  if (l8 == 0) { f.x = (uint32_t)first; if (MAP) f.y = (uint32_t)(first >> 32); }
+  reinterpret_cast<uint4*>(slab_ptr(G, s))[l8] = f;
+  if (l8 == 0) G.owner[s] = u;
+  __threadfence();
+  __syncwarp(gmask);
+  return s;
+}
+
+// Link a fresh slab holding `item` into *link (a lane-31 next word, or a vertex's
+// head word) under a LINKING lock, so exactly one group allocates per link point
+// and no slab is ever lost to a race ("chained at the end of the last
+// filled slab").  Returns 1: our slab (holding the key) is linked; -1: pool
+// exhausted; 0: another group linked first — *next_out is its slab, or
+// INVALID_SLAB if that group failed to allocate.
+template <bool MAP>
+__device__ int group_link(const GraphDev& G, uint32_t u, uint64_t item, uint32_t* link, uint32_t& next_out, int l8,
+                          uint32_t gmask) {
+  uint32_t old = 0;
+  if (l8 == 0) old = atomicCAS(link, INVALID_SLAB, LINKING);
+  old = __shfl_sync(gmask, old, 0, GROUP);
+  if (old == INVALID_SLAB) {
+    const uint32_t s = group_alloc<MAP>(G, u, item, l8, gmask);   // fenced before publication
+    if (l8 == 0) atomicExch(link, s);                              // s == INVALID_SLAB releases the lock
+    __syncwarp(gmask);
+    return s == INVALID_SLAB ? -1 : 1;
+  }
+  while (old == LINKING) {   // another group holds the lock: wait for its pointer
+    __nanosleep(64);
+    if (l8 == 0) old = *reinterpret_cast<volatile uint32_t*>(link);
+    old = __shfl_sync(gmask, old, 0, GROUP);
+  }
+  next_out = old;
+  return 0;
+}
+
+__device__ __forceinline__ uint32_t ld_head_cg(const GraphDev& G, uint32_t u) {
+  return __ldcg(reinterpret_cast<const unsigned int*>(&G.vmeta[u].x));
+}
+
+// ------------------------------------------------------------------ insert (C9)
+
+// Returns 1 = inserted (key was absent), 0 = present (weight min-upserted), -1 = pool exhausted.
+template <bool MAP>
+__device__ int group_insert(const GraphDev& G, uint32_t u, uint32_t v, uint32_t wt, int l8, uint32_t gmask,
+                            int gbase) {
+  using F = Frag<MAP>;
+  constexpr int NK = F::NK;
+  const uint64_t item = MAP ? (((uint64_t)wt << 32) | v) : (uint64_t)v;
+  const uint32_t count = G.vmeta[u].y;
+  uint32_t head = ld_head_cg(G, u);
+  int result = 0;
+  while (head == INVALID_SLAB || head == LINKING) {
+    // vertex without a head slab yet (hint 0, reading C22b): publish one holding the key
+    uint32_t nxt = INVALID_SLAB;
+    const int r = group_link<MAP>(G, u, item, reinterpret_cast<uint32_t*>(&G.vmeta[u].x), nxt, l8, gmask);
+    if (r != 0) return r;
+    head = nxt;
+  }
+  uint32_t cur = head + bucket_of(v, count, G.seed);
+  for (;;) {
+    // ---- pass 1: search up to the first slab with an EMPTY cell, remember the first writable cell
+    uint32_t cand_slab = INVALID_SLAB, tail = INVALID_SLAB;
+    int cand_cell = -1;
+    uint64_t cand_old = 0;
+    uint32_t s = cur;
+    int found_cell = -1;
+    uint32_t found_slab = INVALID_SLAB;
+    for (;;) {
+      const uint4 d = ld_slab_cg(slab_ptr(G, s), l8);
+      uint32_t mb = 0, wb = 0, eb = 0;
+#pragma unroll
+      for (int k = 0; k < NK; k++) {
+        const uint32_t key = F::key(d, k);
+        const bool ok = F::valid_cell(l8, k);
+        mb |= (uint32_t)(ok && key == v) << k;
+        wb |= (uint32_t)(ok && (key == EMPTY_KEY || key == TOMBSTONE_KEY)) << k;
+        eb |= (uint32_t)(ok && key == EMPTY_KEY) << k;
+      }
+      const int mc = group_first_cell<NK>(mb, gmask, gbase);
+      if (mc >= 0) { found_cell = mc; found_slab = s; break; }
+      if (cand_slab == INVALID_SLAB) {
+        const int wc = group_first_cell<NK>(wb, gmask, gbase);
+        if (wc >= 0) {
+          const int src_lane = wc / NK, k = wc % NK;
+          uint32_t lo = MAP ? (k == 0 ? d.x : d.z) : F::key(d, k);
+          uint32_t hi = MAP ? (k == 0 ? d.y : d.w) : 0u;
+          lo = __shfl_sync(gmask, lo, src_lane, GROUP);
+          hi = __shfl_sync(gmask, hi, src_lane, GROUP);
+          cand_slab = s; cand_cell = wc; cand_old = ((uint64_t)hi << 32) | lo;
+        }
+      }
+      const bool has_empty = ((__ballot_sync(gmask, eb != 0) >> gbase) & 0xFFu) != 0;
+      const uint32_t nxt = __shfl_sync(gmask, d.w, GROUP - 1, GROUP);
+      if (has_empty || nxt == INVALID_SLAB || nxt == LINKING) { tail = s; break; }
+      s = nxt;
+    }
+    if (found_cell >= 0) {
+      // present: min-weight upsert on the <key, w> pair (C8); the key half is equal
+      if (MAP && l8 == 0)
+        atomicMin(reinterpret_cast<unsigned long long*>(slab_ptr(G, found_slab) + 2 * found_cell),
+                  (unsigned long long)item);
+      result = 0;
+      break;
+    }
+    if (cand_slab != INVALID_SLAB) {
+      // ---- pass 2: claim the remembered first writable cell
+      bool ok = false;
+      if (l8 == 0) {
+        if (MAP) {
+          unsigned long long* cell = reinterpret_cast<unsigned long long*>(slab_ptr(G, cand_slab) + 2 * cand_cell);
+          ok = atomicCAS(cell, (unsigned long long)cand_old, (unsigned long long)item) == cand_old;
+        } else {
+          unsigned int* cell = slab_ptr(G, cand_slab) + cand_cell;
+          ok = atomicCAS(cell, (unsigned int)cand_old, (unsigned int)item) == (unsigned int)cand_old;
+        }
+      }
+      ok = __shfl_sync(gmask, (int)ok, 0, GROUP);
+      if (ok) { result = 1; break; }
+      cur = cand_slab;  // the cell changed under us: rescan from its slab
+      continue;
+    }
+    // ---- list full: link a pool slab holding the key after the tail
+    uint32_t nxt = INVALID_SLAB;
+    const int r = group_link<MAP>(G, u, item, slab_ptr(G, tail) + (SLAB_WORDS - 1), nxt, l8, gmask);
+    if (r != 0) { result = r; break; }
+    cur = nxt == INVALID_SLAB ? tail : nxt;   // continue in the slab another group linked
+  }
+  return result;
+}
+
+// Block-aggregated add of a per-thread count into two global counters (one atomic each per block).
+__device__ __forceinline__ void block_add(unsigned long long* d0, unsigned long long* d1, uint32_t v) {
+  __shared__ unsigned long long acc;
+  if (threadIdx.x == 0) acc = 0;
+  __syncthreads();
+  v = __reduce_add_sync(0xFFFFFFFFu, v);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(&acc, (unsigned long long)v);
+  __syncthreads();
+  if (threadIdx.x == 0 && acc) { atomicAdd(d0, acc); atomicAdd(d1, acc); }
+}
+
+__device__ __forceinline__ void block_or_err(unsigned int* dst, uint32_t e) {
+  e = __reduce_or_sync(0xFFFFFFFFu, e);
+  if ((threadIdx.x & 31) == 0 && e) atomicOr(dst, e);
+}
+
+constexpr int UPD_BLOCK = 256;
+
+template <bool MAP>
+__global__ void __launch_bounds__(UPD_BLOCK) k_insert(GraphDev G, const uint32_t* __restrict__ src,
+                                                      const uint32_t* __restrict__ dst,
+                                                      const uint32_t* __restrict__ w, uint64_t n) {
+  const int lane = lane_id(), l8 = lane & 7, gbase = lane & 24;
+  const uint32_t gmask = 0xFFu << gbase;
+  const uint64_t ng = ((uint64_t)gridDim.x * blockDim.x) / GROUP;
+  uint32_t added = 0, err = 0;
+  for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / GROUP; i < n; i += ng) {
+    const uint32_t u = src[i], v = dst[i], wt = MAP ? w[i] : 0u;
+    if (u >= G.V || v >= G.V) { err |= ERR_RANGE; continue; }
+    if (MAP && (wt == 0 || wt >= W_LIMIT)) { err |= ERR_WEIGHT; continue; }
+    const int r = group_insert<MAP>(G, u, v, wt, l8, gmask, gbase);
+    if (r < 0) err |= ERR_CAPACITY;
+    else if (l8 == 0) added += (uint32_t)r;
+  }
+  block_or_err(&G.ctrl->err, err);
+  block_add(&G.ctrl->n_inserted, &G.ctrl->ins_total, added);
+}
+
+// ------------------------------------------------------------------ delete / query
+
+// Walk the slab list of (u, bucket(v)) up to the first slab with an EMPTY cell.
+// Returns the matching cell (or -1) and its slab / observed value.
+template <bool MAP>
+__device__ int group_find(const GraphDev& G, uint32_t u, uint32_t v, int l8, uint32_t gmask, int gbase,
+                          uint32_t& slab_out, uint64_t& val_out) {
+  using F = Frag<MAP>;
+  constexpr int NK = F::NK;
+  const uint32_t head = ld_head_cg(G, u);
+  if (head == INVALID_SLAB) return -1;
+  uint32_t s = head + bucket_of(v, G.vmeta[u].y, G.seed);
+  for (;;) {
+    const uint4 d = ld_slab_cg(slab_ptr(G, s), l8);
+    uint32_t mb = 0, eb = 0;
+#pragma unroll
+    for (int k = 0; k < NK; k++) {
+      const uint32_t key = F::key(d, k);
+      const bool ok = F::valid_cell(l8, k);
+      mb |= (uint32_t)(ok && key == v) << k;
+      eb |= (uint32_t)(ok && key == EMPTY_KEY) << k;
+    }
+    const int mc = group_first_cell<NK>(mb, gmask, gbase);
+    if (mc >= 0) {
+      const int src_lane = mc / NK, k = mc % NK;
+      uint32_t lo = MAP ? (k == 0 ? d.x : d.z) : F::key(d, k);
+      uint32_t hi = MAP ? (k == 0 ? d.y : d.w) : 0u;
+      lo = __shfl_sync(gmask, lo, src_lane, GROUP);
+      hi = __shfl_sync(gmask, hi, src_lane, GROUP);
+      slab_out = s;
+      val_out = ((uint64_t)hi << 32) | lo;
+      return mc;
+    }
+    const bool has_empty = ((__ballot_sync(gmask, eb != 0) >> gbase) & 0xFFu) != 0;
+    const uint32_t nxt = __shfl_sync(gmask, d.w, GROUP - 1, GROUP);
+    if (has_empty || nxt == INVALID_SLAB) return -1;
+    s = nxt;
+  }
+}
+
+template <bool MAP>
+__global__ void __launch_bounds__(UPD_BLOCK) k_delete(GraphDev G, const uint32_t* __restrict__ src,
+                                                      const uint32_t* __restrict__ dst, uint64_t n) {
+  const int lane = lane_id(), l8 = lane & 7, gbase = lane & 24;
+  const uint32_t gmask = 0xFFu << gbase;
+  const uint64_t ng = ((uint64_t)gridDim.x * blockDim.x) / GROUP;
+  uint32_t removed = 0, err = 0;
+  for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / GROUP; i < n; i += ng) {
+    const uint32_t u = src[i], v = dst[i];
+    if (u >= G.V || v >= G.V) { err |= ERR_RANGE; continue; }
+    uint32_t slab; uint64_t val;
+    const int c = group_find<MAP>(G, u, v, l8, gmask, gbase, slab, val);
+    if (c < 0 || l8 != 0) continue;
+    // TOMBSTONE the cell; a failed CAS means a duplicate in this batch won
+    bool ok;
+    if (MAP) ok = atomicCAS(reinterpret_cast<unsigned long long*>(slab_ptr(G, slab) + 2 * c),
+                            (unsigned long long)val, (unsigned long long)TOMB_PAIR) == val;
+    else ok = atomicCAS(slab_ptr(G, slab) + c, (unsigned int)val, TOMBSTONE_KEY) == (unsigned int)val;
+    removed += ok;
+  }
+  block_or_err(&G.ctrl->err, err);
+  block_add(&G.ctrl->n_deleted, &G.ctrl->del_total, removed);
+}
+
+template <bool MAP>
+__global__ void __launch_bounds__(UPD_BLOCK) k_query(GraphDev G, const uint32_t* __restrict__ src,
+                                                     const uint32_t* __restrict__ dst, uint64_t n,
+                                                     uint8_t* __restrict__ found, uint32_t* __restrict__ w_out) {
+  const int lane = lane_id(), l8 = lane & 7, gbase = lane & 24;
+  const uint32_t gmask = 0xFFu << gbase;
+  const uint64_t ng = ((uint64_t)gridDim.x * blockDim.x) / GROUP;
+  uint32_t err = 0;
+  for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / GROUP; i < n; i += ng) {
+    const uint32_t u = src[i], v = dst[i];
+    int c = -1;
+    uint32_t slab; uint64_t val = 0;
+    if (u >= G.V || v >= G.V) err |= ERR_RANGE;
+    else c = group_find<MAP>(G, u, v, l8, gmask, gbase, slab, val);
+    if (l8 == 0) {
+      found[i] = c >= 0;
+      if (w_out) w_out[i] = (MAP && c >= 0) ? (uint32_t)(val >> 32) : 0u;
+    }
+  }
+  block_or_err(&G.ctrl->err, err);
+}
+
+// ------------------------------------------------------------------ export (streaming)
+
+template <bool MAP>
+__global__ void __launch_bounds__(UPD_BLOCK) k_export(GraphDev G, uint64_t n_slabs, uint32_t* __restrict__ os,
+                                                      uint32_t* __restrict__ od, uint32_t* __restrict__ ow,
+                                                      uint64_t cap) {
+  using F = Frag<MAP>;
+  constexpr int NK = F::NK;
+  const int lane = lane_id(), l8 = lane & 7;
+  const uint64_t ng = ((uint64_t)gridDim.x * blockDim.x) / GROUP;
+  const uint64_t g0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / GROUP;
+  const uint64_t trips = (n_slabs + ng - 1) / ng;  // warp-uniform trip count
+  for (uint64_t t = 0; t < trips; t++) {
+    const uint64_t s = g0 + t * ng;
+    uint4 d = make_uint4(EMPTY_KEY, EMPTY_KEY, EMPTY_KEY, EMPTY_KEY);
+    uint32_t own = NO_OWNER;
+    if (s < n_slabs) {
+      own = G.owner[s];
+      if (own != NO_OWNER) d = ld_slab_cg(slab_ptr(G, (uint32_t)s), l8);
+    }
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int k = 0; k < NK; k++) {
+      const uint32_t key = F::key(d, k);
+      cnt += (own != NO_OWNER && F::valid_cell(l8, k) && key != EMPTY_KEY && key != TOMBSTONE_KEY);
+    }
+    // warp-aggregated append (warpenqueuefrontier pattern)
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    unsigned long long base = 0;
+    if (lane == 31 && total) base = atomicAdd(&G.ctrl->export_n, (unsigned long long)total);
+    base = __shfl_sync(0xFFFFFFFFu, base, 31);
+    uint64_t o = base + incl - cnt;
+#pragma unroll
+    for (int k = 0; k < NK; k++) {
+      const uint32_t key = F::key(d, k);
+      if (own != NO_OWNER && F::valid_cell(l8, k) && key != EMPTY_KEY && key != TOMBSTONE_KEY) {
+        if (o < cap) { os[o] = own; od[o] = key; if (ow) ow[o] = MAP ? F::weight(d, k) : 0u; }
+        o++;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ construction
+
+__global__ void k_bucket_counts(const uint32_t* __restrict__ hints, uint32_t V, double lf_cap, int hashing,
+                                uint32_t* __restrict__ count, uint64_t* __restrict__ heads,
+                                unsigned long long* __restrict__ total) {
+  unsigned long long mine = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t trips = (V + stride - 1) / stride;
+  for (uint64_t t = 0; t < trips; t++) {
+    const uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x + t * stride;
+    if (v >= V) continue;
+    const uint32_t hint = hints ? hints[v] : 1u;   // no hints: one bucket per vertex
+    uint32_t c = 1;
+    if (hashing && hint > 0) {
+      const double q = ceil((double)hint / lf_cap);   // ceil(hint / (lf * capacity))
+      c = q < 1.0 ? 1u : (q > 4294967295.0 ? 0xFFFFFFFFu : (uint32_t)q);
+    }
+    count[v] = c;
+    heads[v] = hint > 0 ? c : 0;   // hint 0: no arena head, allocated lazily on first insert (C22b)
+    mine += c;
+  }
+  for (int o = 16; o; o >>= 1) mine += __shfl_down_sync(0xFFFFFFFFu, mine, o);
+  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(total, mine);
+}
+
+__global__ void k_init_meta(GraphDev G, const uint32_t* __restrict__ count, const uint64_t* __restrict__ first,
+                            const uint64_t* __restrict__ heads) {
+  for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < G.V; v += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t h = heads[v], f = first[v];
+    G.vmeta[v] = make_uint2(h ? (uint32_t)f : INVALID_SLAB, count[v]);
+    for (uint64_t i = 0; i < h; i++) G.owner[f + i] = (uint32_t)v;
+  }
+}
+
+__global__ void k_fill(uint32_t* __restrict__ slabs, uint64_t n_slabs, int map) {
+  const uint64_t n16 = n_slabs * (SLAB_WORDS / 4);
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (uint64_t)gridDim.x * blockDim.x) {
+    const int w0 = (int)(i & 7) * 4;
+    uint4 f;
+    f.x = fill_word(map, w0); f.y = fill_word(map, w0 + 1); f.z = fill_word(map, w0 + 2); f.w = fill_word(map, w0 + 3);
+    reinterpret_cast<uint4*>(slabs)[i] = f;
+  }
+}
+
+// ------------------------------------------------------------------ host launchers
+
+static inline unsigned grid_for(meerkat_graph* g, uint64_t groups) {
+  const uint64_t per_block = UPD_BLOCK / GROUP;
+  uint64_t b = (groups + per_block - 1) / per_block;
+  const uint64_t cap = (uint64_t)g->sm_count * 8;   // 8 resident 256-thread blocks per SM
+  if (b > cap) b = cap;
+  return (unsigned)(b ? b : 1);
+}
+
+cudaError_t launch_build(meerkat_graph* g, const uint32_t* d_hints) {
+  const uint32_t V = g->V;
+  const int cap = g->weighted ? MAP_CAP : SET_CAP;
+  uint32_t* count = nullptr;
+  uint64_t *heads = nullptr, *first = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  cudaError_t e;
+#define CK(x) do { e = (x); if (e != cudaSuccess) goto out; } while (0)
+  CK(cudaMalloc(&count, (size_t)V * 4));
+  CK(cudaMalloc(&heads, (size_t)V * 8));
+  CK(cudaMalloc(&first, ((size_t)V + 2) * 8));
+  {
+    const unsigned gb = (unsigned)std::min<uint64_t>((V + 255) / 256, (uint64_t)g->sm_count * 16);
+    unsigned long long* total = reinterpret_cast<unsigned long long*>(first + V + 1);
+    CK(cudaMemsetAsync(total, 0, 8, g->stream));
+    k_bucket_counts<<<gb, 256, 0, g->stream>>>(d_hints, V, (double)g->lf * cap, g->hashing ? 1 : 0, count, heads,
+                                               total);
+    g->launches++;
+    CK(cudaGetLastError());
+    CK(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, heads, first + 1, V, g->stream));
+    CK(cudaMalloc(&tmp, tmp_bytes));
+    CK(cudaMemsetAsync(first, 0, 8, g->stream));
+    CK(cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, heads, first + 1, V, g->stream));   // first = exclusive scan
+    g->launches++;
+    uint64_t HB[2] = {0, 0};
+    CK(cudaMemcpyAsync(HB, first + V, 16, cudaMemcpyDeviceToHost, g->stream));
+    CK(cudaStreamSynchronize(g->stream));
+    const uint64_t H = HB[0];
+    g->buckets = HB[1];
+    // total slab lists = arena heads + one lazy head per hint-0 vertex
+    g->H = H;
+    if (g->P == 0) g->P = H / 2 + V / 2 + 65536;
+    if (g->H + g->P >= 0xFFFFFFF0ull) { e = cudaErrorInvalidValue; goto out; }
+    const size_t nslab = (size_t)(g->H + g->P);
+    CK(cudaMalloc(&g->dev.slabs, nslab * 128));             // ONE allocation: head arena + pool
+    CK(cudaMalloc(&g->dev.owner, nslab * 4));
+    CK(cudaMalloc(&g->dev.vmeta, (size_t)V * 8));
+    CK(cudaMalloc(&g->dev.ctrl, sizeof(GraphCtrl)));
+    CK(cudaMemsetAsync(g->dev.ctrl, 0, sizeof(GraphCtrl), g->stream));
+    g->bytes = nslab * 132 + (size_t)V * 8 + sizeof(GraphCtrl);
+    g->dev.V = V; g->dev.H = (uint32_t)g->H; g->dev.P = (uint32_t)g->P;
+    if (g->H) {
+      const unsigned gf = (unsigned)std::min<uint64_t>((g->H * 8 + 255) / 256, (uint64_t)g->sm_count * 16);
+      k_fill<<<gf, 256, 0, g->stream>>>(g->dev.slabs, g->H, g->weighted ? 1 : 0);
+      g->launches++;
+    }
+    k_init_meta<<<gb, 256, 0, g->stream>>>(g->dev, count, first, heads);
+    g->launches++;
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(g->stream));
+  }
+out:
+#undef CK
+  cudaFree(count); cudaFree(heads); cudaFree(first); cudaFree(tmp);
+  return e;
+}
+
+cudaError_t launch_insert(meerkat_graph* g, const uint32_t* s, const uint32_t* d, const uint32_t* w, uint64_t n) {
+  if (!n) return cudaSuccess;
+  const unsigned gb = grid_for(g, n);
+  if (g->weighted) k_insert<true><<<gb, UPD_BLOCK, 0, g->stream>>>(g->dev, s, d, w, n);
+  else k_insert<false><<<gb, UPD_BLOCK, 0, g->stream>>>(g->dev, s, d, nullptr, n);
+  g->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_delete(meerkat_graph* g, const uint32_t* s, const uint32_t* d, uint64_t n) {
+  if (!n) return cudaSuccess;
+  const unsigned gb = grid_for(g, n);
+  if (g->weighted) k_delete<true><<<gb, UPD_BLOCK, 0, g->stream>>>(g->dev, s, d, n);
+  else k_delete<false><<<gb, UPD_BLOCK, 0, g->stream>>>(g->dev, s, d, n);
+  g->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_query(meerkat_graph* g, const uint32_t* s, const uint32_t* d, uint64_t n, uint8_t* found,
+                         uint32_t* w_out) {
+  if (!n) return cudaSuccess;
+  const unsigned gb = grid_for(g, n);
+  if (g->weighted) k_query<true><<<gb, UPD_BLOCK, 0, g->stream>>>(g->dev, s, d, n, found, w_out);
+  else k_query<false><<<gb, UPD_BLOCK, 0, g->stream>>>(g->dev, s, d, n, found, w_out);
+  g->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_export(meerkat_graph* g, uint32_t* s, uint32_t* d, uint32_t* w, uint64_t cap) {
+  cudaError_t e = cudaMemsetAsync(&g->dev.ctrl->export_n, 0, 8, g->stream);
+  if (e != cudaSuccess) return e;
+  // slabs in use: arena + pool handed out so far (read on the host: export synchronises anyway)
+  e = cudaMemcpyAsync(g->hctrl, g->dev.ctrl, sizeof(GraphCtrl), cudaMemcpyDeviceToHost, g->stream);
+  if (e != cudaSuccess) return e;
+  e = cudaStreamSynchronize(g->stream);
+  if (e != cudaSuccess) return e;
+  const uint64_t used = std::min<uint64_t>(g->hctrl->pool_top, g->P);
+  const uint64_t n_slabs = g->H + used;
+  if (!n_slabs) return cudaSuccess;
+  const unsigned gb = grid_for(g, n_slabs);
+  if (g->weighted) k_export<true><<<gb, UPD_BLOCK, 0, g->stream>>>(g->dev, n_slabs, s, d, w, cap);
+  else k_export<false><<<gb, UPD_BLOCK, 0, g->stream>>>(g->dev, n_slabs, s, d, w, cap);
+  g->launches++;
+  return cudaGetLastError();
+}
+
+}  // namespace mk

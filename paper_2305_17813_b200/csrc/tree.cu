@@ -1,0 +1,457 @@
+// tree.cu — batch-dynamic SSSP / BFS over the slab store, as ONE persistent
+// cooperative kernel per tree call (no host round trip per frontier round).
+//
+// Method:
+//  * tree node = <distance, parent> packed in 64 bits, distance high, relaxed by
+//    one 64-bit atomicMin (footnote P:28-30; readings C1-C3);
+//  * static: node[v] <- UNREACHED, node[SRC] <- <0,SRC>, frontier from
+//    SRC (C16), repeat the relax kernel until the next frontier is empty
+//    (P:108-133); BFS static is the level-synchronous special case w = 1;
+//  * incremental prologue: the inserted batch is the initial frontier;
+//  * decremental prologue: invalidate v for every deleted tree edge
+//    (parent(v), v), propagate to the whole subtree T_v
+//    (done top-down over out-edges, reading C14), then seed from all
+//    edges (u, x) with u valid and x invalid (C15).
+//
+// B200 design:
+//  * frontier items are (vertex, bucket) pairs — the paper's <v, i> work list of
+//    IterationScheme2 — so a hub's slab lists spread over groups;
+//  * an item is expanded by an 8-lane group (one LDG.128 per lane per slab),
+//    relaxations are fused into the expansion (a vertex frontier with
+//    per-round de-duplication stamps instead of the paper's edge frontier, C17);
+//  * enqueue is the paper's warpenqueuefrontier (ballot, one atomicAdd per warp,
+//    prefix offsets), extended to write all bucket items of a vertex;
+//  * the decremental valid->invalid scan STREAMS the slab array in address order
+//    (arena + pool, owner[] gives each slab's source vertex) instead of chasing
+//    chains, tests each destination against a shared-memory hashed filter of the
+//    invalid set, and relaxes hits directly — a pure HBM stream;
+//  * rounds are separated by grid-wide barriers inside one launch.
+#include <cooperative_groups.h>
+
+#include "graph.h"
+
+namespace cg = cooperative_groups;
+
+namespace mk {
+
+constexpr int TREE_BLOCK = 512;
+constexpr int FILTER_WORDS = 16384;   // 64 KiB smem filter = 2^19 bits per block (decremental scan)
+constexpr int SCAN_UNROLL = 4;        // independent slabs in flight per group in the scan
+constexpr unsigned FULL = 0xFFFFFFFFu;
+
+enum Visit { RELAX = 0, PROPAGATE = 1 };
+
+struct TreeArgs {
+  GraphDev G;
+  TreeDev T;
+  const uint32_t* bs;   // batch (device)
+  const uint32_t* bd;
+  const uint32_t* bw;
+  uint64_t bn;
+  uint32_t unit;        // 1: BFS (w = 1)
+  uint32_t weighted;    // graph has weights (map store)
+  uint32_t filter_words;
+};
+
+struct Counters {
+  uint32_t items = 0, slabs = 0, visited = 0, improved = 0, scan_slabs = 0, hits = 0, batch = 0, err = 0;
+};
+
+__device__ __forceinline__ uint32_t filt_hash(uint32_t x, uint32_t nbits_mask) {
+  return mix32(x * 0x9E3779B9u + 0x7F4A7C15u) & nbits_mask;
+}
+
+__device__ __forceinline__ bool bit_test(const uint32_t* bits, uint32_t x) {
+  return (__ldcg(bits + (x >> 5)) >> (x & 31)) & 1u;
+}
+
+// warpenqueuefrontier: all 32 lanes call; lanes with `has` append
+// every (bucket, x) item of vertex x.  One atomicAdd per warp.
+__device__ __forceinline__ void warp_enqueue(const GraphDev& G, const TreeDev& T, uint64_t* fr,
+                                             unsigned long long* sz, bool has, uint32_t x, Counters& c) {
+  if (!__ballot_sync(FULL, has)) return;
+  const int lane = lane_id();
+  uint32_t cnt = 0;
+  if (has) {
+    const uint2 m = __ldcg(G.vmeta + x);
+    cnt = m.x == INVALID_SLAB ? 0u : m.y;   // a vertex without a head slab has no out-edges
+  }
+  uint32_t incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const uint32_t total = __shfl_sync(FULL, incl, 31);
+  if (!total) return;
+  unsigned long long base = 0;
+  if (lane == 31) base = atomicAdd(sz, (unsigned long long)total);
+  base = __shfl_sync(FULL, base, 31);
+  if (base + total > T.fr_cap) { c.err |= ERR_CAPACITY; return; }
+  const uint64_t off = base + incl - cnt;
+  if (cnt <= 8) {
+    for (uint32_t j = 0; j < cnt; j++) fr[off + j] = ((uint64_t)j << 32) | x;
+  }
+  uint32_t big = __ballot_sync(FULL, cnt > 8);
+  while (big) {
+    const int l = __ffs(big) - 1;
+    big &= big - 1;
+    const uint32_t xb = __shfl_sync(FULL, x, l);
+    const uint64_t ob = __shfl_sync(FULL, off, l);
+    const uint32_t cb = __shfl_sync(FULL, cnt, l);
+    for (uint32_t j = lane; j < cb; j += 32) fr[ob + j] = ((uint64_t)j << 32) | xb;
+  }
+}
+
+__device__ __forceinline__ void mark_invalid(const TreeDev& T, uint32_t x) {
+  atomicOr(T.inval_bits + (x >> 5), 1u << (x & 31));
+  const unsigned long long i = atomicAdd(&T.ctrl->inval_n, 1ull);
+  T.inval_list[i] = x;
+}
+
+// Relax candidate <dist, parent> into node[x]; true iff x must be (re-)expanded next round.
+__device__ __forceinline__ bool relax(const TreeDev& T, uint32_t x, uint64_t dist, uint32_t parent,
+                                      uint32_t epoch_next, Counters& c) {
+  if (dist >= INF_DIST) { c.err |= ERR_OVERFLOW; return false; }   // C5
+  const uint64_t cand = (dist << 32) | parent;
+  if (cand >= ld_cg_u64(T.node + x)) return false;                   // filter: node[] only decreases
+  const unsigned long long old = atomicMin(reinterpret_cast<unsigned long long*>(T.node + x), cand);
+  if (cand >= old) return false;
+  c.improved++;
+  return atomicExch(T.stamp + x, epoch_next) != epoch_next;
+}
+
+// Next live item of this group (grid-stride over [it, n)): sets v / slab / du.
+template <int VISIT>
+__device__ __forceinline__ bool fetch_item(const TreeArgs& A, const uint64_t* fr, uint64_t n, uint64_t ng,
+                                           uint64_t& it, uint32_t& v, uint32_t& slab, uint32_t& du, int l8,
+                                           Counters& c) {
+  for (; it < n; it += ng) {
+    const uint64_t item = fr[it];
+    v = (uint32_t)item;
+    const uint32_t head = __ldcg(reinterpret_cast<const unsigned int*>(&A.G.vmeta[v].x));
+    if (l8 == 0) c.items++;
+    if (head == INVALID_SLAB) continue;
+    slab = head + (uint32_t)(item >> 32);
+    if (VISIT == PROPAGATE) return true;
+    const uint64_t nv = ld_cg_u64(A.T.node + v);
+    if (nv != UNREACHED) { du = (uint32_t)(nv >> 32); return true; }
+  }
+  return false;
+}
+
+// Expand the frontier items [0, n) of `fr` (one 8-lane group per item), applying
+// VISIT to every live edge; successful vertices go to `fnext`.
+template <bool MAP, int VISIT>
+__device__ __forceinline__ void expand(const TreeArgs& A, const uint64_t* fr, uint64_t n, uint64_t* fnext,
+                                       unsigned long long* sznext, uint32_t epoch_next, Counters& c) {
+  using F = Frag<MAP>;
+  constexpr int NK = F::NK;
+  const GraphDev& G = A.G;
+  const TreeDev& T = A.T;
+  const int lane = lane_id(), l8 = lane & 7;
+  const uint64_t ng = ((uint64_t)gridDim.x * blockDim.x) / GROUP;
+  uint64_t it = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / GROUP;
+  uint32_t v = 0, slab = 0, du = 0;
+  bool active = fetch_item<VISIT>(A, fr, n, ng, it, v, slab, du, l8, c);
+  while (__any_sync(FULL, active)) {
+    uint4 d = make_uint4(EMPTY_KEY, EMPTY_KEY, EMPTY_KEY, INVALID_SLAB);
+    if (active) {
+      d = ld_slab_ro(slab_ptr(G, slab), l8);
+      if (l8 == 0) c.slabs++;
+    }
+#pragma unroll
+    for (int k = 0; k < NK; k++) {
+      const uint32_t x = F::key(d, k);
+      const bool live = active && F::valid_cell(l8, k) && x != EMPTY_KEY && x != TOMBSTONE_KEY;
+      bool enq = false;
+      if (live) {
+        c.visited++;
+        if (VISIT == RELAX) {
+          const uint32_t w = A.unit ? 1u : F::weight(d, k);
+          enq = relax(T, x, (uint64_t)du + w, v, epoch_next, c);
+        } else {
+          // PropagateInvalidation, top-down (C14): a child x of invalid v in T_G
+          const uint64_t cur = ld_cg_u64(T.node + x);
+          if (cur != UNREACHED && (uint32_t)cur == v && x != T.source) {
+            if (atomicCAS(reinterpret_cast<unsigned long long*>(T.node + x), (unsigned long long)cur,
+                          (unsigned long long)UNREACHED) == cur) {
+              mark_invalid(T, x);
+              enq = true;
+            }
+          }
+        }
+      }
+      warp_enqueue(G, T, fnext, sznext, enq, x, c);
+    }
+    const uint32_t nxt = __shfl_sync(FULL, d.w, (lane & 24) + GROUP - 1);
+    if (active) {
+      if (nxt != INVALID_SLAB) slab = nxt;
+      else { it += ng; active = fetch_item<VISIT>(A, fr, n, ng, it, v, slab, du, l8, c); }
+    }
+  }
+}
+
+// Frontier rounds until empty.  Round r reads fr[r&1] / size[r%3], writes
+// fr[(r+1)&1] / size[(r+1)%3]; size[(r+2)%3] (consumed two rounds ago) is
+// zeroed during round r so it is clean when it becomes "next".
+template <bool MAP, int VISIT>
+__device__ __forceinline__ uint32_t run_rounds(const TreeArgs& A, uint32_t epoch, cg::grid_group& grid, uint32_t r,
+                                               Counters& c) {
+  TreeCtrl* tc = A.T.ctrl;
+  for (;;) {
+    const uint64_t n = __ldcg(&tc->size[r % 3]);
+    if (n == 0) break;
+    if (blockIdx.x == 0 && threadIdx.x == 0) tc->size[(r + 2) % 3] = 0;
+    expand<MAP, VISIT>(A, A.T.fr[r & 1], n, A.T.fr[(r + 1) & 1], &tc->size[(r + 1) % 3], epoch + r + 1, c);
+    grid.sync();
+    r++;
+  }
+  return r;
+}
+
+__device__ void flush_counters(const TreeArgs& A, Counters& c, bool rounds_owner, uint32_t relax_rounds,
+                               uint32_t prop_rounds) {
+  TreeCtrl* tc = A.T.ctrl;
+  auto red = [](uint32_t v) { return __reduce_add_sync(FULL, v); };
+  const uint32_t items = red(c.items), slabs = red(c.slabs), visited = red(c.visited), imp = red(c.improved),
+                 ss = red(c.scan_slabs), hits = red(c.hits), batch = red(c.batch);
+  const uint32_t err = __reduce_or_sync(FULL, c.err);
+  if (lane_id() == 0) {
+    if (items) atomicAdd(&tc->items, (unsigned long long)items);
+    if (slabs) atomicAdd(&tc->slabs_read, (unsigned long long)slabs);
+    if (visited) atomicAdd(&tc->visited, (unsigned long long)visited);
+    if (imp) atomicAdd(&tc->improved, (unsigned long long)imp);
+    if (ss) atomicAdd(&tc->scan_slabs, (unsigned long long)ss);
+    if (hits) atomicAdd(&tc->scan_hits, (unsigned long long)hits);
+    if (batch) atomicAdd(&tc->batch_edges, (unsigned long long)batch);
+    if (err) atomicOr(&A.G.ctrl->err, err);
+  }
+  if (rounds_owner) { tc->rounds = relax_rounds; tc->prop_rounds = prop_rounds; }
+}
+
+// ------------------------------------------------------------------ static
+
+template <bool MAP>
+__global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_static(const __grid_constant__ TreeArgs A) {
+  const uint32_t epoch = __ldcg(A.T.epoch_ptr);
+  cg::grid_group grid = cg::this_grid();
+  Counters c;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
+  // init: every node <INF, INVALID>, SRC <0, SRC>
+  for (uint64_t v = tid; v < A.G.V; v += nt) A.T.node[v] = (v == A.T.source) ? (uint64_t)A.T.source : UNREACHED;
+  grid.sync();
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    const bool has = threadIdx.x == 0;
+    if (has) A.T.stamp[A.T.source] = epoch;
+    warp_enqueue(A.G, A.T, A.T.fr[0], &A.T.ctrl->size[0], has, A.T.source, c);   // frontier from SRC (C16)
+  }
+  grid.sync();
+  const uint32_t r = run_rounds<MAP, RELAX>(A, epoch, grid, 0, c);
+  if (tid == 0) *A.T.epoch_ptr = epoch + r + 2;   // every thread read the base before the first grid.sync
+  flush_counters(A, c, tid == 0, r, 0);
+}
+
+// ------------------------------------------------------------------ incremental
+
+template <bool MAP>
+__global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_inc(const __grid_constant__ TreeArgs A) {
+  const uint32_t epoch = __ldcg(A.T.epoch_ptr);
+  cg::grid_group grid = cg::this_grid();
+  Counters c;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t trips = (A.bn + nt - 1) / nt;   // warp-uniform trip count (warp_enqueue is collective)
+  for (uint64_t t = 0; t < trips; t++) {
+    const uint64_t i = tid + t * nt;
+    bool enq = false;
+    uint32_t v = 0;
+    if (i < A.bn) {
+      const uint32_t u = A.bs[i];
+      v = A.bd[i];
+      const uint32_t w = A.unit ? 1u : A.bw[i];
+      c.batch++;
+      const bool ok = u < A.G.V && v < A.G.V && (A.unit || (w != 0 && w < W_LIMIT));   // skipped at insert too
+      if (ok) {
+        const uint64_t nu = ld_cg_u64(A.T.node + u);
+        if (nu != UNREACHED) enq = relax(A.T, v, (nu >> 32) + w, u, epoch, c);
+      }
+    }
+    warp_enqueue(A.G, A.T, A.T.fr[0], &A.T.ctrl->size[0], enq, v, c);
+  }
+  grid.sync();
+  const uint32_t r = run_rounds<MAP, RELAX>(A, epoch, grid, 0, c);
+  if (tid == 0) *A.T.epoch_ptr = epoch + r + 2;
+  flush_counters(A, c, tid == 0, r, 0);
+}
+
+// ------------------------------------------------------------------ decremental
+
+template <bool MAP>
+__device__ __forceinline__ void dec_scan(const TreeArgs& A, const uint32_t* filt, uint32_t fmask, bool use_filter,
+                         uint64_t n_slabs, uint64_t* fnext, unsigned long long* sznext, uint32_t epoch_next,
+                         Counters& c) {
+  using F = Frag<MAP>;
+  constexpr int NK = F::NK;
+  const GraphDev& G = A.G;
+  const TreeDev& T = A.T;
+  const int l8 = lane_id() & 7;
+  const uint64_t ng = ((uint64_t)gridDim.x * blockDim.x) / GROUP;
+  const uint64_t g0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / GROUP;
+  const uint64_t span = ng * SCAN_UNROLL;
+  const uint64_t trips = (n_slabs + span - 1) / span;
+  for (uint64_t t = 0; t < trips; t++) {
+    uint4 d[SCAN_UNROLL];
+    uint64_t s[SCAN_UNROLL];
+#pragma unroll
+    for (int q = 0; q < SCAN_UNROLL; q++) {   // SCAN_UNROLL independent 16-B loads in flight per lane
+      s[q] = t * span + (uint64_t)q * ng + g0;
+      d[q] = s[q] < n_slabs ? ld_slab_ro(slab_ptr(G, (uint32_t)s[q]), l8)
+                            : make_uint4(EMPTY_KEY, EMPTY_KEY, EMPTY_KEY, INVALID_SLAB);
+    }
+#pragma unroll
+    for (int q = 0; q < SCAN_UNROLL; q++) {
+      if (s[q] < n_slabs && l8 == 0) c.scan_slabs++;
+#pragma unroll
+      for (int k = 0; k < NK; k++) {
+        const uint32_t x = F::key(d[q], k);
+        bool enq = false;
+        if (F::valid_cell(l8, k) && x < G.V) {   // live key (sentinels are >= V)
+          const uint32_t h = use_filter ? filt_hash(x, fmask) : 0u;
+          if ((!use_filter || ((filt[h >> 5] >> (h & 31)) & 1u)) && bit_test(T.inval_bits, x)) {
+            // x in V_invalid: is the slab's source vertex u valid (C15)?
+            const uint32_t u = __ldcg(G.owner + s[q]);
+            if (u != NO_OWNER && !bit_test(T.inval_bits, u)) {
+              const uint64_t nu = ld_cg_u64(T.node + u);
+              if (nu != UNREACHED) {
+                c.hits++;
+                const uint32_t w = A.unit ? 1u : F::weight(d[q], k);
+                enq = relax(T, x, (nu >> 32) + w, u, epoch_next, c);
+              }
+            }
+          }
+        }
+        warp_enqueue(G, T, fnext, sznext, enq, x, c);
+      }
+    }
+  }
+}
+
+template <bool MAP>
+__global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_dec(const __grid_constant__ TreeArgs A) {
+  extern __shared__ uint32_t filt[];
+  const uint32_t epoch = __ldcg(A.T.epoch_ptr);
+  cg::grid_group grid = cg::this_grid();
+  Counters c;
+  TreeCtrl* tc = A.T.ctrl;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
+  // (i) Invalidate: deleted tree edges (parent(v), v), v != SRC (C4)
+  const uint64_t trips = (A.bn + nt - 1) / nt;
+  for (uint64_t t = 0; t < trips; t++) {
+    const uint64_t i = tid + t * nt;
+    bool enq = false;
+    uint32_t v = 0;
+    if (i < A.bn) {
+      const uint32_t u = A.bs[i];
+      v = A.bd[i];
+      c.batch++;
+      if (u < A.G.V && v < A.G.V && v != A.T.source) {
+        const uint64_t cur = ld_cg_u64(A.T.node + v);
+        if (cur != UNREACHED && (uint32_t)cur == u &&
+            atomicCAS(reinterpret_cast<unsigned long long*>(A.T.node + v), (unsigned long long)cur,
+                      (unsigned long long)UNREACHED) == cur) {
+          mark_invalid(A.T, v);
+          atomicAdd(&tc->direct_n, 1ull);
+          enq = true;
+        }
+      }
+    }
+    warp_enqueue(A.G, A.T, A.T.fr[0], &tc->size[0], enq, v, c);
+  }
+  grid.sync();
+  // (ii) PropagateInvalidation to all of T_v
+  const uint32_t r1 = run_rounds<MAP, PROPAGATE>(A, epoch, grid, 0, c);
+  // (iii) valid -> invalid frontier, fused with the first relaxation
+  const uint64_t n_inv = __ldcg(&tc->inval_n);
+  if (n_inv) {
+    const uint32_t fw = A.filter_words;
+    const bool use_filter = fw && n_inv * 16 <= (uint64_t)fw * 32;   // keep the false-positive rate low
+    const uint32_t fmask = fw * 32 - 1;
+    if (use_filter) {
+      for (uint32_t i = threadIdx.x; i < fw; i += blockDim.x) filt[i] = 0;
+      __syncthreads();
+      for (uint64_t i = threadIdx.x; i < n_inv; i += blockDim.x) {
+        const uint32_t h = filt_hash(__ldcg(A.T.inval_list + i), fmask);
+        atomicOr(&filt[h >> 5], 1u << (h & 31));
+      }
+      __syncthreads();
+    }
+    const uint64_t n_slabs = A.G.H + min((unsigned long long)A.G.P, __ldcg(&A.G.ctrl->pool_top));
+    dec_scan<MAP>(A, filt, fmask, use_filter, n_slabs, A.T.fr[r1 & 1], &tc->size[r1 % 3], epoch + r1, c);
+  }
+  grid.sync();
+  // (iv) common epilogue
+  const uint32_t r2 = run_rounds<MAP, RELAX>(A, epoch, grid, r1, c);
+  // clear the invalid bit set for the next call (the list is kept for meerkat_tree_invalidated)
+  for (uint64_t i = tid; i < n_inv; i += nt) {
+    const uint32_t x = A.T.inval_list[i];
+    atomicAnd(A.T.inval_bits + (x >> 5), ~(1u << (x & 31)));
+  }
+  if (tid == 0) *A.T.epoch_ptr = epoch + r2 + 2;
+  flush_counters(A, c, tid == 0, r2 - r1, r1);
+}
+
+// ------------------------------------------------------------------ host side
+
+template <typename K>
+static cudaError_t occ(K kernel, int smem, int* out) {
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, kernel, TREE_BLOCK, smem);
+}
+
+cudaError_t tree_occupancy(meerkat_graph* g) {
+  cudaError_t e;
+  const int fbytes = FILTER_WORDS * 4;
+  if (g->weighted) {
+    if ((e = occ(k_tree_static<true>, 0, &g->tree_blocks_per_sm[0])) != cudaSuccess) return e;
+    if ((e = occ(k_tree_inc<true>, 0, &g->tree_blocks_per_sm[1])) != cudaSuccess) return e;
+    if ((e = occ(k_tree_dec<true>, fbytes, &g->tree_blocks_per_sm[2])) != cudaSuccess) return e;
+  } else {
+    if ((e = occ(k_tree_static<false>, 0, &g->tree_blocks_per_sm[0])) != cudaSuccess) return e;
+    if ((e = occ(k_tree_inc<false>, 0, &g->tree_blocks_per_sm[1])) != cudaSuccess) return e;
+    if ((e = occ(k_tree_dec<false>, fbytes, &g->tree_blocks_per_sm[2])) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t launch_tree(meerkat_graph* g, meerkat_tree* t, int mode, const uint32_t* s, const uint32_t* d,
+                        const uint32_t* w, uint64_t n) {
+  TreeArgs A;
+  A.G = g->dev;
+  A.T = t->dev;
+  A.bs = s; A.bd = d; A.bw = w; A.bn = n;
+  A.unit = t->unit ? 1u : 0u;
+  A.weighted = g->weighted ? 1u : 0u;
+  A.filter_words = FILTER_WORDS;
+  cudaError_t e = cudaMemsetAsync(t->dev.ctrl, 0, sizeof(TreeCtrl), g->stream);
+  if (e != cudaSuccess) return e;
+  const int bps = g->tree_blocks_per_sm[mode];
+  if (bps <= 0) return cudaErrorInvalidConfiguration;
+  dim3 grid((unsigned)(bps * g->sm_count)), block(TREE_BLOCK);
+  void* args[] = {&A};
+  const size_t smem = mode == MODE_DECREMENTAL ? (size_t)FILTER_WORDS * 4 : 0;
+  void* fn;
+  if (g->weighted)
+    fn = mode == MODE_STATIC ? (void*)k_tree_static<true> : mode == MODE_INCREMENTAL ? (void*)k_tree_inc<true>
+                                                                                     : (void*)k_tree_dec<true>;
+  else
+    fn = mode == MODE_STATIC ? (void*)k_tree_static<false> : mode == MODE_INCREMENTAL ? (void*)k_tree_inc<false>
+                                                                                      : (void*)k_tree_dec<false>;
+  e = cudaLaunchCooperativeKernel(fn, grid, block, args, smem, g->stream);
+  g->launches++;
+  return e;
+}
+
+}  // namespace mk

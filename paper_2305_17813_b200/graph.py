@@ -1,0 +1,221 @@
+"""Thin Python binding of include/meerkat.h (argument marshalling only).
+
+Every step of the hot path runs in libmeerkat.so's CUDA kernels; this module
+turns torch tensors / numpy arrays into pointers and statuses into exceptions.
+Arrays may live on the device (torch CUDA tensors) or on the host (numpy,
+CPU tensors); host arrays are staged by the library (meerkat.h "Pointer
+arguments").  Vertex ids and weights are 32-bit (uint32 or int32 bit patterns).
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from ._lib import check
+
+try:  # torch is plumbing only (device memory, streams)
+    import torch
+except Exception:  # pragma: no cover
+    torch = None
+
+
+def _is_torch(x):
+    return torch is not None and isinstance(x, torch.Tensor)
+
+
+def _u32(x):
+    """(pointer, keepalive, n) for a 32-bit id/weight array."""
+    if x is None:
+        return None, None, 0
+    if _is_torch(x):
+        if x.dtype not in (torch.int32, torch.uint32):
+            x = x.to(torch.int32)
+        x = x.contiguous()
+        return ctypes.c_void_p(x.data_ptr()), x, x.numel()
+    a = np.ascontiguousarray(np.asarray(x), dtype=np.uint32)
+    return ctypes.c_void_p(a.ctypes.data), a, a.size
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+class Graph:
+    """A dynamic graph G stored as per-vertex SlabHash tables on one GPU."""
+
+    def __init__(self, vertex_n: int, weighted: bool = True, hashing: bool = True, load_factor: float = 0.7,
+                 degree_hints=None, pool_slabs: int = 0, hash_seed: int = 0, device: int = 0, stream=None):
+        L = _lib.lib()
+        hp, self._hints_keep, _ = _u32(degree_hints)
+        cfg = _lib.Config(vertex_n=vertex_n, weighted=int(weighted), hashing=int(hashing),
+                          load_factor=float(load_factor), degree_hints=hp, pool_slabs=int(pool_slabs),
+                          hash_seed=int(hash_seed), device=int(device), stream=_stream_ptr(stream))
+        h = ctypes.c_void_p()
+        check(L.meerkat_create(ctypes.byref(cfg), ctypes.byref(h)), "meerkat_create")
+        self._h = h
+        self.vertex_n = int(vertex_n)
+        self.weighted = bool(weighted)
+        self.device = int(device)
+        self._trees = []
+
+    # ------------------------------------------------------------------ lifecycle
+    def close(self):
+        if getattr(self, "_h", None):
+            for t in list(self._trees):
+                t.close()
+            _lib.lib().meerkat_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream):
+        check(_lib.lib().meerkat_set_stream(self._h, _stream_ptr(stream)), "meerkat_set_stream")
+
+    def sync(self):
+        check(_lib.lib().meerkat_sync(self._h), "meerkat_sync")
+
+    # ------------------------------------------------------------------ batches
+    def insert(self, src, dst, w=None, count: bool = True, raise_on_error: bool = True):
+        sp, ks, n = _u32(src)
+        dp, kd, n2 = _u32(dst)
+        wp, kw, n3 = _u32(w)
+        assert n == n2 and (w is None or n3 == n)
+        out = ctypes.c_uint64(0)
+        st = _lib.lib().meerkat_insert_batch(self._h, sp, dp, wp, n, ctypes.byref(out) if count else None)
+        if raise_on_error:
+            check(st, "meerkat_insert_batch")
+        return (int(out.value) if count else None) if raise_on_error else (st, int(out.value))
+
+    def delete(self, src, dst, count: bool = True, raise_on_error: bool = True):
+        sp, ks, n = _u32(src)
+        dp, kd, n2 = _u32(dst)
+        assert n == n2
+        out = ctypes.c_uint64(0)
+        st = _lib.lib().meerkat_delete_batch(self._h, sp, dp, n, ctypes.byref(out) if count else None)
+        if raise_on_error:
+            check(st, "meerkat_delete_batch")
+        return (int(out.value) if count else None) if raise_on_error else (st, int(out.value))
+
+    def query(self, src, dst, raise_on_error: bool = True):
+        """found (uint8) and stored weight (uint32, 0 when absent) per queried edge."""
+        sp, ks, n = _u32(src)
+        dp, kd, n2 = _u32(dst)
+        assert n == n2
+        if _is_torch(src) and src.is_cuda:
+            found = torch.empty(n, dtype=torch.uint8, device=src.device)
+            w = torch.empty(n, dtype=torch.int32, device=src.device)
+            fp, wp = found.data_ptr(), w.data_ptr()
+        else:
+            found = np.zeros(n, np.uint8)
+            w = np.zeros(n, np.uint32)
+            fp, wp = found.ctypes.data, w.ctypes.data
+        st = _lib.lib().meerkat_query_batch(self._h, sp, dp, n, ctypes.c_void_p(fp), ctypes.c_void_p(wp))
+        if raise_on_error:
+            check(st, "meerkat_query_batch")
+            return found, w
+        return st, found, w
+
+    def export_edges(self):
+        """All live edges (src, dst, w) as host uint32 arrays, sorted by (src, dst)."""
+        L = _lib.lib()
+        n = ctypes.c_uint64(0)
+        st = L.meerkat_export_edges(self._h, None, None, None, 0, ctypes.byref(n))
+        if st not in (_lib.OK, _lib.E_CAPACITY):
+            check(st, "meerkat_export_edges")
+        cap = int(n.value)
+        s = np.zeros(max(cap, 1), np.uint32); d = np.zeros(max(cap, 1), np.uint32); w = np.zeros(max(cap, 1), np.uint32)
+        check(L.meerkat_export_edges(self._h, ctypes.c_void_p(s.ctypes.data), ctypes.c_void_p(d.ctypes.data),
+                                     ctypes.c_void_p(w.ctypes.data), cap, ctypes.byref(n)), "meerkat_export_edges")
+        m = int(n.value)
+        s, d, w = s[:m], d[:m], w[:m]
+        order = np.lexsort((d, s))
+        return s[order], d[order], w[order]
+
+    def stats(self) -> dict:
+        st = _lib.Stats()
+        check(_lib.lib().meerkat_stats_get(self._h, ctypes.byref(st)), "meerkat_stats_get")
+        return st.as_dict()
+
+    # ------------------------------------------------------------------ trees
+    def sssp(self, source: int) -> "Tree":
+        return Tree(self, source, unit=False)
+
+    def bfs(self, source: int) -> "Tree":
+        return Tree(self, source, unit=True)
+
+
+class Tree:
+    """Dependence tree T_G of packed <distance, parent> words."""
+
+    def __init__(self, graph: Graph, source: int, unit: bool):
+        L = _lib.lib()
+        h = ctypes.c_void_p()
+        fn = L.meerkat_bfs_create if unit else L.meerkat_sssp_create
+        check(fn(graph._h, source, ctypes.byref(h)), "meerkat_bfs_create" if unit else "meerkat_sssp_create")
+        self._h = h
+        self.graph = graph
+        self.unit = unit
+        self.source = source
+        graph._trees.append(self)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.lib().meerkat_tree_destroy(self._h)
+            self._h = None
+            if self in self.graph._trees:
+                self.graph._trees.remove(self)
+
+    def incremental(self, src, dst, w=None):
+        sp, ks, n = _u32(src)
+        dp, kd, _ = _u32(dst)
+        L = _lib.lib()
+        if self.unit:
+            check(L.meerkat_bfs_incremental(self.graph._h, self._h, sp, dp, n), "meerkat_bfs_incremental")
+        else:
+            wp, kw, _ = _u32(w)
+            check(L.meerkat_sssp_incremental(self.graph._h, self._h, sp, dp, wp, n), "meerkat_sssp_incremental")
+
+    def decremental(self, src, dst):
+        sp, ks, n = _u32(src)
+        dp, kd, _ = _u32(dst)
+        L = _lib.lib()
+        fn = L.meerkat_bfs_decremental if self.unit else L.meerkat_sssp_decremental
+        check(fn(self.graph._h, self._h, sp, dp, n), fn.__name__)
+
+    def recompute(self):
+        check(_lib.lib().meerkat_tree_recompute(self.graph._h, self._h), "meerkat_tree_recompute")
+
+    def nodes(self, out=None):
+        """Packed nodes, uint64 numpy array (or into a given int64 CUDA tensor)."""
+        if out is not None:
+            check(_lib.lib().meerkat_tree_nodes(self._h, ctypes.c_void_p(out.data_ptr())), "meerkat_tree_nodes")
+            return out
+        a = np.empty(self.graph.vertex_n, np.uint64)
+        check(_lib.lib().meerkat_tree_nodes(self._h, ctypes.c_void_p(a.ctypes.data)), "meerkat_tree_nodes")
+        return a
+
+    def invalidated(self):
+        L = _lib.lib()
+        n = ctypes.c_uint64(0)
+        st = L.meerkat_tree_invalidated(self._h, None, 0, ctypes.byref(n))
+        if st not in (_lib.OK, _lib.E_CAPACITY):
+            check(st, "meerkat_tree_invalidated")
+        a = np.zeros(max(int(n.value), 1), np.uint32)
+        check(L.meerkat_tree_invalidated(self._h, ctypes.c_void_p(a.ctypes.data), int(n.value), ctypes.byref(n)),
+              "meerkat_tree_invalidated")
+        return np.sort(a[: int(n.value)])
+
+    def stats(self) -> dict:
+        st = _lib.TreeStats()
+        check(_lib.lib().meerkat_tree_stats_get(self._h, ctypes.byref(st)), "meerkat_tree_stats_get")
+        return st.as_dict()

@@ -1,0 +1,84 @@
+"""C-ABI library checks that need no GPU: the in-tree libmeerkat.so loads and
+exports every function include/meerkat.h declares; status strings; create
+fails loudly (no CPU fallback) when no device is present; the product package
+never imports the oracle."""
+import ctypes
+import os
+import re
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _header_functions():
+    txt = open(os.path.join(ROOT, "include", "meerkat.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(meerkat_[a-z_]+)\s*\(", txt)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2305_17813_b200 import build, _lib
+    build.build()
+    return _lib.lib()
+
+
+def test_header_declares_expected_calls():
+    fns = _header_functions()
+    from paper_2305_17813_b200 import _lib
+    assert fns == sorted(_lib.EXPORTS)
+    for must in ("meerkat_create", "meerkat_insert_batch", "meerkat_delete_batch", "meerkat_query_batch",
+                 "meerkat_sssp_incremental", "meerkat_sssp_decremental", "meerkat_bfs_incremental",
+                 "meerkat_bfs_decremental", "meerkat_destroy"):
+        assert must in fns
+
+
+def test_library_exports_every_header_symbol(lib):
+    out = subprocess.run(["nm", "-D", "--defined-only", lib._name], capture_output=True, text=True).stdout
+    syms = set(re.findall(r" T (meerkat_\w+)", out))
+    missing = set(_header_functions()) - syms
+    assert not missing, missing
+
+
+def test_library_is_sm100a(lib):
+    out = subprocess.run(["cuobjdump", "--list-elf", lib._name], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_status_strings(lib):
+    assert lib.meerkat_status_string(0) == b"MEERKAT_OK"
+    assert lib.meerkat_status_string(6) == b"MEERKAT_E_STATE"
+
+
+def test_null_args_rejected(lib):
+    from paper_2305_17813_b200 import _lib
+    assert lib.meerkat_create(None, None) == _lib.E_INVALID_ARG
+    assert lib.meerkat_destroy(None) == _lib.E_INVALID_ARG
+    assert lib.meerkat_insert_batch(None, None, None, None, 0, None) == _lib.E_INVALID_ARG
+    cfg = _lib.Config(vertex_n=0)
+    h = ctypes.c_void_p()
+    assert lib.meerkat_create(ctypes.byref(cfg), ctypes.byref(h)) == _lib.E_INVALID_ARG
+    cfg = _lib.Config(vertex_n=10, load_factor=1.5)
+    assert lib.meerkat_create(ctypes.byref(cfg), ctypes.byref(h)) == _lib.E_INVALID_ARG
+
+
+def test_no_cpu_fallback_without_gpu(lib):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    from paper_2305_17813_b200 import Graph, MeerkatError
+    with pytest.raises(MeerkatError):
+        Graph(16)
+
+
+def test_product_package_does_not_import_oracle():
+    code = ("import sys; import paper_2305_17813_b200, paper_2305_17813_b200.graph; "
+            "bad=[m for m in sys.modules if m=='oracle' or m.startswith('oracle.')]; print(bad); assert not bad")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    for f in os.listdir(os.path.join(ROOT, "paper_2305_17813_b200")):
+        if f.endswith(".py"):
+            assert "import oracle" not in open(os.path.join(ROOT, "paper_2305_17813_b200", f)).read()
