@@ -47,6 +47,9 @@ def parse():
     p.add_argument("--batch", type=int, default=100_000)
     p.add_argument("--lf", type=float, default=0.7)
     p.add_argument("--no-hashing", action="store_true")
+    p.add_argument("--frontier", choices=["scan", "reverse"], default="scan",
+                   help="decremental valid->invalid frontier: stream every slab (paper, P:156-164) or "
+                        "read the in-edges of V_invalid from an in-edge mirror store")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-scale", type=int, default=20, help="R-MAT scale of the oracle's bounded sample")
@@ -209,8 +212,10 @@ def run_ours(args, ws, rank, local):
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.uint32).view(np.int32)).to(dev)
     bs, bd, bw = W.base
     hints = np.bincount(bs, minlength=V).astype(np.uint32)
+    rev = args.frontier == "reverse"
+    ihints = np.bincount(bd, minlength=V).astype(np.uint32) if rev else None
     g = Graph(V, weighted=True, hashing=not args.no_hashing, load_factor=args.lf, degree_hints=T(hints),
-              device=local, stream=stream)
+              device=local, stream=stream, reverse=rev, in_degree_hints=T(ihints) if rev else None)
     base_t = (T(bs), T(bd), T(bw))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -357,6 +362,7 @@ def run_ours(args, ws, rank, local):
                                f"batches (BASELINE config 3)",
                    "vertices": V, "edges": int(n_base), "batch": args.batch, "source": W.source,
                    "hashing": not args.no_hashing, "load_factor": args.lf,
+                   "decremental_frontier": args.frontier,
                    "parallelism": "single GPU" if ws == 1 else f"{ws} independent replicas",
                    "l2": "flushed between timed steps (256 MiB write, outside the intervals); store > L2"},
         "update_edges_per_s": 2 * args.batch / ((mean["insert"] + mean["delete"]) / 1e3),

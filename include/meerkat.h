@@ -77,6 +77,10 @@ typedef struct {
   uint64_t hash_seed;           /* bucket hash seed (storage only; results do not depend on it) */
   int device;                   /* CUDA device ordinal */
   void* stream;                 /* cudaStream_t for every call on this graph; NULL = default stream */
+  uint32_t reverse;             /* 1: also keep an in-edge mirror store, so the decremental
+                                   valid->invalid frontier reads only the in-edges of V_invalid
+                                   instead of scanning every slab (same result) */
+  const uint32_t* in_degree_hints; /* host or device [vertex_n] (in-degrees), or NULL; reverse only */
 } meerkat_config;
 
 typedef struct {
@@ -89,6 +93,9 @@ typedef struct {
   uint64_t bytes_device;    /* device bytes owned by the graph (excluding trees) */
   uint64_t kernel_launches; /* kernels this graph and its trees have launched since creation */
   uint64_t version;         /* mutation counter */
+  uint64_t in_edges;        /* reverse store: live in-edges (equals edges) */
+  uint64_t in_head_slabs;   /* reverse store: head arena slabs */
+  uint64_t in_pool_used;    /* reverse store: pool slabs handed out */
 } meerkat_stats;
 
 typedef struct {

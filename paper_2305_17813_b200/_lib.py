@@ -40,13 +40,14 @@ class Config(ctypes.Structure):
         ("vertex_n", ctypes.c_uint32), ("weighted", ctypes.c_uint32), ("hashing", ctypes.c_uint32),
         ("load_factor", ctypes.c_float), ("degree_hints", ctypes.c_void_p), ("pool_slabs", ctypes.c_uint64),
         ("hash_seed", ctypes.c_uint64), ("device", ctypes.c_int), ("stream", ctypes.c_void_p),
+        ("reverse", ctypes.c_uint32), ("in_degree_hints", ctypes.c_void_p),
     ]
 
 
 class Stats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint64) for n in (
         "vertex_n", "edges", "head_slabs", "buckets", "pool_capacity", "pool_used", "bytes_device",
-        "kernel_launches", "version")]
+        "kernel_launches", "version", "in_edges", "in_head_slabs", "in_pool_used")]
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}

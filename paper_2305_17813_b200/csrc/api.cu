@@ -70,12 +70,16 @@ cudaError_t stage_in(meerkat_graph* g, int slot, const void* p, size_t bytes, co
 
 // Read the control block back (synchronises); returns and clears the sticky error.
 meerkat_status collect(meerkat_graph* g) {
-  cudaError_t e = cudaMemcpyAsync(g->hctrl, g->dev.ctrl, sizeof(GraphCtrl), cudaMemcpyDeviceToHost, g->stream);
+  cudaError_t e = cudaMemcpyAsync(g->out.hctrl, g->out.dev.ctrl, sizeof(GraphCtrl), cudaMemcpyDeviceToHost, g->stream);
+  if (e == cudaSuccess && g->reverse)
+    e = cudaMemcpyAsync(g->in.hctrl, g->in.dev.ctrl, sizeof(GraphCtrl), cudaMemcpyDeviceToHost, g->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
   if (e != cudaSuccess) return MEERKAT_E_CUDA;
-  const uint32_t err = g->hctrl->err;
+  uint32_t err = g->out.hctrl->err;
+  if (g->reverse) err |= g->in.hctrl->err;
   if (err) {
-    if (cudaMemsetAsync(&g->dev.ctrl->err, 0, 4, g->stream) != cudaSuccess) return MEERKAT_E_CUDA;
+    if (cudaMemsetAsync(&g->out.dev.ctrl->err, 0, 4, g->stream) != cudaSuccess) return MEERKAT_E_CUDA;
+    if (g->reverse && cudaMemsetAsync(&g->in.dev.ctrl->err, 0, 4, g->stream) != cudaSuccess) return MEERKAT_E_CUDA;
   }
   return from_err(err);
 }
@@ -125,13 +129,17 @@ meerkat_status meerkat_create(const meerkat_config* cfg, meerkat_graph** out) {
   g->weighted = cfg->weighted != 0;
   g->hashing = cfg->hashing != 0;
   g->lf = lf;
-  g->P = cfg->pool_slabs;
-  g->dev.seed = (uint32_t)(cfg->hash_seed ^ (cfg->hash_seed >> 32)) ^ 0x5bd1e995u;
+  g->reverse = cfg->reverse != 0;
+  g->out.dev.seed = (uint32_t)(cfg->hash_seed ^ (cfg->hash_seed >> 32)) ^ 0x5bd1e995u;
+  g->in.dev.seed = g->out.dev.seed ^ 0x27d4eb2fu;
   cudaError_t e = cudaDeviceGetAttribute(&g->sm_count, cudaDevAttrMultiProcessorCount, g->device);
   const void* hints = nullptr;
-  if (e == cudaSuccess) e = cudaMallocHost(&g->hctrl, sizeof(GraphCtrl));
   if (e == cudaSuccess) e = stage_in(g, 0, cfg->degree_hints, (size_t)g->V * 4, &hints);
-  if (e == cudaSuccess) e = launch_build(g, static_cast<const uint32_t*>(hints));
+  if (e == cudaSuccess) e = launch_build(g, g->out, static_cast<const uint32_t*>(hints), cfg->pool_slabs);
+  if (e == cudaSuccess && g->reverse) {
+    e = stage_in(g, 1, cfg->in_degree_hints, (size_t)g->V * 4, &hints);
+    if (e == cudaSuccess) e = launch_build(g, g->in, static_cast<const uint32_t*>(hints), cfg->pool_slabs);
+  }
   if (e == cudaSuccess) e = tree_occupancy(g);
   if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
   if (e != cudaSuccess) {
@@ -139,7 +147,6 @@ meerkat_status meerkat_create(const meerkat_config* cfg, meerkat_graph** out) {
     meerkat_destroy(g);
     return MEERKAT_E_CUDA;
   }
-  std::memset(g->hctrl, 0, sizeof(GraphCtrl));
   *out = g;
   return MEERKAT_OK;
 }
@@ -148,12 +155,9 @@ meerkat_status meerkat_destroy(meerkat_graph* g) {
   if (!g) return MEERKAT_E_INVALID_ARG;
   DeviceGuard dg(g->device);
   cudaStreamSynchronize(g->stream);
-  cudaFree(g->dev.slabs);
-  cudaFree(g->dev.owner);
-  cudaFree(g->dev.vmeta);
-  cudaFree(g->dev.ctrl);
+  free_store(g->out);
+  free_store(g->in);
   for (int i = 0; i < 4; i++) cudaFree(g->stage[i]);
-  if (g->hctrl) cudaFreeHost(g->hctrl);
   delete g;
   return MEERKAT_OK;
 }
@@ -182,15 +186,17 @@ meerkat_status meerkat_insert_batch(meerkat_graph* g, const uint32_t* src, const
   cudaError_t e = stage_in(g, 0, src, n * 4, &s);
   if (e == cudaSuccess) e = stage_in(g, 1, dst, n * 4, &d);
   if (e == cudaSuccess && w) e = stage_in(g, 2, w, n * 4, &ww);
-  if (e == cudaSuccess && n_inserted) e = cudaMemsetAsync(&g->dev.ctrl->n_inserted, 0, 8, g->stream);
+  if (e == cudaSuccess && n_inserted) e = cudaMemsetAsync(&g->out.dev.ctrl->n_inserted, 0, 8, g->stream);
   if (e == cudaSuccess)
-    e = launch_insert(g, (const uint32_t*)s, (const uint32_t*)d, (const uint32_t*)ww, n);
+    e = launch_insert(g, g->out, (const uint32_t*)s, (const uint32_t*)d, (const uint32_t*)ww, n);
+  if (e == cudaSuccess && g->reverse)   // in-edge mirror: (dst, src, w)
+    e = launch_insert(g, g->in, (const uint32_t*)d, (const uint32_t*)s, (const uint32_t*)ww, n);
   if (e != cudaSuccess) return MEERKAT_E_CUDA;
   g->version++;
   g->last_kind = 1;
   if (!n_inserted) return MEERKAT_OK;
   st = collect(g);
-  *n_inserted = g->hctrl->n_inserted;
+  *n_inserted = g->out.hctrl->n_inserted;
   return st;
 }
 
@@ -202,14 +208,15 @@ meerkat_status meerkat_delete_batch(meerkat_graph* g, const uint32_t* src, const
   const void *s, *d;
   cudaError_t e = stage_in(g, 0, src, n * 4, &s);
   if (e == cudaSuccess) e = stage_in(g, 1, dst, n * 4, &d);
-  if (e == cudaSuccess && n_deleted) e = cudaMemsetAsync(&g->dev.ctrl->n_deleted, 0, 8, g->stream);
-  if (e == cudaSuccess) e = launch_delete(g, (const uint32_t*)s, (const uint32_t*)d, n);
+  if (e == cudaSuccess && n_deleted) e = cudaMemsetAsync(&g->out.dev.ctrl->n_deleted, 0, 8, g->stream);
+  if (e == cudaSuccess) e = launch_delete(g, g->out, (const uint32_t*)s, (const uint32_t*)d, n);
+  if (e == cudaSuccess && g->reverse) e = launch_delete(g, g->in, (const uint32_t*)d, (const uint32_t*)s, n);
   if (e != cudaSuccess) return MEERKAT_E_CUDA;
   g->version++;
   g->last_kind = 2;
   if (!n_deleted) return MEERKAT_OK;
   st = collect(g);
-  *n_deleted = g->hctrl->n_deleted;
+  *n_deleted = g->out.hctrl->n_deleted;
   return st;
 }
 
@@ -229,7 +236,7 @@ meerkat_status meerkat_query_batch(meerkat_graph* g, const uint32_t* src, const 
   uint32_t* dw = w_out;
   if (host_f) { e = ensure_stage(g, 2, n); df = (uint8_t*)g->stage[2]; }
   if (e == cudaSuccess && host_w) { e = ensure_stage(g, 3, n * 4); dw = (uint32_t*)g->stage[3]; }
-  if (e == cudaSuccess) e = launch_query(g, (const uint32_t*)s, (const uint32_t*)d, n, df, dw);
+  if (e == cudaSuccess) e = launch_query(g, g->out, (const uint32_t*)s, (const uint32_t*)d, n, df, dw);
   if (e == cudaSuccess && host_f) e = cudaMemcpyAsync(found, df, n, cudaMemcpyDeviceToHost, g->stream);
   if (e == cudaSuccess && host_w) e = cudaMemcpyAsync(w_out, dw, n * 4, cudaMemcpyDeviceToHost, g->stream);
   if (e != cudaSuccess) return MEERKAT_E_CUDA;
@@ -250,10 +257,10 @@ meerkat_status meerkat_export_edges(meerkat_graph* g, uint32_t* src, uint32_t* d
     if (e == cudaSuccess && w) e = ensure_stage(g, 2, capacity * 4);
     ds = (uint32_t*)g->stage[0]; dd = (uint32_t*)g->stage[1]; dw = w ? (uint32_t*)g->stage[2] : nullptr;
   }
-  if (e == cudaSuccess) e = launch_export(g, ds, dd, dw, capacity);
+  if (e == cudaSuccess) e = launch_export(g, g->out, ds, dd, dw, capacity);
   if (e != cudaSuccess) return MEERKAT_E_CUDA;
   meerkat_status st = collect(g);
-  const uint64_t n = g->hctrl->export_n;
+  const uint64_t n = g->out.hctrl->export_n;
   *n_out = n;
   if (host) {
     const uint64_t m = std::min(n, capacity);
@@ -270,17 +277,25 @@ meerkat_status meerkat_export_edges(meerkat_graph* g, uint32_t* src, uint32_t* d
 meerkat_status meerkat_stats_get(meerkat_graph* g, meerkat_stats* out) {
   if (!g || !out) return MEERKAT_E_INVALID_ARG;
   DeviceGuard dg(g->device);
-  cudaError_t e = cudaMemcpyAsync(g->hctrl, g->dev.ctrl, sizeof(GraphCtrl), cudaMemcpyDeviceToHost, g->stream);
+  cudaError_t e = cudaMemcpyAsync(g->out.hctrl, g->out.dev.ctrl, sizeof(GraphCtrl), cudaMemcpyDeviceToHost, g->stream);
+  if (e == cudaSuccess && g->reverse)
+    e = cudaMemcpyAsync(g->in.hctrl, g->in.dev.ctrl, sizeof(GraphCtrl), cudaMemcpyDeviceToHost, g->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
   if (e != cudaSuccess) return MEERKAT_E_CUDA;
   std::memset(out, 0, sizeof(*out));
+  const Store& o = g->out;
   out->vertex_n = g->V;
-  out->edges = g->hctrl->ins_total - g->hctrl->del_total;
-  out->head_slabs = g->H;
-  out->buckets = g->buckets;
-  out->pool_capacity = g->P;
-  out->pool_used = std::min<uint64_t>(g->hctrl->pool_top, g->P);
-  out->bytes_device = g->bytes;
+  out->edges = o.hctrl->ins_total - o.hctrl->del_total;
+  out->head_slabs = o.H;
+  out->buckets = o.buckets;
+  out->pool_capacity = o.P;
+  out->pool_used = std::min<uint64_t>(o.hctrl->pool_top, o.P);
+  out->bytes_device = o.bytes + g->in.bytes;
+  if (g->reverse) {
+    out->in_head_slabs = g->in.H;
+    out->in_pool_used = std::min<uint64_t>(g->in.hctrl->pool_top, g->in.P);
+    out->in_edges = g->in.hctrl->ins_total - g->in.hctrl->del_total;
+  }
   out->kernel_launches = g->launches;
   out->version = g->version;
   return MEERKAT_OK;
@@ -300,7 +315,7 @@ static meerkat_status tree_create(meerkat_graph* g, uint32_t source, bool unit, 
   t->unit = unit;
   TreeDev& T = t->dev;
   T.source = source;
-  T.fr_cap = std::max<uint64_t>(g->buckets, 1);
+  T.fr_cap = std::max<uint64_t>(std::max(g->out.buckets, g->in.buckets), 1);
   const size_t V = g->V, words = (V + 31) / 32;
   cudaError_t e = cudaMalloc(&T.node, V * 8);
   if (e == cudaSuccess) e = cudaMalloc(&T.stamp, V * 4);

@@ -22,6 +22,7 @@ struct TreeCtrl {
   unsigned long long improved;      // successful atomicMin
   unsigned long long visited;       // live edges visited by expansion (one node[x] probe each)
   unsigned long long batch_edges;   // batch edges examined by the prologue
+  unsigned long long pull_n;        // (invalid vertex, in-bucket) items of the reverse-store frontier
 };
 
 struct TreeDev {
@@ -38,20 +39,28 @@ struct TreeDev {
 
 }  // namespace mk
 
+namespace mk {
+// One slab store (out-edges, or the optional in-edge mirror) on the device.
+struct Store {
+  GraphDev dev{};
+  uint64_t H = 0, P = 0, buckets = 0;   // arena slabs, pool capacity, slab lists
+  size_t bytes = 0;
+  GraphCtrl* hctrl = nullptr;           // pinned mirror of dev.ctrl
+};
+}  // namespace mk
+
 struct meerkat_graph {
   int device = 0;
   cudaStream_t stream = nullptr;
   uint32_t V = 0;
-  bool weighted = false, hashing = true;
+  bool weighted = false, hashing = true, reverse = false;
   float lf = 0.7f;
-  uint64_t H = 0, P = 0, buckets = 0;
-  mk::GraphDev dev{};
-  mk::GraphCtrl* hctrl = nullptr;   // pinned mirror of dev.ctrl
+  mk::Store out;                    // out-edge store (the paper's SlabGraph)
+  mk::Store in;                     // in-edge mirror (reverse store), only when reverse
   uint64_t version = 0;
   int last_kind = 0;                // 0 none, 1 insert, 2 delete
   uint64_t launches = 0;
   int sm_count = 0;
-  size_t bytes = 0;
   void* stage[4] = {nullptr, nullptr, nullptr, nullptr};   // staging for host inputs / outputs
   size_t stage_bytes[4] = {0, 0, 0, 0};
   int tree_blocks_per_sm[3] = {0, 0, 0};   // cooperative occupancy: static/incremental, decremental (set, map)
@@ -69,12 +78,14 @@ struct meerkat_tree {
 
 namespace mk {
 // store.cu
-cudaError_t launch_build(meerkat_graph* g, const uint32_t* d_hints);
-cudaError_t launch_insert(meerkat_graph* g, const uint32_t* s, const uint32_t* d, const uint32_t* w, uint64_t n);
-cudaError_t launch_delete(meerkat_graph* g, const uint32_t* s, const uint32_t* d, uint64_t n);
-cudaError_t launch_query(meerkat_graph* g, const uint32_t* s, const uint32_t* d, uint64_t n, uint8_t* found,
-                         uint32_t* w_out);
-cudaError_t launch_export(meerkat_graph* g, uint32_t* s, uint32_t* d, uint32_t* w, uint64_t cap);
+cudaError_t launch_build(meerkat_graph* g, Store& st, const uint32_t* d_hints, uint64_t pool_request);
+void free_store(Store& st);
+cudaError_t launch_insert(meerkat_graph* g, Store& st, const uint32_t* s, const uint32_t* d, const uint32_t* w,
+                          uint64_t n);
+cudaError_t launch_delete(meerkat_graph* g, Store& st, const uint32_t* s, const uint32_t* d, uint64_t n);
+cudaError_t launch_query(meerkat_graph* g, Store& st, const uint32_t* s, const uint32_t* d, uint64_t n,
+                         uint8_t* found, uint32_t* w_out);
+cudaError_t launch_export(meerkat_graph* g, Store& st, uint32_t* s, uint32_t* d, uint32_t* w, uint64_t cap);
 // tree.cu
 cudaError_t tree_occupancy(meerkat_graph* g);
 enum TreeMode { MODE_STATIC = 0, MODE_INCREMENTAL = 1, MODE_DECREMENTAL = 2 };

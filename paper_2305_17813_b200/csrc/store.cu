@@ -13,6 +13,8 @@
 //    from it on failure; a full list gets a pool slab linked into lane 31 by
 //    CAS ("chained at the end of the last filled slab").  A present key
 //    keeps the minimum weight via a 64-bit atomicMin on the <key, w> pair (C8).
+#include <cstring>
+
 #include <cub/cub.cuh>
 
 #include "graph.h"
@@ -396,7 +398,7 @@ static inline unsigned grid_for(meerkat_graph* g, uint64_t groups) {
   return (unsigned)(b ? b : 1);
 }
 
-cudaError_t launch_build(meerkat_graph* g, const uint32_t* d_hints) {
+cudaError_t launch_build(meerkat_graph* g, Store& st, const uint32_t* d_hints, uint64_t pool_request) {
   const uint32_t V = g->V;
   const int cap = g->weighted ? MAP_CAP : SET_CAP;
   uint32_t* count = nullptr;
@@ -425,25 +427,27 @@ cudaError_t launch_build(meerkat_graph* g, const uint32_t* d_hints) {
     CK(cudaMemcpyAsync(HB, first + V, 16, cudaMemcpyDeviceToHost, g->stream));
     CK(cudaStreamSynchronize(g->stream));
     const uint64_t H = HB[0];
-    g->buckets = HB[1];
+    st.buckets = HB[1];
     // total slab lists = arena heads + one lazy head per hint-0 vertex
-    g->H = H;
-    if (g->P == 0) g->P = H / 2 + V / 2 + 65536;
-    if (g->H + g->P >= 0xFFFFFFF0ull) { e = cudaErrorInvalidValue; goto out; }
-    const size_t nslab = (size_t)(g->H + g->P);
-    CK(cudaMalloc(&g->dev.slabs, nslab * 128));             // ONE allocation: head arena + pool
-    CK(cudaMalloc(&g->dev.owner, nslab * 4));
-    CK(cudaMalloc(&g->dev.vmeta, (size_t)V * 8));
-    CK(cudaMalloc(&g->dev.ctrl, sizeof(GraphCtrl)));
-    CK(cudaMemsetAsync(g->dev.ctrl, 0, sizeof(GraphCtrl), g->stream));
-    g->bytes = nslab * 132 + (size_t)V * 8 + sizeof(GraphCtrl);
-    g->dev.V = V; g->dev.H = (uint32_t)g->H; g->dev.P = (uint32_t)g->P;
-    if (g->H) {
-      const unsigned gf = (unsigned)std::min<uint64_t>((g->H * 8 + 255) / 256, (uint64_t)g->sm_count * 16);
-      k_fill<<<gf, 256, 0, g->stream>>>(g->dev.slabs, g->H, g->weighted ? 1 : 0);
+    st.H = H;
+    st.P = pool_request ? pool_request : H / 2 + V / 2 + 65536;
+    if (st.H + st.P >= 0xFFFFFFF0ull) { e = cudaErrorInvalidValue; goto out; }
+    const size_t nslab = (size_t)(st.H + st.P);
+    CK(cudaMalloc(&st.dev.slabs, nslab * 128));             // ONE allocation: head arena + pool
+    CK(cudaMalloc(&st.dev.owner, nslab * 4));
+    CK(cudaMalloc(&st.dev.vmeta, (size_t)V * 8));
+    CK(cudaMalloc(&st.dev.ctrl, sizeof(GraphCtrl)));
+    CK(cudaMemsetAsync(st.dev.ctrl, 0, sizeof(GraphCtrl), g->stream));
+    CK(cudaMallocHost(&st.hctrl, sizeof(GraphCtrl)));
+    memset(st.hctrl, 0, sizeof(GraphCtrl));
+    st.bytes = nslab * 132 + (size_t)V * 8 + sizeof(GraphCtrl);
+    st.dev.V = V; st.dev.H = (uint32_t)st.H; st.dev.P = (uint32_t)st.P;
+    if (st.H) {
+      const unsigned gf = (unsigned)std::min<uint64_t>((st.H * 8 + 255) / 256, (uint64_t)g->sm_count * 16);
+      k_fill<<<gf, 256, 0, g->stream>>>(st.dev.slabs, st.H, g->weighted ? 1 : 0);
       g->launches++;
     }
-    k_init_meta<<<gb, 256, 0, g->stream>>>(g->dev, count, first, heads);
+    k_init_meta<<<gb, 256, 0, g->stream>>>(st.dev, count, first, heads);
     g->launches++;
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(g->stream));
@@ -454,50 +458,59 @@ out:
   return e;
 }
 
-cudaError_t launch_insert(meerkat_graph* g, const uint32_t* s, const uint32_t* d, const uint32_t* w, uint64_t n) {
+cudaError_t launch_insert(meerkat_graph* g, Store& st, const uint32_t* s, const uint32_t* d, const uint32_t* w, uint64_t n) {
   if (!n) return cudaSuccess;
   const unsigned gb = grid_for(g, n);
-  if (g->weighted) k_insert<true><<<gb, UPD_BLOCK, 0, g->stream>>>(g->dev, s, d, w, n);
-  else k_insert<false><<<gb, UPD_BLOCK, 0, g->stream>>>(g->dev, s, d, nullptr, n);
+  if (g->weighted) k_insert<true><<<gb, UPD_BLOCK, 0, g->stream>>>(st.dev, s, d, w, n);
+  else k_insert<false><<<gb, UPD_BLOCK, 0, g->stream>>>(st.dev, s, d, nullptr, n);
   g->launches++;
   return cudaGetLastError();
 }
 
-cudaError_t launch_delete(meerkat_graph* g, const uint32_t* s, const uint32_t* d, uint64_t n) {
+cudaError_t launch_delete(meerkat_graph* g, Store& st, const uint32_t* s, const uint32_t* d, uint64_t n) {
   if (!n) return cudaSuccess;
   const unsigned gb = grid_for(g, n);
-  if (g->weighted) k_delete<true><<<gb, UPD_BLOCK, 0, g->stream>>>(g->dev, s, d, n);
-  else k_delete<false><<<gb, UPD_BLOCK, 0, g->stream>>>(g->dev, s, d, n);
+  if (g->weighted) k_delete<true><<<gb, UPD_BLOCK, 0, g->stream>>>(st.dev, s, d, n);
+  else k_delete<false><<<gb, UPD_BLOCK, 0, g->stream>>>(st.dev, s, d, n);
   g->launches++;
   return cudaGetLastError();
 }
 
-cudaError_t launch_query(meerkat_graph* g, const uint32_t* s, const uint32_t* d, uint64_t n, uint8_t* found,
+cudaError_t launch_query(meerkat_graph* g, Store& st, const uint32_t* s, const uint32_t* d, uint64_t n, uint8_t* found,
                          uint32_t* w_out) {
   if (!n) return cudaSuccess;
   const unsigned gb = grid_for(g, n);
-  if (g->weighted) k_query<true><<<gb, UPD_BLOCK, 0, g->stream>>>(g->dev, s, d, n, found, w_out);
-  else k_query<false><<<gb, UPD_BLOCK, 0, g->stream>>>(g->dev, s, d, n, found, w_out);
+  if (g->weighted) k_query<true><<<gb, UPD_BLOCK, 0, g->stream>>>(st.dev, s, d, n, found, w_out);
+  else k_query<false><<<gb, UPD_BLOCK, 0, g->stream>>>(st.dev, s, d, n, found, w_out);
   g->launches++;
   return cudaGetLastError();
 }
 
-cudaError_t launch_export(meerkat_graph* g, uint32_t* s, uint32_t* d, uint32_t* w, uint64_t cap) {
-  cudaError_t e = cudaMemsetAsync(&g->dev.ctrl->export_n, 0, 8, g->stream);
+cudaError_t launch_export(meerkat_graph* g, Store& st, uint32_t* s, uint32_t* d, uint32_t* w, uint64_t cap) {
+  cudaError_t e = cudaMemsetAsync(&st.dev.ctrl->export_n, 0, 8, g->stream);
   if (e != cudaSuccess) return e;
   // slabs in use: arena + pool handed out so far (read on the host: export synchronises anyway)
-  e = cudaMemcpyAsync(g->hctrl, g->dev.ctrl, sizeof(GraphCtrl), cudaMemcpyDeviceToHost, g->stream);
+  e = cudaMemcpyAsync(st.hctrl, st.dev.ctrl, sizeof(GraphCtrl), cudaMemcpyDeviceToHost, g->stream);
   if (e != cudaSuccess) return e;
   e = cudaStreamSynchronize(g->stream);
   if (e != cudaSuccess) return e;
-  const uint64_t used = std::min<uint64_t>(g->hctrl->pool_top, g->P);
-  const uint64_t n_slabs = g->H + used;
+  const uint64_t used = std::min<uint64_t>(st.hctrl->pool_top, st.P);
+  const uint64_t n_slabs = st.H + used;
   if (!n_slabs) return cudaSuccess;
   const unsigned gb = grid_for(g, n_slabs);
-  if (g->weighted) k_export<true><<<gb, UPD_BLOCK, 0, g->stream>>>(g->dev, n_slabs, s, d, w, cap);
-  else k_export<false><<<gb, UPD_BLOCK, 0, g->stream>>>(g->dev, n_slabs, s, d, w, cap);
+  if (g->weighted) k_export<true><<<gb, UPD_BLOCK, 0, g->stream>>>(st.dev, n_slabs, s, d, w, cap);
+  else k_export<false><<<gb, UPD_BLOCK, 0, g->stream>>>(st.dev, n_slabs, s, d, w, cap);
   g->launches++;
   return cudaGetLastError();
+}
+
+void free_store(Store& st) {
+  cudaFree(st.dev.slabs);
+  cudaFree(st.dev.owner);
+  cudaFree(st.dev.vmeta);
+  cudaFree(st.dev.ctrl);
+  if (st.hctrl) cudaFreeHost(st.hctrl);
+  st = Store{};
 }
 
 }  // namespace mk

@@ -35,14 +35,15 @@ namespace cg = cooperative_groups;
 namespace mk {
 
 constexpr int TREE_BLOCK = 512;
-constexpr int FILTER_WORDS = 16384;   // 64 KiB smem filter = 2^19 bits per block (decremental scan)
+constexpr int FILTER_WORDS = 24576;   // 96 KiB smem Bloom filter per block (decremental scan), 2 blocks/SM
 constexpr int SCAN_UNROLL = 4;        // independent slabs in flight per group in the scan
 constexpr unsigned FULL = 0xFFFFFFFFu;
 
-enum Visit { RELAX = 0, PROPAGATE = 1 };
+enum Visit { RELAX = 0, PROPAGATE = 1, PULL = 2 };
 
 struct TreeArgs {
-  GraphDev G;
+  GraphDev G;           // out-edge store
+  GraphDev R;           // in-edge mirror (R.slabs == nullptr when the graph keeps none)
   TreeDev T;
   const uint32_t* bs;   // batch (device)
   const uint32_t* bd;
@@ -56,10 +57,6 @@ struct TreeArgs {
 struct Counters {
   uint32_t items = 0, slabs = 0, visited = 0, improved = 0, scan_slabs = 0, hits = 0, batch = 0, err = 0;
 };
-
-__device__ __forceinline__ uint32_t filt_hash(uint32_t x, uint32_t nbits_mask) {
-  return mix32(x * 0x9E3779B9u + 0x7F4A7C15u) & nbits_mask;
-}
 
 __device__ __forceinline__ bool bit_test(const uint32_t* bits, uint32_t x) {
   return (__ldcg(bits + (x >> 5)) >> (x & 31)) & 1u;
@@ -123,17 +120,17 @@ __device__ __forceinline__ bool relax(const TreeDev& T, uint32_t x, uint64_t dis
 
 // Next live item of this group (grid-stride over [it, n)): sets v / slab / du.
 template <int VISIT>
-__device__ __forceinline__ bool fetch_item(const TreeArgs& A, const uint64_t* fr, uint64_t n, uint64_t ng,
-                                           uint64_t& it, uint32_t& v, uint32_t& slab, uint32_t& du, int l8,
-                                           Counters& c) {
+__device__ __forceinline__ bool fetch_item(const TreeArgs& A, const GraphDev& S, const uint64_t* fr, uint64_t n,
+                                           uint64_t ng, uint64_t& it, uint32_t& v, uint32_t& slab, uint32_t& du,
+                                           int l8, Counters& c) {
   for (; it < n; it += ng) {
     const uint64_t item = fr[it];
     v = (uint32_t)item;
-    const uint32_t head = __ldcg(reinterpret_cast<const unsigned int*>(&A.G.vmeta[v].x));
+    const uint32_t head = __ldcg(reinterpret_cast<const unsigned int*>(&S.vmeta[v].x));
     if (l8 == 0) c.items++;
     if (head == INVALID_SLAB) continue;
     slab = head + (uint32_t)(item >> 32);
-    if (VISIT == PROPAGATE) return true;
+    if (VISIT != RELAX) return true;
     const uint64_t nv = ld_cg_u64(A.T.node + v);
     if (nv != UNREACHED) { du = (uint32_t)(nv >> 32); return true; }
   }
@@ -148,16 +145,17 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const uint64_t* fr, ui
   using F = Frag<MAP>;
   constexpr int NK = F::NK;
   const GraphDev& G = A.G;
+  const GraphDev& S = VISIT == PULL ? A.R : A.G;   // store whose slab lists are walked
   const TreeDev& T = A.T;
   const int lane = lane_id(), l8 = lane & 7;
   const uint64_t ng = ((uint64_t)gridDim.x * blockDim.x) / GROUP;
   uint64_t it = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / GROUP;
   uint32_t v = 0, slab = 0, du = 0;
-  bool active = fetch_item<VISIT>(A, fr, n, ng, it, v, slab, du, l8, c);
+  bool active = fetch_item<VISIT>(A, S, fr, n, ng, it, v, slab, du, l8, c);
   while (__any_sync(FULL, active)) {
     uint4 d = make_uint4(EMPTY_KEY, EMPTY_KEY, EMPTY_KEY, INVALID_SLAB);
     if (active) {
-      d = ld_slab_ro(slab_ptr(G, slab), l8);
+      d = ld_slab_ro(slab_ptr(S, slab), l8);
       if (l8 == 0) c.slabs++;
     }
 #pragma unroll
@@ -170,6 +168,17 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const uint64_t* fr, ui
         if (VISIT == RELAX) {
           const uint32_t w = A.unit ? 1u : F::weight(d, k);
           enq = relax(T, x, (uint64_t)du + w, v, epoch_next, c);
+        } else if (VISIT == PULL) {
+          // in-edge (x -> v) of invalid v: a valid->invalid frontier edge iff x is valid and reached
+          // (C15); relax v from it
+          if (!bit_test(T.inval_bits, x)) {
+            const uint64_t nx = ld_cg_u64(T.node + x);
+            if (nx != UNREACHED) {
+              c.hits++;
+              const uint32_t w = A.unit ? 1u : F::weight(d, k);
+              enq = relax(T, v, (nx >> 32) + w, x, epoch_next, c);
+            }
+          }
         } else {
           // PropagateInvalidation, top-down (C14): a child x of invalid v in T_G
           const uint64_t cur = ld_cg_u64(T.node + x);
@@ -182,12 +191,12 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const uint64_t* fr, ui
           }
         }
       }
-      warp_enqueue(G, T, fnext, sznext, enq, x, c);
+      warp_enqueue(G, T, fnext, sznext, enq, VISIT == PULL ? v : x, c);
     }
     const uint32_t nxt = __shfl_sync(FULL, d.w, (lane & 24) + GROUP - 1);
     if (active) {
       if (nxt != INVALID_SLAB) slab = nxt;
-      else { it += ng; active = fetch_item<VISIT>(A, fr, n, ng, it, v, slab, du, l8, c); }
+      else { it += ng; active = fetch_item<VISIT>(A, S, fr, n, ng, it, v, slab, du, l8, c); }
     }
   }
 }
@@ -286,47 +295,79 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_inc(const __grid_constan
 
 // ------------------------------------------------------------------ decremental
 
+// Blocked two-bit Bloom filter of V_invalid in shared memory: one word per key,
+// two bits within it (false-positive rate ~ load^2).  Exact membership is the
+// global bit set; the filter only keeps non-members off the slow path.
+__device__ __forceinline__ void filter_loc(uint32_t x, uint32_t fwords, uint32_t& w, uint32_t& m) {
+  uint32_t h = x * 0x9E3779B1u;
+  h ^= h >> 15;
+  w = __umulhi(h * 0x85EBCA6Bu, fwords);
+  m = (1u << (h & 31)) | (1u << ((h >> 5) & 31));
+}
+
+// Valid->invalid frontier (C15) as a STREAM over the slab array
+// [0, n_slabs): each 8-lane group reads whole slabs (LDG.128 per lane, U slabs in
+// flight); owner[] names the source vertex.  Fast path per key: one shared-memory
+// filter probe.  Slow path (warp-uniform, only for positions where some lane hit
+// the filter): exact bit-set test, source validity, relaxation and enqueue.
 template <bool MAP>
-__device__ __forceinline__ void dec_scan(const TreeArgs& A, const uint32_t* filt, uint32_t fmask, bool use_filter,
-                         uint64_t n_slabs, uint64_t* fnext, unsigned long long* sznext, uint32_t epoch_next,
-                         Counters& c) {
+__device__ __forceinline__ void dec_scan(const TreeArgs& A, const uint32_t* filt, uint32_t fwords, uint32_t n_slabs,
+                                         uint64_t* fnext, unsigned long long* sznext, uint32_t epoch_next,
+                                         Counters& c) {
   using F = Frag<MAP>;
   constexpr int NK = F::NK;
+  constexpr int U = SCAN_UNROLL;
   const GraphDev& G = A.G;
   const TreeDev& T = A.T;
+  const uint32_t V = G.V;
   const int l8 = lane_id() & 7;
-  const uint64_t ng = ((uint64_t)gridDim.x * blockDim.x) / GROUP;
-  const uint64_t g0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / GROUP;
-  const uint64_t span = ng * SCAN_UNROLL;
-  const uint64_t trips = (n_slabs + span - 1) / span;
-  for (uint64_t t = 0; t < trips; t++) {
-    uint4 d[SCAN_UNROLL];
-    uint64_t s[SCAN_UNROLL];
+  const uint32_t ng = (gridDim.x * blockDim.x) / GROUP;
+  const uint32_t g0 = (blockIdx.x * blockDim.x + threadIdx.x) / GROUP;
+  const uint32_t span = ng * U;
+  const uint32_t trips = (n_slabs + span - 1) / span;   // warp-uniform
+  const uint4* __restrict__ base = reinterpret_cast<const uint4*>(G.slabs) + l8;
+  for (uint32_t t = 0; t < trips; t++) {
+    const uint32_t s0 = t * span + g0;
+    uint4 d[U];
 #pragma unroll
-    for (int q = 0; q < SCAN_UNROLL; q++) {   // SCAN_UNROLL independent 16-B loads in flight per lane
-      s[q] = t * span + (uint64_t)q * ng + g0;
-      d[q] = s[q] < n_slabs ? ld_slab_ro(slab_ptr(G, (uint32_t)s[q]), l8)
-                            : make_uint4(EMPTY_KEY, EMPTY_KEY, EMPTY_KEY, INVALID_SLAB);
+    for (int q = 0; q < U; q++) {
+      const uint32_t s = s0 + q * ng;
+      d[q] = make_uint4(EMPTY_KEY, EMPTY_KEY, EMPTY_KEY, INVALID_SLAB);
+      if (s < n_slabs) d[q] = ld_slab_ro(reinterpret_cast<const uint32_t*>(base + (size_t)s * 8), 0);
     }
+    uint32_t hm = 0;
 #pragma unroll
-    for (int q = 0; q < SCAN_UNROLL; q++) {
-      if (s[q] < n_slabs && l8 == 0) c.scan_slabs++;
+    for (int q = 0; q < U; q++) {
 #pragma unroll
       for (int k = 0; k < NK; k++) {
         const uint32_t x = F::key(d[q], k);
+        bool hit = x < V && (MAP || F::valid_cell(l8, k));   // live key (sentinels are >= V)
+        if (fwords) {
+          uint32_t w, m;
+          filter_loc(x, fwords, w, m);
+          hit = hit && (filt[w] & m) == m;
+        }
+        hm |= (uint32_t)hit << (q * NK + k);
+      }
+    }
+    const uint32_t pos = __reduce_or_sync(FULL, hm);
+    if (!pos) continue;
+#pragma unroll
+    for (int q = 0; q < U; q++) {
+#pragma unroll
+      for (int k = 0; k < NK; k++) {
+        if (!((pos >> (q * NK + k)) & 1u)) continue;   // warp-uniform
+        const uint32_t x = F::key(d[q], k);
         bool enq = false;
-        if (F::valid_cell(l8, k) && x < G.V) {   // live key (sentinels are >= V)
-          const uint32_t h = use_filter ? filt_hash(x, fmask) : 0u;
-          if ((!use_filter || ((filt[h >> 5] >> (h & 31)) & 1u)) && bit_test(T.inval_bits, x)) {
-            // x in V_invalid: is the slab's source vertex u valid (C15)?
-            const uint32_t u = __ldcg(G.owner + s[q]);
-            if (u != NO_OWNER && !bit_test(T.inval_bits, u)) {
-              const uint64_t nu = ld_cg_u64(T.node + u);
-              if (nu != UNREACHED) {
-                c.hits++;
-                const uint32_t w = A.unit ? 1u : F::weight(d[q], k);
-                enq = relax(T, x, (nu >> 32) + w, u, epoch_next, c);
-              }
+        if (((hm >> (q * NK + k)) & 1u) && bit_test(T.inval_bits, x)) {
+          // x in V_invalid: is the slab's source vertex u valid and reached?
+          const uint32_t u = __ldg(G.owner + s0 + q * ng);
+          if (u != NO_OWNER && !bit_test(T.inval_bits, u)) {
+            const uint64_t nu = ld_cg_u64(T.node + u);
+            if (nu != UNREACHED) {
+              c.hits++;
+              const uint32_t w = A.unit ? 1u : F::weight(d[q], k);
+              enq = relax(T, x, (nu >> 32) + w, u, epoch_next, c);
             }
           }
         }
@@ -372,21 +413,33 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_dec(const __grid_constan
   const uint32_t r1 = run_rounds<MAP, PROPAGATE>(A, epoch, grid, 0, c);
   // (iii) valid -> invalid frontier, fused with the first relaxation
   const uint64_t n_inv = __ldcg(&tc->inval_n);
-  if (n_inv) {
-    const uint32_t fw = A.filter_words;
-    const bool use_filter = fw && n_inv * 16 <= (uint64_t)fw * 32;   // keep the false-positive rate low
-    const uint32_t fmask = fw * 32 - 1;
-    if (use_filter) {
+  if (n_inv && A.R.slabs) {
+    // in-edge mirror present: the frontier is exactly the in-edges of V_invalid from valid sources
+    uint64_t* pull = A.T.fr[(r1 + 1) & 1];
+    const uint64_t ptrips = (n_inv + nt - 1) / nt;
+    for (uint64_t t = 0; t < ptrips; t++) {
+      const uint64_t i = tid + t * nt;
+      const bool has = i < n_inv;
+      warp_enqueue(A.R, A.T, pull, &tc->pull_n, has, has ? __ldcg(A.T.inval_list + i) : 0u, c);
+    }
+    grid.sync();
+    expand<MAP, PULL>(A, pull, __ldcg(&tc->pull_n), A.T.fr[r1 & 1], &tc->size[r1 % 3], epoch + r1, c);
+  } else if (n_inv) {
+    // filter only while sparse enough: two bits per member, bit load <= 1/4 (false positives <= ~6%)
+    const uint32_t fw = (n_inv * 8 <= (uint64_t)A.filter_words * 32) ? A.filter_words : 0u;
+    if (fw) {
       for (uint32_t i = threadIdx.x; i < fw; i += blockDim.x) filt[i] = 0;
       __syncthreads();
       for (uint64_t i = threadIdx.x; i < n_inv; i += blockDim.x) {
-        const uint32_t h = filt_hash(__ldcg(A.T.inval_list + i), fmask);
-        atomicOr(&filt[h >> 5], 1u << (h & 31));
+        uint32_t w, m;
+        filter_loc(__ldcg(A.T.inval_list + i), fw, w, m);
+        atomicOr(&filt[w], m);
       }
       __syncthreads();
     }
-    const uint64_t n_slabs = A.G.H + min((unsigned long long)A.G.P, __ldcg(&A.G.ctrl->pool_top));
-    dec_scan<MAP>(A, filt, fmask, use_filter, n_slabs, A.T.fr[r1 & 1], &tc->size[r1 % 3], epoch + r1, c);
+    const uint32_t n_slabs = A.G.H + (uint32_t)min((unsigned long long)A.G.P, __ldcg(&A.G.ctrl->pool_top));
+    if (tid == 0) c.scan_slabs = n_slabs;
+    dec_scan<MAP>(A, filt, fw, n_slabs, A.T.fr[r1 & 1], &tc->size[r1 % 3], epoch + r1, c);
   }
   grid.sync();
   // (iv) common epilogue
@@ -429,7 +482,8 @@ cudaError_t tree_occupancy(meerkat_graph* g) {
 cudaError_t launch_tree(meerkat_graph* g, meerkat_tree* t, int mode, const uint32_t* s, const uint32_t* d,
                         const uint32_t* w, uint64_t n) {
   TreeArgs A;
-  A.G = g->dev;
+  A.G = g->out.dev;
+  A.R = g->reverse ? g->in.dev : GraphDev{};
   A.T = t->dev;
   A.bs = s; A.bd = d; A.bw = w; A.bn = n;
   A.unit = t->unit ? 1u : 0u;

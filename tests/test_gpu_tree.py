@@ -92,12 +92,13 @@ def _config1_batches(rng, o, V, src, kind):
     return s, d, None
 
 
-@pytest.mark.parametrize("hashing", [True, False])
-def test_config1_dynamic_sssp_bfs(hashing):
+@pytest.mark.parametrize("hashing,reverse", [(True, False), (False, False), (True, True)])
+def test_config1_dynamic_sssp_bfs(hashing, reverse):
     """BASELINE config 1: 1K vertices / 8K edges, 4 insert + 4 delete batches of 64, SSSP + BFS from 0."""
     V, src = 1024, 0
     s, d, w = synth.uniform(V, 8192)
-    g = G(V, weighted=True, hashing=hashing, degree_hints=synth.degrees(s, V))
+    g = G(V, weighted=True, hashing=hashing, degree_hints=synth.degrees(s, V), reverse=reverse,
+          in_degree_hints=synth.degrees(d, V))
     o = oracle.OracleGraph(V)
     assert g.insert(cuda(s), cuda(d), cuda(w)) == o.insert(s, d, w)[1]
     t, b = g.sssp(src), g.bfs(src)
@@ -127,14 +128,19 @@ def test_config1_dynamic_sssp_bfs(hashing):
     assert_same_edges(g, o)
 
 
-@pytest.mark.parametrize("scale,hashing,lf", [(14, True, 0.7), (14, False, 0.7), (16, True, 0.5), (17, True, 1.0)])
-def test_rmat_dynamic_vs_oracle(scale, hashing, lf):
+@pytest.mark.parametrize("scale,hashing,lf,reverse", [(14, True, 0.7, False), (14, False, 0.7, False),
+                                                       (16, True, 0.5, False), (17, True, 1.0, False),
+                                                       (14, True, 0.7, True), (16, False, 0.7, True),
+                                                       (17, True, 0.7, True)])
+def test_rmat_dynamic_vs_oracle(scale, hashing, lf, reverse):
     """R-MAT (SURVEY §8(d) generator) with held-out inserts and sampled deletes; both trees
-    bit-exact after every batch; several tiles, hub vertices, chained slabs."""
+    bit-exact after every batch; several tiles, hub vertices, chained slabs; with and
+    without the in-edge mirror (decremental frontier by scan vs by in-edges)."""
     W = synth.rmat_dynamic(scale, 16, batch=1000 if scale < 16 else 5000, n_ins=3, n_del=3)
     V, src = W.vertex_n, W.source
     bs, bd, bw = W.base
-    g = G(V, weighted=True, hashing=hashing, load_factor=lf, degree_hints=synth.degrees(bs, V))
+    g = G(V, weighted=True, hashing=hashing, load_factor=lf, degree_hints=synth.degrees(bs, V), reverse=reverse,
+          in_degree_hints=synth.degrees(bd, V))
     o = oracle.OracleGraph(V)
     assert g.insert(cuda(bs), cuda(bd), cuda(bw)) == o.insert(bs, bd, bw)[1]
     t, b = g.sssp(src), g.bfs(src)
@@ -164,7 +170,7 @@ def test_unweighted_graph_bfs_and_sssp_rejected():
     from paper_2305_17813_b200 import MeerkatError
     V = 3000
     s, d, _ = synth.uniform(V, 20000, seed_graph=9)
-    g = G(V, weighted=False, degree_hints=synth.degrees(s, V))
+    g = G(V, weighted=False, degree_hints=synth.degrees(s, V), reverse=True)
     o = oracle.OracleGraph(V, weighted=False)
     assert g.insert(s, d) == o.insert(s, d)[1]
     with pytest.raises(MeerkatError):
