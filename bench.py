@@ -11,7 +11,10 @@ path over one batch pair:
     delete_batch(100K present edges)  -> sssp_decremental -> bfs_decremental
 
 value = 200K edge updates / device time of the step (inputs resident in HBM),
-with per-call times reported beside it.  L2 is flushed (256 MiB write) between
+with per-call times reported beside it.  The decremental valid->invalid
+frontier is read from an in-edge mirror store by default (--frontier reverse);
+the paper's full slab scan (--frontier scan) is timed too and reported under
+"alt" (--no-compare skips it).  L2 is flushed (256 MiB write) between
 timed steps, outside the timed intervals.  `e2e` repeats the step through the
 C ABI with pinned HOST batch arrays (staged by the library inside each call)
 and reads the insert/delete counts back to the host.
@@ -47,7 +50,9 @@ def parse():
     p.add_argument("--batch", type=int, default=100_000)
     p.add_argument("--lf", type=float, default=0.7)
     p.add_argument("--no-hashing", action="store_true")
-    p.add_argument("--frontier", choices=["scan", "reverse"], default="scan",
+    p.add_argument("--compare", action=argparse.BooleanOptionalAction, default=True,
+                   help="also time the other decremental-frontier mode (reported under 'alt')")
+    p.add_argument("--frontier", choices=["scan", "reverse"], default="reverse",
                    help="decremental valid->invalid frontier: stream every slab (paper, P:156-164) or "
                         "read the in-edges of V_invalid from an in-edge mirror store")
     p.add_argument("--no-e2e", action="store_true")
@@ -199,20 +204,14 @@ def run_reference(args, ws, rank):
 
 # ------------------------------------------------------------------ our arm
 
-def run_ours(args, ws, rank, local):
+def build(args, W, frontier, dev, local, stream, T):
+    """Graph + SSSP/BFS trees for workload W (not timed, except the bulk build as its own datum)."""
     import torch
     from paper_2305_17813_b200 import Graph
-
-    dev = torch.device("cuda", local)
-    torch.cuda.set_device(dev)
-    K, Wm = args.steps, args.warmup
-    W, gen_s = make_workload(args, K + Wm, rank)
     V = W.vertex_n
-    stream = torch.cuda.current_stream(dev)
-    T = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.uint32).view(np.int32)).to(dev)
     bs, bd, bw = W.base
     hints = np.bincount(bs, minlength=V).astype(np.uint32)
-    rev = args.frontier == "reverse"
+    rev = frontier == "reverse"
     ihints = np.bincount(bd, minlength=V).astype(np.uint32) if rev else None
     g = Graph(V, weighted=True, hashing=not args.no_hashing, load_factor=args.lf, degree_hints=T(hints),
               device=local, stream=stream, reverse=rev, in_degree_hints=T(ihints) if rev else None)
@@ -224,94 +223,141 @@ def run_ours(args, ws, rank, local):
     torch.cuda.synchronize()
     bulk_ms = e0.elapsed_time(e1)
     del base_t
-    t_create0 = time.time()
     sp = g.sssp(W.source)
     bf = g.bfs(W.source)
     torch.cuda.synchronize()
+    return g, sp, bf, int(n_base), bulk_ms
+
+
+NAMES = ["insert", "sssp_inc", "bfs_inc", "delete", "sssp_dec", "bfs_dec"]
+
+
+def one_step(g, sp, bf, ins, dels, evs, stream):
+    """The hot path over one batch pair: mutate, then update both trees."""
+    s, d, w = ins
+    evs[0].record(stream)
+    g.insert(s, d, w, count=False)
+    evs[1].record(stream)
+    sp.incremental(s, d, w)
+    evs[2].record(stream)
+    bf.incremental(s, d)
+    evs[3].record(stream)
+    s, d = dels
+    g.delete(s, d, count=False)
+    evs[4].record(stream)
+    sp.decremental(s, d)
+    evs[5].record(stream)
+    bf.decremental(s, d)
+    evs[6].record(stream)
+
+
+def measure(args, ws, W, frontier, dev, local, stream, T, flush, K, Wm, clocks=None):
+    import torch
+    g, sp, bf, n_base, bulk_ms = build(args, W, frontier, dev, local, stream, T)
     ins = [tuple(T(x) for x in b) for b in W.inserts]
     dels = [tuple(T(x) for x in b[:2]) for b in W.deletes]
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-
-    names = ["insert", "sssp_inc", "bfs_inc", "delete", "sssp_dec", "bfs_dec"]
-
-    def step(i, evs):
-        s, d, w = ins[i]
-        evs[0].record(stream)
-        g.insert(s, d, w, count=False)
-        evs[1].record(stream)
-        sp.incremental(s, d, w)
-        evs[2].record(stream)
-        bf.incremental(s, d)
-        evs[3].record(stream)
-        s, d = dels[i]
-        g.delete(s, d, count=False)
-        evs[4].record(stream)
-        sp.decremental(s, d)
-        evs[5].record(stream)
-        bf.decremental(s, d)
-        evs[6].record(stream)
-
+    ev = lambda: [torch.cuda.Event(enable_timing=True) for _ in range(7)]
     for i in range(Wm):
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
-        step(i, evs)
+        one_step(g, sp, bf, ins[i], dels[i], ev(), stream)
         flush.zero_()
     torch.cuda.synchronize()
     g.sync()
     st0 = g.stats()
-    per_call = {n: [] for n in names}
-    tstats = {"sssp_dec": [], "bfs_dec": [], "sssp_inc": [], "bfs_inc": []}
-    clocks = ClockSampler(local)
-    clocks.start()
+    per_call = {n: [] for n in NAMES}
+    tstats = {"sssp_dec": [], "bfs_dec": []}
+    if clocks:
+        clocks.start()
     barrier(ws)
     torch.cuda.synchronize()
+    torch.cuda.nvtx.range_push(f"timed_{frontier}")   # ncu --nvtx --nvtx-include "timed_<mode>/" selects these
     total_ms = 0.0
     for k in range(K):
         i = Wm + k
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
-        step(i, evs)
+        evs = ev()
+        one_step(g, sp, bf, ins[i], dels[i], evs, stream)
         evs[6].synchronize()
-        for j, n in enumerate(names):
+        for j, n in enumerate(NAMES):
             per_call[n].append(evs[j].elapsed_time(evs[j + 1]))
         total_ms += evs[0].elapsed_time(evs[6])
-        # per-call algorithmic bytes of the tree kernels (device counters, read outside the intervals)
-        tstats["sssp_dec"].append(sp.stats())
+        tstats["sssp_dec"].append(sp.stats())   # device counters of the last call, read outside the intervals
         tstats["bfs_dec"].append(bf.stats())
         flush.zero_()
     torch.cuda.synchronize()
+    torch.cuda.nvtx.range_pop()
     barrier(ws)
-    clk = clocks.stop()
+    clk = clocks.stop() if clocks else None
     g.sync()
     st1 = g.stats()
     total_ms = allreduce_max(total_ms, ws)
-    ms_per_step = total_ms / K
-    edges = 2 * args.batch * K * ws
-    value = edges / (total_ms / 1e3)
-
-    # the dominant call and its roofline (HBM-bound: slab streaming / pointer chasing)
+    # static recompute on the final graph: the s_b^n baseline (P:1725-1730)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    static = {}
+    for name, t in (("sssp", sp), ("bfs", bf)):
+        flush.zero_()
+        a.record(stream)
+        t.recompute()
+        b.record(stream)
+        b.synchronize()
+        static[name] = a.elapsed_time(b)
     mean = {n: float(np.mean(v)) for n, v in per_call.items()}
+    res = {
+        "frontier": frontier, "K": K, "total_ms": total_ms, "ms_per_step": total_ms / K, "mean": mean,
+        "per_call": per_call, "tstats": tstats, "clocks": clk, "n_base": n_base, "bulk_ms": bulk_ms,
+        "launches": int(st1["kernel_launches"] - st0["kernel_launches"]), "static_ms": static,
+        "store": {k: g.stats()[k] for k in ("head_slabs", "buckets", "pool_used", "bytes_device")},
+    }
+    return res, (g, sp, bf)
+
+
+def roofline_of(res, peak, peak_src, traffic_file):
+    mean = res["mean"]
     dom = max(mean, key=mean.get)
+    if dom not in res["tstats"]:
+        return {"bound": "hbm", "kernel": dom, "achieved": None, "peak": peak, "unit": "GB/s", "frac": None,
+                "traffic": None}
+    ab = float(np.mean([s["alg_bytes"] for s in res["tstats"][dom]]))
+    ach = ab / (mean[dom] * 1e-3) / 1e9
+    traffic = None
+    try:
+        traffic = json.load(open(traffic_file)).get(f"{res['frontier']}/{dom}")
+    except Exception:
+        pass
+    return {"bound": "hbm", "kernel": f"k_tree_dec ({dom}, {res['frontier']} frontier)", "achieved": ach,
+            "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": traffic, "alg_bytes_per_launch": ab,
+            "peak_source": peak_src}
+
+
+def tree_detail(res):
+    return {n: {k: float(np.mean([s[k] for s in v])) for k in
+                ("rounds", "propagate_rounds", "invalidated", "frontier_edges", "scan_slabs", "slabs_read",
+                 "alg_bytes")} for n, v in res["tstats"].items() if v}
+
+
+def run_ours(args, ws, rank, local):
+    import torch
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    K, Wm = args.steps, args.warmup
+    W, gen_s = make_workload(args, K + Wm, rank)
+    V = W.vertex_n
+    stream = torch.cuda.current_stream(dev)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.uint32).view(np.int32)).to(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
     peak = peaks.get("hbm_gbs") or 6650.0
-    peak_src = "measured" if peaks.get("hbm_gbs") else "fallback"
-    roof = None
-    if dom in tstats and tstats[dom]:
-        ab = float(np.mean([s["alg_bytes"] for s in tstats[dom]]))
-        ach = ab / (mean[dom] * 1e-3) / 1e9
-        traffic = None
-        try:
-            tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-            traffic = tr.get(dom)
-        except Exception:
-            pass
-        roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                "traffic": traffic, "alg_bytes_per_launch": ab, "peak_source": peak_src}
-    tree_detail = {n: {k: float(np.mean([s[k] for s in v])) for k in
-                       ("rounds", "propagate_rounds", "invalidated", "frontier_edges", "scan_slabs", "slabs_read",
-                        "alg_bytes")} for n, v in tstats.items() if v}
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if peaks.get("hbm_gbs") else "fallback (B200_PROFILING.md)"
+    traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
+
+    res, (g, sp, bf) = measure(args, ws, W, args.frontier, dev, local, stream, T, flush, K, Wm,
+                               clocks=ClockSampler(local))
+    edges = 2 * args.batch * K * ws
+    value = edges / (res["total_ms"] / 1e3)
+    mean = res["mean"]
 
     # ---------------- e2e through the C ABI with pinned host buffers
     e2e = None
@@ -319,7 +365,7 @@ def run_ours(args, ws, rank, local):
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.uint32).view(np.int32)).pin_memory()
         hi = [tuple(pin(x) for x in b) for b in W.inserts[Wm:Wm + K]]
         hd = [tuple(pin(x) for x in b[:2]) for b in W.deletes[Wm:Wm + K]]
-        # the timed steps above already applied these batches: undo them first (not timed)
+        # the timed steps already applied these batches: undo them (not timed), then replay from host memory
         for k in reversed(range(K)):
             g.insert(*[T(x) for x in W.deletes[Wm + k]], count=False)
             g.delete(*[T(x) for x in W.inserts[Wm + k][:2]], count=False)
@@ -331,11 +377,11 @@ def run_ours(args, ws, rank, local):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             s, d, w = hi[k]
-            n_i = g.insert(s, d, w, count=True)          # H2D staged inside the call, count read back (D2H)
+            g.insert(s, d, w, count=True)          # H2D staged inside the call, count read back (D2H)
             sp.incremental(s, d, w)
             bf.incremental(s, d)
             s, d = hd[k]
-            n_d = g.delete(s, d, count=True)
+            g.delete(s, d, count=True)
             sp.decremental(s, d)
             bf.decremental(s, d)
             b.record(stream)
@@ -347,20 +393,34 @@ def run_ours(args, ws, rank, local):
         e2e = {"value": edges / (e_ms / 1e3), "unit": "edges/s",
                "h2d_bytes_per_step": n * 4 * (3 + 3 + 2 + 2 + 2 + 2), "d2h_bytes_per_step": 2 * 64,
                "ms_per_step": e_ms / K}
+    g.close()
+    del g, sp, bf
+    torch.cuda.empty_cache()
+
+    # ---------------- the paper's own decremental frontier (full slab scan) for comparison
+    alt = None
+    if args.compare:
+        other = "scan" if args.frontier == "reverse" else "reverse"
+        r2, objs = measure(args, ws, W, other, dev, local, stream, T, flush, K, Wm)
+        objs[0].close()
+        del objs
+        alt = {"decremental_frontier": other, "value": edges / (r2["total_ms"] / 1e3),
+               "ms_per_step": r2["ms_per_step"], "per_call_ms": r2["mean"],
+               "roofline": roofline_of(r2, peak, peak_src, traffic_file), "tree_calls": tree_detail(r2)}
 
     cb = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline(args, args.cpu_steps)
         cb = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
-    gs = g.stats()
+    dyn = {"sssp": mean["sssp_inc"] + mean["sssp_dec"], "bfs": mean["bfs_inc"] + mean["bfs_dec"]}
     line = {
         "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": ws, "steps": K, "warmup": Wm,
-        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": res["ms_per_step"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u64", "data": "synthetic",
         "config": {"workload": f"rmat-s{args.scale}-ef{args.ef} dynamic SSSP+BFS, {args.batch}-edge insert+delete "
                                f"batches (BASELINE config 3)",
-                   "vertices": V, "edges": int(n_base), "batch": args.batch, "source": W.source,
+                   "vertices": V, "edges": res["n_base"], "batch": args.batch, "source": W.source,
                    "hashing": not args.no_hashing, "load_factor": args.lf,
                    "decremental_frontier": args.frontier,
                    "parallelism": "single GPU" if ws == 1 else f"{ws} independent replicas",
@@ -371,14 +431,17 @@ def run_ours(args, ws, rank, local):
         "sssp_ms_per_batch": {"incremental": mean["sssp_inc"], "decremental": mean["sssp_dec"]},
         "bfs_ms_per_batch": {"incremental": mean["bfs_inc"], "decremental": mean["bfs_dec"]},
         "per_call_ms": mean,
-        "bulk_build": {"edges": int(n_base), "ms": bulk_ms, "edges_per_s": n_base / (bulk_ms / 1e3)},
-        "tree_calls": tree_detail,
-        "roofline": roof,
+        "static_recompute_ms": res["static_ms"],
+        "self_relative_speedup": {k: res["static_ms"][k] / (dyn[k] / 2) for k in dyn},
+        "bulk_build": {"edges": res["n_base"], "ms": res["bulk_ms"], "edges_per_s": res["n_base"] / (res["bulk_ms"] / 1e3)},
+        "tree_calls": tree_detail(res),
+        "roofline": roofline_of(res, peak, peak_src, traffic_file),
         "cpu_baseline": cb,
         "e2e": e2e,
-        "gpu_launches": int(st1["kernel_launches"] - st0["kernel_launches"]),
-        "clocks": clk,
-        "store": {k: gs[k] for k in ("head_slabs", "buckets", "pool_used", "bytes_device")},
+        "gpu_launches": res["launches"],
+        "clocks": res["clocks"],
+        "store": res["store"],
+        "alt": alt,
         "generate_s": gen_s,
     }
     if rank == 0:
