@@ -64,7 +64,8 @@ typedef enum {
   MEERKAT_E_OVERFLOW = 5,     /* a distance would reach 2^32-1; that relaxation is not applied (C5) */
   MEERKAT_E_STATE = 6,        /* tree/graph version mismatch; SSSP on an unweighted graph */
   MEERKAT_E_CUDA = 7,         /* CUDA runtime error (out of memory, launch failure, no device) */
-  MEERKAT_E_NCCL = 8          /* reserved for the multi-GPU router */
+  MEERKAT_E_NCCL = 8,         /* reserved */
+  MEERKAT_E_PARTITION = 9     /* an edge's source (or a message's target) is not held by this rank (skipped) */
 } meerkat_status;
 
 typedef struct {
@@ -81,6 +82,9 @@ typedef struct {
                                    valid->invalid frontier reads only the in-edges of V_invalid
                                    instead of scanning every slab (same result) */
   const uint32_t* in_degree_hints; /* host or device [vertex_n] (in-degrees), or NULL; reverse only */
+  uint32_t world_size;          /* vertex partition (multi-GPU): 0 or 1 = whole graph here;   */
+  uint32_t rank;                /* otherwise this graph holds the out-edges of every u with u % world_size  */
+                                /* == rank; degree hints are then indexed by u / world_size                */
 } meerkat_config;
 
 typedef struct {
@@ -171,6 +175,54 @@ meerkat_status meerkat_tree_nodes(meerkat_tree* t, uint64_t* out);
 meerkat_status meerkat_tree_invalidated(meerkat_tree* t, uint32_t* out, uint64_t capacity, uint64_t* n_out);
 meerkat_status meerkat_tree_stats_get(meerkat_tree* t, meerkat_tree_stats* out); /* synchronises */
 meerkat_status meerkat_tree_destroy(meerkat_tree* t);
+
+/* ---------------------------------------------------------------------------------------------
+ * Vertex-partitioned trees (world_size > 1).  Each rank holds node[] of its own
+ * vertices; a tree update is a sequence of PHASES run by every rank in lock step, with the
+ * caller moving messages between ranks in between (one all-to-all per round, e.g. NCCL through
+ * torch.distributed) and summing local frontier sizes for termination.  The method and the
+ * result are the single-GPU ones: relaxations of a vertex owned elsewhere
+ * become messages <x, packed candidate> to owner(x); invalidations of a child owned elsewhere
+ * become messages <x, expected parent>.  Results are bit-identical to world_size 1.
+ *
+ * Messages are (x, payload) pairs of uint64 grouped by destination rank; `msg_counts[r]` is the
+ * number of pairs for rank r.  The device buffer in meerkat_dresult stays valid until the next
+ * phase call on the tree.  Every phase synchronises the graph's stream.
+ * ------------------------------------------------------------------------------------------- */
+typedef enum {
+  MEERKAT_D_STATIC_INIT = 0,      /* node <- UNREACHED, SRC <- <0,SRC> on its owner; frontier = {SRC} */
+  MEERKAT_D_INC_SEED = 1,         /* a,b,c,n = inserted batch edges with u owned here        */
+  MEERKAT_D_DEC_INVALIDATE = 2,   /* a,b,n = deleted batch edges with v owned here          */
+  MEERKAT_D_PROPAGATE = 3,        /* expand the frontier of invalid vertices               */
+  MEERKAT_D_APPLY_PROPAGATE = 4,  /* a = received <x, expected parent> pairs, n pairs                   */
+  MEERKAT_D_DEC_SCAN = 5,         /* a = ALL ranks' invalid vertices (u32, global ids), n    */
+  MEERKAT_D_RELAX = 6,            /* expand the frontier of improved vertices              */
+  MEERKAT_D_APPLY_RELAX = 7,      /* a = received <x, candidate> pairs, n pairs                         */
+  MEERKAT_D_FINISH = 8            /* a = ALL ranks' invalid vertices, n: clear marks; tree reflects the graph */
+} meerkat_dphase;
+
+#define MEERKAT_MAX_RANKS 64
+
+typedef struct {
+  const uint64_t* msgs;                   /* device: outgoing pairs grouped by destination rank */
+  uint64_t msg_counts[MEERKAT_MAX_RANKS]; /* pairs per destination rank */
+  uint64_t frontier;                      /* local frontier size for the next expansion */
+  const uint32_t* invalid;                /* device: vertices this rank invalidated so far (global ids) */
+  uint64_t invalid_n;
+} meerkat_dresult;
+
+meerkat_status meerkat_dtree_create(meerkat_graph* g, uint32_t source, uint32_t unit_weights, meerkat_tree** out);
+meerkat_status meerkat_dtree_phase(meerkat_graph* g, meerkat_tree* t, meerkat_dphase phase, const void* a,
+                                   const void* b, const void* c, uint64_t n, meerkat_dresult* out);
+/* Stable partition of a batch by owner(key[i]) = key[i] % world_size (key = src for insert/delete/
+ * query and incremental seeds, dst for decremental invalidation): writes the permuted a,b,c
+ * (c may be NULL) to the device outputs and per-rank counts to counts[world_size] (host). */
+/* Copy `bytes` between host/device buffers on the graph's stream and synchronise (lets a caller
+ * move phase messages into its own communication buffers). */
+meerkat_status meerkat_memcpy(meerkat_graph* g, void* dst, const void* src, uint64_t bytes);
+meerkat_status meerkat_route(meerkat_graph* g, int key_is_b, const uint32_t* a, const uint32_t* b,
+                             const uint32_t* c, uint64_t n, uint32_t* out_a, uint32_t* out_b, uint32_t* out_c,
+                             uint64_t* counts);
 
 #ifdef __cplusplus
 }

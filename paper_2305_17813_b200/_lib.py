@@ -15,9 +15,12 @@ SO_PATH = os.path.join(HERE, "libmeerkat.so")
 STATUS = {
     0: "MEERKAT_OK", 1: "MEERKAT_E_INVALID_ARG", 2: "MEERKAT_E_VERTEX_RANGE", 3: "MEERKAT_E_WEIGHT",
     4: "MEERKAT_E_CAPACITY", 5: "MEERKAT_E_OVERFLOW", 6: "MEERKAT_E_STATE", 7: "MEERKAT_E_CUDA",
-    8: "MEERKAT_E_NCCL",
+    8: "MEERKAT_E_NCCL", 9: "MEERKAT_E_PARTITION",
 }
-OK, E_INVALID_ARG, E_VERTEX_RANGE, E_WEIGHT, E_CAPACITY, E_OVERFLOW, E_STATE, E_CUDA, E_NCCL = range(9)
+OK, E_INVALID_ARG, E_VERTEX_RANGE, E_WEIGHT, E_CAPACITY, E_OVERFLOW, E_STATE, E_CUDA, E_NCCL, E_PARTITION = range(10)
+MAX_RANKS = 64
+(D_STATIC_INIT, D_INC_SEED, D_DEC_INVALIDATE, D_PROPAGATE, D_APPLY_PROPAGATE, D_DEC_SCAN, D_RELAX, D_APPLY_RELAX,
+ D_FINISH) = range(9)
 
 # Every function include/meerkat.h declares (checked by tests/test_abi.py).
 EXPORTS = [
@@ -26,6 +29,7 @@ EXPORTS = [
     "meerkat_stats_get", "meerkat_sssp_create", "meerkat_bfs_create", "meerkat_sssp_incremental",
     "meerkat_bfs_incremental", "meerkat_sssp_decremental", "meerkat_bfs_decremental", "meerkat_tree_recompute",
     "meerkat_tree_nodes", "meerkat_tree_invalidated", "meerkat_tree_stats_get", "meerkat_tree_destroy",
+    "meerkat_dtree_create", "meerkat_dtree_phase", "meerkat_memcpy", "meerkat_route",
 ]
 
 
@@ -41,6 +45,7 @@ class Config(ctypes.Structure):
         ("load_factor", ctypes.c_float), ("degree_hints", ctypes.c_void_p), ("pool_slabs", ctypes.c_uint64),
         ("hash_seed", ctypes.c_uint64), ("device", ctypes.c_int), ("stream", ctypes.c_void_p),
         ("reverse", ctypes.c_uint32), ("in_degree_hints", ctypes.c_void_p),
+        ("world_size", ctypes.c_uint32), ("rank", ctypes.c_uint32),
     ]
 
 
@@ -61,6 +66,11 @@ class TreeStats(ctypes.Structure):
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}
+
+
+class DResult(ctypes.Structure):
+    _fields_ = [("msgs", ctypes.c_void_p), ("msg_counts", ctypes.c_uint64 * MAX_RANKS), ("frontier", ctypes.c_uint64),
+                ("invalid", ctypes.c_void_p), ("invalid_n", ctypes.c_uint64)]
 
 
 _lib = None
@@ -99,6 +109,10 @@ def lib():
         "meerkat_tree_invalidated": (ctypes.c_int, [vp, vp, u64, pu64]),
         "meerkat_tree_stats_get": (ctypes.c_int, [vp, ctypes.POINTER(TreeStats)]),
         "meerkat_tree_destroy": (ctypes.c_int, [vp]),
+        "meerkat_dtree_create": (ctypes.c_int, [vp, u32, u32, pvp]),
+        "meerkat_dtree_phase": (ctypes.c_int, [vp, vp, ctypes.c_int, vp, vp, vp, u64, ctypes.POINTER(DResult)]),
+        "meerkat_memcpy": (ctypes.c_int, [vp, vp, vp, u64]),
+        "meerkat_route": (ctypes.c_int, [vp, ctypes.c_int, vp, vp, vp, u64, vp, vp, vp, pu64]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

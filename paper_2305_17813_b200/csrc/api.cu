@@ -14,6 +14,7 @@ namespace {
 meerkat_status from_cuda(cudaError_t e) { return e == cudaSuccess ? MEERKAT_OK : MEERKAT_E_CUDA; }
 
 meerkat_status from_err(uint32_t err) {
+  if (err & ERR_PARTITION) return MEERKAT_E_PARTITION;
   if (err & ERR_RANGE) return MEERKAT_E_VERTEX_RANGE;
   if (err & ERR_WEIGHT) return MEERKAT_E_WEIGHT;
   if (err & ERR_CAPACITY) return MEERKAT_E_CAPACITY;
@@ -105,6 +106,7 @@ const char* meerkat_status_string(meerkat_status s) {
     case MEERKAT_E_STATE: return "MEERKAT_E_STATE";
     case MEERKAT_E_CUDA: return "MEERKAT_E_CUDA";
     case MEERKAT_E_NCCL: return "MEERKAT_E_NCCL";
+    case MEERKAT_E_PARTITION: return "MEERKAT_E_PARTITION";
   }
   return "MEERKAT_E_UNKNOWN";
 }
@@ -126,6 +128,13 @@ meerkat_status meerkat_create(const meerkat_config* cfg, meerkat_graph** out) {
   g->device = cfg->device;
   g->stream = static_cast<cudaStream_t>(cfg->stream);
   g->V = cfg->vertex_n;
+  g->ws = cfg->world_size > 1 ? cfg->world_size : 1;
+  g->rank = g->ws > 1 ? cfg->rank : 0;
+  if (g->ws > MEERKAT_MAX_RANKS || g->rank >= g->ws || g->V <= g->rank) {
+    delete g;
+    return MEERKAT_E_INVALID_ARG;
+  }
+  g->Vl = (g->V - g->rank + g->ws - 1) / g->ws;   // vertices v < V with v % ws == rank
   g->weighted = cfg->weighted != 0;
   g->hashing = cfg->hashing != 0;
   g->lf = lf;
@@ -134,10 +143,10 @@ meerkat_status meerkat_create(const meerkat_config* cfg, meerkat_graph** out) {
   g->in.dev.seed = g->out.dev.seed ^ 0x27d4eb2fu;
   cudaError_t e = cudaDeviceGetAttribute(&g->sm_count, cudaDevAttrMultiProcessorCount, g->device);
   const void* hints = nullptr;
-  if (e == cudaSuccess) e = stage_in(g, 0, cfg->degree_hints, (size_t)g->V * 4, &hints);
+  if (e == cudaSuccess) e = stage_in(g, 0, cfg->degree_hints, (size_t)g->Vl * 4, &hints);
   if (e == cudaSuccess) e = launch_build(g, g->out, static_cast<const uint32_t*>(hints), cfg->pool_slabs);
   if (e == cudaSuccess && g->reverse) {
-    e = stage_in(g, 1, cfg->in_degree_hints, (size_t)g->V * 4, &hints);
+    e = stage_in(g, 1, cfg->in_degree_hints, (size_t)g->Vl * 4, &hints);
     if (e == cudaSuccess) e = launch_build(g, g->in, static_cast<const uint32_t*>(hints), cfg->pool_slabs);
   }
   if (e == cudaSuccess) e = tree_occupancy(g);
@@ -157,6 +166,8 @@ meerkat_status meerkat_destroy(meerkat_graph* g) {
   cudaStreamSynchronize(g->stream);
   free_store(g->out);
   free_store(g->in);
+  cudaFree(g->rscratch);
+  if (g->hrscratch) cudaFreeHost(g->hrscratch);
   for (int i = 0; i < 4; i++) cudaFree(g->stage[i]);
   delete g;
   return MEERKAT_OK;
@@ -303,11 +314,12 @@ meerkat_status meerkat_stats_get(meerkat_graph* g, meerkat_stats* out) {
 
 // ------------------------------------------------------------------ trees
 
-static meerkat_status tree_create(meerkat_graph* g, uint32_t source, bool unit, meerkat_tree** out) {
+static meerkat_status tree_create(meerkat_graph* g, uint32_t source, bool unit, bool dist, meerkat_tree** out) {
   if (!g || !out) return MEERKAT_E_INVALID_ARG;
   *out = nullptr;
   if (source >= g->V) return MEERKAT_E_VERTEX_RANGE;
   if (!unit && !g->weighted) return MEERKAT_E_STATE;   // SSSP needs weights
+  if (dist != (g->ws > 1)) return MEERKAT_E_INVALID_ARG;  // partitioned graphs use the meerkat_dtree_* calls
   DeviceGuard dg(g->device);
   meerkat_tree* t = new (std::nothrow) meerkat_tree();
   if (!t) return MEERKAT_E_CUDA;
@@ -316,7 +328,8 @@ static meerkat_status tree_create(meerkat_graph* g, uint32_t source, bool unit, 
   TreeDev& T = t->dev;
   T.source = source;
   T.fr_cap = std::max<uint64_t>(std::max(g->out.buckets, g->in.buckets), 1);
-  const size_t V = g->V, words = (V + 31) / 32;
+  // node / stamp / invalid list: the vertices held here; invalid bit set: all vertices (global ids)
+  const size_t V = g->Vl, words = ((size_t)g->V + 31) / 32;
   cudaError_t e = cudaMalloc(&T.node, V * 8);
   if (e == cudaSuccess) e = cudaMalloc(&T.stamp, V * 4);
   if (e == cudaSuccess) e = cudaMalloc(&T.inval_bits, words * 4);
@@ -335,11 +348,21 @@ static meerkat_status tree_create(meerkat_graph* g, uint32_t source, bool unit, 
     if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
   }
   t->bytes = V * 8 + V * 4 + words * 4 + V * 4 + 2 * T.fr_cap * 8 + sizeof(TreeCtrl) + 4;
-  if (e == cudaSuccess) e = launch_tree(g, t, MODE_STATIC, nullptr, nullptr, nullptr, 0);
   if (e != cudaSuccess) {
     cudaGetLastError();
     meerkat_tree_destroy(t);
     return MEERKAT_E_CUDA;
+  }
+  if (dist) {
+    const meerkat_status st = dtree_init(g, t);
+    if (st != MEERKAT_OK) { meerkat_tree_destroy(t); return st; }
+  } else {
+    e = launch_tree(g, t, MODE_STATIC, nullptr, nullptr, nullptr, 0);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      meerkat_tree_destroy(t);
+      return MEERKAT_E_CUDA;
+    }
   }
   t->version = g->version;
   *out = t;
@@ -347,18 +370,18 @@ static meerkat_status tree_create(meerkat_graph* g, uint32_t source, bool unit, 
 }
 
 meerkat_status meerkat_sssp_create(meerkat_graph* g, uint32_t source, meerkat_tree** out) {
-  return tree_create(g, source, false, out);
+  return tree_create(g, source, false, false, out);
 }
 
 meerkat_status meerkat_bfs_create(meerkat_graph* g, uint32_t source, meerkat_tree** out) {
-  return tree_create(g, source, true, out);
+  return tree_create(g, source, true, false, out);
 }
 
 static meerkat_status tree_update(meerkat_graph* g, meerkat_tree* t, bool unit, int kind, const uint32_t* src,
                                   const uint32_t* dst, const uint32_t* w, uint64_t n) {
   meerkat_status st = check_batch(g, src, dst, n);
   if (st != MEERKAT_OK) return st;
-  if (!t || t->g != g || t->unit != unit) return MEERKAT_E_INVALID_ARG;
+  if (!t || t->g != g || t->unit != unit || t->dist) return MEERKAT_E_INVALID_ARG;
   // ordering contract: the batch must be the mutation just applied
   if (g->last_kind != kind || t->version + 1 != g->version) return MEERKAT_E_STATE;
   if (kind == 1 && !unit && n && !w) return MEERKAT_E_INVALID_ARG;
@@ -396,7 +419,7 @@ meerkat_status meerkat_bfs_decremental(meerkat_graph* g, meerkat_tree* t, const 
 }
 
 meerkat_status meerkat_tree_recompute(meerkat_graph* g, meerkat_tree* t) {
-  if (!g || !t || t->g != g) return MEERKAT_E_INVALID_ARG;
+  if (!g || !t || t->g != g || t->dist) return MEERKAT_E_INVALID_ARG;
   DeviceGuard dg(g->device);
   cudaError_t e = launch_tree(g, t, MODE_STATIC, nullptr, nullptr, nullptr, 0);
   if (e != cudaSuccess) return MEERKAT_E_CUDA;
@@ -409,7 +432,7 @@ meerkat_status meerkat_tree_nodes(meerkat_tree* t, uint64_t* out) {
   meerkat_graph* g = t->g;
   DeviceGuard dg(g->device);
   const bool host = !is_device_ptr(out);
-  cudaError_t e = cudaMemcpyAsync(out, t->dev.node, (size_t)g->V * 8,
+  cudaError_t e = cudaMemcpyAsync(out, t->dev.node, (size_t)g->Vl * 8,
                                   host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, g->stream);
   if (e != cudaSuccess) return MEERKAT_E_CUDA;
   if (host) return collect(g);
@@ -473,8 +496,54 @@ meerkat_status meerkat_tree_destroy(meerkat_tree* t) {
   cudaFree(T.node); cudaFree(T.stamp); cudaFree(T.inval_bits); cudaFree(T.inval_list);
   cudaFree(T.fr[0]); cudaFree(T.fr[1]); cudaFree(T.ctrl); cudaFree(T.epoch_ptr);
   if (t->hctrl) cudaFreeHost(t->hctrl);
+  dtree_free(t);
   delete t;
   return MEERKAT_OK;
+}
+
+// ------------------------------------------------------------------ vertex-partitioned trees
+
+meerkat_status meerkat_dtree_create(meerkat_graph* g, uint32_t source, uint32_t unit_weights, meerkat_tree** out) {
+  return tree_create(g, source, unit_weights != 0, true, out);
+}
+
+meerkat_status meerkat_dtree_phase(meerkat_graph* g, meerkat_tree* t, meerkat_dphase phase, const void* a,
+                                   const void* b, const void* c, uint64_t n, meerkat_dresult* out) {
+  if (!g || !t || t->g != g || !t->dist) return MEERKAT_E_INVALID_ARG;
+  DeviceGuard dg(g->device);
+  // batch inputs may live on the host (staged like every other call); received messages likewise
+  const void *da = a, *db = b, *dc = c;
+  cudaError_t e = cudaSuccess;
+  const bool pairs = phase == MEERKAT_D_APPLY_PROPAGATE || phase == MEERKAT_D_APPLY_RELAX;
+  if (a) e = stage_in(g, 0, a, n * (pairs ? 16 : 4), &da);
+  if (e == cudaSuccess && b) e = stage_in(g, 1, b, n * 4, &db);
+  if (e == cudaSuccess && c) e = stage_in(g, 2, c, n * 4, &dc);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  return dtree_phase(g, t, (int)phase, da, db, dc, n, out);
+}
+
+meerkat_status meerkat_memcpy(meerkat_graph* g, void* dst, const void* src, uint64_t bytes) {
+  if (!g || (bytes && (!dst || !src))) return MEERKAT_E_INVALID_ARG;
+  if (!bytes) return MEERKAT_OK;
+  DeviceGuard dg(g->device);
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, g->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  return from_cuda(e);
+}
+
+meerkat_status meerkat_route(meerkat_graph* g, int key_is_b, const uint32_t* a, const uint32_t* b, const uint32_t* c,
+                             uint64_t n, uint32_t* out_a, uint32_t* out_b, uint32_t* out_c, uint64_t* counts) {
+  if (!g || !counts || (n && (!a || !b || !out_a || !out_b || (c && !out_c)))) return MEERKAT_E_INVALID_ARG;
+  if (n && (!is_device_ptr(out_a) || !is_device_ptr(out_b) || (c && !is_device_ptr(out_c))))
+    return MEERKAT_E_INVALID_ARG;
+  DeviceGuard dg(g->device);
+  const void *da = a, *db = b, *dc = c;
+  cudaError_t e = stage_in(g, 0, a, n * 4, &da);
+  if (e == cudaSuccess) e = stage_in(g, 1, b, n * 4, &db);
+  if (e == cudaSuccess && c) e = stage_in(g, 2, c, n * 4, &dc);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  return route_batch(g, key_is_b, (const uint32_t*)da, (const uint32_t*)db, (const uint32_t*)dc, n, out_a, out_b,
+                     out_c, counts);
 }
 
 }  // extern "C"

@@ -1,0 +1,673 @@
+// dtree.cu — vertex-partitioned (multi-GPU) SSSP / BFS phases, SURVEY §8(e).
+//
+// Rank r holds the out-edges and the tree nodes of every vertex v with
+// v % world_size == r (local row v / world_size).  A tree update is the
+// single-GPU method run as lock-step PHASES on every rank:
+// an expansion relaxes edges into vertices held here directly and turns every
+// relaxation of a vertex held elsewhere into a message <x, packed candidate>
+// (or, while propagating invalidation, <x, expected parent>); the caller moves
+// the messages with one all-to-all per round (NCCL over NVLink) and the owner
+// applies them with the same packed atomicMin / CAS.  The fixpoint does not
+// depend on the order of relaxations, so results are
+// bit-identical to world_size 1.  Frontier rounds are host-driven here because
+// every round carries an exchange.
+#include <algorithm>
+#include <cstring>
+
+#include "tree_common.cuh"
+
+namespace mk {
+
+constexpr int D_BLOCK = 256;
+
+struct DArgs {
+  GraphDev G;
+  TreeDev T;
+  uint64_t* msgs;               // raw outgoing pairs (x, payload), 2 u64 each
+  unsigned long long* msg_n;    // raw pair count
+  uint64_t msg_cap;             // pairs
+  const uint64_t* fr;           // frontier being expanded (local rows)
+  uint64_t n;                   // its size
+  uint64_t* fnext;
+  unsigned long long* sznext;
+  uint32_t epoch;               // stamp epoch of fnext
+  uint32_t unit;
+};
+
+__device__ __forceinline__ bool owned(const GraphDev& G, uint32_t x) { return x % G.ws == G.rank; }
+__device__ __forceinline__ uint32_t lrow(const GraphDev& G, uint32_t x) { return x / G.ws; }
+__device__ __forceinline__ uint32_t grow(const GraphDev& G, uint32_t l) { return l * G.ws + G.rank; }
+
+// Warp-aggregated append of messages (same pattern as warpenqueuefrontier).
+__device__ __forceinline__ void warp_emit(const DArgs& A, bool has, uint32_t x, uint64_t payload, Counters& c) {
+  const uint32_t m = __ballot_sync(FULL, has);
+  if (!m) return;
+  const int lane = lane_id();
+  unsigned long long base = 0;
+  const int leader = __ffs(m) - 1;
+  if (lane == leader) base = atomicAdd(A.msg_n, (unsigned long long)__popc(m));
+  base = __shfl_sync(FULL, base, leader);
+  if (has) {
+    const uint64_t p = base + __popc(m & ((1u << lane) - 1));
+    if (p < A.msg_cap) { A.msgs[2 * p] = x; A.msgs[2 * p + 1] = payload; }
+    else c.err |= ERR_CAPACITY;
+  }
+}
+
+// relax() with an already packed candidate (received message)
+__device__ __forceinline__ bool relax_packed(const TreeDev& T, uint32_t lx, uint64_t cand, uint32_t epoch,
+                                             Counters& c) {
+  if (cand >= ld_cg_u64(T.node + lx)) return false;
+  const unsigned long long old = atomicMin(reinterpret_cast<unsigned long long*>(T.node + lx), cand);
+  if (cand >= old) return false;
+  c.improved++;
+  return atomicExch(T.stamp + lx, epoch) != epoch;
+}
+
+__global__ void k_dinit(DArgs A) {
+  for (uint64_t l = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; l < A.G.V; l += (uint64_t)gridDim.x * blockDim.x)
+    A.T.node[l] = (grow(A.G, (uint32_t)l) == A.T.source) ? (uint64_t)A.T.source : UNREACHED;
+}
+
+__global__ void k_dseed_source(DArgs A) {   // one warp: frontier = {SRC} on its owner (C16)
+  Counters c;
+  const bool has = threadIdx.x == 0 && owned(A.G, A.T.source);
+  const uint32_t l = lrow(A.G, A.T.source);
+  if (has) A.T.stamp[l] = A.epoch;
+  warp_enqueue(A.G, A.T, A.fnext, A.sznext, has, l, c);
+}
+
+// Incremental prologue: batch edges (u, v, w) with u held here.
+__global__ void __launch_bounds__(D_BLOCK) k_dinc_seed(DArgs A, const uint32_t* bs, const uint32_t* bd,
+                                                       const uint32_t* bw, uint64_t bn) {
+  Counters c;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t trips = (bn + nt - 1) / nt;
+  for (uint64_t t = 0; t < trips; t++) {
+    const uint64_t i = tid + t * nt;
+    bool enq = false, emit = false;
+    uint32_t v = 0, lv = 0;
+    uint64_t cand = 0;
+    if (i < bn) {
+      const uint32_t u = bs[i];
+      v = bd[i];
+      const uint32_t w = A.unit ? 1u : bw[i];
+      c.batch++;
+      if (u < A.G.Vg && v < A.G.Vg && (A.unit || (w != 0 && w < W_LIMIT))) {
+        if (!owned(A.G, u)) c.err |= ERR_PARTITION;
+        else {
+          const uint64_t nu = ld_cg_u64(A.T.node + lrow(A.G, u));
+          if (nu != UNREACHED) {
+            const uint64_t dist = (nu >> 32) + w;
+            if (dist >= INF_DIST) c.err |= ERR_OVERFLOW;
+            else if (owned(A.G, v)) { lv = lrow(A.G, v); enq = relax(A.T, lv, dist, u, A.epoch, c); }
+            else { emit = true; cand = (dist << 32) | u; }
+          }
+        }
+      }
+    }
+    warp_enqueue(A.G, A.T, A.fnext, A.sznext, enq, lv, c);
+    warp_emit(A, emit, v, cand, c);
+  }
+  flush_counters(A.G, A.T, c, false, 0, 0);
+}
+
+// Decremental Invalidate: deleted edges (u, v) with v held here.
+__global__ void __launch_bounds__(D_BLOCK) k_ddec_inval(DArgs A, const uint32_t* bs, const uint32_t* bd, uint64_t bn) {
+  Counters c;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t trips = (bn + nt - 1) / nt;
+  for (uint64_t t = 0; t < trips; t++) {
+    const uint64_t i = tid + t * nt;
+    bool enq = false;
+    uint32_t lv = 0;
+    if (i < bn) {
+      const uint32_t u = bs[i], v = bd[i];
+      c.batch++;
+      if (u < A.G.Vg && v < A.G.Vg && v != A.T.source) {
+        if (!owned(A.G, v)) c.err |= ERR_PARTITION;
+        else {
+          lv = lrow(A.G, v);
+          const uint64_t cur = ld_cg_u64(A.T.node + lv);
+          if (cur != UNREACHED && (uint32_t)cur == u &&
+              atomicCAS(reinterpret_cast<unsigned long long*>(A.T.node + lv), (unsigned long long)cur,
+                        (unsigned long long)UNREACHED) == cur) {
+            mark_invalid(A.T, v);
+            atomicAdd(&A.T.ctrl->direct_n, 1ull);
+            enq = true;
+          }
+        }
+      }
+    }
+    warp_enqueue(A.G, A.T, A.fnext, A.sznext, enq, lv, c);
+  }
+  flush_counters(A.G, A.T, c, false, 0, 0);
+}
+
+// One round of expansion of the local frontier (P:113-133 relax, or P:149-154 propagate).
+template <bool MAP, int VISIT>
+__global__ void __launch_bounds__(D_BLOCK) k_dexpand(DArgs A) {
+  using F = Frag<MAP>;
+  constexpr int NK = F::NK;
+  Counters c;
+  const GraphDev& G = A.G;
+  const TreeDev& T = A.T;
+  const int lane = lane_id(), l8 = lane & 7;
+  const uint64_t ng = ((uint64_t)gridDim.x * blockDim.x) / GROUP;
+  uint64_t it = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / GROUP;
+  uint32_t v = 0, slab = 0, du = 0;
+  auto fetch = [&]() -> bool {
+    for (; it < A.n; it += ng) {
+      const uint64_t item = A.fr[it];
+      v = (uint32_t)item;
+      const uint32_t head = __ldcg(reinterpret_cast<const unsigned int*>(&G.vmeta[v].x));
+      if (l8 == 0) c.items++;
+      if (head == INVALID_SLAB) continue;
+      slab = head + (uint32_t)(item >> 32);
+      if (VISIT == PROPAGATE) return true;
+      const uint64_t nv = ld_cg_u64(T.node + v);
+      if (nv != UNREACHED) { du = (uint32_t)(nv >> 32); return true; }
+    }
+    return false;
+  };
+  bool active = fetch();
+  while (__any_sync(FULL, active)) {
+    uint4 d = make_uint4(EMPTY_KEY, EMPTY_KEY, EMPTY_KEY, INVALID_SLAB);
+    if (active) {
+      d = ld_slab_ro(slab_ptr(G, slab), l8);
+      if (l8 == 0) c.slabs++;
+    }
+    const uint32_t vg = grow(G, v);
+#pragma unroll
+    for (int k = 0; k < NK; k++) {
+      const uint32_t x = F::key(d, k);
+      const bool live = active && F::valid_cell(l8, k) && x < G.Vg;
+      bool enq = false, emit = false;
+      uint64_t payload = 0;
+      uint32_t lx = 0;
+      if (live) {
+        c.visited++;
+        if (VISIT == RELAX) {
+          const uint64_t dist = (uint64_t)du + (A.unit ? 1u : F::weight(d, k));
+          if (dist >= INF_DIST) c.err |= ERR_OVERFLOW;
+          else if (owned(G, x)) { lx = lrow(G, x); enq = relax(T, lx, dist, vg, A.epoch, c); }
+          else { emit = true; payload = (dist << 32) | vg; }
+        } else {
+          if (owned(G, x)) {
+            lx = lrow(G, x);
+            const uint64_t cur = ld_cg_u64(T.node + lx);
+            if (cur != UNREACHED && (uint32_t)cur == vg && x != T.source &&
+                atomicCAS(reinterpret_cast<unsigned long long*>(T.node + lx), (unsigned long long)cur,
+                          (unsigned long long)UNREACHED) == cur) {
+              mark_invalid(T, x);
+              enq = true;
+            }
+          } else {
+            emit = true;
+            payload = vg;
+          }
+        }
+      }
+      warp_enqueue(G, T, A.fnext, A.sznext, enq, lx, c);
+      warp_emit(A, emit, x, payload, c);
+    }
+    const uint32_t nxt = __shfl_sync(FULL, d.w, (lane & 24) + GROUP - 1);
+    if (active) {
+      if (nxt != INVALID_SLAB) slab = nxt;
+      else { it += ng; active = fetch(); }
+    }
+  }
+  flush_counters(A.G, A.T, c, false, 0, 0);
+}
+
+// Apply received messages (x held here): relaxation candidates or invalidation requests.
+template <int VISIT>
+__global__ void __launch_bounds__(D_BLOCK) k_dapply(DArgs A, const uint64_t* in, uint64_t n_in) {
+  Counters c;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t trips = (n_in + nt - 1) / nt;
+  for (uint64_t t = 0; t < trips; t++) {
+    const uint64_t i = tid + t * nt;
+    bool enq = false;
+    uint32_t lx = 0;
+    if (i < n_in) {
+      const uint32_t x = (uint32_t)in[2 * i];
+      const uint64_t p = in[2 * i + 1];
+      if (x >= A.G.Vg || !owned(A.G, x)) c.err |= ERR_PARTITION;
+      else {
+        lx = lrow(A.G, x);
+        if (VISIT == RELAX) {
+          enq = relax_packed(A.T, lx, p, A.epoch, c);
+        } else {
+          const uint64_t cur = ld_cg_u64(A.T.node + lx);
+          if (cur != UNREACHED && (uint32_t)cur == (uint32_t)p && x != A.T.source &&
+              atomicCAS(reinterpret_cast<unsigned long long*>(A.T.node + lx), (unsigned long long)cur,
+                        (unsigned long long)UNREACHED) == cur) {
+            mark_invalid(A.T, x);
+            enq = true;
+          }
+        }
+      }
+    }
+    warp_enqueue(A.G, A.T, A.fnext, A.sznext, enq, lx, c);
+  }
+  flush_counters(A.G, A.T, c, false, 0, 0);
+}
+
+// Set / clear the marks of ALL ranks' invalid vertices (global bit set).
+__global__ void k_dmark(uint32_t* bits, const uint32_t* list, uint64_t n, int set) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t x = list[i];
+    if (set) atomicOr(bits + (x >> 5), 1u << (x & 31));
+    else atomicAnd(bits + (x >> 5), ~(1u << (x & 31)));
+  }
+}
+
+// Valid->invalid frontier over this rank's slabs: stream + smem filter,
+// as dec_scan in tree.cu, with relaxations of remote invalid vertices sent as messages.
+template <bool MAP>
+__global__ void __launch_bounds__(TREE_BLOCK, 2) k_dscan(DArgs A, const uint32_t* list, uint64_t n_inv,
+                                                         uint32_t fwords, uint32_t n_slabs) {
+  using F = Frag<MAP>;
+  constexpr int NK = F::NK;
+  constexpr int U = SCAN_UNROLL;
+  extern __shared__ uint32_t filt[];
+  Counters c;
+  const GraphDev& G = A.G;
+  const TreeDev& T = A.T;
+  if (fwords) {
+    for (uint32_t i = threadIdx.x; i < fwords; i += blockDim.x) filt[i] = 0;
+    __syncthreads();
+    for (uint64_t i = threadIdx.x; i < n_inv; i += blockDim.x) {
+      uint32_t w, m;
+      filter_loc(__ldg(list + i), fwords, w, m);
+      atomicOr(&filt[w], m);
+    }
+    __syncthreads();
+  }
+  const int l8 = lane_id() & 7;
+  const uint32_t ng = (gridDim.x * blockDim.x) / GROUP;
+  const uint32_t g0 = (blockIdx.x * blockDim.x + threadIdx.x) / GROUP;
+  const uint32_t span = ng * U;
+  const uint32_t trips = (n_slabs + span - 1) / span;
+  const uint4* __restrict__ base = reinterpret_cast<const uint4*>(G.slabs) + l8;
+  for (uint32_t t = 0; t < trips; t++) {
+    const uint32_t s0 = t * span + g0;
+    uint4 d[U];
+#pragma unroll
+    for (int q = 0; q < U; q++) {
+      const uint32_t s = s0 + q * ng;
+      d[q] = make_uint4(EMPTY_KEY, EMPTY_KEY, EMPTY_KEY, INVALID_SLAB);
+      if (s < n_slabs) d[q] = ld_slab_ro(reinterpret_cast<const uint32_t*>(base + (size_t)s * 8), 0);
+    }
+    uint32_t hm = 0;
+#pragma unroll
+    for (int q = 0; q < U; q++)
+#pragma unroll
+      for (int k = 0; k < NK; k++) {
+        const uint32_t x = F::key(d[q], k);
+        bool hit = x < G.Vg && (MAP || F::valid_cell(l8, k));
+        if (fwords) {
+          uint32_t w, m;
+          filter_loc(x, fwords, w, m);
+          hit = hit && (filt[w] & m) == m;
+        }
+        hm |= (uint32_t)hit << (q * NK + k);
+      }
+    const uint32_t pos = __reduce_or_sync(FULL, hm);
+    if (!pos) continue;
+#pragma unroll
+    for (int q = 0; q < U; q++)
+#pragma unroll
+      for (int k = 0; k < NK; k++) {
+        if (!((pos >> (q * NK + k)) & 1u)) continue;
+        const uint32_t x = F::key(d[q], k);
+        bool enq = false, emit = false;
+        uint32_t lx = 0;
+        uint64_t payload = 0;
+        if (((hm >> (q * NK + k)) & 1u) && bit_test(T.inval_bits, x)) {
+          const uint32_t ul = __ldg(G.owner + s0 + q * ng);
+          const uint32_t ug = ul == NO_OWNER ? NO_OWNER : grow(G, ul);
+          if (ul != NO_OWNER && !bit_test(T.inval_bits, ug)) {
+            const uint64_t nu = ld_cg_u64(T.node + ul);
+            if (nu != UNREACHED) {
+              c.hits++;
+              const uint64_t dist = (nu >> 32) + (A.unit ? 1u : F::weight(d[q], k));
+              if (dist >= INF_DIST) c.err |= ERR_OVERFLOW;
+              else if (owned(G, x)) { lx = lrow(G, x); enq = relax(T, lx, dist, ug, A.epoch, c); }
+              else { emit = true; payload = (dist << 32) | ug; }
+            }
+          }
+        }
+        warp_enqueue(G, T, A.fnext, A.sznext, enq, lx, c);
+        warp_emit(A, emit, x, payload, c);
+      }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) c.scan_slabs = n_slabs;
+  flush_counters(A.G, A.T, c, false, 0, 0);
+}
+
+// ---- group messages by owner rank: histogram, exclusive scan, scatter
+__global__ void k_msg_hist(const uint64_t* msgs, const unsigned long long* n_ptr, uint32_t ws,
+                           unsigned long long* counts) {
+  __shared__ unsigned int h[MEERKAT_MAX_RANKS];
+  for (uint32_t i = threadIdx.x; i < ws; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const uint64_t n = *n_ptr;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    atomicAdd(&h[(uint32_t)msgs[2 * i] % ws], 1u);
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < ws; i += blockDim.x)
+    if (h[i]) atomicAdd(&counts[i], (unsigned long long)h[i]);
+}
+
+__global__ void k_msg_scan(const unsigned long long* counts, uint32_t ws, unsigned long long* cursor) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    unsigned long long run = 0;
+    for (uint32_t i = 0; i < ws; i++) { cursor[i] = run; run += counts[i]; }
+  }
+}
+
+__global__ void k_msg_scatter(const uint64_t* msgs, const unsigned long long* n_ptr, uint32_t ws,
+                              unsigned long long* cursor, uint64_t* out) {
+  const uint64_t n = *n_ptr;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t x = msgs[2 * i];
+    const unsigned long long p = atomicAdd(&cursor[(uint32_t)x % ws], 1ull);
+    out[2 * p] = x;
+    out[2 * p + 1] = msgs[2 * i + 1];
+  }
+}
+
+// ---- batch routing by owner(key)
+__global__ void k_route_hist(const uint32_t* key, uint64_t n, uint32_t ws, unsigned long long* counts) {
+  __shared__ unsigned int h[MEERKAT_MAX_RANKS];
+  for (uint32_t i = threadIdx.x; i < ws; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    atomicAdd(&h[key[i] % ws], 1u);
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < ws; i += blockDim.x)
+    if (h[i]) atomicAdd(&counts[i], (unsigned long long)h[i]);
+}
+
+__global__ void k_route_scatter(const uint32_t* a, const uint32_t* b, const uint32_t* c3, const uint32_t* key,
+                                uint64_t n, uint32_t ws, unsigned long long* cursor, uint32_t* oa, uint32_t* ob,
+                                uint32_t* oc) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long p = atomicAdd(&cursor[key[i] % ws], 1ull);
+    oa[p] = a[i];
+    ob[p] = b[i];
+    if (c3) oc[p] = c3[i];
+  }
+}
+
+// ------------------------------------------------------------------ host launchers
+
+static unsigned dgrid(meerkat_graph* g, uint64_t threads) {
+  uint64_t b = (threads + D_BLOCK - 1) / D_BLOCK;
+  const uint64_t cap = (uint64_t)g->sm_count * 8;
+  return (unsigned)std::max<uint64_t>(1, std::min(b, cap));
+}
+
+cudaError_t dlaunch(meerkat_graph* g, int kind, DArgs& A, const void* a, const void* b, const void* c, uint64_t n,
+                    uint32_t fwords, uint32_t n_slabs) {
+  cudaStream_t st = g->stream;
+  const bool map = g->weighted;
+  switch (kind) {
+    case 0:   // init + seed source
+      k_dinit<<<dgrid(g, A.G.V), D_BLOCK, 0, st>>>(A);
+      k_dseed_source<<<1, 32, 0, st>>>(A);
+      g->launches += 2;
+      break;
+    case 1:
+      k_dinc_seed<<<dgrid(g, n), D_BLOCK, 0, st>>>(A, (const uint32_t*)a, (const uint32_t*)b, (const uint32_t*)c, n);
+      g->launches++;
+      break;
+    case 2:
+      k_ddec_inval<<<dgrid(g, n), D_BLOCK, 0, st>>>(A, (const uint32_t*)a, (const uint32_t*)b, n);
+      g->launches++;
+      break;
+    case 3:
+      if (map) k_dexpand<true, PROPAGATE><<<dgrid(g, A.n * GROUP), D_BLOCK, 0, st>>>(A);
+      else k_dexpand<false, PROPAGATE><<<dgrid(g, A.n * GROUP), D_BLOCK, 0, st>>>(A);
+      g->launches++;
+      break;
+    case 4:
+      k_dapply<PROPAGATE><<<dgrid(g, n), D_BLOCK, 0, st>>>(A, (const uint64_t*)a, n);
+      g->launches++;
+      break;
+    case 5: {
+      const size_t smem = (size_t)fwords * 4;
+      const unsigned grid = (unsigned)(g->sm_count * std::max(1, g->tree_blocks_per_sm[2]));
+      if (map) k_dscan<true><<<grid, TREE_BLOCK, smem, st>>>(A, (const uint32_t*)a, n, fwords, n_slabs);
+      else k_dscan<false><<<grid, TREE_BLOCK, smem, st>>>(A, (const uint32_t*)a, n, fwords, n_slabs);
+      g->launches++;
+      break;
+    }
+    case 6:
+      if (map) k_dexpand<true, RELAX><<<dgrid(g, A.n * GROUP), D_BLOCK, 0, st>>>(A);
+      else k_dexpand<false, RELAX><<<dgrid(g, A.n * GROUP), D_BLOCK, 0, st>>>(A);
+      g->launches++;
+      break;
+    case 7:
+      k_dapply<RELAX><<<dgrid(g, n), D_BLOCK, 0, st>>>(A, (const uint64_t*)a, n);
+      g->launches++;
+      break;
+    case 9:   // mark / clear: a = list, n, c != 0 means set
+      k_dmark<<<dgrid(g, n), D_BLOCK, 0, st>>>(A.T.inval_bits, (const uint32_t*)a, n, c != nullptr);
+      g->launches++;
+      break;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t dsort_msgs(meerkat_graph* g, const uint64_t* raw, const unsigned long long* n_ptr, uint64_t n_host,
+                       unsigned long long* counts, unsigned long long* cursor, uint64_t* out) {
+  cudaError_t e = cudaMemsetAsync(counts, 0, MEERKAT_MAX_RANKS * 8, g->stream);
+  if (e != cudaSuccess || n_host == 0) return e;
+  const unsigned gb = dgrid(g, n_host);
+  k_msg_hist<<<gb, D_BLOCK, 0, g->stream>>>(raw, n_ptr, g->ws, counts);
+  k_msg_scan<<<1, 32, 0, g->stream>>>(counts, g->ws, cursor);
+  k_msg_scatter<<<gb, D_BLOCK, 0, g->stream>>>(raw, n_ptr, g->ws, cursor, out);
+  g->launches += 3;
+  return cudaGetLastError();
+}
+
+cudaError_t droute(meerkat_graph* g, const uint32_t* a, const uint32_t* b, const uint32_t* c, const uint32_t* key,
+                   uint64_t n, uint32_t* oa, uint32_t* ob, uint32_t* oc, unsigned long long* counts,
+                   unsigned long long* cursor) {
+  cudaError_t e = cudaMemsetAsync(counts, 0, MEERKAT_MAX_RANKS * 8, g->stream);
+  if (e != cudaSuccess || n == 0) return e;
+  const unsigned gb = dgrid(g, n);
+  k_route_hist<<<gb, D_BLOCK, 0, g->stream>>>(key, n, g->ws, counts);
+  k_msg_scan<<<1, 32, 0, g->stream>>>(counts, g->ws, cursor);
+  k_route_scatter<<<gb, D_BLOCK, 0, g->stream>>>(a, b, c, key, n, g->ws, cursor, oa, ob, oc);
+  g->launches += 3;
+  return cudaGetLastError();
+}
+
+cudaError_t dscan_attr(meerkat_graph* g) {
+  const int smem = FILTER_WORDS * 4;
+  cudaError_t e = cudaFuncSetAttribute(k_dscan<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_dscan<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  return e;
+}
+
+}  // namespace mk
+
+// ------------------------------------------------------------------ host side of the phases
+
+namespace mk {
+
+static meerkat_status status_of(cudaError_t e) { return e == cudaSuccess ? MEERKAT_OK : MEERKAT_E_CUDA; }
+
+static meerkat_status graph_err(meerkat_graph* g) {
+  // read and clear the sticky error of the out store (phase kernels report there)
+  cudaError_t e = cudaMemcpyAsync(g->out.hctrl, g->out.dev.ctrl, sizeof(GraphCtrl), cudaMemcpyDeviceToHost, g->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  const uint32_t err = g->out.hctrl->err;
+  if (!err) return MEERKAT_OK;
+  cudaMemsetAsync(&g->out.dev.ctrl->err, 0, 4, g->stream);
+  if (err & ERR_PARTITION) return MEERKAT_E_PARTITION;
+  if (err & ERR_RANGE) return MEERKAT_E_VERTEX_RANGE;
+  if (err & ERR_WEIGHT) return MEERKAT_E_WEIGHT;
+  if (err & ERR_CAPACITY) return MEERKAT_E_CAPACITY;
+  if (err & ERR_OVERFLOW) return MEERKAT_E_OVERFLOW;
+  return MEERKAT_E_STATE;
+}
+
+static cudaError_t ensure_msgs(meerkat_graph* g, meerkat_tree* t, uint64_t need) {
+  if (need <= t->msg_cap) return cudaSuccess;
+  cudaError_t e = cudaStreamSynchronize(g->stream);
+  if (e != cudaSuccess) return e;
+  cudaFree(t->msg_raw);
+  cudaFree(t->msg_out);
+  t->msg_raw = t->msg_out = nullptr;
+  t->msg_cap = 0;
+  const uint64_t cap = std::max<uint64_t>(need + need / 4, 1 << 16);
+  e = cudaMalloc(&t->msg_raw, cap * 16);
+  if (e == cudaSuccess) e = cudaMalloc(&t->msg_out, cap * 16);
+  if (e == cudaSuccess) t->msg_cap = cap;
+  return e;
+}
+
+meerkat_status dtree_init(meerkat_graph* g, meerkat_tree* t) {
+  t->dist = true;
+  cudaError_t e = cudaMalloc(&t->dcnt, (2 * MEERKAT_MAX_RANKS + 1) * 8);
+  if (e == cudaSuccess) e = cudaMallocHost(&t->hcnt, (MEERKAT_MAX_RANKS + 4) * 8);
+  if (e == cudaSuccess) e = dscan_attr(g);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  return dtree_phase(g, t, MEERKAT_D_STATIC_INIT, nullptr, nullptr, nullptr, 0, nullptr);
+}
+
+void dtree_free(meerkat_tree* t) {
+  cudaFree(t->msg_raw);
+  cudaFree(t->msg_out);
+  cudaFree(t->dcnt);
+  if (t->hcnt) cudaFreeHost(t->hcnt);
+}
+
+meerkat_status dtree_phase(meerkat_graph* g, meerkat_tree* t, int phase, const void* a, const void* b, const void* c,
+                           uint64_t n, meerkat_dresult* out) {
+  const bool seed = phase == MEERKAT_D_STATIC_INIT || phase == MEERKAT_D_INC_SEED ||
+                    phase == MEERKAT_D_DEC_INVALIDATE || phase == MEERKAT_D_DEC_SCAN;
+  const bool expands = phase == MEERKAT_D_PROPAGATE || phase == MEERKAT_D_RELAX;
+  const bool apply = phase == MEERKAT_D_APPLY_PROPAGATE || phase == MEERKAT_D_APPLY_RELAX;
+  const bool emits = phase == MEERKAT_D_INC_SEED || expands || phase == MEERKAT_D_DEC_SCAN;
+  if (!seed && !expands && !apply && phase != MEERKAT_D_FINISH) return MEERKAT_E_INVALID_ARG;
+  if (n && (phase == MEERKAT_D_INC_SEED || phase == MEERKAT_D_DEC_INVALIDATE) && (!a || !b)) return MEERKAT_E_INVALID_ARG;
+  if (n && (apply || phase == MEERKAT_D_DEC_SCAN || phase == MEERKAT_D_FINISH) && !a) return MEERKAT_E_INVALID_ARG;
+  if (phase == MEERKAT_D_INC_SEED && !t->unit && n && !c) return MEERKAT_E_INVALID_ARG;
+  // ordering contract, as for the single-GPU calls
+  if (phase == MEERKAT_D_INC_SEED && (g->last_kind != 1 || t->version + 1 != g->version)) return MEERKAT_E_STATE;
+  if (phase == MEERKAT_D_DEC_INVALIDATE && (g->last_kind != 2 || t->version + 1 != g->version)) return MEERKAT_E_STATE;
+  TreeDev& T = t->dev;
+  cudaError_t e = cudaSuccess;
+  if (phase == MEERKAT_D_STATIC_INIT || phase == MEERKAT_D_INC_SEED || phase == MEERKAT_D_DEC_INVALIDATE) {
+    e = cudaMemsetAsync(T.ctrl, 0, sizeof(TreeCtrl), g->stream);   // a new update: counters and sizes
+    t->hctrl->inval_n = 0;
+  }
+  // frontier buffers: `cur` holds the frontier filled last; new frontiers go to the other one
+  int nb = t->cur;
+  uint64_t cur_n = 0;
+  if (seed || expands) {
+    if (expands) {
+      e = cudaMemcpyAsync(t->hcnt + MEERKAT_MAX_RANKS + 1, &T.ctrl->size[t->cur], 8, cudaMemcpyDeviceToHost, g->stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+      cur_n = t->hcnt[MEERKAT_MAX_RANKS + 1];
+    }
+    nb = 1 - t->cur;
+    if (e == cudaSuccess) e = cudaMemsetAsync(&T.ctrl->size[nb], 0, 8, g->stream);
+    t->depoch++;
+  }
+  if (e == cudaSuccess && emits) {
+    uint64_t need = n;
+    if (phase != MEERKAT_D_INC_SEED) {
+      e = cudaMemcpyAsync(g->out.hctrl, g->out.dev.ctrl, sizeof(GraphCtrl), cudaMemcpyDeviceToHost, g->stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+      need = g->out.hctrl->ins_total - g->out.hctrl->del_total;   // one message per visited edge at most
+    }
+    if (e == cudaSuccess) e = ensure_msgs(g, t, need + 1024);
+    if (e == cudaSuccess) e = cudaMemsetAsync(t->dcnt + 2 * MEERKAT_MAX_RANKS, 0, 8, g->stream);
+  }
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  DArgs A;
+  A.G = g->out.dev;
+  A.T = T;
+  A.msgs = t->msg_raw;
+  A.msg_n = t->dcnt + 2 * MEERKAT_MAX_RANKS;
+  A.msg_cap = t->msg_cap;
+  A.fr = T.fr[t->cur];
+  A.n = cur_n;
+  A.fnext = T.fr[nb];
+  A.sznext = &T.ctrl->size[nb];
+  A.epoch = t->depoch;
+  A.unit = t->unit ? 1u : 0u;
+  switch (phase) {
+    case MEERKAT_D_STATIC_INIT: e = dlaunch(g, 0, A, nullptr, nullptr, nullptr, 0, 0, 0); break;
+    case MEERKAT_D_INC_SEED: e = dlaunch(g, 1, A, a, b, c, n, 0, 0); break;
+    case MEERKAT_D_DEC_INVALIDATE: e = dlaunch(g, 2, A, a, b, nullptr, n, 0, 0); break;
+    case MEERKAT_D_PROPAGATE: if (cur_n) e = dlaunch(g, 3, A, nullptr, nullptr, nullptr, 0, 0, 0); break;
+    case MEERKAT_D_APPLY_PROPAGATE: e = dlaunch(g, 4, A, a, nullptr, nullptr, n, 0, 0); break;
+    case MEERKAT_D_RELAX: if (cur_n) e = dlaunch(g, 6, A, nullptr, nullptr, nullptr, 0, 0, 0); break;
+    case MEERKAT_D_APPLY_RELAX: e = dlaunch(g, 7, A, a, nullptr, nullptr, n, 0, 0); break;
+    case MEERKAT_D_DEC_SCAN: {
+      if (n) {
+        e = dlaunch(g, 9, A, a, nullptr, (const void*)1, n, 0, 0);   // mark every rank's invalid vertices
+        const uint32_t fw = (n * 8 <= (uint64_t)FILTER_WORDS * 32) ? FILTER_WORDS : 0u;
+        const uint32_t n_slabs = (uint32_t)(g->out.H + std::min<uint64_t>(g->out.hctrl->pool_top, g->out.P));
+        if (e == cudaSuccess) e = dlaunch(g, 5, A, a, nullptr, nullptr, n, fw, n_slabs);
+      }
+      break;
+    }
+    case MEERKAT_D_FINISH:
+      if (n) e = dlaunch(g, 9, A, a, nullptr, nullptr, n, 0, 0);   // clear the marks
+      t->version = g->version;
+      break;
+  }
+  if (e == cudaSuccess && emits) {
+    unsigned long long* counts = t->dcnt;
+    unsigned long long* cursor = t->dcnt + MEERKAT_MAX_RANKS;
+    e = cudaMemcpyAsync(t->hcnt + MEERKAT_MAX_RANKS, A.msg_n, 8, cudaMemcpyDeviceToHost, g->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+    const uint64_t raw = t->hcnt[MEERKAT_MAX_RANKS];
+    if (e == cudaSuccess) e = dsort_msgs(g, t->msg_raw, A.msg_n, raw, counts, cursor, t->msg_out);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(t->hcnt, counts, MEERKAT_MAX_RANKS * 8, cudaMemcpyDeviceToHost, g->stream);
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(t->hctrl, T.ctrl, sizeof(TreeCtrl), cudaMemcpyDeviceToHost, g->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  if (seed || expands) t->cur = nb;
+  if (phase == MEERKAT_D_INC_SEED || phase == MEERKAT_D_DEC_INVALIDATE || phase == MEERKAT_D_STATIC_INIT)
+    t->version = g->version;
+  if (out) {
+    std::memset(out, 0, sizeof(*out));
+    out->msgs = t->msg_out;
+    if (emits)
+      for (uint32_t r = 0; r < g->ws && r < MEERKAT_MAX_RANKS; r++) out->msg_counts[r] = t->hcnt[r];
+    out->frontier = t->hctrl->size[t->cur];
+    out->invalid = T.inval_list;
+    out->invalid_n = t->hctrl->inval_n;
+  }
+  return graph_err(g);
+}
+
+meerkat_status route_batch(meerkat_graph* g, int key_is_b, const uint32_t* a, const uint32_t* b, const uint32_t* c,
+                           uint64_t n, uint32_t* oa, uint32_t* ob, uint32_t* oc, uint64_t* counts) {
+  cudaError_t e = cudaSuccess;
+  if (!g->rscratch) e = cudaMalloc(&g->rscratch, 2 * MEERKAT_MAX_RANKS * 8);   // counts[64] + cursor[64]
+  if (e == cudaSuccess && !g->hrscratch) e = cudaMallocHost(&g->hrscratch, MEERKAT_MAX_RANKS * 8);
+  unsigned long long* scratch = g->rscratch;
+  unsigned long long* hscratch = g->hrscratch;
+  if (e == cudaSuccess)
+    e = droute(g, a, b, c, key_is_b ? b : a, n, oa, ob, oc, scratch, scratch + MEERKAT_MAX_RANKS);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(hscratch, scratch, MEERKAT_MAX_RANKS * 8, cudaMemcpyDeviceToHost, g->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  for (uint32_t r = 0; r < g->ws; r++) counts[r] = n ? hscratch[r] : 0;
+  return MEERKAT_OK;
+}
+
+}  // namespace mk

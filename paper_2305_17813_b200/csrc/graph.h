@@ -52,7 +52,9 @@ struct Store {
 struct meerkat_graph {
   int device = 0;
   cudaStream_t stream = nullptr;
-  uint32_t V = 0;
+  uint32_t V = 0;                   // global vertex count
+  uint32_t Vl = 0;                  // vertices held by this partition
+  uint32_t ws = 1, rank = 0;        // vertex partition (owner(v) = v % ws)
   bool weighted = false, hashing = true, reverse = false;
   float lf = 0.7f;
   mk::Store out;                    // out-edge store (the paper's SlabGraph)
@@ -63,7 +65,9 @@ struct meerkat_graph {
   int sm_count = 0;
   void* stage[4] = {nullptr, nullptr, nullptr, nullptr};   // staging for host inputs / outputs
   size_t stage_bytes[4] = {0, 0, 0, 0};
-  int tree_blocks_per_sm[3] = {0, 0, 0};   // cooperative occupancy: static/incremental, decremental (set, map)
+  int tree_blocks_per_sm[3] = {0, 0, 0};   // cooperative occupancy: static, incremental, decremental
+  unsigned long long* rscratch = nullptr;   // meerkat_route: device counts + cursors
+  unsigned long long* hrscratch = nullptr;  // pinned counts
 };
 
 struct meerkat_tree {
@@ -72,6 +76,15 @@ struct meerkat_tree {
   mk::TreeCtrl* hctrl = nullptr;
   bool unit = false;     // BFS
   uint64_t version = 0;
+  // vertex-partitioned trees (dtree.cu)
+  bool dist = false;
+  int cur = 0;                              // frontier buffer filled by the last phase
+  uint32_t depoch = 0;                      // stamp epoch of the frontier being filled
+  uint64_t* msg_raw = nullptr;              // outgoing pairs, unsorted
+  uint64_t* msg_out = nullptr;              // outgoing pairs grouped by destination rank
+  uint64_t msg_cap = 0;                     // pairs
+  unsigned long long* dcnt = nullptr;       // device: counts[64], cursor[64], msg_n
+  unsigned long long* hcnt = nullptr;       // pinned mirror of counts + msg_n
   uint32_t last_inval_n = 0;
   size_t bytes = 0;
 };
@@ -91,4 +104,11 @@ cudaError_t tree_occupancy(meerkat_graph* g);
 enum TreeMode { MODE_STATIC = 0, MODE_INCREMENTAL = 1, MODE_DECREMENTAL = 2 };
 cudaError_t launch_tree(meerkat_graph* g, meerkat_tree* t, int mode, const uint32_t* s, const uint32_t* d,
                         const uint32_t* w, uint64_t n);
+// dtree.cu
+meerkat_status dtree_phase(meerkat_graph* g, meerkat_tree* t, int phase, const void* a, const void* b,
+                           const void* c, uint64_t n, meerkat_dresult* out);
+meerkat_status dtree_init(meerkat_graph* g, meerkat_tree* t);
+void dtree_free(meerkat_tree* t);
+meerkat_status route_batch(meerkat_graph* g, int key_is_b, const uint32_t* a, const uint32_t* b, const uint32_t* c,
+                           uint64_t n, uint32_t* oa, uint32_t* ob, uint32_t* oc, uint64_t* counts);
 }  // namespace mk

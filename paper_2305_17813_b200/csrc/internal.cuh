@@ -33,7 +33,8 @@ constexpr int SLAB_WORDS = 32;
 constexpr int GROUP = 8;                                 // lanes per slab
 constexpr int SET_CAP = 31, MAP_CAP = 15;
 
-enum ErrBits : uint32_t { ERR_RANGE = 1, ERR_WEIGHT = 2, ERR_CAPACITY = 4, ERR_OVERFLOW = 8, ERR_STATE = 16 };
+enum ErrBits : uint32_t { ERR_RANGE = 1, ERR_WEIGHT = 2, ERR_CAPACITY = 4, ERR_OVERFLOW = 8, ERR_STATE = 16,
+                        ERR_PARTITION = 32 };
 
 struct GraphCtrl {
   unsigned long long pool_top;    // bump pointer of the growth pool
@@ -51,8 +52,16 @@ struct GraphDev {
   uint32_t* owner;   // source vertex of every slab (the paper's bucket_vertex[])
   uint2* vmeta;      // per vertex {first head slab | INVALID_SLAB, bucket_count}
   GraphCtrl* ctrl;
-  uint32_t V, H, P, seed;
+  uint32_t V, H, P, seed;   // V: vertices held here (vmeta entries); H/P: arena / pool slabs
+  uint32_t Vg;              // global vertex count: the key range
+  uint32_t ws, rank;        // vertex partition: this store holds sources u with u % ws == rank, at u / ws
 };
+
+// Source id -> local row, or INVALID_SLAB if u is not held by this partition.
+__device__ __forceinline__ uint32_t local_row(const GraphDev& G, uint32_t u) {
+  if (G.ws <= 1) return u;
+  return (u % G.ws == G.rank) ? u / G.ws : INVALID_SLAB;
+}
 
 __device__ __forceinline__ uint32_t* slab_ptr(const GraphDev& G, uint32_t s) {
   return G.slabs + (size_t)s * SLAB_WORDS;

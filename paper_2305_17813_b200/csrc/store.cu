@@ -199,9 +199,11 @@ __global__ void __launch_bounds__(UPD_BLOCK) k_insert(GraphDev G, const uint32_t
   uint32_t added = 0, err = 0;
   for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / GROUP; i < n; i += ng) {
     const uint32_t u = src[i], v = dst[i], wt = MAP ? w[i] : 0u;
-    if (u >= G.V || v >= G.V) { err |= ERR_RANGE; continue; }
+    if (u >= G.Vg || v >= G.Vg) { err |= ERR_RANGE; continue; }
     if (MAP && (wt == 0 || wt >= W_LIMIT)) { err |= ERR_WEIGHT; continue; }
-    const int r = group_insert<MAP>(G, u, v, wt, l8, gmask, gbase);
+    const uint32_t ul = local_row(G, u);
+    if (ul == INVALID_SLAB) { err |= ERR_PARTITION; continue; }
+    const int r = group_insert<MAP>(G, ul, v, wt, l8, gmask, gbase);
     if (r < 0) err |= ERR_CAPACITY;
     else if (l8 == 0) added += (uint32_t)r;
   }
@@ -258,9 +260,11 @@ __global__ void __launch_bounds__(UPD_BLOCK) k_delete(GraphDev G, const uint32_t
   uint32_t removed = 0, err = 0;
   for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / GROUP; i < n; i += ng) {
     const uint32_t u = src[i], v = dst[i];
-    if (u >= G.V || v >= G.V) { err |= ERR_RANGE; continue; }
+    if (u >= G.Vg || v >= G.Vg) { err |= ERR_RANGE; continue; }
+    const uint32_t ul = local_row(G, u);
+    if (ul == INVALID_SLAB) { err |= ERR_PARTITION; continue; }
     uint32_t slab; uint64_t val;
-    const int c = group_find<MAP>(G, u, v, l8, gmask, gbase, slab, val);
+    const int c = group_find<MAP>(G, ul, v, l8, gmask, gbase, slab, val);
     if (c < 0 || l8 != 0) continue;
     // TOMBSTONE the cell; a failed CAS means a duplicate in this batch won
     bool ok;
@@ -285,8 +289,10 @@ __global__ void __launch_bounds__(UPD_BLOCK) k_query(GraphDev G, const uint32_t*
     const uint32_t u = src[i], v = dst[i];
     int c = -1;
     uint32_t slab; uint64_t val = 0;
-    if (u >= G.V || v >= G.V) err |= ERR_RANGE;
-    else c = group_find<MAP>(G, u, v, l8, gmask, gbase, slab, val);
+    const uint32_t ul = u < G.Vg ? local_row(G, u) : INVALID_SLAB;
+    if (u >= G.Vg || v >= G.Vg) err |= ERR_RANGE;
+    else if (ul == INVALID_SLAB) err |= ERR_PARTITION;
+    else c = group_find<MAP>(G, ul, v, l8, gmask, gbase, slab, val);
     if (l8 == 0) {
       found[i] = c >= 0;
       if (w_out) w_out[i] = (MAP && c >= 0) ? (uint32_t)(val >> 32) : 0u;
@@ -337,7 +343,7 @@ __global__ void __launch_bounds__(UPD_BLOCK) k_export(GraphDev G, uint64_t n_sla
     for (int k = 0; k < NK; k++) {
       const uint32_t key = F::key(d, k);
       if (own != NO_OWNER && F::valid_cell(l8, k) && key != EMPTY_KEY && key != TOMBSTONE_KEY) {
-        if (o < cap) { os[o] = own; od[o] = key; if (ow) ow[o] = MAP ? F::weight(d, k) : 0u; }
+        if (o < cap) { os[o] = own * G.ws + G.rank; od[o] = key; if (ow) ow[o] = MAP ? F::weight(d, k) : 0u; }
         o++;
       }
     }
@@ -399,7 +405,7 @@ static inline unsigned grid_for(meerkat_graph* g, uint64_t groups) {
 }
 
 cudaError_t launch_build(meerkat_graph* g, Store& st, const uint32_t* d_hints, uint64_t pool_request) {
-  const uint32_t V = g->V;
+  const uint32_t V = g->Vl;   // vertices held by this partition (all of them when world_size == 1)
   const int cap = g->weighted ? MAP_CAP : SET_CAP;
   uint32_t* count = nullptr;
   uint64_t *heads = nullptr, *first = nullptr;
@@ -442,6 +448,7 @@ cudaError_t launch_build(meerkat_graph* g, Store& st, const uint32_t* d_hints, u
     memset(st.hctrl, 0, sizeof(GraphCtrl));
     st.bytes = nslab * 132 + (size_t)V * 8 + sizeof(GraphCtrl);
     st.dev.V = V; st.dev.H = (uint32_t)st.H; st.dev.P = (uint32_t)st.P;
+    st.dev.Vg = g->V; st.dev.ws = g->ws; st.dev.rank = g->rank;
     if (st.H) {
       const unsigned gf = (unsigned)std::min<uint64_t>((st.H * 8 + 255) / 256, (uint64_t)g->sm_count * 16);
       k_fill<<<gf, 256, 0, g->stream>>>(st.dev.slabs, st.H, g->weighted ? 1 : 0);

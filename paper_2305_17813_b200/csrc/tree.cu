@@ -28,95 +28,10 @@
 //  * rounds are separated by grid-wide barriers inside one launch.
 #include <cooperative_groups.h>
 
-#include "graph.h"
+#include "tree_common.cuh"
 
-namespace cg = cooperative_groups;
 
 namespace mk {
-
-constexpr int TREE_BLOCK = 512;
-constexpr int FILTER_WORDS = 24576;   // 96 KiB smem Bloom filter per block (decremental scan), 2 blocks/SM
-constexpr int SCAN_UNROLL = 4;        // independent slabs in flight per group in the scan
-constexpr unsigned FULL = 0xFFFFFFFFu;
-
-enum Visit { RELAX = 0, PROPAGATE = 1, PULL = 2 };
-
-struct TreeArgs {
-  GraphDev G;           // out-edge store
-  GraphDev R;           // in-edge mirror (R.slabs == nullptr when the graph keeps none)
-  TreeDev T;
-  const uint32_t* bs;   // batch (device)
-  const uint32_t* bd;
-  const uint32_t* bw;
-  uint64_t bn;
-  uint32_t unit;        // 1: BFS (w = 1)
-  uint32_t weighted;    // graph has weights (map store)
-  uint32_t filter_words;
-};
-
-struct Counters {
-  uint32_t items = 0, slabs = 0, visited = 0, improved = 0, scan_slabs = 0, hits = 0, batch = 0, err = 0;
-};
-
-__device__ __forceinline__ bool bit_test(const uint32_t* bits, uint32_t x) {
-  return (__ldcg(bits + (x >> 5)) >> (x & 31)) & 1u;
-}
-
-// warpenqueuefrontier: all 32 lanes call; lanes with `has` append
-// every (bucket, x) item of vertex x.  One atomicAdd per warp.
-__device__ __forceinline__ void warp_enqueue(const GraphDev& G, const TreeDev& T, uint64_t* fr,
-                                             unsigned long long* sz, bool has, uint32_t x, Counters& c) {
-  if (!__ballot_sync(FULL, has)) return;
-  const int lane = lane_id();
-  uint32_t cnt = 0;
-  if (has) {
-    const uint2 m = __ldcg(G.vmeta + x);
-    cnt = m.x == INVALID_SLAB ? 0u : m.y;   // a vertex without a head slab has no out-edges
-  }
-  uint32_t incl = cnt;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(FULL, incl, o);
-    if (lane >= o) incl += y;
-  }
-  const uint32_t total = __shfl_sync(FULL, incl, 31);
-  if (!total) return;
-  unsigned long long base = 0;
-  if (lane == 31) base = atomicAdd(sz, (unsigned long long)total);
-  base = __shfl_sync(FULL, base, 31);
-  if (base + total > T.fr_cap) { c.err |= ERR_CAPACITY; return; }
-  const uint64_t off = base + incl - cnt;
-  if (cnt <= 8) {
-    for (uint32_t j = 0; j < cnt; j++) fr[off + j] = ((uint64_t)j << 32) | x;
-  }
-  uint32_t big = __ballot_sync(FULL, cnt > 8);
-  while (big) {
-    const int l = __ffs(big) - 1;
-    big &= big - 1;
-    const uint32_t xb = __shfl_sync(FULL, x, l);
-    const uint64_t ob = __shfl_sync(FULL, off, l);
-    const uint32_t cb = __shfl_sync(FULL, cnt, l);
-    for (uint32_t j = lane; j < cb; j += 32) fr[ob + j] = ((uint64_t)j << 32) | xb;
-  }
-}
-
-__device__ __forceinline__ void mark_invalid(const TreeDev& T, uint32_t x) {
-  atomicOr(T.inval_bits + (x >> 5), 1u << (x & 31));
-  const unsigned long long i = atomicAdd(&T.ctrl->inval_n, 1ull);
-  T.inval_list[i] = x;
-}
-
-// Relax candidate <dist, parent> into node[x]; true iff x must be (re-)expanded next round.
-__device__ __forceinline__ bool relax(const TreeDev& T, uint32_t x, uint64_t dist, uint32_t parent,
-                                      uint32_t epoch_next, Counters& c) {
-  if (dist >= INF_DIST) { c.err |= ERR_OVERFLOW; return false; }   // C5
-  const uint64_t cand = (dist << 32) | parent;
-  if (cand >= ld_cg_u64(T.node + x)) return false;                   // filter: node[] only decreases
-  const unsigned long long old = atomicMin(reinterpret_cast<unsigned long long*>(T.node + x), cand);
-  if (cand >= old) return false;
-  c.improved++;
-  return atomicExch(T.stamp + x, epoch_next) != epoch_next;
-}
 
 // Next live item of this group (grid-stride over [it, n)): sets v / slab / du.
 template <int VISIT>
@@ -219,26 +134,6 @@ __device__ __forceinline__ uint32_t run_rounds(const TreeArgs& A, uint32_t epoch
   return r;
 }
 
-__device__ void flush_counters(const TreeArgs& A, Counters& c, bool rounds_owner, uint32_t relax_rounds,
-                               uint32_t prop_rounds) {
-  TreeCtrl* tc = A.T.ctrl;
-  auto red = [](uint32_t v) { return __reduce_add_sync(FULL, v); };
-  const uint32_t items = red(c.items), slabs = red(c.slabs), visited = red(c.visited), imp = red(c.improved),
-                 ss = red(c.scan_slabs), hits = red(c.hits), batch = red(c.batch);
-  const uint32_t err = __reduce_or_sync(FULL, c.err);
-  if (lane_id() == 0) {
-    if (items) atomicAdd(&tc->items, (unsigned long long)items);
-    if (slabs) atomicAdd(&tc->slabs_read, (unsigned long long)slabs);
-    if (visited) atomicAdd(&tc->visited, (unsigned long long)visited);
-    if (imp) atomicAdd(&tc->improved, (unsigned long long)imp);
-    if (ss) atomicAdd(&tc->scan_slabs, (unsigned long long)ss);
-    if (hits) atomicAdd(&tc->scan_hits, (unsigned long long)hits);
-    if (batch) atomicAdd(&tc->batch_edges, (unsigned long long)batch);
-    if (err) atomicOr(&A.G.ctrl->err, err);
-  }
-  if (rounds_owner) { tc->rounds = relax_rounds; tc->prop_rounds = prop_rounds; }
-}
-
 // ------------------------------------------------------------------ static
 
 template <bool MAP>
@@ -258,7 +153,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_static(const __grid_cons
   grid.sync();
   const uint32_t r = run_rounds<MAP, RELAX>(A, epoch, grid, 0, c);
   if (tid == 0) *A.T.epoch_ptr = epoch + r + 2;   // every thread read the base before the first grid.sync
-  flush_counters(A, c, tid == 0, r, 0);
+  flush_counters(A.G, A.T, c, tid == 0, r, 0);
 }
 
 // ------------------------------------------------------------------ incremental
@@ -290,20 +185,10 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_inc(const __grid_constan
   grid.sync();
   const uint32_t r = run_rounds<MAP, RELAX>(A, epoch, grid, 0, c);
   if (tid == 0) *A.T.epoch_ptr = epoch + r + 2;
-  flush_counters(A, c, tid == 0, r, 0);
+  flush_counters(A.G, A.T, c, tid == 0, r, 0);
 }
 
 // ------------------------------------------------------------------ decremental
-
-// Blocked two-bit Bloom filter of V_invalid in shared memory: one word per key,
-// two bits within it (false-positive rate ~ load^2).  Exact membership is the
-// global bit set; the filter only keeps non-members off the slow path.
-__device__ __forceinline__ void filter_loc(uint32_t x, uint32_t fwords, uint32_t& w, uint32_t& m) {
-  uint32_t h = x * 0x9E3779B1u;
-  h ^= h >> 15;
-  w = __umulhi(h * 0x85EBCA6Bu, fwords);
-  m = (1u << (h & 31)) | (1u << ((h >> 5) & 31));
-}
 
 // Valid->invalid frontier (C15) as a STREAM over the slab array
 // [0, n_slabs): each 8-lane group reads whole slabs (LDG.128 per lane, U slabs in
@@ -450,7 +335,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_dec(const __grid_constan
     atomicAnd(A.T.inval_bits + (x >> 5), ~(1u << (x & 31)));
   }
   if (tid == 0) *A.T.epoch_ptr = epoch + r2 + 2;
-  flush_counters(A, c, tid == 0, r2 - r1, r1);
+  flush_counters(A.G, A.T, c, tid == 0, r2 - r1, r1);
 }
 
 // ------------------------------------------------------------------ host side

@@ -51,20 +51,22 @@ class Graph:
 
     def __init__(self, vertex_n: int, weighted: bool = True, hashing: bool = True, load_factor: float = 0.7,
                  degree_hints=None, pool_slabs: int = 0, hash_seed: int = 0, device: int = 0, stream=None,
-                 reverse: bool = False, in_degree_hints=None):
+                 reverse: bool = False, in_degree_hints=None, world_size: int = 1, rank: int = 0):
         L = _lib.lib()
         hp, self._hints_keep, _ = _u32(degree_hints)
         ip, self._ihints_keep, _ = _u32(in_degree_hints)
         cfg = _lib.Config(vertex_n=vertex_n, weighted=int(weighted), hashing=int(hashing),
                           load_factor=float(load_factor), degree_hints=hp, pool_slabs=int(pool_slabs),
                           hash_seed=int(hash_seed), device=int(device), stream=_stream_ptr(stream),
-                          reverse=int(reverse), in_degree_hints=ip)
+                          reverse=int(reverse), in_degree_hints=ip, world_size=int(world_size), rank=int(rank))
         h = ctypes.c_void_p()
         check(L.meerkat_create(ctypes.byref(cfg), ctypes.byref(h)), "meerkat_create")
         self._h = h
         self.vertex_n = int(vertex_n)
         self.weighted = bool(weighted)
         self.reverse = bool(reverse)
+        self.world_size = int(world_size)
+        self.rank = int(rank)
         self.device = int(device)
         self._trees = []
 

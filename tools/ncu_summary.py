@@ -57,18 +57,22 @@ def rep(path, top=25):
 
 
 def launches(path):
-    rows = [r for r in csv.reader(open(path)) if len(r) > 10 and r[0] != "ID"]
+    lines = [l for l in open(path) if l.startswith('"')]
+    rows = list(csv.reader(lines))
+    hdr = rows[0]
+    ki, mi, ui, vi = (hdr.index(k) for k in ("Kernel Name", "Metric Name", "Metric Unit", "Metric Value"))
     agg = defaultdict(lambda: [0, 0.0])
-    for r in rows:
-        if r[12] != "gpu__time_duration.sum":
+    for r in rows[1:]:
+        if r[mi] != "gpu__time_duration.sum":
             continue
-        name = r[4].split("(")[0]
+        name = r[ki].split("(")[0]
+        scale = {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}.get(r[ui], 1e-3)
         agg[name][0] += 1
-        agg[name][1] += float(r[14]) * (1e-3 if r[13] == "ns" else (1.0 if r[13] == "us" else 1e3))
+        agg[name][1] += float(r[vi].replace(",", "")) * scale
     tot = sum(v[1] for v in agg.values()) or 1
-    print(f"{'kernel':60s} {'launches':>8s} {'total us':>12s} {'share':>7s}")
+    print(f"{'kernel':60s} {'launches':>8s} {'total us':>12s} {'mean us':>10s} {'share':>7s}")
     for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1]):
-        print(f"{k[:60]:60s} {v[0]:8d} {v[1]:12.1f} {100 * v[1] / tot:6.1f}%")
+        print(f"{k[:60]:60s} {v[0]:8d} {v[1]:12.1f} {v[1] / v[0]:10.1f} {100 * v[1] / tot:6.1f}%")
 
 
 if __name__ == "__main__":
