@@ -60,6 +60,8 @@ def parse():
     p.add_argument("--cpu-scale", type=int, default=20, help="R-MAT scale of the oracle's bounded sample")
     p.add_argument("--cpu-steps", type=int, default=2)
     p.add_argument("--json-out", default=None)
+    p.add_argument("--partitioned", action="store_true",
+                   help="use the vertex-partitioned multi-GPU path even at --gpus 1 (NCCL, world size 1)")
     return p.parse_args()
 
 
@@ -69,11 +71,17 @@ def dist_init(args):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if ws > 1:
+    if ws > 1 or (args.partitioned and args.impl == "ours"):
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if not dist.is_initialized():
+            if ws == 1:
+                os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+                os.environ.setdefault("MASTER_PORT", "29533")
+                os.environ.setdefault("RANK", "0")
+                os.environ.setdefault("WORLD_SIZE", "1")
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return ws, rank, local
 
 
@@ -451,15 +459,88 @@ def run_ours(args, ws, rank, local):
                 json.dump(line, f, indent=1)
 
 
+def run_dist(args, ws, rank, local):
+    """Vertex-partitioned path: the SAME config-3 graph split over `ws` GPUs by
+    owner(v) = v mod ws; every rank brings 1/ws of each batch; one all-to-all routes it; tree updates
+    exchange <x, candidate> messages once per round (NCCL all-to-all) -> strong scaling."""
+    import torch
+    from paper_2305_17813_b200.dist import DistGraph
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    K, Wm = args.steps, args.warmup
+    W, gen_s = make_workload(args, K + Wm, 0)
+    V = W.vertex_n
+    stream = torch.cuda.current_stream(dev)
+    sl = lambda a: np.ascontiguousarray(a[rank::ws])
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.uint32).view(np.int32)).to(dev)
+    bs, bd, bw = W.base
+    g = DistGraph(V, hashing=not args.no_hashing, load_factor=args.lf,
+                  degree_hints=np.bincount(bs, minlength=V).astype(np.uint32), device=dev)
+    barrier(ws)
+    t0 = time.time()
+    n_base = g.insert(T(sl(bs)), T(sl(bd)), T(sl(bw)))
+    sp, bf = g.sssp(W.source), g.bfs(W.source)
+    build_s = time.time() - t0
+    ins = [tuple(T(sl(x)) for x in b) for b in W.inserts]
+    dels = [tuple(T(sl(x)) for x in b[:2]) for b in W.deletes]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for i in range(Wm):
+        one_step(g, sp, bf, ins[i], dels[i], [torch.cuda.Event(enable_timing=True) for _ in range(7)], stream)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    per_call = {n: [] for n in NAMES}
+    total_ms = 0.0
+    for k in range(K):
+        flush.zero_()
+        torch.cuda.synchronize()
+        barrier(ws)
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
+        one_step(g, sp, bf, ins[Wm + k], dels[Wm + k], evs, stream)
+        evs[6].synchronize()
+        step_ms = allreduce_max(evs[0].elapsed_time(evs[6]), ws)
+        total_ms += step_ms
+        for j, n in enumerate(NAMES):
+            per_call[n].append(allreduce_max(evs[j].elapsed_time(evs[j + 1]), ws))
+    clk = clocks.stop()
+    mean = {n: float(np.mean(v)) for n, v in per_call.items()}
+    edges = 2 * args.batch * K
+    line = {
+        "metric": METRIC, "value": edges / (total_ms / 1e3), "unit": "edges/s", "n_gpus": ws, "steps": K,
+        "warmup": Wm, "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": f"rmat-s{args.scale}-ef{args.ef} dynamic SSSP+BFS, {args.batch}-edge insert+delete "
+                               f"batches (BASELINE config 3)", "vertices": V, "edges": int(n_base),
+                   "batch": args.batch, "source": W.source, "hashing": not args.no_hashing,
+                   "load_factor": args.lf, "decremental_frontier": "scan (per partition)",
+                   "parallelism": f"vertex-partitioned over {ws} GPUs (owner = v mod {ws}), NCCL all-to-all per round",
+                   "l2": "flushed before every timed step; store > L2"},
+        "update_edges_per_s": 2 * args.batch / ((mean["insert"] + mean["delete"]) / 1e3),
+        "sssp_ms_per_batch": {"incremental": mean["sssp_inc"], "decremental": mean["sssp_dec"]},
+        "bfs_ms_per_batch": {"incremental": mean["bfs_inc"], "decremental": mean["bfs_dec"]},
+        "per_call_ms": mean, "build_s": build_s, "roofline": None, "cpu_baseline": None,
+        "e2e": None, "gpu_launches": None, "clocks": clk, "generate_s": gen_s,
+        "note": "host-driven rounds (one NCCL all-to-all + all-reduce per frontier round); timings are max over ranks",
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
+    ws_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws_env > 1:   # N generator processes on one host: split the cores
+        os.environ.setdefault("OMP_NUM_THREADS", str(max(1, (os.cpu_count() or 8) // ws_env)))
     ws, rank, local = dist_init(args)
     if args.impl == "reference":
         run_reference(args, ws, rank)
+    elif ws > 1 or args.partitioned:
+        run_dist(args, ws, rank, local)
     else:
         run_ours(args, ws, rank, local)
-    if ws > 1:
-        import torch.distributed as dist
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
         dist.destroy_process_group()
 
 

@@ -319,7 +319,7 @@ static meerkat_status tree_create(meerkat_graph* g, uint32_t source, bool unit, 
   *out = nullptr;
   if (source >= g->V) return MEERKAT_E_VERTEX_RANGE;
   if (!unit && !g->weighted) return MEERKAT_E_STATE;   // SSSP needs weights
-  if (dist != (g->ws > 1)) return MEERKAT_E_INVALID_ARG;  // partitioned graphs use the meerkat_dtree_* calls
+  if (!dist && g->ws > 1) return MEERKAT_E_INVALID_ARG;  // partitioned graphs use the meerkat_dtree_* calls
   DeviceGuard dg(g->device);
   meerkat_tree* t = new (std::nothrow) meerkat_tree();
   if (!t) return MEERKAT_E_CUDA;
