@@ -2,6 +2,7 @@
 // staging, stream ordering, version checks and status translation around the
 // launchers in store.cu and tree.cu.  No compute happens here.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -150,6 +151,7 @@ meerkat_status meerkat_create(const meerkat_config* cfg, meerkat_graph** out) {
     if (e == cudaSuccess) e = launch_build(g, g->in, static_cast<const uint32_t*>(hints), cfg->pool_slabs);
   }
   if (e == cudaSuccess) e = tree_occupancy(g);
+  if (const char* s = std::getenv("MEERKAT_LATENCY_BLOCKS_PER_SM")) g->latency_bps = std::atoi(s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
   if (e != cudaSuccess) {
     cudaGetLastError();

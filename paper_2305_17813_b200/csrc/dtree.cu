@@ -160,10 +160,8 @@ __global__ void __launch_bounds__(D_BLOCK) k_dexpand(DArgs A) {
     for (; it < A.n; it += ng) {
       const uint64_t item = A.fr[it];
       v = (uint32_t)item;
-      const uint32_t head = __ldcg(reinterpret_cast<const unsigned int*>(&G.vmeta[v].x));
       if (l8 == 0) c.items++;
-      if (head == INVALID_SLAB) continue;
-      slab = head + (uint32_t)(item >> 32);
+      slab = (uint32_t)(item >> 32);
       if (VISIT == PROPAGATE) return true;
       const uint64_t nv = ld_cg_u64(T.node + v);
       if (nv != UNREACHED) { du = (uint32_t)(nv >> 32); return true; }

@@ -28,32 +28,27 @@
 //  * rounds are separated by grid-wide barriers inside one launch.
 #include <cooperative_groups.h>
 
+#include <algorithm>
+
 #include "tree_common.cuh"
 
 
 namespace mk {
 
-// Next live item of this group (grid-stride over [it, n)): sets v / slab / du.
-template <int VISIT>
-__device__ __forceinline__ bool fetch_item(const TreeArgs& A, const GraphDev& S, const uint64_t* fr, uint64_t n,
-                                           uint64_t ng, uint64_t& it, uint32_t& v, uint32_t& slab, uint32_t& du,
+// Next item of this group (grid-stride over [it, n)): vertex and slab come from the item.
+__device__ __forceinline__ bool fetch_item(const uint64_t* fr, uint64_t n, uint64_t& it, uint32_t& v, uint32_t& slab,
                                            int l8, Counters& c) {
-  for (; it < n; it += ng) {
-    const uint64_t item = fr[it];
-    v = (uint32_t)item;
-    const uint32_t head = __ldcg(reinterpret_cast<const unsigned int*>(&S.vmeta[v].x));
-    if (l8 == 0) c.items++;
-    if (head == INVALID_SLAB) continue;
-    slab = head + (uint32_t)(item >> 32);
-    if (VISIT != RELAX) return true;
-    const uint64_t nv = ld_cg_u64(A.T.node + v);
-    if (nv != UNREACHED) { du = (uint32_t)(nv >> 32); return true; }
-  }
-  return false;
+  if (it >= n) return false;
+  const uint64_t item = fr[it];
+  v = (uint32_t)item;
+  slab = (uint32_t)(item >> 32);
+  if (l8 == 0) c.items++;
+  return true;
 }
 
 // Expand the frontier items [0, n) of `fr` (one 8-lane group per item), applying
-// VISIT to every live edge; successful vertices go to `fnext`.
+// VISIT to every live edge; successful vertices go to `fnext`.  The first slab of
+// an item and d(v) are loaded together (independent requests).
 template <bool MAP, int VISIT>
 __device__ __forceinline__ void expand(const TreeArgs& A, const uint64_t* fr, uint64_t n, uint64_t* fnext,
                                        unsigned long long* sznext, uint32_t epoch_next, Counters& c) {
@@ -64,25 +59,36 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const uint64_t* fr, ui
   const TreeDev& T = A.T;
   const int lane = lane_id(), l8 = lane & 7;
   const uint64_t ng = ((uint64_t)gridDim.x * blockDim.x) / GROUP;
+  const bool probe = n > PROBE_MIN_ITEMS;
   uint64_t it = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / GROUP;
   uint32_t v = 0, slab = 0, du = 0;
-  bool active = fetch_item<VISIT>(A, S, fr, n, ng, it, v, slab, du, l8, c);
+  bool active = fetch_item(fr, n, it, v, slab, l8, c);
+  bool fresh = active;
   while (__any_sync(FULL, active)) {
     uint4 d = make_uint4(EMPTY_KEY, EMPTY_KEY, EMPTY_KEY, INVALID_SLAB);
+    uint64_t nv = 0;
     if (active) {
       d = ld_slab_ro(slab_ptr(S, slab), l8);
+      if (VISIT == RELAX && fresh) nv = ld_cg_u64(T.node + v);
       if (l8 == 0) c.slabs++;
     }
+    bool dead = false;
+    if (VISIT == RELAX && active && fresh) {
+      dead = nv == UNREACHED;
+      du = (uint32_t)(nv >> 32);
+    }
+    fresh = false;
+    const bool use = active && !dead;
 #pragma unroll
     for (int k = 0; k < NK; k++) {
       const uint32_t x = F::key(d, k);
-      const bool live = active && F::valid_cell(l8, k) && x != EMPTY_KEY && x != TOMBSTONE_KEY;
+      const bool live = use && F::valid_cell(l8, k) && x != EMPTY_KEY && x != TOMBSTONE_KEY;
       bool enq = false;
       if (live) {
         c.visited++;
         if (VISIT == RELAX) {
           const uint32_t w = A.unit ? 1u : F::weight(d, k);
-          enq = relax(T, x, (uint64_t)du + w, v, epoch_next, c);
+          enq = relax(T, x, (uint64_t)du + w, v, epoch_next, c, probe);
         } else if (VISIT == PULL) {
           // in-edge (x -> v) of invalid v: a valid->invalid frontier edge iff x is valid and reached
           // (C15); relax v from it
@@ -91,7 +97,7 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const uint64_t* fr, ui
             if (nx != UNREACHED) {
               c.hits++;
               const uint32_t w = A.unit ? 1u : F::weight(d, k);
-              enq = relax(T, v, (nx >> 32) + w, x, epoch_next, c);
+              enq = relax(T, v, (nx >> 32) + w, x, epoch_next, c, false);
             }
           }
         } else {
@@ -110,8 +116,8 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const uint64_t* fr, ui
     }
     const uint32_t nxt = __shfl_sync(FULL, d.w, (lane & 24) + GROUP - 1);
     if (active) {
-      if (nxt != INVALID_SLAB) slab = nxt;
-      else { it += ng; active = fetch_item<VISIT>(A, S, fr, n, ng, it, v, slab, du, l8, c); }
+      if (nxt != INVALID_SLAB && !dead) slab = nxt;
+      else { it += ng; active = fetch_item(fr, n, it, v, slab, l8, c); fresh = active; }
     }
   }
 }
@@ -177,7 +183,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_inc(const __grid_constan
       const bool ok = u < A.G.V && v < A.G.V && (A.unit || (w != 0 && w < W_LIMIT));   // skipped at insert too
       if (ok) {
         const uint64_t nu = ld_cg_u64(A.T.node + u);
-        if (nu != UNREACHED) enq = relax(A.T, v, (nu >> 32) + w, u, epoch, c);
+        if (nu != UNREACHED) enq = relax(A.T, v, (nu >> 32) + w, u, epoch, c, false);
       }
     }
     warp_enqueue(A.G, A.T, A.T.fr[0], &A.T.ctrl->size[0], enq, v, c);
@@ -376,8 +382,11 @@ cudaError_t launch_tree(meerkat_graph* g, meerkat_tree* t, int mode, const uint3
   A.filter_words = FILTER_WORDS;
   cudaError_t e = cudaMemsetAsync(t->dev.ctrl, 0, sizeof(TreeCtrl), g->stream);
   if (e != cudaSuccess) return e;
-  const int bps = g->tree_blocks_per_sm[mode];
+  int bps = g->tree_blocks_per_sm[mode];
   if (bps <= 0) return cudaErrorInvalidConfiguration;
+  // latency-bound calls (no full-store scan) may run on fewer blocks: cheaper grid barriers
+  if (g->latency_bps > 0 && mode != MODE_STATIC && !(mode == MODE_DECREMENTAL && !g->reverse))
+    bps = std::min(bps, g->latency_bps);
   dim3 grid((unsigned)(bps * g->sm_count)), block(TREE_BLOCK);
   void* args[] = {&A};
   const size_t smem = mode == MODE_DECREMENTAL ? (size_t)FILTER_WORDS * 4 : 0;

@@ -13,6 +13,7 @@ constexpr int TREE_BLOCK = 512;
 constexpr int FILTER_WORDS = 24576;   // 96 KiB smem Bloom filter per block (decremental scan), 2 blocks/SM
 constexpr int SCAN_UNROLL = 4;        // independent slabs in flight per group in the scan
 constexpr unsigned FULL = 0xFFFFFFFFu;
+constexpr uint64_t PROBE_MIN_ITEMS = 65536;   // frontiers at least this large probe node[x] before the atomic
 
 enum Visit { RELAX = 0, PROPAGATE = 1, PULL = 2 };
 
@@ -38,14 +39,15 @@ __device__ __forceinline__ bool bit_test(const uint32_t* bits, uint32_t x) {
 }
 
 // warpenqueuefrontier: all 32 lanes call; lanes with `has` append
-// every (bucket, x) item of vertex x.  One atomicAdd per warp.
+// one item per slab list (bucket) of vertex x.  One atomicAdd per warp.
 __device__ __forceinline__ void warp_enqueue(const GraphDev& G, const TreeDev& T, uint64_t* fr,
                                              unsigned long long* sz, bool has, uint32_t x, Counters& c) {
   if (!__ballot_sync(FULL, has)) return;
   const int lane = lane_id();
-  uint32_t cnt = 0;
+  uint32_t cnt = 0, head = 0;
   if (has) {
     const uint2 m = __ldcg(G.vmeta + x);
+    head = m.x;
     cnt = m.x == INVALID_SLAB ? 0u : m.y;   // a vertex without a head slab has no out-edges
   }
   uint32_t incl = cnt;
@@ -61,17 +63,19 @@ __device__ __forceinline__ void warp_enqueue(const GraphDev& G, const TreeDev& T
   base = __shfl_sync(FULL, base, 31);
   if (base + total > T.fr_cap) { c.err |= ERR_CAPACITY; return; }
   const uint64_t off = base + incl - cnt;
+  // item = (head slab of the bucket << 32) | vertex: the expander needs no vmeta lookup
   if (cnt <= 8) {
-    for (uint32_t j = 0; j < cnt; j++) fr[off + j] = ((uint64_t)j << 32) | x;
+    for (uint32_t j = 0; j < cnt; j++) fr[off + j] = ((uint64_t)(head + j) << 32) | x;
   }
   uint32_t big = __ballot_sync(FULL, cnt > 8);
   while (big) {
     const int l = __ffs(big) - 1;
     big &= big - 1;
     const uint32_t xb = __shfl_sync(FULL, x, l);
+    const uint32_t hb = __shfl_sync(FULL, head, l);
     const uint64_t ob = __shfl_sync(FULL, off, l);
     const uint32_t cb = __shfl_sync(FULL, cnt, l);
-    for (uint32_t j = lane; j < cb; j += 32) fr[ob + j] = ((uint64_t)j << 32) | xb;
+    for (uint32_t j = lane; j < cb; j += 32) fr[ob + j] = ((uint64_t)(hb + j) << 32) | xb;
   }
 }
 
@@ -82,11 +86,14 @@ __device__ __forceinline__ void mark_invalid(const TreeDev& T, uint32_t x) {
 }
 
 // Relax candidate <dist, parent> into node[x]; true iff x must be (re-)expanded next round.
+// probe: read node[x] first and skip the atomic when it cannot win (node values only
+// decrease, so a stale read can only cost a spare atomic) — saves atomics on large
+// frontiers, costs one round trip on small ones.
 __device__ __forceinline__ bool relax(const TreeDev& T, uint32_t x, uint64_t dist, uint32_t parent,
-                                      uint32_t epoch_next, Counters& c) {
+                                      uint32_t epoch_next, Counters& c, bool probe = true) {
   if (dist >= INF_DIST) { c.err |= ERR_OVERFLOW; return false; }   // C5
   const uint64_t cand = (dist << 32) | parent;
-  if (cand >= ld_cg_u64(T.node + x)) return false;                   // filter: node[] only decreases
+  if (probe && cand >= ld_cg_u64(T.node + x)) return false;
   const unsigned long long old = atomicMin(reinterpret_cast<unsigned long long*>(T.node + x), cand);
   if (cand >= old) return false;
   c.improved++;

@@ -151,15 +151,15 @@ class DistGraph:
         rows = recv.view(-1, cols)
         return [rows[:, i].contiguous() for i in range(cols)], rcounts, list(counts)
 
-    def insert(self, src, dst, w=None) -> int:
+    def insert(self, src, dst, w=None, count: bool = True):
         (cols, _, _) = self.route(src, dst, w)
-        n = self.g.insert(cols[0], cols[1], cols[2] if w is not None else None)
-        return self.tp.allreduce_sum(n)
+        n = self.g.insert(cols[0], cols[1], cols[2] if w is not None else None, count=count)
+        return self.tp.allreduce_sum(n) if count else None
 
-    def delete(self, src, dst) -> int:
+    def delete(self, src, dst, count: bool = True):
         (cols, _, _) = self.route(src, dst)
-        n = self.g.delete(cols[0], cols[1])
-        return self.tp.allreduce_sum(n)
+        n = self.g.delete(cols[0], cols[1], count=count)
+        return self.tp.allreduce_sum(n) if count else None
 
     def query(self, src, dst):
         """found / weight per queried edge, in this rank's input order."""
