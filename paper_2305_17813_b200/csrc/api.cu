@@ -490,6 +490,19 @@ meerkat_status meerkat_tree_stats_get(meerkat_tree* t, meerkat_tree_stats* out) 
   return MEERKAT_OK;
 }
 
+meerkat_status meerkat_tree_timeline(meerkat_tree* t, uint64_t* out, uint64_t capacity, uint64_t* n_out) {
+  if (!t || !n_out || (capacity && !out)) return MEERKAT_E_INVALID_ARG;
+  meerkat_graph* g = t->g;
+  DeviceGuard dg(g->device);
+  cudaError_t e = cudaMemcpyAsync(t->hctrl, t->dev.ctrl, sizeof(TreeCtrl), cudaMemcpyDeviceToHost, g->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  const uint64_t n = std::min<uint64_t>(t->hctrl->nts, 48);
+  *n_out = n;
+  for (uint64_t i = 0; i < n && i < capacity; i++) out[i] = t->hctrl->tstamp[i];
+  return MEERKAT_OK;
+}
+
 meerkat_status meerkat_tree_destroy(meerkat_tree* t) {
   if (!t) return MEERKAT_E_INVALID_ARG;
   DeviceGuard dg(t->g->device);

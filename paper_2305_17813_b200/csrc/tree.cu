@@ -135,6 +135,7 @@ __device__ __forceinline__ uint32_t run_rounds(const TreeArgs& A, uint32_t epoch
     if (blockIdx.x == 0 && threadIdx.x == 0) tc->size[(r + 2) % 3] = 0;
     expand<MAP, VISIT>(A, A.T.fr[r & 1], n, A.T.fr[(r + 1) & 1], &tc->size[(r + 1) % 3], epoch + r + 1, c);
     grid.sync();
+    timeline(A.T.ctrl);
     r++;
   }
   return r;
@@ -145,18 +146,21 @@ __device__ __forceinline__ uint32_t run_rounds(const TreeArgs& A, uint32_t epoch
 template <bool MAP>
 __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_static(const __grid_constant__ TreeArgs A) {
   const uint32_t epoch = __ldcg(A.T.epoch_ptr);
+  timeline(A.T.ctrl);
   cg::grid_group grid = cg::this_grid();
   Counters c;
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
   // init: every node <INF, INVALID>, SRC <0, SRC>
   for (uint64_t v = tid; v < A.G.V; v += nt) A.T.node[v] = (v == A.T.source) ? (uint64_t)A.T.source : UNREACHED;
   grid.sync();
+    timeline(A.T.ctrl);
   if (blockIdx.x == 0 && threadIdx.x < 32) {
     const bool has = threadIdx.x == 0;
     if (has) A.T.stamp[A.T.source] = epoch;
     warp_enqueue(A.G, A.T, A.T.fr[0], &A.T.ctrl->size[0], has, A.T.source, c);   // frontier from SRC (C16)
   }
   grid.sync();
+    timeline(A.T.ctrl);
   const uint32_t r = run_rounds<MAP, RELAX>(A, epoch, grid, 0, c);
   if (tid == 0) *A.T.epoch_ptr = epoch + r + 2;   // every thread read the base before the first grid.sync
   flush_counters(A.G, A.T, c, tid == 0, r, 0);
@@ -167,6 +171,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_static(const __grid_cons
 template <bool MAP>
 __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_inc(const __grid_constant__ TreeArgs A) {
   const uint32_t epoch = __ldcg(A.T.epoch_ptr);
+  timeline(A.T.ctrl);
   cg::grid_group grid = cg::this_grid();
   Counters c;
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
@@ -189,6 +194,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_inc(const __grid_constan
     warp_enqueue(A.G, A.T, A.T.fr[0], &A.T.ctrl->size[0], enq, v, c);
   }
   grid.sync();
+    timeline(A.T.ctrl);
   const uint32_t r = run_rounds<MAP, RELAX>(A, epoch, grid, 0, c);
   if (tid == 0) *A.T.epoch_ptr = epoch + r + 2;
   flush_counters(A.G, A.T, c, tid == 0, r, 0);
@@ -272,6 +278,7 @@ template <bool MAP>
 __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_dec(const __grid_constant__ TreeArgs A) {
   extern __shared__ uint32_t filt[];
   const uint32_t epoch = __ldcg(A.T.epoch_ptr);
+  timeline(A.T.ctrl);
   cg::grid_group grid = cg::this_grid();
   Counters c;
   TreeCtrl* tc = A.T.ctrl;
@@ -300,6 +307,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_dec(const __grid_constan
     warp_enqueue(A.G, A.T, A.T.fr[0], &tc->size[0], enq, v, c);
   }
   grid.sync();
+    timeline(A.T.ctrl);
   // (ii) PropagateInvalidation to all of T_v
   const uint32_t r1 = run_rounds<MAP, PROPAGATE>(A, epoch, grid, 0, c);
   // (iii) valid -> invalid frontier, fused with the first relaxation
@@ -314,6 +322,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_dec(const __grid_constan
       warp_enqueue(A.R, A.T, pull, &tc->pull_n, has, has ? __ldcg(A.T.inval_list + i) : 0u, c);
     }
     grid.sync();
+    timeline(A.T.ctrl);
     expand<MAP, PULL>(A, pull, __ldcg(&tc->pull_n), A.T.fr[r1 & 1], &tc->size[r1 % 3], epoch + r1, c);
   } else if (n_inv) {
     // filter only while sparse enough: two bits per member, bit load <= 1/4 (false positives <= ~6%)
@@ -333,6 +342,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_dec(const __grid_constan
     dec_scan<MAP>(A, filt, fw, n_slabs, A.T.fr[r1 & 1], &tc->size[r1 % 3], epoch + r1, c);
   }
   grid.sync();
+    timeline(A.T.ctrl);
   // (iv) common epilogue
   const uint32_t r2 = run_rounds<MAP, RELAX>(A, epoch, grid, r1, c);
   // clear the invalid bit set for the next call (the list is kept for meerkat_tree_invalidated)

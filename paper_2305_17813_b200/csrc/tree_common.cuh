@@ -38,6 +38,16 @@ __device__ __forceinline__ bool bit_test(const uint32_t* bits, uint32_t x) {
   return (__ldcg(bits + (x >> 5)) >> (x & 31)) & 1u;
 }
 
+__device__ __forceinline__ void timeline(TreeCtrl* tc) {   // block 0 / thread 0 only
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const unsigned long long i = tc->nts;
+    if (i < 48) tc->tstamp[i] = t;
+    tc->nts = i + 1;
+  }
+}
+
 // warpenqueuefrontier: all 32 lanes call; lanes with `has` append
 // one item per slab list (bucket) of vertex x.  One atomicAdd per warp.
 __device__ __forceinline__ void warp_enqueue(const GraphDev& G, const TreeDev& T, uint64_t* fr,

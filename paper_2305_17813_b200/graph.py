@@ -221,6 +221,14 @@ class Tree:
               "meerkat_tree_invalidated")
         return np.sort(a[: int(n.value)])
 
+    def timeline(self):
+        """Device timestamps (ns) of the last call: start and every grid barrier; returns deltas in us."""
+        buf = (ctypes.c_uint64 * 48)()
+        n = ctypes.c_uint64(0)
+        check(_lib.lib().meerkat_tree_timeline(self._h, buf, 48, ctypes.byref(n)), "meerkat_tree_timeline")
+        ts = [int(buf[i]) for i in range(int(n.value))]
+        return [(b - a) / 1e3 for a, b in zip(ts, ts[1:])]
+
     def stats(self) -> dict:
         st = _lib.TreeStats()
         check(_lib.lib().meerkat_tree_stats_get(self._h, ctypes.byref(st)), "meerkat_tree_stats_get")
