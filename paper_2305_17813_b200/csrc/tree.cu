@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_static(const __grid_cons
   const uint32_t r = run_rounds<MAP, RELAX>(A, epoch, grid, 0, c);
   if (tid == 0) *A.T.epoch_ptr = epoch + r + 2;   // every thread read the base before the first grid.sync
   flush_counters(A.G, A.T, c, tid == 0, r, 0);
+  timeline(A.T.ctrl);
 }
 
 // ------------------------------------------------------------------ incremental
@@ -198,6 +199,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_inc(const __grid_constan
   const uint32_t r = run_rounds<MAP, RELAX>(A, epoch, grid, 0, c);
   if (tid == 0) *A.T.epoch_ptr = epoch + r + 2;
   flush_counters(A.G, A.T, c, tid == 0, r, 0);
+  timeline(A.T.ctrl);
 }
 
 // ------------------------------------------------------------------ decremental
@@ -326,7 +328,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_dec(const __grid_constan
     expand<MAP, PULL>(A, pull, __ldcg(&tc->pull_n), A.T.fr[r1 & 1], &tc->size[r1 % 3], epoch + r1, c);
   } else if (n_inv) {
     // filter only while sparse enough: two bits per member, bit load <= 1/4 (false positives <= ~6%)
-    const uint32_t fw = (n_inv * 8 <= (uint64_t)A.filter_words * 32) ? A.filter_words : 0u;
+    const uint32_t fw = (A.filter_words && n_inv * 8 <= (uint64_t)A.filter_words * 32) ? A.filter_words : 0u;
     if (fw) {
       for (uint32_t i = threadIdx.x; i < fw; i += blockDim.x) filt[i] = 0;
       __syncthreads();
@@ -352,6 +354,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_dec(const __grid_constan
   }
   if (tid == 0) *A.T.epoch_ptr = epoch + r2 + 2;
   flush_counters(A.G, A.T, c, tid == 0, r2 - r1, r1);
+  timeline(A.T.ctrl);
 }
 
 // ------------------------------------------------------------------ host side
@@ -389,7 +392,7 @@ cudaError_t launch_tree(meerkat_graph* g, meerkat_tree* t, int mode, const uint3
   A.bs = s; A.bd = d; A.bw = w; A.bn = n;
   A.unit = t->unit ? 1u : 0u;
   A.weighted = g->weighted ? 1u : 0u;
-  A.filter_words = FILTER_WORDS;
+  A.filter_words = g->reverse ? 0u : FILTER_WORDS;
   cudaError_t e = cudaMemsetAsync(t->dev.ctrl, 0, sizeof(TreeCtrl), g->stream);
   if (e != cudaSuccess) return e;
   int bps = g->tree_blocks_per_sm[mode];
@@ -399,7 +402,8 @@ cudaError_t launch_tree(meerkat_graph* g, meerkat_tree* t, int mode, const uint3
     bps = std::min(bps, g->latency_bps);
   dim3 grid((unsigned)(bps * g->sm_count)), block(TREE_BLOCK);
   void* args[] = {&A};
-  const size_t smem = mode == MODE_DECREMENTAL ? (size_t)FILTER_WORDS * 4 : 0;
+  // the shared-memory filter is only used by the full-store scan (no in-edge mirror)
+  const size_t smem = (mode == MODE_DECREMENTAL && !g->reverse) ? (size_t)FILTER_WORDS * 4 : 0;
   void* fn;
   if (g->weighted)
     fn = mode == MODE_STATIC ? (void*)k_tree_static<true> : mode == MODE_INCREMENTAL ? (void*)k_tree_inc<true>

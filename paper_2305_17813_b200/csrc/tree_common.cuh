@@ -110,24 +110,34 @@ __device__ __forceinline__ bool relax(const TreeDev& T, uint32_t x, uint64_t dis
   return atomicExch(T.stamp + x, epoch_next) != epoch_next;
 }
 
+// Counter flush at kernel end: warp reduce -> shared-memory block reduce -> one global
+// atomic per counter per block (a warp-level flush put ~5K same-address atomics per
+// counter on the kernel's tail).  All threads of the block must call it.
 __device__ __forceinline__ void flush_counters(const GraphDev& G, const TreeDev& T, Counters& c, bool rounds_owner,
                                                uint32_t relax_rounds, uint32_t prop_rounds) {
+  __shared__ unsigned long long acc[8];
   TreeCtrl* tc = T.ctrl;
+  if (threadIdx.x < 8) acc[threadIdx.x] = 0;
+  __syncthreads();
   auto red = [](uint32_t v) { return __reduce_add_sync(FULL, v); };
-  const uint32_t items = red(c.items), slabs = red(c.slabs), visited = red(c.visited), imp = red(c.improved),
-                 ss = red(c.scan_slabs), hits = red(c.hits), batch = red(c.batch);
+  const uint32_t v[7] = {red(c.items), red(c.slabs), red(c.visited), red(c.improved), red(c.scan_slabs),
+                         red(c.hits), red(c.batch)};
   const uint32_t err = __reduce_or_sync(FULL, c.err);
   if (lane_id() == 0) {
-    if (items) atomicAdd(&tc->items, (unsigned long long)items);
-    if (slabs) atomicAdd(&tc->slabs_read, (unsigned long long)slabs);
-    if (visited) atomicAdd(&tc->visited, (unsigned long long)visited);
-    if (imp) atomicAdd(&tc->improved, (unsigned long long)imp);
-    if (ss) atomicAdd(&tc->scan_slabs, (unsigned long long)ss);
-    if (hits) atomicAdd(&tc->scan_hits, (unsigned long long)hits);
-    if (batch) atomicAdd(&tc->batch_edges, (unsigned long long)batch);
-    if (err) atomicOr(&G.ctrl->err, err);
+#pragma unroll
+    for (int i = 0; i < 7; i++)
+      if (v[i]) atomicAdd(&acc[i], (unsigned long long)v[i]);
+    if (err) atomicOr(reinterpret_cast<unsigned int*>(&acc[7]), err);
+  }
+  __syncthreads();
+  if (threadIdx.x < 8 && acc[threadIdx.x]) {
+    unsigned long long* dst[7] = {&tc->items, &tc->slabs_read, &tc->visited, &tc->improved, &tc->scan_slabs,
+                                  &tc->scan_hits, &tc->batch_edges};
+    if (threadIdx.x < 7) atomicAdd(dst[threadIdx.x], acc[threadIdx.x]);
+    else atomicOr(&G.ctrl->err, (unsigned int)acc[7]);
   }
   if (rounds_owner) { tc->rounds = relax_rounds; tc->prop_rounds = prop_rounds; }
+}
 }
 
 // Blocked two-bit Bloom filter of V_invalid in shared memory: one word per key,
