@@ -138,7 +138,6 @@ __device__ __forceinline__ void flush_counters(const GraphDev& G, const TreeDev&
   }
   if (rounds_owner) { tc->rounds = relax_rounds; tc->prop_rounds = prop_rounds; }
 }
-}
 
 // Blocked two-bit Bloom filter of V_invalid in shared memory: one word per key,
 // two bits within it (false-positive rate ~ load^2).  Exact membership is the

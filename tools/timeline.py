@@ -29,17 +29,31 @@ g.insert(T(bs), T(bd), T(bw))
 sp, bf = g.sssp(W.source), g.bfs(W.source)
 fmt = lambda xs: " ".join(f"{x:.1f}" for x in xs)
 print("static sssp", fmt(sp.timeline()))
+st = torch.cuda.current_stream()
+
+
+def timed(fn):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    fn()
+    e1.record(st)
+    e1.synchronize()
+    return 1e3 * e0.elapsed_time(e1)
+
+
 for i in range(a.steps + 1):
     s, d, w = (T(x) for x in W.inserts[i])
     g.insert(s, d, w, count=False)
-    sp.incremental(s, d, w); t1 = sp.timeline()
-    bf.incremental(s, d); t2 = bf.timeline()
+    ev1 = timed(lambda: sp.incremental(s, d, w)); t1 = sp.timeline()
+    ev2 = timed(lambda: bf.incremental(s, d)); t2 = bf.timeline()
     s, d = (T(x) for x in W.deletes[i][:2])
     g.delete(s, d, count=False)
-    sp.decremental(s, d); t3 = sp.timeline(); st3 = sp.stats()
-    bf.decremental(s, d); t4 = bf.timeline()
+    ev3 = timed(lambda: sp.decremental(s, d)); t3 = sp.timeline(); st3 = sp.stats()
+    ev4 = timed(lambda: bf.decremental(s, d)); t4 = bf.timeline()
     if i:
-        print(f"step {i}: sssp_inc total {sum(t1):.1f} us: {fmt(t1)}")
-        print(f"        bfs_inc  total {sum(t2):.1f} us: {fmt(t2)}")
-        print(f"        sssp_dec total {sum(t3):.1f} us (prop {st3['propagate_rounds']}, relax {st3['rounds']}): {fmt(t3)}")
-        print(f"        bfs_dec  total {sum(t4):.1f} us: {fmt(t4)}")
+        print(f"step {i}: sssp_inc event {ev1:.1f} us, in-kernel {sum(t1):.1f} us: {fmt(t1)}")
+        print(f"        bfs_inc  event {ev2:.1f} us, in-kernel {sum(t2):.1f} us: {fmt(t2)}")
+        print(f"        sssp_dec event {ev3:.1f} us, in-kernel {sum(t3):.1f} us (prop {st3['propagate_rounds']}, "
+              f"relax {st3['rounds']}): {fmt(t3)}")
+        print(f"        bfs_dec  event {ev4:.1f} us, in-kernel {sum(t4):.1f} us: {fmt(t4)}")
