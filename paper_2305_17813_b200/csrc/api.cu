@@ -152,6 +152,7 @@ meerkat_status meerkat_create(const meerkat_config* cfg, meerkat_graph** out) {
   }
   if (e == cudaSuccess) e = tree_occupancy(g);
   if (const char* s = std::getenv("MEERKAT_LATENCY_BLOCKS_PER_SM")) g->latency_bps = std::atoi(s);
+  if (const char* s = std::getenv("MEERKAT_LOCAL_STACKS")) g->local_stacks = std::atoi(s) != 0;
   if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
   if (e != cudaSuccess) {
     cudaGetLastError();
@@ -338,7 +339,9 @@ static meerkat_status tree_create(meerkat_graph* g, uint32_t source, bool unit, 
   if (e == cudaSuccess) e = cudaMalloc(&T.inval_list, V * 4);
   if (e == cudaSuccess) e = cudaMalloc(&T.fr[0], T.fr_cap * 8);
   if (e == cudaSuccess) e = cudaMalloc(&T.fr[1], T.fr_cap * 8);
-  if (e == cudaSuccess) e = cudaMalloc(&T.ctrl, sizeof(TreeCtrl));
+  if (e == cudaSuccess) e = cudaMalloc(&t->ctrl_base, 2 * sizeof(TreeCtrl));   // double-buffered (tree.cu)
+  if (e == cudaSuccess) e = cudaMemsetAsync(t->ctrl_base, 0, 2 * sizeof(TreeCtrl), g->stream);
+  T.ctrl = t->ctrl_base;
   if (e == cudaSuccess) e = cudaMalloc(&T.epoch_ptr, 4);
   if (e == cudaSuccess) e = cudaMallocHost(&t->hctrl, sizeof(TreeCtrl));
   if (e == cudaSuccess) e = cudaMemsetAsync(T.stamp, 0, V * 4, g->stream);
@@ -349,7 +352,7 @@ static meerkat_status tree_create(meerkat_graph* g, uint32_t source, bool unit, 
     e = cudaMemcpyAsync(T.epoch_ptr, &one, 4, cudaMemcpyHostToDevice, g->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
   }
-  t->bytes = V * 8 + V * 4 + words * 4 + V * 4 + 2 * T.fr_cap * 8 + sizeof(TreeCtrl) + 4;
+  t->bytes = V * 8 + V * 4 + words * 4 + V * 4 + 2 * T.fr_cap * 8 + 2 * sizeof(TreeCtrl) + 4;
   if (e != cudaSuccess) {
     cudaGetLastError();
     meerkat_tree_destroy(t);
@@ -509,7 +512,7 @@ meerkat_status meerkat_tree_destroy(meerkat_tree* t) {
   cudaStreamSynchronize(t->g->stream);
   TreeDev& T = t->dev;
   cudaFree(T.node); cudaFree(T.stamp); cudaFree(T.inval_bits); cudaFree(T.inval_list);
-  cudaFree(T.fr[0]); cudaFree(T.fr[1]); cudaFree(T.ctrl); cudaFree(T.epoch_ptr);
+  cudaFree(T.fr[0]); cudaFree(T.fr[1]); cudaFree(t->ctrl_base); cudaFree(T.epoch_ptr);
   if (t->hctrl) cudaFreeHost(t->hctrl);
   dtree_free(t);
   delete t;

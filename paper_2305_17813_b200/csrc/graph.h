@@ -69,6 +69,7 @@ struct meerkat_graph {
   size_t stage_bytes[4] = {0, 0, 0, 0};
   int tree_blocks_per_sm[3] = {0, 0, 0};   // cooperative occupancy: static, incremental, decremental
   int latency_bps = 0;                      // blocks/SM for latency-bound tree calls (0 = occupancy)
+  bool local_stacks = true;                 // in-round local stacks for incremental / decremental calls
   unsigned long long* rscratch = nullptr;   // meerkat_route: device counts + cursors
   unsigned long long* hrscratch = nullptr;  // pinned counts
 };
@@ -79,6 +80,8 @@ struct meerkat_tree {
   mk::TreeCtrl* hctrl = nullptr;
   bool unit = false;     // BFS
   uint64_t version = 0;
+  mk::TreeCtrl* ctrl_base = nullptr;   // two control blocks: a call uses one and zeroes the other
+  int parity = 0;
   // vertex-partitioned trees (dtree.cu)
   bool dist = false;
   int cur = 0;                              // frontier buffer filled by the last phase

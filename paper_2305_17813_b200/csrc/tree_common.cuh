@@ -13,7 +13,10 @@ constexpr int TREE_BLOCK = 512;
 constexpr int FILTER_WORDS = 24576;   // 96 KiB smem Bloom filter per block (decremental scan), 2 blocks/SM
 constexpr int SCAN_UNROLL = 4;        // independent slabs in flight per group in the scan
 constexpr unsigned FULL = 0xFFFFFFFFu;
-constexpr uint64_t PROBE_MIN_ITEMS = 65536;   // frontiers at least this large probe node[x] before the atomic
+constexpr uint64_t PROBE_MIN_ITEMS = 65536;
+constexpr int LOCAL_STACK = 16;              // items per group's shared-memory stack
+constexpr int LOCAL_MAX_BUCKETS = 4;         // vertices with more slab lists always go to the frontier
+constexpr uint64_t LOCAL_MAX_ITEMS = 65536;  // local stacks only for frontiers smaller than this   // frontiers at least this large probe node[x] before the atomic
 
 enum Visit { RELAX = 0, PROPAGATE = 1, PULL = 2 };
 
@@ -28,7 +31,16 @@ struct TreeArgs {
   uint32_t unit;        // 1: BFS (w = 1)
   uint32_t weighted;    // graph has weights (map store)
   uint32_t filter_words;
+  uint32_t local;       // 1: allow in-round local stacks (not for static: keeps BFS level-synchronous)
+  TreeCtrl* clear_ctrl; // the other control block: zeroed at kernel end for the next call (no memset launch)
 };
+
+// Zero the next call's control block (block 0, after the last grid barrier).
+__device__ __forceinline__ void clear_next_ctrl(TreeCtrl* p) {
+  if (blockIdx.x != 0 || !p) return;
+  unsigned long long* w = reinterpret_cast<unsigned long long*>(p);
+  for (uint32_t i = threadIdx.x; i < sizeof(TreeCtrl) / 8; i += blockDim.x) w[i] = 0;
+}
 
 struct Counters {
   uint32_t items = 0, slabs = 0, visited = 0, improved = 0, scan_slabs = 0, hits = 0, batch = 0, err = 0;
