@@ -152,7 +152,6 @@ meerkat_status meerkat_create(const meerkat_config* cfg, meerkat_graph** out) {
   }
   if (e == cudaSuccess) e = tree_occupancy(g);
   if (const char* s = std::getenv("MEERKAT_LATENCY_BLOCKS_PER_SM")) g->latency_bps = std::atoi(s);
-  if (const char* s = std::getenv("MEERKAT_LOCAL_STACKS")) g->local_stacks = std::atoi(s) != 0;
   if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
   if (e != cudaSuccess) {
     cudaGetLastError();

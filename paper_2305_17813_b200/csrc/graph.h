@@ -69,7 +69,6 @@ struct meerkat_graph {
   size_t stage_bytes[4] = {0, 0, 0, 0};
   int tree_blocks_per_sm[3] = {0, 0, 0};   // cooperative occupancy: static, incremental, decremental
   int latency_bps = 0;                      // blocks/SM for latency-bound tree calls (0 = occupancy)
-  bool local_stacks = true;                 // in-round local stacks for incremental / decremental calls
   unsigned long long* rscratch = nullptr;   // meerkat_route: device counts + cursors
   unsigned long long* hrscratch = nullptr;  // pinned counts
 };

@@ -35,68 +35,34 @@
 
 namespace mk {
 
+// Next item of this group (grid-stride over [it, n)): vertex and slab come from the item.
+__device__ __forceinline__ bool fetch_item(const uint64_t* fr, uint64_t n, uint64_t& it, uint32_t& v, uint32_t& slab,
+                                           int l8, Counters& c) {
+  if (it >= n) return false;
+  const uint64_t item = fr[it];
+  v = (uint32_t)item;
+  slab = (uint32_t)(item >> 32);
+  if (l8 == 0) c.items++;
+  return true;
+}
+
 // Expand the frontier items [0, n) of `fr` (one 8-lane group per item), applying
 // VISIT to every live edge; successful vertices go to `fnext`.  The first slab of
 // an item and d(v) are loaded together (independent requests).
-//
-// Small frontiers (incremental / decremental work) additionally use a per-group
-// LOCAL STACK in shared memory: a vertex this group improves (or invalidates) is
-// expanded by the same group within the same round instead of waiting for the
-// next grid barrier — chaotic relaxation, which reaches the same fixpoint
-// (SURVEY §8(c)).  A popped vertex's stamp is cleared before d(v) is read, so any
-// later improvement in the round enqueues it again.
-struct LocalStacks {
-  uint64_t item[TREE_BLOCK / GROUP][LOCAL_STACK];
-  int top[TREE_BLOCK / GROUP];
-};
-
 template <bool MAP, int VISIT>
 __device__ __forceinline__ void expand(const TreeArgs& A, const uint64_t* fr, uint64_t n, uint64_t* fnext,
-                                       unsigned long long* sznext, uint32_t epoch_next, Counters& c,
-                                       LocalStacks& ls) {
+                                       unsigned long long* sznext, uint32_t epoch_next, Counters& c) {
   using F = Frag<MAP>;
   constexpr int NK = F::NK;
-  auto& lstk = ls.item;
-  auto& ltop = ls.top;
   const GraphDev& G = A.G;
   const GraphDev& S = VISIT == PULL ? A.R : A.G;   // store whose slab lists are walked
   const TreeDev& T = A.T;
-  const int lane = lane_id(), l8 = lane & 7, gib = threadIdx.x / GROUP;
-  const uint32_t gmask = 0xFFu << (lane & 24);
+  const int lane = lane_id(), l8 = lane & 7;
   const uint64_t ng = ((uint64_t)gridDim.x * blockDim.x) / GROUP;
   const bool probe = n > PROBE_MIN_ITEMS;
-  const bool local = VISIT != PULL && A.local && n < LOCAL_MAX_ITEMS;
-  if (l8 == 0) ltop[gib] = 0;
-  __syncwarp();
   uint64_t it = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / GROUP;
   uint32_t v = 0, slab = 0, du = 0;
-  // next item: this group's local stack first (depth first), then the round's frontier
-  auto fetch = [&]() -> bool {
-    if (local) {
-      const int top = ltop[gib];
-      if (top > 0) {
-        const uint64_t item = lstk[gib][top - 1];
-        __syncwarp(gmask);
-        if (l8 == 0) {
-          ltop[gib] = top - 1;
-          if (VISIT == RELAX) { T.stamp[(uint32_t)item] = 0; __threadfence(); }
-        }
-        __syncwarp(gmask);
-        v = (uint32_t)item;
-        slab = (uint32_t)(item >> 32);
-        if (l8 == 0) c.items++;
-        return true;
-      }
-    }
-    if (it >= n) return false;
-    const uint64_t item = fr[it];
-    it += ng;
-    v = (uint32_t)item;
-    slab = (uint32_t)(item >> 32);
-    if (l8 == 0) c.items++;
-    return true;
-  };
-  bool active = fetch();
+  bool active = fetch_item(fr, n, it, v, slab, l8, c);
   bool fresh = active;
   while (__any_sync(FULL, active)) {
     uint4 d = make_uint4(EMPTY_KEY, EMPTY_KEY, EMPTY_KEY, INVALID_SLAB);
@@ -146,31 +112,12 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const uint64_t* fr, ui
           }
         }
       }
-      bool glob = enq;
-      if (local && enq) {   // try this group's stack: reserve with CAS (no rollback races)
-        const uint2 m = __ldcg(G.vmeta + x);
-        const int cnt = m.x == INVALID_SLAB ? 0 : (int)m.y;
-        if (cnt == 0) glob = false;
-        else if (cnt <= LOCAL_MAX_BUCKETS) {
-          int old = ltop[gib];
-          while (old + cnt <= LOCAL_STACK) {
-            const int r = atomicCAS(&ltop[gib], old, old + cnt);
-            if (r == old) {
-              for (int j = 0; j < cnt; j++) lstk[gib][old + j] = ((uint64_t)(m.x + j) << 32) | x;
-              glob = false;
-              break;
-            }
-            old = r;
-          }
-        }
-      }
-      warp_enqueue(G, T, fnext, sznext, glob, VISIT == PULL ? v : x, c);
+      warp_enqueue(G, T, fnext, sznext, enq, VISIT == PULL ? v : x, c);
     }
-    __syncwarp();
     const uint32_t nxt = __shfl_sync(FULL, d.w, (lane & 24) + GROUP - 1);
     if (active) {
       if (nxt != INVALID_SLAB && !dead) slab = nxt;
-      else { active = fetch(); fresh = active; }
+      else { it += ng; active = fetch_item(fr, n, it, v, slab, l8, c); fresh = active; }
     }
   }
 }
@@ -180,13 +127,13 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const uint64_t* fr, ui
 // zeroed during round r so it is clean when it becomes "next".
 template <bool MAP, int VISIT>
 __device__ __forceinline__ uint32_t run_rounds(const TreeArgs& A, uint32_t epoch, cg::grid_group& grid, uint32_t r,
-                                               Counters& c, LocalStacks& ls) {
+                                               Counters& c) {
   TreeCtrl* tc = A.T.ctrl;
   for (;;) {
     const uint64_t n = __ldcg(&tc->size[r % 3]);
     if (n == 0) break;
     if (blockIdx.x == 0 && threadIdx.x == 0) tc->size[(r + 2) % 3] = 0;
-    expand<MAP, VISIT>(A, A.T.fr[r & 1], n, A.T.fr[(r + 1) & 1], &tc->size[(r + 1) % 3], epoch + r + 1, c, ls);
+    expand<MAP, VISIT>(A, A.T.fr[r & 1], n, A.T.fr[(r + 1) & 1], &tc->size[(r + 1) % 3], epoch + r + 1, c);
     grid.sync();
     timeline(A.T.ctrl);
     r++;
@@ -199,7 +146,6 @@ __device__ __forceinline__ uint32_t run_rounds(const TreeArgs& A, uint32_t epoch
 template <bool MAP>
 __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_static(const __grid_constant__ TreeArgs A) {
   const uint32_t epoch = __ldcg(A.T.epoch_ptr);
-  __shared__ LocalStacks ls;
   timeline(A.T.ctrl);
   cg::grid_group grid = cg::this_grid();
   Counters c;
@@ -215,7 +161,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_static(const __grid_cons
   }
   grid.sync();
     timeline(A.T.ctrl);
-  const uint32_t r = run_rounds<MAP, RELAX>(A, epoch, grid, 0, c, ls);
+  const uint32_t r = run_rounds<MAP, RELAX>(A, epoch, grid, 0, c);
   if (tid == 0) *A.T.epoch_ptr = epoch + r + 2;   // every thread read the base before the first grid.sync
   flush_counters(A.G, A.T, c, tid == 0, r, 0);
   clear_next_ctrl(A.clear_ctrl);
@@ -227,7 +173,6 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_static(const __grid_cons
 template <bool MAP>
 __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_inc(const __grid_constant__ TreeArgs A) {
   const uint32_t epoch = __ldcg(A.T.epoch_ptr);
-  __shared__ LocalStacks ls;
   timeline(A.T.ctrl);
   cg::grid_group grid = cg::this_grid();
   Counters c;
@@ -252,7 +197,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_inc(const __grid_constan
   }
   grid.sync();
     timeline(A.T.ctrl);
-  const uint32_t r = run_rounds<MAP, RELAX>(A, epoch, grid, 0, c, ls);
+  const uint32_t r = run_rounds<MAP, RELAX>(A, epoch, grid, 0, c);
   if (tid == 0) *A.T.epoch_ptr = epoch + r + 2;
   flush_counters(A.G, A.T, c, tid == 0, r, 0);
   clear_next_ctrl(A.clear_ctrl);
@@ -337,7 +282,6 @@ template <bool MAP>
 __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_dec(const __grid_constant__ TreeArgs A) {
   extern __shared__ uint32_t filt[];
   const uint32_t epoch = __ldcg(A.T.epoch_ptr);
-  __shared__ LocalStacks ls;
   timeline(A.T.ctrl);
   cg::grid_group grid = cg::this_grid();
   Counters c;
@@ -369,7 +313,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_dec(const __grid_constan
   grid.sync();
     timeline(A.T.ctrl);
   // (ii) PropagateInvalidation to all of T_v
-  const uint32_t r1 = run_rounds<MAP, PROPAGATE>(A, epoch, grid, 0, c, ls);
+  const uint32_t r1 = run_rounds<MAP, PROPAGATE>(A, epoch, grid, 0, c);
   // (iii) valid -> invalid frontier, fused with the first relaxation
   const uint64_t n_inv = __ldcg(&tc->inval_n);
   if (n_inv && A.R.slabs) {
@@ -383,7 +327,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_dec(const __grid_constan
     }
     grid.sync();
     timeline(A.T.ctrl);
-    expand<MAP, PULL>(A, pull, __ldcg(&tc->pull_n), A.T.fr[r1 & 1], &tc->size[r1 % 3], epoch + r1, c, ls);
+    expand<MAP, PULL>(A, pull, __ldcg(&tc->pull_n), A.T.fr[r1 & 1], &tc->size[r1 % 3], epoch + r1, c);
   } else if (n_inv) {
     // filter only while sparse enough: two bits per member, bit load <= 1/4 (false positives <= ~6%)
     const uint32_t fw = (A.filter_words && n_inv * 8 <= (uint64_t)A.filter_words * 32) ? A.filter_words : 0u;
@@ -404,7 +348,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_dec(const __grid_constan
   grid.sync();
     timeline(A.T.ctrl);
   // (iv) common epilogue
-  const uint32_t r2 = run_rounds<MAP, RELAX>(A, epoch, grid, r1, c, ls);
+  const uint32_t r2 = run_rounds<MAP, RELAX>(A, epoch, grid, r1, c);
   // clear the invalid bit set for the next call (the list is kept for meerkat_tree_invalidated)
   for (uint64_t i = tid; i < n_inv; i += nt) {
     const uint32_t x = A.T.inval_list[i];
@@ -452,7 +396,6 @@ cudaError_t launch_tree(meerkat_graph* g, meerkat_tree* t, int mode, const uint3
   A.unit = t->unit ? 1u : 0u;
   A.weighted = g->weighted ? 1u : 0u;
   A.filter_words = g->reverse ? 0u : FILTER_WORDS;
-  A.local = (mode != MODE_STATIC && g->local_stacks) ? 1u : 0u;
   // control blocks alternate between calls: this call's was zeroed by the previous kernel
   A.T.ctrl = t->ctrl_base + t->parity;
   A.clear_ctrl = t->ctrl_base + (1 - t->parity);

@@ -31,7 +31,6 @@ struct TreeArgs {
   uint32_t unit;        // 1: BFS (w = 1)
   uint32_t weighted;    // graph has weights (map store)
   uint32_t filter_words;
-  uint32_t local;       // 1: allow in-round local stacks (not for static: keeps BFS level-synchronous)
   TreeCtrl* clear_ctrl; // the other control block: zeroed at kernel end for the next call (no memset launch)
 };
 
