@@ -60,6 +60,9 @@ def parse():
     p.add_argument("--cpu-scale", type=int, default=20, help="R-MAT scale of the oracle's bounded sample")
     p.add_argument("--cpu-steps", type=int, default=2)
     p.add_argument("--json-out", default=None)
+    p.add_argument("--sweep", action=argparse.BooleanOptionalAction, default=True,
+                   help="also run the config-2 insert/delete/query batch-size sweep (reported under store_sweep)")
+    p.add_argument("--sweep-scale", type=int, default=20)
     p.add_argument("--partitioned", action="store_true",
                    help="use the vertex-partitioned multi-GPU path even at --gpus 1 (NCCL, world size 1)")
     return p.parse_args()
@@ -341,6 +344,65 @@ def tree_detail(res):
                  "alg_bytes")} for n, v in res["tstats"].items() if v}
 
 
+def store_sweep(args, dev, stream):
+    """BASELINE config 2: R-MAT scale 20, batch insert / delete / query at
+    1K..1M edges per batch.  Inserts are fresh R-MAT draws (graph seed 11, duplicates and
+    self-loops kept as drawn), deletes are sampled present edges, queries are 50% present /
+    50% absent.  Median device time of `reps` batches per point; algorithmic bytes per edge
+    161 / 157 / 154 B."""
+    import torch
+    import synth
+    from paper_2305_17813_b200 import Graph
+    scale, reps = args.sweep_scale, 5
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.uint32).view(np.int32)).to(dev)
+    s, d, w = synth.rmat(scale, 16)
+    V = 1 << scale
+    g = Graph(V, weighted=True, hashing=not args.no_hashing, load_factor=args.lf,
+              degree_hints=T(np.bincount(s, minlength=V).astype(np.uint32)), device=dev.index or 0, stream=stream)
+    g.insert(T(s), T(d), T(w), count=False)
+    g.sync()
+    sizes = [1000, 10000, 100000, 1000000]
+    need = sum(sizes) * reps
+    dels = synth.sample_distinct(len(s), need, 17)
+    fresh = synth.rmat_draws(scale, need, 0, 11)
+    rng = np.random.default_rng(5)
+    out, di, fi = {}, 0, 0
+    ev = lambda: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    for b in sizes:
+        t_ins, t_del, t_q = [], [], []
+        for r in range(reps):
+            ins = tuple(T(x[fi:fi + b]) for x in fresh)
+            fi += b
+            dl = dels[di:di + b]
+            di += b
+            ds, dd = T(s[dl]), T(d[dl])
+            half = b // 2
+            qs = T(np.concatenate([s[rng.integers(0, len(s), half)], rng.integers(0, V, b - half)]))
+            qd = T(np.concatenate([d[rng.integers(0, len(s), half)], rng.integers(0, V, b - half)]))
+            qs2 = torch.cat([ds[:0], qs])
+            torch.cuda.synchronize()
+            for lst, fn in ((t_ins, lambda: g.insert(*ins, count=False)),
+                            (t_del, lambda: g.delete(ds, dd, count=False)),
+                            (t_q, lambda: g.query(qs2, qd))):
+                e0, e1 = ev()
+                e0.record(stream)
+                fn()
+                e1.record(stream)
+                e1.synchronize()
+                lst.append(e0.elapsed_time(e1))
+        med = lambda x: float(np.median(x))
+        out[str(b)] = {"insert_edges_per_s": b / (med(t_ins) / 1e3), "delete_edges_per_s": b / (med(t_del) / 1e3),
+                       "query_edges_per_s": b / (med(t_q) / 1e3),
+                       "insert_GBps_alg": 161 * b / (med(t_ins) / 1e3) / 1e9,
+                       "delete_GBps_alg": 157 * b / (med(t_del) / 1e3) / 1e9,
+                       "query_GBps_alg": 154 * b / (med(t_q) / 1e3) / 1e9,
+                       "ms": {"insert": med(t_ins), "delete": med(t_del), "query": med(t_q)}}
+    g.sync()
+    g.close()
+    return {"workload": f"rmat-s{scale}-ef16 (BASELINE config 2), {len(s)} edges, hashing "
+                        f"{'off' if args.no_hashing else 'on'} lf {args.lf}", "by_batch": out}
+
+
 def run_ours(args, ws, rank, local):
     import torch
 
@@ -416,6 +478,8 @@ def run_ours(args, ws, rank, local):
                "ms_per_step": r2["ms_per_step"], "per_call_ms": r2["mean"],
                "roofline": roofline_of(r2, peak, peak_src, traffic_file), "tree_calls": tree_detail(r2)}
 
+    sweep = store_sweep(args, dev, stream) if args.sweep and ws == 1 else None
+
     cb = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline(args, args.cpu_steps)
@@ -450,6 +514,7 @@ def run_ours(args, ws, rank, local):
         "clocks": res["clocks"],
         "store": res["store"],
         "alt": alt,
+        "store_sweep": sweep,
         "generate_s": gen_s,
     }
     if rank == 0:
