@@ -13,6 +13,7 @@
 //    from it on failure; a full list gets a pool slab linked into lane 31 by
 //    CAS ("chained at the end of the last filled slab").  A present key
 //    keeps the minimum weight via a 64-bit atomicMin on the <key, w> pair (C8).
+#include <cstdio>
 #include <cstring>
 
 #include <cub/cub.cuh>
@@ -20,6 +21,8 @@
 #include "graph.h"
 
 namespace mk {
+
+constexpr uint32_t WATCHDOG = 1u << 22;   // loop bound that turns a would-be hang into MEERKAT_E_STATE
 
 // ------------------------------------------------------------------ helpers
 
@@ -67,10 +70,18 @@ __device__ int group_link(const GraphDev& G, uint32_t u, uint64_t item, uint32_t
     __syncwarp(gmask);
     return s == INVALID_SLAB ? -1 : 1;
   }
+  uint32_t spins = 0;
   while (old == LINKING) {   // another group holds the lock: wait for its pointer
     __nanosleep(64);
     if (l8 == 0) old = *reinterpret_cast<volatile uint32_t*>(link);
     old = __shfl_sync(gmask, old, 0, GROUP);
+    if (++spins == WATCHDOG) {   // never expected: report instead of hanging
+      if (l8 == 0) {
+        printf("meerkat watchdog: link wait u=%u link=%p\n", u, link);
+        atomicOr(&G.ctrl->err, (unsigned)ERR_STATE);
+      }
+      return -1;
+    }
   }
   next_out = old;
   return 0;
@@ -100,7 +111,15 @@ __device__ int group_insert(const GraphDev& G, uint32_t u, uint32_t v, uint32_t 
     head = nxt;
   }
   uint32_t cur = head + bucket_of(v, count, G.seed);
+  uint32_t guard = 0;
   for (;;) {
+    if (++guard == WATCHDOG) {
+      if (l8 == 0) {
+        printf("meerkat watchdog: insert retry loop u=%u v=%u cur=%u\n", u, v, cur);
+        atomicOr(&G.ctrl->err, (unsigned)ERR_STATE);
+      }
+      return -1;
+    }
     // ---- pass 1: search up to the first slab with an EMPTY cell, remember the first writable cell
     uint32_t cand_slab = INVALID_SLAB, tail = INVALID_SLAB;
     int cand_cell = -1;
@@ -135,6 +154,13 @@ __device__ int group_insert(const GraphDev& G, uint32_t u, uint32_t v, uint32_t 
       const bool has_empty = ((__ballot_sync(gmask, eb != 0) >> gbase) & 0xFFu) != 0;
       const uint32_t nxt = __shfl_sync(gmask, d.w, GROUP - 1, GROUP);
       if (has_empty || nxt == INVALID_SLAB || nxt == LINKING) { tail = s; break; }
+      if (++guard == WATCHDOG || nxt >= G.H + G.P) {
+        if (l8 == 0) {
+          printf("meerkat watchdog: insert walk u=%u v=%u s=%u nxt=%u\n", u, v, s, nxt);
+          atomicOr(&G.ctrl->err, (unsigned)ERR_STATE);
+        }
+        return -1;
+      }
       s = nxt;
     }
     if (found_cell >= 0) {
@@ -223,6 +249,7 @@ __device__ int group_find(const GraphDev& G, uint32_t u, uint32_t v, int l8, uin
   const uint32_t head = ld_head_cg(G, u);
   if (head == INVALID_SLAB) return -1;
   uint32_t s = head + bucket_of(v, G.vmeta[u].y, G.seed);
+  uint32_t guard = 0;
   for (;;) {
     const uint4 d = ld_slab_cg(slab_ptr(G, s), l8);
     uint32_t mb = 0, eb = 0;
@@ -247,6 +274,13 @@ __device__ int group_find(const GraphDev& G, uint32_t u, uint32_t v, int l8, uin
     const bool has_empty = ((__ballot_sync(gmask, eb != 0) >> gbase) & 0xFFu) != 0;
     const uint32_t nxt = __shfl_sync(gmask, d.w, GROUP - 1, GROUP);
     if (has_empty || nxt == INVALID_SLAB) return -1;
+    if (++guard == WATCHDOG || nxt >= G.H + G.P) {
+      if (l8 == 0) {
+        printf("meerkat watchdog: find walk u=%u v=%u s=%u nxt=%u\n", u, v, s, nxt);
+        atomicOr(&G.ctrl->err, (unsigned)ERR_STATE);
+      }
+      return -1;
+    }
     s = nxt;
   }
 }
