@@ -149,6 +149,10 @@ meerkat_status meerkat_query_batch(meerkat_graph* g, const uint32_t* src, const 
 meerkat_status meerkat_export_edges(meerkat_graph* g, uint32_t* src, uint32_t* dst, uint32_t* w,
                                     uint64_t capacity, uint64_t* n_out);
 meerkat_status meerkat_stats_get(meerkat_graph* g, meerkat_stats* out); /* synchronises */
+/* Structural check of the slab store(s) (owner of every slab, next pointers, no leftover link
+ * lock, finite chains, EMPTY-suffix invariant).  info[5] (host): violations, then the first one's
+ * vertex, slab, next, kind.  MEERKAT_E_STATE if any; synchronises. */
+meerkat_status meerkat_check(meerkat_graph* g, uint64_t* info);
 
 /* Static SSSP (weighted graphs only) / level-based static BFS
  * (hop counts, weights ignored).  The new tree reflects the current

@@ -287,6 +287,23 @@ meerkat_status meerkat_export_edges(meerkat_graph* g, uint32_t* src, uint32_t* d
   return n > capacity ? MEERKAT_E_CAPACITY : MEERKAT_OK;
 }
 
+meerkat_status meerkat_check(meerkat_graph* g, uint64_t* info) {
+  if (!g || !info) return MEERKAT_E_INVALID_ARG;
+  DeviceGuard dg(g->device);
+  unsigned long long* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, 10 * 8);
+  if (e == cudaSuccess) e = launch_fsck(g, g->out, d);
+  if (e == cudaSuccess && g->reverse) e = launch_fsck(g, g->in, d + 5);
+  uint64_t h[10] = {0};
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h, d, 10 * 8, cudaMemcpyDeviceToHost, g->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  cudaFree(d);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  for (int i = 0; i < 5; i++) info[i] = h[i] ? h[i] : h[5 + i];
+  info[0] = h[0] + (g->reverse ? h[5] : 0);
+  return info[0] ? MEERKAT_E_STATE : MEERKAT_OK;
+}
+
 meerkat_status meerkat_stats_get(meerkat_graph* g, meerkat_stats* out) {
   if (!g || !out) return MEERKAT_E_INVALID_ARG;
   DeviceGuard dg(g->device);

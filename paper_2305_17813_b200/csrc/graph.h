@@ -104,6 +104,7 @@ cudaError_t launch_delete(meerkat_graph* g, Store& st, const uint32_t* s, const 
 cudaError_t launch_query(meerkat_graph* g, Store& st, const uint32_t* s, const uint32_t* d, uint64_t n,
                          uint8_t* found, uint32_t* w_out);
 cudaError_t launch_export(meerkat_graph* g, Store& st, uint32_t* s, uint32_t* d, uint32_t* w, uint64_t cap);
+cudaError_t launch_fsck(meerkat_graph* g, Store& st, unsigned long long* info_dev);
 // tree.cu
 cudaError_t tree_occupancy(meerkat_graph* g);
 enum TreeMode { MODE_STATIC = 0, MODE_INCREMENTAL = 1, MODE_DECREMENTAL = 2 };

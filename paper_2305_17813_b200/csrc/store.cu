@@ -22,7 +22,7 @@
 
 namespace mk {
 
-constexpr uint32_t WATCHDOG = 1u << 22;   // loop bound that turns a would-be hang into MEERKAT_E_STATE
+constexpr uint32_t WATCHDOG = 1u << 16;   // loop bound that turns a would-be hang into MEERKAT_E_STATE
 
 // ------------------------------------------------------------------ helpers
 
@@ -115,7 +115,16 @@ __device__ int group_insert(const GraphDev& G, uint32_t u, uint32_t v, uint32_t 
   for (;;) {
     if (++guard == WATCHDOG) {
       if (l8 == 0) {
-        printf("meerkat watchdog: insert retry loop u=%u v=%u cur=%u\n", u, v, cur);
+        const uint32_t h0 = G.vmeta[u].x, cnt0 = G.vmeta[u].y;
+        printf("meerkat watchdog: insert retry loop u=%u v=%u cur=%u head=%u count=%u bucket=%u owner(cur)=%u "
+               "H=%u P=%u\n", u, v, cur, h0, cnt0, bucket_of(v, cnt0, G.seed), G.owner[cur], G.H, G.P);
+        uint32_t x = cur;
+        for (int k = 0; k < 6 && x < G.H + G.P; k++) {
+          const uint32_t* p = slab_ptr(G, x);
+          printf("  slab %u owner %u next %u w0..5 %x %x %x %x %x %x w28..30 %x %x %x\n", x, G.owner[x], p[31],
+                 p[0], p[1], p[2], p[3], p[4], p[5], p[28], p[29], p[30]);
+          x = p[31];
+        }
         atomicOr(&G.ctrl->err, (unsigned)ERR_STATE);
       }
       return -1;
@@ -428,6 +437,49 @@ __global__ void k_fill(uint32_t* __restrict__ slabs, uint64_t n_slabs, int map) 
   }
 }
 
+// ------------------------------------------------------------------ consistency check (fsck)
+
+// One thread per vertex walks every slab list of the vertex and checks the store's
+// structural invariants: each slab's owner is the vertex, next pointers are INVALID
+// or pool slabs, no LINKING lock survives a kernel, chains are finite, and no slab
+// follows a slab that still has an EMPTY cell (EMPTY-suffix invariant, §4.2).
+// info[0] = violations, info[1..4] = first violation (vertex, slab, next, kind).
+template <bool MAP>
+__global__ void k_fsck(GraphDev G, unsigned long long* info) {
+  using F = Frag<MAP>;
+  for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < G.V; u += (uint64_t)gridDim.x * blockDim.x) {
+    const uint2 m = G.vmeta[u];
+    if (m.x == INVALID_SLAB) continue;
+    int kind = 0;
+    uint32_t bad_s = 0, bad_n = 0;
+    if (m.x == LINKING) { kind = 1; }
+    for (uint32_t b = 0; b < m.y && !kind; b++) {
+      uint32_t s = m.x + b, steps = 0;
+      while (!kind) {
+        if (s >= G.H + G.P) { kind = 2; bad_s = s; break; }
+        if (G.owner[s] != (uint32_t)u) { kind = 3; bad_s = s; break; }
+        const uint32_t* p = slab_ptr(G, s);
+        bool has_empty = false;
+        for (int w = 0; w < SLAB_WORDS - 1; w++) {
+          const bool keyword = MAP ? ((w & 1) == 0 && w < 30) : true;
+          if (keyword && p[w] == EMPTY_KEY) has_empty = true;
+        }
+        const uint32_t nx = p[SLAB_WORDS - 1];
+        if (nx == INVALID_SLAB) break;
+        if (nx == LINKING) { kind = 4; bad_s = s; bad_n = nx; break; }
+        if (nx < G.H || nx >= G.H + G.P) { kind = 5; bad_s = s; bad_n = nx; break; }
+        if (has_empty) { kind = 6; bad_s = s; bad_n = nx; break; }
+        if (++steps > (1u << 24)) { kind = 7; bad_s = s; break; }
+        s = nx;
+      }
+    }
+    if (kind) {
+      const unsigned long long k = atomicAdd(&info[0], 1ull);
+      if (k == 0) { info[1] = u; info[2] = bad_s; info[3] = bad_n; info[4] = kind; }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ host launchers
 
 static inline unsigned grid_for(meerkat_graph* g, uint64_t groups) {
@@ -523,6 +575,16 @@ cudaError_t launch_query(meerkat_graph* g, Store& st, const uint32_t* s, const u
   const unsigned gb = grid_for(g, n);
   if (g->weighted) k_query<true><<<gb, UPD_BLOCK, 0, g->stream>>>(st.dev, s, d, n, found, w_out);
   else k_query<false><<<gb, UPD_BLOCK, 0, g->stream>>>(st.dev, s, d, n, found, w_out);
+  g->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fsck(meerkat_graph* g, Store& st, unsigned long long* info_dev) {
+  cudaError_t e = cudaMemsetAsync(info_dev, 0, 5 * 8, g->stream);
+  if (e != cudaSuccess) return e;
+  const unsigned gb = (unsigned)std::min<uint64_t>((st.dev.V + 255) / 256, (uint64_t)g->sm_count * 16);
+  if (g->weighted) k_fsck<true><<<std::max(gb, 1u), 256, 0, g->stream>>>(st.dev, info_dev);
+  else k_fsck<false><<<std::max(gb, 1u), 256, 0, g->stream>>>(st.dev, info_dev);
   g->launches++;
   return cudaGetLastError();
 }

@@ -147,6 +147,12 @@ class Graph:
         order = np.lexsort((d, s))
         return s[order], d[order], w[order]
 
+    def check(self):
+        """Structural store check (meerkat_check): (violations, vertex, slab, next, kind) of the first."""
+        info = (ctypes.c_uint64 * 5)()
+        _lib.lib().meerkat_check(self._h, info)
+        return tuple(int(x) for x in info)
+
     def stats(self) -> dict:
         st = _lib.Stats()
         check(_lib.lib().meerkat_stats_get(self._h, ctypes.byref(st)), "meerkat_stats_get")
