@@ -163,7 +163,9 @@ __global__ void __launch_bounds__(D_BLOCK) k_dexpand(DArgs A) {
       if (l8 == 0) c.items++;
       slab = (uint32_t)(item >> 32);
       if (VISIT == PROPAGATE) return true;
-      const uint64_t nv = ld_cg_u64(T.node + v);
+      uint64_t nv = 0;
+      if (l8 == 0) nv = ld_cg_u64(T.node + v);   // one read per group, broadcast (d(v) may change)
+      nv = __shfl_sync(0xFFu << (lane & 24), nv, 0, GROUP);
       if (nv != UNREACHED) { du = (uint32_t)(nv >> 32); return true; }
     }
     return false;

@@ -101,7 +101,11 @@ __device__ int group_insert(const GraphDev& G, uint32_t u, uint32_t v, uint32_t 
   constexpr int NK = F::NK;
   const uint64_t item = MAP ? (((uint64_t)wt << 32) | v) : (uint64_t)v;
   const uint32_t count = G.vmeta[u].y;
-  uint32_t head = ld_head_cg(G, u);
+  // vmeta.x of a lazily-headed vertex changes under concurrent inserts (INVALID -> LINKING -> slab):
+  // one lane reads it and broadcasts, so every branch below stays uniform across the group
+  uint32_t head = 0;
+  if (l8 == 0) head = ld_head_cg(G, u);
+  head = __shfl_sync(gmask, head, 0, GROUP);
   int result = 0;
   while (head == INVALID_SLAB || head == LINKING) {
     // vertex without a head slab yet (hint 0, reading C22b): publish one holding the key

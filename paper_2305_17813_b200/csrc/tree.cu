@@ -69,9 +69,10 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const uint64_t* fr, ui
     uint64_t nv = 0;
     if (active) {
       d = ld_slab_ro(slab_ptr(S, slab), l8);
-      if (VISIT == RELAX && fresh) nv = ld_cg_u64(T.node + v);
-      if (l8 == 0) c.slabs++;
+      if (VISIT == RELAX && fresh && l8 == 0) nv = ld_cg_u64(T.node + v);   // one read per group, broadcast:
+      if (l8 == 0) c.slabs++;                                               // d(v) may change concurrently
     }
+    if (VISIT == RELAX) nv = __shfl_sync(FULL, nv, lane & 24);
     bool dead = false;
     if (VISIT == RELAX && active && fresh) {
       dead = nv == UNREACHED;
