@@ -174,3 +174,25 @@ def test_pool_exhaustion_reports_capacity():
     assert 31 <= n <= 93 and len(dd) == n and len(np.unique(dd)) == n and set(dd.tolist()) <= set(d.tolist())
     assert g.stats()["pool_used"] == 2
     assert g.stats()["edges"] == n
+
+
+@pytest.mark.parametrize("hashing", [True, False])
+def test_fresh_draw_stress_with_fsck(hashing):
+    """Large batches of fresh R-MAT draws (duplicates, self-loops, hub rows, vertices whose head slab is
+    created lazily by racing groups) then deletes, with the structural check after every kernel and the
+    edge set / counts against the oracle.  Regression test for a group-divergence race on lazy heads."""
+    scale = 16
+    s, d, w = synth.rmat(scale, 16)
+    V = 1 << scale
+    g = G(V, weighted=True, hashing=hashing, degree_hints=synth.degrees(s, V))
+    o = oracle.OracleGraph(V)
+    assert g.insert(cuda(s), cuda(d), cuda(w)) == o.insert(s, d, w)[1]
+    assert g.check()[0] == 0
+    for r in range(4):
+        fs, fd, fw = synth.rmat_draws(scale, 200000, r * 200000, 11)
+        assert g.insert(cuda(fs), cuda(fd), cuda(fw)) == o.insert(fs, fd, fw)[1]
+        assert g.check()[0] == 0, g.check()
+        pick = synth.sample_distinct(len(s), 100000, 100 + r)
+        assert g.delete(cuda(s[pick]), cuda(d[pick])) == o.delete(s[pick], d[pick])[1]
+        assert g.check()[0] == 0, g.check()
+    assert_same_edges(g, o)
