@@ -400,9 +400,9 @@ __global__ void __launch_bounds__(UPD_BLOCK) k_export(GraphDev G, uint64_t n_sla
 // ------------------------------------------------------------------ construction
 
 __global__ void k_bucket_counts(const uint32_t* __restrict__ hints, uint32_t V, double lf_cap, int hashing,
-                                uint32_t* __restrict__ count, uint64_t* __restrict__ heads,
+                                uint32_t cap, uint32_t* __restrict__ count, uint64_t* __restrict__ heads,
                                 unsigned long long* __restrict__ total) {
-  unsigned long long mine = 0;
+  unsigned long long mine = 0, full = 0;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t trips = (V + stride - 1) / stride;
   for (uint64_t t = 0; t < trips; t++) {
@@ -417,9 +417,14 @@ __global__ void k_bucket_counts(const uint32_t* __restrict__ hints, uint32_t V, 
     count[v] = c;
     heads[v] = hint > 0 ? c : 0;   // hint 0: no arena head, allocated lazily on first insert (C22b)
     mine += c;
+    full += (hint + cap - 1) / cap;   // slabs the hinted degree fills at 100% occupancy
   }
-  for (int o = 16; o; o >>= 1) mine += __shfl_down_sync(0xFFFFFFFFu, mine, o);
+  for (int o = 16; o; o >>= 1) {
+    mine += __shfl_down_sync(0xFFFFFFFFu, mine, o);
+    full += __shfl_down_sync(0xFFFFFFFFu, full, o);
+  }
   if ((threadIdx.x & 31) == 0 && mine) atomicAdd(total, mine);
+  if ((threadIdx.x & 31) == 0 && full) atomicAdd(total + 1, full);
 }
 
 __global__ void k_init_meta(GraphDev G, const uint32_t* __restrict__ count, const uint64_t* __restrict__ first,
@@ -486,10 +491,13 @@ __global__ void k_fsck(GraphDev G, unsigned long long* info) {
 
 // ------------------------------------------------------------------ host launchers
 
-static inline unsigned grid_for(meerkat_graph* g, uint64_t groups) {
+// One work item per group up to `per_group_cap` waves of resident blocks: blocks retire
+// independently, so a block held up by a contended slab list (hub rows of an R-MAT batch)
+// does not make the rest of the GPU wait at a grid-wide tail.
+static inline unsigned grid_for(meerkat_graph* g, uint64_t groups, uint64_t waves = 64) {
   const uint64_t per_block = UPD_BLOCK / GROUP;
   uint64_t b = (groups + per_block - 1) / per_block;
-  const uint64_t cap = (uint64_t)g->sm_count * 8;   // 8 resident 256-thread blocks per SM
+  const uint64_t cap = (uint64_t)g->sm_count * 8 * waves;   // 8 resident 256-thread blocks per SM
   if (b > cap) b = cap;
   return (unsigned)(b ? b : 1);
 }
@@ -505,13 +513,13 @@ cudaError_t launch_build(meerkat_graph* g, Store& st, const uint32_t* d_hints, u
 #define CK(x) do { e = (x); if (e != cudaSuccess) goto out; } while (0)
   CK(cudaMalloc(&count, (size_t)V * 4));
   CK(cudaMalloc(&heads, (size_t)V * 8));
-  CK(cudaMalloc(&first, ((size_t)V + 2) * 8));
+  CK(cudaMalloc(&first, ((size_t)V + 3) * 8));
   {
     const unsigned gb = (unsigned)std::min<uint64_t>((V + 255) / 256, (uint64_t)g->sm_count * 16);
     unsigned long long* total = reinterpret_cast<unsigned long long*>(first + V + 1);
-    CK(cudaMemsetAsync(total, 0, 8, g->stream));
-    k_bucket_counts<<<gb, 256, 0, g->stream>>>(d_hints, V, (double)g->lf * cap, g->hashing ? 1 : 0, count, heads,
-                                               total);
+    CK(cudaMemsetAsync(total, 0, 16, g->stream));
+    k_bucket_counts<<<gb, 256, 0, g->stream>>>(d_hints, V, (double)g->lf * cap, g->hashing ? 1 : 0, (uint32_t)cap,
+                                               count, heads, total);
     g->launches++;
     CK(cudaGetLastError());
     CK(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, heads, first + 1, V, g->stream));
@@ -519,14 +527,18 @@ cudaError_t launch_build(meerkat_graph* g, Store& st, const uint32_t* d_hints, u
     CK(cudaMemsetAsync(first, 0, 8, g->stream));
     CK(cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, heads, first + 1, V, g->stream));   // first = exclusive scan
     g->launches++;
-    uint64_t HB[2] = {0, 0};
-    CK(cudaMemcpyAsync(HB, first + V, 16, cudaMemcpyDeviceToHost, g->stream));
+    uint64_t HB[3] = {0, 0, 0};
+    CK(cudaMemcpyAsync(HB, first + V, 24, cudaMemcpyDeviceToHost, g->stream));
     CK(cudaStreamSynchronize(g->stream));
     const uint64_t H = HB[0];
     st.buckets = HB[1];
+    const uint64_t full = HB[2];
     // total slab lists = arena heads + one lazy head per hint-0 vertex
     st.H = H;
-    st.P = pool_request ? pool_request : H / 2 + V / 2 + 65536;
+    // automatic pool: chains for the hinted degrees beyond the heads (x2: chains are partly empty),
+    // plus room to grow by half the arena, lazy heads for an eighth of the vertices, and a floor
+    const uint64_t overflow = full > H ? full - H : 0;
+    st.P = pool_request ? pool_request : 2 * overflow + H / 2 + V / 8 + 65536;
     if (st.H + st.P >= 0xFFFFFFF0ull) { e = cudaErrorInvalidValue; goto out; }
     const size_t nslab = (size_t)(st.H + st.P);
     CK(cudaMalloc(&st.dev.slabs, nslab * 128));             // ONE allocation: head arena + pool
@@ -604,7 +616,7 @@ cudaError_t launch_export(meerkat_graph* g, Store& st, uint32_t* s, uint32_t* d,
   const uint64_t used = std::min<uint64_t>(st.hctrl->pool_top, st.P);
   const uint64_t n_slabs = st.H + used;
   if (!n_slabs) return cudaSuccess;
-  const unsigned gb = grid_for(g, n_slabs);
+  const unsigned gb = grid_for(g, n_slabs, 1);
   if (g->weighted) k_export<true><<<gb, UPD_BLOCK, 0, g->stream>>>(st.dev, n_slabs, s, d, w, cap);
   else k_export<false><<<gb, UPD_BLOCK, 0, g->stream>>>(st.dev, n_slabs, s, d, w, cap);
   g->launches++;
