@@ -14,6 +14,7 @@
 //    CAS ("chained at the end of the last filled slab").  A present key
 //    keeps the minimum weight via a 64-bit atomicMin on the <key, w> pair (C8).
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include <cub/cub.cuh>
@@ -22,7 +23,8 @@
 
 namespace mk {
 
-constexpr uint32_t WATCHDOG = 1u << 16;   // loop bound that turns a would-be hang into MEERKAT_E_STATE
+constexpr uint32_t WATCHDOG = 1u << 20;   // loop bounds that turn a would-be hang into MEERKAT_E_STATE
+constexpr uint32_t WALK_LIMIT = 1u << 26;  // slabs walked by one operation (a chain longer than any pool)
 
 // ------------------------------------------------------------------ helpers
 
@@ -115,7 +117,7 @@ __device__ int group_insert(const GraphDev& G, uint32_t u, uint32_t v, uint32_t 
     head = nxt;
   }
   uint32_t cur = head + bucket_of(v, count, G.seed);
-  uint32_t guard = 0;
+  uint32_t guard = 0, walk = 0;
   for (;;) {
     if (++guard == WATCHDOG) {
       if (l8 == 0) {
@@ -167,7 +169,7 @@ __device__ int group_insert(const GraphDev& G, uint32_t u, uint32_t v, uint32_t 
       const bool has_empty = ((__ballot_sync(gmask, eb != 0) >> gbase) & 0xFFu) != 0;
       const uint32_t nxt = __shfl_sync(gmask, d.w, GROUP - 1, GROUP);
       if (has_empty || nxt == INVALID_SLAB || nxt == LINKING) { tail = s; break; }
-      if (++guard == WATCHDOG || nxt >= G.H + G.P) {
+      if (++walk == WALK_LIMIT || nxt >= G.H + G.P) {
         if (l8 == 0) {
           printf("meerkat watchdog: insert walk u=%u v=%u s=%u nxt=%u\n", u, v, s, nxt);
           atomicOr(&G.ctrl->err, (unsigned)ERR_STATE);
@@ -287,7 +289,7 @@ __device__ int group_find(const GraphDev& G, uint32_t u, uint32_t v, int l8, uin
     const bool has_empty = ((__ballot_sync(gmask, eb != 0) >> gbase) & 0xFFu) != 0;
     const uint32_t nxt = __shfl_sync(gmask, d.w, GROUP - 1, GROUP);
     if (has_empty || nxt == INVALID_SLAB) return -1;
-    if (++guard == WATCHDOG || nxt >= G.H + G.P) {
+    if (++guard == WALK_LIMIT || nxt >= G.H + G.P) {
       if (l8 == 0) {
         printf("meerkat watchdog: find walk u=%u v=%u s=%u nxt=%u\n", u, v, s, nxt);
         atomicOr(&G.ctrl->err, (unsigned)ERR_STATE);
@@ -494,7 +496,14 @@ __global__ void k_fsck(GraphDev G, unsigned long long* info) {
 // One work item per group up to `per_group_cap` waves of resident blocks: blocks retire
 // independently, so a block held up by a contended slab list (hub rows of an R-MAT batch)
 // does not make the rest of the GPU wait at a grid-wide tail.
-static inline unsigned grid_for(meerkat_graph* g, uint64_t groups, uint64_t waves = 64) {
+static uint64_t g_upd_waves = 0;   // MEERKAT_UPD_WAVES (experiments); 0 = default
+
+static inline unsigned grid_for(meerkat_graph* g, uint64_t groups, uint64_t waves = 1) {
+  if (waves != 1 && g_upd_waves == 0) {
+    const char* e = std::getenv("MEERKAT_UPD_WAVES");
+    g_upd_waves = e ? std::strtoull(e, nullptr, 10) : 1;
+  }
+  if (waves != 1) waves = g_upd_waves ? g_upd_waves : 1;
   const uint64_t per_block = UPD_BLOCK / GROUP;
   uint64_t b = (groups + per_block - 1) / per_block;
   const uint64_t cap = (uint64_t)g->sm_count * 8 * waves;   // 8 resident 256-thread blocks per SM
@@ -569,7 +578,7 @@ out:
 
 cudaError_t launch_insert(meerkat_graph* g, Store& st, const uint32_t* s, const uint32_t* d, const uint32_t* w, uint64_t n) {
   if (!n) return cudaSuccess;
-  const unsigned gb = grid_for(g, n);
+  const unsigned gb = grid_for(g, n, 0);
   if (g->weighted) k_insert<true><<<gb, UPD_BLOCK, 0, g->stream>>>(st.dev, s, d, w, n);
   else k_insert<false><<<gb, UPD_BLOCK, 0, g->stream>>>(st.dev, s, d, nullptr, n);
   g->launches++;
@@ -578,7 +587,7 @@ cudaError_t launch_insert(meerkat_graph* g, Store& st, const uint32_t* s, const 
 
 cudaError_t launch_delete(meerkat_graph* g, Store& st, const uint32_t* s, const uint32_t* d, uint64_t n) {
   if (!n) return cudaSuccess;
-  const unsigned gb = grid_for(g, n);
+  const unsigned gb = grid_for(g, n, 0);
   if (g->weighted) k_delete<true><<<gb, UPD_BLOCK, 0, g->stream>>>(st.dev, s, d, n);
   else k_delete<false><<<gb, UPD_BLOCK, 0, g->stream>>>(st.dev, s, d, n);
   g->launches++;
@@ -588,7 +597,7 @@ cudaError_t launch_delete(meerkat_graph* g, Store& st, const uint32_t* s, const 
 cudaError_t launch_query(meerkat_graph* g, Store& st, const uint32_t* s, const uint32_t* d, uint64_t n, uint8_t* found,
                          uint32_t* w_out) {
   if (!n) return cudaSuccess;
-  const unsigned gb = grid_for(g, n);
+  const unsigned gb = grid_for(g, n, 0);
   if (g->weighted) k_query<true><<<gb, UPD_BLOCK, 0, g->stream>>>(st.dev, s, d, n, found, w_out);
   else k_query<false><<<gb, UPD_BLOCK, 0, g->stream>>>(st.dev, s, d, n, found, w_out);
   g->launches++;
@@ -616,7 +625,7 @@ cudaError_t launch_export(meerkat_graph* g, Store& st, uint32_t* s, uint32_t* d,
   const uint64_t used = std::min<uint64_t>(st.hctrl->pool_top, st.P);
   const uint64_t n_slabs = st.H + used;
   if (!n_slabs) return cudaSuccess;
-  const unsigned gb = grid_for(g, n_slabs, 1);
+  const unsigned gb = grid_for(g, n_slabs);
   if (g->weighted) k_export<true><<<gb, UPD_BLOCK, 0, g->stream>>>(st.dev, n_slabs, s, d, w, cap);
   else k_export<false><<<gb, UPD_BLOCK, 0, g->stream>>>(st.dev, n_slabs, s, d, w, cap);
   g->launches++;
