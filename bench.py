@@ -106,58 +106,73 @@ def allreduce_max(x, ws):
 
 # ------------------------------------------------------------------ clocks
 
+_SAMPLER = r"""
+import sys, time, pynvml
+pynvml.nvmlInit()
+h = pynvml.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+print("max", pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM), flush=True)
+while True:
+    try:
+        print(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+              pynvml.nvmlDeviceGetCurrentClocksEventReasons(h), flush=True)
+    except Exception:
+        pass
+    time.sleep(0.002)
+"""
+
+
 class ClockSampler:
-    """SM clock and clock-event (throttle) reasons sampled every 5 ms via NVML during the timed region."""
+    """SM clock and clock-event (throttle) reasons sampled every ~2 ms via NVML by a separate
+    process (no GIL contention with the timed loop) during the timed region."""
     REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap",
                0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, device):
-        self.device = device
-        self.rows = []
-        self.stop_flag = threading.Event()
-        self.h = None
+        idx = device
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:
+            try:
+                idx = int(vis.split(",")[device])
+            except (ValueError, IndexError):
+                pass
+        self.idx = idx
+        self.proc = None
+        self.lines = []
 
     def start(self):
+        import subprocess
         try:
-            import pynvml
-            pynvml.nvmlInit()
-            idx = self.device
-            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
-            if vis:
-                try:
-                    idx = int(vis.split(",")[self.device])
-                except ValueError:
-                    pass
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
-            self.nv = pynvml
-            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
-        except Exception as e:  # pragma: no cover
-            self.err = str(e)
-            self.h = None
-            return
-        self.t = threading.Thread(target=self._run, daemon=True)
-        self.t.start()
-
-    def _run(self):
-        nv = self.nv
-        while not self.stop_flag.is_set():
-            try:
-                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
-                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                self.rows.append((sm, rs))
-            except Exception:
-                pass
-            time.sleep(0.005)
+            self.proc = subprocess.Popen([sys.executable, "-c", _SAMPLER, str(self.idx)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=lambda: self.lines.extend(self.proc.stdout), daemon=True)
+            self.t.start()
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 20:   # wait until sampling runs
+                time.sleep(0.01)
+        except Exception:
+            self.proc = None
 
     def stop(self):
-        if self.h is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
-        self.stop_flag.set()
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml sampler unavailable"]}
+        time.sleep(0.01)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
         self.t.join(timeout=2)
-        sm = [r[0] for r in self.rows]
-        reasons = sorted({name for _, rs in self.rows for bit, name in self.REASONS.items() if rs & bit})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": self.max_sm, "reasons": reasons,
-                "samples": len(self.rows)}
+        mx, sm, reasons = None, [], set()
+        for ln in self.lines:
+            p = ln.split()
+            if p and p[0] == "max":
+                mx = int(p[1])
+            elif len(p) == 2:
+                sm.append(int(p[0]))
+                rs = int(p[1])
+                reasons |= {n for bit, n in self.REASONS.items() if rs & bit}
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
 
 
 # ------------------------------------------------------------------ workload
