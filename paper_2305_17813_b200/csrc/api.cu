@@ -152,7 +152,6 @@ meerkat_status meerkat_create(const meerkat_config* cfg, meerkat_graph** out) {
   }
   if (e == cudaSuccess) e = tree_occupancy(g);
   if (const char* s = std::getenv("MEERKAT_LATENCY_BLOCKS_PER_SM")) g->latency_bps = std::atoi(s);
-  if (const char* s = std::getenv("MEERKAT_ASYNC")) g->async_rounds = std::atoi(s) != 0;
   if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
   if (e != cudaSuccess) {
     cudaGetLastError();
@@ -356,13 +355,6 @@ static meerkat_status tree_create(meerkat_graph* g, uint32_t source, bool unit, 
   if (e == cudaSuccess) e = cudaMalloc(&T.inval_list, V * 4);
   if (e == cudaSuccess) e = cudaMalloc(&T.fr[0], T.fr_cap * 8);
   if (e == cudaSuccess) e = cudaMalloc(&T.fr[1], T.fr_cap * 8);
-  // asynchronous queue: >= 4 x #slab lists slots (at most one queued item per slab list), 1 bit per slab
-  T.ring_cap = std::max<uint64_t>(4 * T.fr_cap, 1 << 20);
-  const size_t nslabs = (size_t)(g->out.H + g->out.P), bwords = (nslabs + 31) / 32;
-  if (e == cudaSuccess && !dist) e = cudaMalloc(&T.ring, T.ring_cap * 8);
-  if (e == cudaSuccess && !dist) e = cudaMemsetAsync(T.ring, 0xFF, T.ring_cap * 8, g->stream);
-  if (e == cudaSuccess && !dist) e = cudaMalloc(&T.bflag, bwords * 4);
-  if (e == cudaSuccess && !dist) e = cudaMemsetAsync(T.bflag, 0, bwords * 4, g->stream);
   if (e == cudaSuccess) e = cudaMalloc(&t->ctrl_base, 2 * sizeof(TreeCtrl));   // double-buffered (tree.cu)
   if (e == cudaSuccess) e = cudaMemsetAsync(t->ctrl_base, 0, 2 * sizeof(TreeCtrl), g->stream);
   T.ctrl = t->ctrl_base;
@@ -376,8 +368,7 @@ static meerkat_status tree_create(meerkat_graph* g, uint32_t source, bool unit, 
     e = cudaMemcpyAsync(T.epoch_ptr, &one, 4, cudaMemcpyHostToDevice, g->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
   }
-  t->bytes = V * 8 + V * 4 + words * 4 + V * 4 + 2 * T.fr_cap * 8 + 2 * sizeof(TreeCtrl) + 4 +
-             (dist ? 0 : T.ring_cap * 8 + bwords * 4);
+  t->bytes = V * 8 + V * 4 + words * 4 + V * 4 + 2 * T.fr_cap * 8 + 2 * sizeof(TreeCtrl) + 4;
   if (e != cudaSuccess) {
     cudaGetLastError();
     meerkat_tree_destroy(t);
@@ -538,7 +529,6 @@ meerkat_status meerkat_tree_destroy(meerkat_tree* t) {
   TreeDev& T = t->dev;
   cudaFree(T.node); cudaFree(T.stamp); cudaFree(T.inval_bits); cudaFree(T.inval_list);
   cudaFree(T.fr[0]); cudaFree(T.fr[1]); cudaFree(t->ctrl_base); cudaFree(T.epoch_ptr);
-  cudaFree(T.ring); cudaFree(T.bflag);
   if (t->hctrl) cudaFreeHost(t->hctrl);
   dtree_free(t);
   delete t;

@@ -23,8 +23,6 @@ struct TreeCtrl {
   unsigned long long visited;       // live edges visited by expansion (one node[x] probe each)
   unsigned long long batch_edges;   // batch edges examined by the prologue
   unsigned long long pull_n;        // (invalid vertex, in-bucket) items of the reverse-store frontier
-  unsigned long long aq[2][4];      // async queue per phase (0 propagate, 1 relax): tickets handed out,
-                                    // slots reserved, items produced and not yet finished, -
   unsigned long long nts;           // device timeline: %globaltimer at kernel start and after every grid barrier
   unsigned long long tstamp[48];
 };
@@ -39,10 +37,6 @@ struct TreeDev {
   uint32_t* epoch_ptr;   // device-resident stamp epoch base, advanced by each call
   uint64_t fr_cap;       // items per frontier buffer (= number of slab lists)
   uint32_t source;
-  // asynchronous work queue (incremental / decremental calls, tree.cu "async rounds")
-  uint64_t* ring;        // item slots, EMPTY (all ones) when free; never wraps within a phase
-  uint64_t ring_cap;
-  uint32_t* bflag;       // one bit per slab: set while a (head slab, vertex) item is queued
 };
 
 }  // namespace mk
@@ -75,7 +69,6 @@ struct meerkat_graph {
   size_t stage_bytes[4] = {0, 0, 0, 0};
   int tree_blocks_per_sm[3] = {0, 0, 0};   // cooperative occupancy: static, incremental, decremental
   int latency_bps = 0;                      // blocks/SM for latency-bound tree calls (0 = occupancy)
-  bool async_rounds = true;                 // incremental / decremental on the asynchronous queue
   unsigned long long* rscratch = nullptr;   // meerkat_route: device counts + cursors
   unsigned long long* hrscratch = nullptr;  // pinned counts
 };

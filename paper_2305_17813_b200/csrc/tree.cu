@@ -49,9 +49,9 @@ __device__ __forceinline__ bool fetch_item(const uint64_t* fr, uint64_t n, uint6
 // Expand the frontier items [0, n) of `fr` (one 8-lane group per item), applying
 // VISIT to every live edge; successful vertices go to `fnext`.  The first slab of
 // an item and d(v) are loaded together (independent requests).
-template <bool MAP, int VISIT, class Sink>
-__device__ __forceinline__ void expand(const TreeArgs& A, const uint64_t* fr, uint64_t n, const Sink& sink,
-                                       uint32_t epoch_next, Counters& c) {
+template <bool MAP, int VISIT>
+__device__ __forceinline__ void expand(const TreeArgs& A, const uint64_t* fr, uint64_t n, uint64_t* fnext,
+                                       unsigned long long* sznext, uint32_t epoch_next, Counters& c) {
   using F = Frag<MAP>;
   constexpr int NK = F::NK;
   const GraphDev& G = A.G;
@@ -89,7 +89,7 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const uint64_t* fr, ui
         c.visited++;
         if (VISIT == RELAX) {
           const uint32_t w = A.unit ? 1u : F::weight(d, k);
-          enq = relax(T, x, (uint64_t)du + w, v, epoch_next, c, probe, Sink::stamped);
+          enq = relax(T, x, (uint64_t)du + w, v, epoch_next, c, probe);
         } else if (VISIT == PULL) {
           // in-edge (x -> v) of invalid v: a valid->invalid frontier edge iff x is valid and reached
           // (C15); relax v from it
@@ -98,7 +98,7 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const uint64_t* fr, ui
             if (nx != UNREACHED) {
               c.hits++;
               const uint32_t w = A.unit ? 1u : F::weight(d, k);
-              enq = relax(T, v, (nx >> 32) + w, x, epoch_next, c, false, Sink::stamped);
+              enq = relax(T, v, (nx >> 32) + w, x, epoch_next, c, false);
             }
           }
         } else {
@@ -113,115 +113,12 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const uint64_t* fr, ui
           }
         }
       }
-      sink.push(G, T, enq, VISIT == PULL ? v : x, c);
+      warp_enqueue(G, T, fnext, sznext, enq, VISIT == PULL ? v : x, c);
     }
     const uint32_t nxt = __shfl_sync(FULL, d.w, (lane & 24) + GROUP - 1);
     if (active) {
       if (nxt != INVALID_SLAB && !dead) slab = nxt;
       else { it += ng; active = fetch_item(fr, n, it, v, slab, l8, c); fresh = active; }
-    }
-  }
-}
-
-// Asynchronous rounds: every group takes items from the phase's queue as they are produced
-// (ticket = position in the ring) and expands them; no grid barrier separates "rounds", so a
-// chain of improvements advances at the latency of one expansion per hop.  Packed atomicMin
-// makes the order irrelevant to the result.  Groups leave when their ticket is
-// beyond every reserved slot and nothing is pending.
-template <bool MAP, int VISIT>
-__device__ __forceinline__ void async_loop(const TreeArgs& A, unsigned long long* aq, Counters& c) {
-  using F = Frag<MAP>;
-  constexpr int NK = F::NK;
-  const GraphDev& G = A.G;
-  const TreeDev& T = A.T;
-  const AsyncSink sink{aq};
-  const int lane = lane_id(), l8 = lane & 7;
-  const uint32_t gmask = 0xFFu << (lane & 24);
-  int state = 0;   // 0 needs a ticket, 1 waits on its ticket, 2 expands an item, 3 done
-  unsigned long long ticket = 0;
-  uint32_t v = 0, slab = 0, du = 0;
-  bool fresh = false;
-  for (;;) {
-    if (state == 0) {
-      if (l8 == 0) ticket = atomicAdd(&aq[0], 1ull);
-      ticket = __shfl_sync(gmask, ticket, 0, GROUP);
-      state = 1;
-    }
-    if (state == 1) {
-      unsigned long long item = EMPTY_ITEM;
-      int st = 1;
-      if (l8 == 0) {
-        if (ticket < *reinterpret_cast<volatile unsigned long long*>(&aq[1])) {
-          item = *reinterpret_cast<volatile unsigned long long*>(T.ring + ticket);
-          if (item != EMPTY_ITEM) {
-            T.ring[ticket] = EMPTY_ITEM;                       // slot free again for the next phase
-            const uint32_t s = (uint32_t)(item >> 32);
-            atomicAnd(T.bflag + (s >> 5), ~(1u << (s & 31)));  // later improvements re-enqueue
-            __threadfence();                                   // ... before d(v) is read
-            st = 2;
-          }
-        } else if (*reinterpret_cast<volatile unsigned long long*>(&aq[2]) == 0) {
-          st = 3;
-        }
-      }
-      st = __shfl_sync(gmask, st, 0, GROUP);
-      item = __shfl_sync(gmask, item, 0, GROUP);
-      if (st == 2) {
-        v = (uint32_t)item;
-        slab = (uint32_t)(item >> 32);
-        fresh = true;
-        if (l8 == 0) c.items++;
-      }
-      state = st;
-    }
-    if (!__any_sync(FULL, state != 3)) break;
-    const bool active = state == 2;
-    if (!__any_sync(FULL, active)) { __nanosleep(64); continue; }
-    uint4 d = make_uint4(EMPTY_KEY, EMPTY_KEY, EMPTY_KEY, INVALID_SLAB);
-    uint64_t nv = 0;
-    if (active) {
-      d = ld_slab_ro(slab_ptr(G, slab), l8);
-      if (VISIT == RELAX && fresh && l8 == 0) nv = ld_cg_u64(T.node + v);
-      if (l8 == 0) c.slabs++;
-    }
-    if (VISIT == RELAX) nv = __shfl_sync(FULL, nv, lane & 24);
-    bool dead = false;
-    if (VISIT == RELAX && active && fresh) {
-      dead = nv == UNREACHED;
-      du = (uint32_t)(nv >> 32);
-    }
-    fresh = false;
-    const bool use = active && !dead;
-#pragma unroll
-    for (int k = 0; k < NK; k++) {
-      const uint32_t x = F::key(d, k);
-      const bool live = use && F::valid_cell(l8, k) && x != EMPTY_KEY && x != TOMBSTONE_KEY;
-      bool enq = false;
-      if (live) {
-        c.visited++;
-        if (VISIT == RELAX) {
-          const uint32_t w = A.unit ? 1u : F::weight(d, k);
-          enq = relax(T, x, (uint64_t)du + w, v, 0, c, false, false);
-        } else {
-          const uint64_t cur = ld_cg_u64(T.node + x);
-          if (cur != UNREACHED && (uint32_t)cur == v && x != T.source &&
-              atomicCAS(reinterpret_cast<unsigned long long*>(T.node + x), (unsigned long long)cur,
-                        (unsigned long long)UNREACHED) == cur) {
-            mark_invalid(T, x);
-            enq = true;
-          }
-        }
-      }
-      sink.push(G, T, enq, x, c);
-    }
-    const uint32_t nxt = __shfl_sync(FULL, d.w, (lane & 24) + GROUP - 1);
-    if (active) {
-      if (nxt != INVALID_SLAB && !dead) slab = nxt;
-      else {
-        if (l8 == 0) atomicAdd(&aq[2], ~0ull);   // item finished (after everything it produced)
-        __syncwarp(gmask);
-        state = 0;
-      }
     }
   }
 }
@@ -237,7 +134,7 @@ __device__ __forceinline__ uint32_t run_rounds(const TreeArgs& A, uint32_t epoch
     const uint64_t n = __ldcg(&tc->size[r % 3]);
     if (n == 0) break;
     if (blockIdx.x == 0 && threadIdx.x == 0) tc->size[(r + 2) % 3] = 0;
-    expand<MAP, VISIT>(A, A.T.fr[r & 1], n, RoundSink{A.T.fr[(r + 1) & 1], &tc->size[(r + 1) % 3]}, epoch + r + 1, c);
+    expand<MAP, VISIT>(A, A.T.fr[r & 1], n, A.T.fr[(r + 1) & 1], &tc->size[(r + 1) % 3], epoch + r + 1, c);
     grid.sync();
     timeline(A.T.ctrl);
     r++;
@@ -294,17 +191,14 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_inc(const __grid_constan
       const bool ok = u < A.G.V && v < A.G.V && (A.unit || (w != 0 && w < W_LIMIT));   // skipped at insert too
       if (ok) {
         const uint64_t nu = ld_cg_u64(A.T.node + u);
-        if (nu != UNREACHED) enq = relax(A.T, v, (nu >> 32) + w, u, epoch, c, false, !A.async);
+        if (nu != UNREACHED) enq = relax(A.T, v, (nu >> 32) + w, u, epoch, c, false);
       }
     }
-    if (A.async) async_enqueue(A.G, A.T, A.T.ctrl->aq[1], enq, v, c);
-    else warp_enqueue(A.G, A.T, A.T.fr[0], &A.T.ctrl->size[0], enq, v, c);
+    warp_enqueue(A.G, A.T, A.T.fr[0], &A.T.ctrl->size[0], enq, v, c);
   }
   grid.sync();
     timeline(A.T.ctrl);
-  uint32_t r = 0;
-  if (A.async) async_loop<MAP, RELAX>(A, A.T.ctrl->aq[1], c);
-  else r = run_rounds<MAP, RELAX>(A, epoch, grid, 0, c);
+  const uint32_t r = run_rounds<MAP, RELAX>(A, epoch, grid, 0, c);
   if (tid == 0) *A.T.epoch_ptr = epoch + r + 2;
   flush_counters(A.G, A.T, c, tid == 0, r, 0);
   clear_next_ctrl(A.clear_ctrl);
@@ -318,9 +212,10 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_inc(const __grid_constan
 // flight); owner[] names the source vertex.  Fast path per key: one shared-memory
 // filter probe.  Slow path (warp-uniform, only for positions where some lane hit
 // the filter): exact bit-set test, source validity, relaxation and enqueue.
-template <bool MAP, class Sink>
+template <bool MAP>
 __device__ __forceinline__ void dec_scan(const TreeArgs& A, const uint32_t* filt, uint32_t fwords, uint32_t n_slabs,
-                                         const Sink& sink, uint32_t epoch_next, Counters& c) {
+                                         uint64_t* fnext, unsigned long long* sznext, uint32_t epoch_next,
+                                         Counters& c) {
   using F = Frag<MAP>;
   constexpr int NK = F::NK;
   constexpr int U = SCAN_UNROLL;
@@ -374,11 +269,11 @@ __device__ __forceinline__ void dec_scan(const TreeArgs& A, const uint32_t* filt
             if (nu != UNREACHED) {
               c.hits++;
               const uint32_t w = A.unit ? 1u : F::weight(d[q], k);
-              enq = relax(T, x, (nu >> 32) + w, u, epoch_next, c, true, Sink::stamped);
+              enq = relax(T, x, (nu >> 32) + w, u, epoch_next, c);
             }
           }
         }
-        sink.push(G, T, enq, x, c);
+        warp_enqueue(G, T, fnext, sznext, enq, x, c);
       }
     }
   }
@@ -414,20 +309,12 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_dec(const __grid_constan
         }
       }
     }
-    if (A.async) async_enqueue(A.G, A.T, tc->aq[0], enq, v, c);
-    else warp_enqueue(A.G, A.T, A.T.fr[0], &tc->size[0], enq, v, c);
+    warp_enqueue(A.G, A.T, A.T.fr[0], &tc->size[0], enq, v, c);
   }
   grid.sync();
     timeline(A.T.ctrl);
   // (ii) PropagateInvalidation to all of T_v
-  uint32_t r1 = 0;
-  if (A.async) {
-    async_loop<MAP, PROPAGATE>(A, tc->aq[0], c);
-    grid.sync();   // V_invalid is final before the frontier is built
-    timeline(A.T.ctrl);
-  } else {
-    r1 = run_rounds<MAP, PROPAGATE>(A, epoch, grid, 0, c);
-  }
+  const uint32_t r1 = run_rounds<MAP, PROPAGATE>(A, epoch, grid, 0, c);
   // (iii) valid -> invalid frontier, fused with the first relaxation
   const uint64_t n_inv = __ldcg(&tc->inval_n);
   if (n_inv && A.R.slabs) {
@@ -441,8 +328,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_dec(const __grid_constan
     }
     grid.sync();
     timeline(A.T.ctrl);
-    if (A.async) expand<MAP, PULL>(A, pull, __ldcg(&tc->pull_n), AsyncSink{tc->aq[1]}, epoch + r1, c);
-    else expand<MAP, PULL>(A, pull, __ldcg(&tc->pull_n), RoundSink{A.T.fr[r1 & 1], &tc->size[r1 % 3]}, epoch + r1, c);
+    expand<MAP, PULL>(A, pull, __ldcg(&tc->pull_n), A.T.fr[r1 & 1], &tc->size[r1 % 3], epoch + r1, c);
   } else if (n_inv) {
     // filter only while sparse enough: two bits per member, bit load <= 1/4 (false positives <= ~6%)
     const uint32_t fw = (A.filter_words && n_inv * 8 <= (uint64_t)A.filter_words * 32) ? A.filter_words : 0u;
@@ -458,15 +344,12 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_dec(const __grid_constan
     }
     const uint32_t n_slabs = A.G.H + (uint32_t)min((unsigned long long)A.G.P, __ldcg(&A.G.ctrl->pool_top));
     if (tid == 0) c.scan_slabs = n_slabs;
-    if (A.async) dec_scan<MAP>(A, filt, fw, n_slabs, AsyncSink{tc->aq[1]}, epoch + r1, c);
-    else dec_scan<MAP>(A, filt, fw, n_slabs, RoundSink{A.T.fr[r1 & 1], &tc->size[r1 % 3]}, epoch + r1, c);
+    dec_scan<MAP>(A, filt, fw, n_slabs, A.T.fr[r1 & 1], &tc->size[r1 % 3], epoch + r1, c);
   }
   grid.sync();
     timeline(A.T.ctrl);
   // (iv) common epilogue
-  uint32_t r2 = r1;
-  if (A.async) async_loop<MAP, RELAX>(A, tc->aq[1], c);
-  else r2 = run_rounds<MAP, RELAX>(A, epoch, grid, r1, c);
+  const uint32_t r2 = run_rounds<MAP, RELAX>(A, epoch, grid, r1, c);
   // clear the invalid bit set for the next call (the list is kept for meerkat_tree_invalidated)
   for (uint64_t i = tid; i < n_inv; i += nt) {
     const uint32_t x = A.T.inval_list[i];
@@ -514,7 +397,6 @@ cudaError_t launch_tree(meerkat_graph* g, meerkat_tree* t, int mode, const uint3
   A.unit = t->unit ? 1u : 0u;
   A.weighted = g->weighted ? 1u : 0u;
   A.filter_words = g->reverse ? 0u : FILTER_WORDS;
-  A.async = g->async_rounds ? 1u : 0u;
   // control blocks alternate between calls: this call's was zeroed by the previous kernel
   A.T.ctrl = t->ctrl_base + t->parity;
   A.clear_ctrl = t->ctrl_base + (1 - t->parity);

@@ -32,7 +32,6 @@ struct TreeArgs {
   uint32_t weighted;    // graph has weights (map store)
   uint32_t filter_words;
   TreeCtrl* clear_ctrl; // the other control block: zeroed at kernel end for the next call (no memset launch)
-  uint32_t async;       // 1: incremental / decremental work runs on the asynchronous queue (no round barriers)
 };
 
 // Zero the next call's control block (block 0, after the last grid barrier).
@@ -111,111 +110,16 @@ __device__ __forceinline__ void mark_invalid(const TreeDev& T, uint32_t x) {
 // probe: read node[x] first and skip the atomic when it cannot win (node values only
 // decrease, so a stale read can only cost a spare atomic) — saves atomics on large
 // frontiers, costs one round trip on small ones.
-// stamped = false (async queue): return "improved" and let the queue's per-bucket flags de-duplicate.
 __device__ __forceinline__ bool relax(const TreeDev& T, uint32_t x, uint64_t dist, uint32_t parent,
-                                      uint32_t epoch_next, Counters& c, bool probe = true, bool stamped = true) {
+                                      uint32_t epoch_next, Counters& c, bool probe = true) {
   if (dist >= INF_DIST) { c.err |= ERR_OVERFLOW; return false; }   // C5
   const uint64_t cand = (dist << 32) | parent;
   if (probe && cand >= ld_cg_u64(T.node + x)) return false;
   const unsigned long long old = atomicMin(reinterpret_cast<unsigned long long*>(T.node + x), cand);
   if (cand >= old) return false;
   c.improved++;
-  if (!stamped) return true;
   return atomicExch(T.stamp + x, epoch_next) != epoch_next;
 }
-
-// ---- asynchronous work queue ------------------------------------------------------------
-// Items are (head slab of a bucket << 32) | vertex.  A bucket's bit in T.bflag is set while an
-// item for it is queued (set by the producer, cleared by the consumer before it reads d(v)), so
-// at most one item per slab list is outstanding and the ring (>= 4 x #slab lists) cannot fill.
-// aq_pending counts produced-but-unfinished items; a producer adds its items before finishing
-// its own, so aq_pending == 0 with no ticket served means quiescence (the fixpoint is reached).
-constexpr uint64_t EMPTY_ITEM = ~0ull;
-
-// warp-collective: lanes with `has` enqueue every bucket of vertex x whose bit was clear
-__device__ __forceinline__ void async_enqueue(const GraphDev& G, const TreeDev& T, unsigned long long* aq,
-                                              bool has, uint32_t x, Counters& c) {
-  if (!__ballot_sync(FULL, has)) return;
-  const int lane = lane_id();
-  uint32_t head = 0, cnt = 0;
-  if (has) {
-    const uint2 m = __ldcg(G.vmeta + x);
-    head = m.x;
-    cnt = m.x == INVALID_SLAB ? 0u : m.y;
-  }
-  // small vertices: each lane claims its own buckets' bits
-  uint32_t mine = 0;
-  if (cnt <= 8) {
-    for (uint32_t j = 0; j < cnt; j++) {
-      const uint32_t s = head + j;
-      if (!(atomicOr(T.bflag + (s >> 5), 1u << (s & 31)) & (1u << (s & 31)))) mine |= 1u << j;
-    }
-  }
-  const uint32_t k = __popc(mine);
-  uint32_t incl = k;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(FULL, incl, o);
-    if (lane >= o) incl += y;
-  }
-  const uint32_t total = __shfl_sync(FULL, incl, 31);
-  if (total) {
-    unsigned long long base = 0;
-    if (lane == 31) {
-      atomicAdd(&aq[2], (unsigned long long)total);
-      base = atomicAdd(&aq[1], (unsigned long long)total);
-    }
-    base = __shfl_sync(FULL, base, 31);
-    if (base + total > T.ring_cap) c.err |= ERR_CAPACITY;
-    else {
-      uint64_t p = base + incl - k;
-      for (uint32_t m = mine; m; m &= m - 1) {
-        const uint32_t j = __ffs(m) - 1;
-        T.ring[p++] = ((uint64_t)(head + j) << 32) | x;
-      }
-    }
-  }
-  // hubs: the whole warp claims and writes their buckets, 32 at a time
-  uint32_t big = __ballot_sync(FULL, cnt > 8);
-  while (big) {
-    const int l = __ffs(big) - 1;
-    big &= big - 1;
-    const uint32_t xb = __shfl_sync(FULL, x, l);
-    const uint32_t hb = __shfl_sync(FULL, head, l);
-    const uint32_t cb = __shfl_sync(FULL, cnt, l);
-    for (uint32_t j0 = 0; j0 < cb; j0 += 32) {
-      const uint32_t j = j0 + lane, s = hb + j;
-      const bool got = j < cb && !(atomicOr(T.bflag + (s >> 5), 1u << (s & 31)) & (1u << (s & 31)));
-      const uint32_t bm = __ballot_sync(FULL, got);
-      if (!bm) continue;
-      unsigned long long base = 0;
-      if (lane == 0) {
-        atomicAdd(&aq[2], (unsigned long long)__popc(bm));
-        base = atomicAdd(&aq[1], (unsigned long long)__popc(bm));
-      }
-      base = __shfl_sync(FULL, base, 0);
-      if (base + __popc(bm) > T.ring_cap) { c.err |= ERR_CAPACITY; continue; }
-      if (got) T.ring[base + __popc(bm & ((1u << lane) - 1))] = ((uint64_t)s << 32) | xb;
-    }
-  }
-}
-
-// Where expansion results go: the next round's frontier (round mode) or the async queue.
-struct RoundSink {
-  uint64_t* fr;
-  unsigned long long* sz;
-  static constexpr bool stamped = true;
-  __device__ __forceinline__ void push(const GraphDev& G, const TreeDev& T, bool has, uint32_t x, Counters& c) const {
-    warp_enqueue(G, T, fr, sz, has, x, c);
-  }
-};
-struct AsyncSink {
-  unsigned long long* aq;   // {tickets, reserved, pending} of the phase's queue
-  static constexpr bool stamped = false;
-  __device__ __forceinline__ void push(const GraphDev& G, const TreeDev& T, bool has, uint32_t x, Counters& c) const {
-    async_enqueue(G, T, aq, has, x, c);
-  }
-};
 
 // Counter flush at kernel end: warp reduce -> shared-memory block reduce -> one global
 // atomic per counter per block (a warp-level flush put ~5K same-address atomics per
