@@ -228,15 +228,24 @@ __device__ __forceinline__ void dec_scan(const TreeArgs& A, const uint32_t* filt
   const uint32_t span = ng * U;
   const uint32_t trips = (n_slabs + span - 1) / span;   // warp-uniform
   const uint4* __restrict__ base = reinterpret_cast<const uint4*>(G.slabs) + l8;
+  // register double buffering: the next trip's U slabs are requested before this trip's keys are
+  // tested, so every group always has loads in flight
+  uint4 nd[U];
+  auto load_trip = [&](uint32_t t, uint4 (&dst)[U]) {
+#pragma unroll
+    for (int q = 0; q < U; q++) {
+      const uint32_t s = t * span + g0 + q * ng;
+      dst[q] = make_uint4(EMPTY_KEY, EMPTY_KEY, EMPTY_KEY, INVALID_SLAB);
+      if (s < n_slabs) dst[q] = ld_slab_ro(reinterpret_cast<const uint32_t*>(base + (size_t)s * 8), 0);
+    }
+  };
+  if (trips) load_trip(0, nd);
   for (uint32_t t = 0; t < trips; t++) {
     const uint32_t s0 = t * span + g0;
     uint4 d[U];
 #pragma unroll
-    for (int q = 0; q < U; q++) {
-      const uint32_t s = s0 + q * ng;
-      d[q] = make_uint4(EMPTY_KEY, EMPTY_KEY, EMPTY_KEY, INVALID_SLAB);
-      if (s < n_slabs) d[q] = ld_slab_ro(reinterpret_cast<const uint32_t*>(base + (size_t)s * 8), 0);
-    }
+    for (int q = 0; q < U; q++) d[q] = nd[q];
+    if (t + 1 < trips) load_trip(t + 1, nd);
     uint32_t hm = 0;
 #pragma unroll
     for (int q = 0; q < U; q++) {

@@ -11,7 +11,7 @@ namespace mk {
 
 constexpr int TREE_BLOCK = 512;
 constexpr int FILTER_WORDS = 24576;   // 96 KiB smem Bloom filter per block (decremental scan), 2 blocks/SM
-constexpr int SCAN_UNROLL = 4;        // independent slabs in flight per group in the scan
+constexpr int SCAN_UNROLL = 2;        // independent slabs in flight per group in the scan
 constexpr unsigned FULL = 0xFFFFFFFFu;
 constexpr uint64_t PROBE_MIN_ITEMS = 65536;
 constexpr int LOCAL_STACK = 16;              // items per group's shared-memory stack

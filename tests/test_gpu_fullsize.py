@@ -69,3 +69,37 @@ def test_config3_fullsize_certified(workload, reverse):
     assert np.array_equal(f.cpu().numpy(), ef) and np.array_equal(qw.cpu().numpy().view(np.uint32), eww)
     assert g.check()[0] == 0
     g.close()
+
+
+def test_config4_mixed_batches_certified():
+    """BASELINE config 4: power-law R-MAT scale 22, edge factor 24 (~97 M edges, 'LJ/Orkut-shaped'),
+    dynamic SSSP + BFS under mixed batches: each round deletes 1% of E then inserts 1% held-out edges
+    (SURVEY §8(c) C25); two rounds here, every tree certified by the oracle after every batch."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2305_17813_b200 import Graph
+    n1 = 970_000
+    W = synth.rmat_dynamic(22, 24, batch=n1, n_ins=2, n_del=2)
+    V, src = W.vertex_n, W.source
+    bs, bd, bw = W.base
+    o = oracle.OracleGraph(V)
+    o.insert(bs, bd, bw)
+    g = Graph(V, weighted=True, degree_hints=cuda(np.bincount(bs, minlength=V).astype(np.uint32)), reverse=True,
+              in_degree_hints=cuda(np.bincount(bd, minlength=V).astype(np.uint32)))
+    assert g.insert(cuda(bs), cuda(bd), cuda(bw)) == o.num_edges
+    t, b = g.sssp(src), g.bfs(src)
+    for r in range(2):
+        s, d, _ = W.deletes[r]
+        assert g.delete(cuda(s), cuda(d)) == o.delete(s, d)[1]
+        t.decremental(cuda(s), cuda(d))
+        b.decremental(cuda(s), cuda(d))
+        assert o.check_tree(src, t.nodes(), False) == (0, 0xFFFFFFFF)
+        assert o.check_tree(src, b.nodes(), True) == (0, 0xFFFFFFFF)
+        s, d, w = W.inserts[r]
+        assert g.insert(cuda(s), cuda(d), cuda(w)) == o.insert(s, d, w)[1]
+        t.incremental(cuda(s), cuda(d), cuda(w))
+        b.incremental(cuda(s), cuda(d))
+        assert o.check_tree(src, t.nodes(), False) == (0, 0xFFFFFFFF)
+        assert o.check_tree(src, b.nodes(), True) == (0, 0xFFFFFFFF)
+    assert g.check()[0] == 0 and g.stats()["edges"] == o.num_edges
+    g.close()
