@@ -171,6 +171,14 @@ meerkat_status meerkat_sssp_decremental(meerkat_graph* g, meerkat_tree* t, const
                                         const uint32_t* dst, uint64_t n);
 meerkat_status meerkat_bfs_decremental(meerkat_graph* g, meerkat_tree* t, const uint32_t* src,
                                        const uint32_t* dst, uint64_t n);
+/* Fused update of up to 2 trees of g (e.g. an SSSP and a BFS tree) with the batch just applied:
+ * one launch; the trees share every frontier round's grid barrier and, for a decremental batch
+ * without an in-edge mirror, ONE stream over the slab array serves all of them.  Same results as
+ * the per-tree calls.  w: the batch's weights (needed iff some tree is an SSSP tree). */
+meerkat_status meerkat_trees_incremental(meerkat_graph* g, meerkat_tree* const* trees, uint32_t n_trees,
+                                         const uint32_t* src, const uint32_t* dst, const uint32_t* w, uint64_t n);
+meerkat_status meerkat_trees_decremental(meerkat_graph* g, meerkat_tree* const* trees, uint32_t n_trees,
+                                         const uint32_t* src, const uint32_t* dst, uint64_t n);
 /* Static re-run on the current graph (the s_b^n baseline). */
 meerkat_status meerkat_tree_recompute(meerkat_graph* g, meerkat_tree* t);
 /* node[v] = dist << 32 | parent for every v, UINT64_MAX when unreached (C3). */

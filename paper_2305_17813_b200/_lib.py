@@ -30,7 +30,7 @@ EXPORTS = [
     "meerkat_bfs_incremental", "meerkat_sssp_decremental", "meerkat_bfs_decremental", "meerkat_tree_recompute",
     "meerkat_tree_nodes", "meerkat_tree_invalidated", "meerkat_tree_stats_get", "meerkat_tree_destroy",
     "meerkat_dtree_create", "meerkat_dtree_phase", "meerkat_memcpy", "meerkat_route", "meerkat_tree_timeline",
-    "meerkat_check",
+    "meerkat_check", "meerkat_trees_incremental", "meerkat_trees_decremental",
 ]
 
 
@@ -112,6 +112,8 @@ def lib():
         "meerkat_tree_destroy": (ctypes.c_int, [vp]),
         "meerkat_tree_timeline": (ctypes.c_int, [vp, pu64, u64, pu64]),
         "meerkat_check": (ctypes.c_int, [vp, pu64]),
+        "meerkat_trees_incremental": (ctypes.c_int, [vp, pvp, u32, vp, vp, vp, u64]),
+        "meerkat_trees_decremental": (ctypes.c_int, [vp, pvp, u32, vp, vp, u64]),
         "meerkat_dtree_create": (ctypes.c_int, [vp, u32, u32, pvp]),
         "meerkat_dtree_phase": (ctypes.c_int, [vp, vp, ctypes.c_int, vp, vp, vp, u64, ctypes.POINTER(DResult)]),
         "meerkat_memcpy": (ctypes.c_int, [vp, vp, vp, u64]),

@@ -378,7 +378,7 @@ static meerkat_status tree_create(meerkat_graph* g, uint32_t source, bool unit, 
     const meerkat_status st = dtree_init(g, t);
     if (st != MEERKAT_OK) { meerkat_tree_destroy(t); return st; }
   } else {
-    e = launch_tree(g, t, MODE_STATIC, nullptr, nullptr, nullptr, 0);
+    e = launch_tree(g, &t, 1, MODE_STATIC, nullptr, nullptr, nullptr, 0);
     if (e != cudaSuccess) {
       cudaGetLastError();
       meerkat_tree_destroy(t);
@@ -398,25 +398,50 @@ meerkat_status meerkat_bfs_create(meerkat_graph* g, uint32_t source, meerkat_tre
   return tree_create(g, source, true, false, out);
 }
 
-static meerkat_status tree_update(meerkat_graph* g, meerkat_tree* t, bool unit, int kind, const uint32_t* src,
-                                  const uint32_t* dst, const uint32_t* w, uint64_t n) {
+// Mutation-following update of one or more trees of g with the same batch (fused launch).
+static meerkat_status trees_update(meerkat_graph* g, meerkat_tree* const* ts, uint32_t k, int kind, const uint32_t* src,
+                                   const uint32_t* dst, const uint32_t* w, uint64_t n) {
   meerkat_status st = check_batch(g, src, dst, n);
   if (st != MEERKAT_OK) return st;
-  if (!t || t->g != g || t->unit != unit || t->dist) return MEERKAT_E_INVALID_ARG;
-  // ordering contract: the batch must be the mutation just applied
-  if (g->last_kind != kind || t->version + 1 != g->version) return MEERKAT_E_STATE;
-  if (kind == 1 && !unit && n && !w) return MEERKAT_E_INVALID_ARG;
+  if (!ts || k == 0 || k > (uint32_t)MAX_TREES) return MEERKAT_E_INVALID_ARG;
+  bool need_w = false;
+  for (uint32_t i = 0; i < k; i++) {
+    meerkat_tree* t = ts[i];
+    if (!t || t->g != g || t->dist) return MEERKAT_E_INVALID_ARG;
+    for (uint32_t j = 0; j < i; j++)
+      if (ts[j] == t) return MEERKAT_E_INVALID_ARG;
+    // ordering contract: the batch must be the mutation just applied
+    if (g->last_kind != kind || t->version + 1 != g->version) return MEERKAT_E_STATE;
+    need_w |= kind == 1 && !t->unit;
+  }
+  if (need_w && n && !w) return MEERKAT_E_INVALID_ARG;
   DeviceGuard dg(g->device);
   const void *s, *d, *ww = nullptr;
   cudaError_t e = stage_in(g, 0, src, n * 4, &s);
   if (e == cudaSuccess) e = stage_in(g, 1, dst, n * 4, &d);
-  if (e == cudaSuccess && kind == 1 && !unit) e = stage_in(g, 2, w, n * 4, &ww);
+  if (e == cudaSuccess && need_w) e = stage_in(g, 2, w, n * 4, &ww);
   if (e == cudaSuccess)
-    e = launch_tree(g, t, kind == 1 ? MODE_INCREMENTAL : MODE_DECREMENTAL, (const uint32_t*)s, (const uint32_t*)d,
+    e = launch_tree(g, ts, k, kind == 1 ? MODE_INCREMENTAL : MODE_DECREMENTAL, (const uint32_t*)s, (const uint32_t*)d,
                     (const uint32_t*)ww, n);
   if (e != cudaSuccess) return MEERKAT_E_CUDA;
-  t->version = g->version;
+  for (uint32_t i = 0; i < k; i++) ts[i]->version = g->version;
   return MEERKAT_OK;
+}
+
+static meerkat_status tree_update(meerkat_graph* g, meerkat_tree* t, bool unit, int kind, const uint32_t* src,
+                                  const uint32_t* dst, const uint32_t* w, uint64_t n) {
+  if (!t || t->unit != unit) return MEERKAT_E_INVALID_ARG;
+  return trees_update(g, &t, 1, kind, src, dst, unit ? nullptr : w, n);
+}
+
+meerkat_status meerkat_trees_incremental(meerkat_graph* g, meerkat_tree* const* trees, uint32_t n_trees,
+                                         const uint32_t* src, const uint32_t* dst, const uint32_t* w, uint64_t n) {
+  return trees_update(g, trees, n_trees, 1, src, dst, w, n);
+}
+
+meerkat_status meerkat_trees_decremental(meerkat_graph* g, meerkat_tree* const* trees, uint32_t n_trees,
+                                         const uint32_t* src, const uint32_t* dst, uint64_t n) {
+  return trees_update(g, trees, n_trees, 2, src, dst, nullptr, n);
 }
 
 meerkat_status meerkat_sssp_incremental(meerkat_graph* g, meerkat_tree* t, const uint32_t* src, const uint32_t* dst,
@@ -442,7 +467,7 @@ meerkat_status meerkat_bfs_decremental(meerkat_graph* g, meerkat_tree* t, const 
 meerkat_status meerkat_tree_recompute(meerkat_graph* g, meerkat_tree* t) {
   if (!g || !t || t->g != g || t->dist) return MEERKAT_E_INVALID_ARG;
   DeviceGuard dg(g->device);
-  cudaError_t e = launch_tree(g, t, MODE_STATIC, nullptr, nullptr, nullptr, 0);
+  cudaError_t e = launch_tree(g, &t, 1, MODE_STATIC, nullptr, nullptr, nullptr, 0);
   if (e != cudaSuccess) return MEERKAT_E_CUDA;
   t->version = g->version;
   return MEERKAT_OK;

@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(D_BLOCK) k_dinc_seed(DArgs A, const uint32_t* 
     warp_enqueue(A.G, A.T, A.fnext, A.sznext, enq, lv, c);
     warp_emit(A, emit, v, cand, c);
   }
-  flush_counters(A.G, A.T, c, false, 0, 0);
+  flush_counters(A.G, A.T, c, 0, false, 0, 0);
 }
 
 // Decremental Invalidate: deleted edges (u, v) with v held here.
@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(D_BLOCK) k_ddec_inval(DArgs A, const uint32_t*
     }
     warp_enqueue(A.G, A.T, A.fnext, A.sznext, enq, lv, c);
   }
-  flush_counters(A.G, A.T, c, false, 0, 0);
+  flush_counters(A.G, A.T, c, 0, false, 0, 0);
 }
 
 // One round of expansion of the local frontier (P:113-133 relax, or P:149-154 propagate).
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(D_BLOCK) k_dexpand(DArgs A) {
       else { it += ng; active = fetch(); }
     }
   }
-  flush_counters(A.G, A.T, c, false, 0, 0);
+  flush_counters(A.G, A.T, c, 0, false, 0, 0);
 }
 
 // Apply received messages (x held here): relaxation candidates or invalidation requests.
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(D_BLOCK) k_dapply(DArgs A, const uint64_t* in,
     }
     warp_enqueue(A.G, A.T, A.fnext, A.sznext, enq, lx, c);
   }
-  flush_counters(A.G, A.T, c, false, 0, 0);
+  flush_counters(A.G, A.T, c, 0, false, 0, 0);
 }
 
 // Set / clear the marks of ALL ranks' invalid vertices (global bit set).
@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_dscan(DArgs A, const uint32_t
           if (ul != NO_OWNER && !bit_test(T.inval_bits, ug)) {
             const uint64_t nu = ld_cg_u64(T.node + ul);
             if (nu != UNREACHED) {
-              c.hits++;
+              c.hits[0]++;
               const uint64_t dist = (nu >> 32) + (A.unit ? 1u : F::weight(d[q], k));
               if (dist >= INF_DIST) c.err |= ERR_OVERFLOW;
               else if (owned(G, x)) { lx = lrow(G, x); enq = relax(T, lx, dist, ug, A.epoch, c); }
@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_dscan(DArgs A, const uint32_t
       }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) c.scan_slabs = n_slabs;
-  flush_counters(A.G, A.T, c, false, 0, 0);
+  flush_counters(A.G, A.T, c, 0, false, 0, 0);
 }
 
 // ---- group messages by owner rank: histogram, exclusive scan, scatter

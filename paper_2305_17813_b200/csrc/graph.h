@@ -9,6 +9,8 @@
 
 namespace mk {
 
+constexpr int MAX_TREES = 2;   // trees updated together by one fused call (e.g. SSSP + BFS)
+
 struct TreeCtrl {
   unsigned long long size[3];       // rotating frontier sizes (see tree.cu, "round protocol")
   unsigned long long inval_n;       // |V_invalid| of this call
@@ -37,6 +39,7 @@ struct TreeDev {
   uint32_t* epoch_ptr;   // device-resident stamp epoch base, advanced by each call
   uint64_t fr_cap;       // items per frontier buffer (= number of slab lists)
   uint32_t source;
+  uint32_t unit;         // 1: BFS (every w = 1)
 };
 
 }  // namespace mk
@@ -108,8 +111,8 @@ cudaError_t launch_fsck(meerkat_graph* g, Store& st, unsigned long long* info_de
 // tree.cu
 cudaError_t tree_occupancy(meerkat_graph* g);
 enum TreeMode { MODE_STATIC = 0, MODE_INCREMENTAL = 1, MODE_DECREMENTAL = 2 };
-cudaError_t launch_tree(meerkat_graph* g, meerkat_tree* t, int mode, const uint32_t* s, const uint32_t* d,
-                        const uint32_t* w, uint64_t n);
+cudaError_t launch_tree(meerkat_graph* g, meerkat_tree* const* trees, uint32_t ntrees, int mode, const uint32_t* s,
+                        const uint32_t* d, const uint32_t* w, uint64_t n);
 // dtree.cu
 meerkat_status dtree_phase(meerkat_graph* g, meerkat_tree* t, int phase, const void* a, const void* b,
                            const void* c, uint64_t n, meerkat_dresult* out);

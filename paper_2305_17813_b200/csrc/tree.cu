@@ -25,7 +25,11 @@
 //    (arena + pool, owner[] gives each slab's source vertex) instead of chasing
 //    chains, tests each destination against a shared-memory hashed filter of the
 //    invalid set, and relaxes hits directly — a pure HBM stream;
-//  * rounds are separated by grid-wide barriers inside one launch.
+//  * rounds are separated by grid-wide barriers inside one launch;
+//  * FUSED trees: up to MAX_TREES trees of the same graph (an SSSP and a BFS tree,
+//    say) are updated by one launch for the same batch — their frontier rounds share
+//    the grid barriers, and the decremental scan streams the slab array ONCE for all
+//    of them (one shared-memory filter per tree).
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -46,17 +50,17 @@ __device__ __forceinline__ bool fetch_item(const uint64_t* fr, uint64_t n, uint6
   return true;
 }
 
-// Expand the frontier items [0, n) of `fr` (one 8-lane group per item), applying
-// VISIT to every live edge; successful vertices go to `fnext`.  The first slab of
-// an item and d(v) are loaded together (independent requests).
+// Expand the frontier items [0, n) of `fr` (one 8-lane group per item) for tree T (index k),
+// applying VISIT to every live edge; successful vertices go to (fnext, sznext).  The first slab
+// of an item and d(v) are loaded together (independent requests).
 template <bool MAP, int VISIT>
-__device__ __forceinline__ void expand(const TreeArgs& A, const uint64_t* fr, uint64_t n, uint64_t* fnext,
-                                       unsigned long long* sznext, uint32_t epoch_next, Counters& c) {
+__device__ __forceinline__ void expand(const TreeArgs& A, const TreeDev& T, int k, const uint64_t* fr, uint64_t n,
+                                       uint64_t* fnext, unsigned long long* sznext, uint32_t epoch_next,
+                                       Counters& c) {
   using F = Frag<MAP>;
   constexpr int NK = F::NK;
   const GraphDev& G = A.G;
   const GraphDev& S = VISIT == PULL ? A.R : A.G;   // store whose slab lists are walked
-  const TreeDev& T = A.T;
   const int lane = lane_id(), l8 = lane & 7;
   const uint64_t ng = ((uint64_t)gridDim.x * blockDim.x) / GROUP;
   const bool probe = n > PROBE_MIN_ITEMS;
@@ -81,14 +85,14 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const uint64_t* fr, ui
     fresh = false;
     const bool use = active && !dead;
 #pragma unroll
-    for (int k = 0; k < NK; k++) {
-      const uint32_t x = F::key(d, k);
-      const bool live = use && F::valid_cell(l8, k) && x != EMPTY_KEY && x != TOMBSTONE_KEY;
+    for (int kk = 0; kk < NK; kk++) {
+      const uint32_t x = F::key(d, kk);
+      const bool live = use && F::valid_cell(l8, kk) && x != EMPTY_KEY && x != TOMBSTONE_KEY;
       bool enq = false;
       if (live) {
         c.visited++;
         if (VISIT == RELAX) {
-          const uint32_t w = A.unit ? 1u : F::weight(d, k);
+          const uint32_t w = T.unit ? 1u : F::weight(d, kk);
           enq = relax(T, x, (uint64_t)du + w, v, epoch_next, c, probe);
         } else if (VISIT == PULL) {
           // in-edge (x -> v) of invalid v: a valid->invalid frontier edge iff x is valid and reached
@@ -96,8 +100,8 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const uint64_t* fr, ui
           if (!bit_test(T.inval_bits, x)) {
             const uint64_t nx = ld_cg_u64(T.node + x);
             if (nx != UNREACHED) {
-              c.hits++;
-              const uint32_t w = A.unit ? 1u : F::weight(d, k);
+              c.hits[k]++;
+              const uint32_t w = T.unit ? 1u : F::weight(d, kk);
               enq = relax(T, v, (nx >> 32) + w, x, epoch_next, c, false);
             }
           }
@@ -123,104 +127,127 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const uint64_t* fr, ui
   }
 }
 
-// Frontier rounds until empty.  Round r reads fr[r&1] / size[r%3], writes
-// fr[(r+1)&1] / size[(r+1)%3]; size[(r+2)%3] (consumed two rounds ago) is
-// zeroed during round r so it is clean when it becomes "next".
+// Frontier rounds of all trees of the call, until every frontier is empty.  Round r reads
+// fr[r&1] / size[r%3] of each tree and writes fr[(r+1)&1] / size[(r+1)%3]; size[(r+2)%3]
+// (consumed two rounds ago) is zeroed during round r so it is clean when it becomes "next".
+// The trees share the grid barrier of every round.
 template <bool MAP, int VISIT>
-__device__ __forceinline__ uint32_t run_rounds(const TreeArgs& A, uint32_t epoch, cg::grid_group& grid, uint32_t r,
-                                               Counters& c) {
-  TreeCtrl* tc = A.T.ctrl;
+__device__ __forceinline__ uint32_t run_rounds(const TreeArgs& A, const uint32_t* epoch, cg::grid_group& grid,
+                                               uint32_t r, Counters& c) {
   for (;;) {
-    const uint64_t n = __ldcg(&tc->size[r % 3]);
-    if (n == 0) break;
-    if (blockIdx.x == 0 && threadIdx.x == 0) tc->size[(r + 2) % 3] = 0;
-    expand<MAP, VISIT>(A, A.T.fr[r & 1], n, A.T.fr[(r + 1) & 1], &tc->size[(r + 1) % 3], epoch + r + 1, c);
+    uint64_t n[MAX_TREES];
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < MAX_TREES; k++) {
+      n[k] = k < (int)A.ntrees ? __ldcg(&A.T[k].ctrl->size[r % 3]) : 0;
+      any |= n[k] != 0;
+    }
+    if (!any) break;
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+      for (uint32_t k = 0; k < A.ntrees; k++) A.T[k].ctrl->size[(r + 2) % 3] = 0;
+#pragma unroll
+    for (int k = 0; k < MAX_TREES; k++) {
+      if (!n[k]) continue;
+      const TreeDev& T = A.T[k];
+      expand<MAP, VISIT>(A, T, k, T.fr[r & 1], n[k], T.fr[(r + 1) & 1], &T.ctrl->size[(r + 1) % 3],
+                         epoch[k] + r + 1, c);
+    }
     grid.sync();
-    timeline(A.T.ctrl);
+    timeline(A.T[0].ctrl);
     r++;
   }
   return r;
+}
+
+__device__ __forceinline__ void finish(const TreeArgs& A, Counters& c, const uint32_t* epoch, bool owner,
+                                       uint32_t rounds_total, uint32_t relax_rounds, uint32_t prop_rounds) {
+  for (uint32_t k = 0; k < A.ntrees; k++) {
+    if (owner) *A.T[k].epoch_ptr = epoch[k] + rounds_total + 2;   // every thread read the base before a barrier
+    flush_counters(A.G, A.T[k], c, k, owner, relax_rounds, prop_rounds);
+    clear_next_ctrl(A.clear_ctrl[k]);
+  }
+  timeline(A.T[0].ctrl);
 }
 
 // ------------------------------------------------------------------ static
 
 template <bool MAP>
 __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_static(const __grid_constant__ TreeArgs A) {
-  const uint32_t epoch = __ldcg(A.T.epoch_ptr);
-  timeline(A.T.ctrl);
+  const TreeDev& T = A.T[0];
+  const uint32_t epoch[MAX_TREES] = {__ldcg(T.epoch_ptr)};
+  timeline(T.ctrl);
   cg::grid_group grid = cg::this_grid();
   Counters c;
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
   // init: every node <INF, INVALID>, SRC <0, SRC>
-  for (uint64_t v = tid; v < A.G.V; v += nt) A.T.node[v] = (v == A.T.source) ? (uint64_t)A.T.source : UNREACHED;
+  for (uint64_t v = tid; v < A.G.V; v += nt) T.node[v] = (v == T.source) ? (uint64_t)T.source : UNREACHED;
   grid.sync();
-    timeline(A.T.ctrl);
   if (blockIdx.x == 0 && threadIdx.x < 32) {
     const bool has = threadIdx.x == 0;
-    if (has) A.T.stamp[A.T.source] = epoch;
-    warp_enqueue(A.G, A.T, A.T.fr[0], &A.T.ctrl->size[0], has, A.T.source, c);   // frontier from SRC (C16)
+    if (has) T.stamp[T.source] = epoch[0];
+    warp_enqueue(A.G, T, T.fr[0], &T.ctrl->size[0], has, T.source, c);   // frontier from SRC (C16)
   }
   grid.sync();
-    timeline(A.T.ctrl);
+  timeline(T.ctrl);
   const uint32_t r = run_rounds<MAP, RELAX>(A, epoch, grid, 0, c);
-  if (tid == 0) *A.T.epoch_ptr = epoch + r + 2;   // every thread read the base before the first grid.sync
-  flush_counters(A.G, A.T, c, tid == 0, r, 0);
-  clear_next_ctrl(A.clear_ctrl);
-  timeline(A.T.ctrl);
+  finish(A, c, epoch, tid == 0, r, r, 0);
 }
 
 // ------------------------------------------------------------------ incremental
 
 template <bool MAP>
 __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_inc(const __grid_constant__ TreeArgs A) {
-  const uint32_t epoch = __ldcg(A.T.epoch_ptr);
-  timeline(A.T.ctrl);
+  uint32_t epoch[MAX_TREES] = {};
+  for (uint32_t k = 0; k < A.ntrees; k++) epoch[k] = __ldcg(A.T[k].epoch_ptr);
+  timeline(A.T[0].ctrl);
   cg::grid_group grid = cg::this_grid();
   Counters c;
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t trips = (A.bn + nt - 1) / nt;   // warp-uniform trip count (warp_enqueue is collective)
   for (uint64_t t = 0; t < trips; t++) {
     const uint64_t i = tid + t * nt;
-    bool enq = false;
-    uint32_t v = 0;
+    uint32_t u = 0, v = 0, w = 0;
+    bool ok = false;
     if (i < A.bn) {
-      const uint32_t u = A.bs[i];
+      u = A.bs[i];
       v = A.bd[i];
-      const uint32_t w = A.unit ? 1u : A.bw[i];
+      w = A.bw ? A.bw[i] : 1u;
       c.batch++;
-      const bool ok = u < A.G.V && v < A.G.V && (A.unit || (w != 0 && w < W_LIMIT));   // skipped at insert too
-      if (ok) {
-        const uint64_t nu = ld_cg_u64(A.T.node + u);
-        if (nu != UNREACHED) enq = relax(A.T, v, (nu >> 32) + w, u, epoch, c, false);
-      }
+      ok = u < A.G.V && v < A.G.V;   // invalid edges were skipped at insert too
     }
-    warp_enqueue(A.G, A.T, A.T.fr[0], &A.T.ctrl->size[0], enq, v, c);
+#pragma unroll
+    for (int k = 0; k < MAX_TREES; k++) {
+      if (k >= (int)A.ntrees) break;
+      const TreeDev& T = A.T[k];
+      const uint32_t wk = T.unit ? 1u : w;
+      bool enq = false;
+      if (ok && (T.unit || (wk != 0 && wk < W_LIMIT))) {
+        const uint64_t nu = ld_cg_u64(T.node + u);
+        if (nu != UNREACHED) enq = relax(T, v, (nu >> 32) + wk, u, epoch[k], c, false);
+      }
+      warp_enqueue(A.G, T, T.fr[0], &T.ctrl->size[0], enq, v, c);
+    }
   }
   grid.sync();
-    timeline(A.T.ctrl);
+  timeline(A.T[0].ctrl);
   const uint32_t r = run_rounds<MAP, RELAX>(A, epoch, grid, 0, c);
-  if (tid == 0) *A.T.epoch_ptr = epoch + r + 2;
-  flush_counters(A.G, A.T, c, tid == 0, r, 0);
-  clear_next_ctrl(A.clear_ctrl);
-  timeline(A.T.ctrl);
+  finish(A, c, epoch, tid == 0, r, r, 0);
 }
 
 // ------------------------------------------------------------------ decremental
 
-// Valid->invalid frontier (C15) as a STREAM over the slab array
-// [0, n_slabs): each 8-lane group reads whole slabs (LDG.128 per lane, U slabs in
-// flight); owner[] names the source vertex.  Fast path per key: one shared-memory
-// filter probe.  Slow path (warp-uniform, only for positions where some lane hit
-// the filter): exact bit-set test, source validity, relaxation and enqueue.
+// Valid->invalid frontier (C15) of every tree of the call as ONE STREAM over the
+// slab array [0, n_slabs): each 8-lane group reads whole slabs (LDG.128 per lane, register
+// double-buffered so loads are always in flight); owner[] names the source vertex.  Fast path
+// per key and tree: one shared-memory filter probe.  Slow path (warp-uniform, only for positions
+// where some lane hit a filter): exact bit-set test, source validity, relaxation and enqueue.
 template <bool MAP>
-__device__ __forceinline__ void dec_scan(const TreeArgs& A, const uint32_t* filt, uint32_t fwords, uint32_t n_slabs,
-                                         uint64_t* fnext, unsigned long long* sznext, uint32_t epoch_next,
-                                         Counters& c) {
+__device__ __forceinline__ void dec_scan(const TreeArgs& A, const uint32_t* filt, const uint32_t* fwords,
+                                         uint32_t n_slabs, uint32_t r1, const uint32_t* epoch, Counters& c) {
   using F = Frag<MAP>;
   constexpr int NK = F::NK;
   constexpr int U = SCAN_UNROLL;
   const GraphDev& G = A.G;
-  const TreeDev& T = A.T;
   const uint32_t V = G.V;
   const int l8 = lane_id() & 7;
   const uint32_t ng = (gridDim.x * blockDim.x) / GROUP;
@@ -228,8 +255,6 @@ __device__ __forceinline__ void dec_scan(const TreeArgs& A, const uint32_t* filt
   const uint32_t span = ng * U;
   const uint32_t trips = (n_slabs + span - 1) / span;   // warp-uniform
   const uint4* __restrict__ base = reinterpret_cast<const uint4*>(G.slabs) + l8;
-  // register double buffering: the next trip's U slabs are requested before this trip's keys are
-  // tested, so every group always has loads in flight
   uint4 nd[U];
   auto load_trip = [&](uint32_t t, uint4 (&dst)[U]) {
 #pragma unroll
@@ -246,43 +271,49 @@ __device__ __forceinline__ void dec_scan(const TreeArgs& A, const uint32_t* filt
 #pragma unroll
     for (int q = 0; q < U; q++) d[q] = nd[q];
     if (t + 1 < trips) load_trip(t + 1, nd);
-    uint32_t hm = 0;
 #pragma unroll
-    for (int q = 0; q < U; q++) {
+    for (int k = 0; k < MAX_TREES; k++) {
+      if (k >= (int)A.ntrees) break;
+      const TreeDev& T = A.T[k];
+      const uint32_t* fk = filt + k * A.filter_words;
+      uint32_t hm = 0;
 #pragma unroll
-      for (int k = 0; k < NK; k++) {
-        const uint32_t x = F::key(d[q], k);
-        bool hit = x < V && (MAP || F::valid_cell(l8, k));   // live key (sentinels are >= V)
-        if (fwords) {
-          uint32_t w, m;
-          filter_loc(x, fwords, w, m);
-          hit = hit && (filt[w] & m) == m;
+      for (int q = 0; q < U; q++) {
+#pragma unroll
+        for (int kk = 0; kk < NK; kk++) {
+          const uint32_t x = F::key(d[q], kk);
+          bool hit = x < V && (MAP || F::valid_cell(l8, kk));   // live key (sentinels are >= V)
+          if (fwords[k]) {
+            uint32_t w, m;
+            filter_loc(x, fwords[k], w, m);
+            hit = hit && (fk[w] & m) == m;
+          }
+          hm |= (uint32_t)hit << (q * NK + kk);
         }
-        hm |= (uint32_t)hit << (q * NK + k);
       }
-    }
-    const uint32_t pos = __reduce_or_sync(FULL, hm);
-    if (!pos) continue;
+      const uint32_t pos = __reduce_or_sync(FULL, hm);
+      if (!pos) continue;
 #pragma unroll
-    for (int q = 0; q < U; q++) {
+      for (int q = 0; q < U; q++) {
 #pragma unroll
-      for (int k = 0; k < NK; k++) {
-        if (!((pos >> (q * NK + k)) & 1u)) continue;   // warp-uniform
-        const uint32_t x = F::key(d[q], k);
-        bool enq = false;
-        if (((hm >> (q * NK + k)) & 1u) && bit_test(T.inval_bits, x)) {
-          // x in V_invalid: is the slab's source vertex u valid and reached?
-          const uint32_t u = __ldg(G.owner + s0 + q * ng);
-          if (u != NO_OWNER && !bit_test(T.inval_bits, u)) {
-            const uint64_t nu = ld_cg_u64(T.node + u);
-            if (nu != UNREACHED) {
-              c.hits++;
-              const uint32_t w = A.unit ? 1u : F::weight(d[q], k);
-              enq = relax(T, x, (nu >> 32) + w, u, epoch_next, c);
+        for (int kk = 0; kk < NK; kk++) {
+          if (!((pos >> (q * NK + kk)) & 1u)) continue;   // warp-uniform
+          const uint32_t x = F::key(d[q], kk);
+          bool enq = false;
+          if (((hm >> (q * NK + kk)) & 1u) && bit_test(T.inval_bits, x)) {
+            // x in V_invalid: is the slab's source vertex u valid and reached?
+            const uint32_t u = __ldg(G.owner + s0 + q * ng);
+            if (u != NO_OWNER && !bit_test(T.inval_bits, u)) {
+              const uint64_t nu = ld_cg_u64(T.node + u);
+              if (nu != UNREACHED) {
+                c.hits[k]++;
+                const uint32_t w = T.unit ? 1u : F::weight(d[q], kk);
+                enq = relax(T, x, (nu >> 32) + w, u, epoch[k] + r1, c);
+              }
             }
           }
+          warp_enqueue(G, T, T.fr[r1 & 1], &T.ctrl->size[r1 % 3], enq, x, c);
         }
-        warp_enqueue(G, T, fnext, sznext, enq, x, c);
       }
     }
   }
@@ -291,83 +322,100 @@ __device__ __forceinline__ void dec_scan(const TreeArgs& A, const uint32_t* filt
 template <bool MAP>
 __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_dec(const __grid_constant__ TreeArgs A) {
   extern __shared__ uint32_t filt[];
-  const uint32_t epoch = __ldcg(A.T.epoch_ptr);
-  timeline(A.T.ctrl);
+  uint32_t epoch[MAX_TREES] = {};
+  for (uint32_t k = 0; k < A.ntrees; k++) epoch[k] = __ldcg(A.T[k].epoch_ptr);
+  timeline(A.T[0].ctrl);
   cg::grid_group grid = cg::this_grid();
   Counters c;
-  TreeCtrl* tc = A.T.ctrl;
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
   // (i) Invalidate: deleted tree edges (parent(v), v), v != SRC (C4)
   const uint64_t trips = (A.bn + nt - 1) / nt;
   for (uint64_t t = 0; t < trips; t++) {
     const uint64_t i = tid + t * nt;
-    bool enq = false;
-    uint32_t v = 0;
+    uint32_t u = 0, v = 0;
+    bool ok = false;
     if (i < A.bn) {
-      const uint32_t u = A.bs[i];
+      u = A.bs[i];
       v = A.bd[i];
       c.batch++;
-      if (u < A.G.V && v < A.G.V && v != A.T.source) {
-        const uint64_t cur = ld_cg_u64(A.T.node + v);
+      ok = u < A.G.V && v < A.G.V;
+    }
+#pragma unroll
+    for (int k = 0; k < MAX_TREES; k++) {
+      if (k >= (int)A.ntrees) break;
+      const TreeDev& T = A.T[k];
+      bool enq = false;
+      if (ok && v != T.source) {
+        const uint64_t cur = ld_cg_u64(T.node + v);
         if (cur != UNREACHED && (uint32_t)cur == u &&
-            atomicCAS(reinterpret_cast<unsigned long long*>(A.T.node + v), (unsigned long long)cur,
+            atomicCAS(reinterpret_cast<unsigned long long*>(T.node + v), (unsigned long long)cur,
                       (unsigned long long)UNREACHED) == cur) {
-          mark_invalid(A.T, v);
-          atomicAdd(&tc->direct_n, 1ull);
+          mark_invalid(T, v);
+          atomicAdd(&T.ctrl->direct_n, 1ull);
           enq = true;
         }
       }
+      warp_enqueue(A.G, T, T.fr[0], &T.ctrl->size[0], enq, v, c);
     }
-    warp_enqueue(A.G, A.T, A.T.fr[0], &tc->size[0], enq, v, c);
   }
   grid.sync();
-    timeline(A.T.ctrl);
+  timeline(A.T[0].ctrl);
   // (ii) PropagateInvalidation to all of T_v
   const uint32_t r1 = run_rounds<MAP, PROPAGATE>(A, epoch, grid, 0, c);
   // (iii) valid -> invalid frontier, fused with the first relaxation
-  const uint64_t n_inv = __ldcg(&tc->inval_n);
-  if (n_inv && A.R.slabs) {
+  uint64_t n_inv[MAX_TREES] = {};
+  uint64_t n_inv_all = 0;
+  for (uint32_t k = 0; k < A.ntrees; k++) { n_inv[k] = __ldcg(&A.T[k].ctrl->inval_n); n_inv_all += n_inv[k]; }
+  if (n_inv_all && A.R.slabs) {
     // in-edge mirror present: the frontier is exactly the in-edges of V_invalid from valid sources
-    uint64_t* pull = A.T.fr[(r1 + 1) & 1];
-    const uint64_t ptrips = (n_inv + nt - 1) / nt;
-    for (uint64_t t = 0; t < ptrips; t++) {
-      const uint64_t i = tid + t * nt;
-      const bool has = i < n_inv;
-      warp_enqueue(A.R, A.T, pull, &tc->pull_n, has, has ? __ldcg(A.T.inval_list + i) : 0u, c);
+    for (uint32_t k = 0; k < A.ntrees; k++) {
+      const TreeDev& T = A.T[k];
+      const uint64_t ptrips = (n_inv[k] + nt - 1) / nt;
+      for (uint64_t t = 0; t < ptrips; t++) {
+        const uint64_t i = tid + t * nt;
+        const bool has = i < n_inv[k];
+        warp_enqueue(A.R, T, T.fr[(r1 + 1) & 1], &T.ctrl->pull_n, has, has ? __ldcg(T.inval_list + i) : 0u, c);
+      }
     }
     grid.sync();
-    timeline(A.T.ctrl);
-    expand<MAP, PULL>(A, pull, __ldcg(&tc->pull_n), A.T.fr[r1 & 1], &tc->size[r1 % 3], epoch + r1, c);
-  } else if (n_inv) {
-    // filter only while sparse enough: two bits per member, bit load <= 1/4 (false positives <= ~6%)
-    const uint32_t fw = (A.filter_words && n_inv * 8 <= (uint64_t)A.filter_words * 32) ? A.filter_words : 0u;
-    if (fw) {
-      for (uint32_t i = threadIdx.x; i < fw; i += blockDim.x) filt[i] = 0;
-      __syncthreads();
-      for (uint64_t i = threadIdx.x; i < n_inv; i += blockDim.x) {
-        uint32_t w, m;
-        filter_loc(__ldcg(A.T.inval_list + i), fw, w, m);
-        atomicOr(&filt[w], m);
-      }
-      __syncthreads();
+    timeline(A.T[0].ctrl);
+    for (uint32_t k = 0; k < A.ntrees; k++) {
+      const TreeDev& T = A.T[k];
+      expand<MAP, PULL>(A, T, k, T.fr[(r1 + 1) & 1], __ldcg(&T.ctrl->pull_n), T.fr[r1 & 1], &T.ctrl->size[r1 % 3],
+                        epoch[k] + r1, c);
     }
+  } else if (n_inv_all) {
+    // one shared-memory filter per tree while sparse enough: two bits per member, bit load <= 1/4
+    uint32_t fw[MAX_TREES] = {};
+    for (uint32_t k = 0; k < A.ntrees; k++)
+      fw[k] = (A.filter_words && n_inv[k] * 8 <= (uint64_t)A.filter_words * 32) ? A.filter_words : 0u;
+    for (uint32_t k = 0; k < A.ntrees; k++) {
+      if (!fw[k]) continue;
+      uint32_t* fk = filt + k * A.filter_words;
+      for (uint32_t i = threadIdx.x; i < fw[k]; i += blockDim.x) fk[i] = 0;
+      __syncthreads();
+      for (uint64_t i = threadIdx.x; i < n_inv[k]; i += blockDim.x) {
+        uint32_t w, m;
+        filter_loc(__ldcg(A.T[k].inval_list + i), fw[k], w, m);
+        atomicOr(&fk[w], m);
+      }
+    }
+    __syncthreads();
     const uint32_t n_slabs = A.G.H + (uint32_t)min((unsigned long long)A.G.P, __ldcg(&A.G.ctrl->pool_top));
     if (tid == 0) c.scan_slabs = n_slabs;
-    dec_scan<MAP>(A, filt, fw, n_slabs, A.T.fr[r1 & 1], &tc->size[r1 % 3], epoch + r1, c);
+    dec_scan<MAP>(A, filt, fw, n_slabs, r1, epoch, c);
   }
   grid.sync();
-    timeline(A.T.ctrl);
+  timeline(A.T[0].ctrl);
   // (iv) common epilogue
   const uint32_t r2 = run_rounds<MAP, RELAX>(A, epoch, grid, r1, c);
-  // clear the invalid bit set for the next call (the list is kept for meerkat_tree_invalidated)
-  for (uint64_t i = tid; i < n_inv; i += nt) {
-    const uint32_t x = A.T.inval_list[i];
-    atomicAnd(A.T.inval_bits + (x >> 5), ~(1u << (x & 31)));
-  }
-  if (tid == 0) *A.T.epoch_ptr = epoch + r2 + 2;
-  flush_counters(A.G, A.T, c, tid == 0, r2 - r1, r1);
-  clear_next_ctrl(A.clear_ctrl);
-  timeline(A.T.ctrl);
+  // clear the invalid bit sets for the next call (the lists are kept for meerkat_tree_invalidated)
+  for (uint32_t k = 0; k < A.ntrees; k++)
+    for (uint64_t i = tid; i < n_inv[k]; i += nt) {
+      const uint32_t x = A.T[k].inval_list[i];
+      atomicAnd(A.T[k].inval_bits + (x >> 5), ~(1u << (x & 31)));
+    }
+  finish(A, c, epoch, tid == 0, r2, r2 - r1, r1);
 }
 
 // ------------------------------------------------------------------ host side
@@ -396,28 +444,31 @@ cudaError_t tree_occupancy(meerkat_graph* g) {
   return cudaSuccess;
 }
 
-cudaError_t launch_tree(meerkat_graph* g, meerkat_tree* t, int mode, const uint32_t* s, const uint32_t* d,
-                        const uint32_t* w, uint64_t n) {
+cudaError_t launch_tree(meerkat_graph* g, meerkat_tree* const* trees, uint32_t ntrees, int mode, const uint32_t* s,
+                        const uint32_t* d, const uint32_t* w, uint64_t n) {
+  if (ntrees == 0 || ntrees > (uint32_t)MAX_TREES) return cudaErrorInvalidValue;
   TreeArgs A;
   A.G = g->out.dev;
   A.R = g->reverse ? g->in.dev : GraphDev{};
-  A.T = t->dev;
+  A.ntrees = ntrees;
+  for (uint32_t k = 0; k < (uint32_t)MAX_TREES; k++) {
+    meerkat_tree* t = trees[k < ntrees ? k : 0];
+    A.T[k] = t->dev;
+    A.T[k].unit = t->unit ? 1u : 0u;
+    // control blocks alternate between calls: this call's was zeroed by the previous kernel
+    A.T[k].ctrl = t->ctrl_base + t->parity;
+    A.clear_ctrl[k] = k < ntrees ? t->ctrl_base + (1 - t->parity) : nullptr;
+  }
   A.bs = s; A.bd = d; A.bw = w; A.bn = n;
-  A.unit = t->unit ? 1u : 0u;
   A.weighted = g->weighted ? 1u : 0u;
-  A.filter_words = g->reverse ? 0u : FILTER_WORDS;
-  // control blocks alternate between calls: this call's was zeroed by the previous kernel
-  A.T.ctrl = t->ctrl_base + t->parity;
-  A.clear_ctrl = t->ctrl_base + (1 - t->parity);
-  cudaError_t e = cudaSuccess;
+  // one filter per tree in shared memory (scan only); two trees share the budget of one
+  A.filter_words = g->reverse ? 0u : FILTER_WORDS / ntrees;
   int bps = g->tree_blocks_per_sm[mode];
   if (bps <= 0) return cudaErrorInvalidConfiguration;
-  // latency-bound calls (no full-store scan) may run on fewer blocks: cheaper grid barriers
   if (g->latency_bps > 0 && mode != MODE_STATIC && !(mode == MODE_DECREMENTAL && !g->reverse))
     bps = std::min(bps, g->latency_bps);
   dim3 grid((unsigned)(bps * g->sm_count)), block(TREE_BLOCK);
   void* args[] = {&A};
-  // the shared-memory filter is only used by the full-store scan (no in-edge mirror)
   const size_t smem = (mode == MODE_DECREMENTAL && !g->reverse) ? (size_t)FILTER_WORDS * 4 : 0;
   void* fn;
   if (g->weighted)
@@ -426,11 +477,13 @@ cudaError_t launch_tree(meerkat_graph* g, meerkat_tree* t, int mode, const uint3
   else
     fn = mode == MODE_STATIC ? (void*)k_tree_static<false> : mode == MODE_INCREMENTAL ? (void*)k_tree_inc<false>
                                                                                       : (void*)k_tree_dec<false>;
-  e = cudaLaunchCooperativeKernel(fn, grid, block, args, smem, g->stream);
+  cudaError_t e = cudaLaunchCooperativeKernel(fn, grid, block, args, smem, g->stream);
   if (e != cudaSuccess) return e;
   g->launches++;
-  t->dev.ctrl = A.T.ctrl;   // stats / timeline / invalidated readers see this call's block
-  t->parity ^= 1;
+  for (uint32_t k = 0; k < ntrees; k++) {
+    trees[k]->dev.ctrl = A.T[k].ctrl;   // stats / timeline / invalidated readers see this call's block
+    trees[k]->parity ^= 1;
+  }
   return e;
 }
 

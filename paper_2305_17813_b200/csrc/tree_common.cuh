@@ -13,25 +13,22 @@ constexpr int TREE_BLOCK = 512;
 constexpr int FILTER_WORDS = 24576;   // 96 KiB smem Bloom filter per block (decremental scan), 2 blocks/SM
 constexpr int SCAN_UNROLL = 2;        // independent slabs in flight per group in the scan
 constexpr unsigned FULL = 0xFFFFFFFFu;
-constexpr uint64_t PROBE_MIN_ITEMS = 65536;
-constexpr int LOCAL_STACK = 16;              // items per group's shared-memory stack
-constexpr int LOCAL_MAX_BUCKETS = 4;         // vertices with more slab lists always go to the frontier
-constexpr uint64_t LOCAL_MAX_ITEMS = 65536;  // local stacks only for frontiers smaller than this   // frontiers at least this large probe node[x] before the atomic
+constexpr uint64_t PROBE_MIN_ITEMS = 65536;  // frontiers at least this large probe node[x] before the atomic
 
 enum Visit { RELAX = 0, PROPAGATE = 1, PULL = 2 };
 
 struct TreeArgs {
   GraphDev G;           // out-edge store
   GraphDev R;           // in-edge mirror (R.slabs == nullptr when the graph keeps none)
-  TreeDev T;
+  TreeDev T[MAX_TREES]; // the trees this call updates (same graph, same batch)
+  TreeCtrl* clear_ctrl[MAX_TREES];   // each tree's other control block: zeroed at kernel end (no memset launch)
+  uint32_t ntrees;
   const uint32_t* bs;   // batch (device)
   const uint32_t* bd;
   const uint32_t* bw;
   uint64_t bn;
-  uint32_t unit;        // 1: BFS (w = 1)
   uint32_t weighted;    // graph has weights (map store)
-  uint32_t filter_words;
-  TreeCtrl* clear_ctrl; // the other control block: zeroed at kernel end for the next call (no memset launch)
+  uint32_t filter_words;   // per tree
 };
 
 // Zero the next call's control block (block 0, after the last grid barrier).
@@ -41,8 +38,10 @@ __device__ __forceinline__ void clear_next_ctrl(TreeCtrl* p) {
   for (uint32_t i = threadIdx.x; i < sizeof(TreeCtrl) / 8; i += blockDim.x) w[i] = 0;
 }
 
+// Per-thread statistics; valid->invalid frontier edges are kept per tree, the rest per call.
 struct Counters {
-  uint32_t items = 0, slabs = 0, visited = 0, improved = 0, scan_slabs = 0, hits = 0, batch = 0, err = 0;
+  uint32_t items = 0, slabs = 0, visited = 0, improved = 0, scan_slabs = 0, batch = 0, err = 0;
+  uint32_t hits[MAX_TREES] = {};
 };
 
 __device__ __forceinline__ bool bit_test(const uint32_t* bits, uint32_t x) {
@@ -124,15 +123,15 @@ __device__ __forceinline__ bool relax(const TreeDev& T, uint32_t x, uint64_t dis
 // Counter flush at kernel end: warp reduce -> shared-memory block reduce -> one global
 // atomic per counter per block (a warp-level flush put ~5K same-address atomics per
 // counter on the kernel's tail).  All threads of the block must call it.
-__device__ __forceinline__ void flush_counters(const GraphDev& G, const TreeDev& T, Counters& c, bool rounds_owner,
-                                               uint32_t relax_rounds, uint32_t prop_rounds) {
+__device__ __forceinline__ void flush_counters(const GraphDev& G, const TreeDev& T, Counters& c, int k,
+                                               bool rounds_owner, uint32_t relax_rounds, uint32_t prop_rounds) {
   __shared__ unsigned long long acc[8];
   TreeCtrl* tc = T.ctrl;
   if (threadIdx.x < 8) acc[threadIdx.x] = 0;
   __syncthreads();
   auto red = [](uint32_t v) { return __reduce_add_sync(FULL, v); };
   const uint32_t v[7] = {red(c.items), red(c.slabs), red(c.visited), red(c.improved), red(c.scan_slabs),
-                         red(c.hits), red(c.batch)};
+                         red(c.hits[k]), red(c.batch)};
   const uint32_t err = __reduce_or_sync(FULL, c.err);
   if (lane_id() == 0) {
 #pragma unroll

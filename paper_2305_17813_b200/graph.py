@@ -159,6 +159,22 @@ class Graph:
         return st.as_dict()
 
     # ------------------------------------------------------------------ trees
+    def trees_incremental(self, trees, src, dst, w=None):
+        """Fused incremental update of several trees with the batch just inserted (one launch)."""
+        sp, ks, n = _u32(src)
+        dp, kd, _ = _u32(dst)
+        wp, kw, _ = _u32(w)
+        arr = (ctypes.c_void_p * len(trees))(*[t._h.value for t in trees])
+        check(_lib.lib().meerkat_trees_incremental(self._h, arr, len(trees), sp, dp, wp, n),
+              "meerkat_trees_incremental")
+
+    def trees_decremental(self, trees, src, dst):
+        """Fused decremental update of several trees with the batch just deleted (one launch)."""
+        sp, ks, n = _u32(src)
+        dp, kd, _ = _u32(dst)
+        arr = (ctypes.c_void_p * len(trees))(*[t._h.value for t in trees])
+        check(_lib.lib().meerkat_trees_decremental(self._h, arr, len(trees), sp, dp, n), "meerkat_trees_decremental")
+
     def sssp(self, source: int) -> "Tree":
         return Tree(self, source, unit=False)
 

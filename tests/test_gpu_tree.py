@@ -232,3 +232,40 @@ def test_overflow_reported():
     with pytest.raises(MeerkatError) as e:
         g.sync()
     assert e.value.status == _lib.E_OVERFLOW
+
+
+@pytest.mark.parametrize("reverse,hashing", [(False, True), (True, True), (False, False)])
+def test_fused_trees_match_oracle(reverse, hashing):
+    """meerkat_trees_incremental / _decremental: SSSP and BFS trees updated by ONE launch (shared
+    round barriers, one slab-array stream for both) give the same nodes and intermediates."""
+    W = synth.rmat_dynamic(15, 16, batch=2000, n_ins=3, n_del=3)
+    V, src = W.vertex_n, W.source
+    bs, bd, bw = W.base
+    g = G(V, weighted=True, hashing=hashing, degree_hints=synth.degrees(bs, V), reverse=reverse,
+          in_degree_hints=synth.degrees(bd, V))
+    o = oracle.OracleGraph(V)
+    g.insert(cuda(bs), cuda(bd), cuda(bw)); o.insert(bs, bd, bw)
+    t, b = g.sssp(src), g.bfs(src)
+    for (s, d, w) in W.inserts:
+        g.insert(cuda(s), cuda(d), cuda(w)); o.insert(s, d, w)
+        g.trees_incremental([t, b], cuda(s), cuda(d), cuda(w))
+        assert_nodes(t.nodes(), o.sssp(src)[1], "fused inc sssp")
+        assert_nodes(b.nodes(), o.bfs(src)[1], "fused inc bfs")
+    for (s, d, _w) in W.deletes:
+        old_s, old_b = o.sssp(src)[1], o.bfs(src)[1]
+        g.delete(cuda(s), cuda(d)); o.delete(s, d)
+        g.trees_decremental([t, b], cuda(s), cuda(d))
+        for tree, old in ((t, old_s), (b, old_b)):
+            flag, nd = oracle.invalidated(V, src, old, s, d)
+            st = tree.stats()
+            assert tree.invalidated().tolist() == np.nonzero(flag)[0].tolist()
+            assert st["direct_invalid"] == nd
+            assert st["frontier_edges"] == o.dec_frontier_count(old, flag)
+        assert_nodes(t.nodes(), o.sssp(src)[1], "fused dec sssp")
+        assert_nodes(b.nodes(), o.bfs(src)[1], "fused dec bfs")
+    # mixing per-tree and fused calls keeps the version contract
+    s, d, w = W.inserts[0]
+    g.delete(cuda(s), cuda(d)); o.delete(s, d)
+    t.decremental(cuda(s), cuda(d))
+    b.decremental(cuda(s), cuda(d))
+    assert_nodes(t.nodes(), o.sssp(src)[1], "per-tree after fused")
