@@ -50,6 +50,10 @@ def parse():
     p.add_argument("--batch", type=int, default=100_000)
     p.add_argument("--lf", type=float, default=0.7)
     p.add_argument("--no-hashing", action="store_true")
+    p.add_argument("--fused", action=argparse.BooleanOptionalAction, default=True,
+                   help="update the SSSP and BFS trees with one fused launch per batch (meerkat_trees_*)")
+    p.add_argument("--per-tree", action=argparse.BooleanOptionalAction, default=True,
+                   help="with --fused, also time per-tree calls for the SSSP / BFS split")
     p.add_argument("--compare", action=argparse.BooleanOptionalAction, default=True,
                    help="also time the other decremental-frontier mode (reported under 'alt')")
     p.add_argument("--frontier", choices=["scan", "reverse"], default="reverse",
@@ -256,11 +260,25 @@ def build(args, W, frontier, dev, local, stream, T):
 
 
 NAMES = ["insert", "sssp_inc", "bfs_inc", "delete", "sssp_dec", "bfs_dec"]
+NAMES_FUSED = ["insert", "trees_inc", "delete", "trees_dec"]
 
 
-def one_step(g, sp, bf, ins, dels, evs, stream):
-    """The hot path over one batch pair: mutate, then update both trees."""
+def one_step(g, sp, bf, ins, dels, evs, stream, fused=False):
+    """The hot path over one batch pair: mutate, then update both trees.  fused: one
+    launch updates the SSSP and the BFS tree together (meerkat_trees_*)."""
     s, d, w = ins
+    if fused:
+        evs[0].record(stream)
+        g.insert(s, d, w, count=False)
+        evs[1].record(stream)
+        g.trees_incremental([sp, bf], s, d, w)
+        evs[2].record(stream)
+        s, d = dels
+        g.delete(s, d, count=False)
+        evs[3].record(stream)
+        g.trees_decremental([sp, bf], s, d)
+        evs[4].record(stream)
+        return
     evs[0].record(stream)
     g.insert(s, d, w, count=False)
     evs[1].record(stream)
@@ -277,20 +295,21 @@ def one_step(g, sp, bf, ins, dels, evs, stream):
     evs[6].record(stream)
 
 
-def measure(args, ws, W, frontier, dev, local, stream, T, flush, K, Wm, clocks=None):
+def measure(args, ws, W, frontier, dev, local, stream, T, flush, K, Wm, clocks=None, fused=True):
     import torch
     g, sp, bf, n_base, bulk_ms = build(args, W, frontier, dev, local, stream, T)
     ins = [tuple(T(x) for x in b) for b in W.inserts]
     dels = [tuple(T(x) for x in b[:2]) for b in W.deletes]
-    ev = lambda: [torch.cuda.Event(enable_timing=True) for _ in range(7)]
+    names = NAMES_FUSED if fused else NAMES
+    ev = lambda: [torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)]
     for i in range(Wm):
-        one_step(g, sp, bf, ins[i], dels[i], ev(), stream)
+        one_step(g, sp, bf, ins[i], dels[i], ev(), stream, fused)
         flush.zero_()
     torch.cuda.synchronize()
     g.sync()
     st0 = g.stats()
-    per_call = {n: [] for n in NAMES}
-    tstats = {"sssp_dec": [], "bfs_dec": []}
+    per_call = {n: [] for n in names}
+    tstats = {("trees_dec" if fused else "sssp_dec"): [], "bfs_dec": []}
     if clocks:
         clocks.start()
     barrier(ws)
@@ -300,13 +319,18 @@ def measure(args, ws, W, frontier, dev, local, stream, T, flush, K, Wm, clocks=N
     for k in range(K):
         i = Wm + k
         evs = ev()
-        one_step(g, sp, bf, ins[i], dels[i], evs, stream)
-        evs[6].synchronize()
-        for j, n in enumerate(NAMES):
+        one_step(g, sp, bf, ins[i], dels[i], evs, stream, fused)
+        evs[-1].synchronize()
+        for j, n in enumerate(names):
             per_call[n].append(evs[j].elapsed_time(evs[j + 1]))
-        total_ms += evs[0].elapsed_time(evs[6])
-        tstats["sssp_dec"].append(sp.stats())   # device counters of the last call, read outside the intervals
-        tstats["bfs_dec"].append(bf.stats())
+        total_ms += evs[0].elapsed_time(evs[-1])
+        s1, s2 = sp.stats(), bf.stats()   # device counters of the last call, read outside the intervals
+        if fused:   # one launch: per-call counters are shared, frontier edges (16 B each) per tree
+            s1 = dict(s1, alg_bytes=s1["alg_bytes"] + 16 * s2["frontier_edges"])
+            tstats["trees_dec"].append(s1)
+        else:
+            tstats["sssp_dec"].append(s1)
+        tstats["bfs_dec"].append(s2)
         flush.zero_()
     torch.cuda.synchronize()
     torch.cuda.nvtx.range_pop()
@@ -327,7 +351,7 @@ def measure(args, ws, W, frontier, dev, local, stream, T, flush, K, Wm, clocks=N
         static[name] = a.elapsed_time(b)
     mean = {n: float(np.mean(v)) for n, v in per_call.items()}
     res = {
-        "frontier": frontier, "K": K, "total_ms": total_ms, "ms_per_step": total_ms / K, "mean": mean,
+        "frontier": frontier, "fused": fused, "K": K, "total_ms": total_ms, "ms_per_step": total_ms / K, "mean": mean,
         "per_call": per_call, "tstats": tstats, "clocks": clk, "n_base": n_base, "bulk_ms": bulk_ms,
         "launches": int(st1["kernel_launches"] - st0["kernel_launches"]), "static_ms": static,
         "store": {k: g.stats()[k] for k in ("head_slabs", "buckets", "pool_used", "bytes_device")},
@@ -348,7 +372,8 @@ def roofline_of(res, peak, peak_src, traffic_file):
         traffic = json.load(open(traffic_file)).get(f"{res['frontier']}/{dom}")
     except Exception:
         pass
-    return {"bound": "hbm", "kernel": f"k_tree_dec ({dom}, {res['frontier']} frontier)", "achieved": ach,
+    return {"bound": "hbm", "kernel": f"k_tree_dec ({dom}, {res['frontier']} frontier{', fused SSSP+BFS' if res['fused'] else ''})",
+            "achieved": ach,
             "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": traffic, "alg_bytes_per_launch": ab,
             "peak_source": peak_src}
 
@@ -439,7 +464,7 @@ def run_ours(args, ws, rank, local):
     traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
 
     res, (g, sp, bf) = measure(args, ws, W, args.frontier, dev, local, stream, T, flush, K, Wm,
-                               clocks=ClockSampler(local))
+                               clocks=ClockSampler(local), fused=args.fused)
     edges = 2 * args.batch * K * ws
     value = edges / (res["total_ms"] / 1e3)
     mean = res["mean"]
@@ -463,12 +488,18 @@ def run_ours(args, ws, rank, local):
             a.record(stream)
             s, d, w = hi[k]
             g.insert(s, d, w, count=True)          # H2D staged inside the call, count read back (D2H)
-            sp.incremental(s, d, w)
-            bf.incremental(s, d)
+            if args.fused:
+                g.trees_incremental([sp, bf], s, d, w)
+            else:
+                sp.incremental(s, d, w)
+                bf.incremental(s, d)
             s, d = hd[k]
             g.delete(s, d, count=True)
-            sp.decremental(s, d)
-            bf.decremental(s, d)
+            if args.fused:
+                g.trees_decremental([sp, bf], s, d)
+            else:
+                sp.decremental(s, d)
+                bf.decremental(s, d)
             b.record(stream)
             b.synchronize()
             e_ms += a.elapsed_time(b)
@@ -476,17 +507,26 @@ def run_ours(args, ws, rank, local):
         e_ms = allreduce_max(e_ms, ws)
         n = args.batch
         e2e = {"value": edges / (e_ms / 1e3), "unit": "edges/s",
-               "h2d_bytes_per_step": n * 4 * (3 + 3 + 2 + 2 + 2 + 2), "d2h_bytes_per_step": 2 * 64,
+               "h2d_bytes_per_step": n * 4 * ((3 + 3 + 2 + 2) if args.fused else (3 + 3 + 2 + 2 + 2 + 2)),
+               "d2h_bytes_per_step": 2 * 64,
                "ms_per_step": e_ms / K}
     g.close()
     del g, sp, bf
     torch.cuda.empty_cache()
 
     # ---------------- the paper's own decremental frontier (full slab scan) for comparison
+    # ---------------- per-tree calls (unfused) for the SSSP / BFS split of the same step
+    per_tree = None
+    if args.fused and args.per_tree:
+        r1, objs = measure(args, ws, W, args.frontier, dev, local, stream, T, flush, K, Wm, fused=False)
+        objs[0].close()
+        del objs
+        per_tree = r1["mean"]
+
     alt = None
     if args.compare:
         other = "scan" if args.frontier == "reverse" else "reverse"
-        r2, objs = measure(args, ws, W, other, dev, local, stream, T, flush, K, Wm)
+        r2, objs = measure(args, ws, W, other, dev, local, stream, T, flush, K, Wm, fused=args.fused)
         objs[0].close()
         del objs
         alt = {"decremental_frontier": other, "value": edges / (r2["total_ms"] / 1e3),
@@ -500,7 +540,8 @@ def run_ours(args, ws, rank, local):
         cb = cpu_baseline(args, args.cpu_steps)
         cb = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
-    dyn = {"sssp": mean["sssp_inc"] + mean["sssp_dec"], "bfs": mean["bfs_inc"] + mean["bfs_dec"]}
+    split = mean if not args.fused else per_tree
+    dyn = {"sssp": split["sssp_inc"] + split["sssp_dec"], "bfs": split["bfs_inc"] + split["bfs_dec"]} if split else None
     line = {
         "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": ws, "steps": K, "warmup": Wm,
         "ms_per_step": res["ms_per_step"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -510,16 +551,21 @@ def run_ours(args, ws, rank, local):
                    "vertices": V, "edges": res["n_base"], "batch": args.batch, "source": W.source,
                    "hashing": not args.no_hashing, "load_factor": args.lf,
                    "decremental_frontier": args.frontier,
+                   "tree_updates": "fused SSSP+BFS (meerkat_trees_*)" if args.fused else "per tree",
                    "parallelism": "single GPU" if ws == 1 else f"{ws} independent replicas",
                    "l2": "flushed between timed steps (256 MiB write, outside the intervals); store > L2"},
         "update_edges_per_s": 2 * args.batch / ((mean["insert"] + mean["delete"]) / 1e3),
         "insert_edges_per_s": args.batch / (mean["insert"] / 1e3),
         "delete_edges_per_s": args.batch / (mean["delete"] / 1e3),
-        "sssp_ms_per_batch": {"incremental": mean["sssp_inc"], "decremental": mean["sssp_dec"]},
-        "bfs_ms_per_batch": {"incremental": mean["bfs_inc"], "decremental": mean["bfs_dec"]},
+        "sssp_bfs_fused_ms_per_batch": ({"incremental": mean["trees_inc"], "decremental": mean["trees_dec"]}
+                                        if args.fused else None),
+        "sssp_ms_per_batch": ({"incremental": split["sssp_inc"], "decremental": split["sssp_dec"],
+                               "measured": "per-tree calls, separate run" if args.fused else "in the timed steps"}
+                              if split else None),
+        "bfs_ms_per_batch": ({"incremental": split["bfs_inc"], "decremental": split["bfs_dec"]} if split else None),
         "per_call_ms": mean,
         "static_recompute_ms": res["static_ms"],
-        "self_relative_speedup": {k: res["static_ms"][k] / (dyn[k] / 2) for k in dyn},
+        "self_relative_speedup": ({k: res["static_ms"][k] / (dyn[k] / 2) for k in dyn} if dyn else None),
         "bulk_build": {"edges": res["n_base"], "ms": res["bulk_ms"], "edges_per_s": res["n_base"] / (res["bulk_ms"] / 1e3)},
         "tree_calls": tree_detail(res),
         "roofline": roofline_of(res, peak, peak_src, traffic_file),
