@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_dscan(DArgs A, const uint32_t
     __syncthreads();
     for (uint64_t i = threadIdx.x; i < n_inv; i += blockDim.x) {
       uint32_t w, m;
-      filter_loc(__ldg(list + i), fwords, w, m);
+      filter_loc(__ldg(list + i), 32 - FILTER_LOG2, w, m);
       atomicOr(&filt[w], m);
     }
     __syncthreads();
@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_dscan(DArgs A, const uint32_t
         bool hit = x < G.Vg && (MAP || F::valid_cell(l8, k));
         if (fwords) {
           uint32_t w, m;
-          filter_loc(x, fwords, w, m);
+          filter_loc(x, 32 - FILTER_LOG2, w, m);
           hit = hit && (filt[w] & m) == m;
         }
         hm |= (uint32_t)hit << (q * NK + k);

@@ -242,8 +242,8 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_inc(const __grid_constan
 // per key and tree: one shared-memory filter probe.  Slow path (warp-uniform, only for positions
 // where some lane hit a filter): exact bit-set test, source validity, relaxation and enqueue.
 template <bool MAP>
-__device__ __forceinline__ void dec_scan(const TreeArgs& A, const uint32_t* filt, const uint32_t* fwords,
-                                         uint32_t n_slabs, uint32_t r1, const uint32_t* epoch, Counters& c) {
+__device__ __forceinline__ void dec_scan(const TreeArgs& A, const uint32_t* filt, bool use_filter, uint32_t n_slabs,
+                                         uint32_t r1, const uint32_t* epoch, Counters& c) {
   using F = Frag<MAP>;
   constexpr int NK = F::NK;
   constexpr int U = SCAN_UNROLL;
@@ -271,37 +271,38 @@ __device__ __forceinline__ void dec_scan(const TreeArgs& A, const uint32_t* filt
 #pragma unroll
     for (int q = 0; q < U; q++) d[q] = nd[q];
     if (t + 1 < trips) load_trip(t + 1, nd);
+    // fast path: one probe of the union filter (every tree's V_invalid) per key
+    uint32_t hm = 0;
 #pragma unroll
-    for (int k = 0; k < MAX_TREES; k++) {
-      if (k >= (int)A.ntrees) break;
-      const TreeDev& T = A.T[k];
-      const uint32_t* fk = filt + k * A.filter_words;
-      uint32_t hm = 0;
+    for (int q = 0; q < U; q++) {
 #pragma unroll
-      for (int q = 0; q < U; q++) {
-#pragma unroll
-        for (int kk = 0; kk < NK; kk++) {
-          const uint32_t x = F::key(d[q], kk);
-          bool hit = x < V && (MAP || F::valid_cell(l8, kk));   // live key (sentinels are >= V)
-          if (fwords[k]) {
-            uint32_t w, m;
-            filter_loc(x, fwords[k], w, m);
-            hit = hit && (fk[w] & m) == m;
-          }
-          hm |= (uint32_t)hit << (q * NK + kk);
+      for (int kk = 0; kk < NK; kk++) {
+        const uint32_t x = F::key(d[q], kk);
+        bool hit = x < V && (MAP || F::valid_cell(l8, kk));   // live key (sentinels are >= V)
+        if (use_filter) {
+          uint32_t w, m;
+          filter_loc(x, 32 - FILTER_LOG2, w, m);
+          hit = hit && (filt[w] & m) == m;
         }
+        hm |= (uint32_t)hit << (q * NK + kk);
       }
-      const uint32_t pos = __reduce_or_sync(FULL, hm);
-      if (!pos) continue;
+    }
+    const uint32_t pos = __reduce_or_sync(FULL, hm);
+    if (!pos) continue;
 #pragma unroll
-      for (int q = 0; q < U; q++) {
+    for (int q = 0; q < U; q++) {
 #pragma unroll
-        for (int kk = 0; kk < NK; kk++) {
-          if (!((pos >> (q * NK + kk)) & 1u)) continue;   // warp-uniform
-          const uint32_t x = F::key(d[q], kk);
+      for (int kk = 0; kk < NK; kk++) {
+        if (!((pos >> (q * NK + kk)) & 1u)) continue;   // warp-uniform
+        const uint32_t x = F::key(d[q], kk);
+        const bool cand = (hm >> (q * NK + kk)) & 1u;
+#pragma unroll
+        for (int k = 0; k < MAX_TREES; k++) {
+          if (k >= (int)A.ntrees) break;
+          const TreeDev& T = A.T[k];
           bool enq = false;
-          if (((hm >> (q * NK + kk)) & 1u) && bit_test(T.inval_bits, x)) {
-            // x in V_invalid: is the slab's source vertex u valid and reached?
+          if (cand && bit_test(T.inval_bits, x)) {
+            // x in V_invalid of tree k: is the slab's source vertex u valid and reached in it?
             const uint32_t u = __ldg(G.owner + s0 + q * ng);
             if (u != NO_OWNER && !bit_test(T.inval_bits, u)) {
               const uint64_t nu = ld_cg_u64(T.node + u);
@@ -385,25 +386,23 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_dec(const __grid_constan
                         epoch[k] + r1, c);
     }
   } else if (n_inv_all) {
-    // one shared-memory filter per tree while sparse enough: two bits per member, bit load <= 1/4
-    uint32_t fw[MAX_TREES] = {};
-    for (uint32_t k = 0; k < A.ntrees; k++)
-      fw[k] = (A.filter_words && n_inv[k] * 8 <= (uint64_t)A.filter_words * 32) ? A.filter_words : 0u;
-    for (uint32_t k = 0; k < A.ntrees; k++) {
-      if (!fw[k]) continue;
-      uint32_t* fk = filt + k * A.filter_words;
-      for (uint32_t i = threadIdx.x; i < fw[k]; i += blockDim.x) fk[i] = 0;
+    // one shared-memory filter of the union of the trees' V_invalid, while sparse enough
+    // (two bits per member, bit load <= 1/4)
+    const bool use_filter = A.filter_words && n_inv_all * 8 <= (uint64_t)FILTER_WORDS * 32;
+    if (use_filter) {
+      for (uint32_t i = threadIdx.x; i < FILTER_WORDS; i += blockDim.x) filt[i] = 0;
       __syncthreads();
-      for (uint64_t i = threadIdx.x; i < n_inv[k]; i += blockDim.x) {
-        uint32_t w, m;
-        filter_loc(__ldcg(A.T[k].inval_list + i), fw[k], w, m);
-        atomicOr(&fk[w], m);
-      }
+      for (uint32_t k = 0; k < A.ntrees; k++)
+        for (uint64_t i = threadIdx.x; i < n_inv[k]; i += blockDim.x) {
+          uint32_t w, m;
+          filter_loc(__ldcg(A.T[k].inval_list + i), 32 - FILTER_LOG2, w, m);
+          atomicOr(&filt[w], m);
+        }
+      __syncthreads();
     }
-    __syncthreads();
     const uint32_t n_slabs = A.G.H + (uint32_t)min((unsigned long long)A.G.P, __ldcg(&A.G.ctrl->pool_top));
     if (tid == 0) c.scan_slabs = n_slabs;
-    dec_scan<MAP>(A, filt, fw, n_slabs, r1, epoch, c);
+    dec_scan<MAP>(A, filt, use_filter, n_slabs, r1, epoch, c);
   }
   grid.sync();
   timeline(A.T[0].ctrl);
@@ -461,8 +460,7 @@ cudaError_t launch_tree(meerkat_graph* g, meerkat_tree* const* trees, uint32_t n
   }
   A.bs = s; A.bd = d; A.bw = w; A.bn = n;
   A.weighted = g->weighted ? 1u : 0u;
-  // one filter per tree in shared memory (scan only); two trees share the budget of one
-  A.filter_words = g->reverse ? 0u : FILTER_WORDS / ntrees;
+  A.filter_words = g->reverse ? 0u : FILTER_WORDS;   // shared-memory union filter (scan only)
   int bps = g->tree_blocks_per_sm[mode];
   if (bps <= 0) return cudaErrorInvalidConfiguration;
   if (g->latency_bps > 0 && mode != MODE_STATIC && !(mode == MODE_DECREMENTAL && !g->reverse))

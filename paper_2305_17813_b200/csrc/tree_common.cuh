@@ -10,7 +10,8 @@ namespace cg = cooperative_groups;
 namespace mk {
 
 constexpr int TREE_BLOCK = 512;
-constexpr int FILTER_WORDS = 24576;   // 96 KiB smem Bloom filter per block (decremental scan), 2 blocks/SM
+constexpr int FILTER_LOG2 = 14;
+constexpr int FILTER_WORDS = 1 << FILTER_LOG2;   // 64 KiB smem Bloom filter per block (decremental scan)
 constexpr int SCAN_UNROLL = 2;        // independent slabs in flight per group in the scan
 constexpr unsigned FULL = 0xFFFFFFFFu;
 constexpr uint64_t PROBE_MIN_ITEMS = 65536;  // frontiers at least this large probe node[x] before the atomic
@@ -149,14 +150,13 @@ __device__ __forceinline__ void flush_counters(const GraphDev& G, const TreeDev&
   if (rounds_owner) { tc->rounds = relax_rounds; tc->prop_rounds = prop_rounds; }
 }
 
-// Blocked two-bit Bloom filter of V_invalid in shared memory: one word per key,
-// two bits within it (false-positive rate ~ load^2).  Exact membership is the
-// global bit set; the filter only keeps non-members off the slow path.
-__device__ __forceinline__ void filter_loc(uint32_t x, uint32_t fwords, uint32_t& w, uint32_t& m) {
-  uint32_t h = x * 0x9E3779B1u;
-  h ^= h >> 15;
-  w = __umulhi(h * 0x85EBCA6Bu, fwords);
-  m = (1u << (h & 31)) | (1u << ((h >> 5) & 31));
+// Blocked two-bit Bloom filter of V_invalid in shared memory: one word per key, two bits within
+// it (false-positive rate ~ load^2).  Exact membership is the global bit set; the filter only keeps
+// non-members off the slow path.  FILTER_WORDS is a power of two: word = top bits of a
+// multiplicative hash, bits = two 5-bit fields of the (scrambled) id.
+__device__ __forceinline__ void filter_loc(uint32_t x, uint32_t w_shift, uint32_t& w, uint32_t& m) {
+  w = (x * 0x9E3779B1u) >> w_shift;
+  m = (1u << (x & 31)) | (1u << ((x >> 5) & 31));
 }
 
 }  // namespace mk
