@@ -202,7 +202,8 @@ meerkat_status meerkat_tree_destroy(meerkat_tree* t);
  *
  * Messages are (x, payload) pairs of uint64 grouped by destination rank; `msg_counts[r]` is the
  * number of pairs for rank r.  The device buffer in meerkat_dresult stays valid until the next
- * phase call on the tree.  Every phase synchronises the graph's stream.
+ * phase call on the tree.  Every phase synchronises the graph's stream once, except the APPLY
+ * phases, which are stream-ordered (their frontier is reported by the next phase).
  * ------------------------------------------------------------------------------------------- */
 typedef enum {
   MEERKAT_D_STATIC_INIT = 0,      /* node <- UNREACHED, SRC <- <0,SRC> on its owner; frontier = {SRC} */
@@ -232,8 +233,8 @@ meerkat_status meerkat_dtree_phase(meerkat_graph* g, meerkat_tree* t, meerkat_dp
 /* Stable partition of a batch by owner(key[i]) = key[i] % world_size (key = src for insert/delete/
  * query and incremental seeds, dst for decremental invalidation): writes the permuted a,b,c
  * (c may be NULL) to the device outputs and per-rank counts to counts[world_size] (host). */
-/* Copy `bytes` between host/device buffers on the graph's stream and synchronise (lets a caller
- * move phase messages into its own communication buffers). */
+/* Copy `bytes` between host/device buffers on the graph's stream (lets a caller move phase messages
+ * into its own communication buffers); synchronises only when either side is host memory. */
 meerkat_status meerkat_memcpy(meerkat_graph* g, void* dst, const void* src, uint64_t bytes);
 meerkat_status meerkat_route(meerkat_graph* g, int key_is_b, const uint32_t* a, const uint32_t* b,
                              const uint32_t* c, uint64_t n, uint32_t* out_a, uint32_t* out_b, uint32_t* out_c,

@@ -586,7 +586,7 @@ meerkat_status meerkat_memcpy(meerkat_graph* g, void* dst, const void* src, uint
   if (!bytes) return MEERKAT_OK;
   DeviceGuard dg(g->device);
   cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, g->stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  if (e == cudaSuccess && (!is_device_ptr(dst) || !is_device_ptr(src))) e = cudaStreamSynchronize(g->stream);
   return from_cuda(e);
 }
 

@@ -27,7 +27,7 @@ struct DArgs {
   unsigned long long* msg_n;    // raw pair count
   uint64_t msg_cap;             // pairs
   const uint64_t* fr;           // frontier being expanded (local rows)
-  uint64_t n;                   // its size
+  const unsigned long long* n_ptr;   // its size (device: the previous phases may still be in flight)
   uint64_t* fnext;
   unsigned long long* sznext;
   uint32_t epoch;               // stamp epoch of fnext
@@ -156,8 +156,9 @@ __global__ void __launch_bounds__(D_BLOCK) k_dexpand(DArgs A) {
   const uint64_t ng = ((uint64_t)gridDim.x * blockDim.x) / GROUP;
   uint64_t it = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / GROUP;
   uint32_t v = 0, slab = 0, du = 0;
+  const uint64_t n_cur = __ldcg(A.n_ptr);
   auto fetch = [&]() -> bool {
-    for (; it < A.n; it += ng) {
+    for (; it < n_cur; it += ng) {
       const uint64_t item = A.fr[it];
       v = (uint32_t)item;
       if (l8 == 0) c.items++;
@@ -429,8 +430,8 @@ cudaError_t dlaunch(meerkat_graph* g, int kind, DArgs& A, const void* a, const v
       g->launches++;
       break;
     case 3:
-      if (map) k_dexpand<true, PROPAGATE><<<dgrid(g, A.n * GROUP), D_BLOCK, 0, st>>>(A);
-      else k_dexpand<false, PROPAGATE><<<dgrid(g, A.n * GROUP), D_BLOCK, 0, st>>>(A);
+      if (map) k_dexpand<true, PROPAGATE><<<dgrid(g, n * GROUP), D_BLOCK, 0, st>>>(A);
+      else k_dexpand<false, PROPAGATE><<<dgrid(g, n * GROUP), D_BLOCK, 0, st>>>(A);
       g->launches++;
       break;
     case 4:
@@ -446,8 +447,8 @@ cudaError_t dlaunch(meerkat_graph* g, int kind, DArgs& A, const void* a, const v
       break;
     }
     case 6:
-      if (map) k_dexpand<true, RELAX><<<dgrid(g, A.n * GROUP), D_BLOCK, 0, st>>>(A);
-      else k_dexpand<false, RELAX><<<dgrid(g, A.n * GROUP), D_BLOCK, 0, st>>>(A);
+      if (map) k_dexpand<true, RELAX><<<dgrid(g, n * GROUP), D_BLOCK, 0, st>>>(A);
+      else k_dexpand<false, RELAX><<<dgrid(g, n * GROUP), D_BLOCK, 0, st>>>(A);
       g->launches++;
       break;
     case 7:
@@ -462,11 +463,11 @@ cudaError_t dlaunch(meerkat_graph* g, int kind, DArgs& A, const void* a, const v
   return cudaGetLastError();
 }
 
-cudaError_t dsort_msgs(meerkat_graph* g, const uint64_t* raw, const unsigned long long* n_ptr, uint64_t n_host,
+cudaError_t dsort_msgs(meerkat_graph* g, const uint64_t* raw, const unsigned long long* n_ptr, uint64_t n_bound,
                        unsigned long long* counts, unsigned long long* cursor, uint64_t* out) {
   cudaError_t e = cudaMemsetAsync(counts, 0, MEERKAT_MAX_RANKS * 8, g->stream);
-  if (e != cudaSuccess || n_host == 0) return e;
-  const unsigned gb = dgrid(g, n_host);
+  if (e != cudaSuccess || n_bound == 0) return e;
+  const unsigned gb = dgrid(g, n_bound);   // grid-stride kernels read the exact count on the device
   k_msg_hist<<<gb, D_BLOCK, 0, g->stream>>>(raw, n_ptr, g->ws, counts);
   k_msg_scan<<<1, 32, 0, g->stream>>>(counts, g->ws, cursor);
   k_msg_scatter<<<gb, D_BLOCK, 0, g->stream>>>(raw, n_ptr, g->ws, cursor, out);
@@ -501,22 +502,6 @@ cudaError_t dscan_attr(meerkat_graph* g) {
 namespace mk {
 
 static meerkat_status status_of(cudaError_t e) { return e == cudaSuccess ? MEERKAT_OK : MEERKAT_E_CUDA; }
-
-static meerkat_status graph_err(meerkat_graph* g) {
-  // read and clear the sticky error of the out store (phase kernels report there)
-  cudaError_t e = cudaMemcpyAsync(g->out.hctrl, g->out.dev.ctrl, sizeof(GraphCtrl), cudaMemcpyDeviceToHost, g->stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
-  if (e != cudaSuccess) return MEERKAT_E_CUDA;
-  const uint32_t err = g->out.hctrl->err;
-  if (!err) return MEERKAT_OK;
-  cudaMemsetAsync(&g->out.dev.ctrl->err, 0, 4, g->stream);
-  if (err & ERR_PARTITION) return MEERKAT_E_PARTITION;
-  if (err & ERR_RANGE) return MEERKAT_E_VERTEX_RANGE;
-  if (err & ERR_WEIGHT) return MEERKAT_E_WEIGHT;
-  if (err & ERR_CAPACITY) return MEERKAT_E_CAPACITY;
-  if (err & ERR_OVERFLOW) return MEERKAT_E_OVERFLOW;
-  return MEERKAT_E_STATE;
-}
 
 static cudaError_t ensure_msgs(meerkat_graph* g, meerkat_tree* t, uint64_t need) {
   if (need <= t->msg_cap) return cudaSuccess;
@@ -565,31 +550,26 @@ meerkat_status dtree_phase(meerkat_graph* g, meerkat_tree* t, int phase, const v
   if (phase == MEERKAT_D_DEC_INVALIDATE && (g->last_kind != 2 || t->version + 1 != g->version)) return MEERKAT_E_STATE;
   TreeDev& T = t->dev;
   cudaError_t e = cudaSuccess;
-  if (phase == MEERKAT_D_STATIC_INIT || phase == MEERKAT_D_INC_SEED || phase == MEERKAT_D_DEC_INVALIDATE) {
-    e = cudaMemsetAsync(T.ctrl, 0, sizeof(TreeCtrl), g->stream);   // a new update: counters and sizes
+  const bool starts_update =
+      phase == MEERKAT_D_STATIC_INIT || phase == MEERKAT_D_INC_SEED || phase == MEERKAT_D_DEC_INVALIDATE;
+  if (starts_update) {
+    // a new update: counters and sizes; message capacity for the update (at most one message per
+    // visited edge per expansion, i.e. bounded by the live edges held here; plus the batch)
+    e = cudaMemsetAsync(T.ctrl, 0, sizeof(TreeCtrl), g->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(g->out.hctrl, g->out.dev.ctrl, sizeof(GraphCtrl), cudaMemcpyDeviceToHost, g->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+    if (e == cudaSuccess) e = ensure_msgs(g, t, g->out.hctrl->ins_total - g->out.hctrl->del_total + n + 1024);
     t->hctrl->inval_n = 0;
   }
   // frontier buffers: `cur` holds the frontier filled last; new frontiers go to the other one
   int nb = t->cur;
-  uint64_t cur_n = 0;
   if (seed || expands) {
-    if (expands) {
-      e = cudaMemcpyAsync(t->hcnt + MEERKAT_MAX_RANKS + 1, &T.ctrl->size[t->cur], 8, cudaMemcpyDeviceToHost, g->stream);
-      if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
-      cur_n = t->hcnt[MEERKAT_MAX_RANKS + 1];
-    }
     nb = 1 - t->cur;
     if (e == cudaSuccess) e = cudaMemsetAsync(&T.ctrl->size[nb], 0, 8, g->stream);
     t->depoch++;
   }
   if (e == cudaSuccess && emits) {
-    uint64_t need = n;
-    if (phase != MEERKAT_D_INC_SEED) {
-      e = cudaMemcpyAsync(g->out.hctrl, g->out.dev.ctrl, sizeof(GraphCtrl), cudaMemcpyDeviceToHost, g->stream);
-      if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
-      need = g->out.hctrl->ins_total - g->out.hctrl->del_total;   // one message per visited edge at most
-    }
-    if (e == cudaSuccess) e = ensure_msgs(g, t, need + 1024);
+    if (n + 1024 > t->msg_cap && phase == MEERKAT_D_INC_SEED) e = ensure_msgs(g, t, n + 1024);
     if (e == cudaSuccess) e = cudaMemsetAsync(t->dcnt + 2 * MEERKAT_MAX_RANKS, 0, 8, g->stream);
   }
   if (e != cudaSuccess) return MEERKAT_E_CUDA;
@@ -600,18 +580,20 @@ meerkat_status dtree_phase(meerkat_graph* g, meerkat_tree* t, int phase, const v
   A.msg_n = t->dcnt + 2 * MEERKAT_MAX_RANKS;
   A.msg_cap = t->msg_cap;
   A.fr = T.fr[t->cur];
-  A.n = cur_n;
+  A.n_ptr = &T.ctrl->size[t->cur];
   A.fnext = T.fr[nb];
   A.sznext = &T.ctrl->size[nb];
   A.epoch = t->depoch;
   A.unit = t->unit ? 1u : 0u;
+  // grid size for an expansion: the host's bound on the frontier (the kernel reads the exact size)
+  const uint64_t n_front = expands ? std::max<uint64_t>(t->cur_n, 1) : 0;
   switch (phase) {
     case MEERKAT_D_STATIC_INIT: e = dlaunch(g, 0, A, nullptr, nullptr, nullptr, 0, 0, 0); break;
     case MEERKAT_D_INC_SEED: e = dlaunch(g, 1, A, a, b, c, n, 0, 0); break;
     case MEERKAT_D_DEC_INVALIDATE: e = dlaunch(g, 2, A, a, b, nullptr, n, 0, 0); break;
-    case MEERKAT_D_PROPAGATE: if (cur_n) e = dlaunch(g, 3, A, nullptr, nullptr, nullptr, 0, 0, 0); break;
+    case MEERKAT_D_PROPAGATE: e = dlaunch(g, 3, A, nullptr, nullptr, nullptr, n_front, 0, 0); break;
     case MEERKAT_D_APPLY_PROPAGATE: e = dlaunch(g, 4, A, a, nullptr, nullptr, n, 0, 0); break;
-    case MEERKAT_D_RELAX: if (cur_n) e = dlaunch(g, 6, A, nullptr, nullptr, nullptr, 0, 0, 0); break;
+    case MEERKAT_D_RELAX: e = dlaunch(g, 6, A, nullptr, nullptr, nullptr, n_front, 0, 0); break;
     case MEERKAT_D_APPLY_RELAX: e = dlaunch(g, 7, A, a, nullptr, nullptr, n, 0, 0); break;
     case MEERKAT_D_DEC_SCAN: {
       if (n) {
@@ -627,31 +609,44 @@ meerkat_status dtree_phase(meerkat_graph* g, meerkat_tree* t, int phase, const v
       t->version = g->version;
       break;
   }
-  if (e == cudaSuccess && emits) {
-    unsigned long long* counts = t->dcnt;
-    unsigned long long* cursor = t->dcnt + MEERKAT_MAX_RANKS;
-    e = cudaMemcpyAsync(t->hcnt + MEERKAT_MAX_RANKS, A.msg_n, 8, cudaMemcpyDeviceToHost, g->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
-    const uint64_t raw = t->hcnt[MEERKAT_MAX_RANKS];
-    if (e == cudaSuccess) e = dsort_msgs(g, t->msg_raw, A.msg_n, raw, counts, cursor, t->msg_out);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(t->hcnt, counts, MEERKAT_MAX_RANKS * 8, cudaMemcpyDeviceToHost, g->stream);
-  }
-  if (e == cudaSuccess) e = cudaMemcpyAsync(t->hctrl, T.ctrl, sizeof(TreeCtrl), cudaMemcpyDeviceToHost, g->stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
-  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  if (e == cudaSuccess && emits)
+    e = dsort_msgs(g, t->msg_raw, A.msg_n, t->msg_cap, t->dcnt, t->dcnt + MEERKAT_MAX_RANKS, t->msg_out);
   if (seed || expands) t->cur = nb;
   if (phase == MEERKAT_D_INC_SEED || phase == MEERKAT_D_DEC_INVALIDATE || phase == MEERKAT_D_STATIC_INIT)
     t->version = g->version;
+  if (out) std::memset(out, 0, sizeof(*out));
+  if (apply) {   // stream-ordered; the next emitting phase reports the resulting frontier
+    if (e != cudaSuccess) return MEERKAT_E_CUDA;
+    t->cur_n += 8 * n;   // grid bound for the next expansion (each message adds a vertex's buckets)
+    if (out) { out->msgs = t->msg_out; out->invalid = T.inval_list; }
+    return MEERKAT_OK;
+  }
+  // one synchronisation per phase: message counts, tree control block, graph error word
+  if (e == cudaSuccess && emits)
+    e = cudaMemcpyAsync(t->hcnt, t->dcnt, MEERKAT_MAX_RANKS * 8, cudaMemcpyDeviceToHost, g->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(t->hctrl, T.ctrl, sizeof(TreeCtrl), cudaMemcpyDeviceToHost, g->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(g->out.hctrl, g->out.dev.ctrl, sizeof(GraphCtrl), cudaMemcpyDeviceToHost, g->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  t->cur_n = t->hctrl->size[t->cur];
   if (out) {
-    std::memset(out, 0, sizeof(*out));
     out->msgs = t->msg_out;
     if (emits)
       for (uint32_t r = 0; r < g->ws && r < MEERKAT_MAX_RANKS; r++) out->msg_counts[r] = t->hcnt[r];
-    out->frontier = t->hctrl->size[t->cur];
+    out->frontier = t->cur_n;
     out->invalid = T.inval_list;
     out->invalid_n = t->hctrl->inval_n;
   }
-  return graph_err(g);
+  const uint32_t err = g->out.hctrl->err;
+  if (!err) return MEERKAT_OK;
+  cudaMemsetAsync(&g->out.dev.ctrl->err, 0, 4, g->stream);
+  if (err & ERR_PARTITION) return MEERKAT_E_PARTITION;
+  if (err & ERR_RANGE) return MEERKAT_E_VERTEX_RANGE;
+  if (err & ERR_WEIGHT) return MEERKAT_E_WEIGHT;
+  if (err & ERR_CAPACITY) return MEERKAT_E_CAPACITY;
+  if (err & ERR_OVERFLOW) return MEERKAT_E_OVERFLOW;
+  return MEERKAT_E_STATE;
 }
 
 meerkat_status route_batch(meerkat_graph* g, int key_is_b, const uint32_t* a, const uint32_t* b, const uint32_t* c,

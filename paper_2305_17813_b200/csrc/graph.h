@@ -87,6 +87,7 @@ struct meerkat_tree {
   // vertex-partitioned trees (dtree.cu)
   bool dist = false;
   int cur = 0;                              // frontier buffer filled by the last phase
+  uint64_t cur_n = 0;                       // its size as of the last synchronising phase (a grid bound)
   uint32_t depoch = 0;                      // stamp epoch of the frontier being filled
   uint64_t* msg_raw = nullptr;              // outgoing pairs, unsorted
   uint64_t* msg_out = nullptr;              // outgoing pairs grouped by destination rank

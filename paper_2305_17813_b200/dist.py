@@ -79,6 +79,15 @@ class Transport:
         dist.all_to_all_single(recv, s.contiguous(), [c * elem for c in rcl], [c * elem for c in scl], group=self.group)
         return recv.to(self.device) if self.staged else recv, rcl
 
+    def alltoallv_known(self, send: torch.Tensor, send_counts, recv_counts, elem: int = 1) -> torch.Tensor:
+        """alltoallv when both sides' row counts are already known (no count exchange)."""
+        dev = self._dev()
+        s = send.to(dev) if send.device != dev else send
+        recv = torch.empty(sum(recv_counts) * elem, dtype=send.dtype, device=dev)
+        dist.all_to_all_single(recv, s.contiguous(), [c * elem for c in recv_counts], [c * elem for c in send_counts],
+                               group=self.group)
+        return recv.to(self.device) if self.staged else recv
+
     def allreduce_sum(self, x: int) -> int:
         t = torch.tensor([int(x)], dtype=torch.int64, device=self._dev())
         dist.all_reduce(t, group=self.group)
@@ -115,6 +124,8 @@ class DistGraph:
         hints = None
         if degree_hints is not None:
             hints = np.ascontiguousarray(np.asarray(degree_hints, np.uint32)[self.rank::self.ws])
+        if stream is None:   # the library's stream must be the one torch (and NCCL) order against
+            stream = torch.cuda.current_stream(self.device)
         self.g = Graph(vertex_n, weighted=weighted, hashing=hashing, load_factor=load_factor, degree_hints=hints,
                        pool_slabs=pool_slabs, hash_seed=hash_seed, device=self.device.index or 0, stream=stream,
                        world_size=self.ws, rank=self.rank)
@@ -202,7 +213,12 @@ class DistTree:
         self._h = h
         self.rounds = 0
         # static: STATIC_INIT ran inside create; its frontier is {SRC} on the owner
-        self._loop(_lib.D_RELAX, _lib.D_APPLY_RELAX, None)
+        self.recompute()
+
+    def recompute(self):
+        """Static re-run on the current graph."""
+        res = self._phase(_lib.D_STATIC_INIT)
+        self._loop(_lib.D_RELAX, _lib.D_APPLY_RELAX, res)
 
     def close(self):
         if getattr(self, "_h", None):
@@ -217,24 +233,37 @@ class DistTree:
         return res
 
     def _exchange(self, res):
+        """One all-to-all of <count, local frontier, messages sent> triples (which also decides
+        termination: nothing left anywhere) and, if any message moves, one of the messages."""
         ws = self.dg.ws
-        counts = [int(res.msg_counts[r]) for r in range(ws)] if res is not None else [0] * ws
-        total = sum(counts)
-        send = torch.empty(max(total, 1) * 2, dtype=torch.int64, device=self.dg.device)
-        if total:
+        tp = self.dg.tp
+        counts = [int(res.msg_counts[r]) for r in range(ws)]
+        sent = sum(counts)
+        meta = torch.tensor([[counts[p], int(res.frontier), sent] for p in range(ws)], dtype=torch.int64,
+                            device=tp._dev()).view(-1)
+        rmeta, _ = tp.alltoallv(meta, [1] * ws, elem=3)
+        rmeta = rmeta.view(ws, 3).cpu()
+        if int(rmeta[:, 1].sum()) + int(rmeta[:, 2].sum()) == 0:
+            return None, False
+        rcounts = rmeta[:, 0].tolist()
+        send = torch.empty(max(sent, 1) * 2, dtype=torch.int64, device=self.dg.device)
+        if sent:   # stream-ordered device copy out of the library's message buffer
             check(_lib.lib().meerkat_memcpy(self.dg.g._h, ctypes.c_void_p(send.data_ptr()),
-                                            ctypes.c_void_p(res.msgs), total * 16), "meerkat_memcpy")
-        recv, _ = self.dg.tp.alltoallv(send[: total * 2], counts, elem=2)
-        return recv
+                                            ctypes.c_void_p(res.msgs), sent * 16), "meerkat_memcpy")
+        recv = tp.alltoallv_known(send[: sent * 2], counts, rcounts, elem=2)
+        return recv, True
 
     def _loop(self, expand_ph, apply_ph, res):
-        """Rounds until every rank's frontier is empty."""
+        """Rounds until no rank has frontier or messages left.  Per round:
+        one count/termination all-to-all, one message all-to-all, a stream-ordered apply and one
+        synchronising expansion."""
         while True:
-            recv = self._exchange(res)
+            recv, active = self._exchange(res)
+            if not active:
+                return res
             n = recv.numel() // 2
-            r2 = self._phase(apply_ph, recv if n else None, n=n)
-            if self.dg.tp.allreduce_sum(r2.frontier) == 0:
-                return r2
+            if n:
+                self._phase(apply_ph, recv, n=n)
             self.rounds += 1
             res = self._phase(expand_ph)
 

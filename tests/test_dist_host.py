@@ -32,6 +32,9 @@ def _worker(rank, ws, port, q):
         assert rc == [(s + 1) * (rank + 1) for s in range(ws)]
         exp = torch.cat([torch.full(((s + 1) * (rank + 1) * 2,), 100 * s + rank, dtype=torch.int64) for s in range(ws)])
         assert torch.equal(recv, exp)
+        # known counts (no count exchange)
+        rk = tp.alltoallv_known(send, counts, [(s + 1) * (rank + 1) for s in range(ws)], elem=2)
+        assert torch.equal(rk, exp)
         # empty exchange
         recv, rc = tp.alltoallv(torch.empty(0, dtype=torch.int64), [0] * ws, elem=2)
         assert recv.numel() == 0 and rc == [0] * ws
