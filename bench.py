@@ -62,7 +62,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-scale", type=int, default=20, help="R-MAT scale of the oracle's bounded sample")
-    p.add_argument("--cpu-steps", type=int, default=2)
+    p.add_argument("--cpu-steps", type=int, default=8,
+                   help="oracle steps in the cpu_baseline sample (~1.2 s each at scale 20: a 10-s bounded sample)")
     p.add_argument("--json-out", default=None)
     p.add_argument("--sweep", action=argparse.BooleanOptionalAction, default=True,
                    help="also run the config-2 insert/delete/query batch-size sweep (reported under store_sweep)")
@@ -189,6 +190,18 @@ def make_workload(args, n_batches, rank=0):
     return W, time.time() - t0
 
 
+def workload_config(args, V, n_base, source, ws=1):
+    """The `config` object of the JSON line (shared by both arms)."""
+    return {"workload": f"rmat-s{args.scale}-ef{args.ef} dynamic SSSP+BFS, {args.batch}-edge insert+delete "
+                        f"batches (BASELINE config 3)",
+            "vertices": V, "edges": n_base, "batch": args.batch, "source": source,
+            "hashing": not args.no_hashing, "load_factor": args.lf,
+            "decremental_frontier": args.frontier,
+            "tree_updates": "fused SSSP+BFS (meerkat_trees_*)" if args.fused else "per tree",
+            "parallelism": "single GPU" if ws == 1 else f"{ws} independent replicas",
+            "l2": "flushed between timed steps (256 MiB write, outside the intervals); store > L2"}
+
+
 def cpu_baseline(args, steps):
     """The oracle as it stands, on a bounded sample of the same workload recipe (R-MAT at
     --cpu-scale, same generator, same batch size): per step it applies an insert batch and a
@@ -220,12 +233,14 @@ def run_reference(args, ws, rank):
     for _ in range(args.warmup):
         pass   # the oracle has no warm state worth warming; bounded sample only
     cb = cpu_baseline(args, max(1, min(args.steps, args.cpu_steps)))
+    # the line carries our arm's config (the workload this is a bounded sample of); the sample
+    # itself is described in cpu_baseline.sample
+    W = make_workload(args, args.steps + args.warmup)[0]
     line = {"metric": METRIC, "value": cb["value"], "unit": "edges/s", "n_gpus": 0, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * cb["seconds"] / max(1, min(args.steps, args.cpu_steps)),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": f"rmat-s{args.cpu_scale}-ef{args.ef} sample of rmat-s{args.scale}-ef{args.ef}",
-                       "batch": args.batch},
+            "config": workload_config(args, W.vertex_n, int(len(W.base[0])), W.source),
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": cb["value"], "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "wall_s": time.time() - t_all}
@@ -546,14 +561,7 @@ def run_ours(args, ws, rank, local):
         "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": ws, "steps": K, "warmup": Wm,
         "ms_per_step": res["ms_per_step"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u64", "data": "synthetic",
-        "config": {"workload": f"rmat-s{args.scale}-ef{args.ef} dynamic SSSP+BFS, {args.batch}-edge insert+delete "
-                               f"batches (BASELINE config 3)",
-                   "vertices": V, "edges": res["n_base"], "batch": args.batch, "source": W.source,
-                   "hashing": not args.no_hashing, "load_factor": args.lf,
-                   "decremental_frontier": args.frontier,
-                   "tree_updates": "fused SSSP+BFS (meerkat_trees_*)" if args.fused else "per tree",
-                   "parallelism": "single GPU" if ws == 1 else f"{ws} independent replicas",
-                   "l2": "flushed between timed steps (256 MiB write, outside the intervals); store > L2"},
+        "config": workload_config(args, V, res["n_base"], W.source, ws),
         "update_edges_per_s": 2 * args.batch / ((mean["insert"] + mean["delete"]) / 1e3),
         "insert_edges_per_s": args.batch / (mean["insert"] / 1e3),
         "delete_edges_per_s": args.batch / (mean["delete"] / 1e3),

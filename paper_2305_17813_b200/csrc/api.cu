@@ -201,9 +201,8 @@ meerkat_status meerkat_insert_batch(meerkat_graph* g, const uint32_t* src, const
   if (e == cudaSuccess && w) e = stage_in(g, 2, w, n * 4, &ww);
   if (e == cudaSuccess && n_inserted) e = cudaMemsetAsync(&g->out.dev.ctrl->n_inserted, 0, 8, g->stream);
   if (e == cudaSuccess)
-    e = launch_insert(g, g->out, (const uint32_t*)s, (const uint32_t*)d, (const uint32_t*)ww, n);
-  if (e == cudaSuccess && g->reverse)   // in-edge mirror: (dst, src, w)
-    e = launch_insert(g, g->in, (const uint32_t*)d, (const uint32_t*)s, (const uint32_t*)ww, n);
+    e = launch_insert(g, &g->out, g->reverse ? &g->in : nullptr,   // in-edge mirror: (dst, src, w)
+                      (const uint32_t*)s, (const uint32_t*)d, (const uint32_t*)ww, n);
   if (e != cudaSuccess) return MEERKAT_E_CUDA;
   g->version++;
   g->last_kind = 1;
@@ -222,8 +221,8 @@ meerkat_status meerkat_delete_batch(meerkat_graph* g, const uint32_t* src, const
   cudaError_t e = stage_in(g, 0, src, n * 4, &s);
   if (e == cudaSuccess) e = stage_in(g, 1, dst, n * 4, &d);
   if (e == cudaSuccess && n_deleted) e = cudaMemsetAsync(&g->out.dev.ctrl->n_deleted, 0, 8, g->stream);
-  if (e == cudaSuccess) e = launch_delete(g, g->out, (const uint32_t*)s, (const uint32_t*)d, n);
-  if (e == cudaSuccess && g->reverse) e = launch_delete(g, g->in, (const uint32_t*)d, (const uint32_t*)s, n);
+  if (e == cudaSuccess)
+    e = launch_delete(g, &g->out, g->reverse ? &g->in : nullptr, (const uint32_t*)s, (const uint32_t*)d, n);
   if (e != cudaSuccess) return MEERKAT_E_CUDA;
   g->version++;
   g->last_kind = 2;

@@ -102,9 +102,10 @@ namespace mk {
 // store.cu
 cudaError_t launch_build(meerkat_graph* g, Store& st, const uint32_t* d_hints, uint64_t pool_request);
 void free_store(Store& st);
-cudaError_t launch_insert(meerkat_graph* g, Store& st, const uint32_t* s, const uint32_t* d, const uint32_t* w,
-                          uint64_t n);
-cudaError_t launch_delete(meerkat_graph* g, Store& st, const uint32_t* s, const uint32_t* d, uint64_t n);
+// st1 (nullable): the in-edge mirror, updated with (dst, src) in the same launch
+cudaError_t launch_insert(meerkat_graph* g, Store* st0, Store* st1, const uint32_t* s, const uint32_t* d,
+                          const uint32_t* w, uint64_t n);
+cudaError_t launch_delete(meerkat_graph* g, Store* st0, Store* st1, const uint32_t* s, const uint32_t* d, uint64_t n);
 cudaError_t launch_query(meerkat_graph* g, Store& st, const uint32_t* s, const uint32_t* d, uint64_t n,
                          uint8_t* found, uint32_t* w_out);
 cudaError_t launch_export(meerkat_graph* g, Store& st, uint32_t* s, uint32_t* d, uint32_t* w, uint64_t cap);

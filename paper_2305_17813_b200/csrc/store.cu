@@ -230,26 +230,49 @@ __device__ __forceinline__ void block_or_err(unsigned int* dst, uint32_t e) {
 
 constexpr int UPD_BLOCK = 256;
 
+// Update kernels serve the out-edge store and, when the graph keeps one, the in-edge
+// mirror in ONE launch: item i < ns*n is edge i/ns of the batch applied to store i%ns
+// ((u, v) for the out store, (v, u) for the mirror).  Both stores' walks are then in
+// flight together instead of two latency-bound launches back to back.
+struct UpdArgs {
+  GraphDev G[2];
+  const uint32_t* src;
+  const uint32_t* dst;
+  const uint32_t* w;
+  uint64_t n;
+  uint32_t ns;   // stores updated: 1 or 2
+};
+
+__device__ __forceinline__ void upd_item(const UpdArgs& A, uint64_t i, uint32_t& st, uint64_t& e) {
+  st = A.ns == 2 ? (uint32_t)(i & 1) : 0u;
+  e = A.ns == 2 ? i >> 1 : i;
+}
+
 template <bool MAP>
-__global__ void __launch_bounds__(UPD_BLOCK) k_insert(GraphDev G, const uint32_t* __restrict__ src,
-                                                      const uint32_t* __restrict__ dst,
-                                                      const uint32_t* __restrict__ w, uint64_t n) {
+__global__ void __launch_bounds__(UPD_BLOCK) k_insert(const __grid_constant__ UpdArgs A) {
   const int lane = lane_id(), l8 = lane & 7, gbase = lane & 24;
   const uint32_t gmask = 0xFFu << gbase;
   const uint64_t ng = ((uint64_t)gridDim.x * blockDim.x) / GROUP;
-  uint32_t added = 0, err = 0;
-  for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / GROUP; i < n; i += ng) {
-    const uint32_t u = src[i], v = dst[i], wt = MAP ? w[i] : 0u;
-    if (u >= G.Vg || v >= G.Vg) { err |= ERR_RANGE; continue; }
-    if (MAP && (wt == 0 || wt >= W_LIMIT)) { err |= ERR_WEIGHT; continue; }
+  uint32_t added[2] = {0, 0}, err[2] = {0, 0};
+  const uint64_t total = A.n * A.ns;
+  for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / GROUP; i < total; i += ng) {
+    uint32_t st; uint64_t e;
+    upd_item(A, i, st, e);
+    const GraphDev& G = A.G[st];
+    const uint32_t a = A.src[e], b = A.dst[e], wt = MAP ? A.w[e] : 0u;
+    const uint32_t u = st ? b : a, v = st ? a : b;
+    if (u >= G.Vg || v >= G.Vg) { err[st] |= ERR_RANGE; continue; }
+    if (MAP && (wt == 0 || wt >= W_LIMIT)) { err[st] |= ERR_WEIGHT; continue; }
     const uint32_t ul = local_row(G, u);
-    if (ul == INVALID_SLAB) { err |= ERR_PARTITION; continue; }
+    if (ul == INVALID_SLAB) { err[st] |= ERR_PARTITION; continue; }
     const int r = group_insert<MAP>(G, ul, v, wt, l8, gmask, gbase);
-    if (r < 0) err |= ERR_CAPACITY;
-    else if (l8 == 0) added += (uint32_t)r;
+    if (r < 0) err[st] |= ERR_CAPACITY;
+    else if (l8 == 0) added[st] += (uint32_t)r;
   }
-  block_or_err(&G.ctrl->err, err);
-  block_add(&G.ctrl->n_inserted, &G.ctrl->ins_total, added);
+  for (uint32_t k = 0; k < A.ns; k++) {
+    block_or_err(&A.G[k].ctrl->err, err[k]);
+    block_add(&A.G[k].ctrl->n_inserted, &A.G[k].ctrl->ins_total, added[k]);
+  }
 }
 
 // ------------------------------------------------------------------ delete / query
@@ -301,17 +324,21 @@ __device__ int group_find(const GraphDev& G, uint32_t u, uint32_t v, int l8, uin
 }
 
 template <bool MAP>
-__global__ void __launch_bounds__(UPD_BLOCK) k_delete(GraphDev G, const uint32_t* __restrict__ src,
-                                                      const uint32_t* __restrict__ dst, uint64_t n) {
+__global__ void __launch_bounds__(UPD_BLOCK) k_delete(const __grid_constant__ UpdArgs A) {
   const int lane = lane_id(), l8 = lane & 7, gbase = lane & 24;
   const uint32_t gmask = 0xFFu << gbase;
   const uint64_t ng = ((uint64_t)gridDim.x * blockDim.x) / GROUP;
-  uint32_t removed = 0, err = 0;
-  for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / GROUP; i < n; i += ng) {
-    const uint32_t u = src[i], v = dst[i];
-    if (u >= G.Vg || v >= G.Vg) { err |= ERR_RANGE; continue; }
+  uint32_t removed[2] = {0, 0}, err[2] = {0, 0};
+  const uint64_t total = A.n * A.ns;
+  for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / GROUP; i < total; i += ng) {
+    uint32_t st; uint64_t e;
+    upd_item(A, i, st, e);
+    const GraphDev& G = A.G[st];
+    const uint32_t a = A.src[e], b = A.dst[e];
+    const uint32_t u = st ? b : a, v = st ? a : b;
+    if (u >= G.Vg || v >= G.Vg) { err[st] |= ERR_RANGE; continue; }
     const uint32_t ul = local_row(G, u);
-    if (ul == INVALID_SLAB) { err |= ERR_PARTITION; continue; }
+    if (ul == INVALID_SLAB) { err[st] |= ERR_PARTITION; continue; }
     uint32_t slab; uint64_t val;
     const int c = group_find<MAP>(G, ul, v, l8, gmask, gbase, slab, val);
     if (c < 0 || l8 != 0) continue;
@@ -320,10 +347,12 @@ __global__ void __launch_bounds__(UPD_BLOCK) k_delete(GraphDev G, const uint32_t
     if (MAP) ok = atomicCAS(reinterpret_cast<unsigned long long*>(slab_ptr(G, slab) + 2 * c),
                             (unsigned long long)val, (unsigned long long)TOMB_PAIR) == val;
     else ok = atomicCAS(slab_ptr(G, slab) + c, (unsigned int)val, TOMBSTONE_KEY) == (unsigned int)val;
-    removed += ok;
+    removed[st] += ok;
   }
-  block_or_err(&G.ctrl->err, err);
-  block_add(&G.ctrl->n_deleted, &G.ctrl->del_total, removed);
+  for (uint32_t k = 0; k < A.ns; k++) {
+    block_or_err(&A.G[k].ctrl->err, err[k]);
+    block_add(&A.G[k].ctrl->n_deleted, &A.G[k].ctrl->del_total, removed[k]);
+  }
 }
 
 template <bool MAP>
@@ -576,20 +605,29 @@ out:
   return e;
 }
 
-cudaError_t launch_insert(meerkat_graph* g, Store& st, const uint32_t* s, const uint32_t* d, const uint32_t* w, uint64_t n) {
+cudaError_t launch_insert(meerkat_graph* g, Store* st0, Store* st1, const uint32_t* s, const uint32_t* d,
+                          const uint32_t* w, uint64_t n) {
   if (!n) return cudaSuccess;
-  const unsigned gb = grid_for(g, n, 0);
-  if (g->weighted) k_insert<true><<<gb, UPD_BLOCK, 0, g->stream>>>(st.dev, s, d, w, n);
-  else k_insert<false><<<gb, UPD_BLOCK, 0, g->stream>>>(st.dev, s, d, nullptr, n);
+  UpdArgs A{};
+  A.G[0] = st0->dev;
+  if (st1) A.G[1] = st1->dev;
+  A.src = s; A.dst = d; A.w = w; A.n = n; A.ns = st1 ? 2u : 1u;
+  const unsigned gb = grid_for(g, n * A.ns, 0);
+  if (g->weighted) k_insert<true><<<gb, UPD_BLOCK, 0, g->stream>>>(A);
+  else k_insert<false><<<gb, UPD_BLOCK, 0, g->stream>>>(A);
   g->launches++;
   return cudaGetLastError();
 }
 
-cudaError_t launch_delete(meerkat_graph* g, Store& st, const uint32_t* s, const uint32_t* d, uint64_t n) {
+cudaError_t launch_delete(meerkat_graph* g, Store* st0, Store* st1, const uint32_t* s, const uint32_t* d, uint64_t n) {
   if (!n) return cudaSuccess;
-  const unsigned gb = grid_for(g, n, 0);
-  if (g->weighted) k_delete<true><<<gb, UPD_BLOCK, 0, g->stream>>>(st.dev, s, d, n);
-  else k_delete<false><<<gb, UPD_BLOCK, 0, g->stream>>>(st.dev, s, d, n);
+  UpdArgs A{};
+  A.G[0] = st0->dev;
+  if (st1) A.G[1] = st1->dev;
+  A.src = s; A.dst = d; A.w = nullptr; A.n = n; A.ns = st1 ? 2u : 1u;
+  const unsigned gb = grid_for(g, n * A.ns, 0);
+  if (g->weighted) k_delete<true><<<gb, UPD_BLOCK, 0, g->stream>>>(A);
+  else k_delete<false><<<gb, UPD_BLOCK, 0, g->stream>>>(A);
   g->launches++;
   return cudaGetLastError();
 }
