@@ -33,7 +33,7 @@ u8p = ctypes.POINTER(ctypes.c_uint8)
 def build(force: bool = False) -> str:
     src = os.path.join(_HERE, "meerkat_oracle.c")
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(src):
-        subprocess.check_call(["gcc", "-O2", "-shared", "-fPIC", "-Wall", src, "-o", _SO])
+        subprocess.check_call(["gcc", "-O2", "-shared", "-fPIC", "-Wall", src, "-o", _SO, "-lm"])
     return _SO
 
 
@@ -62,6 +62,8 @@ def _L():
         L.orc_dec_frontier_count.argtypes = [vp, u64p, u8p]
         L.orc_check_tree.restype = ctypes.c_uint64
         L.orc_check_tree.argtypes = [vp, ctypes.c_uint32, ctypes.c_int, u64p, u32p]
+        L.orc_pagerank.argtypes = [vp, ctypes.c_double, ctypes.c_double, ctypes.c_uint32,
+                                   ctypes.POINTER(ctypes.c_double), u32p, ctypes.POINTER(ctypes.c_double)]
         _lib = L
     return _lib
 
@@ -132,6 +134,16 @@ class OracleGraph:
         node = np.empty(self.V, np.uint64)
         st = _L().orc_bfs(self._g, source, _p(node, u64p))
         return st, node
+
+    def pagerank(self, d: float = 0.85, eps: float = 1e-5, max_iter: int = 1000, pr=None):
+        """(status, pr f64[V], iterations, last delta).  pr=None: static start 1/V (P:855-856);
+        else a warm start from the given vector (dynamic PageRank)."""
+        x = np.full(self.V, 1.0 / self.V) if pr is None else np.array(pr, dtype=np.float64, copy=True)
+        it = ctypes.c_uint32(0)
+        dl = ctypes.c_double(0.0)
+        st = _L().orc_pagerank(self._g, float(d), float(eps), int(max_iter),
+                               x.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(it), ctypes.byref(dl))
+        return st, x, int(it.value), float(dl.value)
 
     def dec_frontier_count(self, node_old, invalid_flag) -> int:
         n = np.ascontiguousarray(node_old, dtype=np.uint64)

@@ -35,6 +35,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <math.h>
 
 enum { ORC_OK = 0, ORC_E_INVALID_ARG = 1, ORC_E_VERTEX_RANGE = 2, ORC_E_WEIGHT = 3,
        ORC_E_CAPACITY = 4, ORC_E_OVERFLOW = 5, ORC_E_STATE = 6 };
@@ -365,4 +366,64 @@ uint64_t orc_check_tree(const orc_graph* g, uint32_t SRC, int unit, const uint64
   free(best);
   if (first_bad) *first_bad = fb;
   return bad;
+}
+
+/*
+ * PageRank, static and dynamic ("Dynamic PageRank",
+ * Eq. (1) contribution-change P:834-836, Algorithm pr-all as narrated P:852-880;
+ * d = 0.85 and error margin 0.00001 are the paper's experimental values P:1559-1560).
+ * Double precision throughout (the paper states none; BASELINE.json asks 1e-6 relative L1).
+ *
+ * pr[] (in/out, length V) holds the starting vector: 1/vertex_n for every vertex in the
+ * static case, the values computed before the batch in the incremental /
+ * decremental case ("the same static-PageRank algorithm is applied on
+ * the entire graph after performing insertion/deletion").  One super-step i, in the paper's order:
+ *   FindContributionPerVertex: Contribution[u] = PR_{i-1}[u] / out[u] for out[u] > 0;
+ *   Compute (Eq. 1): PR_i[v] = (1-d)/N + d * sum over in-edges u->v of
+ *     Contribution[u];
+ *   FindTeleportProb (reading C27: the sum is scaled by d): if some vertex v_z has
+ *     out-degree 0, every PR_i[v] += d * (sum over such v_z of PR_{i-1}[v_z]) / N;
+ *   delta = sum_v |PR_i[v] - PR_{i-1}[v]| (the L1 norm).
+ * Super-steps repeat while delta > eps and fewer than max_iter have run (at least
+ * one).  Out-degrees count stored edges (self-loops included, C12).
+ * Returns ORC_E_INVALID_ARG for d not in (0,1), eps <= 0 or max_iter == 0 (SPEC BadDamping /
+ * BadEpsilon); *iters = super-steps run, *delta_out = the last delta.
+ */
+int orc_pagerank(const orc_graph* g, double d, double eps, uint32_t max_iter, double* pr, uint32_t* iters,
+                 double* delta_out) {
+  if (!(d > 0.0 && d < 1.0) || !(eps > 0.0) || max_iter == 0) return ORC_E_INVALID_ARG;
+  const uint32_t N = g->V;
+  uint32_t* out = (uint32_t*)calloc((size_t)N + 1, sizeof(uint32_t));
+  for (uint64_t i = 0; i < g->m; i++) out[g->key[i] >> 32]++;
+  int has_zero = 0;
+  for (uint32_t v = 0; v < N; v++) if (out[v] == 0) has_zero = 1;
+  double* contribution = (double*)malloc(((size_t)N + 1) * sizeof(double));
+  double* next = (double*)malloc(((size_t)N + 1) * sizeof(double));
+  uint32_t it = 0;
+  double delta = 0.0;
+  do {
+    /* FindContributionPerVertex */
+    for (uint32_t u = 0; u < N; u++) contribution[u] = out[u] ? pr[u] / (double)out[u] : 0.0;
+    /* Compute: (1-d)/N + d * sum over in-edges */
+    double* sum = next;
+    for (uint32_t v = 0; v < N; v++) sum[v] = 0.0;
+    for (uint64_t i = 0; i < g->m; i++) sum[(uint32_t)g->key[i]] += contribution[g->key[i] >> 32];
+    for (uint32_t v = 0; v < N; v++) next[v] = (1.0 - d) / (double)N + d * sum[v];
+    /* FindTeleportProb, added to every vertex */
+    if (has_zero) {
+      double z = 0.0;
+      for (uint32_t v = 0; v < N; v++) if (out[v] == 0) z += pr[v];
+      const double teleport = d * z / (double)N;
+      for (uint32_t v = 0; v < N; v++) next[v] += teleport;
+    }
+    /* L1 norm between PR_i and PR_{i-1} */
+    delta = 0.0;
+    for (uint32_t v = 0; v < N; v++) delta += fabs(next[v] - pr[v]);
+    memcpy(pr, next, (size_t)N * sizeof(double));
+    it++;
+  } while (delta > eps && it < max_iter);
+  free(next); free(contribution); free(out);
+  if (iters) *iters = it;
+  if (delta_out) *delta_out = delta;
+  return ORC_OK;
 }
