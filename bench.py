@@ -60,6 +60,9 @@ def parse():
                    help="decremental valid->invalid frontier: stream every slab (paper, P:156-164) or "
                         "read the in-edges of V_invalid from an in-edge mirror store")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--pagerank", action=argparse.BooleanOptionalAction, default=True,
+                   help="also time static and dynamic PageRank on the same graph (SURVEY §8(f) NEXT-1; "
+                        "needs the in-edge mirror, i.e. --frontier reverse)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-scale", type=int, default=20, help="R-MAT scale of the oracle's bounded sample")
     p.add_argument("--cpu-steps", type=int, default=8,
@@ -458,6 +461,42 @@ def store_sweep(args, dev, stream):
                         f"{'off' if args.no_hashing else 'on'} lf {args.lf}", "by_batch": out}
 
 
+def measure_pagerank(g, W, T, stream, flush, peak, peak_src):
+    """PageRank on the workload graph (d = 0.85, error margin 1e-5): static (cold start,
+    the s_b^n baseline), then dynamic (warm start) after a 100K-edge insert batch and
+    after the matching delete batch.  One persistent launch per run; CUDA events on the graph's stream."""
+    import torch
+    p = g.pagerank(0.85, 1e-5, 1000)          # allocation + a first static run (untimed)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def timed(fn):
+        flush.zero_()
+        a.record(stream)
+        fn()
+        b.record(stream)
+        b.synchronize()
+        return a.elapsed_time(b), p.stats()
+
+    st_ms, st = timed(p.recompute)
+    s, d, w = W.deletes[0]                      # deleted in warm-up step 0: absent now
+    g.insert(T(s), T(d), T(w), count=False)
+    inc_ms, inc = timed(p.update)
+    g.delete(T(s), T(d), count=False)
+    dec_ms, dec = timed(p.update)
+    p.close()
+    ach = st["alg_bytes"] / (st_ms * 1e-3) / 1e9
+    return {"damping": 0.85, "error_margin": 1e-5, "dtype": "f64",
+            "static_ms": st_ms, "static_iterations": st["iterations"],
+            "incremental_ms": inc_ms, "incremental_iterations": inc["iterations"],
+            "decremental_ms": dec_ms, "decremental_iterations": dec["iterations"],
+            "batch": int(len(s)),
+            "per_iteration": {"slabs": st["slabs"], "in_edges": st["in_edges"], "atomics": st["atomics"],
+                              "ms": st_ms / max(1, st["iterations"])},
+            "roofline": {"bound": "hbm", "kernel": "k_pagerank (static run)", "achieved": ach, "peak": peak,
+                         "unit": "GB/s", "frac": ach / peak, "alg_bytes_per_launch": st["alg_bytes"],
+                         "peak_source": peak_src}}
+
+
 def run_ours(args, ws, rank, local):
     import torch
 
@@ -525,6 +564,9 @@ def run_ours(args, ws, rank, local):
                "h2d_bytes_per_step": n * 4 * ((3 + 3 + 2 + 2) if args.fused else (3 + 3 + 2 + 2 + 2 + 2)),
                "d2h_bytes_per_step": 2 * 64,
                "ms_per_step": e_ms / K}
+    pagerank = None
+    if args.pagerank and args.frontier == "reverse" and ws == 1:
+        pagerank = measure_pagerank(g, W, T, stream, flush, peak, peak_src)
     g.close()
     del g, sp, bf
     torch.cuda.empty_cache()
@@ -584,6 +626,7 @@ def run_ours(args, ws, rank, local):
         "store": res["store"],
         "alt": alt,
         "store_sweep": sweep,
+        "pagerank": pagerank,
         "generate_s": gen_s,
     }
     if rank == 0:

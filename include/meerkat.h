@@ -54,6 +54,7 @@ extern "C" {
 
 typedef struct meerkat_graph meerkat_graph; /* opaque: slab store + metadata on one device */
 typedef struct meerkat_tree meerkat_tree;   /* opaque: one SSSP or BFS tree for one source */
+typedef struct meerkat_pagerank meerkat_pagerank; /* opaque: one PageRank vector of a graph */
 
 typedef enum {
   MEERKAT_OK = 0,
@@ -150,7 +151,7 @@ meerkat_status meerkat_export_edges(meerkat_graph* g, uint32_t* src, uint32_t* d
                                     uint64_t capacity, uint64_t* n_out);
 meerkat_status meerkat_stats_get(meerkat_graph* g, meerkat_stats* out); /* synchronises */
 /* Structural check of the slab store(s) (owner of every slab, next pointers, no leftover link
- * lock, finite chains, EMPTY-suffix invariant).  info[5] (host): violations, then the first one's
+ * lock, finite chains, EMPTY-suffix invariant, per-vertex degree table = live keys).  info[5] (host): violations, then the first one's
  * vertex, slab, next, kind.  MEERKAT_E_STATE if any; synchronises. */
 meerkat_status meerkat_check(meerkat_graph* g, uint64_t* info);
 
@@ -239,6 +240,43 @@ meerkat_status meerkat_memcpy(meerkat_graph* g, void* dst, const void* src, uint
 meerkat_status meerkat_route(meerkat_graph* g, int key_is_b, const uint32_t* a, const uint32_t* b,
                              const uint32_t* c, uint64_t n, uint32_t* out_a, uint32_t* out_b, uint32_t* out_c,
                              uint64_t* counts);
+
+/* ---------------------------------------------------------------------------------------------
+ * PageRank.  Eq. (1):
+ *   PR_i[v] = (1-d)/N + d * sum over in-edges u->v of PR_{i-1}[u] / out[u],
+ * plus d * (sum of PR_{i-1} over zero-out-degree vertices) / N added to every vertex when such a
+ * vertex exists (FindTeleportProb, reading C27), repeated until the L1 norm
+ * sum_v |PR_i[v] - PR_{i-1}[v]| <= error_margin or max_iter super-steps ran (at least
+ * one).  Double precision.  Out-degrees count stored edges (self-loops included).  The graph
+ * must keep the in-edge mirror (cfg.reverse = 1; the Compute kernel walks in-edges)
+ * and be unpartitioned (world_size 1), else MEERKAT_E_STATE.  MEERKAT_E_INVALID_ARG for a
+ * damping outside (0,1), error_margin <= 0 or max_iter 0 (SPEC BadDamping / BadEpsilon).
+ * Every call runs to convergence in one launch and synchronises the graph's stream.
+ * ------------------------------------------------------------------------------------------- */
+typedef struct {
+  uint64_t iterations; /* super-steps of the last run */
+  double delta;        /* its last L1 norm */
+  uint64_t slabs;      /* in-edge slabs streamed per super-step */
+  uint64_t in_edges;   /* live in-edges gathered per super-step */
+  uint64_t atomics;    /* per-vertex accumulator atomics per super-step */
+  uint64_t alg_bytes;  /* algorithmic bytes of the last run (DESIGN.md accounting) */
+  uint64_t version;    /* graph version the values reflect */
+  uint32_t warm;       /* 1 if the last run was warm-started (dynamic) */
+  uint32_t pad;
+} meerkat_pagerank_stats;
+
+/* Static PageRank (PR_0 = 1/N) of the current graph; *out receives the handle. */
+meerkat_status meerkat_pagerank_create(meerkat_graph* g, double damping, double error_margin, uint32_t max_iter,
+                                       meerkat_pagerank** out);
+/* Dynamic PageRank after insert/delete batches: the same algorithm on the whole
+ * graph, warm-started from the current values. */
+meerkat_status meerkat_pagerank_update(meerkat_graph* g, meerkat_pagerank* p);
+/* Static re-run from 1/N on the current graph (the s_b^n baseline). */
+meerkat_status meerkat_pagerank_recompute(meerkat_graph* g, meerkat_pagerank* p);
+/* PR[v] for every v (double, host or device [vertex_n]). */
+meerkat_status meerkat_pagerank_values(meerkat_pagerank* p, double* out);
+meerkat_status meerkat_pagerank_stats_get(meerkat_pagerank* p, meerkat_pagerank_stats* out);
+meerkat_status meerkat_pagerank_destroy(meerkat_pagerank* p);
 
 #ifdef __cplusplus
 }

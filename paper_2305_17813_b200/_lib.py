@@ -31,6 +31,8 @@ EXPORTS = [
     "meerkat_tree_nodes", "meerkat_tree_invalidated", "meerkat_tree_stats_get", "meerkat_tree_destroy",
     "meerkat_dtree_create", "meerkat_dtree_phase", "meerkat_memcpy", "meerkat_route", "meerkat_tree_timeline",
     "meerkat_check", "meerkat_trees_incremental", "meerkat_trees_decremental",
+    "meerkat_pagerank_create", "meerkat_pagerank_update", "meerkat_pagerank_recompute", "meerkat_pagerank_values",
+    "meerkat_pagerank_stats_get", "meerkat_pagerank_destroy",
 ]
 
 
@@ -67,6 +69,16 @@ class TreeStats(ctypes.Structure):
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}
+
+
+class PageRankStats(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_uint64), ("delta", ctypes.c_double), ("slabs", ctypes.c_uint64),
+                ("in_edges", ctypes.c_uint64), ("atomics", ctypes.c_uint64), ("alg_bytes", ctypes.c_uint64),
+                ("version", ctypes.c_uint64), ("warm", ctypes.c_uint32), ("pad", ctypes.c_uint32)]
+
+    def as_dict(self):
+        return {n: (float(getattr(self, n)) if n == "delta" else int(getattr(self, n)))
+                for n, _ in self._fields_ if n != "pad"}
 
 
 class DResult(ctypes.Structure):
@@ -118,6 +130,12 @@ def lib():
         "meerkat_dtree_phase": (ctypes.c_int, [vp, vp, ctypes.c_int, vp, vp, vp, u64, ctypes.POINTER(DResult)]),
         "meerkat_memcpy": (ctypes.c_int, [vp, vp, vp, u64]),
         "meerkat_route": (ctypes.c_int, [vp, ctypes.c_int, vp, vp, vp, u64, vp, vp, vp, pu64]),
+        "meerkat_pagerank_create": (ctypes.c_int, [vp, ctypes.c_double, ctypes.c_double, u32, pvp]),
+        "meerkat_pagerank_update": (ctypes.c_int, [vp, vp]),
+        "meerkat_pagerank_recompute": (ctypes.c_int, [vp, vp]),
+        "meerkat_pagerank_values": (ctypes.c_int, [vp, vp]),
+        "meerkat_pagerank_stats_get": (ctypes.c_int, [vp, ctypes.POINTER(PageRankStats)]),
+        "meerkat_pagerank_destroy": (ctypes.c_int, [vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

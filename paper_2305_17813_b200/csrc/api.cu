@@ -604,4 +604,94 @@ meerkat_status meerkat_route(meerkat_graph* g, int key_is_b, const uint32_t* a, 
                      out_c, counts);
 }
 
+/* ------------------------------------------------------------------ PageRank (pagerank.cu) */
+
+static meerkat_status pagerank_run(meerkat_graph* g, meerkat_pagerank* p, bool warm) {
+  DeviceGuard dg(g->device);
+  cudaError_t e = launch_pagerank(g, p, warm);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(p->hctrl, p->ctrl, sizeof(PRCtrl), cudaMemcpyDeviceToHost, g->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  if (e != cudaSuccess) { cudaGetLastError(); return MEERKAT_E_CUDA; }
+  p->version = g->version;
+  p->warm_last = warm;
+  return MEERKAT_OK;
+}
+
+meerkat_status meerkat_pagerank_create(meerkat_graph* g, double damping, double error_margin, uint32_t max_iter,
+                                       meerkat_pagerank** out) {
+  if (!g || !out) return MEERKAT_E_INVALID_ARG;
+  *out = nullptr;
+  if (!(damping > 0.0 && damping < 1.0) || !(error_margin > 0.0) || max_iter == 0) return MEERKAT_E_INVALID_ARG;
+  if (!g->reverse || g->ws > 1) return MEERKAT_E_STATE;   // Compute walks in-edges
+  DeviceGuard dg(g->device);
+  meerkat_pagerank* p = new (std::nothrow) meerkat_pagerank();
+  if (!p) return MEERKAT_E_CUDA;
+  p->g = g;
+  p->d = damping; p->eps = error_margin; p->max_iter = max_iter;
+  const size_t V = g->V;
+  cudaError_t e = cudaMalloc(&p->pr, V * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&p->contrib, V * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&p->acc, V * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&p->ctrl, sizeof(PRCtrl));
+  if (e == cudaSuccess) e = cudaMallocHost(&p->hctrl, sizeof(PRCtrl));
+  if (e == cudaSuccess) e = pagerank_occupancy(g->weighted, &p->blocks_per_sm);
+  if (e != cudaSuccess || p->blocks_per_sm <= 0) {
+    cudaGetLastError();
+    meerkat_pagerank_destroy(p);
+    return MEERKAT_E_CUDA;
+  }
+  const meerkat_status st = pagerank_run(g, p, false);
+  if (st != MEERKAT_OK) { meerkat_pagerank_destroy(p); return st; }
+  *out = p;
+  return MEERKAT_OK;
+}
+
+meerkat_status meerkat_pagerank_update(meerkat_graph* g, meerkat_pagerank* p) {
+  if (!g || !p || p->g != g) return MEERKAT_E_INVALID_ARG;
+  return pagerank_run(g, p, true);
+}
+
+meerkat_status meerkat_pagerank_recompute(meerkat_graph* g, meerkat_pagerank* p) {
+  if (!g || !p || p->g != g) return MEERKAT_E_INVALID_ARG;
+  return pagerank_run(g, p, false);
+}
+
+meerkat_status meerkat_pagerank_values(meerkat_pagerank* p, double* out) {
+  if (!p || !out) return MEERKAT_E_INVALID_ARG;
+  meerkat_graph* g = p->g;
+  DeviceGuard dg(g->device);
+  cudaError_t e = cudaMemcpyAsync(out, p->pr, (size_t)g->V * 8, cudaMemcpyDefault, g->stream);
+  if (e == cudaSuccess && !is_device_ptr(out)) e = cudaStreamSynchronize(g->stream);
+  return from_cuda(e);
+}
+
+meerkat_status meerkat_pagerank_stats_get(meerkat_pagerank* p, meerkat_pagerank_stats* out) {
+  if (!p || !out) return MEERKAT_E_INVALID_ARG;
+  const PRCtrl& c = *p->hctrl;   // copied back at the end of every run
+  std::memset(out, 0, sizeof(*out));
+  out->iterations = c.iters;
+  out->delta = c.last_delta;
+  out->slabs = c.slabs;
+  out->in_edges = c.keys;
+  out->atomics = c.atomics;
+  // algorithmic bytes: per super-step 128 B per slab + 4 B owner, 8 B Contribution
+  // gather per in-edge, 8 B atomicAdd per combined slab run, 44 B per vertex update (acc r/w, PR r/w,
+  // out[] r, Contribution w); plus the start, 28 B per vertex (PR r/w, out[] r, Contribution w, acc w)
+  const uint64_t V = p->g->V;
+  out->alg_bytes = c.iters * (c.slabs * 132 + c.keys * 8 + c.atomics * 8 + V * 44) + V * 28;
+  out->version = p->version;
+  out->warm = p->warm_last ? 1u : 0u;
+  return MEERKAT_OK;
+}
+
+meerkat_status meerkat_pagerank_destroy(meerkat_pagerank* p) {
+  if (!p) return MEERKAT_E_INVALID_ARG;
+  DeviceGuard dg(p->g->device);
+  cudaStreamSynchronize(p->g->stream);
+  cudaFree(p->pr); cudaFree(p->contrib); cudaFree(p->acc); cudaFree(p->ctrl);
+  if (p->hctrl) cudaFreeHost(p->hctrl);
+  delete p;
+  return MEERKAT_OK;
+}
+
 }  // extern "C"

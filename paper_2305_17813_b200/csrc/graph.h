@@ -29,6 +29,17 @@ struct TreeCtrl {
   unsigned long long tstamp[48];
 };
 
+// PageRank control block (pagerank.cu).  delta / dangling rotate over three slots per super-step.
+struct PRCtrl {
+  double delta[3];             // L1 norm of super-step i in slot i % 3
+  double dangling[3];          // sum of PR over zero-out-degree vertices, read by super-step i from slot i % 3
+  unsigned long long iters;    // super-steps run by the last call
+  double last_delta;
+  unsigned long long slabs;    // in-edge slabs streamed per super-step
+  unsigned long long keys;     // live in-edges gathered per super-step
+  unsigned long long atomics;  // acc[] atomics per super-step
+};
+
 struct TreeDev {
   uint64_t* node;        // packed <dist, parent> per vertex
   uint32_t* stamp;       // last epoch a vertex was enqueued (frontier de-duplication)
@@ -98,7 +109,24 @@ struct meerkat_tree {
   size_t bytes = 0;
 };
 
+struct meerkat_pagerank {
+  meerkat_graph* g = nullptr;
+  double d = 0.85, eps = 1e-5;
+  uint32_t max_iter = 0;
+  double* pr = nullptr;        // PR values [V]
+  double* contrib = nullptr;   // Contribution[u] = PR[u] / out[u]
+  double* acc = nullptr;       // per-vertex sum of in-edge contributions
+  mk::PRCtrl* ctrl = nullptr;
+  mk::PRCtrl* hctrl = nullptr;
+  int blocks_per_sm = 0;
+  uint64_t version = 0;        // graph version the values reflect
+  bool warm_last = false;
+};
+
 namespace mk {
+// pagerank.cu
+cudaError_t pagerank_occupancy(bool weighted, int* blocks_per_sm);
+cudaError_t launch_pagerank(meerkat_graph* g, meerkat_pagerank* p, bool warm);
 // store.cu
 cudaError_t launch_build(meerkat_graph* g, Store& st, const uint32_t* d_hints, uint64_t pool_request);
 void free_store(Store& st);

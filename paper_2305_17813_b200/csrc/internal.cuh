@@ -51,6 +51,8 @@ struct GraphDev {
   uint32_t* slabs;   // (H + P) slabs x 32 words: head arena [0, H) then pool [H, H + P)
   uint32_t* owner;   // source vertex of every slab (the paper's bucket_vertex[])
   uint2* vmeta;      // per vertex {first head slab | INVALID_SLAB, bucket_count}
+  uint32_t* deg;     // per vertex live keys (out-degree in the out store, in-degree in the mirror),
+                     // maintained by insert / delete; PageRank's out[u]
   GraphCtrl* ctrl;
   uint32_t V, H, P, seed;   // V: vertices held here (vmeta entries); H/P: arena / pool slabs
   uint32_t Vg;              // global vertex count: the key range

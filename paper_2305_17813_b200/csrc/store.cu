@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(UPD_BLOCK) k_insert(const __grid_constant__ Up
     if (ul == INVALID_SLAB) { err[st] |= ERR_PARTITION; continue; }
     const int r = group_insert<MAP>(G, ul, v, wt, l8, gmask, gbase);
     if (r < 0) err[st] |= ERR_CAPACITY;
-    else if (l8 == 0) added[st] += (uint32_t)r;
+    else if (l8 == 0 && r) { added[st]++; atomicAdd(G.deg + ul, 1u); }
   }
   for (uint32_t k = 0; k < A.ns; k++) {
     block_or_err(&A.G[k].ctrl->err, err[k]);
@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(UPD_BLOCK) k_delete(const __grid_constant__ Up
     if (MAP) ok = atomicCAS(reinterpret_cast<unsigned long long*>(slab_ptr(G, slab) + 2 * c),
                             (unsigned long long)val, (unsigned long long)TOMB_PAIR) == val;
     else ok = atomicCAS(slab_ptr(G, slab) + c, (unsigned int)val, TOMBSTONE_KEY) == (unsigned int)val;
-    removed[st] += ok;
+    if (ok) { removed[st]++; atomicSub(G.deg + ul, 1u); }
   }
   for (uint32_t k = 0; k < A.ns; k++) {
     block_or_err(&A.G[k].ctrl->err, err[k]);
@@ -482,17 +482,25 @@ __global__ void k_fill(uint32_t* __restrict__ slabs, uint64_t n_slabs, int map) 
 // One thread per vertex walks every slab list of the vertex and checks the store's
 // structural invariants: each slab's owner is the vertex, next pointers are INVALID
 // or pool slabs, no LINKING lock survives a kernel, chains are finite, and no slab
-// follows a slab that still has an EMPTY cell (EMPTY-suffix invariant, §4.2).
+// follows a slab that still has an EMPTY cell (EMPTY-suffix invariant, §4.2), and the
+// degree table equals the vertex's live keys (kind 8: info[2] = live keys, info[3] = deg).
 // info[0] = violations, info[1..4] = first violation (vertex, slab, next, kind).
 template <bool MAP>
 __global__ void k_fsck(GraphDev G, unsigned long long* info) {
   using F = Frag<MAP>;
   for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < G.V; u += (uint64_t)gridDim.x * blockDim.x) {
     const uint2 m = G.vmeta[u];
-    if (m.x == INVALID_SLAB) continue;
+    if (m.x == INVALID_SLAB) {   // no slab list yet: no edges
+      if (G.deg[u] != 0) {
+        const unsigned long long k = atomicAdd(&info[0], 1ull);
+        if (k == 0) { info[1] = u; info[2] = 0; info[3] = G.deg[u]; info[4] = 8; }
+      }
+      continue;
+    }
     int kind = 0;
     uint32_t bad_s = 0, bad_n = 0;
     if (m.x == LINKING) { kind = 1; }
+    uint32_t live = 0;
     for (uint32_t b = 0; b < m.y && !kind; b++) {
       uint32_t s = m.x + b, steps = 0;
       while (!kind) {
@@ -503,6 +511,7 @@ __global__ void k_fsck(GraphDev G, unsigned long long* info) {
         for (int w = 0; w < SLAB_WORDS - 1; w++) {
           const bool keyword = MAP ? ((w & 1) == 0 && w < 30) : true;
           if (keyword && p[w] == EMPTY_KEY) has_empty = true;
+          if (keyword && p[w] < G.Vg) live++;
         }
         const uint32_t nx = p[SLAB_WORDS - 1];
         if (nx == INVALID_SLAB) break;
@@ -513,6 +522,7 @@ __global__ void k_fsck(GraphDev G, unsigned long long* info) {
         s = nx;
       }
     }
+    if (!kind && live != G.deg[u]) { kind = 8; bad_s = live; bad_n = G.deg[u]; }   // degree table
     if (kind) {
       const unsigned long long k = atomicAdd(&info[0], 1ull);
       if (k == 0) { info[1] = u; info[2] = bad_s; info[3] = bad_n; info[4] = kind; }
@@ -582,11 +592,13 @@ cudaError_t launch_build(meerkat_graph* g, Store& st, const uint32_t* d_hints, u
     CK(cudaMalloc(&st.dev.slabs, nslab * 128));             // ONE allocation: head arena + pool
     CK(cudaMalloc(&st.dev.owner, nslab * 4));
     CK(cudaMalloc(&st.dev.vmeta, (size_t)V * 8));
+    CK(cudaMalloc(&st.dev.deg, (size_t)V * 4));
+    CK(cudaMemsetAsync(st.dev.deg, 0, (size_t)V * 4, g->stream));
     CK(cudaMalloc(&st.dev.ctrl, sizeof(GraphCtrl)));
     CK(cudaMemsetAsync(st.dev.ctrl, 0, sizeof(GraphCtrl), g->stream));
     CK(cudaMallocHost(&st.hctrl, sizeof(GraphCtrl)));
     memset(st.hctrl, 0, sizeof(GraphCtrl));
-    st.bytes = nslab * 132 + (size_t)V * 8 + sizeof(GraphCtrl);
+    st.bytes = nslab * 132 + (size_t)V * 12 + sizeof(GraphCtrl);
     st.dev.V = V; st.dev.H = (uint32_t)st.H; st.dev.P = (uint32_t)st.P;
     st.dev.Vg = g->V; st.dev.ws = g->ws; st.dev.rank = g->rank;
     if (st.H) {
@@ -674,6 +686,7 @@ void free_store(Store& st) {
   cudaFree(st.dev.slabs);
   cudaFree(st.dev.owner);
   cudaFree(st.dev.vmeta);
+  cudaFree(st.dev.deg);
   cudaFree(st.dev.ctrl);
   if (st.hctrl) cudaFreeHost(st.hctrl);
   st = Store{};

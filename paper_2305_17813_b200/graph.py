@@ -69,12 +69,15 @@ class Graph:
         self.rank = int(rank)
         self.device = int(device)
         self._trees = []
+        self._pageranks = []
 
     # ------------------------------------------------------------------ lifecycle
     def close(self):
         if getattr(self, "_h", None):
             for t in list(self._trees):
                 t.close()
+            for p in list(self._pageranks):
+                p.close()
             _lib.lib().meerkat_destroy(self._h)
             self._h = None
 
@@ -175,6 +178,10 @@ class Graph:
         arr = (ctypes.c_void_p * len(trees))(*[t._h.value for t in trees])
         check(_lib.lib().meerkat_trees_decremental(self._h, arr, len(trees), sp, dp, n), "meerkat_trees_decremental")
 
+    def pagerank(self, damping: float = 0.85, error_margin: float = 1e-5, max_iter: int = 1000) -> "PageRank":
+        """Static PageRank of the current graph (needs reverse=True: in-edge mirror)."""
+        return PageRank(self, damping, error_margin, max_iter)
+
     def sssp(self, source: int) -> "Tree":
         return Tree(self, source, unit=False)
 
@@ -254,4 +261,45 @@ class Tree:
     def stats(self) -> dict:
         st = _lib.TreeStats()
         check(_lib.lib().meerkat_tree_stats_get(self._h, ctypes.byref(st)), "meerkat_tree_stats_get")
+        return st.as_dict()
+
+
+class PageRank:
+    """PageRank vector of a graph: static on creation, dynamic (warm-started) by update()."""
+
+    def __init__(self, graph: Graph, damping: float, error_margin: float, max_iter: int):
+        h = ctypes.c_void_p()
+        check(_lib.lib().meerkat_pagerank_create(graph._h, float(damping), float(error_margin), int(max_iter),
+                                                 ctypes.byref(h)), "meerkat_pagerank_create")
+        self._h = h
+        self.graph = graph
+        graph._pageranks.append(self)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.lib().meerkat_pagerank_destroy(self._h)
+            self._h = None
+            if self in self.graph._pageranks:
+                self.graph._pageranks.remove(self)
+
+    def update(self):
+        """Dynamic PageRank after batches: warm start from the current values."""
+        check(_lib.lib().meerkat_pagerank_update(self.graph._h, self._h), "meerkat_pagerank_update")
+
+    def recompute(self):
+        check(_lib.lib().meerkat_pagerank_recompute(self.graph._h, self._h), "meerkat_pagerank_recompute")
+
+    def values(self, out=None):
+        """PR as a float64 numpy array (or into a given float64 CUDA tensor)."""
+        if out is not None:
+            check(_lib.lib().meerkat_pagerank_values(self._h, ctypes.c_void_p(out.data_ptr())),
+                  "meerkat_pagerank_values")
+            return out
+        a = np.empty(self.graph.vertex_n, np.float64)
+        check(_lib.lib().meerkat_pagerank_values(self._h, ctypes.c_void_p(a.ctypes.data)), "meerkat_pagerank_values")
+        return a
+
+    def stats(self) -> dict:
+        st = _lib.PageRankStats()
+        check(_lib.lib().meerkat_pagerank_stats_get(self._h, ctypes.byref(st)), "meerkat_pagerank_stats_get")
         return st.as_dict()
