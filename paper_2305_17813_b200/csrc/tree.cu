@@ -84,40 +84,120 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const TreeDev& T, int 
     }
     fresh = false;
     const bool use = active && !dead;
+    // All loads / atomics of one phase are issued for every key of the slab before any result is
+    // consumed, so one slab step costs one dependent round trip per phase (not per key).
+    bool has[NK];
+    uint32_t xs[NK];
+    uint2 mv[NK];
 #pragma unroll
-    for (int kk = 0; kk < NK; kk++) {
-      const uint32_t x = F::key(d, kk);
-      const bool live = use && F::valid_cell(l8, kk) && x != EMPTY_KEY && x != TOMBSTONE_KEY;
-      bool enq = false;
-      if (live) {
-        c.visited++;
-        if (VISIT == RELAX) {
-          const uint32_t w = T.unit ? 1u : F::weight(d, kk);
-          enq = relax(T, x, (uint64_t)du + w, v, epoch_next, c, probe);
-        } else if (VISIT == PULL) {
-          // in-edge (x -> v) of invalid v: a valid->invalid frontier edge iff x is valid and reached
-          // (C15); relax v from it
-          if (!bit_test(T.inval_bits, x)) {
-            const uint64_t nx = ld_cg_u64(T.node + x);
-            if (nx != UNREACHED) {
-              c.hits[k]++;
-              const uint32_t w = T.unit ? 1u : F::weight(d, kk);
-              enq = relax(T, v, (nx >> 32) + w, x, epoch_next, c, false);
-            }
-          }
-        } else {
-          // PropagateInvalidation, top-down (C14): a child x of invalid v in T_G
-          const uint64_t cur = ld_cg_u64(T.node + x);
-          if (cur != UNREACHED && (uint32_t)cur == v && x != T.source) {
-            if (atomicCAS(reinterpret_cast<unsigned long long*>(T.node + x), (unsigned long long)cur,
-                          (unsigned long long)UNREACHED) == cur) {
-              mark_invalid(T, x);
-              enq = true;
-            }
-          }
+    for (int kk = 0; kk < NK; kk++) { has[kk] = false; xs[kk] = F::key(d, kk); mv[kk] = make_uint2(INVALID_SLAB, 0); }
+    if (VISIT == RELAX) {
+      // relax: candidate <d(v) + w, v> into node[x]
+      bool live[NK];
+      uint64_t cand[NK];
+#pragma unroll
+      for (int kk = 0; kk < NK; kk++) {
+        const uint32_t x = xs[kk];
+        live[kk] = use && F::valid_cell(l8, kk) && x != EMPTY_KEY && x != TOMBSTONE_KEY;
+        cand[kk] = 0;
+        if (live[kk]) {
+          c.visited++;
+          const uint64_t dist = (uint64_t)du + (T.unit ? 1u : F::weight(d, kk));
+          if (dist >= INF_DIST) { c.err |= ERR_OVERFLOW; live[kk] = false; }   // C5
+          cand[kk] = (dist << 32) | v;
         }
       }
-      warp_enqueue(G, T, fnext, sznext, enq, VISIT == PULL ? v : x, c);
+      if (probe) {   // node[] only decreases: a stale read can only cost a spare atomic
+        uint64_t pv[NK];
+#pragma unroll
+        for (int kk = 0; kk < NK; kk++) pv[kk] = live[kk] ? ld_cg_u64(T.node + xs[kk]) : 0ull;
+#pragma unroll
+        for (int kk = 0; kk < NK; kk++) live[kk] = live[kk] && cand[kk] < pv[kk];
+      }
+      unsigned long long old[NK];
+#pragma unroll
+      for (int kk = 0; kk < NK; kk++)
+        old[kk] = live[kk] ? atomicMin(reinterpret_cast<unsigned long long*>(T.node + xs[kk]),
+                                       (unsigned long long)cand[kk]) : 0ull;
+      uint32_t st[NK];
+#pragma unroll
+      for (int kk = 0; kk < NK; kk++) {
+        st[kk] = epoch_next;
+        if (live[kk] && cand[kk] < old[kk]) {   // improved: de-dup stamp and vmeta together
+          c.improved++;
+          st[kk] = atomicExch(T.stamp + xs[kk], epoch_next);
+          mv[kk] = __ldcg(G.vmeta + xs[kk]);
+        }
+      }
+#pragma unroll
+      for (int kk = 0; kk < NK; kk++) has[kk] = st[kk] != epoch_next;
+      warp_enqueue_multi<NK>(T, fnext, sznext, has, xs, mv, c);
+    } else if (VISIT == PROPAGATE) {
+      // PropagateInvalidation, top-down (C14): the children x (parent(x) = v) of invalid v
+      bool live[NK];
+      uint64_t cur[NK];
+#pragma unroll
+      for (int kk = 0; kk < NK; kk++) {
+        const uint32_t x = xs[kk];
+        live[kk] = use && F::valid_cell(l8, kk) && x != EMPTY_KEY && x != TOMBSTONE_KEY;
+        cur[kk] = live[kk] ? ld_cg_u64(T.node + x) : UNREACHED;
+        if (live[kk]) c.visited++;
+      }
+#pragma unroll
+      for (int kk = 0; kk < NK; kk++) {
+        const uint32_t x = xs[kk];
+        if (cur[kk] != UNREACHED && (uint32_t)cur[kk] == v && x != T.source &&
+            atomicCAS(reinterpret_cast<unsigned long long*>(T.node + x), (unsigned long long)cur[kk],
+                      (unsigned long long)UNREACHED) == cur[kk]) {
+          mark_invalid(T, x);
+          mv[kk] = __ldcg(G.vmeta + x);
+          has[kk] = true;
+        }
+      }
+      warp_enqueue_multi<NK>(T, fnext, sznext, has, xs, mv, c);
+    } else {
+      // PULL: in-edges (x -> v) of invalid v; a valid->invalid frontier edge iff x is valid and
+      // reached (C15).  The group's candidates for v are min-reduced first: one atomicMin
+      // per slab (the min of the candidates is what the per-edge atomics would leave).
+      uint32_t bw[NK];
+      uint64_t nx[NK];
+      bool live[NK];
+#pragma unroll
+      for (int kk = 0; kk < NK; kk++) {
+        const uint32_t x = xs[kk];
+        live[kk] = use && F::valid_cell(l8, kk) && x != EMPTY_KEY && x != TOMBSTONE_KEY;
+        bw[kk] = live[kk] ? __ldcg(T.inval_bits + (x >> 5)) : 0u;
+        nx[kk] = live[kk] ? ld_cg_u64(T.node + x) : UNREACHED;
+        if (live[kk]) c.visited++;
+      }
+      uint64_t best = UNREACHED;
+#pragma unroll
+      for (int kk = 0; kk < NK; kk++) {
+        const uint32_t x = xs[kk];
+        if (live[kk] && !((bw[kk] >> (x & 31)) & 1u) && nx[kk] != UNREACHED) {
+          c.hits[k]++;
+          const uint64_t dist = (nx[kk] >> 32) + (T.unit ? 1u : F::weight(d, kk));
+          if (dist >= INF_DIST) c.err |= ERR_OVERFLOW;   // C5
+          else best = min(best, (dist << 32) | x);
+        }
+      }
+      best = min(best, (uint64_t)__shfl_xor_sync(FULL, (unsigned long long)best, 1));
+      best = min(best, (uint64_t)__shfl_xor_sync(FULL, (unsigned long long)best, 2));
+      best = min(best, (uint64_t)__shfl_xor_sync(FULL, (unsigned long long)best, 4));
+      bool hv[1] = {false};
+      uint32_t xv[1] = {v};
+      uint2 mv1[1] = {make_uint2(INVALID_SLAB, 0)};
+      if (l8 == 0 && best != UNREACHED) {
+        const unsigned long long o = atomicMin(reinterpret_cast<unsigned long long*>(T.node + v),
+                                               (unsigned long long)best);
+        if (best < o) {
+          c.improved++;
+          const uint32_t stv = atomicExch(T.stamp + v, epoch_next);
+          mv1[0] = __ldcg(G.vmeta + v);
+          hv[0] = stv != epoch_next;
+        }
+      }
+      warp_enqueue_multi<1>(T, fnext, sznext, hv, xv, mv1, c);
     }
     const uint32_t nxt = __shfl_sync(FULL, d.w, (lane & 24) + GROUP - 1);
     if (active) {

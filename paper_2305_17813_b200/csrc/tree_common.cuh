@@ -100,6 +100,56 @@ __device__ __forceinline__ void warp_enqueue(const GraphDev& G, const TreeDev& T
   }
 }
 
+// warpenqueuefrontier for up to NK candidates per lane (one slab step of an expansion): lane
+// candidate k appends the bucket items of vertex x[k] (head slab / bucket count in m[k], read
+// by the caller together with its other loads) when has[k].  One atomicAdd per warp.
+template <int NK>
+__device__ __forceinline__ void warp_enqueue_multi(const TreeDev& T, uint64_t* fr, unsigned long long* sz,
+                                                   const bool (&has)[NK], const uint32_t (&x)[NK],
+                                                   const uint2 (&m)[NK], Counters& c) {
+  uint32_t cnt[NK], mine = 0;
+#pragma unroll
+  for (int k = 0; k < NK; k++) {
+    cnt[k] = (has[k] && m[k].x != INVALID_SLAB) ? m[k].y : 0u;   // no head slab: no out-edges
+    mine += cnt[k];
+  }
+  if (!__any_sync(FULL, mine != 0)) return;
+  const int lane = lane_id();
+  uint32_t incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const uint32_t total = __shfl_sync(FULL, incl, 31);
+  unsigned long long base = 0;
+  if (lane == 31) base = atomicAdd(sz, (unsigned long long)total);
+  base = __shfl_sync(FULL, base, 31);
+  if (base + total > T.fr_cap) { c.err |= ERR_CAPACITY; return; }
+  uint64_t off[NK];
+  uint64_t o = base + incl - mine;
+#pragma unroll
+  for (int k = 0; k < NK; k++) {
+    off[k] = o;
+    o += cnt[k];
+    if (cnt[k] <= 8)
+      for (uint32_t j = 0; j < cnt[k]; j++) fr[off[k] + j] = ((uint64_t)(m[k].x + j) << 32) | x[k];
+  }
+#pragma unroll
+  for (int k = 0; k < NK; k++) {
+    uint32_t big = __ballot_sync(FULL, cnt[k] > 8);
+    while (big) {   // hubs: the whole warp writes the items
+      const int l = __ffs(big) - 1;
+      big &= big - 1;
+      const uint32_t xb = __shfl_sync(FULL, x[k], l);
+      const uint32_t hb = __shfl_sync(FULL, m[k].x, l);
+      const uint64_t ob = __shfl_sync(FULL, off[k], l);
+      const uint32_t cb = __shfl_sync(FULL, cnt[k], l);
+      for (uint32_t j = lane; j < cb; j += 32) fr[ob + j] = ((uint64_t)(hb + j) << 32) | xb;
+    }
+  }
+}
+
 __device__ __forceinline__ void mark_invalid(const TreeDev& T, uint32_t x) {
   atomicOr(T.inval_bits + (x >> 5), 1u << (x & 31));
   const unsigned long long i = atomicAdd(&T.ctrl->inval_n, 1ull);
