@@ -149,11 +149,11 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const TreeDev& T, int 
         if (cur[kk] != UNREACHED && (uint32_t)cur[kk] == v && x != T.source &&
             atomicCAS(reinterpret_cast<unsigned long long*>(T.node + x), (unsigned long long)cur[kk],
                       (unsigned long long)UNREACHED) == cur[kk]) {
-          mark_invalid(T, x);
           mv[kk] = __ldcg(G.vmeta + x);
           has[kk] = true;
         }
       }
+      warp_mark_invalid<NK>(T, has, xs);
       warp_enqueue_multi<NK>(T, fnext, sznext, has, xs, mv, c);
     } else {
       // PULL: in-edges (x -> v) of invalid v; a valid->invalid frontier edge iff x is valid and
@@ -295,18 +295,48 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_inc(const __grid_constan
       c.batch++;
       ok = u < A.G.V && v < A.G.V;   // invalid edges were skipped at insert too
     }
+    // phase-wise over the trees: node[u] of every tree, then the atomicMins, then stamp + vmeta
+    uint64_t cand[MAX_TREES];
+    bool live[MAX_TREES];
 #pragma unroll
     for (int k = 0; k < MAX_TREES; k++) {
-      if (k >= (int)A.ntrees) break;
       const TreeDev& T = A.T[k];
       const uint32_t wk = T.unit ? 1u : w;
-      bool enq = false;
-      if (ok && (T.unit || (wk != 0 && wk < W_LIMIT))) {
-        const uint64_t nu = ld_cg_u64(T.node + u);
-        if (nu != UNREACHED) enq = relax(T, v, (nu >> 32) + wk, u, epoch[k], c, false);
-      }
-      warp_enqueue(A.G, T, T.fr[0], &T.ctrl->size[0], enq, v, c);
+      live[k] = k < (int)A.ntrees && ok && (T.unit || (wk != 0 && wk < W_LIMIT));
+      cand[k] = live[k] ? ld_cg_u64(T.node + u) : UNREACHED;   // node[u], turned into the candidate below
     }
+#pragma unroll
+    for (int k = 0; k < MAX_TREES; k++) {
+      const TreeDev& T = A.T[k];
+      if (live[k] && cand[k] != UNREACHED) {
+        const uint64_t dist = (cand[k] >> 32) + (T.unit ? 1u : w);
+        if (dist >= INF_DIST) { c.err |= ERR_OVERFLOW; live[k] = false; }   // C5
+        cand[k] = (dist << 32) | u;
+      } else {
+        live[k] = false;
+      }
+    }
+    unsigned long long old[MAX_TREES];
+#pragma unroll
+    for (int k = 0; k < MAX_TREES; k++)
+      old[k] = live[k] ? atomicMin(reinterpret_cast<unsigned long long*>(A.T[k].node + v),
+                                   (unsigned long long)cand[k]) : 0ull;
+    bool has[MAX_TREES][1];
+    uint2 m[MAX_TREES][1];
+#pragma unroll
+    for (int k = 0; k < MAX_TREES; k++) {
+      has[k][0] = false;
+      m[k][0] = make_uint2(INVALID_SLAB, 0);
+      if (live[k] && cand[k] < old[k]) {
+        c.improved++;
+        has[k][0] = atomicExch(A.T[k].stamp + v, epoch[k]) != epoch[k];
+        m[k][0] = __ldcg(A.G.vmeta + v);
+      }
+    }
+    const uint32_t xv[1] = {v};
+#pragma unroll
+    for (int k = 0; k < MAX_TREES; k++)
+      if (k < (int)A.ntrees) warp_enqueue_multi<1>(A.T[k], A.T[k].fr[0], &A.T[k].ctrl->size[0], has[k], xv, m[k], c);
   }
   grid.sync();
   timeline(A.T[0].ctrl);
@@ -421,22 +451,27 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_dec(const __grid_constan
       c.batch++;
       ok = u < A.G.V && v < A.G.V;
     }
+    // phase-wise over the trees: node[v] of every tree, then the CASes, then list + enqueue
+    uint64_t cur[MAX_TREES];
+#pragma unroll
+    for (int k = 0; k < MAX_TREES; k++)
+      cur[k] = (k < (int)A.ntrees && ok && v != A.T[k].source) ? ld_cg_u64(A.T[k].node + v) : UNREACHED;
+    bool has[MAX_TREES][1];
+    uint2 m[MAX_TREES][1];
+#pragma unroll
+    for (int k = 0; k < MAX_TREES; k++) {
+      has[k][0] = cur[k] != UNREACHED && (uint32_t)cur[k] == u &&
+                  atomicCAS(reinterpret_cast<unsigned long long*>(A.T[k].node + v), (unsigned long long)cur[k],
+                            (unsigned long long)UNREACHED) == cur[k];
+      m[k][0] = has[k][0] ? __ldcg(A.G.vmeta + v) : make_uint2(INVALID_SLAB, 0);
+      c.direct[k] += has[k][0];
+    }
+    const uint32_t xv[1] = {v};
 #pragma unroll
     for (int k = 0; k < MAX_TREES; k++) {
       if (k >= (int)A.ntrees) break;
-      const TreeDev& T = A.T[k];
-      bool enq = false;
-      if (ok && v != T.source) {
-        const uint64_t cur = ld_cg_u64(T.node + v);
-        if (cur != UNREACHED && (uint32_t)cur == u &&
-            atomicCAS(reinterpret_cast<unsigned long long*>(T.node + v), (unsigned long long)cur,
-                      (unsigned long long)UNREACHED) == cur) {
-          mark_invalid(T, v);
-          atomicAdd(&T.ctrl->direct_n, 1ull);
-          enq = true;
-        }
-      }
-      warp_enqueue(A.G, T, T.fr[0], &T.ctrl->size[0], enq, v, c);
+      warp_mark_invalid<1>(A.T[k], has[k], xv);
+      warp_enqueue_multi<1>(A.T[k], A.T[k].fr[0], &A.T[k].ctrl->size[0], has[k], xv, m[k], c);
     }
   }
   grid.sync();

@@ -43,6 +43,7 @@ __device__ __forceinline__ void clear_next_ctrl(TreeCtrl* p) {
 struct Counters {
   uint32_t items = 0, slabs = 0, visited = 0, improved = 0, scan_slabs = 0, batch = 0, err = 0;
   uint32_t hits[MAX_TREES] = {};
+  uint32_t direct[MAX_TREES] = {};   // vertices invalidated directly by a deleted tree edge
 };
 
 __device__ __forceinline__ bool bit_test(const uint32_t* bits, uint32_t x) {
@@ -150,6 +151,30 @@ __device__ __forceinline__ void warp_enqueue_multi(const TreeDev& T, uint64_t* f
   }
 }
 
+// mark_invalid for up to NK vertices per lane, one atomicAdd on the list length per warp
+// (a per-vertex atomicAdd serialises thousands of same-address atomics at one L2 slice).
+template <int NK>
+__device__ __forceinline__ void warp_mark_invalid(const TreeDev& T, const bool (&has)[NK], const uint32_t (&x)[NK]) {
+  uint32_t mine = 0;
+#pragma unroll
+  for (int k = 0; k < NK; k++)
+    if (has[k]) { atomicOr(T.inval_bits + (x[k] >> 5), 1u << (x[k] & 31)); mine++; }
+  if (!__any_sync(FULL, mine != 0)) return;
+  const int lane = lane_id();
+  uint32_t incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += y;
+  }
+  unsigned long long base = 0;
+  if (lane == 31) base = atomicAdd(&T.ctrl->inval_n, (unsigned long long)incl);
+  base = __shfl_sync(FULL, base, 31) + incl - mine;
+#pragma unroll
+  for (int k = 0; k < NK; k++)
+    if (has[k]) T.inval_list[base++] = x[k];
+}
+
 __device__ __forceinline__ void mark_invalid(const TreeDev& T, uint32_t x) {
   atomicOr(T.inval_bits + (x >> 5), 1u << (x & 31));
   const unsigned long long i = atomicAdd(&T.ctrl->inval_n, 1ull);
@@ -176,26 +201,27 @@ __device__ __forceinline__ bool relax(const TreeDev& T, uint32_t x, uint64_t dis
 // counter on the kernel's tail).  All threads of the block must call it.
 __device__ __forceinline__ void flush_counters(const GraphDev& G, const TreeDev& T, Counters& c, int k,
                                                bool rounds_owner, uint32_t relax_rounds, uint32_t prop_rounds) {
-  __shared__ unsigned long long acc[8];
+  constexpr int NV = 8;
+  __shared__ unsigned long long acc[NV + 1];
   TreeCtrl* tc = T.ctrl;
-  if (threadIdx.x < 8) acc[threadIdx.x] = 0;
+  if (threadIdx.x <= NV) acc[threadIdx.x] = 0;
   __syncthreads();
   auto red = [](uint32_t v) { return __reduce_add_sync(FULL, v); };
-  const uint32_t v[7] = {red(c.items), red(c.slabs), red(c.visited), red(c.improved), red(c.scan_slabs),
-                         red(c.hits[k]), red(c.batch)};
+  const uint32_t v[NV] = {red(c.items), red(c.slabs), red(c.visited), red(c.improved), red(c.scan_slabs),
+                          red(c.hits[k]), red(c.batch), red(c.direct[k])};
   const uint32_t err = __reduce_or_sync(FULL, c.err);
   if (lane_id() == 0) {
 #pragma unroll
-    for (int i = 0; i < 7; i++)
+    for (int i = 0; i < NV; i++)
       if (v[i]) atomicAdd(&acc[i], (unsigned long long)v[i]);
-    if (err) atomicOr(reinterpret_cast<unsigned int*>(&acc[7]), err);
+    if (err) atomicOr(reinterpret_cast<unsigned int*>(&acc[NV]), err);
   }
   __syncthreads();
-  if (threadIdx.x < 8 && acc[threadIdx.x]) {
-    unsigned long long* dst[7] = {&tc->items, &tc->slabs_read, &tc->visited, &tc->improved, &tc->scan_slabs,
-                                  &tc->scan_hits, &tc->batch_edges};
-    if (threadIdx.x < 7) atomicAdd(dst[threadIdx.x], acc[threadIdx.x]);
-    else atomicOr(&G.ctrl->err, (unsigned int)acc[7]);
+  if (threadIdx.x <= NV && acc[threadIdx.x]) {
+    unsigned long long* dst[NV] = {&tc->items, &tc->slabs_read, &tc->visited, &tc->improved, &tc->scan_slabs,
+                                   &tc->scan_hits, &tc->batch_edges, &tc->direct_n};
+    if (threadIdx.x < NV) atomicAdd(dst[threadIdx.x], acc[threadIdx.x]);
+    else atomicOr(&G.ctrl->err, (unsigned int)acc[NV]);
   }
   if (rounds_owner) { tc->rounds = relax_rounds; tc->prop_rounds = prop_rounds; }
 }
