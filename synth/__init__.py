@@ -48,7 +48,7 @@ def _L():
         lib.synth_rmat_draws.restype = None
         lib.synth_rmat_draws.argtypes = [ctypes.c_uint32, ctypes.c_uint64, ctypes.c_double, ctypes.c_double,
                                          ctypes.c_double, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int,
-                                         ctypes.c_uint64, u32p, u32p, u32p]
+                                         ctypes.c_uint64, ctypes.c_uint64, u32p, u32p, u32p]
         lib.synth_scramble.restype = ctypes.c_uint32
         lib.synth_scramble.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64]
         lib.synth_draw.restype = ctypes.c_uint64
@@ -75,12 +75,15 @@ def rmat(scale: int, ef: int, seed_graph: int = SEED_GRAPH, seed_w: int = SEED_W
     return s[:m].copy(), d[:m].copy(), w[:m].copy()
 
 
-def rmat_draws(scale: int, n: int, first: int, seed_graph: int, seed_w: int = SEED_W, scramble: bool = True):
-    """n raw R-MAT draws (duplicates and self-loops kept) starting at draw index `first`."""
+def rmat_draws(scale: int, n: int, first: int, seed_graph: int, seed_w: int = SEED_W, scramble: bool = True,
+               scramble_seed: int = SEED_GRAPH):
+    """n raw R-MAT draws (duplicates and self-loops kept) starting at draw index `first`, from
+    seed_graph's stream; ids scrambled with scramble_seed (default: the base graph's labelling,
+    so the fresh edges' hubs are the base graph's hubs)."""
     s = np.empty(n, np.uint32)
     d = np.empty(n, np.uint32)
     w = np.empty(n, np.uint32)
-    _L().synth_rmat_draws(scale, n, RMAT_A, RMAT_B, RMAT_C, seed_graph, seed_w, int(scramble), first,
+    _L().synth_rmat_draws(scale, n, RMAT_A, RMAT_B, RMAT_C, seed_graph, seed_w, int(scramble), scramble_seed, first,
                           _p32(s), _p32(d), _p32(w))
     return s, d, w
 

@@ -211,9 +211,11 @@ int synth_sample_distinct(uint64_t m, uint64_t k, uint64_t seed, uint64_t* out) 
   return 0;
 }
 
-/* Fresh R-MAT draws (not deduplicated against anything): for config-2 insert sweeps. */
+/* Fresh R-MAT draws (not deduplicated against anything): for config-2 insert sweeps.  The draws
+ * come from seed_graph's stream; ids are scrambled with seed_scramble (pass the base graph's seed
+ * so the fresh edges follow the base graph's vertex labelling: its hubs are their hubs). */
 void synth_rmat_draws(uint32_t scale, uint64_t n, double a, double b, double c, uint64_t seed_graph,
-                      uint64_t seed_w, int scramble, uint64_t first,
+                      uint64_t seed_w, int scramble, uint64_t seed_scramble, uint64_t first,
                       uint32_t* out_src, uint32_t* out_dst, uint32_t* out_w) {
   const double ab = a + b, abc = a + b + c;
 #pragma omp parallel for schedule(static)
@@ -221,7 +223,7 @@ void synth_rmat_draws(uint32_t scale, uint64_t n, double a, double b, double c, 
     uint64_t gi = first + (uint64_t)i;
     uint32_t u = 0, v = 0;
     rmat_edge(scale, a, ab, abc, seed_graph, gi, &u, &v);
-    if (scramble) { u = synth_scramble(u, scale, seed_graph); v = synth_scramble(v, scale, seed_graph); }
+    if (scramble) { u = synth_scramble(u, scale, seed_scramble); v = synth_scramble(v, scale, seed_scramble); }
     out_src[i] = u; out_dst[i] = v;
     out_w[i] = 1 + (uint32_t)(draw(seed_w, 2, gi) % 64);
   }

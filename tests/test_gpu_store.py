@@ -189,7 +189,7 @@ def test_fresh_draw_stress_with_fsck(hashing):
     assert g.insert(cuda(s), cuda(d), cuda(w)) == o.insert(s, d, w)[1]
     assert g.check()[0] == 0
     for r in range(4):
-        fs, fd, fw = synth.rmat_draws(scale, 200000, r * 200000, 11)
+        fs, fd, fw = synth.rmat_draws(scale, 200000, r * 200000, 11, scramble_seed=11)
         assert g.insert(cuda(fs), cuda(fd), cuda(fw)) == o.insert(fs, fd, fw)[1]
         assert g.check()[0] == 0, g.check()
         pick = synth.sample_distinct(len(s), 100000, 100 + r)

@@ -25,7 +25,7 @@ V = 1 << a.scale
 g = Graph(V, hashing=not a.no_hashing, degree_hints=T(np.bincount(s, minlength=V).astype(np.uint32)))
 g.insert(T(s), T(d), T(w))
 for r in range(a.reps):
-    fs, fd, fw = synth.rmat_draws(a.scale, a.batch, r * a.batch, 11)
+    fs, fd, fw = synth.rmat_draws(a.scale, a.batch, r * a.batch, 11, scramble_seed=11)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ins = (T(fs), T(fd), T(fw))
     torch.cuda.synchronize()

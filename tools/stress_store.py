@@ -33,7 +33,7 @@ if a.oracle:
 g.insert(T(s), T(d), T(w))
 print("bulk", g.check(), flush=True)
 for r in range(a.reps):
-    fs, fd, fw = synth.rmat_draws(a.scale, a.batch, r * a.batch, 11)
+    fs, fd, fw = synth.rmat_draws(a.scale, a.batch, r * a.batch, 11, scramble_seed=11)
     n = g.insert(T(fs), T(fd), T(fw))
     c = g.check()
     print(f"rep {r} insert {n} check {c}", flush=True)
