@@ -64,6 +64,8 @@ def _L():
         L.orc_check_tree.argtypes = [vp, ctypes.c_uint32, ctypes.c_int, u64p, u32p]
         L.orc_pagerank.argtypes = [vp, ctypes.c_double, ctypes.c_double, ctypes.c_uint32,
                                    ctypes.POINTER(ctypes.c_double), u32p, ctypes.POINTER(ctypes.c_double)]
+        L.orc_tc_count.restype = ctypes.c_uint64
+        L.orc_tc_count.argtypes = [vp, vp, u32p, u32p, ctypes.c_uint64]
         _lib = L
     return _lib
 
@@ -155,6 +157,34 @@ class OracleGraph:
         fb = ctypes.c_uint32(0)
         bad = _L().orc_check_tree(self._g, source, int(unit), _p(n, u64p), ctypes.byref(fb))
         return int(bad), int(fb.value)
+
+
+def tc_count(g1: OracleGraph, g2: OracleGraph, src, dst) -> int:
+    """Count(G1, G2, edges) = sum over (u, v) of |adj_G1(u) ∩ adj_G2(v)|."""
+    s, d = _a32(src), _a32(dst)
+    return int(_L().orc_tc_count(g1._g, g2._g, _p(s, u32p), _p(d, u32p), len(s)))
+
+
+def tc_static(g: OracleGraph) -> int:
+    """Triangles of an undirected (symmetric) graph: Count(G, G, all directed edges) / 6
+    (P:2069-2072 "degenerates to the static triangle counting case ... six times")."""
+    s, d, _ = g.edges()
+    c = tc_count(g, g, s, d)
+    assert c % 6 == 0, c
+    return c // 6
+
+
+def tc_delta(g_after: OracleGraph, g_update: OracleGraph, src, dst, insert: bool):
+    """Triangles added (insert) or removed (delete) by a batch given in both orientations, by the
+    paper's inclusion-exclusion: S1 = Count(after, after), S2 = Count(after, update),
+    S3 = Count(update, update); added = S1/2 - S2/2 + S3/6, removed = S1/2 + S2/2 + S3/6.
+    Returns (delta, (S1, S2, S3))."""
+    s1 = tc_count(g_after, g_after, src, dst)
+    s2 = tc_count(g_after, g_update, src, dst)
+    s3 = tc_count(g_update, g_update, src, dst)
+    num = 3 * s1 - 3 * s2 + s3 if insert else 3 * s1 + 3 * s2 + s3
+    assert num % 6 == 0, (s1, s2, s3)
+    return num // 6, (s1, s2, s3)
 
 
 def invalidated(vertex_n: int, source: int, node_old, src, dst):

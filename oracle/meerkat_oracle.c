@@ -427,3 +427,34 @@ int orc_pagerank(const orc_graph* g, double d, double eps, uint32_t max_iter, do
   if (delta_out) *delta_out = delta;
   return ORC_OK;
 }
+
+/*
+ * Dynamic triangle counting ("Dynamic Triangle Counting",
+ * P:1643-1656; the Count kernel of Algorithm tc-count).
+ *   Count(G1, G2, edges) = sum over (u, v) in edges of |adjacency_G1(u) ∩ adjacency_G2(v)|
+ * ("the cardinality of the intersection of the adjacency(u) in G1 and adjacency(v)
+ * in G2").  Adjacencies are the stored out-neighbour sets (graphs are undirected, i.e. store both
+ * orientations, for triangle counting).  Plain definition: a merge of the two sorted rows.
+ */
+static uint64_t row_begin(const orc_graph* g, uint32_t u) {
+  uint64_t lo = 0, hi = g->m, k = (uint64_t)u << 32;
+  while (lo < hi) { uint64_t mid = lo + (hi - lo) / 2; if (g->key[mid] < k) lo = mid + 1; else hi = mid; }
+  return lo;
+}
+
+uint64_t orc_tc_count(const orc_graph* g1, const orc_graph* g2, const uint32_t* src, const uint32_t* dst,
+                      uint64_t n) {
+  uint64_t total = 0;
+  for (uint64_t e = 0; e < n; e++) {
+    const uint32_t u = src[e], v = dst[e];
+    if (u >= g1->V || v >= g2->V) continue;
+    uint64_t i = row_begin(g1, u), j = row_begin(g2, v);
+    while (i < g1->m && (g1->key[i] >> 32) == u && j < g2->m && (g2->key[j] >> 32) == v) {
+      const uint32_t a = (uint32_t)g1->key[i], b = (uint32_t)g2->key[j];
+      if (a == b) { total++; i++; j++; }
+      else if (a < b) i++;
+      else j++;
+    }
+  }
+  return total;
+}
