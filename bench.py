@@ -367,11 +367,25 @@ def measure(args, ws, W, frontier, dev, local, stream, T, flush, K, Wm, clocks=N
         b.record(stream)
         b.synchronize()
         static[name] = a.elapsed_time(b)
+    # the paper's vanilla variant (distances only, 32-bit atomics) on the same graph:
+    # the tree-based overhead of P:2313-2317 (17.2% BFS, ~14% SSSP on its GPU)
+    vanilla = {}
+    if fused:
+        for name, mk in (("sssp", g.sssp_vanilla), ("bfs", g.bfs_vanilla)):
+            vt = mk(W.source)
+            flush.zero_()
+            a.record(stream)
+            vt.recompute()
+            b.record(stream)
+            b.synchronize()
+            vanilla[name] = a.elapsed_time(b)
+            vt.close()
     mean = {n: float(np.mean(v)) for n, v in per_call.items()}
     res = {
         "frontier": frontier, "fused": fused, "K": K, "total_ms": total_ms, "ms_per_step": total_ms / K, "mean": mean,
         "per_call": per_call, "tstats": tstats, "clocks": clk, "n_base": n_base, "bulk_ms": bulk_ms,
         "launches": int(st1["kernel_launches"] - st0["kernel_launches"]), "static_ms": static,
+        "vanilla_ms": vanilla,
         "store": {k: g.stats()[k] for k in ("head_slabs", "buckets", "pool_used", "bytes_device")},
     }
     return res, (g, sp, bf)
@@ -615,6 +629,9 @@ def run_ours(args, ws, rank, local):
         "bfs_ms_per_batch": ({"incremental": split["bfs_inc"], "decremental": split["bfs_dec"]} if split else None),
         "per_call_ms": mean,
         "static_recompute_ms": res["static_ms"],
+        "vanilla_static_ms": res["vanilla_ms"] or None,
+        "tree_overhead_vs_vanilla": ({k: res["static_ms"][k] / res["vanilla_ms"][k] - 1 for k in res["vanilla_ms"]}
+                                     if res["vanilla_ms"] else None),
         "self_relative_speedup": ({k: res["static_ms"][k] / (dyn[k] / 2) for k in dyn} if dyn else None),
         "bulk_build": {"edges": res["n_base"], "ms": res["bulk_ms"], "edges_per_s": res["n_base"] / (res["bulk_ms"] / 1e3)},
         "tree_calls": tree_detail(res),

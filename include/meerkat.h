@@ -160,6 +160,14 @@ meerkat_status meerkat_check(meerkat_graph* g, uint64_t* info);
  * graph version. */
 meerkat_status meerkat_sssp_create(meerkat_graph* g, uint32_t source, meerkat_tree** out);
 meerkat_status meerkat_bfs_create(meerkat_graph* g, uint32_t source, meerkat_tree** out);
+/* The VANILLA variant: static SSSP / BFS computing only the shortest distances,
+ * 32-bit distance words relaxed by 32-bit atomicMin (no parent, so no dependence tree: incremental
+ * / decremental calls and meerkat_tree_nodes return MEERKAT_E_STATE; recompute and distances work).
+ * The paper measures the tree-based variant's overhead against it (17.2% BFS, ~14% SSSP). */
+meerkat_status meerkat_sssp_vanilla_create(meerkat_graph* g, uint32_t source, meerkat_tree** out);
+meerkat_status meerkat_bfs_vanilla_create(meerkat_graph* g, uint32_t source, meerkat_tree** out);
+/* dist[v] for every v (UINT32_MAX when unreached), for tree-based and vanilla trees; host or device. */
+meerkat_status meerkat_tree_distances(meerkat_tree* t, uint32_t* out);
 /* Incremental update: the batch just applied by insert_batch is the
  * initial frontier.  w: the batch's weights (NULL for BFS trees). */
 meerkat_status meerkat_sssp_incremental(meerkat_graph* g, meerkat_tree* t, const uint32_t* src,

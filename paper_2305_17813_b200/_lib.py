@@ -33,6 +33,7 @@ EXPORTS = [
     "meerkat_check", "meerkat_trees_incremental", "meerkat_trees_decremental",
     "meerkat_pagerank_create", "meerkat_pagerank_update", "meerkat_pagerank_recompute", "meerkat_pagerank_values",
     "meerkat_pagerank_stats_get", "meerkat_pagerank_destroy",
+    "meerkat_sssp_vanilla_create", "meerkat_bfs_vanilla_create", "meerkat_tree_distances",
 ]
 
 
@@ -136,6 +137,9 @@ def lib():
         "meerkat_pagerank_values": (ctypes.c_int, [vp, vp]),
         "meerkat_pagerank_stats_get": (ctypes.c_int, [vp, ctypes.POINTER(PageRankStats)]),
         "meerkat_pagerank_destroy": (ctypes.c_int, [vp]),
+        "meerkat_sssp_vanilla_create": (ctypes.c_int, [vp, u32, pvp]),
+        "meerkat_bfs_vanilla_create": (ctypes.c_int, [vp, u32, pvp]),
+        "meerkat_tree_distances": (ctypes.c_int, [vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -332,7 +332,8 @@ meerkat_status meerkat_stats_get(meerkat_graph* g, meerkat_stats* out) {
 
 // ------------------------------------------------------------------ trees
 
-static meerkat_status tree_create(meerkat_graph* g, uint32_t source, bool unit, bool dist, meerkat_tree** out) {
+static meerkat_status tree_create(meerkat_graph* g, uint32_t source, bool unit, bool dist, meerkat_tree** out,
+                                  bool vanilla = false) {
   if (!g || !out) return MEERKAT_E_INVALID_ARG;
   *out = nullptr;
   if (source >= g->V) return MEERKAT_E_VERTEX_RANGE;
@@ -343,6 +344,7 @@ static meerkat_status tree_create(meerkat_graph* g, uint32_t source, bool unit, 
   if (!t) return MEERKAT_E_CUDA;
   t->g = g;
   t->unit = unit;
+  t->vanilla = vanilla;
   TreeDev& T = t->dev;
   T.source = source;
   T.fr_cap = std::max<uint64_t>(std::max(g->out.buckets, g->in.buckets), 1);
@@ -397,6 +399,32 @@ meerkat_status meerkat_bfs_create(meerkat_graph* g, uint32_t source, meerkat_tre
   return tree_create(g, source, true, false, out);
 }
 
+meerkat_status meerkat_sssp_vanilla_create(meerkat_graph* g, uint32_t source, meerkat_tree** out) {
+  return tree_create(g, source, false, false, out, true);
+}
+
+meerkat_status meerkat_bfs_vanilla_create(meerkat_graph* g, uint32_t source, meerkat_tree** out) {
+  return tree_create(g, source, true, false, out, true);
+}
+
+meerkat_status meerkat_tree_distances(meerkat_tree* t, uint32_t* out) {
+  if (!t || !out || t->dist) return MEERKAT_E_INVALID_ARG;
+  meerkat_graph* g = t->g;
+  DeviceGuard dg(g->device);
+  const bool host = !is_device_ptr(out);
+  uint32_t* d = out;
+  cudaError_t e = cudaSuccess;
+  if (host) {
+    e = ensure_stage(g, 3, (size_t)g->Vl * 4);
+    d = static_cast<uint32_t*>(g->stage[3]);
+  }
+  if (e == cudaSuccess) e = launch_node_dist(g, t, d);
+  if (e == cudaSuccess && host) e = cudaMemcpyAsync(out, d, (size_t)g->Vl * 4, cudaMemcpyDeviceToHost, g->stream);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  if (host) return collect(g);
+  return MEERKAT_OK;
+}
+
 // Mutation-following update of one or more trees of g with the same batch (fused launch).
 static meerkat_status trees_update(meerkat_graph* g, meerkat_tree* const* ts, uint32_t k, int kind, const uint32_t* src,
                                    const uint32_t* dst, const uint32_t* w, uint64_t n) {
@@ -407,6 +435,7 @@ static meerkat_status trees_update(meerkat_graph* g, meerkat_tree* const* ts, ui
   for (uint32_t i = 0; i < k; i++) {
     meerkat_tree* t = ts[i];
     if (!t || t->g != g || t->dist) return MEERKAT_E_INVALID_ARG;
+    if (t->vanilla) return MEERKAT_E_STATE;   // no dependence tree: static only
     for (uint32_t j = 0; j < i; j++)
       if (ts[j] == t) return MEERKAT_E_INVALID_ARG;
     // ordering contract: the batch must be the mutation just applied
@@ -474,6 +503,7 @@ meerkat_status meerkat_tree_recompute(meerkat_graph* g, meerkat_tree* t) {
 
 meerkat_status meerkat_tree_nodes(meerkat_tree* t, uint64_t* out) {
   if (!t || !out) return MEERKAT_E_INVALID_ARG;
+  if (t->vanilla) return MEERKAT_E_STATE;   // distances only: meerkat_tree_distances
   meerkat_graph* g = t->g;
   DeviceGuard dg(g->device);
   const bool host = !is_device_ptr(out);

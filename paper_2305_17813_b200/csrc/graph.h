@@ -81,7 +81,7 @@ struct meerkat_graph {
   int sm_count = 0;
   void* stage[4] = {nullptr, nullptr, nullptr, nullptr};   // staging for host inputs / outputs
   size_t stage_bytes[4] = {0, 0, 0, 0};
-  int tree_blocks_per_sm[3] = {0, 0, 0};   // cooperative occupancy: static, incremental, decremental
+  int tree_blocks_per_sm[4] = {0, 0, 0, 0};   // cooperative occupancy: static, incremental, decremental, vanilla
   int latency_bps = 0;                      // blocks/SM for latency-bound tree calls (0 = occupancy)
   unsigned long long* rscratch = nullptr;   // meerkat_route: device counts + cursors
   unsigned long long* hrscratch = nullptr;  // pinned counts
@@ -92,6 +92,7 @@ struct meerkat_tree {
   mk::TreeDev dev{};
   mk::TreeCtrl* hctrl = nullptr;
   bool unit = false;     // BFS
+  bool vanilla = false;  // distance-only static variant: node[] holds u32 distances
   uint64_t version = 0;
   mk::TreeCtrl* ctrl_base = nullptr;   // two control blocks: a call uses one and zeroes the other
   int parity = 0;
@@ -143,6 +144,7 @@ cudaError_t tree_occupancy(meerkat_graph* g);
 enum TreeMode { MODE_STATIC = 0, MODE_INCREMENTAL = 1, MODE_DECREMENTAL = 2 };
 cudaError_t launch_tree(meerkat_graph* g, meerkat_tree* const* trees, uint32_t ntrees, int mode, const uint32_t* s,
                         const uint32_t* d, const uint32_t* w, uint64_t n);
+cudaError_t launch_node_dist(meerkat_graph* g, meerkat_tree* t, uint32_t* out);
 // dtree.cu
 meerkat_status dtree_phase(meerkat_graph* g, meerkat_tree* t, int phase, const void* a, const void* b,
                            const void* c, uint64_t n, meerkat_dresult* out);

@@ -53,7 +53,9 @@ __device__ __forceinline__ bool fetch_item(const uint64_t* fr, uint64_t n, uint6
 // Expand the frontier items [0, n) of `fr` (one 8-lane group per item) for tree T (index k),
 // applying VISIT to every live edge; successful vertices go to (fnext, sznext).  The first slab
 // of an item and d(v) are loaded together (independent requests).
-template <bool MAP, int VISIT>
+// V32: the paper's VANILLA variant: node[] holds 32-bit distances only (no parent),
+// relaxed by 32-bit atomicMin (static SSSP / BFS; RELAX only).
+template <bool MAP, int VISIT, bool V32 = false>
 __device__ __forceinline__ void expand(const TreeArgs& A, const TreeDev& T, int k, const uint64_t* fr, uint64_t n,
                                        uint64_t* fnext, unsigned long long* sznext, uint32_t epoch_next,
                                        Counters& c) {
@@ -73,13 +75,14 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const TreeDev& T, int 
     uint64_t nv = 0;
     if (active) {
       d = ld_slab_ro(slab_ptr(S, slab), l8);
-      if (VISIT == RELAX && fresh && l8 == 0) nv = ld_cg_u64(T.node + v);   // one read per group, broadcast:
+      if (VISIT == RELAX && fresh && l8 == 0)                                // one read per group, broadcast:
+        nv = V32 ? (uint64_t)__ldcg(reinterpret_cast<const unsigned int*>(T.node) + v) << 32 : ld_cg_u64(T.node + v);
       if (l8 == 0) c.slabs++;                                               // d(v) may change concurrently
     }
     if (VISIT == RELAX) nv = __shfl_sync(FULL, nv, lane & 24);
     bool dead = false;
     if (VISIT == RELAX && active && fresh) {
-      dead = nv == UNREACHED;
+      dead = V32 ? (nv >> 32) == INF_DIST : nv == UNREACHED;
       du = (uint32_t)(nv >> 32);
     }
     fresh = false;
@@ -107,18 +110,28 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const TreeDev& T, int 
           cand[kk] = (dist << 32) | v;
         }
       }
+      if constexpr (V32) {   // distance only: compare and store the high half
+#pragma unroll
+        for (int kk = 0; kk < NK; kk++) cand[kk] >>= 32;
+      }
+      unsigned int* const node32 = reinterpret_cast<unsigned int*>(T.node);
       if (probe) {   // node[] only decreases: a stale read can only cost a spare atomic
         uint64_t pv[NK];
 #pragma unroll
-        for (int kk = 0; kk < NK; kk++) pv[kk] = live[kk] ? ld_cg_u64(T.node + xs[kk]) : 0ull;
+        for (int kk = 0; kk < NK; kk++)
+          pv[kk] = !live[kk] ? 0ull : V32 ? (uint64_t)__ldcg(node32 + xs[kk]) : ld_cg_u64(T.node + xs[kk]);
 #pragma unroll
         for (int kk = 0; kk < NK; kk++) live[kk] = live[kk] && cand[kk] < pv[kk];
       }
       unsigned long long old[NK];
 #pragma unroll
-      for (int kk = 0; kk < NK; kk++)
-        old[kk] = live[kk] ? atomicMin(reinterpret_cast<unsigned long long*>(T.node + xs[kk]),
-                                       (unsigned long long)cand[kk]) : 0ull;
+      for (int kk = 0; kk < NK; kk++) {
+        if constexpr (V32)
+          old[kk] = live[kk] ? atomicMin(node32 + xs[kk], (unsigned int)cand[kk]) : 0ull;
+        else
+          old[kk] = live[kk] ? atomicMin(reinterpret_cast<unsigned long long*>(T.node + xs[kk]),
+                                         (unsigned long long)cand[kk]) : 0ull;
+      }
       uint32_t st[NK];
 #pragma unroll
       for (int kk = 0; kk < NK; kk++) {
@@ -211,7 +224,7 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const TreeDev& T, int 
 // fr[r&1] / size[r%3] of each tree and writes fr[(r+1)&1] / size[(r+1)%3]; size[(r+2)%3]
 // (consumed two rounds ago) is zeroed during round r so it is clean when it becomes "next".
 // The trees share the grid barrier of every round.
-template <bool MAP, int VISIT>
+template <bool MAP, int VISIT, bool V32 = false>
 __device__ __forceinline__ uint32_t run_rounds(const TreeArgs& A, const uint32_t* epoch, cg::grid_group& grid,
                                                uint32_t r, Counters& c) {
   for (;;) {
@@ -229,8 +242,8 @@ __device__ __forceinline__ uint32_t run_rounds(const TreeArgs& A, const uint32_t
     for (int k = 0; k < MAX_TREES; k++) {
       if (!n[k]) continue;
       const TreeDev& T = A.T[k];
-      expand<MAP, VISIT>(A, T, k, T.fr[r & 1], n[k], T.fr[(r + 1) & 1], &T.ctrl->size[(r + 1) % 3],
-                         epoch[k] + r + 1, c);
+      expand<MAP, VISIT, V32>(A, T, k, T.fr[r & 1], n[k], T.fr[(r + 1) & 1], &T.ctrl->size[(r + 1) % 3],
+                              epoch[k] + r + 1, c);
     }
     grid.sync();
     timeline(A.T[0].ctrl);
@@ -251,7 +264,7 @@ __device__ __forceinline__ void finish(const TreeArgs& A, Counters& c, const uin
 
 // ------------------------------------------------------------------ static
 
-template <bool MAP>
+template <bool MAP, bool V32>
 __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_static(const __grid_constant__ TreeArgs A) {
   const TreeDev& T = A.T[0];
   const uint32_t epoch[MAX_TREES] = {__ldcg(T.epoch_ptr)};
@@ -260,7 +273,10 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_static(const __grid_cons
   Counters c;
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
   // init: every node <INF, INVALID>, SRC <0, SRC>
-  for (uint64_t v = tid; v < A.G.V; v += nt) T.node[v] = (v == T.source) ? (uint64_t)T.source : UNREACHED;
+  if (V32)   // vanilla: distance 0 at SRC, INF elsewhere
+    for (uint64_t v = tid; v < A.G.V; v += nt) reinterpret_cast<uint32_t*>(T.node)[v] = v == T.source ? 0u : INF_DIST;
+  else
+    for (uint64_t v = tid; v < A.G.V; v += nt) T.node[v] = (v == T.source) ? (uint64_t)T.source : UNREACHED;
   grid.sync();
   if (blockIdx.x == 0 && threadIdx.x < 32) {
     const bool has = threadIdx.x == 0;
@@ -269,7 +285,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_static(const __grid_cons
   }
   grid.sync();
   timeline(T.ctrl);
-  const uint32_t r = run_rounds<MAP, RELAX>(A, epoch, grid, 0, c);
+  const uint32_t r = run_rounds<MAP, RELAX, V32>(A, epoch, grid, 0, c);
   finish(A, c, epoch, tid == 0, r, r, 0);
 }
 
@@ -532,6 +548,19 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_dec(const __grid_constan
   finish(A, c, epoch, tid == 0, r2, r2 - r1, r1);
 }
 
+// Distances of a tree: the high halves of the packed nodes (tree-based) or the 32-bit array (vanilla).
+__global__ void k_node_dist(const uint64_t* __restrict__ node, uint32_t V, int vanilla, uint32_t* __restrict__ out) {
+  for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < V; v += (uint64_t)gridDim.x * blockDim.x)
+    out[v] = vanilla ? reinterpret_cast<const uint32_t*>(node)[v] : (uint32_t)(node[v] >> 32);
+}
+
+cudaError_t launch_node_dist(meerkat_graph* g, meerkat_tree* t, uint32_t* out) {
+  const unsigned gb = (unsigned)std::min<uint64_t>((g->Vl + 255) / 256, (uint64_t)g->sm_count * 8);
+  k_node_dist<<<std::max(gb, 1u), 256, 0, g->stream>>>(t->dev.node, g->Vl, t->vanilla ? 1 : 0, out);
+  g->launches++;
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ host side
 
 template <typename K>
@@ -547,11 +576,13 @@ cudaError_t tree_occupancy(meerkat_graph* g) {
   cudaError_t e;
   const int fbytes = FILTER_WORDS * 4;
   if (g->weighted) {
-    if ((e = occ(k_tree_static<true>, 0, &g->tree_blocks_per_sm[0])) != cudaSuccess) return e;
+    if ((e = occ(k_tree_static<true, false>, 0, &g->tree_blocks_per_sm[0])) != cudaSuccess) return e;
+    if ((e = occ(k_tree_static<true, true>, 0, &g->tree_blocks_per_sm[3])) != cudaSuccess) return e;
     if ((e = occ(k_tree_inc<true>, 0, &g->tree_blocks_per_sm[1])) != cudaSuccess) return e;
     if ((e = occ(k_tree_dec<true>, fbytes, &g->tree_blocks_per_sm[2])) != cudaSuccess) return e;
   } else {
-    if ((e = occ(k_tree_static<false>, 0, &g->tree_blocks_per_sm[0])) != cudaSuccess) return e;
+    if ((e = occ(k_tree_static<false, false>, 0, &g->tree_blocks_per_sm[0])) != cudaSuccess) return e;
+    if ((e = occ(k_tree_static<false, true>, 0, &g->tree_blocks_per_sm[3])) != cudaSuccess) return e;
     if ((e = occ(k_tree_inc<false>, 0, &g->tree_blocks_per_sm[1])) != cudaSuccess) return e;
     if ((e = occ(k_tree_dec<false>, fbytes, &g->tree_blocks_per_sm[2])) != cudaSuccess) return e;
   }
@@ -576,7 +607,8 @@ cudaError_t launch_tree(meerkat_graph* g, meerkat_tree* const* trees, uint32_t n
   A.bs = s; A.bd = d; A.bw = w; A.bn = n;
   A.weighted = g->weighted ? 1u : 0u;
   A.filter_words = g->reverse ? 0u : FILTER_WORDS;   // shared-memory union filter (scan only)
-  int bps = g->tree_blocks_per_sm[mode];
+  const bool vanilla = trees[0]->vanilla;   // vanilla trees are static-only and never fused
+  int bps = vanilla ? g->tree_blocks_per_sm[3] : g->tree_blocks_per_sm[mode];
   if (bps <= 0) return cudaErrorInvalidConfiguration;
   if (g->latency_bps > 0 && mode != MODE_STATIC && !(mode == MODE_DECREMENTAL && !g->reverse))
     bps = std::min(bps, g->latency_bps);
@@ -585,10 +617,12 @@ cudaError_t launch_tree(meerkat_graph* g, meerkat_tree* const* trees, uint32_t n
   const size_t smem = (mode == MODE_DECREMENTAL && !g->reverse) ? (size_t)FILTER_WORDS * 4 : 0;
   void* fn;
   if (g->weighted)
-    fn = mode == MODE_STATIC ? (void*)k_tree_static<true> : mode == MODE_INCREMENTAL ? (void*)k_tree_inc<true>
+    fn = mode == MODE_STATIC ? (vanilla ? (void*)k_tree_static<true, true> : (void*)k_tree_static<true, false>)
+         : mode == MODE_INCREMENTAL ? (void*)k_tree_inc<true>
                                                                                      : (void*)k_tree_dec<true>;
   else
-    fn = mode == MODE_STATIC ? (void*)k_tree_static<false> : mode == MODE_INCREMENTAL ? (void*)k_tree_inc<false>
+    fn = mode == MODE_STATIC ? (vanilla ? (void*)k_tree_static<false, true> : (void*)k_tree_static<false, false>)
+         : mode == MODE_INCREMENTAL ? (void*)k_tree_inc<false>
                                                                                       : (void*)k_tree_dec<false>;
   cudaError_t e = cudaLaunchCooperativeKernel(fn, grid, block, args, smem, g->stream);
   if (e != cudaSuccess) return e;

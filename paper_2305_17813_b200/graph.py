@@ -188,15 +188,26 @@ class Graph:
     def bfs(self, source: int) -> "Tree":
         return Tree(self, source, unit=True)
 
+    def sssp_vanilla(self, source: int) -> "Tree":
+        """Static distances only, 32-bit atomics (the paper's vanilla variant)."""
+        return Tree(self, source, unit=False, vanilla=True)
+
+    def bfs_vanilla(self, source: int) -> "Tree":
+        return Tree(self, source, unit=True, vanilla=True)
+
 
 class Tree:
     """Dependence tree T_G of packed <distance, parent> words."""
 
-    def __init__(self, graph: Graph, source: int, unit: bool):
+    def __init__(self, graph: Graph, source: int, unit: bool, vanilla: bool = False):
         L = _lib.lib()
         h = ctypes.c_void_p()
-        fn = L.meerkat_bfs_create if unit else L.meerkat_sssp_create
-        check(fn(graph._h, source, ctypes.byref(h)), "meerkat_bfs_create" if unit else "meerkat_sssp_create")
+        if vanilla:
+            fn = L.meerkat_bfs_vanilla_create if unit else L.meerkat_sssp_vanilla_create
+        else:
+            fn = L.meerkat_bfs_create if unit else L.meerkat_sssp_create
+        check(fn(graph._h, source, ctypes.byref(h)), fn.__name__)
+        self.vanilla = vanilla
         self._h = h
         self.graph = graph
         self.unit = unit
@@ -237,6 +248,15 @@ class Tree:
             return out
         a = np.empty(self.graph.vertex_n, np.uint64)
         check(_lib.lib().meerkat_tree_nodes(self._h, ctypes.c_void_p(a.ctypes.data)), "meerkat_tree_nodes")
+        return a
+
+    def distances(self, out=None):
+        """dist[v] (uint32, UINT32_MAX when unreached) as a numpy array (or into an int32 CUDA tensor)."""
+        if out is not None:
+            check(_lib.lib().meerkat_tree_distances(self._h, ctypes.c_void_p(out.data_ptr())), "meerkat_tree_distances")
+            return out
+        a = np.empty(self.graph.vertex_n, np.uint32)
+        check(_lib.lib().meerkat_tree_distances(self._h, ctypes.c_void_p(a.ctypes.data)), "meerkat_tree_distances")
         return a
 
     def invalidated(self):
