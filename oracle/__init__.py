@@ -64,6 +64,8 @@ def _L():
         L.orc_check_tree.argtypes = [vp, ctypes.c_uint32, ctypes.c_int, u64p, u32p]
         L.orc_pagerank.argtypes = [vp, ctypes.c_double, ctypes.c_double, ctypes.c_uint32,
                                    ctypes.POINTER(ctypes.c_double), u32p, ctypes.POINTER(ctypes.c_double)]
+        L.orc_wcc.restype = ctypes.c_uint64
+        L.orc_wcc.argtypes = [vp, u32p]
         L.orc_tc_count.restype = ctypes.c_uint64
         L.orc_tc_count.argtypes = [vp, vp, u32p, u32p, ctypes.c_uint64]
         _lib = L
@@ -146,6 +148,12 @@ class OracleGraph:
         st = _L().orc_pagerank(self._g, float(d), float(eps), int(max_iter),
                                x.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(it), ctypes.byref(dl))
         return st, x, int(it.value), float(dl.value)
+
+    def wcc(self):
+        """(labels u32[V], components): label[v] = smallest id in v's weakly connected component."""
+        lab = np.empty(self.V, np.uint32)
+        n = _L().orc_wcc(self._g, _p(lab, u32p))
+        return lab, int(n)
 
     def dec_frontier_count(self, node_old, invalid_flag) -> int:
         n = np.ascontiguousarray(node_old, dtype=np.uint64)

@@ -458,3 +458,43 @@ uint64_t orc_tc_count(const orc_graph* g1, const orc_graph* g2, const uint32_t* 
   }
   return total;
 }
+
+/*
+ * Weakly connected components ("Incremental WCC", supplementary
+ * P:381-395 static SamplingWCC).  A WCC of a directed graph is a maximal set of vertices connected
+ * when edge directions are ignored.  Labels are canonical: label[v] = the smallest
+ * vertex id in v's component (what a union-find that always hooks the larger root under the
+ * smaller one ends with after full path compression).  Plain definition: BFS over the
+ * undirected version of the edge set, vertices visited in increasing id order.
+ */
+uint64_t orc_wcc(const orc_graph* g, uint32_t* label) {
+  const uint32_t V = g->V;
+  /* undirected adjacency: CSR over both orientations */
+  uint64_t* off = (uint64_t*)calloc((size_t)V + 1, sizeof(uint64_t));
+  for (uint64_t i = 0; i < g->m; i++) { off[(g->key[i] >> 32) + 1]++; off[(uint32_t)g->key[i] + 1]++; }
+  for (uint32_t v = 0; v < V; v++) off[v + 1] += off[v];
+  uint32_t* adj = (uint32_t*)malloc((off[V] + 1) * sizeof(uint32_t));
+  uint64_t* fill = (uint64_t*)malloc(((size_t)V + 1) * sizeof(uint64_t));
+  memcpy(fill, off, ((size_t)V + 1) * sizeof(uint64_t));
+  for (uint64_t i = 0; i < g->m; i++) {
+    const uint32_t u = (uint32_t)(g->key[i] >> 32), v = (uint32_t)g->key[i];
+    adj[fill[u]++] = v;
+    adj[fill[v]++] = u;
+  }
+  uint32_t* q = (uint32_t*)malloc(((size_t)V + 1) * sizeof(uint32_t));
+  for (uint32_t v = 0; v < V; v++) label[v] = 0xFFFFFFFFu;
+  uint64_t comps = 0;
+  for (uint32_t r = 0; r < V; r++) {   /* r is the smallest id of a not yet labelled component */
+    if (label[r] != 0xFFFFFFFFu) continue;
+    comps++;
+    uint64_t head = 0, tail = 0;
+    label[r] = r; q[tail++] = r;
+    while (head < tail) {
+      const uint32_t x = q[head++];
+      for (uint64_t i = off[x]; i < off[x + 1]; i++)
+        if (label[adj[i]] == 0xFFFFFFFFu) { label[adj[i]] = r; q[tail++] = adj[i]; }
+    }
+  }
+  free(q); free(fill); free(adj); free(off);
+  return comps;
+}
