@@ -60,6 +60,11 @@ def parse():
                    help="decremental valid->invalid frontier: stream every slab (paper, P:156-164) or "
                         "read the in-edges of V_invalid from an in-edge mirror store")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--wcc", action=argparse.BooleanOptionalAction, default=True,
+                   help="also time static and incremental WCC on the workload graph (SURVEY §8(f) NEXT-3)")
+    p.add_argument("--tc", action=argparse.BooleanOptionalAction, default=True,
+                   help="also time triangle counting on a symmetrised R-MAT (--tc-scale) graph (NEXT-4)")
+    p.add_argument("--tc-scale", type=int, default=20)
     p.add_argument("--pagerank", action=argparse.BooleanOptionalAction, default=True,
                    help="also time static and dynamic PageRank on the same graph (SURVEY §8(f) NEXT-1; "
                         "needs the in-edge mirror, i.e. --frontier reverse)")
@@ -511,6 +516,72 @@ def measure_pagerank(g, W, T, stream, flush, peak, peak_src):
                          "peak_source": peak_src}}
 
 
+def measure_wcc(g, W, T, stream, flush):
+    """WCC on the workload graph: static (MinHooking + union + compression) and
+    incremental after a 100K-edge insert batch (union of the batch + compression)."""
+    import torch
+    c = g.wcc()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def timed(fn):
+        flush.zero_()
+        a.record(stream)
+        fn()
+        b.record(stream)
+        b.synchronize()
+        return a.elapsed_time(b)
+
+    st_ms = timed(c.recompute)
+    s, d, w = W.deletes[0]                      # absent at this point (see measure_pagerank)
+    g.insert(T(s), T(d), T(w), count=False)
+    ts, td = T(s), T(d)
+    inc_ms = timed(lambda: c.incremental(ts, td))
+    comps = c.components()
+    g.delete(ts, td, count=False)
+    c.close()
+    return {"static_ms": st_ms, "incremental_ms": inc_ms, "batch": int(len(s)), "components": comps}
+
+
+def measure_tc(args, dev, stream):
+    """Triangle counting on a symmetrised R-MAT graph (both orientations stored, set store): the static
+    count and the dynamic deltas of a 10K-undirected-edge insert and delete batch
+    (inclusion-exclusion, three Count launches each)."""
+    import torch
+    import synth
+    from paper_2305_17813_b200 import Graph
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.uint32).view(np.int32)).to(dev)
+    rs, rd, _ = synth.rmat(args.tc_scale, 16)
+    k = np.unique(np.concatenate([(rs.astype(np.uint64) << np.uint64(32)) | rd,
+                                  (rd.astype(np.uint64) << np.uint64(32)) | rs]))
+    s, d = (k >> np.uint64(32)).astype(np.uint32), (k & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+    keep = s != d
+    s, d = s[keep], d[keep]
+    V = 1 << args.tc_scale
+    rng = np.random.default_rng(7)
+    und = np.nonzero(s < d)[0]
+    pick = rng.choice(und, 10_000, replace=False)
+    bs = np.concatenate([s[pick], d[pick]]); bd = np.concatenate([d[pick], s[pick]])
+    g = Graph(V, weighted=False, degree_hints=T(np.bincount(s, minlength=V).astype(np.uint32)), device=dev.index or 0,
+              stream=stream)
+    g.insert(T(s), T(d), count=False)
+    gu = Graph(V, weighted=False, device=dev.index or 0, stream=stream)
+    gu.insert(T(bs), T(bd), count=False)
+    g.sync(); gu.sync()
+    t0 = time.perf_counter(); tri = g.tc_static(); st_ms = 1e3 * (time.perf_counter() - t0)
+    g.delete(T(bs), T(bd), count=False)
+    g.sync()
+    t0 = time.perf_counter(); removed, _ = g.tc_delta(gu, T(bs), T(bd), insert=False); dec_ms = 1e3 * (time.perf_counter() - t0)
+    g.insert(T(bs), T(bd), count=False)
+    g.sync()
+    t0 = time.perf_counter(); added, S = g.tc_delta(gu, T(bs), T(bd), insert=True); inc_ms = 1e3 * (time.perf_counter() - t0)
+    out = {"graph": f"rmat-s{args.tc_scale}-ef16 symmetrised, {len(s)} directed edges", "triangles": tri,
+           "static_ms": st_ms, "batch_undirected": 10_000, "incremental_ms": inc_ms, "added": added,
+           "decremental_ms": dec_ms, "removed": removed, "S": S,
+           "timing": "host wall clock around each synchronising call (includes the plan scan's host read-back)"}
+    g.close(); gu.close()
+    return out
+
+
 def run_ours(args, ws, rank, local):
     import torch
 
@@ -581,6 +652,7 @@ def run_ours(args, ws, rank, local):
     pagerank = None
     if args.pagerank and args.frontier == "reverse" and ws == 1:
         pagerank = measure_pagerank(g, W, T, stream, flush, peak, peak_src)
+    wcc = measure_wcc(g, W, T, stream, flush) if args.wcc and ws == 1 else None
     g.close()
     del g, sp, bf
     torch.cuda.empty_cache()
@@ -605,6 +677,7 @@ def run_ours(args, ws, rank, local):
                "roofline": roofline_of(r2, peak, peak_src, traffic_file), "tree_calls": tree_detail(r2)}
 
     sweep = store_sweep(args, dev, stream) if args.sweep and ws == 1 else None
+    tc = measure_tc(args, dev, stream) if args.tc and ws == 1 else None
 
     cb = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -644,6 +717,8 @@ def run_ours(args, ws, rank, local):
         "alt": alt,
         "store_sweep": sweep,
         "pagerank": pagerank,
+        "wcc": wcc,
+        "tc": tc,
         "generate_s": gen_s,
     }
     if rank == 0:

@@ -55,6 +55,7 @@ extern "C" {
 typedef struct meerkat_graph meerkat_graph; /* opaque: slab store + metadata on one device */
 typedef struct meerkat_tree meerkat_tree;   /* opaque: one SSSP or BFS tree for one source */
 typedef struct meerkat_pagerank meerkat_pagerank; /* opaque: one PageRank vector of a graph */
+typedef struct meerkat_wcc meerkat_wcc;           /* opaque: weakly connected component labels of a graph */
 
 typedef enum {
   MEERKAT_OK = 0,
@@ -285,6 +286,48 @@ meerkat_status meerkat_pagerank_recompute(meerkat_graph* g, meerkat_pagerank* p)
 meerkat_status meerkat_pagerank_values(meerkat_pagerank* p, double* out);
 meerkat_status meerkat_pagerank_stats_get(meerkat_pagerank* p, meerkat_pagerank_stats* out);
 meerkat_status meerkat_pagerank_destroy(meerkat_pagerank* p);
+
+/* ---------------------------------------------------------------------------------------------
+ * Dynamic triangle counting (Algorithm tc-count).  Graphs are
+ * undirected: both orientations of every edge are stored (unweighted or weighted; weights are
+ * ignored).  Count(G1, G2, edges) = sum over (u, v) in edges of |adjacency_G1(u) ∩ adjacency_G2(v)|
+ * (P:2064-2066); g1 and g2 live on the same device with the same vertex_n and are unpartitioned
+ * (else MEERKAT_E_STATE).  Edges are host or device arrays.  All calls synchronise.
+ * ------------------------------------------------------------------------------------------- */
+meerkat_status meerkat_tc_count(meerkat_graph* g1, meerkat_graph* g2, const uint32_t* src, const uint32_t* dst,
+                                uint64_t n, uint64_t* count);
+/* Triangles of g: Count(G, G, every stored edge) / 6; MEERKAT_E_STATE if the count
+ * is not divisible by 6 (g is not symmetric). */
+meerkat_status meerkat_tc_static(meerkat_graph* g, uint64_t* triangles);
+/* Triangles added by an inserted batch (already applied to g_after; g_update holds exactly the batch;
+ * src/dst list the batch in BOTH orientations): S1 = Count(after, after), S2 = Count(after, update),
+ * S3 = Count(update, update), added = S1/2 - S2/2 + S3/6.  s (host [3], nullable)
+ * receives S1..S3.  MEERKAT_E_STATE if the identity is not an integer (broken precondition). */
+meerkat_status meerkat_tc_incremental(meerkat_graph* g_after, meerkat_graph* g_update, const uint32_t* src,
+                                      const uint32_t* dst, uint64_t n, uint64_t* added, uint64_t* s);
+/* Triangles removed by a deleted batch (already deleted from g_after): S1/2 + S2/2 + S3/6. */
+meerkat_status meerkat_tc_decremental(meerkat_graph* g_after, meerkat_graph* g_update, const uint32_t* src,
+                                      const uint32_t* dst, uint64_t n, uint64_t* removed, uint64_t* s);
+
+/* ---------------------------------------------------------------------------------------------
+ * Weakly connected components (static SamplingWCC P:381-395,
+ * incremental BatchInsert P:486-493; incremental only, as in the paper).  A root-based
+ * union-find over parents[]: label[v] after full path compression.  The larger root always hooks
+ * under the smaller, so label[v] = the smallest vertex id of v's component (edge directions are
+ * ignored).  Unpartitioned graphs only (else MEERKAT_E_STATE).
+ * ------------------------------------------------------------------------------------------- */
+/* Static WCC of the current graph: MinHooking sampling, compression, union of the remaining edges,
+ * compression.  Synchronises. */
+meerkat_status meerkat_wcc_create(meerkat_graph* g, meerkat_wcc** out);
+meerkat_status meerkat_wcc_recompute(meerkat_graph* g, meerkat_wcc* c);
+/* After insert_batch: union(src[i], dst[i]) for the batch, then full compression.
+ * Stream-ordered. */
+meerkat_status meerkat_wcc_incremental(meerkat_graph* g, meerkat_wcc* c, const uint32_t* src, const uint32_t* dst,
+                                       uint64_t n);
+/* label[v] (host or device [vertex_n]). */
+meerkat_status meerkat_wcc_labels(meerkat_wcc* c, uint32_t* out);
+meerkat_status meerkat_wcc_components(meerkat_wcc* c, uint64_t* n_components);
+meerkat_status meerkat_wcc_destroy(meerkat_wcc* c);
 
 #ifdef __cplusplus
 }

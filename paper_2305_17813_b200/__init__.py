@@ -2,6 +2,6 @@
 batch-dynamic SSSP/BFS, as hand-written sm_100a CUDA behind a C ABI
 (include/meerkat.h).  This package is the thin Python binding; see DESIGN.md."""
 from ._lib import MeerkatError, SO_PATH  # noqa: F401
-from .graph import Graph, PageRank, Tree  # noqa: F401
+from .graph import WCC, Graph, PageRank, Tree  # noqa: F401
 
-__all__ = ["Graph", "Tree", "PageRank", "MeerkatError", "SO_PATH"]
+__all__ = ["Graph", "Tree", "PageRank", "WCC", "MeerkatError", "SO_PATH"]

@@ -34,6 +34,9 @@ EXPORTS = [
     "meerkat_pagerank_create", "meerkat_pagerank_update", "meerkat_pagerank_recompute", "meerkat_pagerank_values",
     "meerkat_pagerank_stats_get", "meerkat_pagerank_destroy",
     "meerkat_sssp_vanilla_create", "meerkat_bfs_vanilla_create", "meerkat_tree_distances",
+    "meerkat_tc_count", "meerkat_tc_static", "meerkat_tc_incremental", "meerkat_tc_decremental",
+    "meerkat_wcc_create", "meerkat_wcc_recompute", "meerkat_wcc_incremental", "meerkat_wcc_labels",
+    "meerkat_wcc_components", "meerkat_wcc_destroy",
 ]
 
 
@@ -140,6 +143,16 @@ def lib():
         "meerkat_sssp_vanilla_create": (ctypes.c_int, [vp, u32, pvp]),
         "meerkat_bfs_vanilla_create": (ctypes.c_int, [vp, u32, pvp]),
         "meerkat_tree_distances": (ctypes.c_int, [vp, vp]),
+        "meerkat_tc_count": (ctypes.c_int, [vp, vp, vp, vp, u64, pu64]),
+        "meerkat_tc_static": (ctypes.c_int, [vp, pu64]),
+        "meerkat_tc_incremental": (ctypes.c_int, [vp, vp, vp, vp, u64, pu64, pu64]),
+        "meerkat_tc_decremental": (ctypes.c_int, [vp, vp, vp, vp, u64, pu64, pu64]),
+        "meerkat_wcc_create": (ctypes.c_int, [vp, pvp]),
+        "meerkat_wcc_recompute": (ctypes.c_int, [vp, vp]),
+        "meerkat_wcc_incremental": (ctypes.c_int, [vp, vp, vp, vp, u64]),
+        "meerkat_wcc_labels": (ctypes.c_int, [vp, vp]),
+        "meerkat_wcc_components": (ctypes.c_int, [vp, pu64]),
+        "meerkat_wcc_destroy": (ctypes.c_int, [vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -724,4 +724,174 @@ meerkat_status meerkat_pagerank_destroy(meerkat_pagerank* p) {
   return MEERKAT_OK;
 }
 
+/* ------------------------------------------------------------------ triangle counting (tc.cu) */
+
+static meerkat_status tc_check(meerkat_graph* a, meerkat_graph* b) {
+  if (!a || !b) return MEERKAT_E_INVALID_ARG;
+  if (a->device != b->device || a->V != b->V) return MEERKAT_E_INVALID_ARG;
+  if (a->ws > 1 || b->ws > 1) return MEERKAT_E_STATE;
+  return MEERKAT_OK;
+}
+
+// Count into a device scratch word and read it back (synchronises g1's stream).
+static meerkat_status tc_count_sync(meerkat_graph* g1, meerkat_graph* g2, const uint32_t* src, const uint32_t* dst,
+                                    uint64_t n, uint64_t* out) {
+  DeviceGuard dg(g1->device);
+  if (g2 != g1 && cudaStreamSynchronize(g2->stream) != cudaSuccess) return MEERKAT_E_CUDA;   // g2's updates done
+  const void *s, *d;
+  cudaError_t e = stage_in(g1, 0, src, n * 4, &s);
+  if (e == cudaSuccess) e = stage_in(g1, 1, dst, n * 4, &d);
+  unsigned long long* acc = nullptr;
+  if (e == cudaSuccess) e = cudaMallocAsync(&acc, 8, g1->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(acc, 0, 8, g1->stream);
+  if (e == cudaSuccess) e = launch_tc_count(g1, g2, (const uint32_t*)s, (const uint32_t*)d, n, acc);
+  unsigned long long h = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h, acc, 8, cudaMemcpyDeviceToHost, g1->stream);
+  if (acc) cudaFreeAsync(acc, g1->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g1->stream);
+  if (e != cudaSuccess) { cudaGetLastError(); return MEERKAT_E_CUDA; }
+  *out = h;
+  return MEERKAT_OK;
+}
+
+meerkat_status meerkat_tc_count(meerkat_graph* g1, meerkat_graph* g2, const uint32_t* src, const uint32_t* dst,
+                                uint64_t n, uint64_t* count) {
+  meerkat_status st = tc_check(g1, g2);
+  if (st != MEERKAT_OK) return st;
+  if (!count || (n && (!src || !dst))) return MEERKAT_E_INVALID_ARG;
+  return tc_count_sync(g1, g2, src, dst, n, count);
+}
+
+meerkat_status meerkat_tc_static(meerkat_graph* g, uint64_t* triangles) {
+  meerkat_status st = tc_check(g, g);
+  if (st != MEERKAT_OK) return st;
+  if (!triangles) return MEERKAT_E_INVALID_ARG;
+  DeviceGuard dg(g->device);
+  st = collect(g);
+  if (st != MEERKAT_OK) return st;
+  const uint64_t m = g->out.hctrl->ins_total - g->out.hctrl->del_total;   // live edges
+  uint32_t *s = nullptr, *d = nullptr;
+  cudaError_t e = cudaMemsetAsync(&g->out.dev.ctrl->export_n, 0, 8, g->stream);
+  if (e == cudaSuccess) e = cudaMallocAsync(&s, (m + 1) * 4, g->stream);
+  if (e == cudaSuccess) e = cudaMallocAsync(&d, (m + 1) * 4, g->stream);
+  if (e == cudaSuccess) e = launch_export(g, g->out, s, d, nullptr, m);   // every directed edge (u, v)
+  uint64_t c = 0;
+  if (e == cudaSuccess) st = tc_count_sync(g, g, s, d, m, &c);
+  if (s) cudaFreeAsync(s, g->stream);
+  if (d) cudaFreeAsync(d, g->stream);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  if (st != MEERKAT_OK) return st;
+  if (c % 6) return MEERKAT_E_STATE;   // not an undirected (symmetric) graph
+  *triangles = c / 6;                  // each triangle is found six times
+  return MEERKAT_OK;
+}
+
+static meerkat_status tc_delta(meerkat_graph* after, meerkat_graph* upd, const uint32_t* src, const uint32_t* dst,
+                               uint64_t n, bool insert, uint64_t* delta, uint64_t* s3) {
+  meerkat_status st = tc_check(after, upd);
+  if (st != MEERKAT_OK) return st;
+  if (!delta || (n && (!src || !dst))) return MEERKAT_E_INVALID_ARG;
+  uint64_t s[3] = {0, 0, 0};
+  st = tc_count_sync(after, after, src, dst, n, &s[0]);
+  if (st == MEERKAT_OK) st = tc_count_sync(after, upd, src, dst, n, &s[1]);
+  if (st == MEERKAT_OK) st = tc_count_sync(upd, upd, src, dst, n, &s[2]);
+  if (st != MEERKAT_OK) return st;
+  if (s3) { s3[0] = s[0]; s3[1] = s[1]; s3[2] = s[2]; }
+  // added = S1/2 - S2/2 + S3/6, removed = S1/2 + S2/2 + S3/6, in exact integers
+  const int64_t num = insert ? 3 * (int64_t)s[0] - 3 * (int64_t)s[1] + (int64_t)s[2]
+                             : 3 * (int64_t)s[0] + 3 * (int64_t)s[1] + (int64_t)s[2];
+  if (num < 0 || num % 6) return MEERKAT_E_STATE;   // broken precondition (DivisibilityViolation)
+  *delta = (uint64_t)(num / 6);
+  return MEERKAT_OK;
+}
+
+meerkat_status meerkat_tc_incremental(meerkat_graph* g_after, meerkat_graph* g_update, const uint32_t* src,
+                                      const uint32_t* dst, uint64_t n, uint64_t* added, uint64_t* s) {
+  return tc_delta(g_after, g_update, src, dst, n, true, added, s);
+}
+
+meerkat_status meerkat_tc_decremental(meerkat_graph* g_after, meerkat_graph* g_update, const uint32_t* src,
+                                      const uint32_t* dst, uint64_t n, uint64_t* removed, uint64_t* s) {
+  return tc_delta(g_after, g_update, src, dst, n, false, removed, s);
+}
+
+/* ------------------------------------------------------------------ weakly connected components (wcc.cu) */
+
+meerkat_status meerkat_wcc_create(meerkat_graph* g, meerkat_wcc** out) {
+  if (!g || !out) return MEERKAT_E_INVALID_ARG;
+  *out = nullptr;
+  if (g->ws > 1) return MEERKAT_E_STATE;
+  DeviceGuard dg(g->device);
+  meerkat_wcc* c = new (std::nothrow) meerkat_wcc();
+  if (!c) return MEERKAT_E_CUDA;
+  c->g = g;
+  cudaError_t e = cudaMalloc(&c->parent, (size_t)g->V * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&c->scratch, 16);
+  if (e == cudaSuccess) e = cudaMallocHost(&c->hscratch, 16);
+  if (e == cudaSuccess) e = cudaMemsetAsync(c->scratch, 0, 16, g->stream);
+  if (e == cudaSuccess) e = launch_wcc_static(g, c->parent, c->scratch);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  if (e != cudaSuccess) { cudaGetLastError(); meerkat_wcc_destroy(c); return MEERKAT_E_CUDA; }
+  c->version = g->version;
+  *out = c;
+  return MEERKAT_OK;
+}
+
+meerkat_status meerkat_wcc_recompute(meerkat_graph* g, meerkat_wcc* c) {
+  if (!g || !c || c->g != g) return MEERKAT_E_INVALID_ARG;
+  DeviceGuard dg(g->device);
+  cudaError_t e = launch_wcc_static(g, c->parent, c->scratch);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  c->version = g->version;
+  return MEERKAT_OK;
+}
+
+meerkat_status meerkat_wcc_incremental(meerkat_graph* g, meerkat_wcc* c, const uint32_t* src, const uint32_t* dst,
+                                       uint64_t n) {
+  meerkat_status st = check_batch(g, src, dst, n);
+  if (st != MEERKAT_OK) return st;
+  if (!c || c->g != g) return MEERKAT_E_INVALID_ARG;
+  DeviceGuard dg(g->device);
+  const void *s, *d;
+  cudaError_t e = stage_in(g, 0, src, n * 4, &s);
+  if (e == cudaSuccess) e = stage_in(g, 1, dst, n * 4, &d);
+  if (e == cudaSuccess) e = launch_wcc_batch(g, c->parent, (const uint32_t*)s, (const uint32_t*)d, n);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  c->version = g->version;
+  return MEERKAT_OK;
+}
+
+meerkat_status meerkat_wcc_labels(meerkat_wcc* c, uint32_t* out) {
+  if (!c || !out) return MEERKAT_E_INVALID_ARG;
+  meerkat_graph* g = c->g;
+  DeviceGuard dg(g->device);
+  cudaError_t e = cudaMemcpyAsync(out, c->parent, (size_t)g->V * 4, cudaMemcpyDefault, g->stream);
+  if (e == cudaSuccess && !is_device_ptr(out)) e = cudaStreamSynchronize(g->stream);
+  return from_cuda(e);
+}
+
+meerkat_status meerkat_wcc_components(meerkat_wcc* c, uint64_t* n_components) {
+  if (!c || !n_components) return MEERKAT_E_INVALID_ARG;
+  meerkat_graph* g = c->g;
+  DeviceGuard dg(g->device);
+  cudaError_t e = launch_wcc_roots(g, c->parent, c->scratch + 1);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(c->hscratch, c->scratch, 16, cudaMemcpyDeviceToHost, g->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  *n_components = c->hscratch[1];
+  return MEERKAT_OK;
+}
+
+meerkat_status meerkat_wcc_destroy(meerkat_wcc* c) {
+  if (!c) return MEERKAT_E_INVALID_ARG;
+  DeviceGuard dg(c->g->device);
+  cudaStreamSynchronize(c->g->stream);
+  cudaFree(c->parent);
+  cudaFree(c->scratch);
+  if (c->hscratch) cudaFreeHost(c->hscratch);
+  delete c;
+  return MEERKAT_OK;
+}
+
 }  // extern "C"

@@ -124,7 +124,22 @@ struct meerkat_pagerank {
   bool warm_last = false;
 };
 
+struct meerkat_wcc {
+  meerkat_graph* g = nullptr;
+  uint32_t* parent = nullptr;              // union-find parents; labels after compression
+  unsigned long long* scratch = nullptr;   // device counters: [0] union attempts, [1] roots
+  unsigned long long* hscratch = nullptr;  // pinned mirror
+  uint64_t version = 0;
+};
+
 namespace mk {
+// wcc.cu
+cudaError_t launch_wcc_static(meerkat_graph* g, uint32_t* parent, unsigned long long* scratch);
+cudaError_t launch_wcc_batch(meerkat_graph* g, uint32_t* parent, const uint32_t* s, const uint32_t* d, uint64_t n);
+cudaError_t launch_wcc_roots(meerkat_graph* g, const uint32_t* parent, unsigned long long* out_dev);
+// tc.cu
+cudaError_t launch_tc_count(meerkat_graph* g1, meerkat_graph* g2, const uint32_t* src, const uint32_t* dst,
+                            uint64_t n, unsigned long long* out_dev);
 // pagerank.cu
 cudaError_t pagerank_occupancy(bool weighted, int* blocks_per_sm);
 cudaError_t launch_pagerank(meerkat_graph* g, meerkat_pagerank* p, bool warm);

@@ -70,6 +70,7 @@ class Graph:
         self.device = int(device)
         self._trees = []
         self._pageranks = []
+        self._wccs = []
 
     # ------------------------------------------------------------------ lifecycle
     def close(self):
@@ -78,6 +79,8 @@ class Graph:
                 t.close()
             for p in list(self._pageranks):
                 p.close()
+            for c in list(self._wccs):
+                c.close()
             _lib.lib().meerkat_destroy(self._h)
             self._h = None
 
@@ -181,6 +184,36 @@ class Graph:
     def pagerank(self, damping: float = 0.85, error_margin: float = 1e-5, max_iter: int = 1000) -> "PageRank":
         """Static PageRank of the current graph (needs reverse=True: in-edge mirror)."""
         return PageRank(self, damping, error_margin, max_iter)
+
+    def wcc(self) -> "WCC":
+        """Static weakly connected components of the current graph."""
+        return WCC(self)
+
+    # ------------------------------------------------------------------ triangle counting
+    def tc_count(self, other: "Graph", src, dst) -> int:
+        """Count(self, other, edges) = sum over (u, v) of |adj_self(u) ∩ adj_other(v)|."""
+        sp, ks, n = _u32(src)
+        dp, kd, _ = _u32(dst)
+        out = ctypes.c_uint64(0)
+        check(_lib.lib().meerkat_tc_count(self._h, other._h, sp, dp, n, ctypes.byref(out)), "meerkat_tc_count")
+        return int(out.value)
+
+    def tc_static(self) -> int:
+        """Triangles of this undirected (symmetric) graph."""
+        out = ctypes.c_uint64(0)
+        check(_lib.lib().meerkat_tc_static(self._h, ctypes.byref(out)), "meerkat_tc_static")
+        return int(out.value)
+
+    def tc_delta(self, update: "Graph", src, dst, insert: bool):
+        """Triangles added (insert) / removed by a batch already applied to this graph; `update` holds
+        exactly the batch; src/dst give it in both orientations.  Returns (delta, (S1, S2, S3))."""
+        sp, ks, n = _u32(src)
+        dp, kd, _ = _u32(dst)
+        out = ctypes.c_uint64(0)
+        s3 = (ctypes.c_uint64 * 3)()
+        fn = _lib.lib().meerkat_tc_incremental if insert else _lib.lib().meerkat_tc_decremental
+        check(fn(self._h, update._h, sp, dp, n, ctypes.byref(out), s3), fn.__name__)
+        return int(out.value), tuple(int(x) for x in s3)
 
     def sssp(self, source: int) -> "Tree":
         return Tree(self, source, unit=False)
@@ -323,3 +356,43 @@ class PageRank:
         st = _lib.PageRankStats()
         check(_lib.lib().meerkat_pagerank_stats_get(self._h, ctypes.byref(st)), "meerkat_pagerank_stats_get")
         return st.as_dict()
+
+
+class WCC:
+    """Weakly connected component labels: static on creation, incremental after inserts."""
+
+    def __init__(self, graph: Graph):
+        h = ctypes.c_void_p()
+        check(_lib.lib().meerkat_wcc_create(graph._h, ctypes.byref(h)), "meerkat_wcc_create")
+        self._h = h
+        self.graph = graph
+        graph._wccs.append(self)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.lib().meerkat_wcc_destroy(self._h)
+            self._h = None
+            if self in self.graph._wccs:
+                self.graph._wccs.remove(self)
+
+    def incremental(self, src, dst):
+        """Union of the batch just inserted, then full compression."""
+        sp, ks, n = _u32(src)
+        dp, kd, _ = _u32(dst)
+        check(_lib.lib().meerkat_wcc_incremental(self.graph._h, self._h, sp, dp, n), "meerkat_wcc_incremental")
+
+    def recompute(self):
+        check(_lib.lib().meerkat_wcc_recompute(self.graph._h, self._h), "meerkat_wcc_recompute")
+
+    def labels(self, out=None):
+        if out is not None:
+            check(_lib.lib().meerkat_wcc_labels(self._h, ctypes.c_void_p(out.data_ptr())), "meerkat_wcc_labels")
+            return out
+        a = np.empty(self.graph.vertex_n, np.uint32)
+        check(_lib.lib().meerkat_wcc_labels(self._h, ctypes.c_void_p(a.ctypes.data)), "meerkat_wcc_labels")
+        return a
+
+    def components(self) -> int:
+        out = ctypes.c_uint64(0)
+        check(_lib.lib().meerkat_wcc_components(self._h, ctypes.byref(out)), "meerkat_wcc_components")
+        return int(out.value)

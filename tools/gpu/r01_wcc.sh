@@ -1,0 +1,3 @@
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build10.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_wcc.py tests/test_abi.py -x -q > gpurun_out/pytest10.log 2>&1; echo t=$?
+tail -30 gpurun_out/pytest10.log
