@@ -14,6 +14,7 @@
 //    CAS ("chained at the end of the last filled slab").  A present key
 //    keeps the minimum weight via a 64-bit atomicMin on the <key, w> pair (C8).
 #include <cstdio>
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -379,6 +380,275 @@ __global__ void __launch_bounds__(UPD_BLOCK) k_query(GraphDev G, const uint32_t*
   block_or_err(&G.ctrl->err, err);
 }
 
+// ---------------------------------------------------------- thread-per-edge lookup
+
+// One thread per edge reads whole slabs itself (8 x LDG.128 of the same 128-B line): no group
+// collectives, one divergent path per edge instead of four per warp (large batches, see thread_upd).
+template <bool MAP>
+__global__ void __launch_bounds__(UPD_BLOCK) k_query_t(GraphDev G, const uint32_t* __restrict__ src,
+                                                       const uint32_t* __restrict__ dst, uint64_t n,
+                                                       uint8_t* __restrict__ found, uint32_t* __restrict__ w_out) {
+  using F = Frag<MAP>;
+  uint32_t err = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t u = src[i], v = dst[i];
+    bool hit = false;
+    uint32_t wt = 0;
+    const uint32_t ul = u < G.Vg ? local_row(G, u) : INVALID_SLAB;
+    if (u >= G.Vg || v >= G.Vg) err |= ERR_RANGE;
+    else if (ul == INVALID_SLAB) err |= ERR_PARTITION;
+    else {
+      const uint2 m = __ldcg(G.vmeta + ul);
+      if (m.x != INVALID_SLAB) {
+        uint32_t sl = m.x + bucket_of(v, m.y, G.seed);
+        for (uint32_t guard = 0; guard < WALK_LIMIT; guard++) {
+          const uint4* p = reinterpret_cast<const uint4*>(slab_ptr(G, sl));
+          uint4 q[8];
+#pragma unroll
+          for (int j = 0; j < 8; j++) q[j] = __ldcg(p + j);
+          bool empty = false;
+#pragma unroll
+          for (int j = 0; j < 8; j++) {
+#pragma unroll
+            for (int k = 0; k < F::NK; k++) {
+              if (!F::valid_cell(j, k)) continue;
+              const uint32_t key = F::key(q[j], k);
+              if (key == v) { hit = true; if (MAP) wt = F::weight(q[j], k); }
+              empty |= key == EMPTY_KEY;
+            }
+          }
+          if (hit || empty || q[7].w == INVALID_SLAB) break;
+          sl = q[7].w;
+        }
+      }
+    }
+    found[i] = hit;
+    if (w_out) w_out[i] = hit ? wt : 0u;
+  }
+  block_or_err(&G.ctrl->err, err);
+}
+
+// ---------------------------------------------------------- thread-per-edge updates
+//
+// The same protocols (C9 search-then-claim insert, link lock, TOMBSTONE delete) with ONE thread per
+// edge reading whole slabs (8 x LDG.128 of one 128-B line): no group collectives and one divergent
+// path per edge.  Used for large batches (thread_upd).
+
+template <bool MAP>
+__device__ __forceinline__ void thread_read_slab(const GraphDev& G, uint32_t s, uint4 (&q)[8]) {
+  const uint4* p = reinterpret_cast<const uint4*>(slab_ptr(G, s));
+#pragma unroll
+  for (int j = 0; j < 8; j++) q[j] = __ldcg(p + j);
+}
+
+template <bool MAP>
+__device__ uint32_t thread_alloc(const GraphDev& G, uint32_t u, uint64_t first) {
+  const unsigned long long idx = atomicAdd(&G.ctrl->pool_top, 1ull);
+  if (idx >= G.P) return INVALID_SLAB;
+  const uint32_t s = G.H + (uint32_t)idx;
+  uint4* p = reinterpret_cast<uint4*>(slab_ptr(G, s));
+#pragma unroll
+  for (int j = 0; j < 8; j++) {
+    uint4 f;
+    f.x = fill_word(MAP, 4 * j + 0); f.y = fill_word(MAP, 4 * j + 1);
+    f.z = fill_word(MAP, 4 * j + 2); f.w = fill_word(MAP, 4 * j + 3);
+    if (j == 0) { f.x = (uint32_t)first; if (MAP) f.y = (uint32_t)(first >> 32); }
+    p[j] = f;
+  }
+  G.owner[s] = u;
+  __threadfence();
+  return s;
+}
+
+// Link lock (see group_link): 1 = our slab holding the key is linked, -1 = pool exhausted,
+// 0 = another thread linked first (*next_out = its slab or INVALID_SLAB).
+template <bool MAP>
+__device__ int thread_link(const GraphDev& G, uint32_t u, uint64_t item, uint32_t* link, uint32_t& next_out) {
+  uint32_t old = atomicCAS(link, INVALID_SLAB, LINKING);
+  if (old == INVALID_SLAB) {
+    const uint32_t s = thread_alloc<MAP>(G, u, item);
+    atomicExch(link, s);   // INVALID_SLAB releases the lock
+    return s == INVALID_SLAB ? -1 : 1;
+  }
+  uint32_t spins = 0;
+  while (old == LINKING) {
+    __nanosleep(64);
+    old = *reinterpret_cast<volatile uint32_t*>(link);
+    if (++spins == WATCHDOG) { atomicOr(&G.ctrl->err, (unsigned)ERR_STATE); return -1; }
+  }
+  next_out = old;
+  return 0;
+}
+
+template <bool MAP>
+__device__ int thread_insert(const GraphDev& G, uint32_t u, uint32_t v, uint32_t wt) {
+  using F = Frag<MAP>;
+  constexpr int NK = F::NK;
+  const uint64_t item = MAP ? (((uint64_t)wt << 32) | v) : (uint64_t)v;
+  const uint2 m = __ldcg(G.vmeta + u);
+  uint32_t head = m.x;
+  while (head == INVALID_SLAB || head == LINKING) {   // lazily headed vertex (C22b)
+    uint32_t nxt = INVALID_SLAB;
+    const int r = thread_link<MAP>(G, u, item, reinterpret_cast<uint32_t*>(&G.vmeta[u].x), nxt);
+    if (r != 0) return r;
+    head = nxt;
+  }
+  uint32_t cur = head + bucket_of(v, m.y, G.seed);
+  for (uint32_t guard = 0; guard < WATCHDOG; guard++) {
+    // pass 1: up to the first slab holding an EMPTY cell; first writable cell remembered
+    uint32_t s = cur, cand_slab = INVALID_SLAB, tail = INVALID_SLAB, found_slab = INVALID_SLAB;
+    int cand_cell = -1, found_cell = -1;
+    uint64_t cand_old = 0;
+    for (uint32_t walk = 0; walk < WALK_LIMIT; walk++) {
+      uint4 q[8];
+      thread_read_slab<MAP>(G, s, q);
+      bool empty = false;
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+#pragma unroll
+        for (int k = 0; k < NK; k++) {
+          if (!F::valid_cell(j, k)) continue;
+          const uint32_t key = F::key(q[j], k);
+          const int c = j * NK + k;
+          if (key == v && found_cell < 0) found_cell = c;
+          if ((key == EMPTY_KEY || key == TOMBSTONE_KEY) && cand_slab == INVALID_SLAB && cand_cell < 0) {
+            cand_cell = c;
+            cand_old = MAP ? (((uint64_t)F::weight(q[j], k) << 32) | key) : (uint64_t)key;
+          }
+          empty |= key == EMPTY_KEY;
+        }
+      }
+      if (cand_cell >= 0 && cand_slab == INVALID_SLAB) cand_slab = s;
+      if (found_cell >= 0) { found_slab = s; break; }
+      const uint32_t nxt = q[7].w;
+      if (empty || nxt == INVALID_SLAB || nxt == LINKING) { tail = s; break; }
+      if (nxt >= G.H + G.P) { atomicOr(&G.ctrl->err, (unsigned)ERR_STATE); return -1; }
+      s = nxt;
+    }
+    if (found_cell >= 0) {   // present: min-weight upsert (C8)
+      if (MAP) atomicMin(reinterpret_cast<unsigned long long*>(slab_ptr(G, found_slab) + 2 * found_cell),
+                         (unsigned long long)item);
+      return 0;
+    }
+    if (cand_slab != INVALID_SLAB) {   // pass 2: claim
+      bool ok;
+      if (MAP) {
+        unsigned long long* cell = reinterpret_cast<unsigned long long*>(slab_ptr(G, cand_slab) + 2 * cand_cell);
+        ok = atomicCAS(cell, (unsigned long long)cand_old, (unsigned long long)item) == cand_old;
+      } else {
+        ok = atomicCAS(slab_ptr(G, cand_slab) + cand_cell, (unsigned int)cand_old, (unsigned int)item) ==
+             (unsigned int)cand_old;
+      }
+      if (ok) return 1;
+      cur = cand_slab;   // the cell changed: rescan from its slab
+      continue;
+    }
+    if (tail == INVALID_SLAB) { atomicOr(&G.ctrl->err, (unsigned)ERR_STATE); return -1; }
+    uint32_t nxt = INVALID_SLAB;   // full list: link a pool slab holding the key after the tail
+    const int r = thread_link<MAP>(G, u, item, slab_ptr(G, tail) + (SLAB_WORDS - 1), nxt);
+    if (r != 0) return r;
+    cur = nxt == INVALID_SLAB ? tail : nxt;
+  }
+  atomicOr(&G.ctrl->err, (unsigned)ERR_STATE);
+  return -1;
+}
+
+template <bool MAP>
+__device__ bool thread_delete(const GraphDev& G, uint32_t u, uint32_t v) {
+  using F = Frag<MAP>;
+  constexpr int NK = F::NK;
+  const uint2 m = __ldcg(G.vmeta + u);
+  if (m.x == INVALID_SLAB || m.x == LINKING) return false;
+  uint32_t s = m.x + bucket_of(v, m.y, G.seed);
+  for (uint32_t walk = 0; walk < WALK_LIMIT; walk++) {
+    uint4 q[8];
+    thread_read_slab<MAP>(G, s, q);
+    bool empty = false;
+    int fc = -1;
+    uint64_t val = 0;
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+#pragma unroll
+      for (int k = 0; k < NK; k++) {
+        if (!F::valid_cell(j, k)) continue;
+        const uint32_t key = F::key(q[j], k);
+        if (key == v && fc < 0) { fc = j * NK + k; val = MAP ? (((uint64_t)F::weight(q[j], k) << 32) | key) : key; }
+        empty |= key == EMPTY_KEY;
+      }
+    }
+    if (fc >= 0) {   // TOMBSTONE; a failed CAS means a duplicate in this batch won
+      if (MAP) return atomicCAS(reinterpret_cast<unsigned long long*>(slab_ptr(G, s) + 2 * fc),
+                                (unsigned long long)val, (unsigned long long)TOMB_PAIR) == val;
+      return atomicCAS(slab_ptr(G, s) + fc, (unsigned int)val, TOMBSTONE_KEY) == (unsigned int)val;
+    }
+    const uint32_t nxt = q[7].w;
+    if (empty || nxt == INVALID_SLAB || nxt >= G.H + G.P) return false;
+    s = nxt;
+  }
+  return false;
+}
+
+template <bool MAP>
+__global__ void __launch_bounds__(UPD_BLOCK) k_insert_t(const __grid_constant__ UpdArgs A) {
+  uint32_t added[2] = {0, 0}, err[2] = {0, 0};
+  const uint64_t total = A.n * A.ns;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t st; uint64_t e;
+    upd_item(A, i, st, e);
+    const GraphDev& G = A.G[st];
+    const uint32_t a = A.src[e], b = A.dst[e], wt = MAP ? A.w[e] : 0u;
+    const uint32_t u = st ? b : a, v = st ? a : b;
+    if (u >= G.Vg || v >= G.Vg) { err[st] |= ERR_RANGE; continue; }
+    if (MAP && (wt == 0 || wt >= W_LIMIT)) { err[st] |= ERR_WEIGHT; continue; }
+    const uint32_t ul = local_row(G, u);
+    if (ul == INVALID_SLAB) { err[st] |= ERR_PARTITION; continue; }
+    const int r = thread_insert<MAP>(G, ul, v, wt);
+    if (r < 0) err[st] |= ERR_CAPACITY;
+    else if (r) { added[st]++; atomicAdd(G.deg + ul, 1u); }
+  }
+  for (uint32_t k = 0; k < A.ns; k++) {
+    block_or_err(&A.G[k].ctrl->err, err[k]);
+    block_add(&A.G[k].ctrl->n_inserted, &A.G[k].ctrl->ins_total, added[k]);
+  }
+}
+
+template <bool MAP>
+__global__ void __launch_bounds__(UPD_BLOCK) k_delete_t(const __grid_constant__ UpdArgs A) {
+  uint32_t removed[2] = {0, 0}, err[2] = {0, 0};
+  const uint64_t total = A.n * A.ns;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t st; uint64_t e;
+    upd_item(A, i, st, e);
+    const GraphDev& G = A.G[st];
+    const uint32_t a = A.src[e], b = A.dst[e];
+    const uint32_t u = st ? b : a, v = st ? a : b;
+    if (u >= G.Vg || v >= G.Vg) { err[st] |= ERR_RANGE; continue; }
+    const uint32_t ul = local_row(G, u);
+    if (ul == INVALID_SLAB) { err[st] |= ERR_PARTITION; continue; }
+    if (thread_delete<MAP>(G, ul, v)) { removed[st]++; atomicSub(G.deg + ul, 1u); }
+  }
+  for (uint32_t k = 0; k < A.ns; k++) {
+    block_or_err(&A.G[k].ctrl->err, err[k]);
+    block_add(&A.G[k].ctrl->n_deleted, &A.G[k].ctrl->del_total, removed[k]);
+  }
+}
+
+// Kernel choice by batch size (measured): small batches are latency-bound and the
+// 8-lane groups (four independent slabs per warp instruction, fewer requests per slab) win; large
+// batches are throughput-bound and thread-per-edge wins (no group collectives: 2x at 1M edges and in
+// the bulk build).  MEERKAT_THREAD_UPD=0/1 forces one kind (experiments and tests).
+constexpr uint64_t THREAD_MIN_ITEMS = 400000;
+
+static bool thread_upd(uint64_t items) {
+  const char* e = std::getenv("MEERKAT_THREAD_UPD");
+  if (e && (e[0] == '0' || e[0] == '1')) return e[0] == '1';
+  return items >= THREAD_MIN_ITEMS;
+}
+
+static unsigned grid_threads(meerkat_graph* g, uint64_t n) {
+  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + UPD_BLOCK - 1) / UPD_BLOCK, (uint64_t)g->sm_count * 8));
+}
+
 // ------------------------------------------------------------------ export (streaming)
 
 template <bool MAP>
@@ -624,6 +894,13 @@ cudaError_t launch_insert(meerkat_graph* g, Store* st0, Store* st1, const uint32
   A.G[0] = st0->dev;
   if (st1) A.G[1] = st1->dev;
   A.src = s; A.dst = d; A.w = w; A.n = n; A.ns = st1 ? 2u : 1u;
+  if (thread_upd(n * A.ns)) {
+    const unsigned gt = grid_threads(g, n * A.ns);
+    if (g->weighted) k_insert_t<true><<<gt, UPD_BLOCK, 0, g->stream>>>(A);
+    else k_insert_t<false><<<gt, UPD_BLOCK, 0, g->stream>>>(A);
+    g->launches++;
+    return cudaGetLastError();
+  }
   const unsigned gb = grid_for(g, n * A.ns, 0);
   if (g->weighted) k_insert<true><<<gb, UPD_BLOCK, 0, g->stream>>>(A);
   else k_insert<false><<<gb, UPD_BLOCK, 0, g->stream>>>(A);
@@ -637,6 +914,13 @@ cudaError_t launch_delete(meerkat_graph* g, Store* st0, Store* st1, const uint32
   A.G[0] = st0->dev;
   if (st1) A.G[1] = st1->dev;
   A.src = s; A.dst = d; A.w = nullptr; A.n = n; A.ns = st1 ? 2u : 1u;
+  if (thread_upd(n * A.ns)) {
+    const unsigned gt = grid_threads(g, n * A.ns);
+    if (g->weighted) k_delete_t<true><<<gt, UPD_BLOCK, 0, g->stream>>>(A);
+    else k_delete_t<false><<<gt, UPD_BLOCK, 0, g->stream>>>(A);
+    g->launches++;
+    return cudaGetLastError();
+  }
   const unsigned gb = grid_for(g, n * A.ns, 0);
   if (g->weighted) k_delete<true><<<gb, UPD_BLOCK, 0, g->stream>>>(A);
   else k_delete<false><<<gb, UPD_BLOCK, 0, g->stream>>>(A);
@@ -647,6 +931,14 @@ cudaError_t launch_delete(meerkat_graph* g, Store* st0, Store* st1, const uint32
 cudaError_t launch_query(meerkat_graph* g, Store& st, const uint32_t* s, const uint32_t* d, uint64_t n, uint8_t* found,
                          uint32_t* w_out) {
   if (!n) return cudaSuccess;
+  if (thread_upd(n)) {
+    const unsigned gt = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + UPD_BLOCK - 1) / UPD_BLOCK,
+                                                                         (uint64_t)g->sm_count * 8));
+    if (g->weighted) k_query_t<true><<<gt, UPD_BLOCK, 0, g->stream>>>(st.dev, s, d, n, found, w_out);
+    else k_query_t<false><<<gt, UPD_BLOCK, 0, g->stream>>>(st.dev, s, d, n, found, w_out);
+    g->launches++;
+    return cudaGetLastError();
+  }
   const unsigned gb = grid_for(g, n, 0);
   if (g->weighted) k_query<true><<<gb, UPD_BLOCK, 0, g->stream>>>(st.dev, s, d, n, found, w_out);
   else k_query<false><<<gb, UPD_BLOCK, 0, g->stream>>>(st.dev, s, d, n, found, w_out);

@@ -1,5 +1,6 @@
 """GPU parity of the slab store against the CPU oracle:
-edge sets, insert/delete counts and query answers must be bit-exact."""
+edge sets, insert/delete counts and query answers must be bit-exact — for both update-kernel
+kinds (group-cooperative and thread-per-edge, store.cu thread_upd)."""
 import json
 import os
 
@@ -19,6 +20,14 @@ torch = pytest.importorskip("torch")
 def _need_gpu():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
+
+
+@pytest.fixture(autouse=True, params=["group", "thread"])
+def update_kernel(request, monkeypatch):
+    """Every store test runs with both update-kernel kinds: 8-lane groups (small batches) and
+    thread-per-edge (large batches), forced via MEERKAT_THREAD_UPD (read at each launch)."""
+    monkeypatch.setenv("MEERKAT_THREAD_UPD", "1" if request.param == "thread" else "0")
+    return request.param
 
 
 def G(*a, **k):
