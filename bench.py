@@ -65,6 +65,8 @@ def parse():
     p.add_argument("--tc", action=argparse.BooleanOptionalAction, default=True,
                    help="also time triangle counting on a symmetrised R-MAT (--tc-scale) graph (NEXT-4)")
     p.add_argument("--tc-scale", type=int, default=20)
+    p.add_argument("--config4", action=argparse.BooleanOptionalAction, default=True,
+                   help="also time BASELINE config 4 (R-MAT scale 22, ef 24, mixed 1%%-of-E delete / insert rounds)")
     p.add_argument("--pagerank", action=argparse.BooleanOptionalAction, default=True,
                    help="also time static and dynamic PageRank on the same graph (SURVEY §8(f) NEXT-1; "
                         "needs the in-edge mirror, i.e. --frontier reverse)")
@@ -542,6 +544,53 @@ def measure_wcc(g, W, T, stream, flush):
     return {"static_ms": st_ms, "incremental_ms": inc_ms, "batch": int(len(s)), "components": comps}
 
 
+def measure_config4(args, dev, stream, flush, rounds=4):
+    """BASELINE config 4 (reading C25): R-MAT scale 22, edge factor 24 ('LJ/Orkut-shaped',
+    ~97 M edges); each round deletes 1% of E (970 K edges) and runs the fused decremental SSSP + BFS
+    update, then inserts 970 K held-out edges and runs the fused incremental update.  One warm-up
+    round, then `rounds` timed rounds (CUDA events on the graph's stream, L2 flushed between calls)."""
+    import torch
+    import synth
+    from paper_2305_17813_b200 import Graph
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.uint32).view(np.int32)).to(dev)
+    n1 = 970_000
+    W = synth.rmat_dynamic(22, 24, batch=n1, n_ins=rounds + 1, n_del=rounds + 1)
+    V = W.vertex_n
+    bs, bd, bw = W.base
+    g = Graph(V, weighted=True, degree_hints=T(np.bincount(bs, minlength=V).astype(np.uint32)), reverse=True,
+              in_degree_hints=T(np.bincount(bd, minlength=V).astype(np.uint32)), device=dev.index or 0, stream=stream)
+    g.insert(T(bs), T(bd), T(bw), count=False)
+    sp, bf = g.sssp(W.source), g.bfs(W.source)
+    ev = lambda: [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    names = ["delete", "trees_dec", "insert", "trees_inc"]
+    per = {n: [] for n in names}
+    for r in range(rounds + 1):
+        ds, dd = T(W.deletes[r][0]), T(W.deletes[r][1])
+        is_, id_, iw = (T(x) for x in W.inserts[r])
+        e = ev()
+        flush.zero_()
+        e[0].record(stream); g.delete(ds, dd, count=False); e[1].record(stream)
+        g.trees_decremental([sp, bf], ds, dd); e[2].record(stream)
+        flush.zero_()   # (between calls; the flush is not inside any interval below)
+        e[2].synchronize()
+        e2 = ev()
+        e2[0].record(stream); g.insert(is_, id_, iw, count=False); e2[1].record(stream)
+        g.trees_incremental([sp, bf], is_, id_, iw); e2[2].record(stream)
+        e2[2].synchronize()
+        if r == 0:
+            continue
+        per["delete"].append(e[0].elapsed_time(e[1])); per["trees_dec"].append(e[1].elapsed_time(e[2]))
+        per["insert"].append(e2[0].elapsed_time(e2[1])); per["trees_inc"].append(e2[1].elapsed_time(e2[2]))
+    mean = {n: float(np.mean(v)) for n, v in per.items()}
+    out = {"workload": f"rmat-s22-ef24 (BASELINE config 4), {len(bs)} base edges, {n1}-edge delete + insert rounds",
+           "rounds": rounds, "per_call_ms": mean,
+           "round_ms": sum(mean.values()),
+           "update_edges_per_s": 2 * n1 / ((mean["delete"] + mean["insert"]) / 1e3),
+           "sssp_bfs_fused_ms_per_batch": {"decremental": mean["trees_dec"], "incremental": mean["trees_inc"]}}
+    g.close()
+    return out
+
+
 def measure_tc(args, dev, stream):
     """Triangle counting on a symmetrised R-MAT graph (both orientations stored, set store): the static
     count and the dynamic deltas of a 10K-undirected-edge insert and delete batch
@@ -678,6 +727,7 @@ def run_ours(args, ws, rank, local):
 
     sweep = store_sweep(args, dev, stream) if args.sweep and ws == 1 else None
     tc = measure_tc(args, dev, stream) if args.tc and ws == 1 else None
+    config4 = measure_config4(args, dev, stream, flush) if args.config4 and ws == 1 else None
 
     cb = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -719,6 +769,7 @@ def run_ours(args, ws, rank, local):
         "pagerank": pagerank,
         "wcc": wcc,
         "tc": tc,
+        "config4": config4,
         "generate_s": gen_s,
     }
     if rank == 0:
