@@ -695,7 +695,9 @@ def run_ours(args, ws, rank, local):
         e_ms = allreduce_max(e_ms, ws)
         n = args.batch
         e2e = {"value": edges / (e_ms / 1e3), "unit": "edges/s",
-               "h2d_bytes_per_step": n * 4 * ((3 + 3 + 2 + 2) if args.fused else (3 + 3 + 2 + 2 + 2 + 2)),
+               # src, dst, w of the insert batch and src, dst of the delete batch; the tree calls that
+               # follow with the same host arrays reuse the staged copies (api.cu stage_in_reuse)
+               "h2d_bytes_per_step": n * 4 * (3 + 2),
                "d2h_bytes_per_step": 2 * 64,
                "ms_per_step": e_ms / K}
     pagerank = None

@@ -47,6 +47,7 @@ bool is_device_ptr(const void* p) {
 }
 
 cudaError_t ensure_stage(meerkat_graph* g, int slot, size_t bytes) {
+  g->staged_host[slot] = nullptr;   // the slot's content is about to change
   if (g->stage_bytes[slot] >= bytes) return cudaSuccess;
   cudaError_t e = cudaStreamSynchronize(g->stream);
   if (e != cudaSuccess) return e;
@@ -64,10 +65,28 @@ cudaError_t ensure_stage(meerkat_graph* g, int slot, size_t bytes) {
 cudaError_t stage_in(meerkat_graph* g, int slot, const void* p, size_t bytes, const void** out) {
   *out = p;
   if (!p || !bytes || is_device_ptr(p)) return cudaSuccess;
+  g->staged_host[slot] = nullptr;
   cudaError_t e = ensure_stage(g, slot, bytes);
   if (e != cudaSuccess) return e;
   *out = g->stage[slot];
   return cudaMemcpyAsync(g->stage[slot], p, bytes, cudaMemcpyHostToDevice, g->stream);
+}
+
+// A mutation's host batch, staged in `slot`, stays reusable until the slot is overwritten: the tree
+// update that must follow with the same batch (ordering contract, meerkat.h) does not copy it again.
+void remember_stage(meerkat_graph* g, int slot, const void* p, size_t bytes) {
+  if (!p || !bytes || is_device_ptr(p)) return;
+  g->staged_host[slot] = p;
+  g->staged_len[slot] = bytes;
+  g->staged_version[slot] = g->version;
+}
+
+cudaError_t stage_in_reuse(meerkat_graph* g, int slot, const void* p, size_t bytes, const void** out) {
+  if (p && bytes && p == g->staged_host[slot] && bytes == g->staged_len[slot] && g->staged_version[slot] == g->version) {
+    *out = g->stage[slot];
+    return cudaSuccess;
+  }
+  return stage_in(g, slot, p, bytes, out);
 }
 
 // Read the control block back (synchronises); returns and clears the sticky error.
@@ -206,6 +225,9 @@ meerkat_status meerkat_insert_batch(meerkat_graph* g, const uint32_t* src, const
   if (e != cudaSuccess) return MEERKAT_E_CUDA;
   g->version++;
   g->last_kind = 1;
+  remember_stage(g, 0, src, n * 4);
+  remember_stage(g, 1, dst, n * 4);
+  if (w) remember_stage(g, 2, w, n * 4);
   if (!n_inserted) return MEERKAT_OK;
   st = collect(g);
   *n_inserted = g->out.hctrl->n_inserted;
@@ -226,6 +248,8 @@ meerkat_status meerkat_delete_batch(meerkat_graph* g, const uint32_t* src, const
   if (e != cudaSuccess) return MEERKAT_E_CUDA;
   g->version++;
   g->last_kind = 2;
+  remember_stage(g, 0, src, n * 4);
+  remember_stage(g, 1, dst, n * 4);
   if (!n_deleted) return MEERKAT_OK;
   st = collect(g);
   *n_deleted = g->out.hctrl->n_deleted;
@@ -445,9 +469,9 @@ static meerkat_status trees_update(meerkat_graph* g, meerkat_tree* const* ts, ui
   if (need_w && n && !w) return MEERKAT_E_INVALID_ARG;
   DeviceGuard dg(g->device);
   const void *s, *d, *ww = nullptr;
-  cudaError_t e = stage_in(g, 0, src, n * 4, &s);
-  if (e == cudaSuccess) e = stage_in(g, 1, dst, n * 4, &d);
-  if (e == cudaSuccess && need_w) e = stage_in(g, 2, w, n * 4, &ww);
+  cudaError_t e = stage_in_reuse(g, 0, src, n * 4, &s);
+  if (e == cudaSuccess) e = stage_in_reuse(g, 1, dst, n * 4, &d);
+  if (e == cudaSuccess && need_w) e = stage_in_reuse(g, 2, w, n * 4, &ww);
   if (e == cudaSuccess)
     e = launch_tree(g, ts, k, kind == 1 ? MODE_INCREMENTAL : MODE_DECREMENTAL, (const uint32_t*)s, (const uint32_t*)d,
                     (const uint32_t*)ww, n);

@@ -81,6 +81,10 @@ struct meerkat_graph {
   int sm_count = 0;
   void* stage[4] = {nullptr, nullptr, nullptr, nullptr};   // staging for host inputs / outputs
   size_t stage_bytes[4] = {0, 0, 0, 0};
+  // a mutation's staged host batch, reusable by the tree call that must follow with the same batch
+  const void* staged_host[4] = {nullptr, nullptr, nullptr, nullptr};
+  size_t staged_len[4] = {0, 0, 0, 0};
+  uint64_t staged_version[4] = {0, 0, 0, 0};
   int tree_blocks_per_sm[4] = {0, 0, 0, 0};   // cooperative occupancy: static, incremental, decremental, vanilla
   int latency_bps = 0;                      // blocks/SM for latency-bound tree calls (0 = occupancy)
   unsigned long long* rscratch = nullptr;   // meerkat_route: device counts + cursors

@@ -269,3 +269,39 @@ def test_fused_trees_match_oracle(reverse, hashing):
     t.decremental(cuda(s), cuda(d))
     b.decremental(cuda(s), cuda(d))
     assert_nodes(t.nodes(), o.sssp(src)[1], "per-tree after fused")
+
+
+def test_host_batches_staged_once_and_reused():
+    """Host (numpy) batches: the tree calls that follow a mutation with the SAME host arrays reuse
+    the mutation's staged device copy (api.cu stage_in_reuse); equal arrays at other addresses are
+    staged again.  Both paths must give the oracle's trees (fused and per-tree calls)."""
+    V = 1024
+    s, d, w = synth.uniform(V, 8192)
+    g = G(V, weighted=True, degree_hints=synth.degrees(s, V), reverse=True, in_degree_hints=synth.degrees(d, V))
+    g.insert(s, d, w)
+    o = oracle.OracleGraph(V)
+    o.insert(s, d, w)
+    sp, bf = g.sssp(0), g.bfs(0)
+    rng = np.random.default_rng(21)
+    for step in range(6):
+        if step % 2 == 0:
+            bs = rng.integers(0, V, 200).astype(np.uint32); bd = rng.integers(0, V, 200).astype(np.uint32)
+            bw = rng.integers(1, 65, 200).astype(np.uint32)
+            g.insert(bs, bd, bw)
+            o.insert(bs, bd, bw)
+            if step == 2:   # copies at other addresses: staged again
+                sp.incremental(bs.copy(), bd.copy(), bw.copy()); bf.incremental(bs.copy(), bd.copy())
+            else:
+                g.trees_incremental([sp, bf], bs, bd, bw)
+        else:
+            es, ed, _ = o.edges()
+            pick = rng.choice(len(es), 150, replace=False)
+            bs, bd = es[pick].copy(), ed[pick].copy()
+            g.delete(bs, bd)
+            o.delete(bs, bd)
+            if step == 3:
+                sp.decremental(bs, bd); bf.decremental(bs, bd)
+            else:
+                g.trees_decremental([sp, bf], bs, bd)
+        assert_nodes(sp.nodes(), o.sssp(0)[1], f"sssp step {step}")
+        assert_nodes(bf.nodes(), o.bfs(0)[1], f"bfs step {step}")
