@@ -11,6 +11,8 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.path.join(HERE, "libmeerkat.so")
+if os.environ.get("MEERKAT_SO_PATH"):   # A/B experiments: another in-tree build of the same sources
+    SO_PATH = os.path.abspath(os.environ["MEERKAT_SO_PATH"])
 
 STATUS = {
     0: "MEERKAT_OK", 1: "MEERKAT_E_INVALID_ARG", 2: "MEERKAT_E_VERTEX_RANGE", 3: "MEERKAT_E_WEIGHT",

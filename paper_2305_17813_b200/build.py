@@ -36,7 +36,15 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    """Build OUT (or `out`, with extra -D `defines`, for A/B experiments)."""
+    if out is not None:
+        cmd = [os.environ.get("NVCC", "nvcc"), *NVCC_FLAGS, *[f"-D{d}" for d in defines], *sources(), "-o", out]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("nvcc failed")
+        return out
     if not force and not stale():
         return OUT
     nvcc = os.environ.get("NVCC", "nvcc")

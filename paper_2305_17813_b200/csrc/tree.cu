@@ -227,12 +227,19 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const TreeDev& T, int 
 template <bool MAP, int VISIT, bool V32 = false>
 __device__ __forceinline__ uint32_t run_rounds(const TreeArgs& A, const uint32_t* epoch, cg::grid_group& grid,
                                                uint32_t r, Counters& c) {
+  __shared__ unsigned long long s_n[MAX_TREES];
   for (;;) {
+    // one load of each frontier size per block (not one per thread: ~150 K same-address loads
+    // right after every barrier), broadcast through shared memory; the barrier that ends the
+    // round orders the next round's write after this round's reads
+    if (threadIdx.x < MAX_TREES)
+      s_n[threadIdx.x] = threadIdx.x < A.ntrees ? __ldcg(&A.T[threadIdx.x].ctrl->size[r % 3]) : 0ull;
+    __syncthreads();
     uint64_t n[MAX_TREES];
     bool any = false;
 #pragma unroll
     for (int k = 0; k < MAX_TREES; k++) {
-      n[k] = k < (int)A.ntrees ? __ldcg(&A.T[k].ctrl->size[r % 3]) : 0;
+      n[k] = s_n[k];
       any |= n[k] != 0;
     }
     if (!any) break;
@@ -262,12 +269,22 @@ __device__ __forceinline__ void finish(const TreeArgs& A, Counters& c, const uin
   timeline(A.T[0].ctrl);
 }
 
+// Every tree's stamp-epoch base, loaded once per block and broadcast (not by every thread).
+__device__ __forceinline__ void load_epochs(const TreeArgs& A, uint32_t (&epoch)[MAX_TREES]) {
+  __shared__ uint32_t s_ep[MAX_TREES];
+  if (threadIdx.x < A.ntrees) s_ep[threadIdx.x] = __ldcg(A.T[threadIdx.x].epoch_ptr);
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < MAX_TREES; k++) epoch[k] = k < (int)A.ntrees ? s_ep[k] : 0u;
+}
+
 // ------------------------------------------------------------------ static
 
 template <bool MAP, bool V32>
 __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_static(const __grid_constant__ TreeArgs A) {
   const TreeDev& T = A.T[0];
-  const uint32_t epoch[MAX_TREES] = {__ldcg(T.epoch_ptr)};
+  uint32_t epoch[MAX_TREES];
+  load_epochs(A, epoch);
   timeline(T.ctrl);
   cg::grid_group grid = cg::this_grid();
   Counters c;
@@ -293,8 +310,8 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_static(const __grid_cons
 
 template <bool MAP>
 __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_inc(const __grid_constant__ TreeArgs A) {
-  uint32_t epoch[MAX_TREES] = {};
-  for (uint32_t k = 0; k < A.ntrees; k++) epoch[k] = __ldcg(A.T[k].epoch_ptr);
+  uint32_t epoch[MAX_TREES];
+  load_epochs(A, epoch);
   timeline(A.T[0].ctrl);
   cg::grid_group grid = cg::this_grid();
   Counters c;
@@ -449,8 +466,8 @@ __device__ __forceinline__ void dec_scan(const TreeArgs& A, const uint32_t* filt
 template <bool MAP>
 __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_dec(const __grid_constant__ TreeArgs A) {
   extern __shared__ uint32_t filt[];
-  uint32_t epoch[MAX_TREES] = {};
-  for (uint32_t k = 0; k < A.ntrees; k++) epoch[k] = __ldcg(A.T[k].epoch_ptr);
+  uint32_t epoch[MAX_TREES];
+  load_epochs(A, epoch);
   timeline(A.T[0].ctrl);
   cg::grid_group grid = cg::this_grid();
   Counters c;
@@ -497,7 +514,12 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_dec(const __grid_constan
   // (iii) valid -> invalid frontier, fused with the first relaxation
   uint64_t n_inv[MAX_TREES] = {};
   uint64_t n_inv_all = 0;
-  for (uint32_t k = 0; k < A.ntrees; k++) { n_inv[k] = __ldcg(&A.T[k].ctrl->inval_n); n_inv_all += n_inv[k]; }
+  {
+    __shared__ unsigned long long s_inv[MAX_TREES];
+    if (threadIdx.x < A.ntrees) s_inv[threadIdx.x] = __ldcg(&A.T[threadIdx.x].ctrl->inval_n);
+    __syncthreads();
+    for (uint32_t k = 0; k < A.ntrees; k++) { n_inv[k] = s_inv[k]; n_inv_all += n_inv[k]; }
+  }
   if (n_inv_all && A.R.slabs) {
     // in-edge mirror present: the frontier is exactly the in-edges of V_invalid from valid sources
     for (uint32_t k = 0; k < A.ntrees; k++) {
@@ -511,9 +533,12 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_dec(const __grid_constan
     }
     grid.sync();
     timeline(A.T[0].ctrl);
+    __shared__ unsigned long long s_pull[MAX_TREES];
+    if (threadIdx.x < A.ntrees) s_pull[threadIdx.x] = __ldcg(&A.T[threadIdx.x].ctrl->pull_n);
+    __syncthreads();
     for (uint32_t k = 0; k < A.ntrees; k++) {
       const TreeDev& T = A.T[k];
-      expand<MAP, PULL>(A, T, k, T.fr[(r1 + 1) & 1], __ldcg(&T.ctrl->pull_n), T.fr[r1 & 1], &T.ctrl->size[r1 % 3],
+      expand<MAP, PULL>(A, T, k, T.fr[(r1 + 1) & 1], s_pull[k], T.fr[r1 & 1], &T.ctrl->size[r1 % 3],
                         epoch[k] + r1, c);
     }
   } else if (n_inv_all) {
@@ -531,7 +556,10 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_dec(const __grid_constan
         }
       __syncthreads();
     }
-    const uint32_t n_slabs = A.G.H + (uint32_t)min((unsigned long long)A.G.P, __ldcg(&A.G.ctrl->pool_top));
+    __shared__ unsigned long long s_top;
+    if (threadIdx.x == 0) s_top = __ldcg(&A.G.ctrl->pool_top);
+    __syncthreads();
+    const uint32_t n_slabs = A.G.H + (uint32_t)min((unsigned long long)A.G.P, s_top);
     if (tid == 0) c.scan_slabs = n_slabs;
     dec_scan<MAP>(A, filt, use_filter, n_slabs, r1, epoch, c);
   }
