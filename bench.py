@@ -847,6 +847,9 @@ def run_dist(args, ws, rank, local):
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
+        if args.json_out:
+            with open(args.json_out, "w") as f:
+                f.write(json.dumps(line) + "\n")
 
 
 def main():

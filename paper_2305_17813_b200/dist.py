@@ -241,7 +241,7 @@ class DistTree:
         sent = sum(counts)
         meta = torch.tensor([[counts[p], int(res.frontier), sent] for p in range(ws)], dtype=torch.int64,
                             device=tp._dev()).view(-1)
-        rmeta, _ = tp.alltoallv(meta, [1] * ws, elem=3)
+        rmeta = tp.alltoallv_known(meta, [1] * ws, [1] * ws, elem=3)   # fixed size: no count exchange
         rmeta = rmeta.view(ws, 3).cpu()
         if int(rmeta[:, 1].sum()) + int(rmeta[:, 2].sum()) == 0:
             return None, False
