@@ -807,23 +807,25 @@ def run_dist(args, ws, rank, local):
     ins = [tuple(T(sl(x)) for x in b) for b in W.inserts]
     dels = [tuple(T(sl(x)) for x in b[:2]) for b in W.deletes]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    names = NAMES_FUSED   # SSSP + BFS in lock step: one exchange per round for both trees
     for i in range(Wm):
-        one_step(g, sp, bf, ins[i], dels[i], [torch.cuda.Event(enable_timing=True) for _ in range(7)], stream)
+        one_step(g, sp, bf, ins[i], dels[i], [torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)],
+                 stream, fused=True)
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
-    per_call = {n: [] for n in NAMES}
+    per_call = {n: [] for n in names}
     total_ms = 0.0
     for k in range(K):
         flush.zero_()
         torch.cuda.synchronize()
         barrier(ws)
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
-        one_step(g, sp, bf, ins[Wm + k], dels[Wm + k], evs, stream)
-        evs[6].synchronize()
-        step_ms = allreduce_max(evs[0].elapsed_time(evs[6]), ws)
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)]
+        one_step(g, sp, bf, ins[Wm + k], dels[Wm + k], evs, stream, fused=True)
+        evs[-1].synchronize()
+        step_ms = allreduce_max(evs[0].elapsed_time(evs[-1]), ws)
         total_ms += step_ms
-        for j, n in enumerate(NAMES):
+        for j, n in enumerate(names):
             per_call[n].append(allreduce_max(evs[j].elapsed_time(evs[j + 1]), ws))
     clk = clocks.stop()
     mean = {n: float(np.mean(v)) for n, v in per_call.items()}
@@ -839,8 +841,7 @@ def run_dist(args, ws, rank, local):
                    "parallelism": f"vertex-partitioned over {ws} GPUs (owner = v mod {ws}), NCCL all-to-all per round",
                    "l2": "flushed before every timed step; store > L2"},
         "update_edges_per_s": 2 * args.batch / ((mean["insert"] + mean["delete"]) / 1e3),
-        "sssp_ms_per_batch": {"incremental": mean["sssp_inc"], "decremental": mean["sssp_dec"]},
-        "bfs_ms_per_batch": {"incremental": mean["bfs_inc"], "decremental": mean["bfs_dec"]},
+        "sssp_bfs_fused_ms_per_batch": {"incremental": mean["trees_inc"], "decremental": mean["trees_dec"]},
         "per_call_ms": mean, "build_s": build_s, "roofline": None, "cpu_baseline": None,
         "e2e": None, "gpu_launches": None, "clocks": clk, "generate_s": gen_s,
         "note": "host-driven rounds (one NCCL all-to-all + all-reduce per frontier round); timings are max over ranks",

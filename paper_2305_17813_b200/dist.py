@@ -196,6 +196,94 @@ class DistGraph:
         o = np.lexsort((d, s))
         return s[o], d[o], w[o]
 
+    # ------------------------------------------------------------------ fused tree updates
+    def trees_incremental(self, trees, src, dst, w=None):
+        """Incremental update of several trees (e.g. SSSP + BFS) with the batch just inserted, in
+        lock step: the batch is routed once and every round moves all trees' messages with ONE
+        count exchange and ONE message all-to-all (rounds = the slowest tree's, not the sum)."""
+        cols, _, _ = self.route(src, dst, w)
+        n = cols[0].numel()
+        res = [t._phase(_lib.D_INC_SEED, cols[0] if n else None, cols[1] if n else None,
+                        (cols[2] if (n and not t.unit and w is not None) else None), n) for t in trees]
+        self._fused_loop(trees, _lib.D_RELAX, _lib.D_APPLY_RELAX, res)
+
+    def trees_decremental(self, trees, src, dst):
+        """Decremental update of several trees in lock step (see trees_incremental)."""
+        cols, _, _ = self.route(src, dst, key_is_b=True)
+        n = cols[0].numel()
+        res = [t._phase(_lib.D_DEC_INVALIDATE, cols[0] if n else None, cols[1] if n else None, None, n)
+               for t in trees]
+        res = self._fused_loop(trees, _lib.D_PROPAGATE, _lib.D_APPLY_PROPAGATE, res)
+        glists = []
+        for t, r in zip(trees, res):
+            k = int(r.invalid_n)
+            mine = torch.empty(max(k, 1), dtype=torch.int32, device=self.device)
+            if k:
+                check(_lib.lib().meerkat_memcpy(self.g._h, ctypes.c_void_p(mine.data_ptr()),
+                                                ctypes.c_void_p(r.invalid), k * 4), "meerkat_memcpy")
+            glists.append(torch.cat(self.tp.allgather_var(mine[:k])).contiguous())
+        res = [t._phase(_lib.D_DEC_SCAN, gl if gl.numel() else None, n=gl.numel()) for t, gl in zip(trees, glists)]
+        self._fused_loop(trees, _lib.D_RELAX, _lib.D_APPLY_RELAX, res)
+        for t, gl in zip(trees, glists):
+            t._phase(_lib.D_FINISH, gl if gl.numel() else None, n=gl.numel())
+            t.invalidated_total = gl.numel()
+
+    def _fused_loop(self, trees, expand_ph, apply_ph, res):
+        """Rounds of several trees until no rank has frontier or messages left for any of them."""
+        res = list(res)
+        active = [True] * len(trees)
+        while True:
+            recvs, act = self._exchange_many(trees, res, active)
+            if not any(act):
+                return res
+            for i, t in enumerate(trees):
+                if not act[i]:
+                    active[i] = False
+                    continue
+                n = recvs[i].numel() // 2
+                if n:
+                    t._phase(apply_ph, recvs[i], n=n)
+                t.rounds += 1
+            for i, t in enumerate(trees):
+                if active[i]:
+                    res[i] = t._phase(expand_ph)
+
+    def _exchange_many(self, trees, res, active):
+        """One fixed-size all-to-all of <count, local frontier, messages sent> per (peer, tree) and,
+        if any message moves, ONE all-to-all carrying every tree's messages (per peer: tree 0's,
+        then tree 1's, ...)."""
+        ws, k, tp = self.ws, len(trees), self.tp
+        counts = [[int(res[i].msg_counts[p]) if active[i] else 0 for p in range(ws)] for i in range(k)]
+        sent = [sum(c) for c in counts]
+        meta = torch.tensor([[[counts[i][p], int(res[i].frontier) if active[i] else 0, sent[i]] for i in range(k)]
+                             for p in range(ws)], dtype=torch.int64, device=tp._dev()).view(-1)
+        rmeta = tp.alltoallv_known(meta, [1] * ws, [1] * ws, elem=3 * k).view(ws, k, 3).cpu()
+        act = [active[i] and int(rmeta[:, i, 1].sum()) + int(rmeta[:, i, 2].sum()) > 0 for i in range(k)]
+        if not any(act):
+            return None, act
+        bufs = []
+        for i in range(k):
+            b = torch.empty(max(sent[i], 1) * 2, dtype=torch.int64, device=self.device)
+            if sent[i]:   # stream-ordered device copy out of the library's message buffer
+                check(_lib.lib().meerkat_memcpy(self.g._h, ctypes.c_void_p(b.data_ptr()),
+                                                ctypes.c_void_p(res[i].msgs), sent[i] * 16), "meerkat_memcpy")
+            bufs.append(b)
+        offs = [np.concatenate([[0], np.cumsum(counts[i])]) for i in range(k)]
+        parts = [bufs[i][2 * offs[i][p]: 2 * offs[i][p + 1]] for p in range(ws) for i in range(k)]
+        send = torch.cat(parts) if parts else torch.empty(0, dtype=torch.int64, device=self.device)
+        scounts = [sum(counts[i][p] for i in range(k)) for p in range(ws)]
+        rc = rmeta[:, :, 0].tolist()   # rc[p][i]: pairs peer p sends this rank for tree i
+        rcounts = [sum(rc[p]) for p in range(ws)]
+        recv = tp.alltoallv_known(send, scounts, rcounts, elem=2)
+        per = [[] for _ in range(k)]
+        o = 0
+        for p in range(ws):
+            for i in range(k):
+                per[i].append(recv[2 * o: 2 * (o + rc[p][i])])
+                o += rc[p][i]
+        recvs = [torch.cat(x) if x else torch.empty(0, dtype=torch.int64, device=self.device) for x in per]
+        return recvs, act
+
     def sssp(self, source: int) -> "DistTree":
         return DistTree(self, source, unit=False)
 

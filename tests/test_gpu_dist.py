@@ -57,14 +57,20 @@ def _worker(rank, ws, port, backend, scale, q):
         for i, (s, d, w) in enumerate(W.inserts):
             n = g.insert(sl(s), sl(d), sl(w))
             assert n == o.insert(s, d, w)[1]
-            t.incremental(sl(s), sl(d), sl(w))
-            b.incremental(sl(s), sl(d))
+            if i % 2 == 0:   # fused lock-step update of both trees (DistGraph.trees_incremental)
+                g.trees_incremental([t, b], sl(s), sl(d), sl(w))
+            else:
+                t.incremental(sl(s), sl(d), sl(w))
+                b.incremental(sl(s), sl(d))
             check(f"inc{i}")
         for i, (s, d, _w) in enumerate(W.deletes):
             n = g.delete(sl(s), sl(d))
             assert n == o.delete(s, d)[1]
-            t.decremental(sl(s), sl(d))
-            b.decremental(sl(s), sl(d))
+            if i % 2 == 0:
+                g.trees_decremental([t, b], sl(s), sl(d))
+            else:
+                t.decremental(sl(s), sl(d))
+                b.decremental(sl(s), sl(d))
             check(f"dec{i}")
         # queries in the caller's order, across partitions
         es, ed, ew = o.edges()

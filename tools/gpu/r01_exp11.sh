@@ -1,0 +1,5 @@
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build25.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_dist.py -x -q > gpurun_out/pytest25.log 2>&1; echo t=$?
+tail -15 gpurun_out/pytest25.log
+timeout 900 python bench.py --partitioned --steps 3 --warmup 3 --json-out gpurun_out/bench_part25.json > gpurun_out/bench_part25.log 2>&1; echo part=$?
+python -c "import json;d=json.load(open('gpurun_out/bench_part25.json'));print(d['value'],d['ms_per_step'],d['per_call_ms'])"
