@@ -406,15 +406,18 @@ def roofline_of(res, peak, peak_src, traffic_file):
                 "traffic": None}
     ab = float(np.mean([s["alg_bytes"] for s in res["tstats"][dom]]))
     ach = ab / (mean[dom] * 1e-3) / 1e9
-    traffic = None
+    traffic, l2hit = None, None
     try:
-        traffic = json.load(open(traffic_file)).get(f"{res['frontier']}/{dom}")
+        tj = json.load(open(traffic_file))
+        traffic = tj.get(f"{res['frontier']}/{dom}")
+        l2hit = tj.get("l2_hit_rate", {}).get(f"{res['frontier']}/{dom}")
     except Exception:
         pass
     return {"bound": "hbm", "kernel": f"k_tree_dec ({dom}, {res['frontier']} frontier{', fused SSSP+BFS' if res['fused'] else ''})",
             "achieved": ach,
             "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": traffic, "alg_bytes_per_launch": ab,
-            "peak_source": peak_src}
+            "traffic_frac": (traffic / (mean[dom] * 1e-3) / 1e9 / peak) if traffic else None,
+            "l2_hit_rate_pct": l2hit, "peak_source": peak_src}
 
 
 def tree_detail(res):

@@ -23,7 +23,11 @@ __device__ __forceinline__ void block_add(unsigned long long* d0, unsigned long 
   v = __reduce_add_sync(0xFFFFFFFFu, v);
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(&acc, (unsigned long long)v);
   __syncthreads();
-  if (threadIdx.x == 0 && acc) { atomicAdd(d0, acc); atomicAdd(d1, acc); }
+  if (threadIdx.x == 0) {
+    const unsigned long long a = acc;
+    if (a) { atomicAdd(d0, a); atomicAdd(d1, a); }
+  }
+  __syncthreads();   // acc is reused by the next call (racecheck: no read may trail its reset)
 }
 
 __device__ __forceinline__ void block_or_err(unsigned int* dst, uint32_t e) {
