@@ -60,6 +60,9 @@ def parse():
                    help="decremental valid->invalid frontier: stream every slab (paper, P:156-164) or "
                         "read the in-edges of V_invalid from an in-edge mirror store")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--l2-flush", action=argparse.BooleanOptionalAction, default=True,
+                   help="write a 256 MiB buffer between timed steps (default); --no-l2-flush relies on the "
+                        "inputs (the 12.7 GB store) being larger than L2 instead")
     p.add_argument("--wcc", action=argparse.BooleanOptionalAction, default=True,
                    help="also time static and incremental WCC on the workload graph (SURVEY §8(f) NEXT-3)")
     p.add_argument("--tc", action=argparse.BooleanOptionalAction, default=True,
@@ -209,7 +212,8 @@ def workload_config(args, V, n_base, source, ws=1):
             "decremental_frontier": args.frontier,
             "tree_updates": "fused SSSP+BFS (meerkat_trees_*)" if args.fused else "per tree",
             "parallelism": "single GPU" if ws == 1 else f"{ws} independent replicas",
-            "l2": "flushed between timed steps (256 MiB write, outside the intervals); store > L2"}
+            "l2": ("flushed between timed steps (256 MiB write, outside the intervals); store > L2" if args.l2_flush
+                   else "not flushed: inputs larger than L2 (store > L2), batches back to back")}
 
 
 def cpu_baseline(args, steps):
@@ -644,7 +648,7 @@ def run_ours(args, ws, rank, local):
     V = W.vertex_n
     stream = torch.cuda.current_stream(dev)
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.uint32).view(np.int32)).to(dev)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush = torch.empty((256 << 20) if args.l2_flush else 1, dtype=torch.uint8, device=dev)
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
