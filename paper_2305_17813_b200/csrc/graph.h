@@ -25,6 +25,7 @@ struct TreeCtrl {
   unsigned long long visited;       // live edges visited by expansion (one node[x] probe each)
   unsigned long long batch_edges;   // batch edges examined by the prologue
   unsigned long long pull_n;        // (invalid vertex, in-bucket) items of the reverse-store frontier
+  unsigned long long tail_r;        // round counter after block 0's tail rounds (tree.cu run_rounds)
   unsigned long long nts;           // device timeline: %globaltimer at kernel start and after every grid barrier
   unsigned long long tstamp[48];
 };

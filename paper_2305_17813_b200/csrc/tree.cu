@@ -55,7 +55,8 @@ __device__ __forceinline__ bool fetch_item(const uint64_t* fr, uint64_t n, uint6
 // of an item and d(v) are loaded together (independent requests).
 // V32: the paper's VANILLA variant: node[] holds 32-bit distances only (no parent),
 // relaxed by 32-bit atomicMin (static SSSP / BFS; RELAX only).
-template <bool MAP, int VISIT, bool V32 = false>
+// BLOCK: only the calling block's groups share the items (the tail rounds of run_rounds).
+template <bool MAP, int VISIT, bool V32 = false, bool BLOCK = false>
 __device__ __forceinline__ void expand(const TreeArgs& A, const TreeDev& T, int k, const uint64_t* fr, uint64_t n,
                                        uint64_t* fnext, unsigned long long* sznext, uint32_t epoch_next,
                                        Counters& c) {
@@ -64,9 +65,9 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const TreeDev& T, int 
   const GraphDev& G = A.G;
   const GraphDev& S = VISIT == PULL ? A.R : A.G;   // store whose slab lists are walked
   const int lane = lane_id(), l8 = lane & 7;
-  const uint64_t ng = ((uint64_t)gridDim.x * blockDim.x) / GROUP;
+  const uint64_t ng = BLOCK ? blockDim.x / GROUP : ((uint64_t)gridDim.x * blockDim.x) / GROUP;
   const bool probe = n > PROBE_MIN_ITEMS;
-  uint64_t it = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / GROUP;
+  uint64_t it = BLOCK ? threadIdx.x / GROUP : ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / GROUP;
   uint32_t v = 0, slab = 0, du = 0;
   bool active = fetch_item(fr, n, it, v, slab, l8, c);
   bool fresh = active;
@@ -243,6 +244,42 @@ __device__ __forceinline__ uint32_t run_rounds(const TreeArgs& A, const uint32_t
       any |= n[k] != 0;
     }
     if (!any) break;
+    if (n[0] + n[1] <= TAIL_ITEMS) {
+      // Tail: a frontier this small is one chain per item for block 0's groups alone, so block 0
+      // runs the rounds with block barriers (~0.1 us) instead of grid barriers (~2 us) while the
+      // frontier stays small; the other blocks wait once, then every block resumes the loop.
+      if (blockIdx.x == 0) {
+        for (;;) {
+          if (threadIdx.x == 0)
+            for (uint32_t k = 0; k < A.ntrees; k++) A.T[k].ctrl->size[(r + 2) % 3] = 0;
+#pragma unroll
+          for (int k = 0; k < MAX_TREES; k++) {
+            if (!n[k]) continue;
+            const TreeDev& T = A.T[k];
+            expand<MAP, VISIT, V32, true>(A, T, k, T.fr[r & 1], n[k], T.fr[(r + 1) & 1],
+                                          &T.ctrl->size[(r + 1) % 3], epoch[k] + r + 1, c);
+          }
+          __syncthreads();   // block-wide visibility of this round's frontier and node updates
+          timeline(A.T[0].ctrl);
+          r++;
+          if (threadIdx.x < MAX_TREES)
+            s_n[threadIdx.x] = threadIdx.x < A.ntrees ? __ldcg(&A.T[threadIdx.x].ctrl->size[r % 3]) : 0ull;
+          __syncthreads();
+          any = false;
+#pragma unroll
+          for (int k = 0; k < MAX_TREES; k++) { n[k] = s_n[k]; any |= n[k] != 0; }
+          __syncthreads();   // s_n is rewritten by the next iteration / the resumed loop
+          if (!any || n[0] + n[1] > TAIL_ITEMS) break;
+        }
+        if (threadIdx.x == 0) A.T[0].ctrl->tail_r = r;
+      }
+      grid.sync();
+      if (threadIdx.x == 0) s_n[0] = __ldcg(&A.T[0].ctrl->tail_r);
+      __syncthreads();
+      r = (uint32_t)s_n[0];
+      __syncthreads();
+      continue;
+    }
     if (blockIdx.x == 0 && threadIdx.x == 0)
       for (uint32_t k = 0; k < A.ntrees; k++) A.T[k].ctrl->size[(r + 2) % 3] = 0;
 #pragma unroll
