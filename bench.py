@@ -513,6 +513,12 @@ def measure_pagerank(g, W, T, stream, flush, peak, peak_src):
     dec_ms, dec = timed(p.update)
     p.close()
     ach = st["alg_bytes"] / (st_ms * 1e-3) / 1e9
+    traffic = l2hit = None
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        traffic, l2hit = tj.get("pagerank/static"), tj.get("l2_hit_rate", {}).get("pagerank/static")
+    except Exception:
+        pass
     return {"damping": 0.85, "error_margin": 1e-5, "dtype": "f64",
             "static_ms": st_ms, "static_iterations": st["iterations"],
             "incremental_ms": inc_ms, "incremental_iterations": inc["iterations"],
@@ -522,6 +528,8 @@ def measure_pagerank(g, W, T, stream, flush, peak, peak_src):
                               "ms": st_ms / max(1, st["iterations"])},
             "roofline": {"bound": "hbm", "kernel": "k_pagerank (static run)", "achieved": ach, "peak": peak,
                          "unit": "GB/s", "frac": ach / peak, "alg_bytes_per_launch": st["alg_bytes"],
+                         "traffic": traffic, "l2_hit_rate_pct": l2hit,
+                         "traffic_frac": (traffic / (st_ms * 1e-3) / 1e9 / peak) if traffic else None,
                          "peak_source": peak_src}}
 
 
