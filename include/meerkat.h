@@ -191,6 +191,10 @@ meerkat_status meerkat_trees_decremental(meerkat_graph* g, meerkat_tree* const* 
                                          const uint32_t* src, const uint32_t* dst, uint64_t n);
 /* Static re-run on the current graph (the s_b^n baseline). */
 meerkat_status meerkat_tree_recompute(meerkat_graph* g, meerkat_tree* t);
+/* The same with the paper's iteration scheme chosen: 2 = <vertex, bucket> work items
+ * (IterationScheme2, what every call here uses), 1 = one work item per vertex whose buckets one
+ * group walks in turn (IterationScheme1, SlabIterator).  Same result; for the comparison. */
+meerkat_status meerkat_tree_recompute_scheme(meerkat_graph* g, meerkat_tree* t, uint32_t iteration_scheme);
 /* node[v] = dist << 32 | parent for every v, UINT64_MAX when unreached (C3). */
 meerkat_status meerkat_tree_nodes(meerkat_tree* t, uint64_t* out);
 /* The vertices invalidated by the last decremental call (unordered). */

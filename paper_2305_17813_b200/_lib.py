@@ -38,7 +38,7 @@ EXPORTS = [
     "meerkat_sssp_vanilla_create", "meerkat_bfs_vanilla_create", "meerkat_tree_distances",
     "meerkat_tc_count", "meerkat_tc_static", "meerkat_tc_incremental", "meerkat_tc_decremental",
     "meerkat_wcc_create", "meerkat_wcc_recompute", "meerkat_wcc_incremental", "meerkat_wcc_labels",
-    "meerkat_wcc_components", "meerkat_wcc_destroy",
+    "meerkat_wcc_components", "meerkat_wcc_destroy", "meerkat_tree_recompute_scheme",
 ]
 
 
@@ -155,6 +155,7 @@ def lib():
         "meerkat_wcc_labels": (ctypes.c_int, [vp, vp]),
         "meerkat_wcc_components": (ctypes.c_int, [vp, pu64]),
         "meerkat_wcc_destroy": (ctypes.c_int, [vp]),
+        "meerkat_tree_recompute_scheme": (ctypes.c_int, [vp, vp, u32]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -516,6 +516,18 @@ meerkat_status meerkat_bfs_decremental(meerkat_graph* g, meerkat_tree* t, const 
   return tree_update(g, t, true, 2, src, dst, nullptr, n);
 }
 
+meerkat_status meerkat_tree_recompute_scheme(meerkat_graph* g, meerkat_tree* t, uint32_t iteration_scheme) {
+  if (!g || !t || t->g != g || t->dist || (iteration_scheme != 1 && iteration_scheme != 2))
+    return MEERKAT_E_INVALID_ARG;
+  DeviceGuard dg(g->device);
+  t->dev.scheme1 = iteration_scheme == 1 ? 1u : 0u;
+  cudaError_t e = launch_tree(g, &t, 1, MODE_STATIC, nullptr, nullptr, nullptr, 0);
+  t->dev.scheme1 = 0;   // dynamic updates always use <vertex, bucket> items
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  t->version = g->version;
+  return MEERKAT_OK;
+}
+
 meerkat_status meerkat_tree_recompute(meerkat_graph* g, meerkat_tree* t) {
   if (!g || !t || t->g != g || t->dist) return MEERKAT_E_INVALID_ARG;
   DeviceGuard dg(g->device);

@@ -52,6 +52,8 @@ struct TreeDev {
   uint64_t fr_cap;       // items per frontier buffer (= number of slab lists)
   uint32_t source;
   uint32_t unit;         // 1: BFS (every w = 1)
+  uint32_t scheme1;      // 1: IterationScheme1 items (one per vertex, its buckets walked in turn;
+                         //    static recompute only); 0: <vertex, bucket> items
 };
 
 }  // namespace mk

@@ -69,9 +69,16 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const TreeDev& T, int 
   const bool probe = n > PROBE_MIN_ITEMS;
   uint64_t it = BLOCK ? threadIdx.x / GROUP : ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / GROUP;
   uint32_t v = 0, slab = 0, du = 0;
+  uint32_t b = 0, nb = 1, head0 = 0;   // IterationScheme1: bucket b of nb, first bucket head0
   bool active = fetch_item(fr, n, it, v, slab, l8, c);
   bool fresh = active;
   while (__any_sync(FULL, active)) {
+    if (T.scheme1) {   // (uniform) one item per vertex: walk all its buckets in turn
+      uint32_t cntb = 1;
+      if (active && fresh && l8 == 0) cntb = __ldcg(&G.vmeta[v].y);
+      const uint32_t nbv = __shfl_sync(FULL, cntb, lane & 24);
+      if (active && fresh) { nb = nbv; b = 0; head0 = slab; }
+    }
     uint4 d = make_uint4(EMPTY_KEY, EMPTY_KEY, EMPTY_KEY, INVALID_SLAB);
     uint64_t nv = 0;
     if (active) {
@@ -216,6 +223,7 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const TreeDev& T, int 
     const uint32_t nxt = __shfl_sync(FULL, d.w, (lane & 24) + GROUP - 1);
     if (active) {
       if (nxt != INVALID_SLAB && !dead) slab = nxt;
+      else if (T.scheme1 && !dead && b + 1 < nb) { b++; slab = head0 + b; }
       else { it += ng; active = fetch_item(fr, n, it, v, slab, l8, c); fresh = active; }
     }
   }

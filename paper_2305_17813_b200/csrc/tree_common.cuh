@@ -72,6 +72,7 @@ __device__ __forceinline__ void warp_enqueue(const GraphDev& G, const TreeDev& T
     const uint2 m = __ldcg(G.vmeta + x);
     head = m.x;
     cnt = m.x == INVALID_SLAB ? 0u : m.y;   // a vertex without a head slab has no out-edges
+    if (T.scheme1 && cnt) cnt = 1;           // IterationScheme1: one item per vertex
   }
   uint32_t incl = cnt;
 #pragma unroll
@@ -113,6 +114,7 @@ __device__ __forceinline__ void warp_enqueue_multi(const TreeDev& T, uint64_t* f
 #pragma unroll
   for (int k = 0; k < NK; k++) {
     cnt[k] = (has[k] && m[k].x != INVALID_SLAB) ? m[k].y : 0u;   // no head slab: no out-edges
+    if (T.scheme1 && cnt[k]) cnt[k] = 1;                          // IterationScheme1: one item per vertex
     mine += cnt[k];
   }
   if (!__any_sync(FULL, mine != 0)) return;

@@ -271,8 +271,14 @@ class Tree:
         fn = L.meerkat_bfs_decremental if self.unit else L.meerkat_sssp_decremental
         check(fn(self.graph._h, self._h, sp, dp, n), fn.__name__)
 
-    def recompute(self):
-        check(_lib.lib().meerkat_tree_recompute(self.graph._h, self._h), "meerkat_tree_recompute")
+    def recompute(self, iteration_scheme: int = 2):
+        """Static re-run; iteration_scheme 1 = one work item per vertex (the paper's IterationScheme1),
+        2 = <vertex, bucket> items (default, IterationScheme2)."""
+        if iteration_scheme == 2:
+            check(_lib.lib().meerkat_tree_recompute(self.graph._h, self._h), "meerkat_tree_recompute")
+        else:
+            check(_lib.lib().meerkat_tree_recompute_scheme(self.graph._h, self._h, int(iteration_scheme)),
+                  "meerkat_tree_recompute_scheme")
 
     def nodes(self, out=None):
         """Packed nodes, uint64 numpy array (or into a given int64 CUDA tensor)."""

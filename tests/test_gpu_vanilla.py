@@ -83,3 +83,25 @@ def test_unweighted_store_vanilla_bfs():
     o = oracle.OracleGraph(1024, weighted=False)
     o.insert(s, d)
     assert np.array_equal(g.bfs_vanilla(0).distances(), dist_of(o.bfs(0)[1]))
+
+
+@pytest.mark.parametrize("hashing", [True, False])
+def test_iteration_scheme1_static_equals_scheme2(hashing):
+    """The paper's IterationScheme1 (one work item per vertex, its buckets walked in turn by one
+    group) gives the same static trees / distances as the <vertex, bucket> items."""
+    W = synth.rmat_dynamic(15, 16, batch=1000, n_ins=1, n_del=0)
+    s, d, w = W.base
+    V = W.vertex_n
+    g = G(V, hashing=hashing, degree_hints=synth.degrees(s, V))
+    g.insert(cuda(s), cuda(d), cuda(w))
+    o = oracle.OracleGraph(V)
+    o.insert(s, d, w)
+    for mk, ref in ((g.sssp, o.sssp(W.source)[1]), (g.bfs, o.bfs(W.source)[1])):
+        t = mk(W.source)
+        t.recompute(iteration_scheme=1)
+        assert np.array_equal(t.nodes(), ref)
+        t.recompute(iteration_scheme=2)
+        assert np.array_equal(t.nodes(), ref)
+    vt = g.sssp_vanilla(W.source)
+    vt.recompute(iteration_scheme=1)
+    assert np.array_equal(vt.distances(), dist_of(o.sssp(W.source)[1]))
