@@ -87,6 +87,8 @@ typedef struct {
   uint32_t world_size;          /* vertex partition (multi-GPU): 0 or 1 = whole graph here;   */
   uint32_t rank;                /* otherwise this graph holds the out-edges of every u with u % world_size  */
                                 /* == rank; degree hints are then indexed by u / world_size                */
+  uint32_t update_tracking;     /* 1: keep per-slab-list update tracking (is_updated / first updated slab
+                                   and lane) for meerkat_wcc_incremental_tracked */
 } meerkat_config;
 
 typedef struct {
@@ -328,6 +330,11 @@ meerkat_status meerkat_wcc_recompute(meerkat_graph* g, meerkat_wcc* c);
  * Stream-ordered. */
 meerkat_status meerkat_wcc_incremental(meerkat_graph* g, meerkat_wcc* c, const uint32_t* src, const uint32_t* dst,
                                        uint64_t n);
+/* The paper's UpdateIterator path: union the edges of every slab list written since the
+ * last call, from its first updated cell on (the update tracking of cfg.update_tracking), then full
+ * compression, then reset the tracking (Graph.UpdateSlabPointers).  Same labels as
+ * meerkat_wcc_incremental with the inserted batches; MEERKAT_E_STATE without update tracking. */
+meerkat_status meerkat_wcc_incremental_tracked(meerkat_graph* g, meerkat_wcc* c);
 /* label[v] (host or device [vertex_n]). */
 meerkat_status meerkat_wcc_labels(meerkat_wcc* c, uint32_t* out);
 meerkat_status meerkat_wcc_components(meerkat_wcc* c, uint64_t* n_components);

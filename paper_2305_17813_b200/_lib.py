@@ -39,6 +39,7 @@ EXPORTS = [
     "meerkat_tc_count", "meerkat_tc_static", "meerkat_tc_incremental", "meerkat_tc_decremental",
     "meerkat_wcc_create", "meerkat_wcc_recompute", "meerkat_wcc_incremental", "meerkat_wcc_labels",
     "meerkat_wcc_components", "meerkat_wcc_destroy", "meerkat_tree_recompute_scheme",
+    "meerkat_wcc_incremental_tracked",
 ]
 
 
@@ -54,7 +55,7 @@ class Config(ctypes.Structure):
         ("load_factor", ctypes.c_float), ("degree_hints", ctypes.c_void_p), ("pool_slabs", ctypes.c_uint64),
         ("hash_seed", ctypes.c_uint64), ("device", ctypes.c_int), ("stream", ctypes.c_void_p),
         ("reverse", ctypes.c_uint32), ("in_degree_hints", ctypes.c_void_p),
-        ("world_size", ctypes.c_uint32), ("rank", ctypes.c_uint32),
+        ("world_size", ctypes.c_uint32), ("rank", ctypes.c_uint32), ("update_tracking", ctypes.c_uint32),
     ]
 
 
@@ -156,6 +157,7 @@ def lib():
         "meerkat_wcc_components": (ctypes.c_int, [vp, pu64]),
         "meerkat_wcc_destroy": (ctypes.c_int, [vp]),
         "meerkat_tree_recompute_scheme": (ctypes.c_int, [vp, vp, u32]),
+        "meerkat_wcc_incremental_tracked": (ctypes.c_int, [vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

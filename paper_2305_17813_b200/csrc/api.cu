@@ -169,6 +169,13 @@ meerkat_status meerkat_create(const meerkat_config* cfg, meerkat_graph** out) {
     e = stage_in(g, 1, cfg->in_degree_hints, (size_t)g->Vl * 4, &hints);
     if (e == cudaSuccess) e = launch_build(g, g->in, static_cast<const uint32_t*>(hints), cfg->pool_slabs);
   }
+  if (e == cudaSuccess && cfg->update_tracking) {   // UpdateIterator metadata
+    Store& o = g->out;
+    e = cudaMalloc(&o.dev.upd, (size_t)(o.H + o.P) * 8);
+    if (e == cudaSuccess) e = cudaMemsetAsync(o.dev.upd, 0xFF, (size_t)(o.H + o.P) * 8, g->stream);
+    if (e == cudaSuccess) e = cudaMalloc(&o.dev.updq, (size_t)std::max<uint64_t>(o.buckets, 1) * 4);
+    o.bytes += (size_t)(o.H + o.P) * 8 + (size_t)o.buckets * 4;
+  }
   if (e == cudaSuccess) e = tree_occupancy(g);
   if (const char* s = std::getenv("MEERKAT_LATENCY_BLOCKS_PER_SM")) g->latency_bps = std::atoi(s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
@@ -893,6 +900,16 @@ meerkat_status meerkat_wcc_incremental(meerkat_graph* g, meerkat_wcc* c, const u
   cudaError_t e = stage_in(g, 0, src, n * 4, &s);
   if (e == cudaSuccess) e = stage_in(g, 1, dst, n * 4, &d);
   if (e == cudaSuccess) e = launch_wcc_batch(g, c->parent, (const uint32_t*)s, (const uint32_t*)d, n);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  c->version = g->version;
+  return MEERKAT_OK;
+}
+
+meerkat_status meerkat_wcc_incremental_tracked(meerkat_graph* g, meerkat_wcc* c) {
+  if (!g || !c || c->g != g) return MEERKAT_E_INVALID_ARG;
+  if (!g->out.dev.upd) return MEERKAT_E_STATE;   // the graph keeps no update tracking
+  DeviceGuard dg(g->device);
+  const cudaError_t e = launch_wcc_tracked(g, c->parent);
   if (e != cudaSuccess) return MEERKAT_E_CUDA;
   c->version = g->version;
   return MEERKAT_OK;

@@ -144,6 +144,7 @@ namespace mk {
 cudaError_t launch_wcc_static(meerkat_graph* g, uint32_t* parent, unsigned long long* scratch);
 cudaError_t launch_wcc_batch(meerkat_graph* g, uint32_t* parent, const uint32_t* s, const uint32_t* d, uint64_t n);
 cudaError_t launch_wcc_roots(meerkat_graph* g, const uint32_t* parent, unsigned long long* out_dev);
+cudaError_t launch_wcc_tracked(meerkat_graph* g, uint32_t* parent);
 // tc.cu
 cudaError_t launch_tc_count(meerkat_graph* g1, meerkat_graph* g2, const uint32_t* src, const uint32_t* dst,
                             uint64_t n, unsigned long long* out_dev);

@@ -43,6 +43,7 @@ struct GraphCtrl {
   unsigned long long ins_total;   // cumulative: live edges = ins_total - del_total
   unsigned long long del_total;
   unsigned long long export_n;
+  unsigned long long upd_n;       // update tracking: slab lists queued in updq since the last reset
   unsigned int err;               // sticky ErrBits
   unsigned int pad;
 };
@@ -51,6 +52,9 @@ struct GraphDev {
   uint32_t* slabs;   // (H + P) slabs x 32 words: head arena [0, H) then pool [H, H + P)
   uint32_t* owner;   // source vertex of every slab (the paper's bucket_vertex[])
   uint2* vmeta;      // per vertex {first head slab | INVALID_SLAB, bucket_count}
+  unsigned long long* upd;   // update tracking (nullable): per slab list (indexed by its head slab) the
+                             // earliest cell written since the last reset, (slab << 5) | cell, or ~0
+  uint32_t* updq;            // the slab lists with upd != ~0 (UpdateIterator work list)
   uint32_t* deg;     // per vertex live keys (out-degree in the out store, in-degree in the mirror),
                      // maintained by insert / delete; PageRank's out[u]
   GraphCtrl* ctrl;

@@ -62,6 +62,7 @@ __device__ int group_link(const GraphDev& G, uint32_t u, uint64_t item, uint32_t
     const uint32_t s = group_alloc<MAP>(G, u, item, l8, gmask);   // fenced before publication
     if (l8 == 0) atomicExch(link, s);                              // s == INVALID_SLAB releases the lock
     __syncwarp(gmask);
+    next_out = s;   // the caller's key sits in cell 0 of this slab
     return s == INVALID_SLAB ? -1 : 1;
   }
   uint32_t spins = 0;
@@ -88,9 +89,11 @@ __device__ __forceinline__ uint32_t ld_head_cg(const GraphDev& G, uint32_t u) {
 // ------------------------------------------------------------------ insert (C9)
 
 // Returns 1 = inserted (key was absent), 0 = present (weight min-upserted), -1 = pool exhausted.
+// pos_list / pos (out, valid when 1 is returned): the slab list (its head slab) and the placement
+// (slab << 5) | cell of the new key, for update tracking.
 template <bool MAP>
 __device__ int group_insert(const GraphDev& G, uint32_t u, uint32_t v, uint32_t wt, int l8, uint32_t gmask,
-                            int gbase) {
+                            int gbase, uint32_t& pos_list, unsigned long long& pos) {
   using F = Frag<MAP>;
   constexpr int NK = F::NK;
   const uint64_t item = MAP ? (((uint64_t)wt << 32) | v) : (uint64_t)v;
@@ -105,10 +108,12 @@ __device__ int group_insert(const GraphDev& G, uint32_t u, uint32_t v, uint32_t 
     // vertex without a head slab yet (hint 0, reading C22b): publish one holding the key
     uint32_t nxt = INVALID_SLAB;
     const int r = group_link<MAP>(G, u, item, reinterpret_cast<uint32_t*>(&G.vmeta[u].x), nxt, l8, gmask);
+    if (r == 1) { pos_list = nxt; pos = (unsigned long long)nxt << 5; }
     if (r != 0) return r;
     head = nxt;
   }
   uint32_t cur = head + bucket_of(v, count, G.seed);
+  const uint32_t list0 = cur;
   uint32_t guard = 0, walk = 0;
   for (;;) {
     if (++guard == WATCHDOG) {
@@ -191,13 +196,14 @@ __device__ int group_insert(const GraphDev& G, uint32_t u, uint32_t v, uint32_t 
         }
       }
       ok = __shfl_sync(gmask, (int)ok, 0, GROUP);
-      if (ok) { result = 1; break; }
+      if (ok) { result = 1; pos_list = list0; pos = ((unsigned long long)cand_slab << 5) | (uint32_t)cand_cell; break; }
       cur = cand_slab;  // the cell changed under us: rescan from its slab
       continue;
     }
     // ---- list full: link a pool slab holding the key after the tail
     uint32_t nxt = INVALID_SLAB;
     const int r = group_link<MAP>(G, u, item, slab_ptr(G, tail) + (SLAB_WORDS - 1), nxt, l8, gmask);
+    if (r == 1) { pos_list = list0; pos = (unsigned long long)nxt << 5; }
     if (r != 0) { result = r; break; }
     cur = nxt == INVALID_SLAB ? tail : nxt;   // continue in the slab another group linked
   }
@@ -224,7 +230,8 @@ __device__ __forceinline__ void upd_item(const UpdArgs& A, uint64_t i, uint32_t&
   e = A.ns == 2 ? i >> 1 : i;
 }
 
-template <bool MAP>
+// TRACK: the out store keeps update tracking (compiled out of the default kernels).
+template <bool MAP, bool TRACK>
 __global__ void __launch_bounds__(UPD_BLOCK) k_insert(const __grid_constant__ UpdArgs A) {
   const int lane = lane_id(), l8 = lane & 7, gbase = lane & 24;
   const uint32_t gmask = 0xFFu << gbase;
@@ -241,9 +248,15 @@ __global__ void __launch_bounds__(UPD_BLOCK) k_insert(const __grid_constant__ Up
     if (MAP && (wt == 0 || wt >= W_LIMIT)) { err[st] |= ERR_WEIGHT; continue; }
     const uint32_t ul = local_row(G, u);
     if (ul == INVALID_SLAB) { err[st] |= ERR_PARTITION; continue; }
-    const int r = group_insert<MAP>(G, ul, v, wt, l8, gmask, gbase);
+    uint32_t plist = 0;
+    unsigned long long ppos = 0;
+    const int r = group_insert<MAP>(G, ul, v, wt, l8, gmask, gbase, plist, ppos);
     if (r < 0) err[st] |= ERR_CAPACITY;
-    else if (l8 == 0 && r) { added[st]++; atomicAdd(G.deg + ul, 1u); }
+    else if (l8 == 0 && r) {
+      added[st]++;
+      atomicAdd(G.deg + ul, 1u);
+      if (TRACK && G.upd) track_update(G, plist, ppos);
+    }
   }
   for (uint32_t k = 0; k < A.ns; k++) {
     block_or_err(&A.G[k].ctrl->err, err[k]);
@@ -409,7 +422,7 @@ __global__ void __launch_bounds__(UPD_BLOCK) k_query_t(GraphDev G, const uint32_
 // edge reading whole slabs (8 x LDG.128 of one 128-B line): no group collectives and one divergent
 // path per edge.  Used for large batches (thread_upd).
 
-template <bool MAP>
+template <bool MAP, bool TRACK>
 __global__ void __launch_bounds__(UPD_BLOCK) k_insert_t(const __grid_constant__ UpdArgs A) {
   uint32_t added[2] = {0, 0}, err[2] = {0, 0};
   const uint64_t total = A.n * A.ns;
@@ -423,9 +436,15 @@ __global__ void __launch_bounds__(UPD_BLOCK) k_insert_t(const __grid_constant__ 
     if (MAP && (wt == 0 || wt >= W_LIMIT)) { err[st] |= ERR_WEIGHT; continue; }
     const uint32_t ul = local_row(G, u);
     if (ul == INVALID_SLAB) { err[st] |= ERR_PARTITION; continue; }
-    const int r = thread_insert<MAP>(G, ul, v, wt);
+    uint32_t plist = 0;
+    unsigned long long ppos = 0;
+    const int r = thread_insert<MAP>(G, ul, v, wt, plist, ppos);
     if (r < 0) err[st] |= ERR_CAPACITY;
-    else if (r) { added[st]++; atomicAdd(G.deg + ul, 1u); }
+    else if (r) {
+      added[st]++;
+      atomicAdd(G.deg + ul, 1u);
+      if (TRACK && G.upd) track_update(G, plist, ppos);
+    }
   }
   for (uint32_t k = 0; k < A.ns; k++) {
     block_or_err(&A.G[k].ctrl->err, err[k]);
@@ -717,14 +736,24 @@ cudaError_t launch_insert(meerkat_graph* g, Store* st0, Store* st1, const uint32
   A.src = s; A.dst = d; A.w = w; A.n = n; A.ns = st1 ? 2u : 1u;
   if (thread_upd(n * A.ns)) {
     const unsigned gt = grid_threads(g, n * A.ns);
-    if (g->weighted) k_insert_t<true><<<gt, UPD_BLOCK, 0, g->stream>>>(A);
-    else k_insert_t<false><<<gt, UPD_BLOCK, 0, g->stream>>>(A);
+    if (A.G[0].upd) {
+      if (g->weighted) k_insert_t<true, true><<<gt, UPD_BLOCK, 0, g->stream>>>(A);
+      else k_insert_t<false, true><<<gt, UPD_BLOCK, 0, g->stream>>>(A);
+    } else {
+      if (g->weighted) k_insert_t<true, false><<<gt, UPD_BLOCK, 0, g->stream>>>(A);
+      else k_insert_t<false, false><<<gt, UPD_BLOCK, 0, g->stream>>>(A);
+    }
     g->launches++;
     return cudaGetLastError();
   }
   const unsigned gb = grid_for(g, n * A.ns, 0);
-  if (g->weighted) k_insert<true><<<gb, UPD_BLOCK, 0, g->stream>>>(A);
-  else k_insert<false><<<gb, UPD_BLOCK, 0, g->stream>>>(A);
+  if (A.G[0].upd) {
+    if (g->weighted) k_insert<true, true><<<gb, UPD_BLOCK, 0, g->stream>>>(A);
+    else k_insert<false, true><<<gb, UPD_BLOCK, 0, g->stream>>>(A);
+  } else {
+    if (g->weighted) k_insert<true, false><<<gb, UPD_BLOCK, 0, g->stream>>>(A);
+    else k_insert<false, false><<<gb, UPD_BLOCK, 0, g->stream>>>(A);
+  }
   g->launches++;
   return cudaGetLastError();
 }
@@ -800,6 +829,8 @@ void free_store(Store& st) {
   cudaFree(st.dev.owner);
   cudaFree(st.dev.vmeta);
   cudaFree(st.dev.deg);
+  cudaFree(st.dev.upd);
+  cudaFree(st.dev.updq);
   cudaFree(st.dev.ctrl);
   if (st.hctrl) cudaFreeHost(st.hctrl);
   st = Store{};

@@ -69,6 +69,7 @@ __device__ int thread_link(const GraphDev& G, uint32_t u, uint64_t item, uint32_
   if (old == INVALID_SLAB) {
     const uint32_t s = thread_alloc<MAP>(G, u, item);
     atomicExch(link, s);   // INVALID_SLAB releases the lock
+    next_out = s;   // the caller's key sits in cell 0 of this slab
     return s == INVALID_SLAB ? -1 : 1;
   }
   uint32_t spins = 0;
@@ -81,8 +82,17 @@ __device__ int thread_link(const GraphDev& G, uint32_t u, uint64_t item, uint32_
   return 0;
 }
 
+// UpdateIterator bookkeeping: remember the earliest cell written in the slab list
+// since the last reset; the first write to a list queues it.  Chain order is slab-index order
+// (pool slabs are handed out in increasing order), so the minimum position is the earliest.
+__device__ __forceinline__ void track_update(const GraphDev& G, uint32_t list, unsigned long long pos) {
+  const unsigned long long old = atomicMin(G.upd + list, pos);
+  if (old == ~0ull) G.updq[atomicAdd(&G.ctrl->upd_n, 1ull)] = list;
+}
+
 template <bool MAP>
-__device__ int thread_insert(const GraphDev& G, uint32_t u, uint32_t v, uint32_t wt) {
+__device__ int thread_insert(const GraphDev& G, uint32_t u, uint32_t v, uint32_t wt, uint32_t& pos_list,
+                             unsigned long long& pos) {
   using F = Frag<MAP>;
   constexpr int NK = F::NK;
   const uint64_t item = MAP ? (((uint64_t)wt << 32) | v) : (uint64_t)v;
@@ -91,10 +101,12 @@ __device__ int thread_insert(const GraphDev& G, uint32_t u, uint32_t v, uint32_t
   while (head == INVALID_SLAB || head == LINKING) {   // lazily headed vertex (C22b)
     uint32_t nxt = INVALID_SLAB;
     const int r = thread_link<MAP>(G, u, item, reinterpret_cast<uint32_t*>(&G.vmeta[u].x), nxt);
+    if (r == 1) { pos_list = nxt; pos = (unsigned long long)nxt << 5; }
     if (r != 0) return r;
     head = nxt;
   }
   uint32_t cur = head + bucket_of(v, m.y, G.seed);
+  const uint32_t list0 = cur;
   for (uint32_t guard = 0; guard < WATCHDOG; guard++) {
     // pass 1: up to the first slab holding an EMPTY cell; first writable cell remembered
     uint32_t s = cur, cand_slab = INVALID_SLAB, tail = INVALID_SLAB, found_slab = INVALID_SLAB;
@@ -140,13 +152,14 @@ __device__ int thread_insert(const GraphDev& G, uint32_t u, uint32_t v, uint32_t
         ok = atomicCAS(slab_ptr(G, cand_slab) + cand_cell, (unsigned int)cand_old, (unsigned int)item) ==
              (unsigned int)cand_old;
       }
-      if (ok) return 1;
+      if (ok) { pos_list = list0; pos = ((unsigned long long)cand_slab << 5) | (uint32_t)cand_cell; return 1; }
       cur = cand_slab;   // the cell changed: rescan from its slab
       continue;
     }
     if (tail == INVALID_SLAB) { atomicOr(&G.ctrl->err, (unsigned)ERR_STATE); return -1; }
     uint32_t nxt = INVALID_SLAB;   // full list: link a pool slab holding the key after the tail
     const int r = thread_link<MAP>(G, u, item, slab_ptr(G, tail) + (SLAB_WORDS - 1), nxt);
+    if (r == 1) { pos_list = list0; pos = (unsigned long long)nxt << 5; }
     if (r != 0) return r;
     cur = nxt == INVALID_SLAB ? tail : nxt;
   }

@@ -129,6 +129,38 @@ __global__ void k_wcc_batch(uint32_t* parent, uint32_t V, const uint32_t* __rest
   }
 }
 
+// UpdateIterator: one 8-lane group per queued slab list walks it from its first
+// updated cell (earlier cells and slabs hold only edges older than the tracking window) and unions
+// (owner, key) for every live key; then resets the list's tracking (UpdateSlabPointers).  With
+// TOMBSTONE reuse an old key can sit after the first updated cell: its union is a no-op.
+template <bool MAP>
+__global__ void __launch_bounds__(WCC_BLOCK) k_wcc_update_iter(GraphDev G, uint32_t* parent) {
+  using F = Frag<MAP>;
+  constexpr int NK = F::NK;
+  const int lane = threadIdx.x & 31, l8 = lane & 7;
+  const uint32_t gmask = 0xFFu << (lane & 24);
+  const uint64_t ng = ((uint64_t)gridDim.x * blockDim.x) / GROUP;
+  const uint64_t n = __ldcg(&G.ctrl->upd_n);
+  for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / GROUP; i < n; i += ng) {
+    const uint32_t list = __ldcg(G.updq + i);
+    const unsigned long long pos = __ldcg(G.upd + list);
+    const uint32_t u = __ldg(G.owner + list);
+    uint32_t s = (uint32_t)(pos >> 5);
+    int c0 = (int)(pos & 31);
+    for (uint32_t guard = 0; guard < (1u << 24) && s != INVALID_SLAB; guard++) {
+      const uint4 d = ld_slab_cg(slab_ptr(G, s), l8);
+#pragma unroll
+      for (int k = 0; k < NK; k++) {
+        const uint32_t x = F::key(d, k);
+        if (l8 * NK + k >= c0 && F::valid_cell(l8, k) && x < G.Vg) wcc_union(parent, u, x);
+      }
+      s = __shfl_sync(gmask, d.w, GROUP - 1, GROUP);
+      c0 = 0;
+    }
+    if (l8 == 0) G.upd[list] = ~0ull;   // UpdateSlabPointers
+  }
+}
+
 __global__ void k_wcc_count_roots(const uint32_t* parent, uint32_t V, unsigned long long* out) {
   uint32_t c = 0;
   for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < V; v += (uint64_t)gridDim.x * blockDim.x)
@@ -169,6 +201,19 @@ cudaError_t launch_wcc_batch(meerkat_graph* g, uint32_t* parent, const uint32_t*
     g->launches++;
   }
   k_wcc_compress<<<wcc_grid(g, g->V), WCC_BLOCK, 0, g->stream>>>(parent, g->V);   // Compress(Parents)
+  g->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wcc_tracked(meerkat_graph* g, uint32_t* parent) {
+  Store& st = g->out;
+  const unsigned gs = (unsigned)((uint64_t)g->sm_count * 8);
+  if (g->weighted) k_wcc_update_iter<true><<<gs, WCC_BLOCK, 0, g->stream>>>(st.dev, parent);
+  else k_wcc_update_iter<false><<<gs, WCC_BLOCK, 0, g->stream>>>(st.dev, parent);
+  g->launches++;
+  cudaError_t e = cudaMemsetAsync(&st.dev.ctrl->upd_n, 0, 8, g->stream);
+  if (e != cudaSuccess) return e;
+  k_wcc_compress<<<wcc_grid(g, g->V), WCC_BLOCK, 0, g->stream>>>(parent, g->V);
   g->launches++;
   return cudaGetLastError();
 }

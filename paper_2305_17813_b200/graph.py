@@ -51,14 +51,16 @@ class Graph:
 
     def __init__(self, vertex_n: int, weighted: bool = True, hashing: bool = True, load_factor: float = 0.7,
                  degree_hints=None, pool_slabs: int = 0, hash_seed: int = 0, device: int = 0, stream=None,
-                 reverse: bool = False, in_degree_hints=None, world_size: int = 1, rank: int = 0):
+                 reverse: bool = False, in_degree_hints=None, world_size: int = 1, rank: int = 0,
+                 update_tracking: bool = False):
         L = _lib.lib()
         hp, self._hints_keep, _ = _u32(degree_hints)
         ip, self._ihints_keep, _ = _u32(in_degree_hints)
         cfg = _lib.Config(vertex_n=vertex_n, weighted=int(weighted), hashing=int(hashing),
                           load_factor=float(load_factor), degree_hints=hp, pool_slabs=int(pool_slabs),
                           hash_seed=int(hash_seed), device=int(device), stream=_stream_ptr(stream),
-                          reverse=int(reverse), in_degree_hints=ip, world_size=int(world_size), rank=int(rank))
+                          reverse=int(reverse), in_degree_hints=ip, world_size=int(world_size), rank=int(rank),
+                          update_tracking=int(update_tracking))
         h = ctypes.c_void_p()
         check(L.meerkat_create(ctypes.byref(cfg), ctypes.byref(h)), "meerkat_create")
         self._h = h
@@ -386,6 +388,11 @@ class WCC:
         sp, ks, n = _u32(src)
         dp, kd, _ = _u32(dst)
         check(_lib.lib().meerkat_wcc_incremental(self.graph._h, self._h, sp, dp, n), "meerkat_wcc_incremental")
+
+    def incremental_tracked(self):
+        """The UpdateIterator path: union the edges written since the last call (needs a
+        graph created with update_tracking=True), compress, reset the tracking."""
+        check(_lib.lib().meerkat_wcc_incremental_tracked(self.graph._h, self._h), "meerkat_wcc_incremental_tracked")
 
     def recompute(self):
         check(_lib.lib().meerkat_wcc_recompute(self.graph._h, self._h), "meerkat_wcc_recompute")

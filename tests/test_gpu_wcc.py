@@ -77,3 +77,44 @@ def test_rmat(scale):
         o.insert(bs, bd, bw)
         c.incremental(cuda(bs), cuda(bd))
         assert np.array_equal(c.labels(), o.wcc()[0])
+
+
+@pytest.mark.parametrize("kernel", ["group", "thread"])
+@pytest.mark.parametrize("weighted,hashing,lf", [(False, True, 0.7), (True, True, 0.3), (False, False, 0.7)])
+def test_update_iterator_incremental(kernel, weighted, hashing, lf, monkeypatch):
+    """The paper's UpdateIterator path: with update tracking, unioning the edges of the
+    slab lists written since the last call (from their first updated cell on) gives the oracle's
+    labels; both update-kernel kinds record the placements; tracking resets after every call."""
+    monkeypatch.setenv("MEERKAT_THREAD_UPD", "1" if kernel == "thread" else "0")
+    rng = np.random.default_rng(31)
+    V = 20000
+    s, d = rng.integers(0, V, 12000).astype(np.uint32), rng.integers(0, V, 12000).astype(np.uint32)
+    hints = synth.degrees(s, V)
+    hints[: V // 4] = 0   # lazily headed lists too
+    g = G(V, weighted=weighted, hashing=hashing, load_factor=lf, degree_hints=hints, update_tracking=True)
+    one = lambda n: cuda(np.ones(n, np.uint32)) if weighted else None
+    g.insert(cuda(s), cuda(d), one(len(s)))
+    o = oracle.OracleGraph(V, weighted=False)
+    o.insert(s, d)
+    c = g.wcc()
+    c.incremental_tracked()   # consumes the tracking of the bulk insert (already reflected)
+    assert np.array_equal(c.labels(), o.wcc()[0])
+    for b in range(5):
+        n = 3000
+        bs, bd = rng.integers(0, V, n).astype(np.uint32), rng.integers(0, V, n).astype(np.uint32)
+        g.insert(cuda(bs), cuda(bd), one(n))
+        o.insert(bs, bd)
+        c.incremental_tracked()
+        lab, k = o.wcc()
+        assert np.array_equal(c.labels(), lab), b
+        assert c.components() == k
+    assert g.check()[0] == 0
+
+
+def test_tracking_required():
+    from paper_2305_17813_b200 import MeerkatError
+    g = G(100, weighted=False)
+    g.insert(np.array([1], np.uint32), np.array([2], np.uint32))
+    c = g.wcc()
+    with pytest.raises(MeerkatError):
+        c.incremental_tracked()
