@@ -252,6 +252,18 @@ meerkat_status meerkat_dtree_phase(meerkat_graph* g, meerkat_tree* t, meerkat_dp
 /* Copy `bytes` between host/device buffers on the graph's stream (lets a caller move phase messages
  * into its own communication buffers); synchronises only when either side is host memory. */
 meerkat_status meerkat_memcpy(meerkat_graph* g, void* dst, const void* src, uint64_t bytes);
+/* Fused exchange of k (<= 8) trees updated in lock step (one all-to-all per round for all of them).
+ * pack: from each tree's last emitting phase, writes meta (device int64 [world_size * k * 3]: per
+ * destination rank p, per tree i: pairs for p, the tree's local frontier, pairs it sent) and send
+ * (device, <x, payload> pairs as 2 x uint64: per p, tree 0's pairs for p, then tree 1's, ...), and
+ * send_counts[p] (host, pairs per destination); MEERKAT_E_CAPACITY if the pairs exceed
+ * capacity_pairs.  apply: recv holds, per source rank p, tree 0's recv_counts[p * k] pairs, then tree
+ * 1's recv_counts[p * k + 1], ...; runs each tree's apply phase (APPLY_RELAX / APPLY_PROPAGATE).
+ * Both are stream-ordered. */
+meerkat_status meerkat_dtrees_pack(meerkat_graph* g, meerkat_tree* const* trees, uint32_t k, int64_t* meta,
+                                   uint64_t* send, uint64_t capacity_pairs, uint64_t* send_counts);
+meerkat_status meerkat_dtrees_apply(meerkat_graph* g, meerkat_tree* const* trees, uint32_t k, meerkat_dphase phase,
+                                    const uint64_t* recv, const uint64_t* recv_counts);
 meerkat_status meerkat_route(meerkat_graph* g, int key_is_b, const uint32_t* a, const uint32_t* b,
                              const uint32_t* c, uint64_t n, uint32_t* out_a, uint32_t* out_b, uint32_t* out_c,
                              uint64_t* counts);

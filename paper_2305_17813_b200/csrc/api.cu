@@ -195,6 +195,7 @@ meerkat_status meerkat_destroy(meerkat_graph* g) {
   free_store(g->out);
   free_store(g->in);
   cudaFree(g->rscratch);
+  if (g->hmeta) cudaFreeHost(g->hmeta);
   if (g->hrscratch) cudaFreeHost(g->hrscratch);
   for (int i = 0; i < 4; i++) cudaFree(g->stage[i]);
   delete g;
@@ -660,6 +661,25 @@ meerkat_status meerkat_memcpy(meerkat_graph* g, void* dst, const void* src, uint
   cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, g->stream);
   if (e == cudaSuccess && (!is_device_ptr(dst) || !is_device_ptr(src))) e = cudaStreamSynchronize(g->stream);
   return from_cuda(e);
+}
+
+meerkat_status meerkat_dtrees_pack(meerkat_graph* g, meerkat_tree* const* trees, uint32_t k, int64_t* meta,
+                                   uint64_t* send, uint64_t capacity_pairs, uint64_t* send_counts) {
+  if (!g || !trees || !meta || !send_counts || k == 0 || k > 8) return MEERKAT_E_INVALID_ARG;
+  for (uint32_t i = 0; i < k; i++)
+    if (!trees[i] || trees[i]->g != g || !trees[i]->dist) return MEERKAT_E_INVALID_ARG;
+  DeviceGuard dg(g->device);
+  return dtrees_pack(g, trees, k, meta, send, capacity_pairs, send_counts);
+}
+
+meerkat_status meerkat_dtrees_apply(meerkat_graph* g, meerkat_tree* const* trees, uint32_t k, meerkat_dphase phase,
+                                    const uint64_t* recv, const uint64_t* recv_counts) {
+  if (!g || !trees || !recv_counts || k == 0 || k > 8) return MEERKAT_E_INVALID_ARG;
+  if (phase != MEERKAT_D_APPLY_RELAX && phase != MEERKAT_D_APPLY_PROPAGATE) return MEERKAT_E_INVALID_ARG;
+  for (uint32_t i = 0; i < k; i++)
+    if (!trees[i] || trees[i]->g != g || !trees[i]->dist) return MEERKAT_E_INVALID_ARG;
+  DeviceGuard dg(g->device);
+  return dtrees_apply(g, trees, k, (int)phase, recv, recv_counts);
 }
 
 meerkat_status meerkat_route(meerkat_graph* g, int key_is_b, const uint32_t* a, const uint32_t* b, const uint32_t* c,

@@ -497,6 +497,28 @@ cudaError_t dscan_attr(meerkat_graph* g) {
 
 }  // namespace mk
 
+// ------------------------------------------------------------------ fused exchange packing
+
+constexpr int MAX_SEGS = 2 * MEERKAT_MAX_RANKS;
+struct Segs {
+  const uint64_t* src[MAX_SEGS];   // message pairs (2 x u64 each)
+  uint64_t* dst[MAX_SEGS];
+  uint64_t start[MAX_SEGS + 1];    // exclusive prefix of the segment sizes (pairs)
+  uint32_t n;
+};
+
+// Copy every segment's pairs (one launch for all trees and peers).
+__global__ void k_copy_segs(const __grid_constant__ Segs S) {
+  const uint64_t total = S.start[S.n];
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t lo = 0, hi = S.n;   // segment of pair i: last j with start[j] <= i
+    while (hi - lo > 1) { const uint32_t mid = (lo + hi) / 2; if (S.start[mid] <= i) lo = mid; else hi = mid; }
+    const uint64_t o = i - S.start[lo];
+    const uint4 v = reinterpret_cast<const uint4*>(S.src[lo])[o];
+    reinterpret_cast<uint4*>(S.dst[lo])[o] = v;
+  }
+}
+
 // ------------------------------------------------------------------ host side of the phases
 
 namespace mk {
@@ -516,6 +538,90 @@ static cudaError_t ensure_msgs(meerkat_graph* g, meerkat_tree* t, uint64_t need)
   if (e == cudaSuccess) e = cudaMalloc(&t->msg_out, cap * 16);
   if (e == cudaSuccess) t->msg_cap = cap;
   return e;
+}
+
+// Messages of k trees for ONE all-to-all: per destination p, tree 0's pairs for p, tree 1's, ...
+meerkat_status dtrees_pack(meerkat_graph* g, meerkat_tree* const* trees, uint32_t k, int64_t* meta, uint64_t* send,
+                           uint64_t capacity_pairs, uint64_t* send_counts) {
+  const uint32_t ws = g->ws;
+  if (k == 0 || (uint64_t)ws * k > (uint64_t)MAX_SEGS) return MEERKAT_E_INVALID_ARG;
+  cudaError_t e = cudaSuccess;
+  if (!g->hmeta) e = cudaMallocHost(&g->hmeta, (size_t)MAX_SEGS * 3 * 8);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  Segs S{};
+  uint64_t off[8][MEERKAT_MAX_RANKS];   // per tree, start of each destination's pairs in msg_out
+  for (uint32_t i = 0; i < k; i++) {
+    uint64_t o = 0;
+    for (uint32_t p = 0; p < ws; p++) { off[i][p] = o; o += trees[i]->hcnt[p]; }
+  }
+  uint64_t total = 0;
+  for (uint32_t p = 0; p < ws; p++) {
+    uint64_t sp = 0;
+    for (uint32_t i = 0; i < k; i++) {
+      meerkat_tree* t = trees[i];
+      uint64_t sent = 0;
+      for (uint32_t q = 0; q < ws; q++) sent += t->hcnt[q];
+      int64_t* row = g->hmeta + 3 * ((size_t)p * k + i);
+      row[0] = (int64_t)t->hcnt[p];
+      row[1] = (int64_t)t->last_front;
+      row[2] = (int64_t)sent;
+      const uint32_t j = S.n++;
+      S.src[j] = t->msg_out + 2 * off[i][p];
+      S.dst[j] = send + 2 * total;
+      S.start[j] = total;
+      total += t->hcnt[p];
+      sp += t->hcnt[p];
+    }
+    send_counts[p] = sp;
+  }
+  S.start[S.n] = total;
+  if (total > capacity_pairs) return MEERKAT_E_CAPACITY;
+  e = cudaMemcpyAsync(meta, g->hmeta, (size_t)ws * k * 3 * 8, cudaMemcpyHostToDevice, g->stream);
+  if (e == cudaSuccess && total) {
+    k_copy_segs<<<dgrid(g, total), D_BLOCK, 0, g->stream>>>(S);
+    g->launches++;
+    e = cudaGetLastError();
+  }
+  return status_of(e);
+}
+
+// Received pairs (per source p, tree 0's rc[p*k], tree 1's rc[p*k+1], ...) into each tree's staging
+// buffer (msg_raw: free until its next emitting phase), then each tree's apply phase.
+meerkat_status dtrees_apply(meerkat_graph* g, meerkat_tree* const* trees, uint32_t k, int phase,
+                            const uint64_t* recv, const uint64_t* rc) {
+  const uint32_t ws = g->ws;
+  if (k == 0 || (uint64_t)ws * k > (uint64_t)MAX_SEGS) return MEERKAT_E_INVALID_ARG;
+  uint64_t per[8] = {0};
+  for (uint32_t p = 0; p < ws; p++)
+    for (uint32_t i = 0; i < k; i++) per[i] += rc[(size_t)p * k + i];
+  cudaError_t e = cudaSuccess;
+  for (uint32_t i = 0; i < k && e == cudaSuccess; i++)
+    if (per[i] + 1024 > trees[i]->msg_cap) e = ensure_msgs(g, trees[i], per[i] + 1024);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  Segs S{};
+  uint64_t filled[8] = {0}, total = 0;
+  for (uint32_t p = 0; p < ws; p++)
+    for (uint32_t i = 0; i < k; i++) {
+      const uint32_t j = S.n++;
+      S.src[j] = recv + 2 * total;
+      S.dst[j] = trees[i]->msg_raw + 2 * filled[i];
+      S.start[j] = total;
+      total += rc[(size_t)p * k + i];
+      filled[i] += rc[(size_t)p * k + i];
+    }
+  S.start[S.n] = total;
+  if (total) {
+    k_copy_segs<<<dgrid(g, total), D_BLOCK, 0, g->stream>>>(S);
+    g->launches++;
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  }
+  for (uint32_t i = 0; i < k; i++) {
+    if (!per[i]) continue;
+    const meerkat_status st = dtree_phase(g, trees[i], phase, trees[i]->msg_raw, nullptr, nullptr, per[i], nullptr);
+    if (st != MEERKAT_OK) return st;
+  }
+  return MEERKAT_OK;
 }
 
 meerkat_status dtree_init(meerkat_graph* g, meerkat_tree* t) {
@@ -630,6 +736,7 @@ meerkat_status dtree_phase(meerkat_graph* g, meerkat_tree* t, int phase, const v
   if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
   if (e != cudaSuccess) return MEERKAT_E_CUDA;
   t->cur_n = t->hctrl->size[t->cur];
+  t->last_front = t->cur_n;
   if (out) {
     out->msgs = t->msg_out;
     if (emits)

@@ -92,6 +92,7 @@ struct meerkat_graph {
   int latency_bps = 0;                      // blocks/SM for latency-bound tree calls (0 = occupancy)
   unsigned long long* rscratch = nullptr;   // meerkat_route: device counts + cursors
   unsigned long long* hrscratch = nullptr;  // pinned counts
+  int64_t* hmeta = nullptr;                 // pinned: meerkat_dtrees_pack's meta rows
 };
 
 struct meerkat_tree {
@@ -114,6 +115,7 @@ struct meerkat_tree {
   unsigned long long* dcnt = nullptr;       // device: counts[64], cursor[64], msg_n
   unsigned long long* hcnt = nullptr;       // pinned mirror of counts + msg_n
   uint32_t last_inval_n = 0;
+  uint64_t last_front = 0;                  // local frontier reported by the last synchronising phase
   size_t bytes = 0;
 };
 
@@ -172,6 +174,10 @@ cudaError_t launch_node_dist(meerkat_graph* g, meerkat_tree* t, uint32_t* out);
 meerkat_status dtree_phase(meerkat_graph* g, meerkat_tree* t, int phase, const void* a, const void* b,
                            const void* c, uint64_t n, meerkat_dresult* out);
 meerkat_status dtree_init(meerkat_graph* g, meerkat_tree* t);
+meerkat_status dtrees_pack(meerkat_graph* g, meerkat_tree* const* trees, uint32_t k, int64_t* meta, uint64_t* send,
+                           uint64_t capacity_pairs, uint64_t* send_counts);
+meerkat_status dtrees_apply(meerkat_graph* g, meerkat_tree* const* trees, uint32_t k, int phase,
+                            const uint64_t* recv, const uint64_t* rc);
 void dtree_free(meerkat_tree* t);
 meerkat_status route_batch(meerkat_graph* g, int key_is_b, const uint32_t* a, const uint32_t* b, const uint32_t* c,
                            uint64_t n, uint32_t* oa, uint32_t* ob, uint32_t* oc, uint64_t* counts);

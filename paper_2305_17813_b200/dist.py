@@ -233,56 +233,45 @@ class DistGraph:
         res = list(res)
         active = [True] * len(trees)
         while True:
-            recvs, act = self._exchange_many(trees, res, active)
+            act = self._exchange_apply(trees, res, apply_ph)
             if not any(act):
                 return res
             for i, t in enumerate(trees):
-                if not act[i]:
+                if act[i]:
+                    t.rounds += 1
+                else:
                     active[i] = False
-                    continue
-                n = recvs[i].numel() // 2
-                if n:
-                    t._phase(apply_ph, recvs[i], n=n)
-                t.rounds += 1
             for i, t in enumerate(trees):
                 if active[i]:
                     res[i] = t._phase(expand_ph)
 
-    def _exchange_many(self, trees, res, active):
-        """One fixed-size all-to-all of <count, local frontier, messages sent> per (peer, tree) and,
-        if any message moves, ONE all-to-all carrying every tree's messages (per peer: tree 0's,
-        then tree 1's, ...)."""
+    def _exchange_apply(self, trees, res, apply_ph):
+        """One round's exchange for all trees: the library packs every tree's messages and a fixed-size
+        <pairs, local frontier, pairs sent> row per (peer, tree) (meerkat_dtrees_pack); one all-to-all
+        of the rows decides termination and the receive sizes; ONE all-to-all moves every tree's
+        messages; the library unpacks them and runs each tree's apply phase (meerkat_dtrees_apply).
+        Returns, per tree, whether any rank still has work for it."""
         ws, k, tp = self.ws, len(trees), self.tp
-        counts = [[int(res[i].msg_counts[p]) if active[i] else 0 for p in range(ws)] for i in range(k)]
-        sent = [sum(c) for c in counts]
-        meta = torch.tensor([[[counts[i][p], int(res[i].frontier) if active[i] else 0, sent[i]] for i in range(k)]
-                             for p in range(ws)], dtype=torch.int64, device=tp._dev()).view(-1)
+        L = _lib.lib()
+        arr = (ctypes.c_void_p * k)(*[t._h.value for t in trees])
+        cap = sum(int(r.msg_counts[p]) for r in res for p in range(ws))
+        meta = torch.empty(ws * k * 3, dtype=torch.int64, device=self.device)
+        send = torch.empty(max(cap, 1) * 2, dtype=torch.int64, device=self.device)
+        sc = (ctypes.c_uint64 * ws)()
+        check(L.meerkat_dtrees_pack(self.g._h, arr, k, ctypes.c_void_p(meta.data_ptr()),
+                                    ctypes.c_void_p(send.data_ptr()), cap, sc), "meerkat_dtrees_pack")
         rmeta = tp.alltoallv_known(meta, [1] * ws, [1] * ws, elem=3 * k).view(ws, k, 3).cpu()
-        act = [active[i] and int(rmeta[:, i, 1].sum()) + int(rmeta[:, i, 2].sum()) > 0 for i in range(k)]
+        act = [int(rmeta[:, i, 1].sum()) + int(rmeta[:, i, 2].sum()) > 0 for i in range(k)]
         if not any(act):
-            return None, act
-        bufs = []
-        for i in range(k):
-            b = torch.empty(max(sent[i], 1) * 2, dtype=torch.int64, device=self.device)
-            if sent[i]:   # stream-ordered device copy out of the library's message buffer
-                check(_lib.lib().meerkat_memcpy(self.g._h, ctypes.c_void_p(b.data_ptr()),
-                                                ctypes.c_void_p(res[i].msgs), sent[i] * 16), "meerkat_memcpy")
-            bufs.append(b)
-        offs = [np.concatenate([[0], np.cumsum(counts[i])]) for i in range(k)]
-        parts = [bufs[i][2 * offs[i][p]: 2 * offs[i][p + 1]] for p in range(ws) for i in range(k)]
-        send = torch.cat(parts) if parts else torch.empty(0, dtype=torch.int64, device=self.device)
-        scounts = [sum(counts[i][p] for i in range(k)) for p in range(ws)]
-        rc = rmeta[:, :, 0].tolist()   # rc[p][i]: pairs peer p sends this rank for tree i
-        rcounts = [sum(rc[p]) for p in range(ws)]
-        recv = tp.alltoallv_known(send, scounts, rcounts, elem=2)
-        per = [[] for _ in range(k)]
-        o = 0
-        for p in range(ws):
-            for i in range(k):
-                per[i].append(recv[2 * o: 2 * (o + rc[p][i])])
-                o += rc[p][i]
-        recvs = [torch.cat(x) if x else torch.empty(0, dtype=torch.int64, device=self.device) for x in per]
-        return recvs, act
+            return act
+        scounts = [int(sc[p]) for p in range(ws)]
+        rc = rmeta[:, :, 0].reshape(-1).tolist()          # [p * k + i]
+        rcounts = [sum(rc[p * k:(p + 1) * k]) for p in range(ws)]
+        recv = tp.alltoallv_known(send[: 2 * sum(scounts)], scounts, rcounts, elem=2)
+        rca = (ctypes.c_uint64 * (ws * k))(*rc)
+        check(L.meerkat_dtrees_apply(self.g._h, arr, k, apply_ph, ctypes.c_void_p(recv.data_ptr()), rca),
+              "meerkat_dtrees_apply")
+        return act
 
     def sssp(self, source: int) -> "DistTree":
         return DistTree(self, source, unit=False)

@@ -28,7 +28,7 @@ def main():
     g.insert(T(bs), T(bd), T(bw))
     sp, bf = g.sssp(W.source), g.bfs(W.source)
     acc = defaultdict(float); cnt = defaultdict(int)
-    orig_phase, orig_ex = D.DistTree._phase, D.DistGraph._exchange_many
+    orig_phase, orig_ex = D.DistTree._phase, D.DistGraph._exchange_apply
 
     def phase(self, ph, *x, **k):
         t0 = time.perf_counter(); r = orig_phase(self, ph, *x, **k)
@@ -39,7 +39,7 @@ def main():
         t0 = time.perf_counter(); r = orig_ex(self, *x, **k)
         acc["exchange"] += time.perf_counter() - t0; cnt["exchange"] += 1
         return r
-    D.DistTree._phase, D.DistGraph._exchange_many = phase, ex
+    D.DistTree._phase, D.DistGraph._exchange_apply = phase, ex
     for i in range(3):
         acc.clear(); cnt.clear()
         s, d, w = (T(x) for x in W.inserts[i])
