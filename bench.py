@@ -122,6 +122,16 @@ def allreduce_max(x, ws):
     return float(t.item())
 
 
+def allreduce_sum(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
 # ------------------------------------------------------------------ clocks
 
 _SAMPLER = r"""
@@ -842,6 +852,8 @@ def run_dist(args, ws, rank, local):
     clocks.start()
     per_call = {n: [] for n in names}
     total_ms = 0.0
+    dec_bytes = []
+    l0 = g.g.stats()["kernel_launches"]
     for k in range(K):
         flush.zero_()
         torch.cuda.synchronize()
@@ -853,9 +865,57 @@ def run_dist(args, ws, rank, local):
         total_ms += step_ms
         for j, n in enumerate(names):
             per_call[n].append(allreduce_max(evs[j].elapsed_time(evs[j + 1]), ws))
+        # algorithmic bytes of the decremental call on this rank (both trees), read outside the interval
+        dec_bytes.append(sp.stats()["alg_bytes"] + bf.stats()["alg_bytes"])
+    launches = g.g.stats()["kernel_launches"] - l0
     clk = clocks.stop()
     mean = {n: float(np.mean(v)) for n, v in per_call.items()}
     edges = 2 * args.batch * K
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = peaks.get("hbm_gbs") or 6650.0
+    tot_bytes = allreduce_sum(float(np.mean(dec_bytes)), ws)   # all ranks' bytes of one call
+    ach = tot_bytes / (mean["trees_dec"] * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "kernel": "fused decremental update, all phases (partitioned; host-driven rounds)",
+                "achieved": ach, "peak": peak * ws, "unit": "GB/s", "frac": ach / (peak * ws),
+                "traffic": None, "alg_bytes_per_launch": tot_bytes,
+                "peak_source": ("measured (MEASURED_PEAKS.json hbm_gbs) x " if peaks.get("hbm_gbs") else
+                                "fallback (B200_PROFILING.md) x ") + f"{ws} GPUs"}
+    # e2e: the same fused step from pinned HOST batches through the public API (DistGraph), counts read
+    # back; the timed batches are undone first (not timed) and the trees recomputed
+    e2e = None
+    if not args.no_e2e:
+        for k in reversed(range(K)):
+            s, d, w = W.deletes[Wm + k]
+            g.insert(T(sl(s)), T(sl(d)), T(sl(w)), count=False)
+            s, d, _ = W.inserts[Wm + k]
+            g.delete(T(sl(s)), T(sl(d)), count=False)
+        sp.recompute(); bf.recompute()
+        torch.cuda.synchronize()
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(sl(a), np.uint32).view(np.int32)).pin_memory()
+        hi = [tuple(pin(x) for x in W.inserts[Wm + k]) for k in range(K)]
+        hd = [tuple(pin(x) for x in W.deletes[Wm + k][:2]) for k in range(K)]
+        e_ms = 0.0
+        for k in range(K):
+            barrier(ws)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            s, d, w = hi[k]
+            g.insert(s, d, w, count=True)                # H2D inside, all-reduced count read back
+            g.trees_incremental([sp, bf], s, d, w)
+            s, d = hd[k]
+            g.delete(s, d, count=True)
+            g.trees_decremental([sp, bf], s, d)
+            b.record(stream)
+            b.synchronize()
+            e_ms += allreduce_max(a.elapsed_time(b), ws)
+            flush.zero_()
+        e2e = {"value": edges / (e_ms / 1e3), "unit": "edges/s",
+               "h2d_bytes_per_step": args.batch * 4 * (3 + 3 + 2 + 2), "d2h_bytes_per_step": 2 * 8 * ws,
+               "ms_per_step": e_ms / K}
     line = {
         "metric": METRIC, "value": edges / (total_ms / 1e3), "unit": "edges/s", "n_gpus": ws, "steps": K,
         "warmup": Wm, "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "strong",
@@ -868,8 +928,8 @@ def run_dist(args, ws, rank, local):
                    "l2": "flushed before every timed step; store > L2"},
         "update_edges_per_s": 2 * args.batch / ((mean["insert"] + mean["delete"]) / 1e3),
         "sssp_bfs_fused_ms_per_batch": {"incremental": mean["trees_inc"], "decremental": mean["trees_dec"]},
-        "per_call_ms": mean, "build_s": build_s, "roofline": None, "cpu_baseline": None,
-        "e2e": None, "gpu_launches": None, "clocks": clk, "generate_s": gen_s,
+        "per_call_ms": mean, "build_s": build_s, "roofline": roofline, "cpu_baseline": None,
+        "e2e": e2e, "gpu_launches": allreduce_sum(float(launches), ws), "clocks": clk, "generate_s": gen_s,
         "note": "host-driven rounds (one NCCL all-to-all + all-reduce per frontier round); timings are max over ranks",
     }
     if rank == 0:

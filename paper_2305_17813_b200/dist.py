@@ -370,6 +370,12 @@ class DistTree:
         self._phase(_lib.D_FINISH, glist if m else None, n=m)
         self.invalidated_total = m
 
+    def stats(self) -> dict:
+        """This rank's counters of the last update (meerkat_tree_stats_get)."""
+        st = _lib.TreeStats()
+        check(_lib.lib().meerkat_tree_stats_get(self._h, ctypes.byref(st)), "meerkat_tree_stats_get")
+        return st.as_dict()
+
     def local_nodes(self) -> np.ndarray:
         a = np.empty(self.dg.n_local, np.uint64)
         check(_lib.lib().meerkat_tree_nodes(self._h, ctypes.c_void_p(a.ctypes.data)), "meerkat_tree_nodes")
