@@ -1,6 +1,6 @@
 # same-box A/B of an experimental build (paper_2305_17813_b200/libmeerkat_spec.so) against the default
 S=paper_2305_17813_b200/libmeerkat_spec.so
-MEERKAT_SO_PATH=$S timeout 900 python -m pytest tests/test_gpu_store.py tests/test_gpu_tree.py -x -q > gpurun_out/pytest32.log 2>&1; echo t=$?
+MEERKAT_SO_PATH=$S timeout 600 python -m pytest tests/test_gpu_tree.py tests/test_gpu_vanilla.py -x -q > gpurun_out/pytest32.log 2>&1; echo t=$?
 tail -2 gpurun_out/pytest32.log
 F="--no-compare --no-sweep --no-pagerank --no-wcc --no-tc --no-config4 --no-cpu-baseline --no-e2e"
 for i in 1 2; do
