@@ -264,6 +264,12 @@ meerkat_status meerkat_dtrees_pack(meerkat_graph* g, meerkat_tree* const* trees,
                                    uint64_t* send, uint64_t capacity_pairs, uint64_t* send_counts);
 meerkat_status meerkat_dtrees_apply(meerkat_graph* g, meerkat_tree* const* trees, uint32_t k, meerkat_dphase phase,
                                     const uint64_t* recv, const uint64_t* recv_counts);
+/* The DEC_SCAN phase of up to 2 trees in lock step: ONE stream of this rank's slab array serves both
+ * (invalid_lists[i]: ALL ranks' invalid vertices of tree i, device u32, invalid_counts[i] of them);
+ * outs[i] as the per-tree phase would report.  Synchronises once. */
+meerkat_status meerkat_dtrees_scan(meerkat_graph* g, meerkat_tree* const* trees, uint32_t k,
+                                   const uint32_t* const* invalid_lists, const uint64_t* invalid_counts,
+                                   meerkat_dresult* outs);
 meerkat_status meerkat_route(meerkat_graph* g, int key_is_b, const uint32_t* a, const uint32_t* b,
                              const uint32_t* c, uint64_t n, uint32_t* out_a, uint32_t* out_b, uint32_t* out_c,
                              uint64_t* counts);

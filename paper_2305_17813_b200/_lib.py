@@ -39,7 +39,7 @@ EXPORTS = [
     "meerkat_tc_count", "meerkat_tc_static", "meerkat_tc_incremental", "meerkat_tc_decremental",
     "meerkat_wcc_create", "meerkat_wcc_recompute", "meerkat_wcc_incremental", "meerkat_wcc_labels",
     "meerkat_wcc_components", "meerkat_wcc_destroy", "meerkat_tree_recompute_scheme",
-    "meerkat_wcc_incremental_tracked", "meerkat_dtrees_pack", "meerkat_dtrees_apply",
+    "meerkat_wcc_incremental_tracked", "meerkat_dtrees_pack", "meerkat_dtrees_apply", "meerkat_dtrees_scan",
 ]
 
 
@@ -160,6 +160,7 @@ def lib():
         "meerkat_wcc_incremental_tracked": (ctypes.c_int, [vp, vp]),
         "meerkat_dtrees_pack": (ctypes.c_int, [vp, pvp, u32, vp, vp, u64, pu64]),
         "meerkat_dtrees_apply": (ctypes.c_int, [vp, pvp, u32, ctypes.c_int, vp, pu64]),
+        "meerkat_dtrees_scan": (ctypes.c_int, [vp, pvp, u32, pvp, pu64, ctypes.POINTER(DResult)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -682,6 +682,18 @@ meerkat_status meerkat_dtrees_apply(meerkat_graph* g, meerkat_tree* const* trees
   return dtrees_apply(g, trees, k, (int)phase, recv, recv_counts);
 }
 
+meerkat_status meerkat_dtrees_scan(meerkat_graph* g, meerkat_tree* const* trees, uint32_t k,
+                                   const uint32_t* const* invalid_lists, const uint64_t* invalid_counts,
+                                   meerkat_dresult* outs) {
+  if (!g || !trees || !invalid_lists || !invalid_counts || k == 0 || k > 2) return MEERKAT_E_INVALID_ARG;
+  for (uint32_t i = 0; i < k; i++) {
+    if (!trees[i] || trees[i]->g != g || !trees[i]->dist) return MEERKAT_E_INVALID_ARG;
+    if (invalid_counts[i] && !invalid_lists[i]) return MEERKAT_E_INVALID_ARG;
+  }
+  DeviceGuard dg(g->device);
+  return dtrees_scan(g, trees, k, invalid_lists, invalid_counts, outs);
+}
+
 meerkat_status meerkat_route(meerkat_graph* g, int key_is_b, const uint32_t* a, const uint32_t* b, const uint32_t* c,
                              uint64_t n, uint32_t* out_a, uint32_t* out_b, uint32_t* out_c, uint64_t* counts) {
   if (!g || !counts || (n && (!a || !b || !out_a || !out_b || (c && !out_c)))) return MEERKAT_E_INVALID_ARG;

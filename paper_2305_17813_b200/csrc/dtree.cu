@@ -266,24 +266,33 @@ __global__ void k_dmark(uint32_t* bits, const uint32_t* list, uint64_t n, int se
 
 // Valid->invalid frontier over this rank's slabs: stream + smem filter,
 // as dec_scan in tree.cu, with relaxations of remote invalid vertices sent as messages.
+// Up to two trees updated in lock step share ONE stream of the slab array (one filter of the
+// union of their invalid sets; per key and tree the exact test, relax or message).
+struct DScanArgs {
+  DArgs A[2];
+  const uint32_t* list[2];
+  uint64_t n_inv[2];
+  uint32_t ntrees;
+};
+
 template <bool MAP>
-__global__ void __launch_bounds__(TREE_BLOCK, 2) k_dscan(DArgs A, const uint32_t* list, uint64_t n_inv,
-                                                         uint32_t fwords, uint32_t n_slabs) {
+__global__ void __launch_bounds__(TREE_BLOCK, 2) k_dscan(const __grid_constant__ DScanArgs S, uint32_t fwords,
+                                                         uint32_t n_slabs) {
   using F = Frag<MAP>;
   constexpr int NK = F::NK;
   constexpr int U = SCAN_UNROLL;
   extern __shared__ uint32_t filt[];
   Counters c;
-  const GraphDev& G = A.G;
-  const TreeDev& T = A.T;
+  const GraphDev& G = S.A[0].G;
   if (fwords) {
     for (uint32_t i = threadIdx.x; i < fwords; i += blockDim.x) filt[i] = 0;
     __syncthreads();
-    for (uint64_t i = threadIdx.x; i < n_inv; i += blockDim.x) {
-      uint32_t w, m;
-      filter_loc(__ldg(list + i), 32 - FILTER_LOG2, w, m);
-      atomicOr(&filt[w], m);
-    }
+    for (uint32_t j = 0; j < S.ntrees; j++)
+      for (uint64_t i = threadIdx.x; i < S.n_inv[j]; i += blockDim.x) {
+        uint32_t w, m;
+        filter_loc(__ldg(S.list[j] + i), 32 - FILTER_LOG2, w, m);
+        atomicOr(&filt[w], m);
+      }
     __syncthreads();
   }
   const int l8 = lane_id() & 7;
@@ -323,29 +332,35 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_dscan(DArgs A, const uint32_t
       for (int k = 0; k < NK; k++) {
         if (!((pos >> (q * NK + k)) & 1u)) continue;
         const uint32_t x = F::key(d[q], k);
-        bool enq = false, emit = false;
-        uint32_t lx = 0;
-        uint64_t payload = 0;
-        if (((hm >> (q * NK + k)) & 1u) && bit_test(T.inval_bits, x)) {
-          const uint32_t ul = __ldg(G.owner + s0 + q * ng);
-          const uint32_t ug = ul == NO_OWNER ? NO_OWNER : grow(G, ul);
-          if (ul != NO_OWNER && !bit_test(T.inval_bits, ug)) {
-            const uint64_t nu = ld_cg_u64(T.node + ul);
-            if (nu != UNREACHED) {
-              c.hits[0]++;
-              const uint64_t dist = (nu >> 32) + (A.unit ? 1u : F::weight(d[q], k));
-              if (dist >= INF_DIST) c.err |= ERR_OVERFLOW;
-              else if (owned(G, x)) { lx = lrow(G, x); enq = relax(T, lx, dist, ug, A.epoch, c); }
-              else { emit = true; payload = (dist << 32) | ug; }
+#pragma unroll
+        for (int j = 0; j < 2; j++) {
+          if (j >= (int)S.ntrees) break;
+          const DArgs& A = S.A[j];
+          const TreeDev& T = A.T;
+          bool enq = false, emit = false;
+          uint32_t lx = 0;
+          uint64_t payload = 0;
+          if (((hm >> (q * NK + k)) & 1u) && bit_test(T.inval_bits, x)) {
+            const uint32_t ul = __ldg(G.owner + s0 + q * ng);
+            const uint32_t ug = ul == NO_OWNER ? NO_OWNER : grow(G, ul);
+            if (ul != NO_OWNER && !bit_test(T.inval_bits, ug)) {
+              const uint64_t nu = ld_cg_u64(T.node + ul);
+              if (nu != UNREACHED) {
+                c.hits[j]++;
+                const uint64_t dist = (nu >> 32) + (A.unit ? 1u : F::weight(d[q], k));
+                if (dist >= INF_DIST) c.err |= ERR_OVERFLOW;
+                else if (owned(G, x)) { lx = lrow(G, x); enq = relax(T, lx, dist, ug, A.epoch, c); }
+                else { emit = true; payload = (dist << 32) | ug; }
+              }
             }
           }
+          warp_enqueue(G, T, A.fnext, A.sznext, enq, lx, c);
+          warp_emit(A, emit, x, payload, c);
         }
-        warp_enqueue(G, T, A.fnext, A.sznext, enq, lx, c);
-        warp_emit(A, emit, x, payload, c);
       }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) c.scan_slabs = n_slabs;
-  flush_counters(A.G, A.T, c, 0, false, 0, 0);
+  for (uint32_t j = 0; j < S.ntrees; j++) flush_counters(S.A[j].G, S.A[j].T, c, (int)j, false, 0, 0);
 }
 
 // ---- group messages by owner rank: histogram, exclusive scan, scatter
@@ -411,6 +426,14 @@ static unsigned dgrid(meerkat_graph* g, uint64_t threads) {
   return (unsigned)std::max<uint64_t>(1, std::min(b, cap));
 }
 
+static void e_scan(meerkat_graph* g, const DScanArgs& S, uint32_t fwords, uint32_t n_slabs) {
+  const size_t smem = (size_t)fwords * 4;
+  const unsigned grid = (unsigned)(g->sm_count * std::max(1, g->tree_blocks_per_sm[2]));
+  if (g->weighted) k_dscan<true><<<grid, TREE_BLOCK, smem, g->stream>>>(S, fwords, n_slabs);
+  else k_dscan<false><<<grid, TREE_BLOCK, smem, g->stream>>>(S, fwords, n_slabs);
+  g->launches++;
+}
+
 cudaError_t dlaunch(meerkat_graph* g, int kind, DArgs& A, const void* a, const void* b, const void* c, uint64_t n,
                     uint32_t fwords, uint32_t n_slabs) {
   cudaStream_t st = g->stream;
@@ -439,11 +462,11 @@ cudaError_t dlaunch(meerkat_graph* g, int kind, DArgs& A, const void* a, const v
       g->launches++;
       break;
     case 5: {
-      const size_t smem = (size_t)fwords * 4;
-      const unsigned grid = (unsigned)(g->sm_count * std::max(1, g->tree_blocks_per_sm[2]));
-      if (map) k_dscan<true><<<grid, TREE_BLOCK, smem, st>>>(A, (const uint32_t*)a, n, fwords, n_slabs);
-      else k_dscan<false><<<grid, TREE_BLOCK, smem, st>>>(A, (const uint32_t*)a, n, fwords, n_slabs);
-      g->launches++;
+      DScanArgs S{};
+      S.A[0] = A; S.A[1] = A;
+      S.list[0] = (const uint32_t*)a; S.n_inv[0] = n;
+      S.ntrees = 1;
+      e_scan(g, S, fwords, n_slabs);
       break;
     }
     case 6:
@@ -622,6 +645,81 @@ meerkat_status dtrees_apply(meerkat_graph* g, meerkat_tree* const* trees, uint32
     if (st != MEERKAT_OK) return st;
   }
   return MEERKAT_OK;
+}
+
+// The DEC_SCAN phase of up to two trees in lock step with ONE stream of the slab array: per tree
+// the phase bookkeeping of dtree_phase (new frontier buffer, epoch, message counter, marks of every
+// rank's invalid vertices), then one k_dscan, per-tree message grouping, one synchronisation.
+meerkat_status dtrees_scan(meerkat_graph* g, meerkat_tree* const* trees, uint32_t k, const uint32_t* const* lists,
+                           const uint64_t* ns, meerkat_dresult* outs) {
+  if (k == 0 || k > 2) return MEERKAT_E_INVALID_ARG;
+  cudaError_t e = cudaSuccess;
+  DScanArgs S{};
+  int nb[2] = {0, 0};
+  uint64_t n_all = 0;
+  for (uint32_t j = 0; j < k && e == cudaSuccess; j++) {
+    meerkat_tree* t = trees[j];
+    TreeDev& T = t->dev;
+    nb[j] = 1 - t->cur;
+    e = cudaMemsetAsync(&T.ctrl->size[nb[j]], 0, 8, g->stream);
+    t->depoch++;
+    if (e == cudaSuccess) e = cudaMemsetAsync(t->dcnt + 2 * MEERKAT_MAX_RANKS, 0, 8, g->stream);
+    DArgs A;
+    A.G = g->out.dev; A.T = T;
+    A.msgs = t->msg_raw; A.msg_n = t->dcnt + 2 * MEERKAT_MAX_RANKS; A.msg_cap = t->msg_cap;
+    A.fr = T.fr[t->cur]; A.n_ptr = &T.ctrl->size[t->cur];
+    A.fnext = T.fr[nb[j]]; A.sznext = &T.ctrl->size[nb[j]];
+    A.epoch = t->depoch; A.unit = t->unit ? 1u : 0u;
+    if (e == cudaSuccess && ns[j]) {
+      e = dlaunch(g, 9, A, lists[j], nullptr, (const void*)1, ns[j], 0, 0);   // mark every rank's invalid vertices
+      S.A[S.ntrees] = A;
+      S.list[S.ntrees] = lists[j];
+      S.n_inv[S.ntrees] = ns[j];
+      S.ntrees++;
+      n_all += ns[j];
+    }
+  }
+  if (e == cudaSuccess && S.ntrees) {
+    if (S.ntrees == 1) S.A[1] = S.A[0];
+    const uint32_t fw = (n_all * 8 <= (uint64_t)FILTER_WORDS * 32) ? FILTER_WORDS : 0u;
+    const uint32_t n_slabs = (uint32_t)(g->out.H + std::min<uint64_t>(g->out.hctrl->pool_top, g->out.P));
+    e_scan(g, S, fw, n_slabs);
+    e = cudaGetLastError();
+  }
+  for (uint32_t j = 0; j < k && e == cudaSuccess; j++) {
+    meerkat_tree* t = trees[j];
+    e = dsort_msgs(g, t->msg_raw, t->dcnt + 2 * MEERKAT_MAX_RANKS, t->msg_cap, t->dcnt, t->dcnt + MEERKAT_MAX_RANKS,
+                   t->msg_out);
+    t->cur = nb[j];
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(t->hcnt, t->dcnt, MEERKAT_MAX_RANKS * 8, cudaMemcpyDeviceToHost, g->stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(t->hctrl, t->dev.ctrl, sizeof(TreeCtrl), cudaMemcpyDeviceToHost, g->stream);
+  }
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(g->out.hctrl, g->out.dev.ctrl, sizeof(GraphCtrl), cudaMemcpyDeviceToHost, g->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  for (uint32_t j = 0; j < k; j++) {
+    meerkat_tree* t = trees[j];
+    t->cur_n = t->hctrl->size[t->cur];
+    t->last_front = t->cur_n;
+    if (outs) {
+      meerkat_dresult* out = outs + j;
+      std::memset(out, 0, sizeof(*out));
+      out->msgs = t->msg_out;
+      for (uint32_t r = 0; r < g->ws && r < MEERKAT_MAX_RANKS; r++) out->msg_counts[r] = t->hcnt[r];
+      out->frontier = t->cur_n;
+      out->invalid = t->dev.inval_list;
+      out->invalid_n = t->hctrl->inval_n;
+    }
+  }
+  const uint32_t err = g->out.hctrl->err;
+  if (!err) return MEERKAT_OK;
+  cudaMemsetAsync(&g->out.dev.ctrl->err, 0, 4, g->stream);
+  if (err & ERR_CAPACITY) return MEERKAT_E_CAPACITY;
+  if (err & ERR_OVERFLOW) return MEERKAT_E_OVERFLOW;
+  return MEERKAT_E_STATE;
 }
 
 meerkat_status dtree_init(meerkat_graph* g, meerkat_tree* t) {

@@ -222,7 +222,16 @@ class DistGraph:
                 check(_lib.lib().meerkat_memcpy(self.g._h, ctypes.c_void_p(mine.data_ptr()),
                                                 ctypes.c_void_p(r.invalid), k * 4), "meerkat_memcpy")
             glists.append(torch.cat(self.tp.allgather_var(mine[:k])).contiguous())
-        res = [t._phase(_lib.D_DEC_SCAN, gl if gl.numel() else None, n=gl.numel()) for t, gl in zip(trees, glists)]
+        k = len(trees)
+        if k <= 2:   # one stream of the slab array for both trees (meerkat_dtrees_scan)
+            arr = (ctypes.c_void_p * k)(*[t._h.value for t in trees])
+            lists = (ctypes.c_void_p * k)(*[gl.data_ptr() if gl.numel() else None for gl in glists])
+            ns = (ctypes.c_uint64 * k)(*[gl.numel() for gl in glists])
+            outs = (_lib.DResult * k)()
+            check(_lib.lib().meerkat_dtrees_scan(self.g._h, arr, k, lists, ns, outs), "meerkat_dtrees_scan")
+            res = [outs[i] for i in range(k)]
+        else:
+            res = [t._phase(_lib.D_DEC_SCAN, gl if gl.numel() else None, n=gl.numel()) for t, gl in zip(trees, glists)]
         self._fused_loop(trees, _lib.D_RELAX, _lib.D_APPLY_RELAX, res)
         for t, gl in zip(trees, glists):
             t._phase(_lib.D_FINISH, gl if gl.numel() else None, n=gl.numel())
