@@ -270,6 +270,10 @@ meerkat_status meerkat_dtrees_apply(meerkat_graph* g, meerkat_tree* const* trees
 meerkat_status meerkat_dtrees_scan(meerkat_graph* g, meerkat_tree* const* trees, uint32_t k,
                                    const uint32_t* const* invalid_lists, const uint64_t* invalid_counts,
                                    meerkat_dresult* outs);
+/* An expansion phase (RELAX / PROPAGATE) of k (<= 8) trees in lock step, ONE synchronisation;
+ * outs[i] as the per-tree phase would report. */
+meerkat_status meerkat_dtrees_expand(meerkat_graph* g, meerkat_tree* const* trees, uint32_t k, meerkat_dphase phase,
+                                     meerkat_dresult* outs);
 meerkat_status meerkat_route(meerkat_graph* g, int key_is_b, const uint32_t* a, const uint32_t* b,
                              const uint32_t* c, uint64_t n, uint32_t* out_a, uint32_t* out_b, uint32_t* out_c,
                              uint64_t* counts);

@@ -694,6 +694,16 @@ meerkat_status meerkat_dtrees_scan(meerkat_graph* g, meerkat_tree* const* trees,
   return dtrees_scan(g, trees, k, invalid_lists, invalid_counts, outs);
 }
 
+meerkat_status meerkat_dtrees_expand(meerkat_graph* g, meerkat_tree* const* trees, uint32_t k, meerkat_dphase phase,
+                                     meerkat_dresult* outs) {
+  if (!g || !trees || k == 0 || k > 8) return MEERKAT_E_INVALID_ARG;
+  if (phase != MEERKAT_D_RELAX && phase != MEERKAT_D_PROPAGATE) return MEERKAT_E_INVALID_ARG;
+  for (uint32_t i = 0; i < k; i++)
+    if (!trees[i] || trees[i]->g != g || !trees[i]->dist) return MEERKAT_E_INVALID_ARG;
+  DeviceGuard dg(g->device);
+  return dtrees_expand(g, trees, k, (int)phase, outs);
+}
+
 meerkat_status meerkat_route(meerkat_graph* g, int key_is_b, const uint32_t* a, const uint32_t* b, const uint32_t* c,
                              uint64_t n, uint32_t* out_a, uint32_t* out_b, uint32_t* out_c, uint64_t* counts) {
   if (!g || !counts || (n && (!a || !b || !out_a || !out_b || (c && !out_c)))) return MEERKAT_E_INVALID_ARG;

@@ -738,8 +738,20 @@ void dtree_free(meerkat_tree* t) {
   if (t->hcnt) cudaFreeHost(t->hcnt);
 }
 
+static meerkat_status dtree_finish_phase(meerkat_graph* g, meerkat_tree* t, bool emits, meerkat_dresult* out);
+
+// defer: enqueue the phase only (no synchronisation / read-back); dtrees_expand finishes a batch of
+// deferred phases with one synchronisation.
+meerkat_status dtree_phase_x(meerkat_graph* g, meerkat_tree* t, int phase, const void* a, const void* b,
+                             const void* c, uint64_t n, meerkat_dresult* out, bool defer);
+
 meerkat_status dtree_phase(meerkat_graph* g, meerkat_tree* t, int phase, const void* a, const void* b, const void* c,
                            uint64_t n, meerkat_dresult* out) {
+  return dtree_phase_x(g, t, phase, a, b, c, n, out, false);
+}
+
+meerkat_status dtree_phase_x(meerkat_graph* g, meerkat_tree* t, int phase, const void* a, const void* b,
+                             const void* c, uint64_t n, meerkat_dresult* out, bool defer) {
   const bool seed = phase == MEERKAT_D_STATIC_INIT || phase == MEERKAT_D_INC_SEED ||
                     phase == MEERKAT_D_DEC_INVALIDATE || phase == MEERKAT_D_DEC_SCAN;
   const bool expands = phase == MEERKAT_D_PROPAGATE || phase == MEERKAT_D_RELAX;
@@ -825,14 +837,20 @@ meerkat_status dtree_phase(meerkat_graph* g, meerkat_tree* t, int phase, const v
     if (out) { out->msgs = t->msg_out; out->invalid = T.inval_list; }
     return MEERKAT_OK;
   }
-  // one synchronisation per phase: message counts, tree control block, graph error word
-  if (e == cudaSuccess && emits)
-    e = cudaMemcpyAsync(t->hcnt, t->dcnt, MEERKAT_MAX_RANKS * 8, cudaMemcpyDeviceToHost, g->stream);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(t->hctrl, T.ctrl, sizeof(TreeCtrl), cudaMemcpyDeviceToHost, g->stream);
-  if (e == cudaSuccess)
-    e = cudaMemcpyAsync(g->out.hctrl, g->out.dev.ctrl, sizeof(GraphCtrl), cudaMemcpyDeviceToHost, g->stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
   if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  if (defer) return MEERKAT_OK;
+  return dtree_finish_phase(g, t, emits, out);
+}
+
+// One synchronisation per phase: message counts, tree control block, graph error word.
+static meerkat_status dtree_readback(meerkat_graph* g, meerkat_tree* t, bool emits) {
+  cudaError_t e = cudaSuccess;
+  if (emits) e = cudaMemcpyAsync(t->hcnt, t->dcnt, MEERKAT_MAX_RANKS * 8, cudaMemcpyDeviceToHost, g->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(t->hctrl, t->dev.ctrl, sizeof(TreeCtrl), cudaMemcpyDeviceToHost, g->stream);
+  return e == cudaSuccess ? MEERKAT_OK : MEERKAT_E_CUDA;
+}
+
+static meerkat_status dtree_report(meerkat_graph* g, meerkat_tree* t, bool emits, meerkat_dresult* out) {
   t->cur_n = t->hctrl->size[t->cur];
   t->last_front = t->cur_n;
   if (out) {
@@ -840,9 +858,13 @@ meerkat_status dtree_phase(meerkat_graph* g, meerkat_tree* t, int phase, const v
     if (emits)
       for (uint32_t r = 0; r < g->ws && r < MEERKAT_MAX_RANKS; r++) out->msg_counts[r] = t->hcnt[r];
     out->frontier = t->cur_n;
-    out->invalid = T.inval_list;
+    out->invalid = t->dev.inval_list;
     out->invalid_n = t->hctrl->inval_n;
   }
+  return MEERKAT_OK;
+}
+
+static meerkat_status graph_err_status(meerkat_graph* g) {
   const uint32_t err = g->out.hctrl->err;
   if (!err) return MEERKAT_OK;
   cudaMemsetAsync(&g->out.dev.ctrl->err, 0, 4, g->stream);
@@ -852,6 +874,33 @@ meerkat_status dtree_phase(meerkat_graph* g, meerkat_tree* t, int phase, const v
   if (err & ERR_CAPACITY) return MEERKAT_E_CAPACITY;
   if (err & ERR_OVERFLOW) return MEERKAT_E_OVERFLOW;
   return MEERKAT_E_STATE;
+}
+
+static meerkat_status dtree_finish_phase(meerkat_graph* g, meerkat_tree* t, bool emits, meerkat_dresult* out) {
+  if (dtree_readback(g, t, emits) != MEERKAT_OK) return MEERKAT_E_CUDA;
+  cudaError_t e = cudaMemcpyAsync(g->out.hctrl, g->out.dev.ctrl, sizeof(GraphCtrl), cudaMemcpyDeviceToHost, g->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  dtree_report(g, t, emits, out);
+  return graph_err_status(g);
+}
+
+// An expansion phase (PROPAGATE / RELAX) of k trees in lock step with ONE synchronisation.
+meerkat_status dtrees_expand(meerkat_graph* g, meerkat_tree* const* trees, uint32_t k, int phase,
+                             meerkat_dresult* outs) {
+  for (uint32_t j = 0; j < k; j++) {
+    if (outs) std::memset(outs + j, 0, sizeof(meerkat_dresult));
+    const meerkat_status st = dtree_phase_x(g, trees[j], phase, nullptr, nullptr, nullptr, 0, outs ? outs + j : nullptr,
+                                            true);
+    if (st != MEERKAT_OK) return st;
+  }
+  for (uint32_t j = 0; j < k; j++)
+    if (dtree_readback(g, trees[j], true) != MEERKAT_OK) return MEERKAT_E_CUDA;
+  cudaError_t e = cudaMemcpyAsync(g->out.hctrl, g->out.dev.ctrl, sizeof(GraphCtrl), cudaMemcpyDeviceToHost, g->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  for (uint32_t j = 0; j < k; j++) dtree_report(g, trees[j], true, outs ? outs + j : nullptr);
+  return graph_err_status(g);
 }
 
 meerkat_status route_batch(meerkat_graph* g, int key_is_b, const uint32_t* a, const uint32_t* b, const uint32_t* c,

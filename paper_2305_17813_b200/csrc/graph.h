@@ -180,6 +180,8 @@ meerkat_status dtrees_apply(meerkat_graph* g, meerkat_tree* const* trees, uint32
                             const uint64_t* recv, const uint64_t* rc);
 meerkat_status dtrees_scan(meerkat_graph* g, meerkat_tree* const* trees, uint32_t k, const uint32_t* const* lists,
                            const uint64_t* ns, meerkat_dresult* outs);
+meerkat_status dtrees_expand(meerkat_graph* g, meerkat_tree* const* trees, uint32_t k, int phase,
+                             meerkat_dresult* outs);
 void dtree_free(meerkat_tree* t);
 meerkat_status route_batch(meerkat_graph* g, int key_is_b, const uint32_t* a, const uint32_t* b, const uint32_t* c,
                            uint64_t n, uint32_t* oa, uint32_t* ob, uint32_t* oc, uint64_t* counts);

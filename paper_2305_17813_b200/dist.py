@@ -250,9 +250,14 @@ class DistGraph:
                     t.rounds += 1
                 else:
                     active[i] = False
-            for i, t in enumerate(trees):
-                if active[i]:
-                    res[i] = t._phase(expand_ph)
+            live = [i for i in range(len(trees)) if active[i]]
+            if live:   # every still-active tree's expansion, one synchronisation (meerkat_dtrees_expand)
+                arr = (ctypes.c_void_p * len(live))(*[trees[i]._h.value for i in live])
+                outs = (_lib.DResult * len(live))()
+                check(_lib.lib().meerkat_dtrees_expand(self.g._h, arr, len(live), expand_ph, outs),
+                      "meerkat_dtrees_expand")
+                for j, i in enumerate(live):
+                    res[i] = outs[j]
 
     def _exchange_apply(self, trees, res, apply_ph):
         """One round's exchange for all trees: the library packs every tree's messages and a fixed-size
