@@ -788,6 +788,8 @@ def run_ours(args, ws, rank, local):
                               if split else None),
         "bfs_ms_per_batch": ({"incremental": split["bfs_inc"], "decremental": split["bfs_dec"]} if split else None),
         "per_call_ms": mean,
+        "per_call_ms_p50_p95": {n: [float(np.percentile(v, 50)), float(np.percentile(v, 95))]
+                                for n, v in res["per_call"].items()},
         "static_recompute_ms": res["static_ms"],
         "vanilla_static_ms": res["vanilla_ms"] or None,
         "iteration_scheme1_static_ms": res["scheme1_ms"] or None,
