@@ -50,6 +50,9 @@ def parse():
     p.add_argument("--batch", type=int, default=100_000)
     p.add_argument("--lf", type=float, default=0.7)
     p.add_argument("--no-hashing", action="store_true")
+    p.add_argument("--seed", action=argparse.BooleanOptionalAction, default=True,
+                   help="with --fused, the insert / delete kernels seed the tree calls (batch prologue "
+                        "inside the mutation kernel: meerkat_*_batch_trees)")
     p.add_argument("--fused", action=argparse.BooleanOptionalAction, default=True,
                    help="update the SSSP and BFS trees with one fused launch per batch (meerkat_trees_*)")
     p.add_argument("--per-tree", action=argparse.BooleanOptionalAction, default=True,
@@ -141,8 +144,12 @@ h = pynvml.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
 print("max", pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM), flush=True)
 while True:
     try:
-        print(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
-              pynvml.nvmlDeviceGetCurrentClocksEventReasons(h), flush=True)
+        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+        try:
+            rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except Exception:
+            rs = -1   # reasons unavailable: the clock is still recorded
+        print(sm, rs, flush=True)
     except Exception:
         pass
     time.sleep(0.002)
@@ -166,6 +173,7 @@ class ClockSampler:
         self.idx = idx
         self.proc = None
         self.lines = []
+        self.n0 = 0
 
     def start(self):
         import subprocess
@@ -175,15 +183,19 @@ class ClockSampler:
             self.t = threading.Thread(target=lambda: self.lines.extend(self.proc.stdout), daemon=True)
             self.t.start()
             t0 = time.time()
-            while not self.lines and time.time() - t0 < 20:   # wait until sampling runs
+            while len(self.lines) < 2 and time.time() - t0 < 20:   # wait until samples arrive ("max" + one)
                 time.sleep(0.01)
+            self.n0 = len(self.lines)   # samples from here on are the timed region's
         except Exception:
             self.proc = None
 
     def stop(self):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml sampler unavailable"]}
-        time.sleep(0.01)
+        t0 = time.time()
+        # a timed region shorter than the sampling period still gets the sample that ends it
+        while len(self.lines) <= self.n0 and time.time() - t0 < 2:
+            time.sleep(0.002)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -191,14 +203,17 @@ class ClockSampler:
             self.proc.kill()
         self.t.join(timeout=2)
         mx, sm, reasons = None, [], set()
-        for ln in self.lines:
+        for i, ln in enumerate(self.lines):
             p = ln.split()
             if p and p[0] == "max":
                 mx = int(p[1])
-            elif len(p) == 2:
+            elif len(p) == 2 and i >= self.n0:
                 sm.append(int(p[0]))
                 rs = int(p[1])
-                reasons |= {n for bit, n in self.REASONS.items() if rs & bit}
+                if rs < 0:
+                    reasons.add("reasons unavailable")
+                else:
+                    reasons |= {n for bit, n in self.REASONS.items() if rs & bit}
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
                 "samples": len(sm)}
 
@@ -220,7 +235,8 @@ def workload_config(args, V, n_base, source, ws=1):
             "vertices": V, "edges": n_base, "batch": args.batch, "source": source,
             "hashing": not args.no_hashing, "load_factor": args.lf,
             "decremental_frontier": args.frontier,
-            "tree_updates": "fused SSSP+BFS (meerkat_trees_*)" if args.fused else "per tree",
+            "tree_updates": ("fused SSSP+BFS (meerkat_trees_*)" if args.fused else "per tree")
+                            + (", seeded by the insert / delete kernels" if args.fused and args.seed else ""),
             "parallelism": "single GPU" if ws == 1 else f"{ws} independent replicas",
             "l2": ("flushed between timed steps (256 MiB write, outside the intervals); store > L2" if args.l2_flush
                    else "not flushed: inputs larger than L2 (store > L2), batches back to back")}
@@ -302,18 +318,20 @@ NAMES = ["insert", "sssp_inc", "bfs_inc", "delete", "sssp_dec", "bfs_dec"]
 NAMES_FUSED = ["insert", "trees_inc", "delete", "trees_dec"]
 
 
-def one_step(g, sp, bf, ins, dels, evs, stream, fused=False):
+def one_step(g, sp, bf, ins, dels, evs, stream, fused=False, seed=False):
     """The hot path over one batch pair: mutate, then update both trees.  fused: one
-    launch updates the SSSP and the BFS tree together (meerkat_trees_*)."""
+    launch updates the SSSP and the BFS tree together (meerkat_trees_*); seed: the trees' batch
+    prologue runs inside the insert / delete kernel (meerkat_*_batch_trees)."""
     s, d, w = ins
     if fused:
+        trees = [sp, bf] if seed else None
         evs[0].record(stream)
-        g.insert(s, d, w, count=False)
+        g.insert(s, d, w, count=False, seed=trees)
         evs[1].record(stream)
         g.trees_incremental([sp, bf], s, d, w)
         evs[2].record(stream)
         s, d = dels
-        g.delete(s, d, count=False)
+        g.delete(s, d, count=False, seed=trees)
         evs[3].record(stream)
         g.trees_decremental([sp, bf], s, d)
         evs[4].record(stream)
@@ -336,13 +354,14 @@ def one_step(g, sp, bf, ins, dels, evs, stream, fused=False):
 
 def measure(args, ws, W, frontier, dev, local, stream, T, flush, K, Wm, clocks=None, fused=True):
     import torch
+    seed = fused and getattr(args, "seed", False)
     g, sp, bf, n_base, bulk_ms = build(args, W, frontier, dev, local, stream, T)
     ins = [tuple(T(x) for x in b) for b in W.inserts]
     dels = [tuple(T(x) for x in b[:2]) for b in W.deletes]
     names = NAMES_FUSED if fused else NAMES
     ev = lambda: [torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)]
     for i in range(Wm):
-        one_step(g, sp, bf, ins[i], dels[i], ev(), stream, fused)
+        one_step(g, sp, bf, ins[i], dels[i], ev(), stream, fused, seed)
         flush.zero_()
     torch.cuda.synchronize()
     g.sync()
@@ -358,7 +377,7 @@ def measure(args, ws, W, frontier, dev, local, stream, T, flush, K, Wm, clocks=N
     for k in range(K):
         i = Wm + k
         evs = ev()
-        one_step(g, sp, bf, ins[i], dels[i], evs, stream, fused)
+        one_step(g, sp, bf, ins[i], dels[i], evs, stream, fused, seed)
         evs[-1].synchronize()
         for j, n in enumerate(names):
             per_call[n].append(evs[j].elapsed_time(evs[j + 1]))
@@ -710,14 +729,15 @@ def run_ours(args, ws, rank, local):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             s, d, w = hi[k]
-            g.insert(s, d, w, count=True)          # H2D staged inside the call, count read back (D2H)
+            seed = [sp, bf] if (args.fused and args.seed) else None
+            g.insert(s, d, w, count=True, seed=seed)   # H2D staged inside the call, count read back (D2H)
             if args.fused:
                 g.trees_incremental([sp, bf], s, d, w)
             else:
                 sp.incremental(s, d, w)
                 bf.incremental(s, d)
             s, d = hd[k]
-            g.delete(s, d, count=True)
+            g.delete(s, d, count=True, seed=seed)
             if args.fused:
                 g.trees_decremental([sp, bf], s, d)
             else:

@@ -191,6 +191,22 @@ meerkat_status meerkat_trees_incremental(meerkat_graph* g, meerkat_tree* const* 
                                          const uint32_t* src, const uint32_t* dst, const uint32_t* w, uint64_t n);
 meerkat_status meerkat_trees_decremental(meerkat_graph* g, meerkat_tree* const* trees, uint32_t n_trees,
                                          const uint32_t* src, const uint32_t* dst, uint64_t n);
+/* insert_batch that also SEEDS the trees' next incremental call: the trees' batch prologue
+ * (relax node[v] from node[u] + w for each inserted (u, v), enqueue the improved v; it
+ * reads no slab) runs inside the insert kernel, so the meerkat_trees_incremental (or per-tree
+ * incremental) call that must follow with the same batch and the same trees starts at its first
+ * frontier round: one grid-wide phase and barrier fewer.  The trees (up to 2, of g, not vanilla)
+ * must reflect g's current version and not be seeded already (else MEERKAT_E_STATE); a fused call
+ * must name all seeded trees or none.  Results are those of insert_batch + trees_incremental.
+ * Between the two calls node[] is partial; a static recompute drops an unused seed.  w: NULL iff
+ * the graph is unweighted.  n_inserted as insert_batch. */
+meerkat_status meerkat_insert_batch_trees(meerkat_graph* g, const uint32_t* src, const uint32_t* dst,
+                                          const uint32_t* w, uint64_t n, meerkat_tree* const* trees,
+                                          uint32_t n_trees, uint64_t* n_inserted);
+/* delete_batch that seeds the trees' next decremental call the same way: the invalidation of the
+ * deleted tree edges (C4) runs inside the delete kernel.  n_deleted as delete_batch. */
+meerkat_status meerkat_delete_batch_trees(meerkat_graph* g, const uint32_t* src, const uint32_t* dst, uint64_t n,
+                                          meerkat_tree* const* trees, uint32_t n_trees, uint64_t* n_deleted);
 /* Static re-run on the current graph (the s_b^n baseline). */
 meerkat_status meerkat_tree_recompute(meerkat_graph* g, meerkat_tree* t);
 /* The same with the paper's iteration scheme chosen: 2 = <vertex, bucket> work items

@@ -33,6 +33,7 @@ EXPORTS = [
     "meerkat_tree_nodes", "meerkat_tree_invalidated", "meerkat_tree_stats_get", "meerkat_tree_destroy",
     "meerkat_dtree_create", "meerkat_dtree_phase", "meerkat_memcpy", "meerkat_route", "meerkat_tree_timeline",
     "meerkat_check", "meerkat_trees_incremental", "meerkat_trees_decremental",
+    "meerkat_insert_batch_trees", "meerkat_delete_batch_trees",
     "meerkat_pagerank_create", "meerkat_pagerank_update", "meerkat_pagerank_recompute", "meerkat_pagerank_values",
     "meerkat_pagerank_stats_get", "meerkat_pagerank_destroy",
     "meerkat_sssp_vanilla_create", "meerkat_bfs_vanilla_create", "meerkat_tree_distances",
@@ -134,6 +135,8 @@ def lib():
         "meerkat_check": (ctypes.c_int, [vp, pu64]),
         "meerkat_trees_incremental": (ctypes.c_int, [vp, pvp, u32, vp, vp, vp, u64]),
         "meerkat_trees_decremental": (ctypes.c_int, [vp, pvp, u32, vp, vp, u64]),
+        "meerkat_insert_batch_trees": (ctypes.c_int, [vp, vp, vp, vp, u64, pvp, u32, pu64]),
+        "meerkat_delete_batch_trees": (ctypes.c_int, [vp, vp, vp, u64, pvp, u32, pu64]),
         "meerkat_dtree_create": (ctypes.c_int, [vp, u32, u32, pvp]),
         "meerkat_dtree_phase": (ctypes.c_int, [vp, vp, ctypes.c_int, vp, vp, vp, u64, ctypes.POINTER(DResult)]),
         "meerkat_memcpy": (ctypes.c_int, [vp, vp, vp, u64]),

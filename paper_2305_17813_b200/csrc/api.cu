@@ -472,6 +472,8 @@ static meerkat_status trees_update(meerkat_graph* g, meerkat_tree* const* ts, ui
       if (ts[j] == t) return MEERKAT_E_INVALID_ARG;
     // ordering contract: the batch must be the mutation just applied
     if (g->last_kind != kind || t->version + 1 != g->version) return MEERKAT_E_STATE;
+    // seeded by that mutation (insert_batch_trees / delete_batch_trees): all the call's trees or none
+    if ((t->seeded != 0) != (ts[0]->seeded != 0) || (t->seeded && t->seeded != kind)) return MEERKAT_E_STATE;
     need_w |= kind == 1 && !t->unit;
   }
   if (need_w && n && !w) return MEERKAT_E_INVALID_ARG;
@@ -482,9 +484,9 @@ static meerkat_status trees_update(meerkat_graph* g, meerkat_tree* const* ts, ui
   if (e == cudaSuccess && need_w) e = stage_in_reuse(g, 2, w, n * 4, &ww);
   if (e == cudaSuccess)
     e = launch_tree(g, ts, k, kind == 1 ? MODE_INCREMENTAL : MODE_DECREMENTAL, (const uint32_t*)s, (const uint32_t*)d,
-                    (const uint32_t*)ww, n);
+                    (const uint32_t*)ww, n, ts[0]->seeded != 0);
   if (e != cudaSuccess) return MEERKAT_E_CUDA;
-  for (uint32_t i = 0; i < k; i++) ts[i]->version = g->version;
+  for (uint32_t i = 0; i < k; i++) { ts[i]->version = g->version; ts[i]->seeded = 0; }
   return MEERKAT_OK;
 }
 
@@ -492,6 +494,62 @@ static meerkat_status tree_update(meerkat_graph* g, meerkat_tree* t, bool unit, 
                                   const uint32_t* dst, const uint32_t* w, uint64_t n) {
   if (!t || t->unit != unit) return MEERKAT_E_INVALID_ARG;
   return trees_update(g, &t, 1, kind, src, dst, unit ? nullptr : w, n);
+}
+
+// Mutation that also seeds the trees' next call (P:24-26 order: the batch is applied, then the
+// trees follow): the trees' batch prologue (relaxation of the inserted edges / invalidation of the
+// deleted tree edges) runs inside the insert / delete kernel; the trees_* call that must follow
+// with the same batch starts at its first frontier round.
+static meerkat_status batch_seed(meerkat_graph* g, int kind, const uint32_t* src, const uint32_t* dst,
+                                 const uint32_t* w, uint64_t n, meerkat_tree* const* ts, uint32_t k,
+                                 uint64_t* n_changed) {
+  meerkat_status st = check_batch(g, src, dst, n);
+  if (st != MEERKAT_OK) return st;
+  if (kind == 1 && n && (g->weighted != (w != nullptr))) return MEERKAT_E_INVALID_ARG;
+  if (!ts || k == 0 || k > (uint32_t)MAX_TREES) return MEERKAT_E_INVALID_ARG;
+  for (uint32_t i = 0; i < k; i++) {
+    meerkat_tree* t = ts[i];
+    if (!t || t->g != g || t->dist) return MEERKAT_E_INVALID_ARG;
+    if (t->vanilla) return MEERKAT_E_STATE;   // no dependence tree: static only
+    for (uint32_t j = 0; j < i; j++)
+      if (ts[j] == t) return MEERKAT_E_INVALID_ARG;
+    if (t->version != g->version || t->seeded) return MEERKAT_E_STATE;   // must be current, not seeded
+  }
+  DeviceGuard dg(g->device);
+  const void *s, *d, *ww = nullptr;
+  cudaError_t e = stage_in(g, 0, src, n * 4, &s);
+  if (e == cudaSuccess) e = stage_in(g, 1, dst, n * 4, &d);
+  if (e == cudaSuccess && kind == 1 && w) e = stage_in(g, 2, w, n * 4, &ww);
+  unsigned long long* cnt = kind == 1 ? &g->out.dev.ctrl->n_inserted : &g->out.dev.ctrl->n_deleted;
+  if (e == cudaSuccess && n_changed) e = cudaMemsetAsync(cnt, 0, 8, g->stream);
+  TreePro P;
+  tree_pro_fill(ts, k, P);
+  Store* mirror = g->reverse ? &g->in : nullptr;
+  if (e == cudaSuccess)
+    e = kind == 1 ? launch_insert(g, &g->out, mirror, (const uint32_t*)s, (const uint32_t*)d, (const uint32_t*)ww, n, &P)
+                  : launch_delete(g, &g->out, mirror, (const uint32_t*)s, (const uint32_t*)d, n, &P);
+  if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  g->version++;
+  g->last_kind = kind;
+  remember_stage(g, 0, src, n * 4);
+  remember_stage(g, 1, dst, n * 4);
+  if (ww) remember_stage(g, 2, w, n * 4);
+  for (uint32_t i = 0; i < k; i++) ts[i]->seeded = kind;
+  if (!n_changed) return MEERKAT_OK;
+  st = collect(g);
+  *n_changed = kind == 1 ? g->out.hctrl->n_inserted : g->out.hctrl->n_deleted;
+  return st;
+}
+
+meerkat_status meerkat_insert_batch_trees(meerkat_graph* g, const uint32_t* src, const uint32_t* dst,
+                                          const uint32_t* w, uint64_t n, meerkat_tree* const* trees,
+                                          uint32_t n_trees, uint64_t* n_inserted) {
+  return batch_seed(g, 1, src, dst, w, n, trees, n_trees, n_inserted);
+}
+
+meerkat_status meerkat_delete_batch_trees(meerkat_graph* g, const uint32_t* src, const uint32_t* dst, uint64_t n,
+                                          meerkat_tree* const* trees, uint32_t n_trees, uint64_t* n_deleted) {
+  return batch_seed(g, 2, src, dst, nullptr, n, trees, n_trees, n_deleted);
 }
 
 meerkat_status meerkat_trees_incremental(meerkat_graph* g, meerkat_tree* const* trees, uint32_t n_trees,
@@ -524,12 +582,23 @@ meerkat_status meerkat_bfs_decremental(meerkat_graph* g, meerkat_tree* t, const 
   return tree_update(g, t, true, 2, src, dst, nullptr, n);
 }
 
+// A seeded tree whose trees_* call never came (the graph moved on): drop the seeded frontier,
+// counters and V_invalid marks before a static re-run.
+static cudaError_t unseed(meerkat_graph* g, meerkat_tree* t) {
+  if (!t->seeded) return cudaSuccess;
+  t->seeded = 0;
+  cudaError_t e = cudaMemsetAsync(t->ctrl_base + t->parity, 0, sizeof(TreeCtrl), g->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(t->dev.inval_bits, 0, ((size_t)g->V + 31) / 32 * 4, g->stream);
+  return e;
+}
+
 meerkat_status meerkat_tree_recompute_scheme(meerkat_graph* g, meerkat_tree* t, uint32_t iteration_scheme) {
   if (!g || !t || t->g != g || t->dist || (iteration_scheme != 1 && iteration_scheme != 2))
     return MEERKAT_E_INVALID_ARG;
   DeviceGuard dg(g->device);
   t->dev.scheme1 = iteration_scheme == 1 ? 1u : 0u;
-  cudaError_t e = launch_tree(g, &t, 1, MODE_STATIC, nullptr, nullptr, nullptr, 0);
+  cudaError_t e = unseed(g, t);
+  if (e == cudaSuccess) e = launch_tree(g, &t, 1, MODE_STATIC, nullptr, nullptr, nullptr, 0);
   t->dev.scheme1 = 0;   // dynamic updates always use <vertex, bucket> items
   if (e != cudaSuccess) return MEERKAT_E_CUDA;
   t->version = g->version;
@@ -539,7 +608,8 @@ meerkat_status meerkat_tree_recompute_scheme(meerkat_graph* g, meerkat_tree* t, 
 meerkat_status meerkat_tree_recompute(meerkat_graph* g, meerkat_tree* t) {
   if (!g || !t || t->g != g || t->dist) return MEERKAT_E_INVALID_ARG;
   DeviceGuard dg(g->device);
-  cudaError_t e = launch_tree(g, &t, 1, MODE_STATIC, nullptr, nullptr, nullptr, 0);
+  cudaError_t e = unseed(g, t);
+  if (e == cudaSuccess) e = launch_tree(g, &t, 1, MODE_STATIC, nullptr, nullptr, nullptr, 0);
   if (e != cudaSuccess) return MEERKAT_E_CUDA;
   t->version = g->version;
   return MEERKAT_OK;

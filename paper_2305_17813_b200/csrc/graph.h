@@ -104,6 +104,7 @@ struct meerkat_tree {
   uint64_t version = 0;
   mk::TreeCtrl* ctrl_base = nullptr;   // two control blocks: a call uses one and zeroes the other
   int parity = 0;
+  int seeded = 0;   // 1 / 2: insert_batch_trees / delete_batch_trees ran this call's batch prologue
   // vertex-partitioned trees (dtree.cu)
   bool dist = false;
   int cur = 0;                              // frontier buffer filled by the last phase
@@ -157,9 +158,17 @@ cudaError_t launch_pagerank(meerkat_graph* g, meerkat_pagerank* p, bool warm);
 cudaError_t launch_build(meerkat_graph* g, Store& st, const uint32_t* d_hints, uint64_t pool_request);
 void free_store(Store& st);
 // st1 (nullable): the in-edge mirror, updated with (dst, src) in the same launch
+// Tree prologue fused into a mutation kernel (meerkat_insert_batch_trees / meerkat_delete_batch_trees):
+// the trees' device views with the control blocks of the tree call that follows.
+struct TreePro {
+  TreeDev T[MAX_TREES];
+  uint32_t ntrees;
+};
+void tree_pro_fill(meerkat_tree* const* trees, uint32_t ntrees, TreePro& p);
 cudaError_t launch_insert(meerkat_graph* g, Store* st0, Store* st1, const uint32_t* s, const uint32_t* d,
-                          const uint32_t* w, uint64_t n);
-cudaError_t launch_delete(meerkat_graph* g, Store* st0, Store* st1, const uint32_t* s, const uint32_t* d, uint64_t n);
+                          const uint32_t* w, uint64_t n, const TreePro* pro = nullptr);
+cudaError_t launch_delete(meerkat_graph* g, Store* st0, Store* st1, const uint32_t* s, const uint32_t* d, uint64_t n,
+                          const TreePro* pro = nullptr);
 cudaError_t launch_query(meerkat_graph* g, Store& st, const uint32_t* s, const uint32_t* d, uint64_t n,
                          uint8_t* found, uint32_t* w_out);
 cudaError_t launch_export(meerkat_graph* g, Store& st, uint32_t* s, uint32_t* d, uint32_t* w, uint64_t cap);
@@ -168,7 +177,7 @@ cudaError_t launch_fsck(meerkat_graph* g, Store& st, unsigned long long* info_de
 cudaError_t tree_occupancy(meerkat_graph* g);
 enum TreeMode { MODE_STATIC = 0, MODE_INCREMENTAL = 1, MODE_DECREMENTAL = 2 };
 cudaError_t launch_tree(meerkat_graph* g, meerkat_tree* const* trees, uint32_t ntrees, int mode, const uint32_t* s,
-                        const uint32_t* d, const uint32_t* w, uint64_t n);
+                        const uint32_t* d, const uint32_t* w, uint64_t n, bool pro_done = false);
 cudaError_t launch_node_dist(meerkat_graph* g, meerkat_tree* t, uint32_t* out);
 // dtree.cu
 meerkat_status dtree_phase(meerkat_graph* g, meerkat_tree* t, int phase, const void* a, const void* b,

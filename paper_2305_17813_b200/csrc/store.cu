@@ -21,6 +21,7 @@
 #include <cub/cub.cuh>
 
 #include "store_ops.cuh"
+#include "tree_common.cuh"
 
 namespace mk {
 
@@ -223,7 +224,29 @@ struct UpdArgs {
   const uint32_t* w;
   uint64_t n;
   uint32_t ns;   // stores updated: 1 or 2
+  // fused tree prologue (PRO != 0 kernels): the trees the following tree call updates
+  TreeDev T[MAX_TREES];
+  uint32_t ntrees;
 };
+
+// The batch prologue of the tree call that follows (PRO 1: incremental, 2: decremental), run by
+// every thread of the mutation kernel after its own items: it reads no slab, so the insert /
+// delete and the tree seeding share one launch (tree_prologue_inc / _dec, tree_common.cuh).
+template <int PRO>
+__device__ __forceinline__ void upd_tree_prologue(const UpdArgs& A) {
+  __shared__ uint32_t s_ep[MAX_TREES];
+  if (threadIdx.x < A.ntrees) s_ep[threadIdx.x] = __ldcg(A.T[threadIdx.x].epoch_ptr);
+  __syncthreads();
+  uint32_t epoch[MAX_TREES];
+#pragma unroll
+  for (int k = 0; k < MAX_TREES; k++) epoch[k] = k < (int)A.ntrees ? s_ep[k] : 0u;
+  Counters c;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
+  if (PRO == 1) tree_prologue_inc<true>(A.G[0], A.T, A.ntrees, A.src, A.dst, A.w, A.n, epoch, tid, nt, c);
+  else tree_prologue_dec(A.G[0], A.T, A.ntrees, A.src, A.dst, A.n, tid, nt, c);
+  c.batch = 0;   // the tree call's alg_bytes then covers what its own kernel read
+  for (uint32_t k = 0; k < A.ntrees; k++) flush_counters(A.G[0], A.T[k], c, (int)k, false, 0, 0);
+}
 
 __device__ __forceinline__ void upd_item(const UpdArgs& A, uint64_t i, uint32_t& st, uint64_t& e) {
   st = A.ns == 2 ? (uint32_t)(i & 1) : 0u;
@@ -231,7 +254,8 @@ __device__ __forceinline__ void upd_item(const UpdArgs& A, uint64_t i, uint32_t&
 }
 
 // TRACK: the out store keeps update tracking (compiled out of the default kernels).
-template <bool MAP, bool TRACK>
+// PRO: 1 = also run the incremental tree prologue (upd_tree_prologue).
+template <bool MAP, bool TRACK, int PRO = 0>
 __global__ void __launch_bounds__(UPD_BLOCK) k_insert(const __grid_constant__ UpdArgs A) {
   const int lane = lane_id(), l8 = lane & 7, gbase = lane & 24;
   const uint32_t gmask = 0xFFu << gbase;
@@ -262,6 +286,7 @@ __global__ void __launch_bounds__(UPD_BLOCK) k_insert(const __grid_constant__ Up
     block_or_err(&A.G[k].ctrl->err, err[k]);
     block_add(&A.G[k].ctrl->n_inserted, &A.G[k].ctrl->ins_total, added[k]);
   }
+  if constexpr (PRO != 0) upd_tree_prologue<PRO>(A);
 }
 
 // ------------------------------------------------------------------ delete / query
@@ -312,7 +337,7 @@ __device__ int group_find(const GraphDev& G, uint32_t u, uint32_t v, int l8, uin
   }
 }
 
-template <bool MAP>
+template <bool MAP, int PRO = 0>
 __global__ void __launch_bounds__(UPD_BLOCK) k_delete(const __grid_constant__ UpdArgs A) {
   const int lane = lane_id(), l8 = lane & 7, gbase = lane & 24;
   const uint32_t gmask = 0xFFu << gbase;
@@ -342,6 +367,7 @@ __global__ void __launch_bounds__(UPD_BLOCK) k_delete(const __grid_constant__ Up
     block_or_err(&A.G[k].ctrl->err, err[k]);
     block_add(&A.G[k].ctrl->n_deleted, &A.G[k].ctrl->del_total, removed[k]);
   }
+  if constexpr (PRO != 0) upd_tree_prologue<PRO>(A);
 }
 
 template <bool MAP>
@@ -422,7 +448,7 @@ __global__ void __launch_bounds__(UPD_BLOCK) k_query_t(GraphDev G, const uint32_
 // edge reading whole slabs (8 x LDG.128 of one 128-B line): no group collectives and one divergent
 // path per edge.  Used for large batches (thread_upd).
 
-template <bool MAP, bool TRACK>
+template <bool MAP, bool TRACK, int PRO = 0>
 __global__ void __launch_bounds__(UPD_BLOCK) k_insert_t(const __grid_constant__ UpdArgs A) {
   uint32_t added[2] = {0, 0}, err[2] = {0, 0};
   const uint64_t total = A.n * A.ns;
@@ -450,9 +476,10 @@ __global__ void __launch_bounds__(UPD_BLOCK) k_insert_t(const __grid_constant__ 
     block_or_err(&A.G[k].ctrl->err, err[k]);
     block_add(&A.G[k].ctrl->n_inserted, &A.G[k].ctrl->ins_total, added[k]);
   }
+  if constexpr (PRO != 0) upd_tree_prologue<PRO>(A);
 }
 
-template <bool MAP>
+template <bool MAP, int PRO = 0>
 __global__ void __launch_bounds__(UPD_BLOCK) k_delete_t(const __grid_constant__ UpdArgs A) {
   uint32_t removed[2] = {0, 0}, err[2] = {0, 0};
   const uint64_t total = A.n * A.ns;
@@ -471,6 +498,7 @@ __global__ void __launch_bounds__(UPD_BLOCK) k_delete_t(const __grid_constant__ 
     block_or_err(&A.G[k].ctrl->err, err[k]);
     block_add(&A.G[k].ctrl->n_deleted, &A.G[k].ctrl->del_total, removed[k]);
   }
+  if constexpr (PRO != 0) upd_tree_prologue<PRO>(A);
 }
 
 // Kernel choice by batch size (measured): small batches are latency-bound and the
@@ -727,53 +755,70 @@ out:
   return e;
 }
 
+#define UPD_LAUNCH(K, grid_, A_) do { K<<<grid_, UPD_BLOCK, 0, g->stream>>>(A_); } while (0)
+
+template <bool MAP, bool TRACK>
+static void insert_kind(meerkat_graph* g, const UpdArgs& A, bool thread, unsigned grid) {
+  if (thread) {
+    if (A.ntrees) UPD_LAUNCH((k_insert_t<MAP, TRACK, 1>), grid, A);
+    else UPD_LAUNCH((k_insert_t<MAP, TRACK, 0>), grid, A);
+  } else {
+    if (A.ntrees) UPD_LAUNCH((k_insert<MAP, TRACK, 1>), grid, A);
+    else UPD_LAUNCH((k_insert<MAP, TRACK, 0>), grid, A);
+  }
+}
+
+template <bool MAP>
+static void delete_kind(meerkat_graph* g, const UpdArgs& A, bool thread, unsigned grid) {
+  if (thread) {
+    if (A.ntrees) UPD_LAUNCH((k_delete_t<MAP, 2>), grid, A);
+    else UPD_LAUNCH((k_delete_t<MAP, 0>), grid, A);
+  } else {
+    if (A.ntrees) UPD_LAUNCH((k_delete<MAP, 2>), grid, A);
+    else UPD_LAUNCH((k_delete<MAP, 0>), grid, A);
+  }
+}
+#undef UPD_LAUNCH
+
+static void set_pro(UpdArgs& A, const TreePro* pro) {
+  A.ntrees = pro ? pro->ntrees : 0u;
+  if (pro)
+    for (int k = 0; k < MAX_TREES; k++) A.T[k] = pro->T[k];
+}
+
 cudaError_t launch_insert(meerkat_graph* g, Store* st0, Store* st1, const uint32_t* s, const uint32_t* d,
-                          const uint32_t* w, uint64_t n) {
+                          const uint32_t* w, uint64_t n, const TreePro* pro) {
   if (!n) return cudaSuccess;
   UpdArgs A{};
   A.G[0] = st0->dev;
   if (st1) A.G[1] = st1->dev;
   A.src = s; A.dst = d; A.w = w; A.n = n; A.ns = st1 ? 2u : 1u;
-  if (thread_upd(n * A.ns)) {
-    const unsigned gt = grid_threads(g, n * A.ns);
-    if (A.G[0].upd) {
-      if (g->weighted) k_insert_t<true, true><<<gt, UPD_BLOCK, 0, g->stream>>>(A);
-      else k_insert_t<false, true><<<gt, UPD_BLOCK, 0, g->stream>>>(A);
-    } else {
-      if (g->weighted) k_insert_t<true, false><<<gt, UPD_BLOCK, 0, g->stream>>>(A);
-      else k_insert_t<false, false><<<gt, UPD_BLOCK, 0, g->stream>>>(A);
-    }
-    g->launches++;
-    return cudaGetLastError();
-  }
-  const unsigned gb = grid_for(g, n * A.ns, 0);
+  set_pro(A, pro);
+  const bool thread = thread_upd(n * A.ns);
+  const unsigned grid = thread ? grid_threads(g, n * A.ns) : grid_for(g, n * A.ns, 0);
   if (A.G[0].upd) {
-    if (g->weighted) k_insert<true, true><<<gb, UPD_BLOCK, 0, g->stream>>>(A);
-    else k_insert<false, true><<<gb, UPD_BLOCK, 0, g->stream>>>(A);
+    if (g->weighted) insert_kind<true, true>(g, A, thread, grid);
+    else insert_kind<false, true>(g, A, thread, grid);
   } else {
-    if (g->weighted) k_insert<true, false><<<gb, UPD_BLOCK, 0, g->stream>>>(A);
-    else k_insert<false, false><<<gb, UPD_BLOCK, 0, g->stream>>>(A);
+    if (g->weighted) insert_kind<true, false>(g, A, thread, grid);
+    else insert_kind<false, false>(g, A, thread, grid);
   }
   g->launches++;
   return cudaGetLastError();
 }
 
-cudaError_t launch_delete(meerkat_graph* g, Store* st0, Store* st1, const uint32_t* s, const uint32_t* d, uint64_t n) {
+cudaError_t launch_delete(meerkat_graph* g, Store* st0, Store* st1, const uint32_t* s, const uint32_t* d, uint64_t n,
+                          const TreePro* pro) {
   if (!n) return cudaSuccess;
   UpdArgs A{};
   A.G[0] = st0->dev;
   if (st1) A.G[1] = st1->dev;
   A.src = s; A.dst = d; A.w = nullptr; A.n = n; A.ns = st1 ? 2u : 1u;
-  if (thread_upd(n * A.ns)) {
-    const unsigned gt = grid_threads(g, n * A.ns);
-    if (g->weighted) k_delete_t<true><<<gt, UPD_BLOCK, 0, g->stream>>>(A);
-    else k_delete_t<false><<<gt, UPD_BLOCK, 0, g->stream>>>(A);
-    g->launches++;
-    return cudaGetLastError();
-  }
-  const unsigned gb = grid_for(g, n * A.ns, 0);
-  if (g->weighted) k_delete<true><<<gb, UPD_BLOCK, 0, g->stream>>>(A);
-  else k_delete<false><<<gb, UPD_BLOCK, 0, g->stream>>>(A);
+  set_pro(A, pro);
+  const bool thread = thread_upd(n * A.ns);
+  const unsigned grid = thread ? grid_threads(g, n * A.ns) : grid_for(g, n * A.ns, 0);
+  if (g->weighted) delete_kind<true>(g, A, thread, grid);
+  else delete_kind<false>(g, A, thread, grid);
   g->launches++;
   return cudaGetLastError();
 }

@@ -40,14 +40,23 @@
 namespace mk {
 
 // Next item of this group (grid-stride over [it, n)): vertex and slab come from the item.
-__device__ __forceinline__ bool fetch_item(const uint64_t* fr, uint64_t n, uint64_t& it, uint32_t& v, uint32_t& slab,
-                                           int l8, Counters& c) {
-  if (it >= n) return false;
-  const uint64_t item = fr[it];
-  v = (uint32_t)item;
-  slab = (uint32_t)(item >> 32);
-  if (l8 == 0) c.items++;
-  return true;
+// An item whose slab is LINKING was enqueued by the insert kernel's fused prologue before v's
+// lazy head existed: the head is read from vmeta now (the insert has completed); still none = no
+// out-edges, the item is skipped.
+__device__ __forceinline__ bool fetch_item(const GraphDev& S, const uint64_t* fr, uint64_t n, uint64_t& it,
+                                           uint64_t ng, uint32_t& v, uint32_t& slab, int l8, Counters& c) {
+  for (; it < n; it += ng) {
+    const uint64_t item = fr[it];
+    v = (uint32_t)item;
+    slab = (uint32_t)(item >> 32);
+    if (slab == LINKING) {
+      slab = __ldcg(&S.vmeta[v].x);
+      if (slab == INVALID_SLAB || slab == LINKING) continue;
+    }
+    if (l8 == 0) c.items++;
+    return true;
+  }
+  return false;
 }
 
 // Expand the frontier items [0, n) of `fr` (one 8-lane group per item) for tree T (index k),
@@ -70,7 +79,7 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const TreeDev& T, int 
   uint64_t it = BLOCK ? threadIdx.x / GROUP : ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / GROUP;
   uint32_t v = 0, slab = 0, du = 0;
   uint32_t b = 0, nb = 1, head0 = 0;   // IterationScheme1: bucket b of nb, first bucket head0
-  bool active = fetch_item(fr, n, it, v, slab, l8, c);
+  bool active = fetch_item(S, fr, n, it, ng, v, slab, l8, c);
   bool fresh = active;
   while (__any_sync(FULL, active)) {
     if (T.scheme1) {   // (uniform) one item per vertex: walk all its buckets in turn
@@ -224,7 +233,7 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const TreeDev& T, int 
     if (active) {
       if (nxt != INVALID_SLAB && !dead) slab = nxt;
       else if (T.scheme1 && !dead && b + 1 < nb) { b++; slab = head0 + b; }
-      else { it += ng; active = fetch_item(fr, n, it, v, slab, l8, c); fresh = active; }
+      else { it += ng; active = fetch_item(S, fr, n, it, ng, v, slab, l8, c); fresh = active; }
     }
   }
 }
@@ -361,62 +370,10 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_inc(const __grid_constan
   cg::grid_group grid = cg::this_grid();
   Counters c;
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
-  const uint64_t trips = (A.bn + nt - 1) / nt;   // warp-uniform trip count (warp_enqueue is collective)
-  for (uint64_t t = 0; t < trips; t++) {
-    const uint64_t i = tid + t * nt;
-    uint32_t u = 0, v = 0, w = 0;
-    bool ok = false;
-    if (i < A.bn) {
-      u = A.bs[i];
-      v = A.bd[i];
-      w = A.bw ? A.bw[i] : 1u;
-      c.batch++;
-      ok = u < A.G.V && v < A.G.V;   // invalid edges were skipped at insert too
-    }
-    // phase-wise over the trees: node[u] of every tree, then the atomicMins, then stamp + vmeta
-    uint64_t cand[MAX_TREES];
-    bool live[MAX_TREES];
-#pragma unroll
-    for (int k = 0; k < MAX_TREES; k++) {
-      const TreeDev& T = A.T[k];
-      const uint32_t wk = T.unit ? 1u : w;
-      live[k] = k < (int)A.ntrees && ok && (T.unit || (wk != 0 && wk < W_LIMIT));
-      cand[k] = live[k] ? ld_cg_u64(T.node + u) : UNREACHED;   // node[u], turned into the candidate below
-    }
-#pragma unroll
-    for (int k = 0; k < MAX_TREES; k++) {
-      const TreeDev& T = A.T[k];
-      if (live[k] && cand[k] != UNREACHED) {
-        const uint64_t dist = (cand[k] >> 32) + (T.unit ? 1u : w);
-        if (dist >= INF_DIST) { c.err |= ERR_OVERFLOW; live[k] = false; }   // C5
-        cand[k] = (dist << 32) | u;
-      } else {
-        live[k] = false;
-      }
-    }
-    unsigned long long old[MAX_TREES];
-#pragma unroll
-    for (int k = 0; k < MAX_TREES; k++)
-      old[k] = live[k] ? atomicMin(reinterpret_cast<unsigned long long*>(A.T[k].node + v),
-                                   (unsigned long long)cand[k]) : 0ull;
-    bool has[MAX_TREES][1];
-    uint2 m[MAX_TREES][1];
-#pragma unroll
-    for (int k = 0; k < MAX_TREES; k++) {
-      has[k][0] = false;
-      m[k][0] = make_uint2(INVALID_SLAB, 0);
-      if (live[k] && cand[k] < old[k]) {
-        c.improved++;
-        has[k][0] = atomicExch(A.T[k].stamp + v, epoch[k]) != epoch[k];
-        m[k][0] = __ldcg(A.G.vmeta + v);
-      }
-    }
-    const uint32_t xv[1] = {v};
-#pragma unroll
-    for (int k = 0; k < MAX_TREES; k++)
-      if (k < (int)A.ntrees) warp_enqueue_multi<1>(A.T[k], A.T[k].fr[0], &A.T[k].ctrl->size[0], has[k], xv, m[k], c);
+  if (!A.pro_done) {   // else the insert kernel ran it (meerkat_insert_batch_trees)
+    tree_prologue_inc<false>(A.G, A.T, A.ntrees, A.bs, A.bd, A.bw, A.bn, epoch, tid, nt, c);
+    grid.sync();
   }
-  grid.sync();
   timeline(A.T[0].ctrl);
   const uint32_t r = run_rounds<MAP, RELAX>(A, epoch, grid, 0, c);
   finish(A, c, epoch, tid == 0, r, r, 0);
@@ -518,41 +475,10 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_dec(const __grid_constan
   Counters c;
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
   // (i) Invalidate: deleted tree edges (parent(v), v), v != SRC (C4)
-  const uint64_t trips = (A.bn + nt - 1) / nt;
-  for (uint64_t t = 0; t < trips; t++) {
-    const uint64_t i = tid + t * nt;
-    uint32_t u = 0, v = 0;
-    bool ok = false;
-    if (i < A.bn) {
-      u = A.bs[i];
-      v = A.bd[i];
-      c.batch++;
-      ok = u < A.G.V && v < A.G.V;
-    }
-    // phase-wise over the trees: node[v] of every tree, then the CASes, then list + enqueue
-    uint64_t cur[MAX_TREES];
-#pragma unroll
-    for (int k = 0; k < MAX_TREES; k++)
-      cur[k] = (k < (int)A.ntrees && ok && v != A.T[k].source) ? ld_cg_u64(A.T[k].node + v) : UNREACHED;
-    bool has[MAX_TREES][1];
-    uint2 m[MAX_TREES][1];
-#pragma unroll
-    for (int k = 0; k < MAX_TREES; k++) {
-      has[k][0] = cur[k] != UNREACHED && (uint32_t)cur[k] == u &&
-                  atomicCAS(reinterpret_cast<unsigned long long*>(A.T[k].node + v), (unsigned long long)cur[k],
-                            (unsigned long long)UNREACHED) == cur[k];
-      m[k][0] = has[k][0] ? __ldcg(A.G.vmeta + v) : make_uint2(INVALID_SLAB, 0);
-      c.direct[k] += has[k][0];
-    }
-    const uint32_t xv[1] = {v};
-#pragma unroll
-    for (int k = 0; k < MAX_TREES; k++) {
-      if (k >= (int)A.ntrees) break;
-      warp_mark_invalid<1>(A.T[k], has[k], xv);
-      warp_enqueue_multi<1>(A.T[k], A.T[k].fr[0], &A.T[k].ctrl->size[0], has[k], xv, m[k], c);
-    }
+  if (!A.pro_done) {   // else the delete kernel ran it (meerkat_delete_batch_trees)
+    tree_prologue_dec(A.G, A.T, A.ntrees, A.bs, A.bd, A.bn, tid, nt, c);
+    grid.sync();
   }
-  grid.sync();
   timeline(A.T[0].ctrl);
   // (ii) PropagateInvalidation to all of T_v
   const uint32_t r1 = run_rounds<MAP, PROPAGATE>(A, epoch, grid, 0, c);
@@ -662,19 +588,30 @@ cudaError_t tree_occupancy(meerkat_graph* g) {
   return cudaSuccess;
 }
 
+void tree_pro_fill(meerkat_tree* const* trees, uint32_t ntrees, TreePro& p) {
+  p.ntrees = ntrees;
+  for (uint32_t k = 0; k < (uint32_t)MAX_TREES; k++) {
+    meerkat_tree* t = trees[k < ntrees ? k : 0];
+    p.T[k] = t->dev;
+    p.T[k].unit = t->unit ? 1u : 0u;
+    // control blocks alternate between calls: this call's was zeroed by the previous kernel
+    p.T[k].ctrl = t->ctrl_base + t->parity;
+  }
+}
+
 cudaError_t launch_tree(meerkat_graph* g, meerkat_tree* const* trees, uint32_t ntrees, int mode, const uint32_t* s,
-                        const uint32_t* d, const uint32_t* w, uint64_t n) {
+                        const uint32_t* d, const uint32_t* w, uint64_t n, bool pro_done) {
   if (ntrees == 0 || ntrees > (uint32_t)MAX_TREES) return cudaErrorInvalidValue;
-  TreeArgs A;
+  TreeArgs A{};
+  A.pro_done = pro_done ? 1u : 0u;
   A.G = g->out.dev;
   A.R = g->reverse ? g->in.dev : GraphDev{};
   A.ntrees = ntrees;
+  TreePro P;
+  tree_pro_fill(trees, ntrees, P);
   for (uint32_t k = 0; k < (uint32_t)MAX_TREES; k++) {
     meerkat_tree* t = trees[k < ntrees ? k : 0];
-    A.T[k] = t->dev;
-    A.T[k].unit = t->unit ? 1u : 0u;
-    // control blocks alternate between calls: this call's was zeroed by the previous kernel
-    A.T[k].ctrl = t->ctrl_base + t->parity;
+    A.T[k] = P.T[k];
     A.clear_ctrl[k] = k < ntrees ? t->ctrl_base + (1 - t->parity) : nullptr;
   }
   A.bs = s; A.bd = d; A.bw = w; A.bn = n;

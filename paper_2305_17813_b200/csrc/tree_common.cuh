@@ -31,6 +31,7 @@ struct TreeArgs {
   uint64_t bn;
   uint32_t weighted;    // graph has weights (map store)
   uint32_t filter_words;   // per tree
+  uint32_t pro_done;       // the batch prologue already ran in the mutation kernel (fused calls)
 };
 
 // Zero the next call's control block (block 0, after the last grid barrier).
@@ -227,6 +228,120 @@ __device__ __forceinline__ void flush_counters(const GraphDev& G, const TreeDev&
     else atomicOr(&G.ctrl->err, (unsigned int)acc[NV]);
   }
   if (rounds_owner) { tc->rounds = relax_rounds; tc->prop_rounds = prop_rounds; }
+}
+
+// ---- Per-batch-edge prologues of the incremental / decremental calls.  Neither reads a slab, so
+// besides opening k_tree_inc / k_tree_dec they also run inside the mutation kernel that applies
+// the batch (meerkat_insert_batch_trees / meerkat_delete_batch_trees), which takes one grid-wide
+// phase and barrier off the tree kernel.  The trip count is warp-uniform (warp_enqueue_multi is
+// collective); tid / nt are the calling kernel's thread index and thread count.
+
+// Incremental (P:113-133 for the relaxation): node[v] <- min(node[v], <d(u) + w, u>) for
+// every batch edge (u, v); an improved v is enqueued, de-duplicated by stamp, into the round-0
+// frontier fr[0] / size[0].  LAZY (running inside the insert kernel): v's lazy head slab (C22b)
+// may still be being linked by the same launch, so an improved v seen without a head is enqueued
+// as ONE item whose slab is LINKING — round 0 reads the head from vmeta when it fetches the item
+// (a lazily headed vertex has exactly one bucket).
+template <bool LAZY>
+__device__ __forceinline__ void tree_prologue_inc(const GraphDev& G, const TreeDev (&T)[MAX_TREES], uint32_t ntrees,
+                                                  const uint32_t* bs, const uint32_t* bd, const uint32_t* bw,
+                                                  uint64_t bn, const uint32_t (&epoch)[MAX_TREES], uint64_t tid,
+                                                  uint64_t nt, Counters& c) {
+  const uint64_t trips = (bn + nt - 1) / nt;
+  for (uint64_t t = 0; t < trips; t++) {
+    const uint64_t i = tid + t * nt;
+    uint32_t u = 0, v = 0, w = 0;
+    bool ok = false;
+    if (i < bn) {
+      u = bs[i];
+      v = bd[i];
+      w = bw ? bw[i] : 1u;
+      c.batch++;
+      ok = u < G.V && v < G.V;   // invalid edges were skipped by the insert too
+    }
+    // phase-wise over the trees: node[u] of every tree, then the atomicMins, then stamp + vmeta
+    uint64_t cand[MAX_TREES];
+    bool live[MAX_TREES];
+#pragma unroll
+    for (int k = 0; k < MAX_TREES; k++) {
+      const uint32_t wk = T[k].unit ? 1u : w;
+      live[k] = k < (int)ntrees && ok && (T[k].unit || (wk != 0 && wk < W_LIMIT));
+      cand[k] = live[k] ? ld_cg_u64(T[k].node + u) : UNREACHED;   // node[u], turned into the candidate below
+    }
+#pragma unroll
+    for (int k = 0; k < MAX_TREES; k++) {
+      if (live[k] && cand[k] != UNREACHED) {
+        const uint64_t dist = (cand[k] >> 32) + (T[k].unit ? 1u : w);
+        if (dist >= INF_DIST) { c.err |= ERR_OVERFLOW; live[k] = false; }   // C5
+        cand[k] = (dist << 32) | u;
+      } else {
+        live[k] = false;
+      }
+    }
+    unsigned long long old[MAX_TREES];
+#pragma unroll
+    for (int k = 0; k < MAX_TREES; k++)
+      old[k] = live[k] ? atomicMin(reinterpret_cast<unsigned long long*>(T[k].node + v), (unsigned long long)cand[k])
+                       : 0ull;
+    bool has[MAX_TREES][1];
+    uint2 m[MAX_TREES][1];
+#pragma unroll
+    for (int k = 0; k < MAX_TREES; k++) {
+      has[k][0] = false;
+      m[k][0] = make_uint2(INVALID_SLAB, 0);
+      if (live[k] && cand[k] < old[k]) {
+        c.improved++;
+        has[k][0] = atomicExch(T[k].stamp + v, epoch[k]) != epoch[k];
+        m[k][0] = __ldcg(G.vmeta + v);
+        if (LAZY && (m[k][0].x == INVALID_SLAB || m[k][0].x == LINKING)) m[k][0] = make_uint2(LINKING, 1u);
+      }
+    }
+    const uint32_t xv[1] = {v};
+#pragma unroll
+    for (int k = 0; k < MAX_TREES; k++)
+      if (k < (int)ntrees) warp_enqueue_multi<1>(T[k], T[k].fr[0], &T[k].ctrl->size[0], has[k], xv, m[k], c);
+  }
+}
+
+// Decremental (C4): a deleted tree edge (parent(v), v), v != SRC, invalidates v (CAS
+// to UNREACHED), marks it in V_invalid and enqueues it into the propagation frontier fr[0].
+__device__ __forceinline__ void tree_prologue_dec(const GraphDev& G, const TreeDev (&T)[MAX_TREES], uint32_t ntrees,
+                                                  const uint32_t* bs, const uint32_t* bd, uint64_t bn, uint64_t tid,
+                                                  uint64_t nt, Counters& c) {
+  const uint64_t trips = (bn + nt - 1) / nt;
+  for (uint64_t t = 0; t < trips; t++) {
+    const uint64_t i = tid + t * nt;
+    uint32_t u = 0, v = 0;
+    bool ok = false;
+    if (i < bn) {
+      u = bs[i];
+      v = bd[i];
+      c.batch++;
+      ok = u < G.V && v < G.V;
+    }
+    // phase-wise over the trees: node[v] of every tree, then the CASes, then list + enqueue
+    uint64_t cur[MAX_TREES];
+#pragma unroll
+    for (int k = 0; k < MAX_TREES; k++)
+      cur[k] = (k < (int)ntrees && ok && v != T[k].source) ? ld_cg_u64(T[k].node + v) : UNREACHED;
+    bool has[MAX_TREES][1];
+    uint2 m[MAX_TREES][1];
+#pragma unroll
+    for (int k = 0; k < MAX_TREES; k++) {
+      has[k][0] = cur[k] != UNREACHED && (uint32_t)cur[k] == u &&
+                  atomicCAS(reinterpret_cast<unsigned long long*>(T[k].node + v), (unsigned long long)cur[k],
+                            (unsigned long long)UNREACHED) == cur[k];
+      m[k][0] = has[k][0] ? __ldcg(G.vmeta + v) : make_uint2(INVALID_SLAB, 0);
+      c.direct[k] += has[k][0];
+    }
+    const uint32_t xv[1] = {v};
+#pragma unroll
+    for (int k = 0; k < MAX_TREES; k++) {
+      if (k >= (int)ntrees) break;
+      warp_mark_invalid<1>(T[k], has[k], xv);
+      warp_enqueue_multi<1>(T[k], T[k].fr[0], &T[k].ctrl->size[0], has[k], xv, m[k], c);
+    }
+  }
 }
 
 // Blocked two-bit Bloom filter of V_invalid in shared memory: one word per key, two bits within

@@ -99,25 +99,41 @@ class Graph:
         check(_lib.lib().meerkat_sync(self._h), "meerkat_sync")
 
     # ------------------------------------------------------------------ batches
-    def insert(self, src, dst, w=None, count: bool = True, raise_on_error: bool = True):
+    def insert(self, src, dst, w=None, count: bool = True, raise_on_error: bool = True, seed=None):
+        """InsertEdges.  seed: trees whose next incremental call (same batch) this insert seeds
+        (meerkat_insert_batch_trees)."""
         sp, ks, n = _u32(src)
         dp, kd, n2 = _u32(dst)
         wp, kw, n3 = _u32(w)
         assert n == n2 and (w is None or n3 == n)
         out = ctypes.c_uint64(0)
-        st = _lib.lib().meerkat_insert_batch(self._h, sp, dp, wp, n, ctypes.byref(out) if count else None)
+        ob = ctypes.byref(out) if count else None
+        if seed:
+            arr = (ctypes.c_void_p * len(seed))(*[t._h.value for t in seed])
+            st, fn = _lib.lib().meerkat_insert_batch_trees(self._h, sp, dp, wp, n, arr, len(seed), ob), \
+                "meerkat_insert_batch_trees"
+        else:
+            st, fn = _lib.lib().meerkat_insert_batch(self._h, sp, dp, wp, n, ob), "meerkat_insert_batch"
         if raise_on_error:
-            check(st, "meerkat_insert_batch")
+            check(st, fn)
         return (int(out.value) if count else None) if raise_on_error else (st, int(out.value))
 
-    def delete(self, src, dst, count: bool = True, raise_on_error: bool = True):
+    def delete(self, src, dst, count: bool = True, raise_on_error: bool = True, seed=None):
+        """DeleteEdges.  seed: trees whose next decremental call (same batch) this delete seeds
+        (meerkat_delete_batch_trees)."""
         sp, ks, n = _u32(src)
         dp, kd, n2 = _u32(dst)
         assert n == n2
         out = ctypes.c_uint64(0)
-        st = _lib.lib().meerkat_delete_batch(self._h, sp, dp, n, ctypes.byref(out) if count else None)
+        ob = ctypes.byref(out) if count else None
+        if seed:
+            arr = (ctypes.c_void_p * len(seed))(*[t._h.value for t in seed])
+            st, fn = _lib.lib().meerkat_delete_batch_trees(self._h, sp, dp, n, arr, len(seed), ob), \
+                "meerkat_delete_batch_trees"
+        else:
+            st, fn = _lib.lib().meerkat_delete_batch(self._h, sp, dp, n, ob), "meerkat_delete_batch"
         if raise_on_error:
-            check(st, "meerkat_delete_batch")
+            check(st, fn)
         return (int(out.value) if count else None) if raise_on_error else (st, int(out.value))
 
     def query(self, src, dst, raise_on_error: bool = True):
@@ -182,6 +198,20 @@ class Graph:
         dp, kd, _ = _u32(dst)
         arr = (ctypes.c_void_p * len(trees))(*[t._h.value for t in trees])
         check(_lib.lib().meerkat_trees_decremental(self._h, arr, len(trees), sp, dp, n), "meerkat_trees_decremental")
+
+    def insert_trees(self, trees, src, dst, w=None, count: bool = True):
+        """insert(seed=trees) + trees_incremental(trees): two launches, the trees' batch prologue
+        inside the insert kernel.  Returns the number of edges inserted (count=True)."""
+        n = self.insert(src, dst, w, count=count, seed=trees)
+        self.trees_incremental(trees, src, dst, w)
+        return n
+
+    def delete_trees(self, trees, src, dst, count: bool = True):
+        """delete(seed=trees) + trees_decremental(trees): two launches, the invalidation of the
+        deleted tree edges inside the delete kernel.  Returns the number deleted (count=True)."""
+        n = self.delete(src, dst, count=count, seed=trees)
+        self.trees_decremental(trees, src, dst)
+        return n
 
     def pagerank(self, damping: float = 0.85, error_margin: float = 1e-5, max_iter: int = 1000) -> "PageRank":
         """Static PageRank of the current graph (needs reverse=True: in-edge mirror)."""

@@ -305,3 +305,129 @@ def test_host_batches_staged_once_and_reused():
                 g.trees_decremental([sp, bf], bs, bd)
         assert_nodes(sp.nodes(), o.sssp(0)[1], f"sssp step {step}")
         assert_nodes(bf.nodes(), o.bfs(0)[1], f"bfs step {step}")
+
+
+@pytest.mark.parametrize("reverse,hashing,thread", [(False, True, "0"), (True, True, "0"), (True, True, "1"),
+                                                    (False, False, "1")])
+def test_batch_trees_match_oracle(reverse, hashing, thread, monkeypatch):
+    """meerkat_insert_batch_trees / meerkat_delete_batch_trees: the trees' batch prologue runs
+    inside the insert / delete kernel (both kernel kinds); nodes, invalidated sets, direct counts
+    and frontier sizes must equal the oracle's, and the mutation counts insert / delete's."""
+    monkeypatch.setenv("MEERKAT_THREAD_UPD", thread)
+    W = synth.rmat_dynamic(15, 16, batch=2000, n_ins=3, n_del=3)
+    V, src = W.vertex_n, W.source
+    bs, bd, bw = W.base
+    g = G(V, weighted=True, hashing=hashing, degree_hints=synth.degrees(bs, V), reverse=reverse,
+          in_degree_hints=synth.degrees(bd, V))
+    o = oracle.OracleGraph(V)
+    g.insert(cuda(bs), cuda(bd), cuda(bw)); o.insert(bs, bd, bw)
+    t, b = g.sssp(src), g.bfs(src)
+    for (s, d, w) in W.inserts:
+        before = len(o.edges()[0])
+        o.insert(s, d, w)
+        n_ins = g.insert_trees([t, b], cuda(s), cuda(d), cuda(w))
+        assert n_ins == len(o.edges()[0]) - before
+        assert_nodes(t.nodes(), o.sssp(src)[1], "batch_trees inc sssp")
+        assert_nodes(b.nodes(), o.bfs(src)[1], "batch_trees inc bfs")
+    for (s, d, _w) in W.deletes:
+        old_s, old_b = o.sssp(src)[1], o.bfs(src)[1]
+        before = len(o.edges()[0])
+        o.delete(s, d)
+        n_del = g.delete_trees([t, b], cuda(s), cuda(d))
+        assert n_del == before - len(o.edges()[0])
+        for tree, old in ((t, old_s), (b, old_b)):
+            flag, nd = oracle.invalidated(V, src, old, s, d)
+            st = tree.stats()
+            assert tree.invalidated().tolist() == np.nonzero(flag)[0].tolist()
+            assert st["direct_invalid"] == nd
+            assert st["frontier_edges"] == o.dec_frontier_count(old, flag)
+        assert_nodes(t.nodes(), o.sssp(src)[1], "batch_trees dec sssp")
+        assert_nodes(b.nodes(), o.bfs(src)[1], "batch_trees dec bfs")
+    # a single tree, mixed with the separate calls, keeps the version contract
+    s, d, w = W.inserts[1]
+    o.delete(s, d)
+    g.delete_trees([t], cuda(s), cuda(d))
+    b_nodes_stale = b.nodes()
+    from paper_2305_17813_b200 import MeerkatError, _lib
+    with pytest.raises(MeerkatError) as e:   # b missed the last batch: not current
+        g.insert_trees([b], cuda(s), cuda(d), cuda(w))
+    assert e.value.status == _lib.E_STATE
+    b.decremental(cuda(s), cuda(d))
+    assert_nodes(t.nodes(), o.sssp(src)[1], "single-tree delete_trees")
+    assert_nodes(b.nodes(), o.bfs(src)[1], "per-tree after batch_trees")
+    assert b_nodes_stale.shape == b.nodes().shape
+
+
+@pytest.mark.parametrize("thread", ["0", "1"])
+def test_batch_trees_lazy_heads(thread, monkeypatch):
+    """Vertices with degree hint 0 get their head slab lazily (C22b) from the very insert kernel
+    that runs the fused prologue: a vertex improved before its head exists is enqueued with the
+    LINKING marker and resolved at round 0.  Chains through such vertices must come out exact."""
+    monkeypatch.setenv("MEERKAT_THREAD_UPD", thread)
+    rng = np.random.default_rng(5)
+    V = 4096
+    for rep in range(4):
+        g = G(V, weighted=True, degree_hints=np.zeros(V, np.uint32), reverse=bool(rep & 1),
+              in_degree_hints=np.zeros(V, np.uint32))
+        o = oracle.OracleGraph(V)
+        s0 = np.array([0], np.uint32); d0 = np.array([1], np.uint32); w0 = np.array([1], np.uint32)
+        g.insert(s0, d0, w0); o.insert(s0, d0, w0)
+        t, b = g.sssp(0), g.bfs(0)
+        # long chains 1 -> p1 -> p2 ... over fresh (headless) vertices plus random extra edges
+        perm = rng.permutation(np.arange(2, V)).astype(np.uint32)
+        chain = np.concatenate([[1], perm[:1500]]).astype(np.uint32)
+        cs, cd = chain[:-1], chain[1:]
+        xs = rng.integers(0, V, 3000).astype(np.uint32); xd = rng.integers(0, V, 3000).astype(np.uint32)
+        s = np.concatenate([cs, xs]); d = np.concatenate([cd, xd])
+        w = rng.integers(1, 9, len(s)).astype(np.uint32)
+        order = rng.permutation(len(s))
+        s, d, w = s[order], d[order], w[order]
+        o.insert(s, d, w)
+        g.insert_trees([t, b], cuda(s), cuda(d), cuda(w))
+        assert_nodes(t.nodes(), o.sssp(0)[1], f"lazy sssp rep {rep}")
+        assert_nodes(b.nodes(), o.bfs(0)[1], f"lazy bfs rep {rep}")
+        assert g.check()[0] == 0
+
+
+def test_seed_contract():
+    """insert / delete with seed=trees: the following tree call may name a subset of the seeded
+    trees (each later call completes its own seed), never a mix of seeded and unseeded trees; a
+    static recompute drops an unused seed (its frontier, counters and V_invalid marks)."""
+    from paper_2305_17813_b200 import MeerkatError, _lib
+    W = synth.rmat_dynamic(12, 8, batch=300, n_ins=3, n_del=2)
+    V, src = W.vertex_n, W.source
+    bs, bd, bw = W.base
+    g = G(V, weighted=True, degree_hints=synth.degrees(bs, V), reverse=True, in_degree_hints=synth.degrees(bd, V))
+    o = oracle.OracleGraph(V)
+    g.insert(cuda(bs), cuda(bd), cuda(bw)); o.insert(bs, bd, bw)
+    t, b = g.sssp(src), g.bfs(src)
+    s, d, w = (cuda(x) for x in W.inserts[0])
+    g.insert(s, d, w, seed=[t, b]); o.insert(*W.inserts[0])
+    t.incremental(s, d, w)          # each seeded tree completes its own seed
+    b.incremental(s, d)
+    assert_nodes(t.nodes(), o.sssp(src)[1], "seed split sssp")
+    assert_nodes(b.nodes(), o.bfs(src)[1], "seed split bfs")
+    s, d = (cuda(x) for x in W.deletes[0][:2])
+    g.delete(s, d, seed=[t]); o.delete(*W.deletes[0][:2])
+    with pytest.raises(MeerkatError) as e:   # seeded + unseeded in one fused call
+        g.trees_decremental([t, b], s, d)
+    assert e.value.status == _lib.E_STATE
+    with pytest.raises(MeerkatError) as e:   # already seeded
+        g.insert(*(cuda(x) for x in W.inserts[1]), seed=[t])
+    assert e.value.status == _lib.E_STATE
+    g.trees_decremental([t], s, d)
+    b.decremental(s, d)
+    assert_nodes(t.nodes(), o.sssp(src)[1], "seeded dec sssp")
+    assert_nodes(b.nodes(), o.bfs(src)[1], "unseeded dec bfs")
+    # an unused seed (the trees never followed this delete), then another mutation: recompute drops it
+    s, d = (cuda(x) for x in W.deletes[1][:2])
+    g.delete(s, d, seed=[t, b]); o.delete(*W.deletes[1][:2])
+    s, d, w = (cuda(x) for x in W.inserts[2])
+    g.insert(s, d, w); o.insert(*W.inserts[2])
+    t.recompute(); b.recompute()
+    assert_nodes(t.nodes(), o.sssp(src)[1], "recompute after unused seed")
+    assert_nodes(b.nodes(), o.bfs(src)[1], "recompute after unused seed (bfs)")
+    s, d = (cuda(x) for x in W.inserts[2][:2])
+    g.delete_trees([t, b], s, d); o.delete(*W.inserts[2][:2])
+    assert_nodes(t.nodes(), o.sssp(src)[1], "batch_trees after recompute")
+    assert_nodes(b.nodes(), o.bfs(src)[1], "batch_trees after recompute (bfs)")
