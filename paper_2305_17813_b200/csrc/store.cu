@@ -212,6 +212,13 @@ __device__ int group_insert(const GraphDev& G, uint32_t u, uint32_t v, uint32_t 
 }
 
 constexpr int UPD_BLOCK = 256;
+// The group update kernels are compiled for 8 resident 256-thread blocks per SM (32 registers):
+// at 40 registers only 6 fit, and the 100 K-edge batches' 1184 blocks ran in 1.3 waves.  Measured
+// (same box, 3 x 2 runs): seeded insert 93 -> 87 us, step 0.356 -> 0.348 ms.
+#ifndef MEERKAT_UPD_MINB
+#define MEERKAT_UPD_MINB 8
+#endif
+constexpr int UPD_MINB = MEERKAT_UPD_MINB;
 
 // Update kernels serve the out-edge store and, when the graph keeps one, the in-edge
 // mirror in ONE launch: item i < ns*n is edge i/ns of the batch applied to store i%ns
@@ -256,7 +263,7 @@ __device__ __forceinline__ void upd_item(const UpdArgs& A, uint64_t i, uint32_t&
 // TRACK: the out store keeps update tracking (compiled out of the default kernels).
 // PRO: 1 = also run the incremental tree prologue (upd_tree_prologue).
 template <bool MAP, bool TRACK, int PRO = 0>
-__global__ void __launch_bounds__(UPD_BLOCK) k_insert(const __grid_constant__ UpdArgs A) {
+__global__ void __launch_bounds__(UPD_BLOCK, UPD_MINB) k_insert(const __grid_constant__ UpdArgs A) {
   const int lane = lane_id(), l8 = lane & 7, gbase = lane & 24;
   const uint32_t gmask = 0xFFu << gbase;
   const uint64_t ng = ((uint64_t)gridDim.x * blockDim.x) / GROUP;
@@ -338,7 +345,7 @@ __device__ int group_find(const GraphDev& G, uint32_t u, uint32_t v, int l8, uin
 }
 
 template <bool MAP, int PRO = 0>
-__global__ void __launch_bounds__(UPD_BLOCK) k_delete(const __grid_constant__ UpdArgs A) {
+__global__ void __launch_bounds__(UPD_BLOCK, UPD_MINB) k_delete(const __grid_constant__ UpdArgs A) {
   const int lane = lane_id(), l8 = lane & 7, gbase = lane & 24;
   const uint32_t gmask = 0xFFu << gbase;
   const uint64_t ng = ((uint64_t)gridDim.x * blockDim.x) / GROUP;
@@ -371,7 +378,7 @@ __global__ void __launch_bounds__(UPD_BLOCK) k_delete(const __grid_constant__ Up
 }
 
 template <bool MAP>
-__global__ void __launch_bounds__(UPD_BLOCK) k_query(GraphDev G, const uint32_t* __restrict__ src,
+__global__ void __launch_bounds__(UPD_BLOCK, UPD_MINB) k_query(GraphDev G, const uint32_t* __restrict__ src,
                                                      const uint32_t* __restrict__ dst, uint64_t n,
                                                      uint8_t* __restrict__ found, uint32_t* __restrict__ w_out) {
   const int lane = lane_id(), l8 = lane & 7, gbase = lane & 24;

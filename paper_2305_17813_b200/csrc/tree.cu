@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_static(const __grid_cons
 // ------------------------------------------------------------------ incremental
 
 template <bool MAP>
-__global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_inc(const __grid_constant__ TreeArgs A) {
+__global__ void __launch_bounds__(TREE_BLOCK, TREE_MINB) k_tree_inc(const __grid_constant__ TreeArgs A) {
   uint32_t epoch[MAX_TREES];
   load_epochs(A, epoch);
   timeline(A.T[0].ctrl);
@@ -466,7 +466,7 @@ __device__ __forceinline__ void dec_scan(const TreeArgs& A, const uint32_t* filt
 }
 
 template <bool MAP>
-__global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_dec(const __grid_constant__ TreeArgs A) {
+__global__ void __launch_bounds__(TREE_BLOCK, TREE_MINB) k_tree_dec(const __grid_constant__ TreeArgs A) {
   extern __shared__ uint32_t filt[];
   uint32_t epoch[MAX_TREES];
   load_epochs(A, epoch);

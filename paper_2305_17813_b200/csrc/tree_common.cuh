@@ -10,6 +10,10 @@ namespace cg = cooperative_groups;
 namespace mk {
 
 constexpr int TREE_BLOCK = 512;
+#ifndef MEERKAT_TREE_MINB
+#define MEERKAT_TREE_MINB 2   // resident blocks per SM the dynamic tree kernels are compiled for (A/B)
+#endif
+constexpr int TREE_MINB = MEERKAT_TREE_MINB;
 constexpr int FILTER_LOG2 = 14;
 constexpr int FILTER_WORDS = 1 << FILTER_LOG2;   // 64 KiB smem Bloom filter per block (decremental scan)
 constexpr int SCAN_UNROLL = 2;        // independent slabs in flight per group in the scan
