@@ -218,6 +218,13 @@ constexpr int UPD_BLOCK = 256;
 #ifndef MEERKAT_UPD_MINB
 #define MEERKAT_UPD_MINB 8
 #endif
+// The thread-per-edge kernels (large batches) at 4 blocks per SM (<= 64 registers; k_delete_t used
+// 72): config-4 insert of 970 K edges 0.570 -> 0.496 ms, 1 M-edge sweep insert 0.21 -> 0.16 ms;
+// 8 blocks per SM (32 registers) spilled and was slower (same box, tools/gpu/r01_ab_tminb.sh).
+#ifndef MEERKAT_UPD_T_MINB
+#define MEERKAT_UPD_T_MINB 4
+#endif
+constexpr int UPD_T_MINB = MEERKAT_UPD_T_MINB;
 constexpr int UPD_MINB = MEERKAT_UPD_MINB;
 
 // Update kernels serve the out-edge store and, when the graph keeps one, the in-edge
@@ -406,7 +413,7 @@ __global__ void __launch_bounds__(UPD_BLOCK, UPD_MINB) k_query(GraphDev G, const
 // One thread per edge reads whole slabs itself (8 x LDG.128 of the same 128-B line): no group
 // collectives, one divergent path per edge instead of four per warp (large batches, see thread_upd).
 template <bool MAP>
-__global__ void __launch_bounds__(UPD_BLOCK) k_query_t(GraphDev G, const uint32_t* __restrict__ src,
+__global__ void __launch_bounds__(UPD_BLOCK, UPD_T_MINB) k_query_t(GraphDev G, const uint32_t* __restrict__ src,
                                                        const uint32_t* __restrict__ dst, uint64_t n,
                                                        uint8_t* __restrict__ found, uint32_t* __restrict__ w_out) {
   using F = Frag<MAP>;
@@ -456,7 +463,7 @@ __global__ void __launch_bounds__(UPD_BLOCK) k_query_t(GraphDev G, const uint32_
 // path per edge.  Used for large batches (thread_upd).
 
 template <bool MAP, bool TRACK, int PRO = 0>
-__global__ void __launch_bounds__(UPD_BLOCK) k_insert_t(const __grid_constant__ UpdArgs A) {
+__global__ void __launch_bounds__(UPD_BLOCK, UPD_T_MINB) k_insert_t(const __grid_constant__ UpdArgs A) {
   uint32_t added[2] = {0, 0}, err[2] = {0, 0};
   const uint64_t total = A.n * A.ns;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -487,7 +494,7 @@ __global__ void __launch_bounds__(UPD_BLOCK) k_insert_t(const __grid_constant__ 
 }
 
 template <bool MAP, int PRO = 0>
-__global__ void __launch_bounds__(UPD_BLOCK) k_delete_t(const __grid_constant__ UpdArgs A) {
+__global__ void __launch_bounds__(UPD_BLOCK, UPD_T_MINB) k_delete_t(const __grid_constant__ UpdArgs A) {
   uint32_t removed[2] = {0, 0}, err[2] = {0, 0};
   const uint64_t total = A.n * A.ns;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
