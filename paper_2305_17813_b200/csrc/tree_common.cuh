@@ -19,7 +19,10 @@ constexpr int FILTER_WORDS = 1 << FILTER_LOG2;   // 64 KiB smem Bloom filter per
 constexpr int SCAN_UNROLL = 2;        // independent slabs in flight per group in the scan
 constexpr unsigned FULL = 0xFFFFFFFFu;
 constexpr uint64_t PROBE_MIN_ITEMS = 65536;
-constexpr uint64_t TAIL_ITEMS = 64;          // frontiers this small run in block 0 alone (run_rounds)  // frontiers at least this large probe node[x] before the atomic
+#ifndef MEERKAT_TAIL_ITEMS
+#define MEERKAT_TAIL_ITEMS 64
+#endif
+constexpr uint64_t TAIL_ITEMS = MEERKAT_TAIL_ITEMS;   // frontiers this small run in block 0 alone (run_rounds)
 
 enum Visit { RELAX = 0, PROPAGATE = 1, PULL = 2 };
 
