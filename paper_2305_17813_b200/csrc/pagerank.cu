@@ -34,6 +34,10 @@ namespace cg = cooperative_groups;
 namespace mk {
 
 constexpr int PR_BLOCK = 512;
+#ifndef MEERKAT_PR_MINB
+#define MEERKAT_PR_MINB 2   // resident blocks per SM k_pagerank is compiled for (A/B)
+#endif
+constexpr int PR_MINB = MEERKAT_PR_MINB;
 constexpr int PR_UNROLL = 2;   // slabs in flight per group (register double-buffered)
 
 struct PRArgs {
@@ -152,7 +156,7 @@ __device__ __forceinline__ void pr_accumulate(const PRArgs& A, uint32_t n_slabs,
 }
 
 template <bool MAP>
-__global__ void __launch_bounds__(PR_BLOCK, 2) k_pagerank(const __grid_constant__ PRArgs A) {
+__global__ void __launch_bounds__(PR_BLOCK, PR_MINB) k_pagerank(const __grid_constant__ PRArgs A) {
   cg::grid_group grid = cg::this_grid();
   PRCtrl* C = A.ctrl;
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
