@@ -58,6 +58,9 @@ def test_null_args_rejected(lib):
     assert lib.meerkat_create(None, None) == _lib.E_INVALID_ARG
     assert lib.meerkat_destroy(None) == _lib.E_INVALID_ARG
     assert lib.meerkat_insert_batch(None, None, None, None, 0, None) == _lib.E_INVALID_ARG
+    # seeding mutations: a null graph is rejected before any tree or CUDA state is touched
+    assert lib.meerkat_insert_batch_trees(None, None, None, None, 0, None, 0, None) == _lib.E_INVALID_ARG
+    assert lib.meerkat_delete_batch_trees(None, None, None, 0, None, 0, None) == _lib.E_INVALID_ARG
     cfg = _lib.Config(vertex_n=0)
     h = ctypes.c_void_p()
     assert lib.meerkat_create(ctypes.byref(cfg), ctypes.byref(h)) == _lib.E_INVALID_ARG
