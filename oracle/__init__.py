@@ -52,8 +52,6 @@ def _L():
         L.orc_delete.argtypes = [vp, u32p, u32p, ctypes.c_uint64, u64p]
         L.orc_query.argtypes = [vp, u32p, u32p, ctypes.c_uint64, u8p, u32p]
         L.orc_export.argtypes = [vp, u32p, u32p, u32p]
-        L.orc_out_degree.restype = ctypes.c_uint32
-        L.orc_out_degree.argtypes = [vp, ctypes.c_uint32]
         L.orc_sssp.argtypes = [vp, ctypes.c_uint32, ctypes.c_int, u64p]
         L.orc_bfs.argtypes = [vp, ctypes.c_uint32, u64p]
         L.orc_invalidated.restype = ctypes.c_uint64
@@ -125,9 +123,6 @@ class OracleGraph:
         s = np.empty(m, np.uint32); d = np.empty(m, np.uint32); w = np.empty(m, np.uint32)
         _L().orc_export(self._g, _p(s, u32p), _p(d, u32p), _p(w, u32p))
         return s, d, w
-
-    def out_degree(self, v: int) -> int:
-        return int(_L().orc_out_degree(self._g, v))
 
     def sssp(self, source: int, unit: bool = False):
         node = np.empty(self.V, np.uint64)

@@ -171,15 +171,6 @@ void orc_export(const orc_graph* g, uint32_t* src, uint32_t* dst, uint32_t* w) {
   }
 }
 
-uint32_t orc_out_degree(const orc_graph* g, uint32_t v) {
-  uint32_t c = 0;
-  int64_t lo = 0, hi = (int64_t)g->m;
-  uint64_t k = (uint64_t)v << 32;
-  while (lo < hi) { int64_t mid = (lo + hi) / 2; if (g->key[mid] < k) lo = mid + 1; else hi = mid; }
-  for (uint64_t i = (uint64_t)lo; i < g->m && (g->key[i] >> 32) == v; i++) c++;
-  return c;
-}
-
 /* CSR row offsets of the sorted key array: edges of u are [off[u], off[u+1]). */
 static uint64_t* row_offsets(const orc_graph* g) {
   uint64_t* off = (uint64_t*)calloc((size_t)g->V + 1, sizeof(uint64_t));

@@ -56,6 +56,53 @@ def test_golden_g0(golden_dir):
             assert [hex(int(x)) for x in node] == step["packed"]
 
 
+def test_golden_unreached_sources(golden_dir):
+    """Frontier edges start in V_valid only (P:156-158 with P:53-60's V_unreachable): edges from
+    unreachable vertices into V_invalid are not counted (tests/golden/g1_unreached.json)."""
+    G = json.load(open(os.path.join(golden_dir, "g1_unreached.json")))
+    n, src = G["vertex_n"], G["source"]
+    g = _mk(n, G["edges"])
+    st, node = g.sssp(src)
+    assert st == 0 and _pairs(node) == G["static_sssp"]
+    for step in G["steps"]:
+        old = node.copy()
+        s, d = zip(*step["edges"])
+        g.delete(s, d)
+        flag, _ = oracle.invalidated(n, src, old, s, d)
+        assert sorted(np.nonzero(flag)[0].tolist()) == step["invalid"]
+        assert g.dec_frontier_count(old, flag) == len(step["frontier"]), step["note"]
+        st, node = g.sssp(src)
+        assert _pairs(node) == step["sssp"], step["note"]
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_dec_frontier_count_by_reachability(seed):
+    """dec_frontier_count = |{(u, x) in E_new : u in V_valid, x in V_invalid}| with V_valid taken
+    as the vertices REACHABLE from SRC in the old graph (a plain graph search over the old edge
+    list) that are not invalidated — a route independent of the oracle's packed nodes.
+    Sparse random graphs so that unreachable vertices with edges into V_invalid are common."""
+    rng = random.Random(1000 + seed)
+    n = rng.randint(4, 12)
+    E = refsim.random_graph(rng, n, rng.randint(n // 2, 2 * n), 8)
+    src = 0
+    g = _mk(n, [(u, v, w) for (u, v), w in E.items()])
+    _, old = g.sssp(src)
+    reach, stack = {src}, [src]
+    while stack:
+        u = stack.pop()
+        for (a, b) in E:
+            if a == u and b not in reach:
+                reach.add(b)
+                stack.append(b)
+    batch = rng.sample(sorted(E), rng.randint(1, len(E)))
+    g.delete(*zip(*batch))
+    for k in batch:
+        E.pop(k)
+    flag, _ = oracle.invalidated(n, src, old, *zip(*batch))
+    want = sum(1 for (u, x) in E if u in reach and not flag[u] and flag[x])
+    assert g.dec_frontier_count(old, flag) == want
+
+
 def test_spec_examples(golden_dir):
     S = json.load(open(os.path.join(golden_dir, "spec_examples.json")))
     c = S["sssp_chain"]
