@@ -37,8 +37,18 @@
  * application of an insertion/deletion edge batch; the incremental/decremental
  * SSSP algorithm re-computes"): mutate first, then call the matching tree
  * update with the SAME batch, for every tree of the graph, before the next
- * mutation.  A tree update against any other graph version returns
- * MEERKAT_E_STATE without touching the tree.
+ * mutation.  Enforced three ways, each returning MEERKAT_E_STATE without touching
+ * the tree: (1) on the host, the graph version (the tree must be exactly one
+ * mutation behind), the mutation kind and the batch size n; (2) on the device,
+ * for calls that read the batch (not seeded by meerkat_*_batch_trees): the
+ * mutation kernel sums a 64-bit mix of every (src, dst) and (src, dst, w) of
+ * its batch (an order-independent fingerprint) and the tree kernel sums the
+ * same over the batch it was given before writing anything; on a mismatch the
+ * tree kernel writes nothing, marks its trees STALE and records MEERKAT_E_STATE
+ * (reported by the next synchronising call, e.g. meerkat_sync); (3) a stale
+ * tree refuses every dynamic call the same way until meerkat_tree_recompute.
+ * Seeded calls need no fingerprint: their batch prologue ran inside the
+ * mutation kernel on the batch it applied, so only n is checked.
  *
  * Thread safety: a graph handle (and its trees) must not be used from two
  * host threads at once.
@@ -154,7 +164,7 @@ meerkat_status meerkat_export_edges(meerkat_graph* g, uint32_t* src, uint32_t* d
                                     uint64_t capacity, uint64_t* n_out);
 meerkat_status meerkat_stats_get(meerkat_graph* g, meerkat_stats* out); /* synchronises */
 /* Structural check of the slab store(s) (owner of every slab, next pointers, no leftover link
- * lock, finite chains, EMPTY-suffix invariant, per-vertex degree table = live keys).  info[5] (host): violations, then the first one's
+ * lock, finite chains, EMPTY-suffix invariant).  info[5] (host): violations, then the first one's
  * vertex, slab, next, kind.  MEERKAT_E_STATE if any; synchronises. */
 meerkat_status meerkat_check(meerkat_graph* g, uint64_t* info);
 
@@ -300,7 +310,9 @@ meerkat_status meerkat_route(meerkat_graph* g, int key_is_b, const uint32_t* a, 
  * plus d * (sum of PR_{i-1} over zero-out-degree vertices) / N added to every vertex when such a
  * vertex exists (FindTeleportProb, reading C27), repeated until the L1 norm
  * sum_v |PR_i[v] - PR_{i-1}[v]| <= error_margin or max_iter super-steps ran (at least
- * one).  Double precision.  Out-degrees count stored edges (self-loops included).  The graph
+ * one).  Double precision.  Out-degrees count stored edges (self-loops included); they are
+ * counted by one stream over the out-store's slabs when the graph changed since the last run (the
+ * update kernels keep no degree table).  The graph
  * must keep the in-edge mirror (cfg.reverse = 1; the Compute kernel walks in-edges)
  * and be unpartitioned (world_size 1), else MEERKAT_E_STATE.  MEERKAT_E_INVALID_ARG for a
  * damping outside (0,1), error_margin <= 0 or max_iter 0 (SPEC BadDamping / BadEpsilon).
@@ -365,13 +377,15 @@ meerkat_status meerkat_tc_decremental(meerkat_graph* g_after, meerkat_graph* g_u
 meerkat_status meerkat_wcc_create(meerkat_graph* g, meerkat_wcc** out);
 meerkat_status meerkat_wcc_recompute(meerkat_graph* g, meerkat_wcc* c);
 /* After insert_batch: union(src[i], dst[i]) for the batch, then full compression.
- * Stream-ordered. */
+ * The labels must be current up to that batch (the previous mutation) and n must be its size, else
+ * MEERKAT_E_STATE (there is no decremental WCC: recompute after a delete batch).  Stream-ordered. */
 meerkat_status meerkat_wcc_incremental(meerkat_graph* g, meerkat_wcc* c, const uint32_t* src, const uint32_t* dst,
                                        uint64_t n);
 /* The paper's UpdateIterator path: union the edges of every slab list written since the
  * last call, from its first updated cell on (the update tracking of cfg.update_tracking), then full
  * compression, then reset the tracking (Graph.UpdateSlabPointers).  Same labels as
- * meerkat_wcc_incremental with the inserted batches; MEERKAT_E_STATE without update tracking. */
+ * meerkat_wcc_incremental with the inserted batches; MEERKAT_E_STATE without update tracking or when a
+ * delete batch was applied since the labels were computed. */
 meerkat_status meerkat_wcc_incremental_tracked(meerkat_graph* g, meerkat_wcc* c);
 /* label[v] (host or device [vertex_n]). */
 meerkat_status meerkat_wcc_labels(meerkat_wcc* c, uint32_t* out);

@@ -105,6 +105,18 @@ meerkat_status collect(meerkat_graph* g) {
   return from_err(err);
 }
 
+// Host bookkeeping of a mutation (ordering contract): version, kind and size of the batch; an empty
+// batch launches no kernel, so its (zero) fingerprint slot is written here.
+cudaError_t mutated(meerkat_graph* g, int kind, uint64_t n) {
+  cudaError_t e = cudaSuccess;
+  if (!n) e = cudaMemsetAsync(&g->out.dev.ctrl->fp[0][0], 0, sizeof(g->out.dev.ctrl->fp), g->stream);
+  g->version++;
+  g->last_kind = kind;
+  g->last_n = n;
+  if (kind == 2) g->last_delete_version = g->version;
+  return e;
+}
+
 meerkat_status check_batch(meerkat_graph* g, const uint32_t* s, const uint32_t* d, uint64_t n) {
   if (!g) return MEERKAT_E_INVALID_ARG;
   if (n && (!s || !d)) return MEERKAT_E_INVALID_ARG;
@@ -230,9 +242,8 @@ meerkat_status meerkat_insert_batch(meerkat_graph* g, const uint32_t* src, const
   if (e == cudaSuccess)
     e = launch_insert(g, &g->out, g->reverse ? &g->in : nullptr,   // in-edge mirror: (dst, src, w)
                       (const uint32_t*)s, (const uint32_t*)d, (const uint32_t*)ww, n);
+  if (e == cudaSuccess) e = mutated(g, 1, n);
   if (e != cudaSuccess) return MEERKAT_E_CUDA;
-  g->version++;
-  g->last_kind = 1;
   remember_stage(g, 0, src, n * 4);
   remember_stage(g, 1, dst, n * 4);
   if (w) remember_stage(g, 2, w, n * 4);
@@ -253,9 +264,8 @@ meerkat_status meerkat_delete_batch(meerkat_graph* g, const uint32_t* src, const
   if (e == cudaSuccess && n_deleted) e = cudaMemsetAsync(&g->out.dev.ctrl->n_deleted, 0, 8, g->stream);
   if (e == cudaSuccess)
     e = launch_delete(g, &g->out, g->reverse ? &g->in : nullptr, (const uint32_t*)s, (const uint32_t*)d, n);
+  if (e == cudaSuccess) e = mutated(g, 2, n);
   if (e != cudaSuccess) return MEERKAT_E_CUDA;
-  g->version++;
-  g->last_kind = 2;
   remember_stage(g, 0, src, n * 4);
   remember_stage(g, 1, dst, n * 4);
   if (!n_deleted) return MEERKAT_OK;
@@ -391,11 +401,11 @@ static meerkat_status tree_create(meerkat_graph* g, uint32_t source, bool unit, 
   if (e == cudaSuccess) e = cudaMalloc(&t->ctrl_base, 2 * sizeof(TreeCtrl));   // double-buffered (tree.cu)
   if (e == cudaSuccess) e = cudaMemsetAsync(t->ctrl_base, 0, 2 * sizeof(TreeCtrl), g->stream);
   T.ctrl = t->ctrl_base;
-  if (e == cudaSuccess) e = cudaMalloc(&T.epoch_ptr, 4);
+  if (e == cudaSuccess) e = cudaMalloc(&T.epoch_ptr, 8);   // [0] epoch, [1] stale flag
   if (e == cudaSuccess) e = cudaMallocHost(&t->hctrl, sizeof(TreeCtrl));
   if (e == cudaSuccess) e = cudaMemsetAsync(T.stamp, 0, V * 4, g->stream);
   if (e == cudaSuccess) e = cudaMemsetAsync(T.inval_bits, 0, words * 4, g->stream);
-  if (e == cudaSuccess) e = cudaMemsetAsync(T.epoch_ptr, 0, 4, g->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(T.epoch_ptr, 0, 8, g->stream);
   if (e == cudaSuccess) {
     const uint32_t one = 1;
     e = cudaMemcpyAsync(T.epoch_ptr, &one, 4, cudaMemcpyHostToDevice, g->stream);
@@ -470,8 +480,9 @@ static meerkat_status trees_update(meerkat_graph* g, meerkat_tree* const* ts, ui
     if (t->vanilla) return MEERKAT_E_STATE;   // no dependence tree: static only
     for (uint32_t j = 0; j < i; j++)
       if (ts[j] == t) return MEERKAT_E_INVALID_ARG;
-    // ordering contract: the batch must be the mutation just applied
-    if (g->last_kind != kind || t->version + 1 != g->version) return MEERKAT_E_STATE;
+    // ordering contract: the batch must be the mutation just applied -- same kind, the
+    // very next version, the same size here; the same edges (fingerprint) on the device
+    if (g->last_kind != kind || t->version + 1 != g->version || n != g->last_n) return MEERKAT_E_STATE;
     // seeded by that mutation (insert_batch_trees / delete_batch_trees): all the call's trees or none
     if ((t->seeded != 0) != (ts[0]->seeded != 0) || (t->seeded && t->seeded != kind)) return MEERKAT_E_STATE;
     need_w |= kind == 1 && !t->unit;
@@ -484,7 +495,10 @@ static meerkat_status trees_update(meerkat_graph* g, meerkat_tree* const* ts, ui
   if (e == cudaSuccess && need_w) e = stage_in_reuse(g, 2, w, n * 4, &ww);
   if (e == cudaSuccess)
     e = launch_tree(g, ts, k, kind == 1 ? MODE_INCREMENTAL : MODE_DECREMENTAL, (const uint32_t*)s, (const uint32_t*)d,
-                    (const uint32_t*)ww, n, ts[0]->seeded != 0);
+                    (const uint32_t*)ww, n, ts[0]->seeded != 0,
+                    // seeded: the mutation kernel already ran the prologue on the batch it applied, so
+                    // the tree call reads no batch and needs no fingerprint
+                    ts[0]->seeded ? -1 : (ww ? 1 : 0));
   if (e != cudaSuccess) return MEERKAT_E_CUDA;
   for (uint32_t i = 0; i < k; i++) { ts[i]->version = g->version; ts[i]->seeded = 0; }
   return MEERKAT_OK;
@@ -528,9 +542,8 @@ static meerkat_status batch_seed(meerkat_graph* g, int kind, const uint32_t* src
   if (e == cudaSuccess)
     e = kind == 1 ? launch_insert(g, &g->out, mirror, (const uint32_t*)s, (const uint32_t*)d, (const uint32_t*)ww, n, &P)
                   : launch_delete(g, &g->out, mirror, (const uint32_t*)s, (const uint32_t*)d, n, &P);
+  if (e == cudaSuccess) e = mutated(g, kind, n);
   if (e != cudaSuccess) return MEERKAT_E_CUDA;
-  g->version++;
-  g->last_kind = kind;
   remember_stage(g, 0, src, n * 4);
   remember_stage(g, 1, dst, n * 4);
   if (ww) remember_stage(g, 2, w, n * 4);
@@ -1007,10 +1020,12 @@ meerkat_status meerkat_wcc_incremental(meerkat_graph* g, meerkat_wcc* c, const u
   meerkat_status st = check_batch(g, src, dst, n);
   if (st != MEERKAT_OK) return st;
   if (!c || c->g != g) return MEERKAT_E_INVALID_ARG;
+  // the labels must be current up to the insert batch just applied (there is no decremental WCC)
+  if (g->last_kind != 1 || c->version + 1 != g->version || n != g->last_n) return MEERKAT_E_STATE;
   DeviceGuard dg(g->device);
   const void *s, *d;
-  cudaError_t e = stage_in(g, 0, src, n * 4, &s);
-  if (e == cudaSuccess) e = stage_in(g, 1, dst, n * 4, &d);
+  cudaError_t e = stage_in_reuse(g, 0, src, n * 4, &s);
+  if (e == cudaSuccess) e = stage_in_reuse(g, 1, dst, n * 4, &d);
   if (e == cudaSuccess) e = launch_wcc_batch(g, c->parent, (const uint32_t*)s, (const uint32_t*)d, n);
   if (e != cudaSuccess) return MEERKAT_E_CUDA;
   c->version = g->version;
@@ -1020,6 +1035,9 @@ meerkat_status meerkat_wcc_incremental(meerkat_graph* g, meerkat_wcc* c, const u
 meerkat_status meerkat_wcc_incremental_tracked(meerkat_graph* g, meerkat_wcc* c) {
   if (!g || !c || c->g != g) return MEERKAT_E_INVALID_ARG;
   if (!g->out.dev.upd) return MEERKAT_E_STATE;   // the graph keeps no update tracking
+  // the tracked cells cover every insert since the labels were computed; a delete since then
+  // cannot be undone by unions (there is no decremental WCC): recompute instead
+  if (g->last_delete_version > c->version) return MEERKAT_E_STATE;
   DeviceGuard dg(g->device);
   const cudaError_t e = launch_wcc_tracked(g, c->parent);
   if (e != cudaSuccess) return MEERKAT_E_CUDA;

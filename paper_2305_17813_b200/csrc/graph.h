@@ -26,6 +26,7 @@ struct TreeCtrl {
   unsigned long long batch_edges;   // batch edges examined by the prologue
   unsigned long long pull_n;        // (invalid vertex, in-bucket) items of the reverse-store frontier
   unsigned long long tail_r;        // round counter after block 0's tail rounds (tree.cu run_rounds)
+  unsigned long long fp[2];         // fingerprint of the batch this call was given (ordering contract)
   unsigned long long nts;           // device timeline: %globaltimer at kernel start and after every grid barrier
   unsigned long long tstamp[48];
 };
@@ -48,7 +49,8 @@ struct TreeDev {
   uint32_t* inval_list;  // invalidated vertex ids
   uint64_t* fr[2];       // frontier item buffers: (bucket << 32) | vertex
   TreeCtrl* ctrl;
-  uint32_t* epoch_ptr;   // device-resident stamp epoch base, advanced by each call
+  uint32_t* epoch_ptr;   // device: [0] stamp epoch base, advanced by each call; [1] stale flag (a
+                         // dynamic call was refused on the device: only a static recompute clears it)
   uint64_t fr_cap;       // items per frontier buffer (= number of slab lists)
   uint32_t source;
   uint32_t unit;         // 1: BFS (every w = 1)
@@ -65,6 +67,7 @@ struct Store {
   uint64_t H = 0, P = 0, buckets = 0;   // arena slabs, pool capacity, slab lists
   size_t bytes = 0;
   GraphCtrl* hctrl = nullptr;           // pinned mirror of dev.ctrl
+  uint64_t deg_version = ~0ull;         // graph version dev.deg was counted at (launch_degrees)
 };
 }  // namespace mk
 
@@ -80,6 +83,8 @@ struct meerkat_graph {
   mk::Store in;                     // in-edge mirror (reverse store), only when reverse
   uint64_t version = 0;
   int last_kind = 0;                // 0 none, 1 insert, 2 delete
+  uint64_t last_n = 0;              // batch size of the last mutation (ordering contract)
+  uint64_t last_delete_version = 0; // version created by the last delete batch (incremental WCC)
   uint64_t launches = 0;
   int sm_count = 0;
   void* stage[4] = {nullptr, nullptr, nullptr, nullptr};   // staging for host inputs / outputs
@@ -173,11 +178,13 @@ cudaError_t launch_query(meerkat_graph* g, Store& st, const uint32_t* s, const u
                          uint8_t* found, uint32_t* w_out);
 cudaError_t launch_export(meerkat_graph* g, Store& st, uint32_t* s, uint32_t* d, uint32_t* w, uint64_t cap);
 cudaError_t launch_fsck(meerkat_graph* g, Store& st, unsigned long long* info_dev);
+cudaError_t launch_degrees(meerkat_graph* g, Store& st);   // dev.deg = live keys per row, if stale
 // tree.cu
 cudaError_t tree_occupancy(meerkat_graph* g);
 enum TreeMode { MODE_STATIC = 0, MODE_INCREMENTAL = 1, MODE_DECREMENTAL = 2 };
+// fp_mode: -1 no fingerprint check, 0 check over (src, dst), 1 over (src, dst, w)
 cudaError_t launch_tree(meerkat_graph* g, meerkat_tree* const* trees, uint32_t ntrees, int mode, const uint32_t* s,
-                        const uint32_t* d, const uint32_t* w, uint64_t n, bool pro_done = false);
+                        const uint32_t* d, const uint32_t* w, uint64_t n, bool pro_done = false, int fp_mode = -1);
 cudaError_t launch_node_dist(meerkat_graph* g, meerkat_tree* t, uint32_t* out);
 // dtree.cu
 meerkat_status dtree_phase(meerkat_graph* g, meerkat_tree* t, int phase, const void* a, const void* b,

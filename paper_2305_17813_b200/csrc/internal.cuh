@@ -46,6 +46,9 @@ struct GraphCtrl {
   unsigned long long upd_n;       // update tracking: slab lists queued in updq since the last reset
   unsigned int err;               // sticky ErrBits
   unsigned int pad;
+  // batch fingerprints of the last plain mutation (ordering contract, meerkat.h): slot = version & 1,
+  // [0] over (src, dst), [1] over (src, dst, w).  A mutation accumulates into its slot and zeroes the other.
+  unsigned long long fp[2][2];
 };
 
 struct GraphDev {
@@ -56,7 +59,8 @@ struct GraphDev {
                              // earliest cell written since the last reset, (slab << 5) | cell, or ~0
   uint32_t* updq;            // the slab lists with upd != ~0 (UpdateIterator work list)
   uint32_t* deg;     // per vertex live keys (out-degree in the out store, in-degree in the mirror),
-                     // maintained by insert / delete; PageRank's out[u]
+                     // computed on demand by a stream over the slabs (launch_degrees) for PageRank's
+                     // out[u] and triangle counting -- not maintained by the update kernels
   GraphCtrl* ctrl;
   uint32_t V, H, P, seed;   // V: vertices held here (vmeta entries); H/P: arena / pool slabs
   uint32_t Vg;              // global vertex count: the key range
@@ -112,6 +116,20 @@ template <bool MAP> struct Frag {
 };
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// Batch fingerprint (ordering contract): an order-independent sum over the batch's edges of a
+// 64-bit mix of (src, dst) and of (src, dst, w).  Same function on the mutation and the tree side.
+__host__ __device__ __forceinline__ uint64_t fp_mix(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+__device__ __forceinline__ void fp_edge(uint32_t s, uint32_t d, uint32_t w, uint64_t& a, uint64_t& b) {
+  const uint64_t h = fp_mix(((uint64_t)s << 32) | d);
+  a += h;
+  b += fp_mix(h + w);
+}
 
 // First cell (in chain order) whose per-lane predicate bits are set.
 // bits: NK-bit mask of this lane's cells.  Returns cell index or -1 (group-uniform).

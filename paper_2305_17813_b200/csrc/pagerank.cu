@@ -22,7 +22,8 @@
 //    keys, reduces in-group, and runs of slabs with the same owner within a warp are combined
 //    before ONE fp64 atomicAdd into acc[v] — hubs' thousands of slab lists spread over the whole
 //    GPU instead of serialising on one warp, and no chain is chased;
-//  * out[u] is the store's per-vertex degree table, maintained by the update kernels;
+//  * out[u] is the store's per-vertex degree table, counted by a slab stream (launch_degrees) when
+//    the graph changed since the last count;
 //  * the per-vertex update fuses Eq. (1), the teleport term, the L1 delta, the next super-step's
 //    contributions and the dangling mass, one coalesced pass over the vertex arrays.
 #include <cooperative_groups.h>
@@ -226,7 +227,8 @@ cudaError_t pagerank_occupancy(bool weighted, int* blocks_per_sm) {
 }
 
 cudaError_t launch_pagerank(meerkat_graph* g, meerkat_pagerank* p, bool warm) {
-  cudaError_t e = cudaMemsetAsync(p->ctrl, 0, sizeof(PRCtrl), g->stream);
+  cudaError_t e = launch_degrees(g, g->out);   // out[u], counted when the graph changed
+  if (e == cudaSuccess) e = cudaMemsetAsync(p->ctrl, 0, sizeof(PRCtrl), g->stream);
   if (e != cudaSuccess) return e;
   PRArgs A;
   A.R = g->in.dev;

@@ -238,6 +238,7 @@ struct UpdArgs {
   const uint32_t* w;
   uint64_t n;
   uint32_t ns;   // stores updated: 1 or 2
+  uint32_t fp_slot;   // plain mutation: batch fingerprint slot of the version it creates (version & 1)
   // fused tree prologue (PRO != 0 kernels): the trees the following tree call updates
   TreeDev T[MAX_TREES];
   uint32_t ntrees;
@@ -259,7 +260,37 @@ __device__ __forceinline__ void upd_tree_prologue(const UpdArgs& A) {
   if (PRO == 1) tree_prologue_inc<true>(A.G[0], A.T, A.ntrees, A.src, A.dst, A.w, A.n, epoch, tid, nt, c);
   else tree_prologue_dec(A.G[0], A.T, A.ntrees, A.src, A.dst, A.n, tid, nt, c);
   c.batch = 0;   // the tree call's alg_bytes then covers what its own kernel read
-  for (uint32_t k = 0; k < A.ntrees; k++) flush_counters(A.G[0], A.T[k], c, (int)k, false, 0, 0);
+  FOR_TREES(k, A) flush_counters(A.G[0], A.T[k], c, k, false, 0, 0);
+}
+
+// Batch fingerprint bookkeeping (ordering contract): a plain mutation (PRO == 0) accumulates the
+// fingerprint of its batch into slot fp_slot and zeroes the other slot; a seeding mutation (whose
+// tree call reads no batch) zeroes both, so the next plain mutation starts from a clean slot.
+template <int PRO>
+__device__ __forceinline__ void upd_fp_begin(const UpdArgs& A) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  unsigned long long* f = &A.G[0].ctrl->fp[0][0];
+  if (PRO != 0) { f[0] = 0; f[1] = 0; f[2] = 0; f[3] = 0; }
+  else { f[2 * (A.fp_slot ^ 1)] = 0; f[2 * (A.fp_slot ^ 1) + 1] = 0; }
+}
+
+template <int PRO>
+__device__ __forceinline__ void upd_fp_end(const UpdArgs& A, uint64_t fa, uint64_t fb) {
+  if constexpr (PRO == 0) block_add2_u64(&A.G[0].ctrl->fp[A.fp_slot][0], fa, fb);
+}
+
+template <int PRO>
+__device__ __forceinline__ void upd_finish(const UpdArgs& A, const PerStore& err, const PerStore& cnt, bool ins,
+                                           uint64_t fa, uint64_t fb) {
+#pragma unroll
+  for (int k = 0; k < 2; k++) {
+    if (k >= (int)A.ns) break;
+    block_or_err(&A.G[k].ctrl->err, err.get(k));
+    if (ins) block_add(&A.G[k].ctrl->n_inserted, &A.G[k].ctrl->ins_total, cnt.get(k));
+    else block_add(&A.G[k].ctrl->n_deleted, &A.G[k].ctrl->del_total, cnt.get(k));
+  }
+  upd_fp_end<PRO>(A, fa, fb);
+  if constexpr (PRO != 0) upd_tree_prologue<PRO>(A);
 }
 
 __device__ __forceinline__ void upd_item(const UpdArgs& A, uint64_t i, uint32_t& st, uint64_t& e) {
@@ -274,33 +305,31 @@ __global__ void __launch_bounds__(UPD_BLOCK, UPD_MINB) k_insert(const __grid_con
   const int lane = lane_id(), l8 = lane & 7, gbase = lane & 24;
   const uint32_t gmask = 0xFFu << gbase;
   const uint64_t ng = ((uint64_t)gridDim.x * blockDim.x) / GROUP;
-  uint32_t added[2] = {0, 0}, err[2] = {0, 0};
+  PerStore added, err;
+  uint64_t fa = 0, fb = 0;
+  upd_fp_begin<PRO>(A);
   const uint64_t total = A.n * A.ns;
   for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / GROUP; i < total; i += ng) {
     uint32_t st; uint64_t e;
     upd_item(A, i, st, e);
     const GraphDev& G = A.G[st];
     const uint32_t a = A.src[e], b = A.dst[e], wt = MAP ? A.w[e] : 0u;
+    if (PRO == 0 && st == 0 && l8 == 0) fp_edge(a, b, wt, fa, fb);
     const uint32_t u = st ? b : a, v = st ? a : b;
-    if (u >= G.Vg || v >= G.Vg) { err[st] |= ERR_RANGE; continue; }
-    if (MAP && (wt == 0 || wt >= W_LIMIT)) { err[st] |= ERR_WEIGHT; continue; }
+    if (u >= G.Vg || v >= G.Vg) { err.set(st, ERR_RANGE); continue; }
+    if (MAP && (wt == 0 || wt >= W_LIMIT)) { err.set(st, ERR_WEIGHT); continue; }
     const uint32_t ul = local_row(G, u);
-    if (ul == INVALID_SLAB) { err[st] |= ERR_PARTITION; continue; }
+    if (ul == INVALID_SLAB) { err.set(st, ERR_PARTITION); continue; }
     uint32_t plist = 0;
     unsigned long long ppos = 0;
     const int r = group_insert<MAP>(G, ul, v, wt, l8, gmask, gbase, plist, ppos);
-    if (r < 0) err[st] |= ERR_CAPACITY;
+    if (r < 0) err.set(st, ERR_CAPACITY);
     else if (l8 == 0 && r) {
-      added[st]++;
-      atomicAdd(G.deg + ul, 1u);
+      added.add(st, 1);
       if (TRACK && G.upd) track_update(G, plist, ppos);
     }
   }
-  for (uint32_t k = 0; k < A.ns; k++) {
-    block_or_err(&A.G[k].ctrl->err, err[k]);
-    block_add(&A.G[k].ctrl->n_inserted, &A.G[k].ctrl->ins_total, added[k]);
-  }
-  if constexpr (PRO != 0) upd_tree_prologue<PRO>(A);
+  upd_finish<PRO>(A, err, added, true, fa, fb);
 }
 
 // ------------------------------------------------------------------ delete / query
@@ -356,17 +385,20 @@ __global__ void __launch_bounds__(UPD_BLOCK, UPD_MINB) k_delete(const __grid_con
   const int lane = lane_id(), l8 = lane & 7, gbase = lane & 24;
   const uint32_t gmask = 0xFFu << gbase;
   const uint64_t ng = ((uint64_t)gridDim.x * blockDim.x) / GROUP;
-  uint32_t removed[2] = {0, 0}, err[2] = {0, 0};
+  PerStore removed, err;
+  uint64_t fa = 0, fb = 0;
+  upd_fp_begin<PRO>(A);
   const uint64_t total = A.n * A.ns;
   for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / GROUP; i < total; i += ng) {
     uint32_t st; uint64_t e;
     upd_item(A, i, st, e);
     const GraphDev& G = A.G[st];
     const uint32_t a = A.src[e], b = A.dst[e];
+    if (PRO == 0 && st == 0 && l8 == 0) fp_edge(a, b, 0u, fa, fb);
     const uint32_t u = st ? b : a, v = st ? a : b;
-    if (u >= G.Vg || v >= G.Vg) { err[st] |= ERR_RANGE; continue; }
+    if (u >= G.Vg || v >= G.Vg) { err.set(st, ERR_RANGE); continue; }
     const uint32_t ul = local_row(G, u);
-    if (ul == INVALID_SLAB) { err[st] |= ERR_PARTITION; continue; }
+    if (ul == INVALID_SLAB) { err.set(st, ERR_PARTITION); continue; }
     uint32_t slab; uint64_t val;
     const int c = group_find<MAP>(G, ul, v, l8, gmask, gbase, slab, val);
     if (c < 0 || l8 != 0) continue;
@@ -375,13 +407,9 @@ __global__ void __launch_bounds__(UPD_BLOCK, UPD_MINB) k_delete(const __grid_con
     if (MAP) ok = atomicCAS(reinterpret_cast<unsigned long long*>(slab_ptr(G, slab) + 2 * c),
                             (unsigned long long)val, (unsigned long long)TOMB_PAIR) == val;
     else ok = atomicCAS(slab_ptr(G, slab) + c, (unsigned int)val, TOMBSTONE_KEY) == (unsigned int)val;
-    if (ok) { removed[st]++; atomicSub(G.deg + ul, 1u); }
+    if (ok) removed.add(st, 1);
   }
-  for (uint32_t k = 0; k < A.ns; k++) {
-    block_or_err(&A.G[k].ctrl->err, err[k]);
-    block_add(&A.G[k].ctrl->n_deleted, &A.G[k].ctrl->del_total, removed[k]);
-  }
-  if constexpr (PRO != 0) upd_tree_prologue<PRO>(A);
+  upd_finish<PRO>(A, err, removed, false, fa, fb);
 }
 
 template <bool MAP>
@@ -464,55 +492,52 @@ __global__ void __launch_bounds__(UPD_BLOCK, UPD_T_MINB) k_query_t(GraphDev G, c
 
 template <bool MAP, bool TRACK, int PRO = 0>
 __global__ void __launch_bounds__(UPD_BLOCK, UPD_T_MINB) k_insert_t(const __grid_constant__ UpdArgs A) {
-  uint32_t added[2] = {0, 0}, err[2] = {0, 0};
+  PerStore added, err;
+  uint64_t fa = 0, fb = 0;
+  upd_fp_begin<PRO>(A);
   const uint64_t total = A.n * A.ns;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t st; uint64_t e;
     upd_item(A, i, st, e);
     const GraphDev& G = A.G[st];
     const uint32_t a = A.src[e], b = A.dst[e], wt = MAP ? A.w[e] : 0u;
+    if (PRO == 0 && st == 0) fp_edge(a, b, wt, fa, fb);
     const uint32_t u = st ? b : a, v = st ? a : b;
-    if (u >= G.Vg || v >= G.Vg) { err[st] |= ERR_RANGE; continue; }
-    if (MAP && (wt == 0 || wt >= W_LIMIT)) { err[st] |= ERR_WEIGHT; continue; }
+    if (u >= G.Vg || v >= G.Vg) { err.set(st, ERR_RANGE); continue; }
+    if (MAP && (wt == 0 || wt >= W_LIMIT)) { err.set(st, ERR_WEIGHT); continue; }
     const uint32_t ul = local_row(G, u);
-    if (ul == INVALID_SLAB) { err[st] |= ERR_PARTITION; continue; }
+    if (ul == INVALID_SLAB) { err.set(st, ERR_PARTITION); continue; }
     uint32_t plist = 0;
     unsigned long long ppos = 0;
     const int r = thread_insert<MAP>(G, ul, v, wt, plist, ppos);
-    if (r < 0) err[st] |= ERR_CAPACITY;
+    if (r < 0) err.set(st, ERR_CAPACITY);
     else if (r) {
-      added[st]++;
-      atomicAdd(G.deg + ul, 1u);
+      added.add(st, 1);
       if (TRACK && G.upd) track_update(G, plist, ppos);
     }
   }
-  for (uint32_t k = 0; k < A.ns; k++) {
-    block_or_err(&A.G[k].ctrl->err, err[k]);
-    block_add(&A.G[k].ctrl->n_inserted, &A.G[k].ctrl->ins_total, added[k]);
-  }
-  if constexpr (PRO != 0) upd_tree_prologue<PRO>(A);
+  upd_finish<PRO>(A, err, added, true, fa, fb);
 }
 
 template <bool MAP, int PRO = 0>
 __global__ void __launch_bounds__(UPD_BLOCK, UPD_T_MINB) k_delete_t(const __grid_constant__ UpdArgs A) {
-  uint32_t removed[2] = {0, 0}, err[2] = {0, 0};
+  PerStore removed, err;
+  uint64_t fa = 0, fb = 0;
+  upd_fp_begin<PRO>(A);
   const uint64_t total = A.n * A.ns;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t st; uint64_t e;
     upd_item(A, i, st, e);
     const GraphDev& G = A.G[st];
     const uint32_t a = A.src[e], b = A.dst[e];
+    if (PRO == 0 && st == 0) fp_edge(a, b, 0u, fa, fb);
     const uint32_t u = st ? b : a, v = st ? a : b;
-    if (u >= G.Vg || v >= G.Vg) { err[st] |= ERR_RANGE; continue; }
+    if (u >= G.Vg || v >= G.Vg) { err.set(st, ERR_RANGE); continue; }
     const uint32_t ul = local_row(G, u);
-    if (ul == INVALID_SLAB) { err[st] |= ERR_PARTITION; continue; }
-    if (thread_delete<MAP>(G, ul, v)) { removed[st]++; atomicSub(G.deg + ul, 1u); }
+    if (ul == INVALID_SLAB) { err.set(st, ERR_PARTITION); continue; }
+    if (thread_delete<MAP>(G, ul, v)) removed.add(st, 1);
   }
-  for (uint32_t k = 0; k < A.ns; k++) {
-    block_or_err(&A.G[k].ctrl->err, err[k]);
-    block_add(&A.G[k].ctrl->n_deleted, &A.G[k].ctrl->del_total, removed[k]);
-  }
-  if constexpr (PRO != 0) upd_tree_prologue<PRO>(A);
+  upd_finish<PRO>(A, err, removed, false, fa, fb);
 }
 
 // Kernel choice by batch size (measured): small batches are latency-bound and the
@@ -629,30 +654,52 @@ __global__ void k_fill(uint32_t* __restrict__ slabs, uint64_t n_slabs, int map) 
   }
 }
 
+// ------------------------------------------------------------------ degree table (on demand)
+
+// deg[u] = live keys of u's slab lists, by one address-order stream of the slab array [0, H + pool
+// used): an 8-lane group per slab counts its live cells, one atomicAdd per slab with any (owner[]
+// names the row).  Launched only by consumers of the table (PageRank's out[u], triangle counting's
+// walked-side choice) when the graph changed since the last count, so the update kernels carry no
+// per-edge degree atomics.
+template <bool MAP>
+__global__ void __launch_bounds__(UPD_BLOCK) k_degrees(GraphDev G) {
+  using F = Frag<MAP>;
+  constexpr int NK = F::NK;
+  const int l8 = lane_id() & 7, gbase = lane_id() & 24;
+  const uint32_t gmask = 0xFFu << gbase;
+  const uint64_t n_slabs = G.H + min((unsigned long long)G.P, __ldcg(&G.ctrl->pool_top));
+  const uint64_t ng = ((uint64_t)gridDim.x * blockDim.x) / GROUP;
+  for (uint64_t s = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / GROUP; s < n_slabs; s += ng) {
+    const uint32_t own = __ldg(G.owner + s);   // group-uniform
+    if (own == NO_OWNER) continue;
+    const uint4 d = ld_slab_ro(slab_ptr(G, (uint32_t)s), l8);
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int k = 0; k < NK; k++) {
+      const uint32_t key = F::key(d, k);
+      cnt += F::valid_cell(l8, k) && key < G.Vg;
+    }
+    cnt = __reduce_add_sync(gmask, cnt);
+    if (l8 == 0 && cnt) atomicAdd(G.deg + own, cnt);
+  }
+}
+
 // ------------------------------------------------------------------ consistency check (fsck)
 
 // One thread per vertex walks every slab list of the vertex and checks the store's
 // structural invariants: each slab's owner is the vertex, next pointers are INVALID
 // or pool slabs, no LINKING lock survives a kernel, chains are finite, and no slab
-// follows a slab that still has an EMPTY cell (EMPTY-suffix invariant, §4.2), and the
-// degree table equals the vertex's live keys (kind 8: info[2] = live keys, info[3] = deg).
+// follows a slab that still has an EMPTY cell (EMPTY-suffix invariant, §4.2).
 // info[0] = violations, info[1..4] = first violation (vertex, slab, next, kind).
 template <bool MAP>
 __global__ void k_fsck(GraphDev G, unsigned long long* info) {
   using F = Frag<MAP>;
   for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < G.V; u += (uint64_t)gridDim.x * blockDim.x) {
     const uint2 m = G.vmeta[u];
-    if (m.x == INVALID_SLAB) {   // no slab list yet: no edges
-      if (G.deg[u] != 0) {
-        const unsigned long long k = atomicAdd(&info[0], 1ull);
-        if (k == 0) { info[1] = u; info[2] = 0; info[3] = G.deg[u]; info[4] = 8; }
-      }
-      continue;
-    }
+    if (m.x == INVALID_SLAB) continue;   // no slab list yet: no edges
     int kind = 0;
     uint32_t bad_s = 0, bad_n = 0;
     if (m.x == LINKING) { kind = 1; }
-    uint32_t live = 0;
     for (uint32_t b = 0; b < m.y && !kind; b++) {
       uint32_t s = m.x + b, steps = 0;
       while (!kind) {
@@ -663,7 +710,6 @@ __global__ void k_fsck(GraphDev G, unsigned long long* info) {
         for (int w = 0; w < SLAB_WORDS - 1; w++) {
           const bool keyword = MAP ? ((w & 1) == 0 && w < 30) : true;
           if (keyword && p[w] == EMPTY_KEY) has_empty = true;
-          if (keyword && p[w] < G.Vg) live++;
         }
         const uint32_t nx = p[SLAB_WORDS - 1];
         if (nx == INVALID_SLAB) break;
@@ -674,7 +720,6 @@ __global__ void k_fsck(GraphDev G, unsigned long long* info) {
         s = nx;
       }
     }
-    if (!kind && live != G.deg[u]) { kind = 8; bad_s = live; bad_n = G.deg[u]; }   // degree table
     if (kind) {
       const unsigned long long k = atomicAdd(&info[0], 1ull);
       if (k == 0) { info[1] = u; info[2] = bad_s; info[3] = bad_n; info[4] = kind; }
@@ -807,6 +852,7 @@ cudaError_t launch_insert(meerkat_graph* g, Store* st0, Store* st1, const uint32
   A.G[0] = st0->dev;
   if (st1) A.G[1] = st1->dev;
   A.src = s; A.dst = d; A.w = w; A.n = n; A.ns = st1 ? 2u : 1u;
+  A.fp_slot = (uint32_t)((g->version + 1) & 1);   // the version this mutation creates
   set_pro(A, pro);
   const bool thread = thread_upd(n * A.ns);
   const unsigned grid = thread ? grid_threads(g, n * A.ns) : grid_for(g, n * A.ns, 0);
@@ -828,6 +874,7 @@ cudaError_t launch_delete(meerkat_graph* g, Store* st0, Store* st1, const uint32
   A.G[0] = st0->dev;
   if (st1) A.G[1] = st1->dev;
   A.src = s; A.dst = d; A.w = nullptr; A.n = n; A.ns = st1 ? 2u : 1u;
+  A.fp_slot = (uint32_t)((g->version + 1) & 1);   // the version this mutation creates
   set_pro(A, pro);
   const bool thread = thread_upd(n * A.ns);
   const unsigned grid = thread ? grid_threads(g, n * A.ns) : grid_for(g, n * A.ns, 0);
@@ -853,6 +900,19 @@ cudaError_t launch_query(meerkat_graph* g, Store& st, const uint32_t* s, const u
   else k_query<false><<<gb, UPD_BLOCK, 0, g->stream>>>(st.dev, s, d, n, found, w_out);
   g->launches++;
   return cudaGetLastError();
+}
+
+cudaError_t launch_degrees(meerkat_graph* g, Store& st) {
+  if (st.deg_version == g->version) return cudaSuccess;   // the table is current
+  cudaError_t e = cudaMemsetAsync(st.dev.deg, 0, (size_t)st.dev.V * 4, g->stream);
+  if (e != cudaSuccess) return e;
+  const unsigned gb = grid_for(g, st.H + st.P);
+  if (g->weighted) k_degrees<true><<<gb, UPD_BLOCK, 0, g->stream>>>(st.dev);
+  else k_degrees<false><<<gb, UPD_BLOCK, 0, g->stream>>>(st.dev);
+  g->launches++;
+  e = cudaGetLastError();
+  if (e == cudaSuccess) st.deg_version = g->version;
+  return e;
 }
 
 cudaError_t launch_fsck(meerkat_graph* g, Store& st, unsigned long long* info_dev) {

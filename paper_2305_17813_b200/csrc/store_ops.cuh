@@ -30,6 +30,15 @@ __device__ __forceinline__ void block_add(unsigned long long* d0, unsigned long 
   __syncthreads();   // acc is reused by the next call (racecheck: no read may trail its reset)
 }
 
+// Two per-store values of an update kernel (out store, in-edge mirror) kept in registers: a
+// runtime-indexed [2] array would live in local memory.
+struct PerStore {
+  uint32_t v0 = 0, v1 = 0;
+  __device__ __forceinline__ void add(uint32_t st, uint32_t x) { if (st) v1 += x; else v0 += x; }
+  __device__ __forceinline__ void set(uint32_t st, uint32_t x) { if (st) v1 |= x; else v0 |= x; }
+  __device__ __forceinline__ uint32_t get(int k) const { return k ? v1 : v0; }
+};
+
 __device__ __forceinline__ void block_or_err(unsigned int* dst, uint32_t e) {
   e = __reduce_or_sync(0xFFFFFFFFu, e);
   if ((threadIdx.x & 31) == 0 && e) atomicOr(dst, e);

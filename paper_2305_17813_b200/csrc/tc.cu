@@ -3,8 +3,8 @@
 //   Count(G1, G2, edges) = sum over (u, v) in edges of |adjacency_G1(u) ∩ adjacency_G2(v)|.
 // The paper walks adjacency(v) in G2 with a warp (SlabIterator) and searches each neighbour adj_v
 // in u's table of G1.  The intersection is symmetric in which side is walked, so here
-// the walked side is the endpoint with the smaller degree (degree tables kept by the update
-// kernels) and the other side is probed; the result is the same number.
+// the walked side is the endpoint with the smaller degree (degree tables counted on demand by
+// launch_degrees) and the other side is probed; the result is the same number.
 //
 // B200 design:
 //  * plan: one thread per edge picks the walked side and writes its slab-list (bucket) count;
@@ -144,6 +144,12 @@ cudaError_t launch_tc_count(meerkat_graph* g1, meerkat_graph* g2, const uint32_t
   uint64_t total = 0;
   cudaError_t e;
 #define CK(x) do { e = (x); if (e != cudaSuccess) goto out; } while (0)
+  // degree tables (walked-side choice), counted when a graph changed since the last count
+  CK(launch_degrees(g1, g1->out));
+  if (g2 != g1) {
+    CK(launch_degrees(g2, g2->out));
+    if (g2->stream != st) CK(cudaStreamSynchronize(g2->stream));
+  }
   CK(cudaMallocAsync(&side, n * 4, st));
   CK(cudaMallocAsync(&cnt, (n + 1) * 8, st));
   CK(cudaMallocAsync(&off, (n + 1) * 8, st));

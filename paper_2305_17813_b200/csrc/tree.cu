@@ -268,7 +268,7 @@ __device__ __forceinline__ uint32_t run_rounds(const TreeArgs& A, const uint32_t
       if (blockIdx.x == 0) {
         for (;;) {
           if (threadIdx.x == 0)
-            for (uint32_t k = 0; k < A.ntrees; k++) A.T[k].ctrl->size[(r + 2) % 3] = 0;
+            FOR_TREES(k, A) A.T[k].ctrl->size[(r + 2) % 3] = 0;
 #pragma unroll
           for (int k = 0; k < MAX_TREES; k++) {
             if (!n[k]) continue;
@@ -298,7 +298,7 @@ __device__ __forceinline__ uint32_t run_rounds(const TreeArgs& A, const uint32_t
       continue;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0)
-      for (uint32_t k = 0; k < A.ntrees; k++) A.T[k].ctrl->size[(r + 2) % 3] = 0;
+      FOR_TREES(k, A) A.T[k].ctrl->size[(r + 2) % 3] = 0;
 #pragma unroll
     for (int k = 0; k < MAX_TREES; k++) {
       if (!n[k]) continue;
@@ -313,9 +313,34 @@ __device__ __forceinline__ uint32_t run_rounds(const TreeArgs& A, const uint32_t
   return r;
 }
 
+// Ordering contract (meerkat.h; "G undergoes modifications ... re-computes"): a dynamic call
+// may only touch its trees if none is stale and, when asked, the batch it was given has the
+// fingerprint of the batch the last mutation applied.  Otherwise nothing is written, the trees are
+// marked stale (only a static recompute clears that) and MEERKAT_E_STATE is raised.  Grid-uniform.
+__device__ __forceinline__ bool tree_call_admitted(const TreeArgs& A, cg::grid_group& grid, uint64_t tid,
+                                                   uint64_t nt) {
+  bool bad = false;
+  FOR_TREES(k, A) bad |= __ldcg(A.T[k].epoch_ptr + 1) != 0u;
+  if (A.fp_check) {
+    uint64_t fa = 0, fb = 0;
+    for (uint64_t i = tid; i < A.bn; i += nt) fp_edge(A.bs[i], A.bd[i], A.bw ? A.bw[i] : 0u, fa, fb);
+    block_add2_u64(&A.T[0].ctrl->fp[0], fa, fb);
+    grid.sync();
+    bad |= __ldcg(&A.G.ctrl->fp[A.fp_slot][A.fp_w]) != __ldcg(&A.T[0].ctrl->fp[A.fp_w]);
+  }
+  if (bad) {
+    if (tid == 0) atomicOr(&A.G.ctrl->err, (unsigned)ERR_STATE);
+    FOR_TREES(k, A) {
+      if (tid == 0) A.T[k].epoch_ptr[1] = 1u;
+      clear_next_ctrl(A.clear_ctrl[k]);
+    }
+  }
+  return !bad;
+}
+
 __device__ __forceinline__ void finish(const TreeArgs& A, Counters& c, const uint32_t* epoch, bool owner,
                                        uint32_t rounds_total, uint32_t relax_rounds, uint32_t prop_rounds) {
-  for (uint32_t k = 0; k < A.ntrees; k++) {
+  FOR_TREES(k, A) {
     if (owner) *A.T[k].epoch_ptr = epoch[k] + rounds_total + 2;   // every thread read the base before a barrier
     flush_counters(A.G, A.T[k], c, k, owner, relax_rounds, prop_rounds);
     clear_next_ctrl(A.clear_ctrl[k]);
@@ -343,6 +368,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_static(const __grid_cons
   cg::grid_group grid = cg::this_grid();
   Counters c;
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
+  if (tid == 0) T.epoch_ptr[1] = 0u;   // a static recompute makes a stale tree current again
   // init: every node <INF, INVALID>, SRC <0, SRC>
   if (V32)   // vanilla: distance 0 at SRC, INF elsewhere
     for (uint64_t v = tid; v < A.G.V; v += nt) reinterpret_cast<uint32_t*>(T.node)[v] = v == T.source ? 0u : INF_DIST;
@@ -370,6 +396,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, TREE_MINB) k_tree_inc(const __grid
   cg::grid_group grid = cg::this_grid();
   Counters c;
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
+  if (!tree_call_admitted(A, grid, tid, nt)) return;
   if (!A.pro_done) {   // else the insert kernel ran it (meerkat_insert_batch_trees)
     tree_prologue_inc<false>(A.G, A.T, A.ntrees, A.bs, A.bd, A.bw, A.bn, epoch, tid, nt, c);
     grid.sync();
@@ -474,6 +501,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, TREE_MINB) k_tree_dec(const __grid
   cg::grid_group grid = cg::this_grid();
   Counters c;
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
+  if (!tree_call_admitted(A, grid, tid, nt)) return;
   // (i) Invalidate: deleted tree edges (parent(v), v), v != SRC (C4)
   if (!A.pro_done) {   // else the delete kernel ran it (meerkat_delete_batch_trees)
     tree_prologue_dec(A.G, A.T, A.ntrees, A.bs, A.bd, A.bn, tid, nt, c);
@@ -489,11 +517,11 @@ __global__ void __launch_bounds__(TREE_BLOCK, TREE_MINB) k_tree_dec(const __grid
     __shared__ unsigned long long s_inv[MAX_TREES];
     if (threadIdx.x < A.ntrees) s_inv[threadIdx.x] = __ldcg(&A.T[threadIdx.x].ctrl->inval_n);
     __syncthreads();
-    for (uint32_t k = 0; k < A.ntrees; k++) { n_inv[k] = s_inv[k]; n_inv_all += n_inv[k]; }
+    FOR_TREES(k, A) { n_inv[k] = s_inv[k]; n_inv_all += n_inv[k]; }
   }
   if (n_inv_all && A.R.slabs) {
     // in-edge mirror present: the frontier is exactly the in-edges of V_invalid from valid sources
-    for (uint32_t k = 0; k < A.ntrees; k++) {
+    FOR_TREES(k, A) {
       const TreeDev& T = A.T[k];
       const uint64_t ptrips = (n_inv[k] + nt - 1) / nt;
       for (uint64_t t = 0; t < ptrips; t++) {
@@ -507,7 +535,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, TREE_MINB) k_tree_dec(const __grid
     __shared__ unsigned long long s_pull[MAX_TREES];
     if (threadIdx.x < A.ntrees) s_pull[threadIdx.x] = __ldcg(&A.T[threadIdx.x].ctrl->pull_n);
     __syncthreads();
-    for (uint32_t k = 0; k < A.ntrees; k++) {
+    FOR_TREES(k, A) {
       const TreeDev& T = A.T[k];
       expand<MAP, PULL>(A, T, k, T.fr[(r1 + 1) & 1], s_pull[k], T.fr[r1 & 1], &T.ctrl->size[r1 % 3],
                         epoch[k] + r1, c);
@@ -519,7 +547,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, TREE_MINB) k_tree_dec(const __grid
     if (use_filter) {
       for (uint32_t i = threadIdx.x; i < FILTER_WORDS; i += blockDim.x) filt[i] = 0;
       __syncthreads();
-      for (uint32_t k = 0; k < A.ntrees; k++)
+      FOR_TREES(k, A)
         for (uint64_t i = threadIdx.x; i < n_inv[k]; i += blockDim.x) {
           uint32_t w, m;
           filter_loc(__ldcg(A.T[k].inval_list + i), 32 - FILTER_LOG2, w, m);
@@ -539,7 +567,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, TREE_MINB) k_tree_dec(const __grid
   // (iv) common epilogue
   const uint32_t r2 = run_rounds<MAP, RELAX>(A, epoch, grid, r1, c);
   // clear the invalid bit sets for the next call (the lists are kept for meerkat_tree_invalidated)
-  for (uint32_t k = 0; k < A.ntrees; k++)
+  FOR_TREES(k, A)
     for (uint64_t i = tid; i < n_inv[k]; i += nt) {
       const uint32_t x = A.T[k].inval_list[i];
       atomicAnd(A.T[k].inval_bits + (x >> 5), ~(1u << (x & 31)));
@@ -600,10 +628,13 @@ void tree_pro_fill(meerkat_tree* const* trees, uint32_t ntrees, TreePro& p) {
 }
 
 cudaError_t launch_tree(meerkat_graph* g, meerkat_tree* const* trees, uint32_t ntrees, int mode, const uint32_t* s,
-                        const uint32_t* d, const uint32_t* w, uint64_t n, bool pro_done) {
+                        const uint32_t* d, const uint32_t* w, uint64_t n, bool pro_done, int fp_mode) {
   if (ntrees == 0 || ntrees > (uint32_t)MAX_TREES) return cudaErrorInvalidValue;
   TreeArgs A{};
   A.pro_done = pro_done ? 1u : 0u;
+  A.fp_check = fp_mode >= 0 && n > 0 ? 1u : 0u;
+  A.fp_w = fp_mode > 0 ? 1u : 0u;
+  A.fp_slot = (uint32_t)(g->version & 1);
   A.G = g->out.dev;
   A.R = g->reverse ? g->in.dev : GraphDev{};
   A.ntrees = ntrees;

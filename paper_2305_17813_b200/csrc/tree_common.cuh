@@ -26,6 +26,10 @@ constexpr uint64_t TAIL_ITEMS = MEERKAT_TAIL_ITEMS;   // frontiers this small ru
 
 enum Visit { RELAX = 0, PROPAGATE = 1, PULL = 2 };
 
+// Loop over the trees of a call with a compile-time index, so per-tree register arrays (Counters,
+// epochs, frontier sizes) stay in registers: a runtime index puts them in local memory.
+#define FOR_TREES(k, A) _Pragma("unroll") for (int k = 0; k < MAX_TREES; k++) if (k < (int)(A).ntrees)
+
 struct TreeArgs {
   GraphDev G;           // out-edge store
   GraphDev R;           // in-edge mirror (R.slabs == nullptr when the graph keeps none)
@@ -39,6 +43,9 @@ struct TreeArgs {
   uint32_t weighted;    // graph has weights (map store)
   uint32_t filter_words;   // per tree
   uint32_t pro_done;       // the batch prologue already ran in the mutation kernel (fused calls)
+  uint32_t fp_check;       // ordering contract: compare the batch's fingerprint with the mutation's
+  uint32_t fp_slot;        // GraphCtrl::fp slot of the current graph version
+  uint32_t fp_w;           // 1: the fingerprint includes the weights (bw given)
 };
 
 // Zero the next call's control block (block 0, after the last grid barrier).
@@ -54,6 +61,22 @@ struct Counters {
   uint32_t hits[MAX_TREES] = {};
   uint32_t direct[MAX_TREES] = {};   // vertices invalidated directly by a deleted tree edge
 };
+
+// Block-aggregated add of two per-thread 64-bit sums (batch fingerprints).
+__device__ __forceinline__ void block_add2_u64(unsigned long long* dst, uint64_t a, uint64_t b) {
+  __shared__ unsigned long long acc2[2];
+  if (threadIdx.x < 2) acc2[threadIdx.x] = 0;
+  __syncthreads();
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    a += __shfl_xor_sync(0xFFFFFFFFu, (unsigned long long)a, o);
+    b += __shfl_xor_sync(0xFFFFFFFFu, (unsigned long long)b, o);
+  }
+  if ((threadIdx.x & 31) == 0 && (a | b)) { atomicAdd(&acc2[0], (unsigned long long)a); atomicAdd(&acc2[1], (unsigned long long)b); }
+  __syncthreads();
+  if (threadIdx.x == 0) { atomicAdd(dst, acc2[0]); atomicAdd(dst + 1, acc2[1]); }
+  __syncthreads();
+}
 
 __device__ __forceinline__ bool bit_test(const uint32_t* bits, uint32_t x) {
   return (__ldcg(bits + (x >> 5)) >> (x & 31)) & 1u;

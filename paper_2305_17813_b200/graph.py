@@ -25,17 +25,33 @@ def _is_torch(x):
     return torch is not None and isinstance(x, torch.Tensor)
 
 
-def _u32(x):
-    """(pointer, keepalive, n) for a 32-bit id/weight array."""
+def _u32(x, stream=None):
+    """(pointer, keepalive, n) for a 32-bit id/weight array.  A CUDA tensor that has to be converted
+    (dtype or layout) becomes a temporary allocated on torch's current stream; the library reads it
+    later on the graph's `stream`, so the temporary is recorded on that stream and the caching
+    allocator does not hand its block out again before the library's work there is done."""
     if x is None:
         return None, None, 0
     if _is_torch(x):
-        if x.dtype not in (torch.int32, torch.uint32):
-            x = x.to(torch.int32)
-        x = x.contiguous()
-        return ctypes.c_void_p(x.data_ptr()), x, x.numel()
+        y = x
+        if y.dtype not in (torch.int32, torch.uint32):
+            y = y.to(torch.int32)
+        y = y.contiguous()
+        if y is not x and y.is_cuda and stream is not None:
+            y.record_stream(stream)
+        return ctypes.c_void_p(y.data_ptr()), y, y.numel()
     a = np.ascontiguousarray(np.asarray(x), dtype=np.uint32)
     return ctypes.c_void_p(a.ctypes.data), a, a.size
+
+
+def _torch_stream(stream, device):
+    """The torch stream object of a graph's stream (for record_stream), or None (legacy default
+    stream, which orders against every other stream of the device)."""
+    if torch is None or stream is None:
+        return None
+    if isinstance(stream, int):
+        return torch.cuda.ExternalStream(stream, device=device) if stream else None
+    return stream
 
 
 def _stream_ptr(stream):
@@ -64,6 +80,7 @@ class Graph:
         h = ctypes.c_void_p()
         check(L.meerkat_create(ctypes.byref(cfg), ctypes.byref(h)), "meerkat_create")
         self._h = h
+        self._tstream = _torch_stream(stream, device)
         self.vertex_n = int(vertex_n)
         self.weighted = bool(weighted)
         self.reverse = bool(reverse)
@@ -94,6 +111,7 @@ class Graph:
 
     def set_stream(self, stream):
         check(_lib.lib().meerkat_set_stream(self._h, _stream_ptr(stream)), "meerkat_set_stream")
+        self._tstream = _torch_stream(stream, self.device)
 
     def sync(self):
         check(_lib.lib().meerkat_sync(self._h), "meerkat_sync")
@@ -102,9 +120,9 @@ class Graph:
     def insert(self, src, dst, w=None, count: bool = True, raise_on_error: bool = True, seed=None):
         """InsertEdges.  seed: trees whose next incremental call (same batch) this insert seeds
         (meerkat_insert_batch_trees)."""
-        sp, ks, n = _u32(src)
-        dp, kd, n2 = _u32(dst)
-        wp, kw, n3 = _u32(w)
+        sp, ks, n = _u32(src, self._tstream)
+        dp, kd, n2 = _u32(dst, self._tstream)
+        wp, kw, n3 = _u32(w, self._tstream)
         assert n == n2 and (w is None or n3 == n)
         out = ctypes.c_uint64(0)
         ob = ctypes.byref(out) if count else None
@@ -121,8 +139,8 @@ class Graph:
     def delete(self, src, dst, count: bool = True, raise_on_error: bool = True, seed=None):
         """DeleteEdges.  seed: trees whose next decremental call (same batch) this delete seeds
         (meerkat_delete_batch_trees)."""
-        sp, ks, n = _u32(src)
-        dp, kd, n2 = _u32(dst)
+        sp, ks, n = _u32(src, self._tstream)
+        dp, kd, n2 = _u32(dst, self._tstream)
         assert n == n2
         out = ctypes.c_uint64(0)
         ob = ctypes.byref(out) if count else None
@@ -138,8 +156,8 @@ class Graph:
 
     def query(self, src, dst, raise_on_error: bool = True):
         """found (uint8) and stored weight (uint32, 0 when absent) per queried edge."""
-        sp, ks, n = _u32(src)
-        dp, kd, n2 = _u32(dst)
+        sp, ks, n = _u32(src, self._tstream)
+        dp, kd, n2 = _u32(dst, self._tstream)
         assert n == n2
         if _is_torch(src) and src.is_cuda:
             found = torch.empty(n, dtype=torch.uint8, device=src.device)
@@ -185,17 +203,17 @@ class Graph:
     # ------------------------------------------------------------------ trees
     def trees_incremental(self, trees, src, dst, w=None):
         """Fused incremental update of several trees with the batch just inserted (one launch)."""
-        sp, ks, n = _u32(src)
-        dp, kd, _ = _u32(dst)
-        wp, kw, _ = _u32(w)
+        sp, ks, n = _u32(src, self._tstream)
+        dp, kd, _ = _u32(dst, self._tstream)
+        wp, kw, _ = _u32(w, self._tstream)
         arr = (ctypes.c_void_p * len(trees))(*[t._h.value for t in trees])
         check(_lib.lib().meerkat_trees_incremental(self._h, arr, len(trees), sp, dp, wp, n),
               "meerkat_trees_incremental")
 
     def trees_decremental(self, trees, src, dst):
         """Fused decremental update of several trees with the batch just deleted (one launch)."""
-        sp, ks, n = _u32(src)
-        dp, kd, _ = _u32(dst)
+        sp, ks, n = _u32(src, self._tstream)
+        dp, kd, _ = _u32(dst, self._tstream)
         arr = (ctypes.c_void_p * len(trees))(*[t._h.value for t in trees])
         check(_lib.lib().meerkat_trees_decremental(self._h, arr, len(trees), sp, dp, n), "meerkat_trees_decremental")
 
@@ -224,8 +242,8 @@ class Graph:
     # ------------------------------------------------------------------ triangle counting
     def tc_count(self, other: "Graph", src, dst) -> int:
         """Count(self, other, edges) = sum over (u, v) of |adj_self(u) ∩ adj_other(v)|."""
-        sp, ks, n = _u32(src)
-        dp, kd, _ = _u32(dst)
+        sp, ks, n = _u32(src, self._tstream)
+        dp, kd, _ = _u32(dst, self._tstream)
         out = ctypes.c_uint64(0)
         check(_lib.lib().meerkat_tc_count(self._h, other._h, sp, dp, n, ctypes.byref(out)), "meerkat_tc_count")
         return int(out.value)
@@ -239,8 +257,8 @@ class Graph:
     def tc_delta(self, update: "Graph", src, dst, insert: bool):
         """Triangles added (insert) / removed by a batch already applied to this graph; `update` holds
         exactly the batch; src/dst give it in both orientations.  Returns (delta, (S1, S2, S3))."""
-        sp, ks, n = _u32(src)
-        dp, kd, _ = _u32(dst)
+        sp, ks, n = _u32(src, self._tstream)
+        dp, kd, _ = _u32(dst, self._tstream)
         out = ctypes.c_uint64(0)
         s3 = (ctypes.c_uint64 * 3)()
         fn = _lib.lib().meerkat_tc_incremental if insert else _lib.lib().meerkat_tc_decremental
@@ -287,18 +305,18 @@ class Tree:
                 self.graph._trees.remove(self)
 
     def incremental(self, src, dst, w=None):
-        sp, ks, n = _u32(src)
-        dp, kd, _ = _u32(dst)
+        sp, ks, n = _u32(src, self.graph._tstream)
+        dp, kd, _ = _u32(dst, self.graph._tstream)
         L = _lib.lib()
         if self.unit:
             check(L.meerkat_bfs_incremental(self.graph._h, self._h, sp, dp, n), "meerkat_bfs_incremental")
         else:
-            wp, kw, _ = _u32(w)
+            wp, kw, _ = _u32(w, self.graph._tstream)
             check(L.meerkat_sssp_incremental(self.graph._h, self._h, sp, dp, wp, n), "meerkat_sssp_incremental")
 
     def decremental(self, src, dst):
-        sp, ks, n = _u32(src)
-        dp, kd, _ = _u32(dst)
+        sp, ks, n = _u32(src, self.graph._tstream)
+        dp, kd, _ = _u32(dst, self.graph._tstream)
         L = _lib.lib()
         fn = L.meerkat_bfs_decremental if self.unit else L.meerkat_sssp_decremental
         check(fn(self.graph._h, self._h, sp, dp, n), fn.__name__)
@@ -415,8 +433,8 @@ class WCC:
 
     def incremental(self, src, dst):
         """Union of the batch just inserted, then full compression."""
-        sp, ks, n = _u32(src)
-        dp, kd, _ = _u32(dst)
+        sp, ks, n = _u32(src, self.graph._tstream)
+        dp, kd, _ = _u32(dst, self.graph._tstream)
         check(_lib.lib().meerkat_wcc_incremental(self.graph._h, self._h, sp, dp, n), "meerkat_wcc_incremental")
 
     def incremental_tracked(self):
