@@ -76,6 +76,12 @@ def parse():
     p.add_argument("--pagerank", action=argparse.BooleanOptionalAction, default=True,
                    help="also time static and dynamic PageRank on the same graph (SURVEY §8(f) NEXT-1; "
                         "needs the in-edge mirror, i.e. --frontier reverse)")
+    p.add_argument("--hashing-ab", action=argparse.BooleanOptionalAction, default=True,
+                   help="also time the step, the static recomputes and the config-2 sweep with hashing OFF (one "
+                        "slab list per vertex; the paper's traversal trade-off, P:2282-2286) -> hashing_ab")
+    p.add_argument("--probe", action=argparse.BooleanOptionalAction, default=True,
+                   help="measure DRAM / L2 / atomic latency and the grid-barrier cost on the device and report the "
+                        "tree calls' latency floor (latency_floor)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-scale", type=int, default=20, help="R-MAT scale of the oracle's bounded sample")
     p.add_argument("--cpu-steps", type=int, default=8,
@@ -242,25 +248,48 @@ def workload_config(args, V, n_base, source, ws=1):
                    else "not flushed: inputs larger than L2 (store > L2), batches back to back")}
 
 
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 def cpu_baseline(args, steps):
     """The oracle as it stands, on a bounded sample of the same workload recipe (R-MAT at
     --cpu-scale, same generator, same batch size): per step it applies an insert batch and a
     delete batch and recomputes SSSP + BFS from scratch after each (the oracle has no dynamic
-    algorithm)."""
+    algorithm).  Timed per part: apply, SSSP and BFS seconds per batch."""
     import oracle
     import synth
     W = synth.rmat_dynamic(args.cpu_scale, args.ef, batch=args.batch, n_ins=steps, n_del=steps,
                            seed_batch=BATCH_SEED_BASE)
     o = oracle.OracleGraph(W.vertex_n)
     o.insert(*W.base)
-    t0 = time.perf_counter()
+    n_base = int(len(W.base[0]))
+    parts = {"apply_insert": [], "apply_delete": [], "sssp": [], "bfs": []}
+    clock = time.perf_counter
+
+    def timed(key, fn):
+        t = clock(); fn(); parts[key].append(clock() - t)
+    t0 = clock()
     for i in range(steps):
-        o.insert(*W.inserts[i]); o.sssp(W.source); o.bfs(W.source)
-        o.delete(W.deletes[i][0], W.deletes[i][1]); o.sssp(W.source); o.bfs(W.source)
-    dt = time.perf_counter() - t0
+        timed("apply_insert", lambda: o.insert(*W.inserts[i])); timed("sssp", lambda: o.sssp(W.source))
+        timed("bfs", lambda: o.bfs(W.source))
+        timed("apply_delete", lambda: o.delete(W.deletes[i][0], W.deletes[i][1]))
+        timed("sssp", lambda: o.sssp(W.source)); timed("bfs", lambda: o.bfs(W.source))
+    dt = clock() - t0
     return {"value": 2 * args.batch * steps / dt, "unit": "edges/s", "cores": 1, "kind": "oracle",
+            "host_cores": os.cpu_count(), "cpu_model": cpu_model(), "oracle_threads": 1,
+            "per_batch_s": {k: float(np.median(v)) for k, v in parts.items()},
+            "sample_scale": args.cpu_scale, "sample_vertices": int(W.vertex_n), "sample_edges": n_base,
             "sample": (f"oracle (single-threaded C) on R-MAT scale {args.cpu_scale} ef {args.ef} "
-                       f"(same recipe as the workload, 1/{2 ** (args.scale - args.cpu_scale)} of its vertices), "
+                       f"({W.vertex_n} vertices, {n_base} edges; the workload's recipe at "
+                       f"1/{2 ** max(0, args.scale - args.cpu_scale)} of its vertices), "
                        f"{steps} step(s) of insert {args.batch} + delete {args.batch} edges, each followed by "
                        f"from-scratch SSSP + BFS; {dt:.1f} s"),
             "seconds": dt}
@@ -273,15 +302,24 @@ def run_reference(args, ws, rank):
     for _ in range(args.warmup):
         pass   # the oracle has no warm state worth warming; bounded sample only
     cb = cpu_baseline(args, max(1, min(args.steps, args.cpu_steps)))
-    # the line carries our arm's config (the workload this is a bounded sample of); the sample
-    # itself is described in cpu_baseline.sample
-    W = make_workload(args, args.steps + args.warmup)[0]
+    # the line's config describes what was TIMED: the oracle sample at --cpu-scale (the full workload
+    # our arm runs is named in sample_of); at --cpu-scale == --scale the two are the same workload
+    cfg = workload_config(args, cb["sample_vertices"], cb["sample_edges"], 0)
+    cfg["workload"] = cfg["workload"].replace(f"rmat-s{args.scale}-", f"rmat-s{args.cpu_scale}-")
+    if args.cpu_scale != args.scale:
+        cfg["workload"] += f" -- bounded oracle sample at scale {args.cpu_scale}"
+        cfg["sample_of"] = workload_config(args, 1 << args.scale, None, 0)["workload"]
+    cfg["parallelism"] = "one host thread (the oracle)"
+    cfg["tree_updates"] = "from-scratch SSSP (Dijkstra) + BFS after every batch (the oracle has no dynamic algorithm)"
+    for k in ("decremental_frontier", "l2"):
+        cfg.pop(k, None)
     line = {"metric": METRIC, "value": cb["value"], "unit": "edges/s", "n_gpus": 0, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * cb["seconds"] / max(1, min(args.steps, args.cpu_steps)),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "impl": "reference",
-            "config": workload_config(args, W.vertex_n, int(len(W.base[0])), W.source),
-            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "config": cfg,
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "host_cores", "cpu_model",
+                                                "oracle_threads", "per_batch_s")},
             "e2e": {"value": cb["value"], "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "wall_s": time.time() - t_all}
     print(json.dumps(line), flush=True)
@@ -318,10 +356,11 @@ NAMES = ["insert", "sssp_inc", "bfs_inc", "delete", "sssp_dec", "bfs_dec"]
 NAMES_FUSED = ["insert", "trees_inc", "delete", "trees_dec"]
 
 
-def one_step(g, sp, bf, ins, dels, evs, stream, fused=False, seed=False):
+def one_step(g, sp, bf, ins, dels, evs, stream, fused=False, seed=False, after_inc=None):
     """The hot path over one batch pair: mutate, then update both trees.  fused: one
     launch updates the SSSP and the BFS tree together (meerkat_trees_*); seed: the trees' batch
-    prologue runs inside the insert / delete kernel (meerkat_*_batch_trees)."""
+    prologue runs inside the insert / delete kernel (meerkat_*_batch_trees).  after_inc (untimed
+    warm-up only): called between the incremental and the delete half, e.g. to read tree counters."""
     s, d, w = ins
     if fused:
         trees = [sp, bf] if seed else None
@@ -330,6 +369,8 @@ def one_step(g, sp, bf, ins, dels, evs, stream, fused=False, seed=False):
         evs[1].record(stream)
         g.trees_incremental([sp, bf], s, d, w)
         evs[2].record(stream)
+        if after_inc:
+            after_inc()
         s, d = dels
         g.delete(s, d, count=False, seed=trees)
         evs[3].record(stream)
@@ -360,8 +401,10 @@ def measure(args, ws, W, frontier, dev, local, stream, T, flush, K, Wm, clocks=N
     dels = [tuple(T(x) for x in b[:2]) for b in W.deletes]
     names = NAMES_FUSED if fused else NAMES
     ev = lambda: [torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)]
+    inc_stats = []   # counters of a fused incremental call (last warm-up step): its rounds for the latency floor
     for i in range(Wm):
-        one_step(g, sp, bf, ins[i], dels[i], ev(), stream, fused, seed)
+        grab = (lambda: inc_stats.append(sp.stats())) if (fused and i == Wm - 1) else None
+        one_step(g, sp, bf, ins[i], dels[i], ev(), stream, fused, seed, after_inc=grab)
         flush.zero_()
     torch.cuda.synchronize()
     g.sync()
@@ -435,6 +478,7 @@ def measure(args, ws, W, frontier, dev, local, stream, T, flush, K, Wm, clocks=N
         "frontier": frontier, "fused": fused, "K": K, "total_ms": total_ms, "ms_per_step": total_ms / K, "mean": mean,
         "per_call": per_call, "tstats": tstats, "clocks": clk, "n_base": n_base, "bulk_ms": bulk_ms,
         "launches": int(st1["kernel_launches"] - st0["kernel_launches"]), "static_ms": static,
+        "inc_stats": inc_stats[-1] if inc_stats else None,
         "vanilla_ms": vanilla, "scheme1_ms": scheme1,
         "store": {k: g.stats()[k] for k in ("head_slabs", "buckets", "pool_used", "bytes_device")},
     }
@@ -461,6 +505,50 @@ def roofline_of(res, peak, peak_src, traffic_file):
             "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": traffic, "alg_bytes_per_launch": ab,
             "traffic_frac": (traffic / (mean[dom] * 1e-3) / 1e9 / peak) if traffic else None,
             "l2_hit_rate_pct": l2hit, "peak_source": peak_src}
+
+
+def update_roofline(res, args, peak, peak_src, traffic_file, n_stores, n_trees):
+    """HBM roofline of the seeding insert / delete kernels: SURVEY §8(d)'s per-edge bytes per store
+    (insert 161 B, delete 157 B: batch + vmeta + 128 x 1.04 slabs + CAS) for the out store and the
+    in-edge mirror, plus the fused tree prologue per edge and tree (insert: node[u] + atomicMin
+    node[v] = 16 B; delete: node[v] = 8 B)."""
+    out = {}
+    try:
+        tj = json.load(open(traffic_file))
+    except Exception:
+        tj = {}
+    for name, per_store, per_tree in (("insert", 161, 16), ("delete", 157, 8)):
+        ms = res["mean"][name]
+        ab = args.batch * (n_stores * per_store + n_trees * per_tree)
+        ach = ab / (ms * 1e-3) / 1e9
+        traffic = tj.get(f"{res['frontier']}/{name}")
+        out[name] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                     "alg_bytes_per_launch": ab, "traffic": traffic,
+                     "traffic_over_alg": (traffic / ab) if traffic else None, "peak_source": peak_src}
+    return out
+
+
+def latency_floor(lat, res):
+    """Floor of the latency-bound tree calls from measured device latencies (meerkat_probe_latency):
+    every grid-synchronised phase costs one grid barrier plus its dependent chain -- item fetch (L2),
+    slab load (DRAM), packed atomicMin on node[x] (DRAM atomic), stamp atomicExch + vmeta (DRAM
+    atomic), warp enqueue (L2 atomic) -- so floor = phases x (grid_sync + l2 + dram + 2 x dram_atomic
+    + l2).  Phases: incremental = relax rounds; decremental = propagation rounds + 2 (pull-frontier
+    enqueue, pull) + relax rounds (the last tail rounds run on block barriers, so this overstates
+    them slightly)."""
+    if not lat:
+        return None
+    chain_us = (2 * lat["l2_load_ns"] + lat["dram_load_ns"] + 2 * lat["dram_atomic_ns"]) / 1e3
+    phase_us = lat["grid_sync_us"] + chain_us
+    out = {"probe": lat, "phase_us": phase_us, "chain_us": chain_us}
+    dec = res["tstats"].get("trees_dec") or []
+    if dec:
+        ph = float(np.mean([s["rounds"] + s["propagate_rounds"] + 2 for s in dec]))
+        out["trees_dec"] = {"phases": ph, "floor_us": ph * phase_us, "measured_us": 1e3 * res["mean"]["trees_dec"]}
+    if res.get("inc_stats"):
+        ph = float(res["inc_stats"]["rounds"])
+        out["trees_inc"] = {"phases": ph, "floor_us": ph * phase_us, "measured_us": 1e3 * res["mean"]["trees_inc"]}
+    return out
 
 
 def tree_detail(res):
@@ -670,22 +758,30 @@ def measure_tc(args, dev, stream):
     gu = Graph(V, weighted=False, device=dev.index or 0, stream=stream)
     gu.insert(T(bs), T(bd), count=False)
     g.sync(); gu.sync()
-    def timed(fn, reps=3):   # the counts do not mutate: median of 3 host-timed calls (host hiccups seen)
-        ms, r = [], None
+    def timed(fn, reps=5):   # the counts do not mutate: CUDA events on the graph's stream around each
+        ev, wall, r = [], [], None   # (synchronising) call, median of 5; host wall clock beside it
         for _ in range(reps):
-            t0 = time.perf_counter(); r = fn(); ms.append(1e3 * (time.perf_counter() - t0))
-        return r, float(np.median(ms))
-    tri, st_ms = timed(g.tc_static)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            a.record(stream); r = fn(); b.record(stream)
+            b.synchronize()
+            wall.append(1e3 * (time.perf_counter() - t0)); ev.append(a.elapsed_time(b))
+        return r, float(np.median(ev)), [float(min(ev)), float(max(ev))], float(np.median(wall))
+    tri, st_ms, st_rng, st_wall = timed(g.tc_static)
     g.delete(T(bs), T(bd), count=False)
     g.sync()
-    (removed, _), dec_ms = timed(lambda: g.tc_delta(gu, T(bs), T(bd), insert=False))
+    (removed, _), dec_ms, dec_rng, dec_wall = timed(lambda: g.tc_delta(gu, T(bs), T(bd), insert=False))
     g.insert(T(bs), T(bd), count=False)
     g.sync()
-    (added, S), inc_ms = timed(lambda: g.tc_delta(gu, T(bs), T(bd), insert=True))
+    (added, S), inc_ms, inc_rng, inc_wall = timed(lambda: g.tc_delta(gu, T(bs), T(bd), insert=True))
     out = {"graph": f"rmat-s{args.tc_scale}-ef16 symmetrised, {len(s)} directed edges", "triangles": tri,
            "static_ms": st_ms, "batch_undirected": 10_000, "incremental_ms": inc_ms, "added": added,
            "decremental_ms": dec_ms, "removed": removed, "S": S,
-           "timing": "host wall clock around each synchronising call (includes the plan scan's host read-back), median of 3"}
+           "min_max_ms": {"static": st_rng, "incremental": inc_rng, "decremental": dec_rng},
+           "wall_ms": {"static": st_wall, "incremental": inc_wall, "decremental": dec_wall},
+           "timing": "CUDA events on the graph's stream around each call (a call synchronises once for its plan "
+                     "scan's host read-back, inside the interval), median of 5; wall_ms = host clock"}
     g.close(); gu.close()
     return out
 
@@ -760,6 +856,7 @@ def run_ours(args, ws, rank, local):
                "h2d_bytes_per_step": n * 4 * (3 + 2),
                "d2h_bytes_per_step": 2 * 64,
                "ms_per_step": e_ms / K}
+    lat = g.probe_latency() if args.probe else None
     pagerank = None
     if args.pagerank and args.frontier == "reverse" and ws == 1:
         pagerank = measure_pagerank(g, W, T, stream, flush, peak, peak_src)
@@ -788,13 +885,43 @@ def run_ours(args, ws, rank, local):
                "roofline": roofline_of(r2, peak, peak_src, traffic_file), "tree_calls": tree_detail(r2)}
 
     sweep = store_sweep(args, dev, stream) if args.sweep and ws == 1 else None
+
+    # ---------------- hashing off vs on (hashing disabled ran BFS / SSSP 9-11% faster on the
+    # paper's GPU): the same step and static recomputes on a store with one slab list per vertex
+    hashing_ab = None
+    if args.hashing_ab and not args.no_hashing and ws == 1:
+        import copy
+        a_off = copy.copy(args)
+        a_off.no_hashing = True
+        r3, objs = measure(a_off, ws, W, args.frontier, dev, local, stream, T, flush, K, Wm, fused=args.fused)
+        objs[0].close()
+        del objs
+        sw_off = store_sweep(a_off, dev, stream) if args.sweep else None
+        on = {"ms_per_step": res["ms_per_step"], "per_call_ms": mean, "static_ms": res["static_ms"],
+              "vanilla_static_ms": res["vanilla_ms"], "store": res["store"]}
+        off = {"ms_per_step": r3["ms_per_step"], "per_call_ms": r3["mean"], "static_ms": r3["static_ms"],
+               "vanilla_static_ms": r3["vanilla_ms"], "store": r3["store"],
+               "tree_calls": tree_detail(r3)}
+        faster = lambda x_on, x_off: x_on / x_off - 1   # > 0: hashing off is faster by that fraction
+        hashing_ab = {
+            "on": on, "off": off,
+            "off_faster_by": {
+                "step": faster(on["ms_per_step"], off["ms_per_step"]),
+                **{f"call_{k}": faster(on["per_call_ms"][k], off["per_call_ms"][k]) for k in on["per_call_ms"]},
+                **{f"static_{k}": faster(on["static_ms"][k], off["static_ms"][k]) for k in on["static_ms"]},
+                **{f"vanilla_static_{k}": faster(on["vanilla_static_ms"][k], off["vanilla_static_ms"][k])
+                   for k in (on["vanilla_static_ms"] or {})}},
+            "config2_sweep_off": sw_off,
+            "paper": "hashing disabled: BFS vanilla / tree 10.78% / 9.1% faster, SSSP vanilla / tree 9.9% / 11% faster "
+                     "on average (RTX 2080 Ti, 7 graphs; P:2282-2286)"}
     tc = measure_tc(args, dev, stream) if args.tc and ws == 1 else None
     config4 = measure_config4(args, dev, stream, flush) if args.config4 and ws == 1 else None
 
     cb = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline(args, args.cpu_steps)
-        cb = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        cb = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "host_cores", "cpu_model",
+                                 "oracle_threads", "per_batch_s")}
 
     split = mean if not args.fused else per_tree
     dyn = {"sssp": split["sssp_inc"] + split["sssp_dec"], "bfs": split["bfs_inc"] + split["bfs_dec"]} if split else None
@@ -824,6 +951,10 @@ def run_ours(args, ws, rank, local):
         "bulk_build": {"edges": res["n_base"], "ms": res["bulk_ms"], "edges_per_s": res["n_base"] / (res["bulk_ms"] / 1e3)},
         "tree_calls": tree_detail(res),
         "roofline": roofline_of(res, peak, peak_src, traffic_file),
+        "update_roofline": update_roofline(res, args, peak, peak_src, traffic_file,
+                                           2 if args.frontier == "reverse" else 1, 2 if args.fused else 0),
+        "latency_floor": latency_floor(lat, res),
+        "hashing_ab": hashing_ab,
         "cpu_baseline": cb,
         "e2e": e2e,
         "gpu_launches": res["launches"],
@@ -966,9 +1097,26 @@ def run_dist(args, ws, rank, local):
                 f.write(json.dumps(line) + "\n")
 
 
+def self_launch(n):
+    """`python bench.py --gpus N` outside torchrun: start the N ranks ourselves (one process per GPU,
+    127.0.0.1 rendezvous) exactly as the driver's torchrun command would."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
+
+
 def main():
     args = parse()
     ws_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        self_launch(args.gpus)
+    if args.gpus != ws_env and args.impl == "ours":
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws_env}: launch one rank per GPU "
+                 f"(torchrun --nproc-per-node {args.gpus}) or omit WORLD_SIZE to let bench.py start them")
     if ws_env > 1:   # N generator processes on one host: split the cores
         os.environ.setdefault("OMP_NUM_THREADS", str(max(1, (os.cpu_count() or 8) // ws_env)))
     ws, rank, local = dist_init(args)

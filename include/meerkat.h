@@ -163,6 +163,20 @@ meerkat_status meerkat_query_batch(meerkat_graph* g, const uint32_t* src, const 
 meerkat_status meerkat_export_edges(meerkat_graph* g, uint32_t* src, uint32_t* dst, uint32_t* w,
                                     uint64_t capacity, uint64_t* n_out);
 meerkat_status meerkat_stats_get(meerkat_graph* g, meerkat_stats* out); /* synchronises */
+
+/* Latency probes for the latency floor of the tree calls (SURVEY §8(d) "latency term"; a frontier
+ * round is a chain of dependent memory operations closed by a grid barrier, P:108-112 / P:2189-2207):
+ * measured on g's device and stream with a 2-GiB pointer chase (DRAM), a 4-MiB chase (L2), a chase of
+ * dependent 64-bit atomicMin round trips (DRAM lines), and back-to-back grid.sync() on the tree
+ * kernels' cooperative grid.  Allocates 2 GiB temporarily; synchronises. */
+typedef struct {
+  double dram_load_ns;    /* dependent load, random line, buffer >> L2 */
+  double l2_load_ns;      /* dependent load, random line, buffer << L2 */
+  double dram_atomic_ns;  /* dependent 64-bit atomicMin round trip, random line, buffer >> L2 */
+  double grid_sync_us;    /* one grid-wide barrier of the tree kernels' grid */
+  uint32_t grid_blocks;   /* that grid: blocks of 512 threads */
+} meerkat_latency;
+meerkat_status meerkat_probe_latency(meerkat_graph* g, meerkat_latency* out);
 /* Structural check of the slab store(s) (owner of every slab, next pointers, no leftover link
  * lock, finite chains, EMPTY-suffix invariant).  info[5] (host): violations, then the first one's
  * vertex, slab, next, kind.  MEERKAT_E_STATE if any; synchronises. */

@@ -41,7 +41,7 @@ EXPORTS = [
     "meerkat_wcc_create", "meerkat_wcc_recompute", "meerkat_wcc_incremental", "meerkat_wcc_labels",
     "meerkat_wcc_components", "meerkat_wcc_destroy", "meerkat_tree_recompute_scheme",
     "meerkat_wcc_incremental_tracked", "meerkat_dtrees_pack", "meerkat_dtrees_apply", "meerkat_dtrees_scan",
-    "meerkat_dtrees_expand",
+    "meerkat_dtrees_expand", "meerkat_probe_latency",
 ]
 
 
@@ -93,6 +93,12 @@ class PageRankStats(ctypes.Structure):
 class DResult(ctypes.Structure):
     _fields_ = [("msgs", ctypes.c_void_p), ("msg_counts", ctypes.c_uint64 * MAX_RANKS), ("frontier", ctypes.c_uint64),
                 ("invalid", ctypes.c_void_p), ("invalid_n", ctypes.c_uint64)]
+
+
+class Latency(ctypes.Structure):
+    _fields_ = [("dram_load_ns", ctypes.c_double), ("l2_load_ns", ctypes.c_double),
+                ("dram_atomic_ns", ctypes.c_double), ("grid_sync_us", ctypes.c_double),
+                ("grid_blocks", ctypes.c_uint32)]
 
 
 _lib = None
@@ -166,6 +172,7 @@ def lib():
         "meerkat_dtrees_apply": (ctypes.c_int, [vp, pvp, u32, ctypes.c_int, vp, pu64]),
         "meerkat_dtrees_scan": (ctypes.c_int, [vp, pvp, u32, pvp, pu64, ctypes.POINTER(DResult)]),
         "meerkat_dtrees_expand": (ctypes.c_int, [vp, pvp, u32, ctypes.c_int, ctypes.POINTER(DResult)]),
+        "meerkat_probe_latency": (ctypes.c_int, [vp, ctypes.POINTER(Latency)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

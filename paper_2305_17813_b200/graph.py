@@ -113,6 +113,13 @@ class Graph:
         check(_lib.lib().meerkat_set_stream(self._h, _stream_ptr(stream)), "meerkat_set_stream")
         self._tstream = _torch_stream(stream, self.device)
 
+    def probe_latency(self) -> dict:
+        """DRAM / L2 / atomic dependent-access latency and grid-barrier cost on this graph's device
+        (meerkat_probe_latency): the terms of the tree calls' latency floor."""
+        out = _lib.Latency()
+        check(_lib.lib().meerkat_probe_latency(self._h, ctypes.byref(out)), "meerkat_probe_latency")
+        return {k: getattr(out, k) for k, _ in _lib.Latency._fields_}
+
     def sync(self):
         check(_lib.lib().meerkat_sync(self._h), "meerkat_sync")
 

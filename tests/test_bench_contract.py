@@ -1,6 +1,7 @@
 """bench.py's JSON-line contract on the CPU: the reference arm (--impl reference times the oracle,
 the one arm that runs without a GPU) prints exactly one JSON line with the keys the driver reads,
-the same `config` as our arm and the cpu_baseline / e2e objects."""
+a `config` describing the oracle sample it timed (and the workload it samples), and the cpu_baseline /
+e2e objects."""
 import json
 import os
 import subprocess
@@ -21,7 +22,12 @@ def test_reference_arm_json_line():
               "scaling", "vs_baseline", "dtype", "data", "config", "impl", "cpu_baseline", "e2e"):
         assert k in d, k
     assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "edges/s"
-    assert d["config"]["workload"].startswith("rmat-s12-ef16") and d["config"]["batch"] == 500
+    # the config describes what was timed (the scale-11 sample), and names the workload it samples
+    assert d["config"]["workload"].startswith("rmat-s11-ef16") and d["config"]["batch"] == 500
+    assert d["config"]["sample_of"].startswith("rmat-s12-ef16")
+    assert d["config"]["vertices"] == 1 << 11 and d["config"]["edges"] > 0
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["cores"] == 1 and cb["value"] == d["value"] and "sample" in cb
+    assert cb["host_cores"] >= 1 and cb["cpu_model"] and cb["oracle_threads"] == 1
+    assert set(cb["per_batch_s"]) == {"apply_insert", "apply_delete", "sssp", "bfs"}
     assert d["e2e"] == {"value": d["value"], "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}

@@ -36,11 +36,11 @@ def test_empty_batches_everywhere():
     c = g.wcc()
     assert g.insert(E, E, E) == 0
     g.trees_incremental([sp, bf], E, E, E)
+    c.incremental(E, E)   # incremental WCC follows an insert batch (there is no decremental WCC)
     assert g.delete(E, E) == 0
     g.trees_decremental([sp, bf], E, E)
     f, qw = g.query(E, E)
     assert len(f) == 0
-    c.incremental(E, E)
     pr.update()
     assert pr.stats()["iterations"] == 1   # one verification super-step
     assert np.array_equal(sp.nodes(), o.sssp(0)[1]) and np.array_equal(bf.nodes(), o.bfs(0)[1])
