@@ -243,8 +243,11 @@ meerkat_status meerkat_tree_nodes(meerkat_tree* t, uint64_t* out);
 meerkat_status meerkat_tree_invalidated(meerkat_tree* t, uint32_t* out, uint64_t capacity, uint64_t* n_out);
 meerkat_status meerkat_tree_stats_get(meerkat_tree* t, meerkat_tree_stats* out); /* synchronises */
 /* Device timeline of the last single-GPU tree call: %globaltimer (ns) at kernel start and after
- * every grid-wide barrier (phase / round boundaries), up to 48 entries; *n_out = entries recorded. */
-meerkat_status meerkat_tree_timeline(meerkat_tree* t, uint64_t* out, uint64_t capacity, uint64_t* n_out);
+ * every grid-wide barrier (phase / round boundaries), up to 48 entries; *n_out = entries recorded.
+ * items (nullable, host [capacity]): items[i] = frontier items of the round that starts at entry i
+ * (summed over the call's trees; 0 for an entry that starts a non-round phase). */
+meerkat_status meerkat_tree_timeline(meerkat_tree* t, uint64_t* out, uint64_t* items, uint64_t capacity,
+                                     uint64_t* n_out);
 meerkat_status meerkat_tree_destroy(meerkat_tree* t);
 
 /* ---------------------------------------------------------------------------------------------

@@ -137,7 +137,7 @@ def lib():
         "meerkat_tree_invalidated": (ctypes.c_int, [vp, vp, u64, pu64]),
         "meerkat_tree_stats_get": (ctypes.c_int, [vp, ctypes.POINTER(TreeStats)]),
         "meerkat_tree_destroy": (ctypes.c_int, [vp]),
-        "meerkat_tree_timeline": (ctypes.c_int, [vp, pu64, u64, pu64]),
+        "meerkat_tree_timeline": (ctypes.c_int, [vp, pu64, pu64, u64, pu64]),
         "meerkat_check": (ctypes.c_int, [vp, pu64]),
         "meerkat_trees_incremental": (ctypes.c_int, [vp, pvp, u32, vp, vp, vp, u64]),
         "meerkat_trees_decremental": (ctypes.c_int, [vp, pvp, u32, vp, vp, u64]),

@@ -429,6 +429,7 @@ static meerkat_status tree_create(meerkat_graph* g, uint32_t source, bool unit, 
     }
   }
   t->version = g->version;
+  if (!vanilla) { g->n_trees++; t->counted = true; }
   *out = t;
   return MEERKAT_OK;
 }
@@ -690,7 +691,8 @@ meerkat_status meerkat_tree_stats_get(meerkat_tree* t, meerkat_tree_stats* out) 
   return MEERKAT_OK;
 }
 
-meerkat_status meerkat_tree_timeline(meerkat_tree* t, uint64_t* out, uint64_t capacity, uint64_t* n_out) {
+meerkat_status meerkat_tree_timeline(meerkat_tree* t, uint64_t* out, uint64_t* items, uint64_t capacity,
+                                     uint64_t* n_out) {
   if (!t || !n_out || (capacity && !out)) return MEERKAT_E_INVALID_ARG;
   meerkat_graph* g = t->g;
   DeviceGuard dg(g->device);
@@ -699,7 +701,10 @@ meerkat_status meerkat_tree_timeline(meerkat_tree* t, uint64_t* out, uint64_t ca
   if (e != cudaSuccess) return MEERKAT_E_CUDA;
   const uint64_t n = std::min<uint64_t>(t->hctrl->nts, 48);
   *n_out = n;
-  for (uint64_t i = 0; i < n && i < capacity; i++) out[i] = t->hctrl->tstamp[i];
+  for (uint64_t i = 0; i < n && i < capacity; i++) {
+    out[i] = t->hctrl->tstamp[i];
+    if (items) items[i] = t->hctrl->titems[i];
+  }
   return MEERKAT_OK;
 }
 
@@ -712,6 +717,7 @@ meerkat_status meerkat_tree_destroy(meerkat_tree* t) {
   cudaFree(T.fr[0]); cudaFree(T.fr[1]); cudaFree(t->ctrl_base); cudaFree(T.epoch_ptr);
   if (t->hctrl) cudaFreeHost(t->hctrl);
   dtree_free(t);
+  if (t->counted) t->g->n_trees--;
   delete t;
   return MEERKAT_OK;
 }

@@ -29,6 +29,7 @@ struct TreeCtrl {
   unsigned long long fp[2];         // fingerprint of the batch this call was given (ordering contract)
   unsigned long long nts;           // device timeline: %globaltimer at kernel start and after every grid barrier
   unsigned long long tstamp[48];
+  unsigned long long titems[48];    // frontier items of the round starting at timeline entry i (0: other phase)
 };
 
 // PageRank control block (pagerank.cu).  delta / dangling rotate over three slots per super-step.
@@ -85,6 +86,7 @@ struct meerkat_graph {
   int last_kind = 0;                // 0 none, 1 insert, 2 delete
   uint64_t last_n = 0;              // batch size of the last mutation (ordering contract)
   uint64_t last_delete_version = 0; // version created by the last delete batch (incremental WCC)
+  uint64_t n_trees = 0;             // live dynamic (tree-based) trees of this graph
   uint64_t launches = 0;
   int sm_count = 0;
   void* stage[4] = {nullptr, nullptr, nullptr, nullptr};   // staging for host inputs / outputs
@@ -110,6 +112,7 @@ struct meerkat_tree {
   mk::TreeCtrl* ctrl_base = nullptr;   // two control blocks: a call uses one and zeroes the other
   int parity = 0;
   int seeded = 0;   // 1 / 2: insert_batch_trees / delete_batch_trees ran this call's batch prologue
+  bool counted = false;   // counted in g->n_trees
   // vertex-partitioned trees (dtree.cu)
   bool dist = false;
   int cur = 0;                              // frontier buffer filled by the last phase

@@ -238,7 +238,8 @@ struct UpdArgs {
   const uint32_t* w;
   uint64_t n;
   uint32_t ns;   // stores updated: 1 or 2
-  uint32_t fp_slot;   // plain mutation: batch fingerprint slot of the version it creates (version & 1)
+  uint32_t fp_slot;   // batch fingerprint slot of the version this mutation creates (version & 1)
+  uint32_t fp_on;     // 1: accumulate the batch fingerprint (some tree may follow with an unseeded call)
   // fused tree prologue (PRO != 0 kernels): the trees the following tree call updates
   TreeDev T[MAX_TREES];
   uint32_t ntrees;
@@ -263,20 +264,21 @@ __device__ __forceinline__ void upd_tree_prologue(const UpdArgs& A) {
   FOR_TREES(k, A) flush_counters(A.G[0], A.T[k], c, k, false, 0, 0);
 }
 
-// Batch fingerprint bookkeeping (ordering contract): a plain mutation (PRO == 0) accumulates the
-// fingerprint of its batch into slot fp_slot and zeroes the other slot; a seeding mutation (whose
-// tree call reads no batch) zeroes both, so the next plain mutation starts from a clean slot.
+// Batch fingerprint bookkeeping (ordering contract): with fp_on the mutation accumulates the
+// fingerprint of its batch into slot fp_slot and zeroes the other slot; without (a seeding mutation
+// that seeds every tree of the graph: no tree call will read a batch) it zeroes both, so the next
+// accumulating mutation starts from a clean slot.
 template <int PRO>
 __device__ __forceinline__ void upd_fp_begin(const UpdArgs& A) {
   if (blockIdx.x != 0 || threadIdx.x != 0) return;
   unsigned long long* f = &A.G[0].ctrl->fp[0][0];
-  if (PRO != 0) { f[0] = 0; f[1] = 0; f[2] = 0; f[3] = 0; }
+  if (!A.fp_on) { f[0] = 0; f[1] = 0; f[2] = 0; f[3] = 0; }
   else { f[2 * (A.fp_slot ^ 1)] = 0; f[2 * (A.fp_slot ^ 1) + 1] = 0; }
 }
 
 template <int PRO>
 __device__ __forceinline__ void upd_fp_end(const UpdArgs& A, uint64_t fa, uint64_t fb) {
-  if constexpr (PRO == 0) block_add2_u64(&A.G[0].ctrl->fp[A.fp_slot][0], fa, fb);
+  if (A.fp_on) block_add2_u64(&A.G[0].ctrl->fp[A.fp_slot][0], fa, fb);
 }
 
 template <int PRO>
@@ -314,7 +316,7 @@ __global__ void __launch_bounds__(UPD_BLOCK, UPD_MINB) k_insert(const __grid_con
     upd_item(A, i, st, e);
     const GraphDev& G = A.G[st];
     const uint32_t a = A.src[e], b = A.dst[e], wt = MAP ? A.w[e] : 0u;
-    if (PRO == 0 && st == 0 && l8 == 0) fp_edge(a, b, wt, fa, fb);
+    if (A.fp_on && st == 0 && l8 == 0) fp_edge(a, b, wt, fa, fb);
     const uint32_t u = st ? b : a, v = st ? a : b;
     if (u >= G.Vg || v >= G.Vg) { err.set(st, ERR_RANGE); continue; }
     if (MAP && (wt == 0 || wt >= W_LIMIT)) { err.set(st, ERR_WEIGHT); continue; }
@@ -394,7 +396,7 @@ __global__ void __launch_bounds__(UPD_BLOCK, UPD_MINB) k_delete(const __grid_con
     upd_item(A, i, st, e);
     const GraphDev& G = A.G[st];
     const uint32_t a = A.src[e], b = A.dst[e];
-    if (PRO == 0 && st == 0 && l8 == 0) fp_edge(a, b, 0u, fa, fb);
+    if (A.fp_on && st == 0 && l8 == 0) fp_edge(a, b, 0u, fa, fb);
     const uint32_t u = st ? b : a, v = st ? a : b;
     if (u >= G.Vg || v >= G.Vg) { err.set(st, ERR_RANGE); continue; }
     const uint32_t ul = local_row(G, u);
@@ -501,7 +503,7 @@ __global__ void __launch_bounds__(UPD_BLOCK, UPD_T_MINB) k_insert_t(const __grid
     upd_item(A, i, st, e);
     const GraphDev& G = A.G[st];
     const uint32_t a = A.src[e], b = A.dst[e], wt = MAP ? A.w[e] : 0u;
-    if (PRO == 0 && st == 0) fp_edge(a, b, wt, fa, fb);
+    if (A.fp_on && st == 0) fp_edge(a, b, wt, fa, fb);
     const uint32_t u = st ? b : a, v = st ? a : b;
     if (u >= G.Vg || v >= G.Vg) { err.set(st, ERR_RANGE); continue; }
     if (MAP && (wt == 0 || wt >= W_LIMIT)) { err.set(st, ERR_WEIGHT); continue; }
@@ -530,7 +532,7 @@ __global__ void __launch_bounds__(UPD_BLOCK, UPD_T_MINB) k_delete_t(const __grid
     upd_item(A, i, st, e);
     const GraphDev& G = A.G[st];
     const uint32_t a = A.src[e], b = A.dst[e];
-    if (PRO == 0 && st == 0) fp_edge(a, b, 0u, fa, fb);
+    if (A.fp_on && st == 0) fp_edge(a, b, 0u, fa, fb);
     const uint32_t u = st ? b : a, v = st ? a : b;
     if (u >= G.Vg || v >= G.Vg) { err.set(st, ERR_RANGE); continue; }
     const uint32_t ul = local_row(G, u);
@@ -839,8 +841,11 @@ static void delete_kind(meerkat_graph* g, const UpdArgs& A, bool thread, unsigne
 }
 #undef UPD_LAUNCH
 
-static void set_pro(UpdArgs& A, const TreePro* pro) {
+static void set_pro(meerkat_graph* g, UpdArgs& A, const TreePro* pro) {
   A.ntrees = pro ? pro->ntrees : 0u;
+  // a tree of g that this mutation does not seed may follow with an unseeded call, which checks the
+  // batch against the fingerprint; if every dynamic tree is seeded, no call reads the batch
+  A.fp_on = (!pro || (uint64_t)pro->ntrees < g->n_trees) ? 1u : 0u;
   if (pro)
     for (int k = 0; k < MAX_TREES; k++) A.T[k] = pro->T[k];
 }
@@ -853,7 +858,7 @@ cudaError_t launch_insert(meerkat_graph* g, Store* st0, Store* st1, const uint32
   if (st1) A.G[1] = st1->dev;
   A.src = s; A.dst = d; A.w = w; A.n = n; A.ns = st1 ? 2u : 1u;
   A.fp_slot = (uint32_t)((g->version + 1) & 1);   // the version this mutation creates
-  set_pro(A, pro);
+  set_pro(g, A, pro);
   const bool thread = thread_upd(n * A.ns);
   const unsigned grid = thread ? grid_threads(g, n * A.ns) : grid_for(g, n * A.ns, 0);
   if (A.G[0].upd) {
@@ -875,7 +880,7 @@ cudaError_t launch_delete(meerkat_graph* g, Store* st0, Store* st1, const uint32
   if (st1) A.G[1] = st1->dev;
   A.src = s; A.dst = d; A.w = nullptr; A.n = n; A.ns = st1 ? 2u : 1u;
   A.fp_slot = (uint32_t)((g->version + 1) & 1);   // the version this mutation creates
-  set_pro(A, pro);
+  set_pro(g, A, pro);
   const bool thread = thread_upd(n * A.ns);
   const unsigned grid = thread ? grid_threads(g, n * A.ns) : grid_for(g, n * A.ns, 0);
   if (g->weighted) delete_kind<true>(g, A, thread, grid);

@@ -261,6 +261,11 @@ __device__ __forceinline__ uint32_t run_rounds(const TreeArgs& A, const uint32_t
       any |= n[k] != 0;
     }
     if (!any) break;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {   // diagnostics: this round's size beside its timeline entry
+      TreeCtrl* tc = A.T[0].ctrl;
+      const unsigned long long i = tc->nts;
+      if (i > 0 && i <= 48) tc->titems[i - 1] = n[0] + n[1];
+    }
     if (n[0] + n[1] <= TAIL_ITEMS) {
       // Tail: a frontier this small is one chain per item for block 0's groups alone, so block 0
       // runs the rounds with block barriers (~0.1 us) instead of grid barriers (~2 us) while the
@@ -285,6 +290,11 @@ __device__ __forceinline__ uint32_t run_rounds(const TreeArgs& A, const uint32_t
           any = false;
 #pragma unroll
           for (int k = 0; k < MAX_TREES; k++) { n[k] = s_n[k]; any |= n[k] != 0; }
+          if (threadIdx.x == 0) {
+            TreeCtrl* tc = A.T[0].ctrl;
+            const unsigned long long i = tc->nts;
+            if (any && i > 0 && i <= 48) tc->titems[i - 1] = n[0] + n[1];
+          }
           __syncthreads();   // s_n is rewritten by the next iteration / the resumed loop
           if (!any || n[0] + n[1] > TAIL_ITEMS) break;
         }

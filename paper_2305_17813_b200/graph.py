@@ -366,13 +366,16 @@ class Tree:
               "meerkat_tree_invalidated")
         return np.sort(a[: int(n.value)])
 
-    def timeline(self):
-        """Device timestamps (ns) of the last call: start and every grid barrier; returns deltas in us."""
+    def timeline(self, items: bool = False):
+        """Device timestamps (ns) of the last call: start and every grid barrier; returns the deltas in
+        us (with items=True, pairs (us, frontier items of that interval's round, 0 for other phases))."""
         buf = (ctypes.c_uint64 * 48)()
+        itm = (ctypes.c_uint64 * 48)()
         n = ctypes.c_uint64(0)
-        check(_lib.lib().meerkat_tree_timeline(self._h, buf, 48, ctypes.byref(n)), "meerkat_tree_timeline")
+        check(_lib.lib().meerkat_tree_timeline(self._h, buf, itm, 48, ctypes.byref(n)), "meerkat_tree_timeline")
         ts = [int(buf[i]) for i in range(int(n.value))]
-        return [(b - a) / 1e3 for a, b in zip(ts, ts[1:])]
+        dt = [(b - a) / 1e3 for a, b in zip(ts, ts[1:])]
+        return [(x, int(itm[i])) for i, x in enumerate(dt)] if items else dt
 
     def stats(self) -> dict:
         st = _lib.TreeStats()

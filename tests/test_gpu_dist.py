@@ -93,7 +93,8 @@ def _worker(rank, ws, port, backend, scale, q):
             dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("ws,backend,scale", [(1, "nccl", 12), (2, "gloo", 12), (3, "gloo", 13)])
+@pytest.mark.parametrize("ws,backend,scale", [(1, "nccl", 12), (2, "gloo", 12), (3, "gloo", 13), (4, "gloo", 12),
+                                             (8, "gloo", 12)])
 def test_partitioned_dynamic_sssp_bfs(ws, backend, scale):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
