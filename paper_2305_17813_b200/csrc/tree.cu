@@ -33,11 +33,41 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
 
 #include "tree_common.cuh"
 
 
 namespace mk {
+
+#ifdef MEERKAT_DIAG_ROUNDS
+// Diagnostics build only (-DMEERKAT_DIAG_ROUNDS; the atomics below perturb the timing): per round,
+// the earliest group entry and latest group exit (%globaltimer), the longest group busy time, items,
+// and a histogram of group busy times (1-us buckets); printed by block 0 at kernel end.
+constexpr int DIAG_R = 64;
+__device__ unsigned long long g_tmin[DIAG_R] /* ~earliest entry */, g_tmax[DIAG_R], g_busy[DIAG_R], g_items[DIAG_R];
+__device__ unsigned int g_hist[DIAG_R][16];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ void diag_dump() {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  unsigned long long prev = 0;
+  for (int r = 0; r < DIAG_R; r++) {
+    if (!g_tmax[r]) continue;
+    printf("DIAG r%02d items %6llu span %6.2f busymax %6.2f gap_before %6.2f hist", r, g_items[r],
+           (g_tmax[r] - ~g_tmin[r]) / 1e3, g_busy[r] / 1e3, prev ? ((double)~g_tmin[r] - (double)prev) / 1e3 : 0.0);
+    for (int b = 0; b < 16; b++) printf(" %u", g_hist[r][b]);
+    printf("\n");
+    prev = g_tmax[r];
+    g_tmin[r] = 0; g_tmax[r] = 0; g_busy[r] = 0; g_items[r] = 0;
+    for (int b = 0; b < 16; b++) g_hist[r][b] = 0;
+  }
+  printf("DIAG end\n");
+}
+#endif
 
 // Next item of this group (grid-stride over [it, n)): vertex and slab come from the item.
 // An item whose slab is LINKING was enqueued by the insert kernel's fused prologue before v's
@@ -68,7 +98,11 @@ __device__ __forceinline__ bool fetch_item(const GraphDev& S, const uint64_t* fr
 template <bool MAP, int VISIT, bool V32 = false, bool BLOCK = false>
 __device__ __forceinline__ void expand(const TreeArgs& A, const TreeDev& T, int k, const uint64_t* fr, uint64_t n,
                                        uint64_t* fnext, unsigned long long* sznext, uint32_t epoch_next,
-                                       Counters& c) {
+                                       Counters& c, int diag_round = DIAG_PULL) {
+#ifdef MEERKAT_DIAG_ROUNDS
+  const unsigned long long t_enter = gtime();
+  uint32_t d_items = 0;
+#endif
   using F = Frag<MAP>;
   constexpr int NK = F::NK;
   const GraphDev& G = A.G;
@@ -233,9 +267,24 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const TreeDev& T, int 
     if (active) {
       if (nxt != INVALID_SLAB && !dead) slab = nxt;
       else if (T.scheme1 && !dead && b + 1 < nb) { b++; slab = head0 + b; }
-      else { it += ng; active = fetch_item(S, fr, n, it, ng, v, slab, l8, c); fresh = active; }
+      else {
+#ifdef MEERKAT_DIAG_ROUNDS
+        d_items++;
+#endif
+        it += ng; active = fetch_item(S, fr, n, it, ng, v, slab, l8, c); fresh = active;
+      }
     }
   }
+#ifdef MEERKAT_DIAG_ROUNDS
+  if (!BLOCK && l8 == 0 && d_items && diag_round >= 0 && diag_round < DIAG_R) {
+    const unsigned long long t_exit = gtime(), busy = t_exit - t_enter;
+    atomicMax(&g_tmin[diag_round], ~t_enter);   // holds ~(earliest entry): zero-initialised works
+    atomicMax(&g_tmax[diag_round], t_exit);
+    atomicMax(&g_busy[diag_round], busy);
+    atomicAdd(&g_items[diag_round], (unsigned long long)d_items);
+    atomicAdd(&g_hist[diag_round][min(15ull, busy / 1000)], 1u);
+  }
+#endif
 }
 
 // Frontier rounds of all trees of the call, until every frontier is empty.  Round r reads
@@ -301,6 +350,7 @@ __device__ __forceinline__ uint32_t run_rounds(const TreeArgs& A, const uint32_t
         if (threadIdx.x == 0) A.T[0].ctrl->tail_r = r;
       }
       grid.sync();
+      timeline(A.T[0].ctrl);   // every block resumed after block 0's tail rounds
       if (threadIdx.x == 0) s_n[0] = __ldcg(&A.T[0].ctrl->tail_r);
       __syncthreads();
       r = (uint32_t)s_n[0];
@@ -314,7 +364,7 @@ __device__ __forceinline__ uint32_t run_rounds(const TreeArgs& A, const uint32_t
       if (!n[k]) continue;
       const TreeDev& T = A.T[k];
       expand<MAP, VISIT, V32>(A, T, k, T.fr[r & 1], n[k], T.fr[(r + 1) & 1], &T.ctrl->size[(r + 1) % 3],
-                              epoch[k] + r + 1, c);
+                              epoch[k] + r + 1, c, (VISIT == PROPAGATE ? 0 : 20) + (int)r);
     }
     grid.sync();
     timeline(A.T[0].ctrl);
@@ -350,6 +400,10 @@ __device__ __forceinline__ bool tree_call_admitted(const TreeArgs& A, cg::grid_g
 
 __device__ __forceinline__ void finish(const TreeArgs& A, Counters& c, const uint32_t* epoch, bool owner,
                                        uint32_t rounds_total, uint32_t relax_rounds, uint32_t prop_rounds) {
+  timeline(A.T[0].ctrl);
+#ifdef MEERKAT_DIAG_ROUNDS
+  diag_dump();
+#endif
   FOR_TREES(k, A) {
     if (owner) *A.T[k].epoch_ptr = epoch[k] + rounds_total + 2;   // every thread read the base before a barrier
     flush_counters(A.G, A.T[k], c, k, owner, relax_rounds, prop_rounds);

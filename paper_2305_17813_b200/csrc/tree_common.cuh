@@ -25,6 +25,7 @@ constexpr uint64_t PROBE_MIN_ITEMS = 65536;
 constexpr uint64_t TAIL_ITEMS = MEERKAT_TAIL_ITEMS;   // frontiers this small run in block 0 alone (run_rounds)
 
 enum Visit { RELAX = 0, PROPAGATE = 1, PULL = 2 };
+constexpr int DIAG_PULL = 19;   // diagnostics round slot of the pull phase (MEERKAT_DIAG_ROUNDS builds)
 
 // Loop over the trees of a call with a compile-time index, so per-tree register arrays (Counters,
 // epochs, frontier sizes) stay in registers: a runtime index puts them in local memory.
