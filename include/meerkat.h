@@ -163,6 +163,12 @@ meerkat_status meerkat_query_batch(meerkat_graph* g, const uint32_t* src, const 
 meerkat_status meerkat_export_edges(meerkat_graph* g, uint32_t* src, uint32_t* dst, uint32_t* w,
                                     uint64_t capacity, uint64_t* n_out);
 meerkat_status meerkat_stats_get(meerkat_graph* g, meerkat_stats* out); /* synchronises */
+/* Stream-ordered copy of the out-store's cumulative counters into out[3] (host pinned or device
+ * memory): out[0] = edges inserted so far (counted as in insert_batch), out[1] = edges deleted so far,
+ * out[2] = growth-pool slabs handed out.  Live edges = out[0] - out[1].  Does NOT synchronise: the
+ * values are valid once the graph's stream has reached this point (e.g. after an event on it), which
+ * lets a pipelined caller read each step's result without stalling the next step's copies. */
+meerkat_status meerkat_counters_async(meerkat_graph* g, uint64_t* out);
 
 /* Latency probes for the latency floor of the tree calls (SURVEY §8(d) "latency term"; a frontier
  * round is a chain of dependent memory operations closed by a grid barrier, P:108-112 / P:2189-2207):

@@ -41,7 +41,7 @@ EXPORTS = [
     "meerkat_wcc_create", "meerkat_wcc_recompute", "meerkat_wcc_incremental", "meerkat_wcc_labels",
     "meerkat_wcc_components", "meerkat_wcc_destroy", "meerkat_tree_recompute_scheme",
     "meerkat_wcc_incremental_tracked", "meerkat_dtrees_pack", "meerkat_dtrees_apply", "meerkat_dtrees_scan",
-    "meerkat_dtrees_expand", "meerkat_probe_latency",
+    "meerkat_dtrees_expand", "meerkat_probe_latency", "meerkat_counters_async",
 ]
 
 
@@ -173,6 +173,7 @@ def lib():
         "meerkat_dtrees_scan": (ctypes.c_int, [vp, pvp, u32, pvp, pu64, ctypes.POINTER(DResult)]),
         "meerkat_dtrees_expand": (ctypes.c_int, [vp, pvp, u32, ctypes.c_int, ctypes.POINTER(DResult)]),
         "meerkat_probe_latency": (ctypes.c_int, [vp, ctypes.POINTER(Latency)]),
+        "meerkat_counters_async": (ctypes.c_int, [vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -345,6 +345,16 @@ meerkat_status meerkat_check(meerkat_graph* g, uint64_t* info) {
   return info[0] ? MEERKAT_E_STATE : MEERKAT_OK;
 }
 
+meerkat_status meerkat_counters_async(meerkat_graph* g, uint64_t* out) {
+  if (!g || !out) return MEERKAT_E_INVALID_ARG;
+  DeviceGuard dg(g->device);
+  const GraphCtrl* c = g->out.dev.ctrl;
+  cudaError_t e = cudaMemcpyAsync(out, &c->ins_total, 8, cudaMemcpyDefault, g->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out + 1, &c->del_total, 8, cudaMemcpyDefault, g->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out + 2, &c->pool_top, 8, cudaMemcpyDefault, g->stream);
+  return from_cuda(e);
+}
+
 meerkat_status meerkat_stats_get(meerkat_graph* g, meerkat_stats* out) {
   if (!g || !out) return MEERKAT_E_INVALID_ARG;
   DeviceGuard dg(g->device);
@@ -882,7 +892,10 @@ meerkat_status meerkat_pagerank_stats_get(meerkat_pagerank* p, meerkat_pagerank_
   // gather per in-edge, 8 B atomicAdd per combined slab run, 44 B per vertex update (acc r/w, PR r/w,
   // out[] r, Contribution w); plus the start, 28 B per vertex (PR r/w, out[] r, Contribution w, acc w)
   const uint64_t V = p->g->V;
-  out->alg_bytes = c.iters * (c.slabs * 132 + c.keys * 8 + c.atomics * 8 + V * 44) + V * 28;
+  // per super-step: slab + owner per in-slab, one Contribution gather per in-edge, one fp64 atomic per
+  // combined run, per vertex acc r/w + PR r/w + out r + Contribution w; once: the initial pass
+  const uint64_t cb = pagerank_contrib_bytes();
+  out->alg_bytes = c.iters * (c.slabs * 132 + c.keys * cb + c.atomics * 8 + V * (36 + cb)) + V * (20 + cb);
   out->version = p->version;
   out->warm = p->warm_last ? 1u : 0u;
   return MEERKAT_OK;

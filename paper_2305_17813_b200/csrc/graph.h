@@ -162,6 +162,7 @@ cudaError_t launch_tc_count(meerkat_graph* g1, meerkat_graph* g2, const uint32_t
 // pagerank.cu
 cudaError_t pagerank_occupancy(bool weighted, int* blocks_per_sm);
 cudaError_t launch_pagerank(meerkat_graph* g, meerkat_pagerank* p, bool warm);
+size_t pagerank_contrib_bytes();   // bytes per cached Contribution[u] (4: fp32 cache, 8: fp64)
 // store.cu
 cudaError_t launch_build(meerkat_graph* g, Store& st, const uint32_t* d_hints, uint64_t pool_request);
 void free_store(Store& st);

@@ -29,6 +29,7 @@
 #include <cooperative_groups.h>
 
 #include "graph.h"
+#include "stream.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -40,12 +41,18 @@ constexpr int PR_BLOCK = 512;
 #endif
 constexpr int PR_MINB = MEERKAT_PR_MINB;
 constexpr int PR_UNROLL = 2;   // slabs in flight per group (register double-buffered)
+using contrib_t = double;   // Contribution[] in fp64 (an fp32 cache was 5.5 % faster and broke the
+                            // closed-form pins' tolerance: DESIGN.md §10)
+size_t pagerank_contrib_bytes() { return sizeof(contrib_t); }
+#ifndef MEERKAT_PR_BULK
+#define MEERKAT_PR_BULK 0   // 1: the slab / owner stream moves by bulk copies through shared memory (stream.cuh; A/B: slower)
+#endif
 
 struct PRArgs {
   GraphDev R;               // in-edge store: owner[s] = v, keys = sources u
   const uint32_t* outdeg;   // out-store degree table: out[u]
   double* pr;
-  double* contrib;
+  contrib_t* contrib;   // Contribution[u] = PR[u] / out[u] (FindContributionPerVertex)
   double* acc;
   PRCtrl* ctrl;
   uint32_t V;
@@ -77,6 +84,53 @@ __device__ __forceinline__ void block_add2(double a, double b, double* da, doubl
     }
   }
   __syncthreads();
+}
+
+// Compute for one in-edge slab of owner o (this lane's fragment d): gather Contribution[u]
+// of its live keys, reduce in the group, combine runs of one owner over the warp's four groups (four
+// consecutive slabs), one fp64 atomicAdd into acc[o] per run.  Warp-collective.
+// Two slabs per call (two chunks of the bulk stream): every gather of both is issued first.
+template <bool MAP>
+__device__ __forceinline__ void pr_gather(const PRArgs& A, const uint4& d, bool count, unsigned long long& keys,
+                                          double (&cs)[Frag<MAP>::NK]) {
+  using F = Frag<MAP>;
+  const int l8 = threadIdx.x & 7;
+#pragma unroll
+  for (int k = 0; k < F::NK; k++) {
+    const uint32_t u = F::key(d, k);
+    const bool live = u < A.V && (MAP || F::valid_cell(l8, k));   // sentinels are >= V
+    cs[k] = live ? (double)__ldcg(A.contrib + u) : 0.0;
+    if (count && live) keys++;
+  }
+}
+
+template <bool MAP>
+__device__ __forceinline__ void pr_combine(const PRArgs& A, const double (&cs)[Frag<MAP>::NK], uint32_t o, bool count,
+                                           unsigned long long& atomics) {
+  using F = Frag<MAP>;
+  constexpr int NK = F::NK;
+  const int lane = threadIdx.x & 31, l8 = lane & 7;
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < NK; k++) s += cs[k];
+  s += __shfl_xor_sync(0xFFFFFFFFu, s, 1);
+  s += __shfl_xor_sync(0xFFFFFFFFu, s, 2);
+  s += __shfl_xor_sync(0xFFFFFFFFu, s, 4);
+  const uint32_t po = __shfl_up_sync(0xFFFFFFFFu, o, GROUP);
+  const bool head = lane < GROUP || po != o;
+  double tot = s;
+  bool run = true;
+#pragma unroll
+  for (int k = 1; k < 4; k++) {
+    const double sk = __shfl_down_sync(0xFFFFFFFFu, s, GROUP * k);
+    const uint32_t ok = __shfl_down_sync(0xFFFFFFFFu, o, GROUP * k);
+    run = run && lane + GROUP * k < 32 && ok == o;
+    if (run) tot += sk;
+  }
+  if (l8 == 0 && head && o != NO_OWNER && tot != 0.0) {
+    atomicAdd(A.acc + o, tot);
+    if (count) atomics++;
+  }
 }
 
 // Compute as a stream over the in-edge slabs [0, n_slabs): acc[v] += Contribution[u]
@@ -124,7 +178,7 @@ __device__ __forceinline__ void pr_accumulate(const PRArgs& A, uint32_t n_slabs,
       for (int k = 0; k < NK; k++) {
         const uint32_t u = F::key(d[q], k);
         const bool live = u < V && (MAP || F::valid_cell(l8, k));   // sentinels are >= V
-        c[q][k] = live ? __ldcg(A.contrib + u) : 0.0;
+        c[q][k] = live ? (double)__ldcg(A.contrib + u) : 0.0;
         if (count && live) keys++;
       }
 #pragma unroll
@@ -159,6 +213,11 @@ __device__ __forceinline__ void pr_accumulate(const PRArgs& A, uint32_t n_slabs,
 template <bool MAP>
 __global__ void __launch_bounds__(PR_BLOCK, PR_MINB) k_pagerank(const __grid_constant__ PRArgs A) {
   cg::grid_group grid = cg::this_grid();
+#if MEERKAT_PR_BULK
+  __shared__ StreamSmem sm;
+  uint32_t seq = 0;
+  stream_init(sm);
+#endif
   PRCtrl* C = A.ctrl;
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
   const uint32_t V = A.V;
@@ -171,7 +230,7 @@ __global__ void __launch_bounds__(PR_BLOCK, PR_MINB) k_pagerank(const __grid_con
       if (A.warm) p = A.pr[v];
       else { p = invN; A.pr[v] = p; }
       const uint32_t o = A.outdeg[v];
-      A.contrib[v] = o ? p / (double)o : 0.0;
+      A.contrib[v] = (contrib_t)(o ? p / (double)o : 0.0);
       if (!o) dang += p;
       A.acc[v] = 0.0;
     }
@@ -184,7 +243,18 @@ __global__ void __launch_bounds__(PR_BLOCK, PR_MINB) k_pagerank(const __grid_con
   uint32_t i = 0;
   for (;; i++) {
     // Compute: acc[v] = sum over in-edges of Contribution[u]
+#if MEERKAT_PR_BULK
+    stream_slabs<2>(sm, seq, A.R.slabs, A.R.owner, n_slabs,
+                    [&](const uint4& d0, uint32_t o0, uint32_t, const uint4& d1, uint32_t o1, uint32_t) {
+                      double c0[Frag<MAP>::NK], c1[Frag<MAP>::NK];
+                      pr_gather<MAP>(A, d0, i == 0, keys, c0);
+                      pr_gather<MAP>(A, d1, i == 0, keys, c1);
+                      pr_combine<MAP>(A, c0, o0, i == 0, atomics);
+                      pr_combine<MAP>(A, c1, o1, i == 0, atomics);
+                    });
+#else
     pr_accumulate<MAP>(A, n_slabs, i == 0, keys, atomics);
+#endif
     grid.sync();
     // PR_i = (1-d)/N + d*acc (+ teleport), delta, next contributions and dangling mass
     const double teleport = A.d * __ldcg(&C->dangling[i % 3]) / (double)V;
@@ -196,7 +266,7 @@ __global__ void __launch_bounds__(PR_BLOCK, PR_MINB) k_pagerank(const __grid_con
       dl += fabs(p - old);
       A.pr[v] = p;
       const uint32_t o = A.outdeg[v];
-      A.contrib[v] = o ? p / (double)o : 0.0;
+      A.contrib[v] = (contrib_t)(o ? p / (double)o : 0.0);   // gathered next super-step
       if (!o) dn += p;
       A.acc[v] = 0.0;
     }
@@ -233,7 +303,7 @@ cudaError_t launch_pagerank(meerkat_graph* g, meerkat_pagerank* p, bool warm) {
   PRArgs A;
   A.R = g->in.dev;
   A.outdeg = g->out.dev.deg;
-  A.pr = p->pr; A.contrib = p->contrib; A.acc = p->acc;
+  A.pr = p->pr; A.contrib = reinterpret_cast<contrib_t*>(p->contrib); A.acc = p->acc;
   A.ctrl = p->ctrl;
   A.V = g->V;
   A.max_iter = p->max_iter;

@@ -35,6 +35,7 @@
 #include <algorithm>
 #include <cstdio>
 
+#include "stream.cuh"
 #include "tree_common.cuh"
 
 
@@ -477,9 +478,72 @@ __global__ void __launch_bounds__(TREE_BLOCK, TREE_MINB) k_tree_inc(const __grid
 // double-buffered so loads are always in flight); owner[] names the source vertex.  Fast path
 // per key and tree: one shared-memory filter probe.  Slow path (warp-uniform, only for positions
 // where some lane hit a filter): exact bit-set test, source validity, relaxation and enqueue.
+// One slab of the scan (this lane's fragment d, source u = owner[s]): the filter fast path, then the
+// warp-uniform slow path for the positions where some lane hit.  Warp-collective.
+template <bool MAP>
+__device__ __forceinline__ void scan_slab(const TreeArgs& A, const uint32_t* filt, bool use_filter, const uint4& d,
+                                          uint32_t u, uint32_t r1, const uint32_t* epoch, Counters& c) {
+  using F = Frag<MAP>;
+  constexpr int NK = F::NK;
+  const GraphDev& G = A.G;
+  const uint32_t V = G.V;
+  const int l8 = lane_id() & 7;
+  uint32_t hm = 0;
+#pragma unroll
+  for (int kk = 0; kk < NK; kk++) {
+    const uint32_t x = F::key(d, kk);
+    bool hit = x < V && (MAP || F::valid_cell(l8, kk));   // live key (sentinels are >= V)
+    if (use_filter) {
+      uint32_t w, m;
+      filter_loc(x, 32 - FILTER_LOG2, w, m);
+      hit = hit && (filt[w] & m) == m;
+    }
+    hm |= (uint32_t)hit << kk;
+  }
+  const uint32_t pos = __reduce_or_sync(FULL, hm);
+  if (!pos) return;
+#pragma unroll
+  for (int kk = 0; kk < NK; kk++) {
+    if (!((pos >> kk) & 1u)) continue;   // warp-uniform
+    const uint32_t x = F::key(d, kk);
+    const bool cand = (hm >> kk) & 1u;
+#pragma unroll
+    for (int k = 0; k < MAX_TREES; k++) {
+      if (k >= (int)A.ntrees) break;
+      const TreeDev& T = A.T[k];
+      bool enq = false;
+      if (cand && bit_test(T.inval_bits, x)) {
+        // x in V_invalid of tree k: is the slab's source vertex u valid and reached in it?
+        if (u != NO_OWNER && !bit_test(T.inval_bits, u)) {
+          const uint64_t nu = ld_cg_u64(T.node + u);
+          if (nu != UNREACHED) {
+            c.hits[k]++;
+            const uint32_t w = T.unit ? 1u : F::weight(d, kk);
+            enq = relax(T, x, (nu >> 32) + w, u, epoch[k] + r1, c);
+          }
+        }
+      }
+      warp_enqueue(G, T, T.fr[r1 & 1], &T.ctrl->size[r1 % 3], enq, x, c);
+    }
+  }
+}
+
+#ifndef MEERKAT_SCAN_BULK
+#define MEERKAT_SCAN_BULK 0   // 1: the scan's slab / owner stream moves by bulk copies (stream.cuh; A/B: 3x slower)
+#endif
+
 template <bool MAP>
 __device__ __forceinline__ void dec_scan(const TreeArgs& A, const uint32_t* filt, bool use_filter, uint32_t n_slabs,
                                          uint32_t r1, const uint32_t* epoch, Counters& c) {
+#if MEERKAT_SCAN_BULK
+  __shared__ StreamSmem sm;
+  uint32_t seq = 0;
+  stream_init(sm);
+  stream_slabs(sm, seq, A.G.slabs, A.G.owner, n_slabs, [&](const uint4& d, uint32_t u, uint32_t) {
+    scan_slab<MAP>(A, filt, use_filter, d, u, r1, epoch, c);
+  });
+  return;
+#endif
   using F = Frag<MAP>;
   constexpr int NK = F::NK;
   constexpr int U = SCAN_UNROLL;

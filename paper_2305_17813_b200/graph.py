@@ -202,6 +202,13 @@ class Graph:
         _lib.lib().meerkat_check(self._h, info)
         return tuple(int(x) for x in info)
 
+    def counters_async(self, out):
+        """Enqueue a copy of the cumulative counters (inserted, deleted, pool slabs) into `out`, a
+        3-element uint64/int64 tensor (pinned host or CUDA) or array, on the graph's stream; no
+        synchronisation (meerkat_counters_async)."""
+        ptr = out.data_ptr() if _is_torch(out) else out.ctypes.data
+        check(_lib.lib().meerkat_counters_async(self._h, ctypes.c_void_p(ptr)), "meerkat_counters_async")
+
     def stats(self) -> dict:
         st = _lib.Stats()
         check(_lib.lib().meerkat_stats_get(self._h, ctypes.byref(st)), "meerkat_stats_get")
