@@ -154,3 +154,27 @@ def test_wcc_incremental_checks():
     _state_error(lambda: c.incremental(cuda(s[:9]), cuda(d[:9])))
     c.incremental(cuda(s[:10]), cuda(d[:10]))
     g.close()
+
+
+def test_counters_async_and_latency_probe():
+    """meerkat_counters_async: the cumulative insert / delete counters copied on the graph's stream
+    (no synchronisation) equal the synchronous counts; meerkat_probe_latency returns plausible,
+    positive latencies on the graph's device."""
+    g, o, V = _setup()
+    rng = np.random.default_rng(4)
+    bs, bd, bw = _fresh_batch(o, V, rng)
+    out = torch.zeros(3, dtype=torch.int64).pin_memory()
+    n0 = g.stats()["edges"]
+    g.insert(cuda(bs), cuda(bd), cuda(bw), count=False)
+    g.delete(cuda(bs[:10]), cuda(bd[:10]), count=False)
+    g.counters_async(out)
+    torch.cuda.synchronize()
+    ins, dele, pool = (int(x) for x in out.tolist())
+    assert ins - dele == n0 + len(bs) - 10 == g.stats()["edges"]
+    dev = torch.zeros(3, dtype=torch.int64, device="cuda")
+    g.counters_async(dev)
+    assert dev.cpu().tolist() == out.tolist()
+    lat = g.probe_latency()
+    assert 0 < lat["l2_load_ns"] < lat["dram_load_ns"] < 5000 and 0 < lat["grid_sync_us"] < 100
+    assert lat["grid_blocks"] > 0
+    g.close()
