@@ -48,7 +48,8 @@ def parse():
     p.add_argument("--scale", type=int, default=24)
     p.add_argument("--ef", type=int, default=16)
     p.add_argument("--batch", type=int, default=100_000)
-    p.add_argument("--lf", type=float, default=0.7)
+    p.add_argument("--lf", type=float, default=0.5,
+                   help="load factor of the slab stores (SURVEY C22: a performance knob the paper leaves open; 0.5 measured best for the config-3 step, DESIGN.md §10)")
     p.add_argument("--no-hashing", action="store_true")
     p.add_argument("--seed", action=argparse.BooleanOptionalAction, default=True,
                    help="with --fused, the insert / delete kernels seed the tree calls (batch prologue "
@@ -101,7 +102,7 @@ def dist_init(args):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if ws > 1 or (args.partitioned and args.impl == "ours"):
+    if args.impl == "ours" and (ws > 1 or args.partitioned):   # the reference arm needs no process group
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)

@@ -40,7 +40,10 @@ constexpr int PR_BLOCK = 512;
 #define MEERKAT_PR_MINB 2   // resident blocks per SM k_pagerank is compiled for (A/B)
 #endif
 constexpr int PR_MINB = MEERKAT_PR_MINB;
-constexpr int PR_UNROLL = 2;   // slabs in flight per group (register double-buffered)
+#ifndef MEERKAT_PR_UNROLL
+#define MEERKAT_PR_UNROLL 2
+#endif
+constexpr int PR_UNROLL = MEERKAT_PR_UNROLL;   // slabs in flight per group (register double-buffered)
 using contrib_t = double;   // Contribution[] in fp64 (an fp32 cache was 5.5 % faster and broke the
                             // closed-form pins' tolerance: DESIGN.md §10)
 size_t pagerank_contrib_bytes() { return sizeof(contrib_t); }

@@ -16,9 +16,15 @@ constexpr int TREE_BLOCK = 512;
 constexpr int TREE_MINB = MEERKAT_TREE_MINB;
 constexpr int FILTER_LOG2 = 14;
 constexpr int FILTER_WORDS = 1 << FILTER_LOG2;   // 64 KiB smem Bloom filter per block (decremental scan)
-constexpr int SCAN_UNROLL = 2;        // independent slabs in flight per group in the scan
+#ifndef MEERKAT_SCAN_UNROLL
+#define MEERKAT_SCAN_UNROLL 2
+#endif
+constexpr int SCAN_UNROLL = MEERKAT_SCAN_UNROLL;   // independent slabs in flight per group in the scan
 constexpr unsigned FULL = 0xFFFFFFFFu;
-constexpr uint64_t PROBE_MIN_ITEMS = 65536;
+#ifndef MEERKAT_PROBE_MIN_ITEMS
+#define MEERKAT_PROBE_MIN_ITEMS 65536
+#endif
+constexpr uint64_t PROBE_MIN_ITEMS = MEERKAT_PROBE_MIN_ITEMS;   // frontiers above this read node[x] before the atomicMin
 #ifndef MEERKAT_TAIL_ITEMS
 #define MEERKAT_TAIL_ITEMS 64
 #endif

@@ -1,0 +1,7 @@
+F="--no-compare --no-per-tree --no-cpu-baseline --no-sweep --no-pagerank --no-wcc --no-tc --no-config4 --no-hashing-ab --no-e2e --no-probe"
+for i in 1 2; do
+for v in "" pr0 prn; do
+if [ -z "$v" ]; then SO=""; else SO="MEERKAT_SO_PATH=$PWD/paper_2305_17813_b200/libmeerkat_$v.so"; fi
+env $SO timeout 600 python bench.py $F --json-out gpurun_out/r02_pr.json > /dev/null 2>&1
+python -c "import json;d=json.load(open('gpurun_out/r02_pr.json'));print('$v',round(d['ms_per_step'],4),{k:round(x*1e3,1) for k,x in d['per_call_ms'].items()},d['static_recompute_ms'])"
+done; done
