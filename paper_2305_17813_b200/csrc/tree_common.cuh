@@ -22,7 +22,7 @@ constexpr int FILTER_WORDS = 1 << FILTER_LOG2;   // 64 KiB smem Bloom filter per
 constexpr int SCAN_UNROLL = MEERKAT_SCAN_UNROLL;   // independent slabs in flight per group in the scan
 constexpr unsigned FULL = 0xFFFFFFFFu;
 #ifndef MEERKAT_PROBE_MIN_ITEMS
-#define MEERKAT_PROBE_MIN_ITEMS 65536
+#define MEERKAT_PROBE_MIN_ITEMS 0   // measured: probing on every frontier size is best
 #endif
 constexpr uint64_t PROBE_MIN_ITEMS = MEERKAT_PROBE_MIN_ITEMS;   // frontiers above this read node[x] before the atomicMin
 #ifndef MEERKAT_TAIL_ITEMS
@@ -296,14 +296,17 @@ __device__ __forceinline__ void tree_prologue_inc(const GraphDev& G, const TreeD
       c.batch++;
       ok = u < G.V && v < G.V;   // invalid edges were skipped by the insert too
     }
-    // phase-wise over the trees: node[u] of every tree, then the atomicMins, then stamp + vmeta
-    uint64_t cand[MAX_TREES];
+    // phase-wise over the trees: node[u] and node[v] of every tree (independent loads: node[v] only
+    // filters -- node values only decrease, so a stale read can only cost a spare atomic), then the
+    // atomicMins of the candidates that can still win, then stamp + vmeta
+    uint64_t cand[MAX_TREES], cur_v[MAX_TREES];
     bool live[MAX_TREES];
 #pragma unroll
     for (int k = 0; k < MAX_TREES; k++) {
       const uint32_t wk = T[k].unit ? 1u : w;
       live[k] = k < (int)ntrees && ok && (T[k].unit || (wk != 0 && wk < W_LIMIT));
       cand[k] = live[k] ? ld_cg_u64(T[k].node + u) : UNREACHED;   // node[u], turned into the candidate below
+      cur_v[k] = live[k] ? ld_cg_u64(T[k].node + v) : 0ull;
     }
 #pragma unroll
     for (int k = 0; k < MAX_TREES; k++) {
@@ -311,6 +314,7 @@ __device__ __forceinline__ void tree_prologue_inc(const GraphDev& G, const TreeD
         const uint64_t dist = (cand[k] >> 32) + (T[k].unit ? 1u : w);
         if (dist >= INF_DIST) { c.err |= ERR_OVERFLOW; live[k] = false; }   // C5
         cand[k] = (dist << 32) | u;
+        live[k] = live[k] && cand[k] < cur_v[k];
       } else {
         live[k] = false;
       }

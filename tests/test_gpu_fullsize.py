@@ -125,7 +125,8 @@ def test_config3_bench_sequence_certified(workload):
     W, o0 = workload
     V, src = W.vertex_n, W.source
     bs, bd, bw = W.base
-    g = Graph(V, weighted=True, degree_hints=cuda(np.bincount(bs, minlength=V).astype(np.uint32)), reverse=True,
+    g = Graph(V, weighted=True, load_factor=0.5,   # bench.py's default load factor
+              degree_hints=cuda(np.bincount(bs, minlength=V).astype(np.uint32)), reverse=True,
               in_degree_hints=cuda(np.bincount(bd, minlength=V).astype(np.uint32)))
     g.insert(cuda(bs), cuda(bd), cuda(bw), count=False)
     o = oracle.OracleGraph(V)
