@@ -2,7 +2,7 @@ timeout 900 python -m pytest tests/test_gpu_tree.py tests/test_gpu_contract.py t
 tail -2 gpurun_out/r02_pytest19.log
 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
 F="--no-compare --no-per-tree --no-cpu-baseline --no-sweep --no-pagerank --no-wcc --no-tc --no-config4 --no-hashing-ab --no-e2e --no-probe"
-for i in 1 2 3; do
+for i in 1 2; do
 for v in "" base; do
 if [ -z "$v" ]; then SO=""; else SO="MEERKAT_SO_PATH=$PWD/paper_2305_17813_b200/libmeerkat_$v.so"; fi
 env $SO timeout 600 python bench.py $F --json-out gpurun_out/r02_pp.json > /dev/null 2>&1
