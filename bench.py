@@ -1045,9 +1045,10 @@ def run_ours(args, ws, rank, local):
 
 
 def run_dist(args, ws, rank, local):
-    """Vertex-partitioned path: the SAME config-3 graph split over `ws` GPUs by
-    owner(v) = v mod ws; every rank brings 1/ws of each batch; one all-to-all routes it; tree updates
-    exchange <x, candidate> messages once per round (NCCL all-to-all) -> strong scaling."""
+    """Vertex-partitioned path: the SAME config-3 graph split over `ws` GPUs by the
+    library's placement (owner = mix(v) mod ws); every rank brings 1/ws of each batch and the library
+    routes it (one all-to-all-v); tree updates run as device-driven exchange units over the library's
+    NCCL communicator (a fixed-size all-to-all per unit) -> strong scaling."""
     import torch
     from paper_2305_17813_b200.dist import DistGraph
 
@@ -1060,8 +1061,11 @@ def run_dist(args, ws, rank, local):
     sl = lambda a: np.ascontiguousarray(a[rank::ws])
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.uint32).view(np.int32)).to(dev)
     bs, bd, bw = W.base
+    reverse = args.frontier == "reverse"
     g = DistGraph(V, hashing=not args.no_hashing, load_factor=args.lf,
-                  degree_hints=np.bincount(bs, minlength=V).astype(np.uint32), device=dev)
+                  degree_hints=np.bincount(bs, minlength=V).astype(np.uint32),
+                  in_degree_hints=np.bincount(bd, minlength=V).astype(np.uint32) if reverse else None,
+                  reverse=reverse, device=dev, stream=stream)
     barrier(ws)
     t0 = time.time()
     n_base = g.insert(T(sl(bs)), T(sl(bd)), T(sl(bw)))
@@ -1080,7 +1084,8 @@ def run_dist(args, ws, rank, local):
     per_call = {n: [] for n in names}
     total_ms = 0.0
     dec_bytes = []
-    l0 = g.g.stats()["kernel_launches"]
+    exchanges = []
+    l0 = g.stats()["kernel_launches"]
     for k in range(K):
         flush.zero_()
         torch.cuda.synchronize()
@@ -1094,7 +1099,8 @@ def run_dist(args, ws, rank, local):
             per_call[n].append(allreduce_max(evs[j].elapsed_time(evs[j + 1]), ws))
         # algorithmic bytes of the decremental call on this rank (both trees), read outside the interval
         dec_bytes.append(sp.stats()["alg_bytes"] + bf.stats()["alg_bytes"])
-    launches = g.g.stats()["kernel_launches"] - l0
+        exchanges.append(sp.stats()["exchanges"])
+    launches = g.stats()["kernel_launches"] - l0
     clk = clocks.stop()
     mean = {n: float(np.mean(v)) for n, v in per_call.items()}
     edges = 2 * args.batch * K
@@ -1106,7 +1112,7 @@ def run_dist(args, ws, rank, local):
     peak = peaks.get("hbm_gbs") or 6650.0
     tot_bytes = allreduce_sum(float(np.mean(dec_bytes)), ws)   # all ranks' bytes of one call
     ach = tot_bytes / (mean["trees_dec"] * 1e-3) / 1e9
-    roofline = {"bound": "hbm", "kernel": "fused decremental update, all phases (partitioned; host-driven rounds)",
+    roofline = {"bound": "hbm", "kernel": "fused decremental update, all exchange units (partitioned)",
                 "achieved": ach, "peak": peak * ws, "unit": "GB/s", "frac": ach / (peak * ws),
                 "traffic": None, "alg_bytes_per_launch": tot_bytes,
                 "peak_source": ("measured (MEASURED_PEAKS.json hbm_gbs) x " if peaks.get("hbm_gbs") else
@@ -1150,14 +1156,19 @@ def run_dist(args, ws, rank, local):
         "config": {"workload": f"rmat-s{args.scale}-ef{args.ef} dynamic SSSP+BFS, {args.batch}-edge insert+delete "
                                f"batches (BASELINE config 3)", "vertices": V, "edges": int(n_base),
                    "batch": args.batch, "source": W.source, "hashing": not args.no_hashing,
-                   "load_factor": args.lf, "decremental_frontier": "scan (per partition)",
-                   "parallelism": f"vertex-partitioned over {ws} GPUs (owner = v mod {ws}), NCCL all-to-all per round",
+                   "load_factor": args.lf,
+                   "decremental_frontier": "in-edge mirror, pull requests to owner(u)" if reverse else
+                   "scan (per partition, invalid sets exchanged)",
+                   "parallelism": f"vertex-partitioned over {ws} GPUs (owner = mix(v) mod {ws}), library NCCL "
+                                  f"communicator, one fixed-size all-to-all per exchange unit",
                    "l2": "flushed before every timed step; store > L2"},
         "update_edges_per_s": 2 * args.batch / ((mean["insert"] + mean["delete"]) / 1e3),
         "sssp_bfs_fused_ms_per_batch": {"incremental": mean["trees_inc"], "decremental": mean["trees_dec"]},
         "per_call_ms": mean, "build_s": build_s, "roofline": roofline, "cpu_baseline": None,
         "e2e": e2e, "gpu_launches": allreduce_sum(float(launches), ws), "clocks": clk, "generate_s": gen_s,
-        "note": "host-driven rounds (one NCCL all-to-all + all-reduce per frontier round); timings are max over ranks",
+        "exchanges_per_decremental_call": float(np.mean(exchanges)) if exchanges else None,
+        "note": "device-driven exchange units (the host reads a mode word PIPE units behind); timings are max "
+                "over ranks",
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

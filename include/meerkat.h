@@ -76,9 +76,18 @@ typedef enum {
   MEERKAT_E_OVERFLOW = 5,     /* a distance would reach 2^32-1; that relaxation is not applied (C5) */
   MEERKAT_E_STATE = 6,        /* tree/graph version mismatch; SSSP on an unweighted graph */
   MEERKAT_E_CUDA = 7,         /* CUDA runtime error (out of memory, launch failure, no device) */
-  MEERKAT_E_NCCL = 8,         /* reserved */
+  MEERKAT_E_NCCL = 8,         /* NCCL error (init, or an asynchronous communicator error: the communicator
+                                 is aborted) or a failed exchange callback; partitioned graphs only */
   MEERKAT_E_PARTITION = 9     /* an edge's source (or a message's target) is not held by this rank (skipped) */
 } meerkat_status;
+
+/* Host transport of a partitioned graph: an all-to-all-v over world_size ranks, called collectively
+ * (every rank, same sequence).  `send` holds world_size consecutive segments, segment p (send_bytes[p]
+ * bytes) for rank p; on return `recv` holds world_size consecutive segments, segment q (recv_bytes[q]
+ * bytes, known to the caller) from rank q.  Both are host memory owned by the library.  Return 0 on
+ * success; anything else makes the library call fail with MEERKAT_E_NCCL. */
+typedef int (*meerkat_exchange_fn)(void* ctx, const void* send, const uint64_t* send_bytes, void* recv,
+                                   const uint64_t* recv_bytes);
 
 typedef struct {
   uint32_t vertex_n;            /* |V|, fixed for the graph's lifetime; ids are 0..vertex_n-1 */
@@ -94,11 +103,20 @@ typedef struct {
                                    valid->invalid frontier reads only the in-edges of V_invalid
                                    instead of scanning every slab (same result) */
   const uint32_t* in_degree_hints; /* host or device [vertex_n] (in-degrees), or NULL; reverse only */
-  uint32_t world_size;          /* vertex partition (multi-GPU): 0 or 1 = whole graph here;   */
-  uint32_t rank;                /* otherwise this graph holds the out-edges of every u with u % world_size  */
-                                /* == rank; degree hints are then indexed by u / world_size                */
+  uint32_t world_size;          /* vertex partition (multi-GPU), see "Partitioned graphs" below */
+  uint32_t rank;
   uint32_t update_tracking;     /* 1: keep per-slab-list update tracking (is_updated / first updated slab
                                    and lane) for meerkat_wcc_incremental_tracked */
+  /* Partitioned graphs: a graph is PARTITIONED when it is given a transport -- nccl_id or exchange --
+   * (any world_size >= 1; without one, world_size must be 0 or 1 and the graph is the single-GPU one). */
+  const void* nccl_id;          /* 128-B ncclUniqueId from meerkat_nccl_unique_id() on rank 0, broadcast by the
+                                   caller: the library creates and owns an NCCL communicator over world_size
+                                   ranks (collective call) and exchanges with grouped ncclSend/ncclRecv on
+                                   the graph's stream (NVLink / NVSwitch) */
+  meerkat_exchange_fn exchange; /* or a host all-to-all-v (CPU transports and tests; see below) */
+  void* exchange_ctx;
+  uint32_t exchange_pairs;      /* messages per peer per exchange of a dynamic tree call (0 = 16384; static
+                                   recomputes use 16 x this); more are carried over to the next exchange */
 } meerkat_config;
 
 typedef struct {
@@ -130,6 +148,7 @@ typedef struct {
   uint64_t version;          /* graph version this tree reflects */
   uint32_t source;
   uint32_t unit_weights;     /* 1 for BFS trees */
+  uint64_t exchanges;        /* partitioned trees: exchange units of the last call (0 on one GPU) */
 } meerkat_tree_stats;
 
 const char* meerkat_status_string(meerkat_status s);
@@ -257,75 +276,40 @@ meerkat_status meerkat_tree_timeline(meerkat_tree* t, uint64_t* out, uint64_t* i
 meerkat_status meerkat_tree_destroy(meerkat_tree* t);
 
 /* ---------------------------------------------------------------------------------------------
- * Vertex-partitioned trees (world_size > 1).  Each rank holds node[] of its own
- * vertices; a tree update is a sequence of PHASES run by every rank in lock step, with the
- * caller moving messages between ranks in between (one all-to-all per round, e.g. NCCL through
- * torch.distributed) and summing local frontier sizes for termination.  The method and the
- * result are the single-GPU ones: relaxations of a vertex owned elsewhere
- * become messages <x, packed candidate> to owner(x); invalidations of a child owned elsewhere
- * become messages <x, expected parent>.  Results are bit-identical to world_size 1.
- *
- * Messages are (x, payload) pairs of uint64 grouped by destination rank; `msg_counts[r]` is the
- * number of pairs for rank r.  The device buffer in meerkat_dresult stays valid until the next
- * phase call on the tree.  Every phase synchronises the graph's stream once, except the APPLY
- * phases, which are stream-ordered (their frontier is reported by the next phase).
+ * Partitioned graphs (multi-GPU).  One process per GPU; rank r of world_size holds
+ * the out-edges (and, with `reverse`, the in-edges), the tree nodes and the degree-hint row of every
+ * vertex v with owner(v) == r, where owner(v) = m mod world_size, row(v) = m div world_size and
+ * m = a fixed bijective mix of v on [0, vertex_n) (so unscrambled R-MAT ids are balanced; results do
+ * not depend on it).  degree_hints / in_degree_hints are GLOBAL [vertex_n] arrays on every rank.
+ * Every call on a partitioned graph or its trees is COLLECTIVE: all ranks make the same sequence of
+ * calls, each with its own (possibly empty) batch:
+ *   - insert / delete / query: any rank may pass any edges; the library routes each edge to
+ *     owner(src) (and, for the mirror and for the decremental parent test, to owner(dst)) with one
+ *     all-to-all-v.  n_inserted / n_deleted are GLOBAL counts; query
+ *     answers return to the asking rank in its input order; errors are those of this rank's edges;
+ *   - meerkat_sssp_create / meerkat_bfs_create / meerkat_tree_recompute: collective static trees;
+ *   - the incremental / decremental calls (per tree or fused trees_*) must pass, on every rank, the
+ *     batch that rank passed to the last mutation (ordering contract, checked by fingerprint); the
+ *     library uses the rows it routed then.  The update runs as device-driven exchange units (a
+ *     cooperative kernel -- apply the messages received, local frontier rounds to a fixpoint,
+ *     pack up to exchange_pairs messages per peer -- then one all-to-all of fixed-size blocks);
+ *     phase changes (propagation -> valid->invalid frontier -> relaxation -> done) are decided on
+ *     the device from the exchanged headers, identically on every rank; the host never waits for a
+ *     round.  The valid->invalid frontier walks the in-edge mirror (pull requests to owner(u)) when
+ *     `reverse`, else every rank streams its own slabs against the exchanged invalid sets;
+ *   - meerkat_tree_nodes: all vertex_n nodes in global id order on every rank (an all-gather);
+ *   - meerkat_export_edges / meerkat_stats_get / meerkat_tree_stats_get: this rank's part (local).
+ * PageRank, WCC, triangle counting, vanilla trees, seeded calls and distances are single-GPU only
+ * (MEERKAT_E_STATE / MEERKAT_E_INVALID_ARG).  Results are bit-identical to world_size 1.
  * ------------------------------------------------------------------------------------------- */
-typedef enum {
-  MEERKAT_D_STATIC_INIT = 0,      /* node <- UNREACHED, SRC <- <0,SRC> on its owner; frontier = {SRC} */
-  MEERKAT_D_INC_SEED = 1,         /* a,b,c,n = inserted batch edges with u owned here        */
-  MEERKAT_D_DEC_INVALIDATE = 2,   /* a,b,n = deleted batch edges with v owned here          */
-  MEERKAT_D_PROPAGATE = 3,        /* expand the frontier of invalid vertices               */
-  MEERKAT_D_APPLY_PROPAGATE = 4,  /* a = received <x, expected parent> pairs, n pairs                   */
-  MEERKAT_D_DEC_SCAN = 5,         /* a = ALL ranks' invalid vertices (u32, global ids), n    */
-  MEERKAT_D_RELAX = 6,            /* expand the frontier of improved vertices              */
-  MEERKAT_D_APPLY_RELAX = 7,      /* a = received <x, candidate> pairs, n pairs                         */
-  MEERKAT_D_FINISH = 8            /* a = ALL ranks' invalid vertices, n: clear marks; tree reflects the graph */
-} meerkat_dphase;
-
 #define MEERKAT_MAX_RANKS 64
 
-typedef struct {
-  const uint64_t* msgs;                   /* device: outgoing pairs grouped by destination rank */
-  uint64_t msg_counts[MEERKAT_MAX_RANKS]; /* pairs per destination rank */
-  uint64_t frontier;                      /* local frontier size for the next expansion */
-  const uint32_t* invalid;                /* device: vertices this rank invalidated so far (global ids) */
-  uint64_t invalid_n;
-} meerkat_dresult;
-
-meerkat_status meerkat_dtree_create(meerkat_graph* g, uint32_t source, uint32_t unit_weights, meerkat_tree** out);
-meerkat_status meerkat_dtree_phase(meerkat_graph* g, meerkat_tree* t, meerkat_dphase phase, const void* a,
-                                   const void* b, const void* c, uint64_t n, meerkat_dresult* out);
-/* Stable partition of a batch by owner(key[i]) = key[i] % world_size (key = src for insert/delete/
- * query and incremental seeds, dst for decremental invalidation): writes the permuted a,b,c
- * (c may be NULL) to the device outputs and per-rank counts to counts[world_size] (host). */
-/* Copy `bytes` between host/device buffers on the graph's stream (lets a caller move phase messages
- * into its own communication buffers); synchronises only when either side is host memory. */
-meerkat_status meerkat_memcpy(meerkat_graph* g, void* dst, const void* src, uint64_t bytes);
-/* Fused exchange of k (<= 8) trees updated in lock step (one all-to-all per round for all of them).
- * pack: from each tree's last emitting phase, writes meta (device int64 [world_size * k * 3]: per
- * destination rank p, per tree i: pairs for p, the tree's local frontier, pairs it sent) and send
- * (device, <x, payload> pairs as 2 x uint64: per p, tree 0's pairs for p, then tree 1's, ...), and
- * send_counts[p] (host, pairs per destination); MEERKAT_E_CAPACITY if the pairs exceed
- * capacity_pairs.  apply: recv holds, per source rank p, tree 0's recv_counts[p * k] pairs, then tree
- * 1's recv_counts[p * k + 1], ...; runs each tree's apply phase (APPLY_RELAX / APPLY_PROPAGATE).
- * Both are stream-ordered. */
-meerkat_status meerkat_dtrees_pack(meerkat_graph* g, meerkat_tree* const* trees, uint32_t k, int64_t* meta,
-                                   uint64_t* send, uint64_t capacity_pairs, uint64_t* send_counts);
-meerkat_status meerkat_dtrees_apply(meerkat_graph* g, meerkat_tree* const* trees, uint32_t k, meerkat_dphase phase,
-                                    const uint64_t* recv, const uint64_t* recv_counts);
-/* The DEC_SCAN phase of up to 2 trees in lock step: ONE stream of this rank's slab array serves both
- * (invalid_lists[i]: ALL ranks' invalid vertices of tree i, device u32, invalid_counts[i] of them);
- * outs[i] as the per-tree phase would report.  Synchronises once. */
-meerkat_status meerkat_dtrees_scan(meerkat_graph* g, meerkat_tree* const* trees, uint32_t k,
-                                   const uint32_t* const* invalid_lists, const uint64_t* invalid_counts,
-                                   meerkat_dresult* outs);
-/* An expansion phase (RELAX / PROPAGATE) of k (<= 8) trees in lock step, ONE synchronisation;
- * outs[i] as the per-tree phase would report. */
-meerkat_status meerkat_dtrees_expand(meerkat_graph* g, meerkat_tree* const* trees, uint32_t k, meerkat_dphase phase,
-                                     meerkat_dresult* outs);
-meerkat_status meerkat_route(meerkat_graph* g, int key_is_b, const uint32_t* a, const uint32_t* b,
-                             const uint32_t* c, uint64_t n, uint32_t* out_a, uint32_t* out_b, uint32_t* out_c,
-                             uint64_t* counts);
+/* Writes a fresh ncclUniqueId (128 bytes) to out; MEERKAT_E_NCCL if NCCL cannot be loaded. */
+meerkat_status meerkat_nccl_unique_id(void* out, uint64_t bytes);
+/* Host-only: owner rank and row of n global ids on a partitioned graph of vertex_n vertices over
+ * world_size ranks (the library's placement); either output may be NULL. */
+meerkat_status meerkat_owner_map(uint32_t vertex_n, uint32_t world_size, const uint32_t* ids, uint64_t n,
+                                 uint32_t* owner, uint32_t* row);
 
 /* ---------------------------------------------------------------------------------------------
  * PageRank.  Eq. (1):

@@ -21,8 +21,6 @@ STATUS = {
 }
 OK, E_INVALID_ARG, E_VERTEX_RANGE, E_WEIGHT, E_CAPACITY, E_OVERFLOW, E_STATE, E_CUDA, E_NCCL, E_PARTITION = range(10)
 MAX_RANKS = 64
-(D_STATIC_INIT, D_INC_SEED, D_DEC_INVALIDATE, D_PROPAGATE, D_APPLY_PROPAGATE, D_DEC_SCAN, D_RELAX, D_APPLY_RELAX,
- D_FINISH) = range(9)
 
 # Every function include/meerkat.h declares (checked by tests/test_abi.py).
 EXPORTS = [
@@ -31,7 +29,7 @@ EXPORTS = [
     "meerkat_stats_get", "meerkat_sssp_create", "meerkat_bfs_create", "meerkat_sssp_incremental",
     "meerkat_bfs_incremental", "meerkat_sssp_decremental", "meerkat_bfs_decremental", "meerkat_tree_recompute",
     "meerkat_tree_nodes", "meerkat_tree_invalidated", "meerkat_tree_stats_get", "meerkat_tree_destroy",
-    "meerkat_dtree_create", "meerkat_dtree_phase", "meerkat_memcpy", "meerkat_route", "meerkat_tree_timeline",
+    "meerkat_nccl_unique_id", "meerkat_owner_map", "meerkat_tree_timeline",
     "meerkat_check", "meerkat_trees_incremental", "meerkat_trees_decremental",
     "meerkat_insert_batch_trees", "meerkat_delete_batch_trees",
     "meerkat_pagerank_create", "meerkat_pagerank_update", "meerkat_pagerank_recompute", "meerkat_pagerank_values",
@@ -40,8 +38,7 @@ EXPORTS = [
     "meerkat_tc_count", "meerkat_tc_static", "meerkat_tc_incremental", "meerkat_tc_decremental",
     "meerkat_wcc_create", "meerkat_wcc_recompute", "meerkat_wcc_incremental", "meerkat_wcc_labels",
     "meerkat_wcc_components", "meerkat_wcc_destroy", "meerkat_tree_recompute_scheme",
-    "meerkat_wcc_incremental_tracked", "meerkat_dtrees_pack", "meerkat_dtrees_apply", "meerkat_dtrees_scan",
-    "meerkat_dtrees_expand", "meerkat_probe_latency", "meerkat_counters_async",
+    "meerkat_wcc_incremental_tracked", "meerkat_probe_latency", "meerkat_counters_async",
 ]
 
 
@@ -58,7 +55,14 @@ class Config(ctypes.Structure):
         ("hash_seed", ctypes.c_uint64), ("device", ctypes.c_int), ("stream", ctypes.c_void_p),
         ("reverse", ctypes.c_uint32), ("in_degree_hints", ctypes.c_void_p),
         ("world_size", ctypes.c_uint32), ("rank", ctypes.c_uint32), ("update_tracking", ctypes.c_uint32),
+        ("nccl_id", ctypes.c_void_p), ("exchange", ctypes.c_void_p), ("exchange_ctx", ctypes.c_void_p),
+        ("exchange_pairs", ctypes.c_uint32),
     ]
+
+
+# meerkat_exchange_fn: host all-to-all-v of a partitioned graph's transport
+EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint64),
+                               ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint64))
 
 
 class Stats(ctypes.Structure):
@@ -74,7 +78,8 @@ class TreeStats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint64) for n in (
         "rounds", "propagate_rounds", "direct_invalid", "invalidated", "frontier_edges", "items", "slabs_read",
         "scan_slabs", "improved", "alg_bytes", "version")] + [("source", ctypes.c_uint32),
-                                                             ("unit_weights", ctypes.c_uint32)]
+                                                             ("unit_weights", ctypes.c_uint32),
+                                                             ("exchanges", ctypes.c_uint64)]
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}
@@ -88,11 +93,6 @@ class PageRankStats(ctypes.Structure):
     def as_dict(self):
         return {n: (float(getattr(self, n)) if n == "delta" else int(getattr(self, n)))
                 for n, _ in self._fields_ if n != "pad"}
-
-
-class DResult(ctypes.Structure):
-    _fields_ = [("msgs", ctypes.c_void_p), ("msg_counts", ctypes.c_uint64 * MAX_RANKS), ("frontier", ctypes.c_uint64),
-                ("invalid", ctypes.c_void_p), ("invalid_n", ctypes.c_uint64)]
 
 
 class Latency(ctypes.Structure):
@@ -143,10 +143,8 @@ def lib():
         "meerkat_trees_decremental": (ctypes.c_int, [vp, pvp, u32, vp, vp, u64]),
         "meerkat_insert_batch_trees": (ctypes.c_int, [vp, vp, vp, vp, u64, pvp, u32, pu64]),
         "meerkat_delete_batch_trees": (ctypes.c_int, [vp, vp, vp, u64, pvp, u32, pu64]),
-        "meerkat_dtree_create": (ctypes.c_int, [vp, u32, u32, pvp]),
-        "meerkat_dtree_phase": (ctypes.c_int, [vp, vp, ctypes.c_int, vp, vp, vp, u64, ctypes.POINTER(DResult)]),
-        "meerkat_memcpy": (ctypes.c_int, [vp, vp, vp, u64]),
-        "meerkat_route": (ctypes.c_int, [vp, ctypes.c_int, vp, vp, vp, u64, vp, vp, vp, pu64]),
+        "meerkat_nccl_unique_id": (ctypes.c_int, [vp, u64]),
+        "meerkat_owner_map": (ctypes.c_int, [u32, u32, vp, u64, vp, vp]),
         "meerkat_pagerank_create": (ctypes.c_int, [vp, ctypes.c_double, ctypes.c_double, u32, pvp]),
         "meerkat_pagerank_update": (ctypes.c_int, [vp, vp]),
         "meerkat_pagerank_recompute": (ctypes.c_int, [vp, vp]),
@@ -168,10 +166,6 @@ def lib():
         "meerkat_wcc_destroy": (ctypes.c_int, [vp]),
         "meerkat_tree_recompute_scheme": (ctypes.c_int, [vp, vp, u32]),
         "meerkat_wcc_incremental_tracked": (ctypes.c_int, [vp, vp]),
-        "meerkat_dtrees_pack": (ctypes.c_int, [vp, pvp, u32, vp, vp, u64, pu64]),
-        "meerkat_dtrees_apply": (ctypes.c_int, [vp, pvp, u32, ctypes.c_int, vp, pu64]),
-        "meerkat_dtrees_scan": (ctypes.c_int, [vp, pvp, u32, pvp, pu64, ctypes.POINTER(DResult)]),
-        "meerkat_dtrees_expand": (ctypes.c_int, [vp, pvp, u32, ctypes.c_int, ctypes.POINTER(DResult)]),
         "meerkat_probe_latency": (ctypes.c_int, [vp, ctypes.POINTER(Latency)]),
         "meerkat_counters_async": (ctypes.c_int, [vp, vp]),
     }

@@ -14,9 +14,22 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libmeerkat.so")
 ROOT = os.path.dirname(HERE)
 
+def _nccl_include() -> str:
+    """nccl.h for the types and prototypes of part.cu (libnccl.so.2 itself is opened at run time):
+    the one next to torch's NCCL when present, else the system's."""
+    try:
+        import nvidia.nccl as m   # noqa: PLC0415
+        for p in m.__path__:
+            if os.path.exists(os.path.join(p, "include", "nccl.h")):
+                return os.path.join(p, "include")
+    except Exception:
+        pass
+    return "/usr/include"
+
+
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-    "-Xcompiler", "-fPIC", "-shared", "-cudart", "static", "-Xptxas", "-v",
+    "-Xcompiler", "-fPIC", "-shared", "-cudart", "static", "-Xptxas", "-v", "-I" + _nccl_include(), "-ldl",
 ]
 
 

@@ -36,6 +36,10 @@ struct DeviceGuard {
   }
 };
 
+}  // namespace
+
+namespace mk {
+
 bool is_device_ptr(const void* p) {
   if (!p) return false;
   cudaPointerAttributes a;
@@ -81,6 +85,10 @@ void remember_stage(meerkat_graph* g, int slot, const void* p, size_t bytes) {
   g->staged_version[slot] = g->version;
 }
 
+}  // namespace mk
+
+namespace {
+
 cudaError_t stage_in_reuse(meerkat_graph* g, int slot, const void* p, size_t bytes, const void** out) {
   if (p && bytes && p == g->staged_host[slot] && bytes == g->staged_len[slot] && g->staged_version[slot] == g->version) {
     *out = g->stage[slot];
@@ -88,6 +96,10 @@ cudaError_t stage_in_reuse(meerkat_graph* g, int slot, const void* p, size_t byt
   }
   return stage_in(g, slot, p, bytes, out);
 }
+
+}  // namespace
+
+namespace mk {
 
 // Read the control block back (synchronises); returns and clears the sticky error.
 meerkat_status collect(meerkat_graph* g) {
@@ -116,6 +128,10 @@ cudaError_t mutated(meerkat_graph* g, int kind, uint64_t n) {
   if (kind == 2) g->last_delete_version = g->version;
   return e;
 }
+
+}  // namespace mk
+
+namespace {
 
 meerkat_status check_batch(meerkat_graph* g, const uint32_t* s, const uint32_t* d, uint64_t n) {
   if (!g) return MEERKAT_E_INVALID_ARG;
@@ -160,13 +176,14 @@ meerkat_status meerkat_create(const meerkat_config* cfg, meerkat_graph** out) {
   g->device = cfg->device;
   g->stream = static_cast<cudaStream_t>(cfg->stream);
   g->V = cfg->vertex_n;
+  const bool partitioned = cfg->nccl_id != nullptr || cfg->exchange != nullptr;
   g->ws = cfg->world_size > 1 ? cfg->world_size : 1;
   g->rank = g->ws > 1 ? cfg->rank : 0;
-  if (g->ws > MEERKAT_MAX_RANKS || g->rank >= g->ws || g->V <= g->rank) {
+  if (g->ws > MEERKAT_MAX_RANKS || g->rank >= g->ws || g->V <= g->rank || (g->ws > 1 && !partitioned)) {
     delete g;
     return MEERKAT_E_INVALID_ARG;
   }
-  g->Vl = (g->V - g->rank + g->ws - 1) / g->ws;   // vertices v < V with v % ws == rank
+  g->Vl = (g->V - g->rank + g->ws - 1) / g->ws;   // rows m < V with m % ws == rank (pm_place)
   g->weighted = cfg->weighted != 0;
   g->hashing = cfg->hashing != 0;
   g->lf = lf;
@@ -175,10 +192,15 @@ meerkat_status meerkat_create(const meerkat_config* cfg, meerkat_graph** out) {
   g->in.dev.seed = g->out.dev.seed ^ 0x27d4eb2fu;
   cudaError_t e = cudaDeviceGetAttribute(&g->sm_count, cudaDevAttrMultiProcessorCount, g->device);
   const void* hints = nullptr;
-  if (e == cudaSuccess) e = stage_in(g, 0, cfg->degree_hints, (size_t)g->Vl * 4, &hints);
+  // partitioned: the global hint arrays are gathered into this rank's rows
+  auto hints_of = [&](const uint32_t* h, int slot) -> cudaError_t {
+    if (!partitioned) return stage_in(g, slot, h, (size_t)g->Vl * 4, &hints);
+    return part_hints(g, h, &hints, slot) == MEERKAT_OK ? cudaSuccess : cudaErrorUnknown;
+  };
+  if (e == cudaSuccess) e = hints_of(cfg->degree_hints, 0);
   if (e == cudaSuccess) e = launch_build(g, g->out, static_cast<const uint32_t*>(hints), cfg->pool_slabs);
   if (e == cudaSuccess && g->reverse) {
-    e = stage_in(g, 1, cfg->in_degree_hints, (size_t)g->Vl * 4, &hints);
+    e = hints_of(cfg->in_degree_hints, 1);
     if (e == cudaSuccess) e = launch_build(g, g->in, static_cast<const uint32_t*>(hints), cfg->pool_slabs);
   }
   if (e == cudaSuccess && cfg->update_tracking) {   // UpdateIterator metadata
@@ -196,6 +218,14 @@ meerkat_status meerkat_create(const meerkat_config* cfg, meerkat_graph** out) {
     meerkat_destroy(g);
     return MEERKAT_E_CUDA;
   }
+  if (partitioned) {   // transport (NCCL communicator: collective), rings, exchange blocks
+    const meerkat_status st = part_init(g, cfg);
+    if (st != MEERKAT_OK) {
+      cudaGetLastError();
+      meerkat_destroy(g);
+      return st;
+    }
+  }
   *out = g;
   return MEERKAT_OK;
 }
@@ -204,11 +234,9 @@ meerkat_status meerkat_destroy(meerkat_graph* g) {
   if (!g) return MEERKAT_E_INVALID_ARG;
   DeviceGuard dg(g->device);
   cudaStreamSynchronize(g->stream);
+  part_free(g);
   free_store(g->out);
   free_store(g->in);
-  cudaFree(g->rscratch);
-  if (g->hmeta) cudaFreeHost(g->hmeta);
-  if (g->hrscratch) cudaFreeHost(g->hrscratch);
   for (int i = 0; i < 4; i++) cudaFree(g->stage[i]);
   delete g;
   return MEERKAT_OK;
@@ -238,6 +266,8 @@ meerkat_status meerkat_insert_batch(meerkat_graph* g, const uint32_t* src, const
   cudaError_t e = stage_in(g, 0, src, n * 4, &s);
   if (e == cudaSuccess) e = stage_in(g, 1, dst, n * 4, &d);
   if (e == cudaSuccess && w) e = stage_in(g, 2, w, n * 4, &ww);
+  if (e == cudaSuccess && g->part)   // collective: routed by owner (part.cu)
+    return part_mutate(g, 1, (const uint32_t*)s, (const uint32_t*)d, (const uint32_t*)ww, n, n_inserted);
   if (e == cudaSuccess && n_inserted) e = cudaMemsetAsync(&g->out.dev.ctrl->n_inserted, 0, 8, g->stream);
   if (e == cudaSuccess)
     e = launch_insert(g, &g->out, g->reverse ? &g->in : nullptr,   // in-edge mirror: (dst, src, w)
@@ -261,6 +291,8 @@ meerkat_status meerkat_delete_batch(meerkat_graph* g, const uint32_t* src, const
   const void *s, *d;
   cudaError_t e = stage_in(g, 0, src, n * 4, &s);
   if (e == cudaSuccess) e = stage_in(g, 1, dst, n * 4, &d);
+  if (e == cudaSuccess && g->part)   // collective: routed by owner (part.cu)
+    return part_mutate(g, 2, (const uint32_t*)s, (const uint32_t*)d, nullptr, n, n_deleted);
   if (e == cudaSuccess && n_deleted) e = cudaMemsetAsync(&g->out.dev.ctrl->n_deleted, 0, 8, g->stream);
   if (e == cudaSuccess)
     e = launch_delete(g, &g->out, g->reverse ? &g->in : nullptr, (const uint32_t*)s, (const uint32_t*)d, n);
@@ -284,6 +316,7 @@ meerkat_status meerkat_query_batch(meerkat_graph* g, const uint32_t* src, const 
   cudaError_t e = stage_in(g, 0, src, n * 4, &s);
   if (e == cudaSuccess) e = stage_in(g, 1, dst, n * 4, &d);
   if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  if (g->part) return part_query(g, (const uint32_t*)s, (const uint32_t*)d, n, found, w_out);
   const bool host_f = n && !is_device_ptr(found);
   const bool host_w = n && w_out && !is_device_ptr(w_out);
   uint8_t* df = found;
@@ -384,13 +417,13 @@ meerkat_status meerkat_stats_get(meerkat_graph* g, meerkat_stats* out) {
 
 // ------------------------------------------------------------------ trees
 
-static meerkat_status tree_create(meerkat_graph* g, uint32_t source, bool unit, bool dist, meerkat_tree** out,
+static meerkat_status tree_create(meerkat_graph* g, uint32_t source, bool unit, meerkat_tree** out,
                                   bool vanilla = false) {
   if (!g || !out) return MEERKAT_E_INVALID_ARG;
   *out = nullptr;
   if (source >= g->V) return MEERKAT_E_VERTEX_RANGE;
   if (!unit && !g->weighted) return MEERKAT_E_STATE;   // SSSP needs weights
-  if (!dist && g->ws > 1) return MEERKAT_E_INVALID_ARG;  // partitioned graphs use the meerkat_dtree_* calls
+  if (g->part && vanilla) return MEERKAT_E_INVALID_ARG;   // single-GPU variant only
   DeviceGuard dg(g->device);
   meerkat_tree* t = new (std::nothrow) meerkat_tree();
   if (!t) return MEERKAT_E_CUDA;
@@ -399,6 +432,7 @@ static meerkat_status tree_create(meerkat_graph* g, uint32_t source, bool unit, 
   t->vanilla = vanilla;
   TreeDev& T = t->dev;
   T.source = source;
+  T.unit = unit ? 1u : 0u;
   T.fr_cap = std::max<uint64_t>(std::max(g->out.buckets, g->in.buckets), 1);
   // node / stamp / invalid list: the vertices held here; invalid bit set: all vertices (global ids)
   const size_t V = g->Vl, words = ((size_t)g->V + 31) / 32;
@@ -427,8 +461,8 @@ static meerkat_status tree_create(meerkat_graph* g, uint32_t source, bool unit, 
     meerkat_tree_destroy(t);
     return MEERKAT_E_CUDA;
   }
-  if (dist) {
-    const meerkat_status st = dtree_init(g, t);
+  if (g->part) {   // collective static tree (part.cu)
+    const meerkat_status st = part_tree_init(g, t);
     if (st != MEERKAT_OK) { meerkat_tree_destroy(t); return st; }
   } else {
     e = launch_tree(g, &t, 1, MODE_STATIC, nullptr, nullptr, nullptr, 0);
@@ -445,23 +479,23 @@ static meerkat_status tree_create(meerkat_graph* g, uint32_t source, bool unit, 
 }
 
 meerkat_status meerkat_sssp_create(meerkat_graph* g, uint32_t source, meerkat_tree** out) {
-  return tree_create(g, source, false, false, out);
+  return tree_create(g, source, false, out);
 }
 
 meerkat_status meerkat_bfs_create(meerkat_graph* g, uint32_t source, meerkat_tree** out) {
-  return tree_create(g, source, true, false, out);
+  return tree_create(g, source, true, out);
 }
 
 meerkat_status meerkat_sssp_vanilla_create(meerkat_graph* g, uint32_t source, meerkat_tree** out) {
-  return tree_create(g, source, false, false, out, true);
+  return tree_create(g, source, false, out, true);
 }
 
 meerkat_status meerkat_bfs_vanilla_create(meerkat_graph* g, uint32_t source, meerkat_tree** out) {
-  return tree_create(g, source, true, false, out, true);
+  return tree_create(g, source, true, out, true);
 }
 
 meerkat_status meerkat_tree_distances(meerkat_tree* t, uint32_t* out) {
-  if (!t || !out || t->dist) return MEERKAT_E_INVALID_ARG;
+  if (!t || !out || t->part) return MEERKAT_E_INVALID_ARG;
   meerkat_graph* g = t->g;
   DeviceGuard dg(g->device);
   const bool host = !is_device_ptr(out);
@@ -484,10 +518,14 @@ static meerkat_status trees_update(meerkat_graph* g, meerkat_tree* const* ts, ui
   meerkat_status st = check_batch(g, src, dst, n);
   if (st != MEERKAT_OK) return st;
   if (!ts || k == 0 || k > (uint32_t)MAX_TREES) return MEERKAT_E_INVALID_ARG;
+  if (g->part) {   // collective, device-driven exchange units (part.cu)
+    DeviceGuard dg(g->device);
+    return part_trees(g, ts, k, kind, src, dst, w, n);
+  }
   bool need_w = false;
   for (uint32_t i = 0; i < k; i++) {
     meerkat_tree* t = ts[i];
-    if (!t || t->g != g || t->dist) return MEERKAT_E_INVALID_ARG;
+    if (!t || t->g != g) return MEERKAT_E_INVALID_ARG;
     if (t->vanilla) return MEERKAT_E_STATE;   // no dependence tree: static only
     for (uint32_t j = 0; j < i; j++)
       if (ts[j] == t) return MEERKAT_E_INVALID_ARG;
@@ -531,10 +569,10 @@ static meerkat_status batch_seed(meerkat_graph* g, int kind, const uint32_t* src
   meerkat_status st = check_batch(g, src, dst, n);
   if (st != MEERKAT_OK) return st;
   if (kind == 1 && n && (g->weighted != (w != nullptr))) return MEERKAT_E_INVALID_ARG;
-  if (!ts || k == 0 || k > (uint32_t)MAX_TREES) return MEERKAT_E_INVALID_ARG;
+  if (!ts || k == 0 || k > (uint32_t)MAX_TREES || g->part) return MEERKAT_E_INVALID_ARG;
   for (uint32_t i = 0; i < k; i++) {
     meerkat_tree* t = ts[i];
-    if (!t || t->g != g || t->dist) return MEERKAT_E_INVALID_ARG;
+    if (!t || t->g != g) return MEERKAT_E_INVALID_ARG;
     if (t->vanilla) return MEERKAT_E_STATE;   // no dependence tree: static only
     for (uint32_t j = 0; j < i; j++)
       if (ts[j] == t) return MEERKAT_E_INVALID_ARG;
@@ -617,7 +655,7 @@ static cudaError_t unseed(meerkat_graph* g, meerkat_tree* t) {
 }
 
 meerkat_status meerkat_tree_recompute_scheme(meerkat_graph* g, meerkat_tree* t, uint32_t iteration_scheme) {
-  if (!g || !t || t->g != g || t->dist || (iteration_scheme != 1 && iteration_scheme != 2))
+  if (!g || !t || t->g != g || t->part || (iteration_scheme != 1 && iteration_scheme != 2))
     return MEERKAT_E_INVALID_ARG;
   DeviceGuard dg(g->device);
   t->dev.scheme1 = iteration_scheme == 1 ? 1u : 0u;
@@ -630,8 +668,9 @@ meerkat_status meerkat_tree_recompute_scheme(meerkat_graph* g, meerkat_tree* t, 
 }
 
 meerkat_status meerkat_tree_recompute(meerkat_graph* g, meerkat_tree* t) {
-  if (!g || !t || t->g != g || t->dist) return MEERKAT_E_INVALID_ARG;
+  if (!g || !t || t->g != g) return MEERKAT_E_INVALID_ARG;
   DeviceGuard dg(g->device);
+  if (t->part) return part_trees(g, &t, 1, 0, nullptr, nullptr, nullptr, 0);
   cudaError_t e = unseed(g, t);
   if (e == cudaSuccess) e = launch_tree(g, &t, 1, MODE_STATIC, nullptr, nullptr, nullptr, 0);
   if (e != cudaSuccess) return MEERKAT_E_CUDA;
@@ -644,6 +683,7 @@ meerkat_status meerkat_tree_nodes(meerkat_tree* t, uint64_t* out) {
   if (t->vanilla) return MEERKAT_E_STATE;   // distances only: meerkat_tree_distances
   meerkat_graph* g = t->g;
   DeviceGuard dg(g->device);
+  if (t->part) return part_tree_nodes(t, out);   // collective all-gather, global id order
   const bool host = !is_device_ptr(out);
   cudaError_t e = cudaMemcpyAsync(out, t->dev.node, (size_t)g->Vl * 8,
                                   host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, g->stream);
@@ -698,6 +738,7 @@ meerkat_status meerkat_tree_stats_get(meerkat_tree* t, meerkat_tree_stats* out) 
   out->version = t->version;
   out->source = t->dev.source;
   out->unit_weights = t->unit ? 1 : 0;
+  out->exchanges = t->last_units;
   return MEERKAT_OK;
 }
 
@@ -726,96 +767,10 @@ meerkat_status meerkat_tree_destroy(meerkat_tree* t) {
   cudaFree(T.node); cudaFree(T.stamp); cudaFree(T.inval_bits); cudaFree(T.inval_list);
   cudaFree(T.fr[0]); cudaFree(T.fr[1]); cudaFree(t->ctrl_base); cudaFree(T.epoch_ptr);
   if (t->hctrl) cudaFreeHost(t->hctrl);
-  dtree_free(t);
+  part_tree_free(t);
   if (t->counted) t->g->n_trees--;
   delete t;
   return MEERKAT_OK;
-}
-
-// ------------------------------------------------------------------ vertex-partitioned trees
-
-meerkat_status meerkat_dtree_create(meerkat_graph* g, uint32_t source, uint32_t unit_weights, meerkat_tree** out) {
-  return tree_create(g, source, unit_weights != 0, true, out);
-}
-
-meerkat_status meerkat_dtree_phase(meerkat_graph* g, meerkat_tree* t, meerkat_dphase phase, const void* a,
-                                   const void* b, const void* c, uint64_t n, meerkat_dresult* out) {
-  if (!g || !t || t->g != g || !t->dist) return MEERKAT_E_INVALID_ARG;
-  DeviceGuard dg(g->device);
-  // batch inputs may live on the host (staged like every other call); received messages likewise
-  const void *da = a, *db = b, *dc = c;
-  cudaError_t e = cudaSuccess;
-  const bool pairs = phase == MEERKAT_D_APPLY_PROPAGATE || phase == MEERKAT_D_APPLY_RELAX;
-  if (a) e = stage_in(g, 0, a, n * (pairs ? 16 : 4), &da);
-  if (e == cudaSuccess && b) e = stage_in(g, 1, b, n * 4, &db);
-  if (e == cudaSuccess && c) e = stage_in(g, 2, c, n * 4, &dc);
-  if (e != cudaSuccess) return MEERKAT_E_CUDA;
-  return dtree_phase(g, t, (int)phase, da, db, dc, n, out);
-}
-
-meerkat_status meerkat_memcpy(meerkat_graph* g, void* dst, const void* src, uint64_t bytes) {
-  if (!g || (bytes && (!dst || !src))) return MEERKAT_E_INVALID_ARG;
-  if (!bytes) return MEERKAT_OK;
-  DeviceGuard dg(g->device);
-  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, g->stream);
-  if (e == cudaSuccess && (!is_device_ptr(dst) || !is_device_ptr(src))) e = cudaStreamSynchronize(g->stream);
-  return from_cuda(e);
-}
-
-meerkat_status meerkat_dtrees_pack(meerkat_graph* g, meerkat_tree* const* trees, uint32_t k, int64_t* meta,
-                                   uint64_t* send, uint64_t capacity_pairs, uint64_t* send_counts) {
-  if (!g || !trees || !meta || !send_counts || k == 0 || k > 8) return MEERKAT_E_INVALID_ARG;
-  for (uint32_t i = 0; i < k; i++)
-    if (!trees[i] || trees[i]->g != g || !trees[i]->dist) return MEERKAT_E_INVALID_ARG;
-  DeviceGuard dg(g->device);
-  return dtrees_pack(g, trees, k, meta, send, capacity_pairs, send_counts);
-}
-
-meerkat_status meerkat_dtrees_apply(meerkat_graph* g, meerkat_tree* const* trees, uint32_t k, meerkat_dphase phase,
-                                    const uint64_t* recv, const uint64_t* recv_counts) {
-  if (!g || !trees || !recv_counts || k == 0 || k > 8) return MEERKAT_E_INVALID_ARG;
-  if (phase != MEERKAT_D_APPLY_RELAX && phase != MEERKAT_D_APPLY_PROPAGATE) return MEERKAT_E_INVALID_ARG;
-  for (uint32_t i = 0; i < k; i++)
-    if (!trees[i] || trees[i]->g != g || !trees[i]->dist) return MEERKAT_E_INVALID_ARG;
-  DeviceGuard dg(g->device);
-  return dtrees_apply(g, trees, k, (int)phase, recv, recv_counts);
-}
-
-meerkat_status meerkat_dtrees_scan(meerkat_graph* g, meerkat_tree* const* trees, uint32_t k,
-                                   const uint32_t* const* invalid_lists, const uint64_t* invalid_counts,
-                                   meerkat_dresult* outs) {
-  if (!g || !trees || !invalid_lists || !invalid_counts || k == 0 || k > 2) return MEERKAT_E_INVALID_ARG;
-  for (uint32_t i = 0; i < k; i++) {
-    if (!trees[i] || trees[i]->g != g || !trees[i]->dist) return MEERKAT_E_INVALID_ARG;
-    if (invalid_counts[i] && !invalid_lists[i]) return MEERKAT_E_INVALID_ARG;
-  }
-  DeviceGuard dg(g->device);
-  return dtrees_scan(g, trees, k, invalid_lists, invalid_counts, outs);
-}
-
-meerkat_status meerkat_dtrees_expand(meerkat_graph* g, meerkat_tree* const* trees, uint32_t k, meerkat_dphase phase,
-                                     meerkat_dresult* outs) {
-  if (!g || !trees || k == 0 || k > 8) return MEERKAT_E_INVALID_ARG;
-  if (phase != MEERKAT_D_RELAX && phase != MEERKAT_D_PROPAGATE) return MEERKAT_E_INVALID_ARG;
-  for (uint32_t i = 0; i < k; i++)
-    if (!trees[i] || trees[i]->g != g || !trees[i]->dist) return MEERKAT_E_INVALID_ARG;
-  DeviceGuard dg(g->device);
-  return dtrees_expand(g, trees, k, (int)phase, outs);
-}
-
-meerkat_status meerkat_route(meerkat_graph* g, int key_is_b, const uint32_t* a, const uint32_t* b, const uint32_t* c,
-                             uint64_t n, uint32_t* out_a, uint32_t* out_b, uint32_t* out_c, uint64_t* counts) {
-  if (!g || !counts || (n && (!a || !b || !out_a || !out_b || (c && !out_c)))) return MEERKAT_E_INVALID_ARG;
-  if (n && (!is_device_ptr(out_a) || !is_device_ptr(out_b) || (c && !is_device_ptr(out_c))))
-    return MEERKAT_E_INVALID_ARG;
-  DeviceGuard dg(g->device);
-  const void *da = a, *db = b, *dc = c;
-  cudaError_t e = stage_in(g, 0, a, n * 4, &da);
-  if (e == cudaSuccess) e = stage_in(g, 1, b, n * 4, &db);
-  if (e == cudaSuccess && c) e = stage_in(g, 2, c, n * 4, &dc);
-  if (e != cudaSuccess) return MEERKAT_E_CUDA;
-  return route_batch(g, key_is_b, (const uint32_t*)da, (const uint32_t*)db, (const uint32_t*)dc, n, out_a, out_b,
-                     out_c, counts);
 }
 
 /* ------------------------------------------------------------------ PageRank (pagerank.cu) */
@@ -836,7 +791,7 @@ meerkat_status meerkat_pagerank_create(meerkat_graph* g, double damping, double 
   if (!g || !out) return MEERKAT_E_INVALID_ARG;
   *out = nullptr;
   if (!(damping > 0.0 && damping < 1.0) || !(error_margin > 0.0) || max_iter == 0) return MEERKAT_E_INVALID_ARG;
-  if (!g->reverse || g->ws > 1) return MEERKAT_E_STATE;   // Compute walks in-edges
+  if (!g->reverse || g->part) return MEERKAT_E_STATE;   // Compute walks in-edges
   DeviceGuard dg(g->device);
   meerkat_pagerank* p = new (std::nothrow) meerkat_pagerank();
   if (!p) return MEERKAT_E_CUDA;
@@ -916,7 +871,7 @@ meerkat_status meerkat_pagerank_destroy(meerkat_pagerank* p) {
 static meerkat_status tc_check(meerkat_graph* a, meerkat_graph* b) {
   if (!a || !b) return MEERKAT_E_INVALID_ARG;
   if (a->device != b->device || a->V != b->V) return MEERKAT_E_INVALID_ARG;
-  if (a->ws > 1 || b->ws > 1) return MEERKAT_E_STATE;
+  if (a->part || b->part) return MEERKAT_E_STATE;
   return MEERKAT_OK;
 }
 
@@ -1007,7 +962,7 @@ meerkat_status meerkat_tc_decremental(meerkat_graph* g_after, meerkat_graph* g_u
 meerkat_status meerkat_wcc_create(meerkat_graph* g, meerkat_wcc** out) {
   if (!g || !out) return MEERKAT_E_INVALID_ARG;
   *out = nullptr;
-  if (g->ws > 1) return MEERKAT_E_STATE;
+  if (g->part) return MEERKAT_E_STATE;
   DeviceGuard dg(g->device);
   meerkat_wcc* c = new (std::nothrow) meerkat_wcc();
   if (!c) return MEERKAT_E_CUDA;

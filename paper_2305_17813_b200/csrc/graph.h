@@ -62,6 +62,7 @@ struct TreeDev {
 }  // namespace mk
 
 namespace mk {
+struct PartState;
 // One slab store (out-edges, or the optional in-edge mirror) on the device.
 struct Store {
   GraphDev dev{};
@@ -77,7 +78,7 @@ struct meerkat_graph {
   cudaStream_t stream = nullptr;
   uint32_t V = 0;                   // global vertex count
   uint32_t Vl = 0;                  // vertices held by this partition
-  uint32_t ws = 1, rank = 0;        // vertex partition (owner(v) = v % ws)
+  uint32_t ws = 1, rank = 0;        // vertex partition (owner(v) = pm_mix(v) % ws, internal.cuh)
   bool weighted = false, hashing = true, reverse = false;
   float lf = 0.7f;
   mk::Store out;                    // out-edge store (the paper's SlabGraph)
@@ -97,9 +98,7 @@ struct meerkat_graph {
   uint64_t staged_version[4] = {0, 0, 0, 0};
   int tree_blocks_per_sm[4] = {0, 0, 0, 0};   // cooperative occupancy: static, incremental, decremental, vanilla
   int latency_bps = 0;                      // blocks/SM for latency-bound tree calls (0 = occupancy)
-  unsigned long long* rscratch = nullptr;   // meerkat_route: device counts + cursors
-  unsigned long long* hrscratch = nullptr;  // pinned counts
-  int64_t* hmeta = nullptr;                 // pinned: meerkat_dtrees_pack's meta rows
+  mk::PartState* part = nullptr;            // vertex-partitioned graph (part.cu): transport, rings, routed rows
 };
 
 struct meerkat_tree {
@@ -113,18 +112,10 @@ struct meerkat_tree {
   int parity = 0;
   int seeded = 0;   // 1 / 2: insert_batch_trees / delete_batch_trees ran this call's batch prologue
   bool counted = false;   // counted in g->n_trees
-  // vertex-partitioned trees (dtree.cu)
-  bool dist = false;
-  int cur = 0;                              // frontier buffer filled by the last phase
-  uint64_t cur_n = 0;                       // its size as of the last synchronising phase (a grid bound)
-  uint32_t depoch = 0;                      // stamp epoch of the frontier being filled
-  uint64_t* msg_raw = nullptr;              // outgoing pairs, unsorted
-  uint64_t* msg_out = nullptr;              // outgoing pairs grouped by destination rank
-  uint64_t msg_cap = 0;                     // pairs
-  unsigned long long* dcnt = nullptr;       // device: counts[64], cursor[64], msg_n
-  unsigned long long* hcnt = nullptr;       // pinned mirror of counts + msg_n
-  uint32_t last_inval_n = 0;
-  uint64_t last_front = 0;                  // local frontier reported by the last synchronising phase
+  // vertex-partitioned trees (part.cu)
+  bool part = false;
+  uint64_t* pull_items = nullptr;           // (invalid vertex, in-bucket) items of the mirror frontier
+  uint64_t last_units = 0;                  // exchange units of the last call
   size_t bytes = 0;
 };
 
@@ -190,19 +181,25 @@ enum TreeMode { MODE_STATIC = 0, MODE_INCREMENTAL = 1, MODE_DECREMENTAL = 2 };
 cudaError_t launch_tree(meerkat_graph* g, meerkat_tree* const* trees, uint32_t ntrees, int mode, const uint32_t* s,
                         const uint32_t* d, const uint32_t* w, uint64_t n, bool pro_done = false, int fp_mode = -1);
 cudaError_t launch_node_dist(meerkat_graph* g, meerkat_tree* t, uint32_t* out);
-// dtree.cu
-meerkat_status dtree_phase(meerkat_graph* g, meerkat_tree* t, int phase, const void* a, const void* b,
-                           const void* c, uint64_t n, meerkat_dresult* out);
-meerkat_status dtree_init(meerkat_graph* g, meerkat_tree* t);
-meerkat_status dtrees_pack(meerkat_graph* g, meerkat_tree* const* trees, uint32_t k, int64_t* meta, uint64_t* send,
-                           uint64_t capacity_pairs, uint64_t* send_counts);
-meerkat_status dtrees_apply(meerkat_graph* g, meerkat_tree* const* trees, uint32_t k, int phase,
-                            const uint64_t* recv, const uint64_t* rc);
-meerkat_status dtrees_scan(meerkat_graph* g, meerkat_tree* const* trees, uint32_t k, const uint32_t* const* lists,
-                           const uint64_t* ns, meerkat_dresult* outs);
-meerkat_status dtrees_expand(meerkat_graph* g, meerkat_tree* const* trees, uint32_t k, int phase,
-                             meerkat_dresult* outs);
-void dtree_free(meerkat_tree* t);
-meerkat_status route_batch(meerkat_graph* g, int key_is_b, const uint32_t* a, const uint32_t* b, const uint32_t* c,
-                           uint64_t n, uint32_t* oa, uint32_t* ob, uint32_t* oc, uint64_t* counts);
+// part.cu (vertex-partitioned graphs)
+meerkat_status part_init(meerkat_graph* g, const meerkat_config* cfg);   // after the stores are built
+void part_free(meerkat_graph* g);
+meerkat_status part_hints(meerkat_graph* g, const uint32_t* global_hints, const void** local_hints, int slot);
+meerkat_status part_mutate(meerkat_graph* g, int kind, const uint32_t* s, const uint32_t* d, const uint32_t* w,
+                           uint64_t n, uint64_t* count);
+meerkat_status part_query(meerkat_graph* g, const uint32_t* s, const uint32_t* d, uint64_t n, uint8_t* found,
+                          uint32_t* w_out);
+meerkat_status part_tree_init(meerkat_graph* g, meerkat_tree* t);
+void part_tree_free(meerkat_tree* t);
+// kind: 0 static recompute, 1 incremental, 2 decremental (the batch must be the last mutation's)
+meerkat_status part_trees(meerkat_graph* g, meerkat_tree* const* trees, uint32_t k, int kind, const uint32_t* s,
+                          const uint32_t* d, const uint32_t* w, uint64_t n);
+meerkat_status part_tree_nodes(meerkat_tree* t, uint64_t* out);
+meerkat_status part_allreduce(meerkat_graph* g, uint64_t* vals, uint32_t m);   // sums over ranks (collective)
+// api.cu helpers shared with part.cu
+bool is_device_ptr(const void* p);
+cudaError_t stage_in(meerkat_graph* g, int slot, const void* p, size_t bytes, const void** out);
+cudaError_t ensure_stage(meerkat_graph* g, int slot, size_t bytes);
+meerkat_status collect(meerkat_graph* g);
+cudaError_t mutated(meerkat_graph* g, int kind, uint64_t n);
 }  // namespace mk

@@ -64,13 +64,71 @@ struct GraphDev {
   GraphCtrl* ctrl;
   uint32_t V, H, P, seed;   // V: vertices held here (vmeta entries); H/P: arena / pool slabs
   uint32_t Vg;              // global vertex count: the key range
-  uint32_t ws, rank;        // vertex partition: this store holds sources u with u % ws == rank, at u / ws
+  uint32_t ws, rank;        // vertex partition: this store holds the sources u with owner(u) == rank, at row(u)
+  uint32_t pbits;           // placement domain [0, 2^pbits) of pm_mix (ws > 1)
 };
+
+// ---- Vertex placement of a partitioned graph ("let the library place
+// vertices through a bijective mixer"): m = pm_mix(v) is a bijection on [0, V) -- two rounds of
+// (multiply by an odd constant, xor-shift) on [0, 2^bits), cycle-walked back into [0, V) -- and
+// owner(v) = m % ws, row(v) = m / ws.  Unscrambled R-MAT ids (whose low bits are skewed) land
+// balanced; results do not depend on the placement (tree arrays are exported in global id order).
+// world_size 1 is the identity.
+constexpr uint32_t PM_A1 = 0x9E3779B1u, PM_A2 = 0x85EBCA77u;
+__host__ __device__ constexpr uint32_t pm_inv(uint32_t a) {   // inverse of an odd a mod 2^32 (Newton)
+  uint32_t x = a;
+  for (int i = 0; i < 5; i++) x *= 2u - a * x;
+  return x;
+}
+__host__ __device__ __forceinline__ uint32_t pm_mask(uint32_t bits) { return bits >= 32 ? 0xFFFFFFFFu : (1u << bits) - 1u; }
+__host__ __device__ __forceinline__ uint32_t pm_step(uint32_t x, uint32_t a, uint32_t bits) {
+  x = (x * a) & pm_mask(bits);
+  return x ^ (x >> ((bits + 1) / 2));
+}
+__host__ __device__ __forceinline__ uint32_t pm_unstep(uint32_t y, uint32_t ainv, uint32_t bits) {
+  const uint32_t s = (bits + 1) / 2;
+  uint32_t x = y;
+  for (uint32_t k = s; k < bits; k += s) x = y ^ (x >> s);   // invert x ^ (x >> s)
+  return (x * ainv) & pm_mask(bits);
+}
+__host__ __device__ __forceinline__ uint32_t pm_mix(uint32_t v, uint32_t V, uint32_t bits) {
+  uint32_t x = v;
+  do { x = pm_step(pm_step(x, PM_A1, bits), PM_A2, bits); } while (x >= V);
+  return x;
+}
+__host__ __device__ __forceinline__ uint32_t pm_unmix(uint32_t m, uint32_t V, uint32_t bits) {
+  constexpr uint32_t I1 = pm_inv(PM_A1), I2 = pm_inv(PM_A2);
+  uint32_t x = m;
+  do { x = pm_unstep(pm_unstep(x, I2, bits), I1, bits); } while (x >= V);
+  return x;
+}
+__host__ __device__ __forceinline__ uint32_t pm_bits(uint32_t V) {
+  uint32_t b = 1;
+  while (b < 32 && (1ull << b) < V) b++;
+  return b;
+}
+// owner rank of global id x, and its row there
+__host__ __device__ __forceinline__ uint32_t pm_place(uint32_t x, uint32_t V, uint32_t bits, uint32_t ws, uint32_t& row) {
+  if (ws <= 1) { row = x; return 0; }
+  const uint32_t m = pm_mix(x, V, bits);
+  row = m / ws;
+  return m % ws;
+}
+__host__ __device__ __forceinline__ uint32_t pm_global(uint32_t row, uint32_t rank, uint32_t V, uint32_t bits, uint32_t ws) {
+  return ws <= 1 ? row : pm_unmix(row * ws + rank, V, bits);
+}
+__device__ __forceinline__ uint32_t g_place(const GraphDev& G, uint32_t x, uint32_t& row) {
+  return pm_place(x, G.Vg, G.pbits, G.ws, row);
+}
+__device__ __forceinline__ uint32_t g_global(const GraphDev& G, uint32_t row) {
+  return pm_global(row, G.rank, G.Vg, G.pbits, G.ws);
+}
 
 // Source id -> local row, or INVALID_SLAB if u is not held by this partition.
 __device__ __forceinline__ uint32_t local_row(const GraphDev& G, uint32_t u) {
   if (G.ws <= 1) return u;
-  return (u % G.ws == G.rank) ? u / G.ws : INVALID_SLAB;
+  uint32_t row;
+  return g_place(G, u, row) == G.rank ? row : INVALID_SLAB;
 }
 
 __device__ __forceinline__ uint32_t* slab_ptr(const GraphDev& G, uint32_t s) {

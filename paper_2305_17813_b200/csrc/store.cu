@@ -600,7 +600,7 @@ __global__ void __launch_bounds__(UPD_BLOCK) k_export(GraphDev G, uint64_t n_sla
     for (int k = 0; k < NK; k++) {
       const uint32_t key = F::key(d, k);
       if (own != NO_OWNER && F::valid_cell(l8, k) && key != EMPTY_KEY && key != TOMBSTONE_KEY) {
-        if (o < cap) { os[o] = own * G.ws + G.rank; od[o] = key; if (ow) ow[o] = MAP ? F::weight(d, k) : 0u; }
+        if (o < cap) { os[o] = g_global(G, own); od[o] = key; if (ow) ow[o] = MAP ? F::weight(d, k) : 0u; }
         o++;
       }
     }
@@ -799,7 +799,7 @@ cudaError_t launch_build(meerkat_graph* g, Store& st, const uint32_t* d_hints, u
     memset(st.hctrl, 0, sizeof(GraphCtrl));
     st.bytes = nslab * 132 + (size_t)V * 12 + sizeof(GraphCtrl);
     st.dev.V = V; st.dev.H = (uint32_t)st.H; st.dev.P = (uint32_t)st.P;
-    st.dev.Vg = g->V; st.dev.ws = g->ws; st.dev.rank = g->rank;
+    st.dev.Vg = g->V; st.dev.ws = g->ws; st.dev.rank = g->rank; st.dev.pbits = pm_bits(g->V);
     if (st.H) {
       const unsigned gf = (unsigned)std::min<uint64_t>((st.H * 8 + 255) / 256, (uint64_t)g->sm_count * 16);
       k_fill<<<gf, 256, 0, g->stream>>>(st.dev.slabs, st.H, g->weighted ? 1 : 0);

@@ -1,9 +1,10 @@
 """Vertex-partitioned (multi-GPU) path against the oracle.
 
-The box has one GPU, so world_size 2 and 3 run as separate processes sharing
-cuda:0 and exchanging through host memory (gloo); the partition logic, the
-phase kernels, routing and termination are the ones NCCL drives on 8 GPUs.
-world_size 1 runs through NCCL.  Every result must be bit-identical to the
+The box has one GPU, so world_size 2..8 run as separate processes sharing
+cuda:0 whose library exchanges through host memory (the gloo host transport);
+routing, the exchange units, the device-side phase changes and termination are
+the ones the NCCL transport drives on 8 GPUs.  world_size 1 runs with the
+library's own NCCL communicator.  Every result must be bit-identical to the
 oracle (edge set, counts, query answers, SSSP and BFS nodes after every batch)."""
 import socket
 
@@ -23,7 +24,7 @@ def _port():
     return p
 
 
-def _worker(rank, ws, port, backend, scale, q):
+def _worker(rank, ws, port, backend, scale, reverse, pairs, q):
     import torch.distributed as dist
     try:
         torch.cuda.set_device(0)
@@ -35,9 +36,10 @@ def _worker(rank, ws, port, backend, scale, q):
         W = synth.rmat_dynamic(scale, 16, batch=500, n_ins=2, n_del=2)
         V, src = W.vertex_n, W.source
         bs, bd, bw = W.base
-        # each rank brings a different slice of every batch (routing must gather them)
+        # each rank brings a different slice of every batch (the library routes them)
         sl = lambda a: a[rank::ws]
-        g = DistGraph(V, degree_hints=synth.degrees(bs, V), device=torch.device("cuda", 0))
+        g = DistGraph(V, degree_hints=synth.degrees(bs, V), in_degree_hints=synth.degrees(bd, V) if reverse else None,
+                      reverse=reverse, device=torch.device("cuda", 0), exchange_pairs=pairs)
         o = oracle.OracleGraph(V)
         n = g.insert(sl(bs), sl(bd), sl(bw))
         assert n == o.insert(bs, bd, bw)[1], "bulk insert count"
@@ -57,7 +59,7 @@ def _worker(rank, ws, port, backend, scale, q):
         for i, (s, d, w) in enumerate(W.inserts):
             n = g.insert(sl(s), sl(d), sl(w))
             assert n == o.insert(s, d, w)[1]
-            if i % 2 == 0:   # fused lock-step update of both trees (DistGraph.trees_incremental)
+            if i % 2 == 0:   # fused lock-step update of both trees
                 g.trees_incremental([t, b], sl(s), sl(d), sl(w))
             else:
                 t.incremental(sl(s), sl(d), sl(w))
@@ -72,6 +74,9 @@ def _worker(rank, ws, port, backend, scale, q):
                 t.decremental(sl(s), sl(d))
                 b.decremental(sl(s), sl(d))
             check(f"dec{i}")
+            st = t.stats()
+            if ws > 1 and st["exchanges"] < 2:
+                errs.append(f"dec{i}: {st['exchanges']} exchanges")
         # queries in the caller's order, across partitions
         es, ed, ew = o.edges()
         rng = np.random.default_rng(rank)
@@ -79,11 +84,26 @@ def _worker(rank, ws, port, backend, scale, q):
         qd = np.concatenate([ed[:300], rng.integers(0, V, 300)]).astype(np.uint32)
         f, qw = g.query(qs, qd)
         _, ef, eww = o.query(qs, qd)
-        if not (np.array_equal(f.cpu().numpy(), ef) and np.array_equal(qw.cpu().numpy().view(np.uint32), eww)):
+        if not (np.array_equal(np.asarray(f), ef) and np.array_equal(np.asarray(qw).view(np.uint32), eww)):
             errs.append("query answers")
         gs, gd, gw = g.export_edges()
         if rank == 0 and not (np.array_equal(gs, es) and np.array_equal(gd, ed) and np.array_equal(gw, ew)):
             errs.append("edge set")
+        # static recompute equals the maintained trees
+        before = t.nodes()
+        t.recompute()
+        after = t.nodes()   # collective: every rank calls it
+        if rank == 0 and not np.array_equal(before, after):
+            errs.append("recompute")
+        # ordering contract: a different batch than the last mutation's is refused on every rank
+        s, d, w = W.inserts[0]
+        g.insert(sl(s[:50]), sl(d[:50]), sl(w[:50]))
+        from paper_2305_17813_b200._lib import MeerkatError
+        try:
+            t.incremental(sl(s[50:100]), sl(d[50:100]), sl(w[50:100]))
+            errs.append("wrong batch accepted")
+        except MeerkatError:
+            pass
         q.put((rank, errs))
     except Exception:  # pragma: no cover
         import traceback
@@ -93,18 +113,22 @@ def _worker(rank, ws, port, backend, scale, q):
             dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("ws,backend,scale", [(1, "nccl", 12), (2, "gloo", 12), (3, "gloo", 13), (4, "gloo", 12),
-                                             (8, "gloo", 12)])
-def test_partitioned_dynamic_sssp_bfs(ws, backend, scale):
+# world_size, backend, R-MAT scale, in-edge mirror (pull frontier) or the paper's scan, messages
+# per peer per exchange (small values force carry-over across exchanges)
+@pytest.mark.parametrize("ws,backend,scale,reverse,pairs", [
+    (1, "nccl", 12, False, 0), (1, "nccl", 12, True, 0), (2, "gloo", 12, False, 0), (2, "gloo", 12, True, 0),
+    (3, "gloo", 13, True, 0), (4, "gloo", 12, False, 0), (4, "gloo", 12, True, 64), (8, "gloo", 12, True, 0),
+    (8, "gloo", 12, False, 32)])
+def test_partitioned_dynamic_sssp_bfs(ws, backend, scale, reverse, pairs):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    ps = [ctx.Process(target=_worker, args=(r, ws, port, backend, scale, q)) for r in range(ws)]
+    ps = [ctx.Process(target=_worker, args=(r, ws, port, backend, scale, reverse, pairs, q)) for r in range(ws)]
     for p in ps:
         p.start()
-    res = [q.get(timeout=600) for _ in ps]
+    res = [q.get(timeout=900) for _ in ps]
     for p in ps:
         p.join(timeout=60)
     for r, errs in res:
