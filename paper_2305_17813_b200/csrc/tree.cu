@@ -190,6 +190,27 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const TreeDev& T, int 
         for (int kk = 0; kk < NK; kk++) live[kk] = live[kk] && cand[kk] < pv[kk];
       }
       unsigned long long old[NK];
+      uint32_t st[NK];
+      if constexpr (SPEC_STAMP && !V32 && !SPROBE) {
+        // speculative: the atomicMin, the stamp exchange and the vmeta load of a key that passed the
+        // probe are issued together (one dependent round trip instead of two).  x is enqueued iff this
+        // lane won the stamp: a lane whose atomicMin lost to a smaller candidate of the same round
+        // still enqueues x correctly (x WAS improved this round); every improvement comes from a lane
+        // that passed the probe and tried the stamp, so x is enqueued exactly once when improved.
+#pragma unroll
+        for (int kk = 0; kk < NK; kk++) {
+          old[kk] = live[kk] ? atomicMin(reinterpret_cast<unsigned long long*>(T.node + xs[kk]),
+                                         (unsigned long long)cand[kk]) : 0ull;
+          st[kk] = live[kk] ? atomicExch(T.stamp + xs[kk], epoch_next) : epoch_next;
+          mv[kk] = live[kk] ? __ldcg(G.vmeta + xs[kk]) : make_uint2(INVALID_SLAB, 0);
+        }
+#pragma unroll
+        for (int kk = 0; kk < NK; kk++) {
+          if (live[kk] && cand[kk] < old[kk]) c.improved++;
+          has[kk] = st[kk] != epoch_next;
+        }
+        warp_enqueue_multi<NK>(T, fnext, sznext, has, xs, mv, c);
+      } else {
 #pragma unroll
       for (int kk = 0; kk < NK; kk++) {
         if constexpr (V32)
@@ -198,7 +219,6 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const TreeDev& T, int 
           old[kk] = live[kk] ? atomicMin(reinterpret_cast<unsigned long long*>(T.node + xs[kk]),
                                          (unsigned long long)cand[kk]) : 0ull;
       }
-      uint32_t st[NK];
 #pragma unroll
       for (int kk = 0; kk < NK; kk++) {
         st[kk] = epoch_next;
@@ -213,6 +233,7 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const TreeDev& T, int 
 #pragma unroll
       for (int kk = 0; kk < NK; kk++) has[kk] = st[kk] != epoch_next;
       warp_enqueue_multi<NK>(T, fnext, sznext, has, xs, mv, c);
+      }
     } else if (VISIT == PROPAGATE) {
       // PropagateInvalidation, top-down (C14): the children x (parent(x) = v) of invalid v
       bool live[NK];
@@ -224,15 +245,21 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const TreeDev& T, int 
         cur[kk] = live[kk] ? ld_cg_u64(T.node + x) : UNREACHED;
         if (live[kk]) c.visited++;
       }
+      // the CAS of a child and its vmeta load are issued together (SPEC_STAMP: one round trip)
+      bool child[NK];
+      unsigned long long oc[NK];
 #pragma unroll
       for (int kk = 0; kk < NK; kk++) {
         const uint32_t x = xs[kk];
-        if (cur[kk] != UNREACHED && (uint32_t)cur[kk] == v && x != T.source &&
-            atomicCAS(reinterpret_cast<unsigned long long*>(T.node + x), (unsigned long long)cur[kk],
-                      (unsigned long long)UNREACHED) == cur[kk]) {
-          mv[kk] = __ldcg(G.vmeta + x);
-          has[kk] = true;
-        }
+        child[kk] = cur[kk] != UNREACHED && (uint32_t)cur[kk] == v && x != T.source;
+        oc[kk] = child[kk] ? atomicCAS(reinterpret_cast<unsigned long long*>(T.node + x), (unsigned long long)cur[kk],
+                                       (unsigned long long)UNREACHED) : 0ull;
+        if (SPEC_STAMP && child[kk]) mv[kk] = __ldcg(G.vmeta + x);
+      }
+#pragma unroll
+      for (int kk = 0; kk < NK; kk++) {
+        has[kk] = child[kk] && oc[kk] == cur[kk];
+        if (!SPEC_STAMP && has[kk]) mv[kk] = __ldcg(G.vmeta + xs[kk]);
       }
       warp_mark_invalid<NK>(T, has, xs);
       warp_enqueue_multi<NK>(T, fnext, sznext, has, xs, mv, c);
@@ -269,6 +296,14 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const TreeDev& T, int 
       uint32_t xv[1] = {v};
       uint2 mv1[1] = {make_uint2(INVALID_SLAB, 0)};
       if (l8 == 0 && best != UNREACHED && best < pull_nv) {
+        if (SPEC_STAMP) {   // atomicMin, stamp exchange and vmeta together (see RELAX)
+          const unsigned long long o = atomicMin(reinterpret_cast<unsigned long long*>(T.node + v),
+                                                 (unsigned long long)best);
+          const uint32_t stv = pull_st != epoch_next ? atomicExch(T.stamp + v, epoch_next) : epoch_next;
+          mv1[0] = pull_st != epoch_next ? __ldcg(G.vmeta + v) : make_uint2(INVALID_SLAB, 0);
+          if (best < o) c.improved++;
+          hv[0] = stv != epoch_next;
+        } else {
         const unsigned long long o = atomicMin(reinterpret_cast<unsigned long long*>(T.node + v),
                                                (unsigned long long)best);
         if (best < o) {
@@ -278,6 +313,7 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const TreeDev& T, int 
             mv1[0] = __ldcg(G.vmeta + v);
             hv[0] = stv != epoch_next;
           }
+        }
         }
       }
       warp_enqueue_multi<1>(T, fnext, sznext, hv, xv, mv1, c);

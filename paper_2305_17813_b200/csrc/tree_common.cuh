@@ -28,7 +28,14 @@ constexpr uint64_t PROBE_MIN_ITEMS = MEERKAT_PROBE_MIN_ITEMS;   // frontiers abo
 #ifndef MEERKAT_TAIL_ITEMS
 #define MEERKAT_TAIL_ITEMS 64
 #endif
-constexpr uint64_t TAIL_ITEMS = MEERKAT_TAIL_ITEMS;   // frontiers this small run in block 0 alone (run_rounds)
+constexpr uint64_t TAIL_ITEMS = MEERKAT_TAIL_ITEMS;
+#ifndef MEERKAT_SPEC_STAMP
+#define MEERKAT_SPEC_STAMP 1
+#endif
+// 1: a relaxation that passed the node[x] probe issues its atomicMin, the stamp exchange and the
+// vmeta load together, and a propagation its CAS and vmeta load together: one dependent round trip
+// fewer per slab step (tree.cu expand, the batch prologues).  0: the result-gated sequence.
+constexpr bool SPEC_STAMP = MEERKAT_SPEC_STAMP != 0;   // frontiers this small run in block 0 alone (run_rounds)
 
 enum Visit { RELAX = 0, PROPAGATE = 1, PULL = 2 };
 constexpr int DIAG_PULL = 19;   // diagnostics round slot of the pull phase (MEERKAT_DIAG_ROUNDS builds)
@@ -320,14 +327,26 @@ __device__ __forceinline__ void tree_prologue_inc(const GraphDev& G, const TreeD
       }
     }
     unsigned long long old[MAX_TREES];
-#pragma unroll
-    for (int k = 0; k < MAX_TREES; k++)
-      old[k] = live[k] ? atomicMin(reinterpret_cast<unsigned long long*>(T[k].node + v), (unsigned long long)cand[k])
-                       : 0ull;
     bool has[MAX_TREES][1];
     uint2 m[MAX_TREES][1];
+    uint32_t st[MAX_TREES];
 #pragma unroll
     for (int k = 0; k < MAX_TREES; k++) {
+      old[k] = live[k] ? atomicMin(reinterpret_cast<unsigned long long*>(T[k].node + v), (unsigned long long)cand[k])
+                       : 0ull;
+      if (SPEC_STAMP) {   // stamp exchange and vmeta beside the atomicMin (expand's RELAX explains why)
+        st[k] = live[k] ? atomicExch(T[k].stamp + v, epoch[k]) : epoch[k];
+        m[k][0] = live[k] ? __ldcg(G.vmeta + v) : make_uint2(INVALID_SLAB, 0);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < MAX_TREES; k++) {
+      if (SPEC_STAMP) {
+        if (live[k] && cand[k] < old[k]) c.improved++;
+        has[k][0] = st[k] != epoch[k];
+        if (LAZY && has[k][0] && (m[k][0].x == INVALID_SLAB || m[k][0].x == LINKING)) m[k][0] = make_uint2(LINKING, 1u);
+        continue;
+      }
       has[k][0] = false;
       m[k][0] = make_uint2(INVALID_SLAB, 0);
       if (live[k] && cand[k] < old[k]) {
@@ -369,10 +388,12 @@ __device__ __forceinline__ void tree_prologue_dec(const GraphDev& G, const TreeD
     uint2 m[MAX_TREES][1];
 #pragma unroll
     for (int k = 0; k < MAX_TREES; k++) {
-      has[k][0] = cur[k] != UNREACHED && (uint32_t)cur[k] == u &&
-                  atomicCAS(reinterpret_cast<unsigned long long*>(T[k].node + v), (unsigned long long)cur[k],
-                            (unsigned long long)UNREACHED) == cur[k];
-      m[k][0] = has[k][0] ? __ldcg(G.vmeta + v) : make_uint2(INVALID_SLAB, 0);
+      const bool child = cur[k] != UNREACHED && (uint32_t)cur[k] == u;
+      const unsigned long long oc = child ? atomicCAS(reinterpret_cast<unsigned long long*>(T[k].node + v),
+                                                      (unsigned long long)cur[k], (unsigned long long)UNREACHED) : 0ull;
+      if (SPEC_STAMP) m[k][0] = child ? __ldcg(G.vmeta + v) : make_uint2(INVALID_SLAB, 0);   // beside the CAS
+      has[k][0] = child && oc == cur[k];
+      if (!SPEC_STAMP) m[k][0] = has[k][0] ? __ldcg(G.vmeta + v) : make_uint2(INVALID_SLAB, 0);
       c.direct[k] += has[k][0];
     }
     const uint32_t xv[1] = {v};
