@@ -443,6 +443,8 @@ static meerkat_status tree_create(meerkat_graph* g, uint32_t source, bool unit, 
   if (e == cudaSuccess) e = cudaMalloc(&T.fr[0], T.fr_cap * 8);
   if (e == cudaSuccess) e = cudaMalloc(&T.fr[1], T.fr_cap * 8);
   if (e == cudaSuccess) e = cudaMalloc(&t->ctrl_base, 2 * sizeof(TreeCtrl));   // double-buffered (tree.cu)
+  if (e == cudaSuccess) e = cudaMalloc(&T.bstat, (size_t)STAT_BLOCKS * 8 * 8);
+  if (e == cudaSuccess) e = cudaMemsetAsync(T.bstat, 0, (size_t)STAT_BLOCKS * 8 * 8, g->stream);
   if (e == cudaSuccess) e = cudaMemsetAsync(t->ctrl_base, 0, 2 * sizeof(TreeCtrl), g->stream);
   T.ctrl = t->ctrl_base;
   if (e == cudaSuccess) e = cudaMalloc(&T.epoch_ptr, 8);   // [0] epoch, [1] stale flag
@@ -719,6 +721,18 @@ meerkat_status meerkat_tree_stats_get(meerkat_tree* t, meerkat_tree_stats* out) 
   cudaError_t e = cudaMemcpyAsync(t->hctrl, t->dev.ctrl, sizeof(TreeCtrl), cudaMemcpyDeviceToHost, g->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
   if (e != cudaSuccess) return MEERKAT_E_CUDA;
+  // the last single-GPU call's per-block slots (its finish stored them instead of adding)
+  if (t->stat_blocks && !t->part) {
+    static thread_local unsigned long long slots[STAT_BLOCKS * 8];
+    e = cudaMemcpyAsync(slots, t->dev.bstat, (size_t)t->stat_blocks * 8 * 8, cudaMemcpyDeviceToHost, g->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+    if (e != cudaSuccess) return MEERKAT_E_CUDA;
+    unsigned long long* dst[8] = {&t->hctrl->items, &t->hctrl->slabs_read, &t->hctrl->visited, &t->hctrl->improved,
+                                  &t->hctrl->scan_slabs, &t->hctrl->scan_hits, &t->hctrl->batch_edges,
+                                  &t->hctrl->direct_n};
+    for (uint32_t b = 0; b < t->stat_blocks; b++)
+      for (int i = 0; i < 8; i++) *dst[i] += slots[(size_t)b * 8 + i];
+  }
   const TreeCtrl& c = *t->hctrl;
   std::memset(out, 0, sizeof(*out));
   out->rounds = c.rounds;
@@ -765,7 +779,7 @@ meerkat_status meerkat_tree_destroy(meerkat_tree* t) {
   cudaStreamSynchronize(t->g->stream);
   TreeDev& T = t->dev;
   cudaFree(T.node); cudaFree(T.stamp); cudaFree(T.inval_bits); cudaFree(T.inval_list);
-  cudaFree(T.fr[0]); cudaFree(T.fr[1]); cudaFree(t->ctrl_base); cudaFree(T.epoch_ptr);
+  cudaFree(T.fr[0]); cudaFree(T.fr[1]); cudaFree(t->ctrl_base); cudaFree(T.epoch_ptr); cudaFree(T.bstat);
   if (t->hctrl) cudaFreeHost(t->hctrl);
   part_tree_free(t);
   if (t->counted) t->g->n_trees--;

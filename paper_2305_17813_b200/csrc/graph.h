@@ -10,6 +10,7 @@
 namespace mk {
 
 constexpr int MAX_TREES = 2;   // trees updated together by one fused call (e.g. SSSP + BFS)
+constexpr int STAT_BLOCKS = 2048;   // per-block counter slots of a tree (>= any cooperative grid)
 
 struct TreeCtrl {
   unsigned long long size[3];       // rotating frontier sizes (see tree.cu, "round protocol")
@@ -55,6 +56,7 @@ struct TreeDev {
   uint64_t fr_cap;       // items per frontier buffer (= number of slab lists)
   uint32_t source;
   uint32_t unit;         // 1: BFS (every w = 1)
+  unsigned long long* bstat;   // per-block counter slots [STAT_BLOCKS][8] written by the tree kernels' finish
   uint32_t scheme1;      // 1: IterationScheme1 items (one per vertex, its buckets walked in turn;
                          //    static recompute only); 0: <vertex, bucket> items
 };
@@ -112,6 +114,7 @@ struct meerkat_tree {
   int parity = 0;
   int seeded = 0;   // 1 / 2: insert_batch_trees / delete_batch_trees ran this call's batch prologue
   bool counted = false;   // counted in g->n_trees
+  uint32_t stat_blocks = 0;   // grid of the last single-GPU tree call (its bstat slots)
   // vertex-partitioned trees (part.cu)
   bool part = false;
   uint64_t* pull_items = nullptr;           // (invalid vertex, in-bucket) items of the mirror frontier

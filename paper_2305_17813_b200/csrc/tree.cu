@@ -461,7 +461,7 @@ __device__ __forceinline__ void finish(const TreeArgs& A, Counters& c, const uin
 #endif
   FOR_TREES(k, A) {
     if (owner) *A.T[k].epoch_ptr = epoch[k] + rounds_total + 2;   // every thread read the base before a barrier
-    flush_counters(A.G, A.T[k], c, k, owner, relax_rounds, prop_rounds);
+    flush_counters<STAT_SLOTS>(A.G, A.T[k], c, k, owner, relax_rounds, prop_rounds);
     clear_next_ctrl(A.clear_ctrl[k]);
   }
   timeline(A.T[0].ctrl);
@@ -836,6 +836,7 @@ cudaError_t launch_tree(meerkat_graph* g, meerkat_tree* const* trees, uint32_t n
   if (g->latency_bps > 0 && mode != MODE_STATIC && !(mode == MODE_DECREMENTAL && !g->reverse))
     bps = std::min(bps, g->latency_bps);
   dim3 grid((unsigned)(bps * g->sm_count)), block(TREE_BLOCK);
+  for (uint32_t i = 0; i < ntrees; i++) trees[i]->stat_blocks = STAT_SLOTS ? grid.x : 0;   // slots the finish writes
   void* args[] = {&A};
   const size_t smem = (mode == MODE_DECREMENTAL && !g->reverse) ? (size_t)FILTER_WORDS * 4 : 0;
   void* fn;

@@ -35,7 +35,11 @@ constexpr uint64_t TAIL_ITEMS = MEERKAT_TAIL_ITEMS;
 // 1: a relaxation that passed the node[x] probe issues its atomicMin, the stamp exchange and the
 // vmeta load together, and a propagation its CAS and vmeta load together: one dependent round trip
 // fewer per slab step (tree.cu expand, the batch prologues).  0: the result-gated sequence.
-constexpr bool SPEC_STAMP = MEERKAT_SPEC_STAMP != 0;   // frontiers this small run in block 0 alone (run_rounds)
+constexpr bool SPEC_STAMP = MEERKAT_SPEC_STAMP != 0;
+#ifndef MEERKAT_STAT_SLOTS
+#define MEERKAT_STAT_SLOTS 1
+#endif
+constexpr bool STAT_SLOTS = MEERKAT_STAT_SLOTS != 0;   // tree kernels' counters: per-block slots (1) or atomics   // frontiers this small run in block 0 alone (run_rounds)
 
 enum Visit { RELAX = 0, PROPAGATE = 1, PULL = 2 };
 constexpr int DIAG_PULL = 19;   // diagnostics round slot of the pull phase (MEERKAT_DIAG_ROUNDS builds)
@@ -246,7 +250,11 @@ __device__ __forceinline__ bool relax(const TreeDev& T, uint32_t x, uint64_t dis
 
 // Counter flush at kernel end: warp reduce -> shared-memory block reduce -> one global
 // atomic per counter per block (a warp-level flush put ~5K same-address atomics per
-// counter on the kernel's tail).  All threads of the block must call it.
+// counter on the kernel's tail).  SLOTS (the tree kernels): each block STORES its sums into its own
+// slot T.bstat[block][8] instead -- no same-line atomics on the kernel's tail (2 trees x 8 counters x
+// 296 blocks serialised at one L2 slice); meerkat_tree_stats_get adds the slots of the last call's
+// grid.  All threads of the block must call it.
+template <bool SLOTS = false>
 __device__ __forceinline__ void flush_counters(const GraphDev& G, const TreeDev& T, Counters& c, int k,
                                                bool rounds_owner, uint32_t relax_rounds, uint32_t prop_rounds) {
   constexpr int NV = 8;
@@ -265,7 +273,10 @@ __device__ __forceinline__ void flush_counters(const GraphDev& G, const TreeDev&
     if (err) atomicOr(reinterpret_cast<unsigned int*>(&acc[NV]), err);
   }
   __syncthreads();
-  if (threadIdx.x <= NV && acc[threadIdx.x]) {
+  if (SLOTS && threadIdx.x < NV) {
+    T.bstat[(uint64_t)blockIdx.x * NV + threadIdx.x] = acc[threadIdx.x];
+    if (threadIdx.x == 0 && acc[NV]) atomicOr(&G.ctrl->err, (unsigned int)acc[NV]);
+  } else if (!SLOTS && threadIdx.x <= NV && acc[threadIdx.x]) {
     unsigned long long* dst[NV] = {&tc->items, &tc->slabs_read, &tc->visited, &tc->improved, &tc->scan_slabs,
                                    &tc->scan_hits, &tc->batch_edges, &tc->direct_n};
     if (threadIdx.x < NV) atomicAdd(dst[threadIdx.x], acc[threadIdx.x]);
