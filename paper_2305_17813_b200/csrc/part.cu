@@ -50,7 +50,9 @@ namespace mk {
 
 enum MsgKind : uint32_t { MSG_RELAX = 0, MSG_PROP = 1, MSG_PULLREQ = 2, MSG_MARK = 3 };
 enum PartMode : uint32_t {
-  PM_DONE = 0, PM_SEED_STATIC = 1, PM_SEED_INC = 2, PM_SEED_DEC = 3, PM_RELAX = 4, PM_PROP = 5, PM_MARKS = 6
+  PM_DONE = 0, PM_SEED_STATIC = 1, PM_SEED_INC = 2, PM_SEED_DEC = 3, PM_RELAX = 4, PM_PROP = 5, PM_MARKS = 6,
+  PM_CHECK = 7,     // ordering contract: fingerprint the batch this rank was given (no tree is touched)
+  PM_VERDICT = 8    // every rank's verdict (exchanged in the headers): all good -> seed, else done
 };
 constexpr uint64_t HDR = 4;           // header messages (64 B) at the start of every exchange block
 constexpr uint32_t FLAG_RING = 64;    // per-unit mode words in mapped host memory
@@ -68,6 +70,7 @@ struct PartCtrl {
   unsigned long long tail[MEERKAT_MAX_RANKS];
   unsigned long long pull_n[MAX_TREES];
   unsigned long long local_rounds, prop_rounds;     // of the current call
+  unsigned long long fp[2];                         // fingerprint of the batch given to the call (PM_CHECK)
 };
 
 struct PArgs {
@@ -86,6 +89,14 @@ struct PArgs {
   const uint32_t* bd;
   const uint32_t* bw;
   uint64_t bn;
+  const uint32_t* fs;            // the batch the caller passed to the tree call (ordering contract)
+  const uint32_t* fd;
+  const uint32_t* fw;
+  uint64_t fn;
+  unsigned long long fp_expect[2];   // fingerprint of the last mutation's batch on this rank
+  uint32_t fp_w;                 // compare the weighted half too
+  uint32_t fn_bad;               // the batch size differs from the mutation's
+  uint32_t seed_mode;            // PM_SEED_INC / PM_SEED_DEC after a good verdict
 };
 
 // A message: x = target row at the destination, y = tag (kind << 1 | tree), z/w = payload lo/hi.
@@ -325,48 +336,78 @@ __device__ void p_expand(const PArgs& A, uint64_t r, uint64_t n0, uint64_t n1, c
       d = ld_slab_ro(slab_ptr(G, slab), l8);
       if (l8 == 0) c.slabs++;
     }
+    // phase-wise over the slab's keys (as tree.cu's expand): placement, then every load / atomic of
+    // a phase for all keys before any result is consumed, then one enqueue per tree and the messages
+    const TreeDev& T = A.T[k];
+    uint32_t xs[NK], rows[NK], peer[NK];
+    bool loc[NK], rem[NK], has[NK];
+    uint64_t pay[NK];
+    uint2 mv[NK];
 #pragma unroll
     for (int kk = 0; kk < NK; kk++) {
-      const uint32_t x = F::key(d, kk);
-      const bool live = active && F::valid_cell(l8, kk) && x < G.Vg;
-      bool enq = false, inv = false, emit = false;
-      uint32_t row = 0, peer = 0;
-      uint64_t pay = 0;
-      if (live) {
-        c.visited++;
-        const TreeDev& T = A.T[k];
-        peer = g_place(G, x, row);
-        if (VISIT == RELAX) {
-          const uint64_t dist = (uint64_t)du + (T.unit ? 1u : F::weight(d, kk));
-          if (peer == G.rank) enq = relax(T, row, dist, vg, epoch, c);
-          else if (dist >= INF_DIST) c.err |= ERR_OVERFLOW;
-          else { emit = true; pay = (dist << 32) | vg; }
-        } else {                // children of the invalid vertex v
-          if (peer == G.rank) {
-            const uint64_t cur = ld_cg_u64(T.node + row);
-            if (cur != UNREACHED && (uint32_t)cur == vg && x != T.source &&
-                atomicCAS(reinterpret_cast<unsigned long long*>(T.node + row), (unsigned long long)cur,
-                          (unsigned long long)UNREACHED) == cur)
-              inv = enq = true;
-          } else {
-            emit = true;
-            pay = vg;
-          }
-        }
+      xs[kk] = F::key(d, kk);
+      const bool live = active && F::valid_cell(l8, kk) && xs[kk] < G.Vg;
+      peer[kk] = 0; rows[kk] = 0; pay[kk] = 0; has[kk] = false;
+      mv[kk] = make_uint2(INVALID_SLAB, 0);
+      if (live) { c.visited++; peer[kk] = g_place(G, xs[kk], rows[kk]); }
+      loc[kk] = live && peer[kk] == G.rank;
+      rem[kk] = live && peer[kk] != G.rank;
+      if (VISIT == RELAX && live) {
+        const uint64_t dist = (uint64_t)du + (T.unit ? 1u : F::weight(d, kk));
+        if (dist >= INF_DIST) { c.err |= ERR_OVERFLOW; loc[kk] = rem[kk] = false; }
+        pay[kk] = (dist << 32) | vg;
+      } else if (VISIT == PROPAGATE) {
+        pay[kk] = vg;
+      }
+    }
+    uint64_t cur[NK];
+#pragma unroll
+    for (int kk = 0; kk < NK; kk++) cur[kk] = loc[kk] ? ld_cg_u64(T.node + rows[kk]) : UNREACHED;
+    if (VISIT == RELAX) {
+      // probe passed -> atomicMin, stamp exchange and vmeta together (enqueue iff the stamp was won;
+      // tree.cu's expand explains why that enqueues an improved x exactly once)
+      unsigned long long old[NK];
+      uint32_t st[NK];
+      bool go[NK];
+#pragma unroll
+      for (int kk = 0; kk < NK; kk++) {
+        go[kk] = loc[kk] && pay[kk] < cur[kk];
+        old[kk] = go[kk] ? atomicMin(reinterpret_cast<unsigned long long*>(T.node + rows[kk]),
+                                     (unsigned long long)pay[kk]) : 0ull;
+        st[kk] = go[kk] ? atomicExch(T.stamp + rows[kk], epoch) : epoch;
+        if (go[kk]) mv[kk] = __ldcg(G.vmeta + rows[kk]);
       }
 #pragma unroll
-      for (int k2 = 0; k2 < MAX_TREES; k2++) {
-        if (k2 >= (int)A.ntrees) break;
-        const bool mine = k == (uint32_t)k2;
-        if (VISIT == PROPAGATE) {
-          const bool h1[1] = {inv && mine};
-          const uint32_t x1[1] = {x};
-          warp_mark_invalid<1>(A.T[k2], h1, x1);
-        }
-        warp_enqueue(G, A.T[k2], FR_OF(A, k2, fn), SZ_OF(A, k2, fn), enq && mine, row, c);
+      for (int kk = 0; kk < NK; kk++) {
+        if (go[kk] && pay[kk] < old[kk]) c.improved++;
+        has[kk] = st[kk] != epoch;
       }
-      warp_emit(A, s_head, emit, peer, row, ((VISIT == RELAX ? MSG_RELAX : MSG_PROP) << 1) | k, pay, c);
+    } else {   // children of the invalid vertex v
+      unsigned long long oc[NK];
+      bool child[NK];
+#pragma unroll
+      for (int kk = 0; kk < NK; kk++) {
+        child[kk] = loc[kk] && cur[kk] != UNREACHED && (uint32_t)cur[kk] == vg && xs[kk] != T.source;
+        oc[kk] = child[kk] ? atomicCAS(reinterpret_cast<unsigned long long*>(T.node + rows[kk]),
+                                       (unsigned long long)cur[kk], (unsigned long long)UNREACHED) : 0ull;
+        if (child[kk]) mv[kk] = __ldcg(G.vmeta + rows[kk]);
+      }
+#pragma unroll
+      for (int kk = 0; kk < NK; kk++) has[kk] = child[kk] && oc[kk] == cur[kk];
     }
+#pragma unroll
+    for (int k2 = 0; k2 < MAX_TREES; k2++) {
+      if (k2 >= (int)A.ntrees) break;
+      const bool mine = k == (uint32_t)k2;
+      bool h2[NK];
+#pragma unroll
+      for (int kk = 0; kk < NK; kk++) h2[kk] = has[kk] && mine;
+      if (VISIT == PROPAGATE) warp_mark_invalid<NK>(A.T[k2], h2, xs);
+      warp_enqueue_multi<NK>(A.T[k2], FR_OF(A, k2, fn), SZ_OF(A, k2, fn), h2, rows, mv, c);
+    }
+#pragma unroll
+    for (int kk = 0; kk < NK; kk++)
+      warp_emit(A, s_head, rem[kk], peer[kk], rows[kk], ((VISIT == RELAX ? MSG_RELAX : MSG_PROP) << 1) | k, pay[kk], c);
     const uint32_t nxt = __shfl_sync(FULL, d.w, (lane & 24) + GROUP - 1);
     if (active) {
       if (nxt != INVALID_SLAB) slab = nxt;
@@ -393,7 +434,8 @@ __device__ void pull_enqueue(const PArgs& A, Counters& c) {
   }
 }
 
-// In-edges (u -> x) of the invalid x: u held here -> relax now; else a pull request to owner(u).
+// In-edges (u -> x) of the invalid x: u held here -> relax now (the group's candidates min-reduced,
+// one atomicMin per slab, as tree.cu's PULL); else a pull request to owner(u).
 template <bool MAP>
 __device__ void pull_walk(const PArgs& A, uint64_t f, const unsigned long long* s_head, Counters& c) {
   using F = Frag<MAP>;
@@ -421,42 +463,61 @@ __device__ void pull_walk(const PArgs& A, uint64_t f, const unsigned long long* 
   bool active = fetch();
   while (__any_sync(FULL, active)) {
     uint4 d = make_uint4(EMPTY_KEY, EMPTY_KEY, EMPTY_KEY, INVALID_SLAB);
+    const TreeDev& T = A.T[k];
+    uint64_t nx = 0;
+    uint32_t sx = 0;
     if (active) {
       d = ld_slab_ro(slab_ptr(A.R, slab), l8);
-      if (l8 == 0) c.slabs++;
+      if (l8 == 0) { c.slabs++; nx = ld_cg_u64(T.node + x); sx = __ldcg(T.stamp + x); }
     }
+    uint32_t us[NK], urow[NK], peer[NK], w[NK], bw[NK];
+    bool loc[NK], rem[NK];
+    uint64_t nu[NK];
 #pragma unroll
     for (int kk = 0; kk < NK; kk++) {
-      const uint32_t u = F::key(d, kk);
-      const bool live = active && F::valid_cell(l8, kk) && u < G.Vg;
-      bool enq = false, emit = false;
-      uint32_t urow = 0, peer = 0;
-      uint64_t pay = 0;
-      if (live) {
-        c.visited++;
-        const TreeDev& T = A.T[k];
-        const uint32_t w = T.unit ? 1u : (MAP ? F::weight(d, kk) : 1u);
-        peer = g_place(G, u, urow);
-        if (peer == G.rank) {
-          if (!bit_test(T.inval_bits, u)) {
-            const uint64_t nu = ld_cg_u64(T.node + urow);
-            if (nu != UNREACHED) {
-              count_hit(c, k);
-              enq = relax(T, x, (nu >> 32) + w, u, epoch, c);
-            }
-          }
-        } else {
-          emit = true;
-          pay = ((uint64_t)w << 32) | xg;
-        }
-      }
-#pragma unroll
-      for (int k2 = 0; k2 < MAX_TREES; k2++) {
-        if (k2 >= (int)A.ntrees) break;
-        warp_enqueue(G, A.T[k2], FR_OF(A, k2, f), SZ_OF(A, k2, f), enq && k == (uint32_t)k2, x, c);
-      }
-      warp_emit(A, s_head, emit, peer, urow, (MSG_PULLREQ << 1) | k, pay, c);
+      us[kk] = F::key(d, kk);
+      const bool live = active && F::valid_cell(l8, kk) && us[kk] < G.Vg;
+      w[kk] = T.unit ? 1u : (MAP ? F::weight(d, kk) : 1u);
+      peer[kk] = 0; urow[kk] = 0;
+      if (live) { c.visited++; peer[kk] = g_place(G, us[kk], urow[kk]); }
+      loc[kk] = live && peer[kk] == G.rank;
+      rem[kk] = live && peer[kk] != G.rank;
+      bw[kk] = loc[kk] ? __ldcg(T.inval_bits + (us[kk] >> 5)) : 0u;
+      nu[kk] = loc[kk] ? ld_cg_u64(T.node + urow[kk]) : UNREACHED;
     }
+    uint64_t best = UNREACHED;
+#pragma unroll
+    for (int kk = 0; kk < NK; kk++) {
+      if (loc[kk] && !((bw[kk] >> (us[kk] & 31)) & 1u) && nu[kk] != UNREACHED) {   // valid and reached (C15)
+        count_hit(c, k);
+        const uint64_t dist = (nu[kk] >> 32) + w[kk];
+        if (dist >= INF_DIST) c.err |= ERR_OVERFLOW;
+        else best = min(best, (dist << 32) | us[kk]);
+      }
+    }
+    best = min(best, (uint64_t)__shfl_xor_sync(FULL, (unsigned long long)best, 1));
+    best = min(best, (uint64_t)__shfl_xor_sync(FULL, (unsigned long long)best, 2));
+    best = min(best, (uint64_t)__shfl_xor_sync(FULL, (unsigned long long)best, 4));
+    bool hv[1] = {false};
+    uint32_t xv[1] = {x};
+    uint2 m1[1] = {make_uint2(INVALID_SLAB, 0)};
+    if (l8 == 0 && best != UNREACHED && best < nx) {   // atomicMin, stamp and vmeta together
+      const unsigned long long o = atomicMin(reinterpret_cast<unsigned long long*>(T.node + x),
+                                             (unsigned long long)best);
+      const uint32_t st = sx != epoch ? atomicExch(T.stamp + x, epoch) : epoch;
+      if (sx != epoch) m1[0] = __ldcg(G.vmeta + x);
+      if (best < o) c.improved++;
+      hv[0] = st != epoch;
+    }
+#pragma unroll
+    for (int k2 = 0; k2 < MAX_TREES; k2++) {
+      if (k2 >= (int)A.ntrees) break;
+      const bool h2[1] = {hv[0] && k == (uint32_t)k2};
+      warp_enqueue_multi<1>(A.T[k2], FR_OF(A, k2, f), SZ_OF(A, k2, f), h2, xv, m1, c);
+    }
+#pragma unroll
+    for (int kk = 0; kk < NK; kk++)
+      warp_emit(A, s_head, rem[kk], peer[kk], urow[kk], (MSG_PULLREQ << 1) | k, ((uint64_t)w[kk] << 32) | xg, c);
     const uint32_t nxt = __shfl_sync(FULL, d.w, (lane & 24) + GROUP - 1);
     if (active) {
       if (nxt != INVALID_SLAB) slab = nxt;
@@ -577,9 +638,36 @@ __global__ void __launch_bounds__(TREE_BLOCK, TREE_MINB) k_part_unit(const __gri
   unsigned long long r = __ldcg(&pc->fill);
   bool have_recv = A.start_mode == 0, synced = false;
   uint32_t lrounds = 0, prounds = 0;
+  uint32_t verdict = 0;   // this rank's ordering-contract verdict (ERR_STATE: a different batch)
   while (mode != PM_DONE) {
     const uint64_t f = r + 1;   // the slot this fill writes (zero by the round protocol)
     const uint32_t epoch = (uint32_t)f;
+    if (mode == PM_CHECK) {   // the batch must be the one this rank's last mutation applied
+      const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
+      uint64_t fa = 0, fb = 0;
+      for (uint64_t i = tid; i < A.fn; i += nt) fp_edge(A.fs[i], A.fd[i], A.fw ? A.fw[i] : 0u, fa, fb);
+      block_add2_u64(&pc->fp[0], fa, fb);
+      grid.sync();
+      synced = true;
+      const bool bad = A.fn_bad || __ldcg(&pc->fp[0]) != A.fp_expect[0] ||
+                       (A.fp_w && __ldcg(&pc->fp[1]) != A.fp_expect[1]);
+      verdict = bad ? (uint32_t)ERR_STATE : 0u;
+      mode = PM_VERDICT;
+      if (ws > 1) break;   // the verdicts travel in the headers
+      continue;
+    }
+    if (mode == PM_VERDICT) {
+      uint32_t any = verdict;
+      if (have_recv)
+        for (uint32_t p = 0; p < ws; p++) any |= (uint32_t)hdr_word(A.recv + (uint64_t)p * A.blk, 4);
+      have_recv = false;
+      if (any) {   // some rank was given another batch: no tree is touched anywhere
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&G.ctrl->err, (unsigned)ERR_STATE);
+        mode = PM_DONE;
+        break;
+      }
+      mode = A.seed_mode;
+    }
     if (mode == PM_SEED_STATIC || mode == PM_SEED_INC || mode == PM_SEED_DEC) {
       if (blockIdx.x == 0 && threadIdx.x < MAX_TREES) pc->pull_n[threadIdx.x] = 0;
       if (mode == PM_SEED_STATIC) seed_static(A, f, epoch, c);
@@ -659,7 +747,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, TREE_MINB) k_part_unit(const __gri
       const unsigned long long t = __ldcg(&pc->tail[p]), h = s_head[p];
       const unsigned long long m = min((unsigned long long)A.cap, t - h);
       unsigned long long* hd = reinterpret_cast<unsigned long long*>((p == G.rank ? A.recv : A.send) + (uint64_t)p * A.blk);
-      hd[0] = m; hd[1] = sent; hd[2] = pend; hd[3] = mode;
+      hd[0] = m; hd[1] = sent; hd[2] = pend; hd[3] = mode; hd[4] = verdict;
       pc->head[hpar ^ 1][p] = h + m;
     }
     pc->mode = mode;
@@ -1328,7 +1416,7 @@ meerkat_status part_tree_init(meerkat_graph* g, meerkat_tree* t) {
   if (e != cudaSuccess) return MEERKAT_E_CUDA;
   t->bytes += t->dev.fr_cap * 8;
   meerkat_tree* one[1] = {t};
-  return part_trees(g, one, 1, 0, nullptr, nullptr, nullptr, 0);
+  return part_trees(g, one, 1, 0, nullptr, nullptr, nullptr, 0);   // collective static tree
 }
 
 void part_tree_free(meerkat_tree* t) { cudaFree(t->pull_items); }
@@ -1367,7 +1455,15 @@ static cudaError_t launch_unit(meerkat_graph* g, PArgs& A) {
 
 // Units until the call is done on every rank.  Every rank launches the same number of units: the
 // stop decision reads the mode of unit (launched - PIPE), which every rank computed identically.
-static meerkat_status run_units(meerkat_graph* g, PArgs A) {
+// Copies of the graph's and the trees' control blocks, enqueued before a unit loop's final synchronisation.
+static cudaError_t enqueue_readback(meerkat_graph* g, meerkat_tree* const* trees, uint32_t k) {
+  cudaError_t e = cudaMemcpyAsync(g->out.hctrl, g->out.dev.ctrl, sizeof(GraphCtrl), cudaMemcpyDeviceToHost, g->stream);
+  for (uint32_t i = 0; i < k && e == cudaSuccess; i++)
+    e = cudaMemcpyAsync(trees[i]->hctrl, trees[i]->dev.ctrl, sizeof(TreeCtrl), cudaMemcpyDeviceToHost, g->stream);
+  return e;
+}
+
+static meerkat_status run_units(meerkat_graph* g, PArgs A, meerkat_tree* const* trees, uint32_t k) {
   PartState* ps = g->part;
   const uint32_t ws = g->ws;
   uint64_t sb[MEERKAT_MAX_RANKS], so[MEERKAT_MAX_RANKS];
@@ -1382,7 +1478,8 @@ static meerkat_status run_units(meerkat_graph* g, PArgs A) {
     A.start_mode = 0;
     const uint64_t u = launched++;
     ps->units++;
-    if (ws == 1) {
+    if (ws == 1) {   // one launch chains every phase
+      if (enqueue_readback(g, trees, k) != cudaSuccess) return MEERKAT_E_CUDA;
       if (cudaStreamSynchronize(g->stream) != cudaSuccess) return MEERKAT_E_CUDA;
       return ps->hflags[(base + u) % FLAG_RING] == PM_DONE ? MEERKAT_OK : MEERKAT_E_STATE;
     }
@@ -1390,7 +1487,11 @@ static meerkat_status run_units(meerkat_graph* g, PArgs A) {
       if (cudaStreamSynchronize(g->stream) != cudaSuccess) return MEERKAT_E_CUDA;
       if (trace_on()) fprintf(stderr, "[part r%u] unit %llu mode %u\n", g->rank, (unsigned long long)(base + u),
                               ps->hflags[(base + u) % FLAG_RING]);
-      if (ps->hflags[(base + u) % FLAG_RING] == PM_DONE) break;
+      if (ps->hflags[(base + u) % FLAG_RING] == PM_DONE) {
+        if (enqueue_readback(g, trees, k) != cudaSuccess) return MEERKAT_E_CUDA;
+        if (cudaStreamSynchronize(g->stream) != cudaSuccess) return MEERKAT_E_CUDA;
+        return MEERKAT_OK;
+      }
       uint64_t hs[MEERKAT_MAX_RANKS * 4];
       cudaError_t e = cudaSuccess;
       for (uint32_t p = 0; p < ws && e == cudaSuccess; p++)
@@ -1426,6 +1527,7 @@ static meerkat_status run_units(meerkat_graph* g, PArgs A) {
     }
     if (ps->hflags[(base + v) % FLAG_RING] == PM_DONE) break;
   }
+  if (enqueue_readback(g, trees, k) != cudaSuccess) return MEERKAT_E_CUDA;
   if (cudaStreamSynchronize(g->stream) != cudaSuccess) return MEERKAT_E_CUDA;
   return nccl_check(g);
 }
@@ -1434,38 +1536,32 @@ meerkat_status part_trees(meerkat_graph* g, meerkat_tree* const* trees, uint32_t
                           const uint32_t* d, const uint32_t* w, uint64_t n) {
   PartState* ps = g->part;
   if (k == 0 || k > (uint32_t)MAX_TREES) return MEERKAT_E_INVALID_ARG;
+  bool weights = false;
   for (uint32_t i = 0; i < k; i++) {
     if (!trees[i] || trees[i]->g != g || !trees[i]->part) return MEERKAT_E_INVALID_ARG;
-    if (kind && trees[i]->version + 1 != g->version) return MEERKAT_E_STATE;
     for (uint32_t j = 0; j < i; j++) if (trees[j] == trees[i]) return MEERKAT_E_INVALID_ARG;
+    weights = weights || !trees[i]->unit;
   }
-  bool weights = false;
-  for (uint32_t i = 0; i < k; i++) weights = weights || !trees[i]->unit;
-  // ordering contract: the batch this rank passed to the last mutation, of that kind
-  if (kind && (g->last_kind != kind || n != ps->n_last)) return MEERKAT_E_STATE;
+  // ordering contract, the parts every rank sees alike (the same collective sequence): the
+  // call follows a mutation of its kind and each tree is one mutation behind.  The batch itself (size
+  // and fingerprint per rank) is judged on the device by the first unit, and the verdicts are
+  // exchanged before any tree is touched (PM_CHECK / PM_VERDICT).
+  if (kind) {
+    if (g->last_kind != kind) return MEERKAT_E_STATE;
+    for (uint32_t i = 0; i < k; i++)
+      if (trees[i]->version + 1 != g->version) return MEERKAT_E_STATE;
+  }
+  const bool with_w = kind == 1 && g->weighted && w != nullptr;
+  if (kind == 1 && g->weighted && !w && weights && n) return MEERKAT_E_INVALID_ARG;
   cudaError_t e = cudaSuccess;
+  const void *ds = nullptr, *dd = nullptr, *dw = nullptr;
   if (kind && n) {
-    const void *ds, *dd, *dw = nullptr;
     e = stage_in(g, 0, s, n * 4, &ds);
     if (e == cudaSuccess) e = stage_in(g, 1, d, n * 4, &dd);
-    if (e == cudaSuccess && kind == 1 && w) e = stage_in(g, 2, w, n * 4, &dw);
-    if (e == cudaSuccess) e = cudaMemsetAsync(ps->dscr + SCR_FP, 0, 16, g->stream);
-    if (e == cudaSuccess) {
-      k_fingerprint<<<grid_of(g, n), 256, 0, g->stream>>>((const uint32_t*)ds, (const uint32_t*)dd,
-                                                         (const uint32_t*)dw, n, ps->dscr + SCR_FP);
-      g->launches++;
-      e = cudaGetLastError();
-    }
-    if (e == cudaSuccess) e = cudaMemcpyAsync(ps->hscr + SCR_FP, ps->dscr + SCR_FP, 16, cudaMemcpyDeviceToHost, g->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
-    if (e != cudaSuccess) return MEERKAT_E_CUDA;
-    // the mutation's fingerprint includes the weights only for a weighted insert
-    const bool with_w = kind == 1 && g->weighted;
-    if (ps->hscr[SCR_FP] != ps->fp_last[0] || (with_w && w && ps->hscr[SCR_FP + 1] != ps->fp_last[1]))
-      return MEERKAT_E_STATE;
-    if (with_w && !w && weights) return MEERKAT_E_INVALID_ARG;
+    if (e == cudaSuccess && with_w) e = stage_in(g, 2, w, n * 4, &dw);
   }
-  if (!kind) {   // live-edge count for the rings
+  if (e == cudaSuccess) e = cudaMemsetAsync(ps->pc->fp, 0, sizeof(ps->pc->fp), g->stream);
+  if (e == cudaSuccess && !kind) {   // live-edge count for the rings
     e = cudaMemcpyAsync(g->out.hctrl, g->out.dev.ctrl, sizeof(GraphCtrl), cudaMemcpyDeviceToHost, g->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
   }
@@ -1484,7 +1580,8 @@ meerkat_status part_trees(meerkat_graph* g, meerkat_tree* const* trees, uint32_t
   for (uint32_t i = 0; i < k; i++) { A.T[i] = trees[i]->dev; A.pull[i] = trees[i]->pull_items; }
   for (uint32_t i = k; i < (uint32_t)MAX_TREES; i++) { A.T[i] = trees[0]->dev; A.pull[i] = trees[0]->pull_items; }
   A.ntrees = k;
-  A.start_mode = kind == 0 ? PM_SEED_STATIC : kind == 1 ? PM_SEED_INC : PM_SEED_DEC;
+  A.start_mode = kind == 0 ? PM_SEED_STATIC : PM_CHECK;
+  A.seed_mode = kind == 1 ? PM_SEED_INC : PM_SEED_DEC;
   A.scan = g->reverse ? 0u : 1u;
   A.pc = ps->pc;
   A.flags = ps->dflags;
@@ -1497,16 +1594,16 @@ meerkat_status part_trees(meerkat_graph* g, meerkat_tree* const* trees, uint32_t
   const uint64_t c = ps->rows_cap;
   if (kind == 1) { A.bs = ps->rows; A.bd = ps->rows + c; A.bw = g->weighted ? ps->rows + 2 * c : nullptr; A.bn = ps->n_out; }
   if (kind == 2) { A.bs = ps->rows + 3 * c; A.bd = ps->rows + 4 * c; A.bn = ps->n_in; }
+  A.fs = (const uint32_t*)ds; A.fd = (const uint32_t*)dd; A.fw = (const uint32_t*)dw; A.fn = kind ? n : 0;
+  A.fp_expect[0] = ps->fp_last[0];
+  A.fp_expect[1] = ps->fp_last[1];
+  A.fp_w = with_w ? 1u : 0u;
+  A.fn_bad = kind && n != ps->n_last ? 1u : 0u;
   const uint64_t units0 = ps->units;
-  meerkat_status st = run_units(g, A);
+  meerkat_status st = run_units(g, A, trees, k);
   ps->dirty = st != MEERKAT_OK;
-  // every rank's status: errors anywhere fail the call everywhere
-  e = cudaMemcpyAsync(g->out.hctrl, g->out.dev.ctrl, sizeof(GraphCtrl), cudaMemcpyDeviceToHost, g->stream);
-  for (uint32_t i = 0; i < k && e == cudaSuccess; i++)
-    e = cudaMemcpyAsync(trees[i]->hctrl, trees[i]->dev.ctrl, sizeof(TreeCtrl), cudaMemcpyDeviceToHost, g->stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
-  if (e != cudaSuccess) return MEERKAT_E_CUDA;
   if (st == MEERKAT_E_NCCL || st == MEERKAT_E_CUDA) return st;
+  // every rank's status: errors anywhere (capacity, overflow, a refused batch) fail the call everywhere
   uint64_t err[1] = {(uint64_t)g->out.hctrl->err | (st != MEERKAT_OK ? (uint64_t)ERR_STATE : 0)};
   if (g->ws > 1) {
     const meerkat_status s2 = allgather_small(g, err, 1);
@@ -1514,6 +1611,7 @@ meerkat_status part_trees(meerkat_graph* g, meerkat_tree* const* trees, uint32_t
     for (uint32_t q = 0; q < g->ws; q++) err[0] |= ps->hcoll[q];
   }
   if (g->out.hctrl->err) cudaMemsetAsync(&g->out.dev.ctrl->err, 0, 4, g->stream);
+  if (err[0] & ERR_STATE) return MEERKAT_E_STATE;   // refused: the trees stay one mutation behind
   for (uint32_t i = 0; i < k; i++) {
     trees[i]->version = g->version;
     trees[i]->last_units = g->ws > 1 ? ps->units - units0 : 0;

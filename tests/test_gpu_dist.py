@@ -95,15 +95,24 @@ def _worker(rank, ws, port, backend, scale, reverse, pairs, q):
         after = t.nodes()   # collective: every rank calls it
         if rank == 0 and not np.array_equal(before, after):
             errs.append("recompute")
-        # ordering contract: a different batch than the last mutation's is refused on every rank
-        s, d, w = W.inserts[0]
-        g.insert(sl(s[:50]), sl(d[:50]), sl(w[:50]))
+        # ordering contract: a different batch than the last mutation's -- on one rank only -- is refused
+        # on every rank before any tree is touched; the right batch is then accepted
         from paper_2305_17813_b200._lib import MeerkatError
+        s, d, w = W.inserts[0]
+        s, d, w = s[:60] ^ 1, d[:60], w[:60]   # edges not in the graph (ids flipped in the low bit)
+        g.insert(sl(s), sl(d), sl(w))
+        o.insert(s, d, w)
+        wrong = (sl(s[::-1]), sl(d), sl(w)) if rank == 0 else (sl(s), sl(d), sl(w))
         try:
-            t.incremental(sl(s[50:100]), sl(d[50:100]), sl(w[50:100]))
+            t.incremental(*wrong)
             errs.append("wrong batch accepted")
-        except MeerkatError:
-            pass
+        except MeerkatError as e:
+            if "STATE" not in str(e):
+                errs.append(f"wrong batch: {e}")
+        t.incremental(sl(s), sl(d), sl(w))
+        gs = t.nodes()
+        if rank == 0 and not np.array_equal(gs, o.sssp(src)[1]):
+            errs.append("after a refused batch")
         q.put((rank, errs))
     except Exception:  # pragma: no cover
         import traceback
