@@ -148,7 +148,8 @@ typedef struct {
   uint64_t version;          /* graph version this tree reflects */
   uint32_t source;
   uint32_t unit_weights;     /* 1 for BFS trees */
-  uint64_t exchanges;        /* partitioned trees: exchange units of the last call (0 on one GPU) */
+  uint64_t exchanges;        /* partitioned trees: exchange units of the last call (0 when one rank chains
+                                every phase in one launch) */
 } meerkat_tree_stats;
 
 const char* meerkat_status_string(meerkat_status s);

@@ -97,6 +97,7 @@ struct PArgs {
   uint32_t fp_w;                 // compare the weighted half too
   uint32_t fn_bad;               // the batch size differs from the mutation's
   uint32_t seed_mode;            // PM_SEED_INC / PM_SEED_DEC after a good verdict
+  uint32_t chain;                // one rank: chain the phases in one launch (0: one unit per phase, as P > 1)
 };
 
 // A message: x = target row at the destination, y = tag (kind << 1 | tree), z/w = payload lo/hi.
@@ -653,7 +654,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, TREE_MINB) k_part_unit(const __gri
                        (A.fp_w && __ldcg(&pc->fp[1]) != A.fp_expect[1]);
       verdict = bad ? (uint32_t)ERR_STATE : 0u;
       mode = PM_VERDICT;
-      if (ws > 1) break;   // the verdicts travel in the headers
+      if (ws > 1 || !A.chain) break;   // the verdicts travel in the headers
       continue;
     }
     if (mode == PM_VERDICT) {
@@ -723,7 +724,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, TREE_MINB) k_part_unit(const __gri
       grid.sync();
       r++;
     }
-    if (ws > 1) break;   // an exchange must follow; one rank: nothing was sent, the phase is over
+    if (ws > 1 || !A.chain) break;   // an exchange must follow; one rank: nothing was sent, the phase is over
   }
   if (!synced) grid.sync();   // every block has read pc before block 0 rewrites it
   // (C) pack up to cap messages per peer
@@ -1478,7 +1479,7 @@ static meerkat_status run_units(meerkat_graph* g, PArgs A, meerkat_tree* const* 
     A.start_mode = 0;
     const uint64_t u = launched++;
     ps->units++;
-    if (ws == 1) {   // one launch chains every phase
+    if (A.chain) {   // one rank: one launch chains every phase
       if (enqueue_readback(g, trees, k) != cudaSuccess) return MEERKAT_E_CUDA;
       if (cudaStreamSynchronize(g->stream) != cudaSuccess) return MEERKAT_E_CUDA;
       return ps->hflags[(base + u) % FLAG_RING] == PM_DONE ? MEERKAT_OK : MEERKAT_E_STATE;
@@ -1599,6 +1600,10 @@ meerkat_status part_trees(meerkat_graph* g, meerkat_tree* const* trees, uint32_t
   A.fp_expect[1] = ps->fp_last[1];
   A.fp_w = with_w ? 1u : 0u;
   A.fn_bad = kind && n != ps->n_last ? 1u : 0u;
+  // one rank chains the phases in one launch; MEERKAT_PART_UNITS=1 keeps one unit per phase (the P > 1
+  // protocol, host pipeline included) so a one-GPU box exercises it
+  static const bool force_units = std::getenv("MEERKAT_PART_UNITS") != nullptr;
+  A.chain = g->ws == 1 && !force_units ? 1u : 0u;
   const uint64_t units0 = ps->units;
   meerkat_status st = run_units(g, A, trees, k);
   ps->dirty = st != MEERKAT_OK;
@@ -1614,7 +1619,7 @@ meerkat_status part_trees(meerkat_graph* g, meerkat_tree* const* trees, uint32_t
   if (err[0] & ERR_STATE) return MEERKAT_E_STATE;   // refused: the trees stay one mutation behind
   for (uint32_t i = 0; i < k; i++) {
     trees[i]->version = g->version;
-    trees[i]->last_units = g->ws > 1 ? ps->units - units0 : 0;
+    trees[i]->last_units = A.chain ? 0 : ps->units - units0;
   }
   if (err[0] & ERR_CAPACITY) return MEERKAT_E_CAPACITY;
   if (err[0] & ERR_OVERFLOW) return MEERKAT_E_OVERFLOW;

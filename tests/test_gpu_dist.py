@@ -24,8 +24,11 @@ def _port():
     return p
 
 
-def _worker(rank, ws, port, backend, scale, reverse, pairs, q):
+def _worker(rank, ws, port, backend, scale, reverse, pairs, q, units=False):
+    import os
     import torch.distributed as dist
+    if units:   # one exchange unit per phase at world size 1: the P > 1 protocol and host pipeline
+        os.environ["MEERKAT_PART_UNITS"] = "1"
     try:
         torch.cuda.set_device(0)
         kw = {"device_id": torch.device("cuda", 0)} if backend == "nccl" else {}
@@ -75,7 +78,7 @@ def _worker(rank, ws, port, backend, scale, reverse, pairs, q):
                 b.decremental(sl(s), sl(d))
             check(f"dec{i}")
             st = t.stats()
-            if ws > 1 and st["exchanges"] < 2:
+            if (ws > 1 or units) and st["exchanges"] < 2:
                 errs.append(f"dec{i}: {st['exchanges']} exchanges")
         # queries in the caller's order, across partitions
         es, ed, ew = o.edges()
@@ -129,12 +132,25 @@ def _worker(rank, ws, port, backend, scale, reverse, pairs, q):
     (3, "gloo", 13, True, 0), (4, "gloo", 12, False, 0), (4, "gloo", 12, True, 64), (8, "gloo", 12, True, 0),
     (8, "gloo", 12, False, 32)])
 def test_partitioned_dynamic_sssp_bfs(ws, backend, scale, reverse, pairs):
+    _run(ws, backend, scale, reverse, pairs)
+
+
+@pytest.mark.parametrize("reverse", [True, False])
+def test_partitioned_nccl_unit_pipeline(reverse):
+    """World size 1 through the library's NCCL communicator with one exchange unit per phase
+    (MEERKAT_PART_UNITS=1): the pipelined host loop (units launched PIPE ahead, mode words read from
+    mapped memory) and the device-side phase changes of P > 1, on one GPU."""
+    _run(1, "nccl", 12, reverse, 0, units=True)
+
+
+def _run(ws, backend, scale, reverse, pairs, units=False):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    ps = [ctx.Process(target=_worker, args=(r, ws, port, backend, scale, reverse, pairs, q)) for r in range(ws)]
+    ps = [ctx.Process(target=_worker, args=(r, ws, port, backend, scale, reverse, pairs, q, units))
+          for r in range(ws)]
     for p in ps:
         p.start()
     res = [q.get(timeout=900) for _ in ps]
