@@ -17,7 +17,7 @@ constexpr int TREE_MINB = MEERKAT_TREE_MINB;
 constexpr int FILTER_LOG2 = 14;
 constexpr int FILTER_WORDS = 1 << FILTER_LOG2;   // 64 KiB smem Bloom filter per block (decremental scan)
 #ifndef MEERKAT_SCAN_UNROLL
-#define MEERKAT_SCAN_UNROLL 2
+#define MEERKAT_SCAN_UNROLL 3
 #endif
 constexpr int SCAN_UNROLL = MEERKAT_SCAN_UNROLL;   // independent slabs in flight per group in the scan
 constexpr unsigned FULL = 0xFFFFFFFFu;
