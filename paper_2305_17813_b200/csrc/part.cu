@@ -403,8 +403,8 @@ __device__ void p_expand(const PArgs& A, uint64_t r, uint64_t n0, uint64_t n1, c
       bool h2[NK];
 #pragma unroll
       for (int kk = 0; kk < NK; kk++) h2[kk] = has[kk] && mine;
-      if (VISIT == PROPAGATE) warp_mark_invalid<NK>(A.T[k2], h2, xs);
-      warp_enqueue_multi<NK>(A.T[k2], FR_OF(A, k2, fn), SZ_OF(A, k2, fn), h2, rows, mv, c);
+      if (VISIT == PROPAGATE) warp_mark_enqueue_multi<NK>(A.T[k2], FR_OF(A, k2, fn), SZ_OF(A, k2, fn), h2, xs, rows, mv, c);
+      else warp_enqueue_multi<NK>(A.T[k2], FR_OF(A, k2, fn), SZ_OF(A, k2, fn), h2, rows, mv, c);
     }
 #pragma unroll
     for (int kk = 0; kk < NK; kk++)

@@ -261,8 +261,7 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const TreeDev& T, int 
         has[kk] = child[kk] && oc[kk] == cur[kk];
         if (!SPEC_STAMP && has[kk]) mv[kk] = __ldcg(G.vmeta + xs[kk]);
       }
-      warp_mark_invalid<NK>(T, has, xs);
-      warp_enqueue_multi<NK>(T, fnext, sznext, has, xs, mv, c);
+      warp_mark_enqueue_multi<NK>(T, fnext, sznext, has, xs, xs, mv, c);
     } else {
       // PULL: in-edges (x -> v) of invalid v; a valid->invalid frontier edge iff x is valid and
       // reached (C15).  The group's candidates for v are min-reduced first: one atomicMin

@@ -9,7 +9,10 @@ namespace cg = cooperative_groups;
 
 namespace mk {
 
-constexpr int TREE_BLOCK = 512;
+#ifndef MEERKAT_TREE_BLOCK
+#define MEERKAT_TREE_BLOCK 512
+#endif
+constexpr int TREE_BLOCK = MEERKAT_TREE_BLOCK;   // threads per block of the cooperative tree kernels (A/B)
 #ifndef MEERKAT_TREE_MINB
 #define MEERKAT_TREE_MINB 2   // resident blocks per SM the dynamic tree kernels are compiled for (A/B)
 #endif
@@ -227,6 +230,69 @@ __device__ __forceinline__ void warp_mark_invalid(const TreeDev& T, const bool (
     if (has[k]) T.inval_list[base++] = x[k];
 }
 
+// warp_mark_invalid + warp_enqueue_multi in one pass (invalidation): both prefix sums together and
+// the two warp atomics (list length, frontier size) issued back to back, so an invalidating slab step
+// waits for one L2 atomic round trip instead of two.  xm: ids for the bit set / list (global ids on a
+// partitioned graph), xi: rows for the frontier items.
+template <int NK>
+__device__ __forceinline__ void warp_mark_enqueue_multi(const TreeDev& T, uint64_t* fr, unsigned long long* sz,
+                                                        const bool (&has)[NK], const uint32_t (&xm)[NK],
+                                                        const uint32_t (&xi)[NK], const uint2 (&m)[NK],
+                                                        Counters& c) {
+  uint32_t cnt[NK], mine = 0, marks = 0;
+#pragma unroll
+  for (int k = 0; k < NK; k++) {
+    if (has[k]) { atomicOr(T.inval_bits + (xm[k] >> 5), 1u << (xm[k] & 31)); marks++; }
+    cnt[k] = (has[k] && m[k].x != INVALID_SLAB) ? m[k].y : 0u;
+    if (T.scheme1 && cnt[k]) cnt[k] = 1;
+    mine += cnt[k];
+  }
+  if (!__any_sync(FULL, marks != 0)) return;   // no mark, no item
+  const int lane = lane_id();
+  uint32_t incl = mine, incm = marks;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULL, incl, o);
+    const uint32_t z = __shfl_up_sync(FULL, incm, o);
+    if (lane >= o) { incl += y; incm += z; }
+  }
+  unsigned long long bi = 0, bm = 0;
+  if (lane == 31) {
+    bm = atomicAdd(&T.ctrl->inval_n, (unsigned long long)incm);
+    if (incl) bi = atomicAdd(sz, (unsigned long long)incl);
+  }
+  const uint32_t total = __shfl_sync(FULL, incl, 31);
+  bm = __shfl_sync(FULL, bm, 31) + incm - marks;
+  bi = __shfl_sync(FULL, bi, 31);
+#pragma unroll
+  for (int k = 0; k < NK; k++)
+    if (has[k]) T.inval_list[bm++] = xm[k];
+  if (!total) return;
+  if (bi + total > T.fr_cap) { c.err |= ERR_CAPACITY; return; }
+  uint64_t off[NK];
+  uint64_t o = bi + incl - mine;
+#pragma unroll
+  for (int k = 0; k < NK; k++) {
+    off[k] = o;
+    o += cnt[k];
+    if (cnt[k] <= 8)
+      for (uint32_t j = 0; j < cnt[k]; j++) fr[off[k] + j] = ((uint64_t)(m[k].x + j) << 32) | xi[k];
+  }
+#pragma unroll
+  for (int k = 0; k < NK; k++) {
+    uint32_t big = __ballot_sync(FULL, cnt[k] > 8);
+    while (big) {
+      const int l = __ffs(big) - 1;
+      big &= big - 1;
+      const uint32_t xb = __shfl_sync(FULL, xi[k], l);
+      const uint32_t hb = __shfl_sync(FULL, m[k].x, l);
+      const uint64_t ob = __shfl_sync(FULL, off[k], l);
+      const uint32_t cb = __shfl_sync(FULL, cnt[k], l);
+      for (uint32_t j = lane; j < cb; j += 32) fr[ob + j] = ((uint64_t)(hb + j) << 32) | xb;
+    }
+  }
+}
+
 __device__ __forceinline__ void mark_invalid(const TreeDev& T, uint32_t x) {
   atomicOr(T.inval_bits + (x >> 5), 1u << (x & 31));
   const unsigned long long i = atomicAdd(&T.ctrl->inval_n, 1ull);
@@ -411,8 +477,7 @@ __device__ __forceinline__ void tree_prologue_dec(const GraphDev& G, const TreeD
 #pragma unroll
     for (int k = 0; k < MAX_TREES; k++) {
       if (k >= (int)ntrees) break;
-      warp_mark_invalid<1>(T[k], has[k], xv);
-      warp_enqueue_multi<1>(T[k], T[k].fr[0], &T[k].ctrl->size[0], has[k], xv, m[k], c);
+      warp_mark_enqueue_multi<1>(T[k], T[k].fr[0], &T[k].ctrl->size[0], has[k], xv, xv, m[k], c);
     }
   }
 }
