@@ -138,6 +138,9 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const TreeDev& T, int 
       if (l8 == 0) c.slabs++;                                               // d(v) may change concurrently
     }
     if (VISIT == RELAX) nv = __shfl_sync(FULL, nv, lane & 24);
+    const uint32_t nxt = __shfl_sync(FULL, d.w, (lane & 24) + GROUP - 1);
+    if ((PREFETCH & 1) && active && nxt != INVALID_SLAB && nxt != LINKING)   // the chain's next slab
+      prefetch_l2(reinterpret_cast<const uint4*>(slab_ptr(S, nxt)) + l8);
     bool dead = false;
     if (VISIT == RELAX && active && fresh) {
       dead = V32 ? (nv >> 32) == INF_DIST : nv == UNREACHED;
@@ -209,7 +212,7 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const TreeDev& T, int 
           if (live[kk] && cand[kk] < old[kk]) c.improved++;
           has[kk] = st[kk] != epoch_next;
         }
-        warp_enqueue_multi<NK>(T, fnext, sznext, has, xs, mv, c);
+        warp_enqueue_multi<NK>(T, fnext, sznext, has, xs, mv, c, G.slabs);
       } else {
 #pragma unroll
       for (int kk = 0; kk < NK; kk++) {
@@ -232,7 +235,7 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const TreeDev& T, int 
       }
 #pragma unroll
       for (int kk = 0; kk < NK; kk++) has[kk] = st[kk] != epoch_next;
-      warp_enqueue_multi<NK>(T, fnext, sznext, has, xs, mv, c);
+      warp_enqueue_multi<NK>(T, fnext, sznext, has, xs, mv, c, G.slabs);
       }
     } else if (VISIT == PROPAGATE) {
       // PropagateInvalidation, top-down (C14): the children x (parent(x) = v) of invalid v
@@ -261,7 +264,7 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const TreeDev& T, int 
         has[kk] = child[kk] && oc[kk] == cur[kk];
         if (!SPEC_STAMP && has[kk]) mv[kk] = __ldcg(G.vmeta + xs[kk]);
       }
-      warp_mark_enqueue_multi<NK>(T, fnext, sznext, has, xs, xs, mv, c);
+      warp_mark_enqueue_multi<NK>(T, fnext, sznext, has, xs, xs, mv, c, G.slabs);
     } else {
       // PULL: in-edges (x -> v) of invalid v; a valid->invalid frontier edge iff x is valid and
       // reached (C15).  The group's candidates for v are min-reduced first: one atomicMin
@@ -315,9 +318,8 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const TreeDev& T, int 
         }
         }
       }
-      warp_enqueue_multi<1>(T, fnext, sznext, hv, xv, mv1, c);
+      warp_enqueue_multi<1>(T, fnext, sznext, hv, xv, mv1, c, G.slabs);
     }
-    const uint32_t nxt = __shfl_sync(FULL, d.w, (lane & 24) + GROUP - 1);
     if (active) {
       if (nxt != INVALID_SLAB && !dead) slab = nxt;
       else if (T.scheme1 && !dead && b + 1 < nb) { b++; slab = head0 + b; }

@@ -39,6 +39,16 @@ constexpr uint64_t TAIL_ITEMS = MEERKAT_TAIL_ITEMS;
 // vmeta load together, and a propagation its CAS and vmeta load together: one dependent round trip
 // fewer per slab step (tree.cu expand, the batch prologues).  0: the result-gated sequence.
 constexpr bool SPEC_STAMP = MEERKAT_SPEC_STAMP != 0;
+#ifndef MEERKAT_PREFETCH
+#define MEERKAT_PREFETCH 3
+#endif
+// L2 prefetch of slabs a group will read next (bit 0: the next slab of the chain being walked, as
+// soon as its link word arrives; bit 1: the head slabs of the items a round enqueues, read by the
+// next round) -- the first dependent load of the next step then hits L2.
+constexpr int PREFETCH = MEERKAT_PREFETCH;
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" :: "l"(p));
+}
 #ifndef MEERKAT_STAT_SLOTS
 #define MEERKAT_STAT_SLOTS 1
 #endif
@@ -161,7 +171,8 @@ __device__ __forceinline__ void warp_enqueue(const GraphDev& G, const TreeDev& T
 template <int NK>
 __device__ __forceinline__ void warp_enqueue_multi(const TreeDev& T, uint64_t* fr, unsigned long long* sz,
                                                    const bool (&has)[NK], const uint32_t (&x)[NK],
-                                                   const uint2 (&m)[NK], Counters& c) {
+                                                   const uint2 (&m)[NK], Counters& c,
+                                                   const uint32_t* pf_slabs = nullptr) {
   uint32_t cnt[NK], mine = 0;
 #pragma unroll
   for (int k = 0; k < NK; k++) {
@@ -189,7 +200,13 @@ __device__ __forceinline__ void warp_enqueue_multi(const TreeDev& T, uint64_t* f
     off[k] = o;
     o += cnt[k];
     if (cnt[k] <= 8)
-      for (uint32_t j = 0; j < cnt[k]; j++) fr[off[k] + j] = ((uint64_t)(m[k].x + j) << 32) | x[k];
+      for (uint32_t j = 0; j < cnt[k]; j++) {
+        fr[off[k] + j] = ((uint64_t)(m[k].x + j) << 32) | x[k];
+        if ((PREFETCH & 2) && pf_slabs && m[k].x != LINKING) {   // the next round reads this head slab
+          const uint32_t* sp = pf_slabs + (size_t)(m[k].x + j) * SLAB_WORDS;
+          prefetch_l2(sp); prefetch_l2(sp + 8); prefetch_l2(sp + 16); prefetch_l2(sp + 24);
+        }
+      }
   }
 #pragma unroll
   for (int k = 0; k < NK; k++) {
@@ -238,7 +255,7 @@ template <int NK>
 __device__ __forceinline__ void warp_mark_enqueue_multi(const TreeDev& T, uint64_t* fr, unsigned long long* sz,
                                                         const bool (&has)[NK], const uint32_t (&xm)[NK],
                                                         const uint32_t (&xi)[NK], const uint2 (&m)[NK],
-                                                        Counters& c) {
+                                                        Counters& c, const uint32_t* pf_slabs = nullptr) {
   uint32_t cnt[NK], mine = 0, marks = 0;
 #pragma unroll
   for (int k = 0; k < NK; k++) {
@@ -276,7 +293,13 @@ __device__ __forceinline__ void warp_mark_enqueue_multi(const TreeDev& T, uint64
     off[k] = o;
     o += cnt[k];
     if (cnt[k] <= 8)
-      for (uint32_t j = 0; j < cnt[k]; j++) fr[off[k] + j] = ((uint64_t)(m[k].x + j) << 32) | xi[k];
+      for (uint32_t j = 0; j < cnt[k]; j++) {
+        fr[off[k] + j] = ((uint64_t)(m[k].x + j) << 32) | xi[k];
+        if ((PREFETCH & 2) && pf_slabs && m[k].x != LINKING) {
+          const uint32_t* sp = pf_slabs + (size_t)(m[k].x + j) * SLAB_WORDS;
+          prefetch_l2(sp); prefetch_l2(sp + 8); prefetch_l2(sp + 16); prefetch_l2(sp + 24);
+        }
+      }
   }
 #pragma unroll
   for (int k = 0; k < NK; k++) {
@@ -436,7 +459,7 @@ __device__ __forceinline__ void tree_prologue_inc(const GraphDev& G, const TreeD
     const uint32_t xv[1] = {v};
 #pragma unroll
     for (int k = 0; k < MAX_TREES; k++)
-      if (k < (int)ntrees) warp_enqueue_multi<1>(T[k], T[k].fr[0], &T[k].ctrl->size[0], has[k], xv, m[k], c);
+      if (k < (int)ntrees) warp_enqueue_multi<1>(T[k], T[k].fr[0], &T[k].ctrl->size[0], has[k], xv, m[k], c, G.slabs);
   }
 }
 
@@ -477,7 +500,7 @@ __device__ __forceinline__ void tree_prologue_dec(const GraphDev& G, const TreeD
 #pragma unroll
     for (int k = 0; k < MAX_TREES; k++) {
       if (k >= (int)ntrees) break;
-      warp_mark_enqueue_multi<1>(T[k], T[k].fr[0], &T[k].ctrl->size[0], has[k], xv, xv, m[k], c);
+      warp_mark_enqueue_multi<1>(T[k], T[k].fr[0], &T[k].ctrl->size[0], has[k], xv, xv, m[k], c, G.slabs);
     }
   }
 }
