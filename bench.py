@@ -50,6 +50,8 @@ def parse():
     p.add_argument("--batch", type=int, default=100_000)
     p.add_argument("--lf", type=float, default=0.5,
                    help="load factor of the slab stores (SURVEY C22: a performance knob the paper leaves open; 0.5 measured best for the config-3 step, DESIGN.md §10)")
+    p.add_argument("--in-lf", type=float, default=0.0,
+                   help="load factor of the in-edge mirror (0 = --lf); the mirror is only walked (pull frontier)")
     p.add_argument("--no-hashing", action="store_true")
     p.add_argument("--seed", action=argparse.BooleanOptionalAction, default=True,
                    help="with --fused, the insert / delete kernels seed the tree calls (batch prologue "
@@ -240,7 +242,7 @@ def workload_config(args, V, n_base, source, ws=1):
     return {"workload": f"rmat-s{args.scale}-ef{args.ef} dynamic SSSP+BFS, {args.batch}-edge insert+delete "
                         f"batches (BASELINE config 3)",
             "vertices": V, "edges": n_base, "batch": args.batch, "source": source,
-            "hashing": not args.no_hashing, "load_factor": args.lf,
+            "hashing": not args.no_hashing, "load_factor": args.lf, "in_load_factor": args.in_lf or args.lf,
             "decremental_frontier": args.frontier,
             "tree_updates": ("fused SSSP+BFS (meerkat_trees_*)" if args.fused else "per tree")
                             + (", seeded by the insert / delete kernels" if args.fused and args.seed else ""),
@@ -338,7 +340,8 @@ def build(args, W, frontier, dev, local, stream, T):
     rev = frontier == "reverse"
     ihints = np.bincount(bd, minlength=V).astype(np.uint32) if rev else None
     g = Graph(V, weighted=True, hashing=not args.no_hashing, load_factor=args.lf, degree_hints=T(hints),
-              device=local, stream=stream, reverse=rev, in_degree_hints=T(ihints) if rev else None)
+              device=local, stream=stream, reverse=rev, in_degree_hints=T(ihints) if rev else None,
+              in_load_factor=args.in_lf)
     base_t = (T(bs), T(bd), T(bw))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)

@@ -117,6 +117,9 @@ typedef struct {
   void* exchange_ctx;
   uint32_t exchange_pairs;      /* messages per peer per exchange of a dynamic tree call (0 = 16384; static
                                    recomputes use 16 x this); more are carried over to the next exchange */
+  float in_load_factor;         /* lf of the in-edge mirror (reverse only), in (0,1]; 0 => load_factor.  The
+                                   mirror is only walked (the decremental pull frontier, PageRank), so
+                                   fuller slabs mean fewer work items there */
 } meerkat_config;
 
 typedef struct {

@@ -56,7 +56,7 @@ class Config(ctypes.Structure):
         ("reverse", ctypes.c_uint32), ("in_degree_hints", ctypes.c_void_p),
         ("world_size", ctypes.c_uint32), ("rank", ctypes.c_uint32), ("update_tracking", ctypes.c_uint32),
         ("nccl_id", ctypes.c_void_p), ("exchange", ctypes.c_void_p), ("exchange_ctx", ctypes.c_void_p),
-        ("exchange_pairs", ctypes.c_uint32),
+        ("exchange_pairs", ctypes.c_uint32), ("in_load_factor", ctypes.c_float),
     ]
 
 

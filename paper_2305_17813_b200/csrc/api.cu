@@ -163,7 +163,8 @@ meerkat_status meerkat_create(const meerkat_config* cfg, meerkat_graph** out) {
   if (!cfg || !out) return MEERKAT_E_INVALID_ARG;
   *out = nullptr;
   const float lf = cfg->load_factor == 0.0f ? 0.7f : cfg->load_factor;
-  if (cfg->vertex_n == 0 || cfg->vertex_n >= 0xFFFFFFFCu || !(lf > 0.0f && lf <= 1.0f))
+  if (cfg->vertex_n == 0 || cfg->vertex_n >= 0xFFFFFFFCu || !(lf > 0.0f && lf <= 1.0f) ||
+      !(cfg->in_load_factor >= 0.0f && cfg->in_load_factor <= 1.0f))
     return MEERKAT_E_INVALID_ARG;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || cfg->device < 0 || cfg->device >= ndev) {
@@ -187,6 +188,7 @@ meerkat_status meerkat_create(const meerkat_config* cfg, meerkat_graph** out) {
   g->weighted = cfg->weighted != 0;
   g->hashing = cfg->hashing != 0;
   g->lf = lf;
+  g->lf_in = cfg->in_load_factor == 0.0f ? lf : cfg->in_load_factor;
   g->reverse = cfg->reverse != 0;
   g->out.dev.seed = (uint32_t)(cfg->hash_seed ^ (cfg->hash_seed >> 32)) ^ 0x5bd1e995u;
   g->in.dev.seed = g->out.dev.seed ^ 0x27d4eb2fu;

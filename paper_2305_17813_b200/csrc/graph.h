@@ -83,6 +83,7 @@ struct meerkat_graph {
   uint32_t ws = 1, rank = 0;        // vertex partition (owner(v) = pm_mix(v) % ws, internal.cuh)
   bool weighted = false, hashing = true, reverse = false;
   float lf = 0.7f;
+  float lf_in = 0.7f;               // load factor of the in-edge mirror
   mk::Store out;                    // out-edge store (the paper's SlabGraph)
   mk::Store in;                     // in-edge mirror (reverse store), only when reverse
   uint64_t version = 0;

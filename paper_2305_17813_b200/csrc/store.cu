@@ -765,7 +765,7 @@ cudaError_t launch_build(meerkat_graph* g, Store& st, const uint32_t* d_hints, u
     const unsigned gb = (unsigned)std::min<uint64_t>((V + 255) / 256, (uint64_t)g->sm_count * 16);
     unsigned long long* total = reinterpret_cast<unsigned long long*>(first + V + 1);
     CK(cudaMemsetAsync(total, 0, 16, g->stream));
-    k_bucket_counts<<<gb, 256, 0, g->stream>>>(d_hints, V, (double)g->lf * cap, g->hashing ? 1 : 0, (uint32_t)cap,
+    k_bucket_counts<<<gb, 256, 0, g->stream>>>(d_hints, V, (double)(&st == &g->in ? g->lf_in : g->lf) * cap, g->hashing ? 1 : 0, (uint32_t)cap,
                                                count, heads, total);
     g->launches++;
     CK(cudaGetLastError());

@@ -68,7 +68,8 @@ class Graph:
     def __init__(self, vertex_n: int, weighted: bool = True, hashing: bool = True, load_factor: float = 0.7,
                  degree_hints=None, pool_slabs: int = 0, hash_seed: int = 0, device: int = 0, stream=None,
                  reverse: bool = False, in_degree_hints=None, world_size: int = 1, rank: int = 0,
-                 update_tracking: bool = False, nccl_id=None, exchange=None, exchange_pairs: int = 0):
+                 update_tracking: bool = False, nccl_id=None, exchange=None, exchange_pairs: int = 0,
+                 in_load_factor: float = 0.0):
         """world_size / rank with nccl_id (a 128-byte ctypes buffer) or exchange (a
         _lib.EXCHANGE_FN) make a partitioned graph (see dist.DistGraph); every call is then collective."""
         L = _lib.lib()
@@ -81,7 +82,8 @@ class Graph:
                           update_tracking=int(update_tracking),
                           nccl_id=ctypes.cast(nccl_id, ctypes.c_void_p) if nccl_id is not None else None,
                           exchange=ctypes.cast(exchange, ctypes.c_void_p) if exchange is not None else None,
-                          exchange_ctx=None, exchange_pairs=int(exchange_pairs))
+                          exchange_ctx=None, exchange_pairs=int(exchange_pairs),
+                          in_load_factor=float(in_load_factor))
         self._exchange_keep = exchange
         h = ctypes.c_void_p()
         check(L.meerkat_create(ctypes.byref(cfg), ctypes.byref(h)), "meerkat_create")
