@@ -99,7 +99,7 @@ __device__ __forceinline__ bool fetch_item(const GraphDev& S, const uint64_t* fr
 // SPROBE (static calls): stamp[x] is read beside the node[x] probe, and an improved x already
 // enqueued for the next round skips the stamp exchange -- static rounds improve a vertex many times
 // per round (measured: static SSSP 19.6 -> 14.1 ms); the dynamic calls measured slower with it.
-template <bool MAP, int VISIT, bool V32 = false, bool BLOCK = false, bool SPROBE = false>
+template <bool MAP, int VISIT, bool V32 = false, bool BLOCK = false, bool SPROBE = false, bool DECF = false>
 __device__ __forceinline__ void expand(const TreeArgs& A, const TreeDev& T, int k, const uint64_t* fr, uint64_t n,
                                        uint64_t* fnext, unsigned long long* sznext, uint32_t epoch_next,
                                        Counters& c, int diag_round = DIAG_PULL) {
@@ -170,6 +170,16 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const TreeDev& T, int 
           if (dist >= INF_DIST) { c.err |= ERR_OVERFLOW; live[kk] = false; }   // C5
           cand[kk] = (dist << 32) | v;
         }
+      }
+      if constexpr (DECF) {
+        // decremental relax rounds: only an invalid x can improve (a valid x keeps its optimal distance,
+        // and d(v) + w >= the old d(v) + w >= d(x) with the same tie-break), so the node[x] probe -- a
+        // random DRAM load -- is issued only for keys in V_invalid (the bit set is L2-resident)
+        uint32_t bw[NK];
+#pragma unroll
+        for (int kk = 0; kk < NK; kk++) bw[kk] = live[kk] ? __ldcg(T.inval_bits + (xs[kk] >> 5)) : 0u;
+#pragma unroll
+        for (int kk = 0; kk < NK; kk++) live[kk] = live[kk] && ((bw[kk] >> (xs[kk] & 31)) & 1u);
       }
       if constexpr (V32) {   // distance only: compare and store the high half
 #pragma unroll
@@ -347,7 +357,7 @@ __device__ __forceinline__ void expand(const TreeArgs& A, const TreeDev& T, int 
 // fr[r&1] / size[r%3] of each tree and writes fr[(r+1)&1] / size[(r+1)%3]; size[(r+2)%3]
 // (consumed two rounds ago) is zeroed during round r so it is clean when it becomes "next".
 // The trees share the grid barrier of every round.
-template <bool MAP, int VISIT, bool V32 = false, bool SPROBE = false>
+template <bool MAP, int VISIT, bool V32 = false, bool SPROBE = false, bool DECF = false>
 __device__ __forceinline__ uint32_t run_rounds(const TreeArgs& A, const uint32_t* epoch, cg::grid_group& grid,
                                                uint32_t r, Counters& c) {
   __shared__ unsigned long long s_n[MAX_TREES];
@@ -383,7 +393,7 @@ __device__ __forceinline__ uint32_t run_rounds(const TreeArgs& A, const uint32_t
           for (int k = 0; k < MAX_TREES; k++) {
             if (!n[k]) continue;
             const TreeDev& T = A.T[k];
-            expand<MAP, VISIT, V32, true, SPROBE>(A, T, k, T.fr[r & 1], n[k], T.fr[(r + 1) & 1],
+            expand<MAP, VISIT, V32, true, SPROBE, DECF>(A, T, k, T.fr[r & 1], n[k], T.fr[(r + 1) & 1],
                                           &T.ctrl->size[(r + 1) % 3], epoch[k] + r + 1, c);
           }
           __syncthreads();   // block-wide visibility of this round's frontier and node updates
@@ -419,7 +429,7 @@ __device__ __forceinline__ uint32_t run_rounds(const TreeArgs& A, const uint32_t
     for (int k = 0; k < MAX_TREES; k++) {
       if (!n[k]) continue;
       const TreeDev& T = A.T[k];
-      expand<MAP, VISIT, V32, false, SPROBE>(A, T, k, T.fr[r & 1], n[k], T.fr[(r + 1) & 1], &T.ctrl->size[(r + 1) % 3],
+      expand<MAP, VISIT, V32, false, SPROBE, DECF>(A, T, k, T.fr[r & 1], n[k], T.fr[(r + 1) & 1], &T.ctrl->size[(r + 1) % 3],
                               epoch[k] + r + 1, c, (VISIT == PROPAGATE ? 0 : 20) + (int)r);
     }
     grid.sync();
@@ -748,7 +758,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, TREE_MINB) k_tree_dec(const __grid
   grid.sync();
   timeline(A.T[0].ctrl);
   // (iv) common epilogue
-  const uint32_t r2 = run_rounds<MAP, RELAX>(A, epoch, grid, r1, c);
+  const uint32_t r2 = run_rounds<MAP, RELAX, false, false, DEC_FILTER>(A, epoch, grid, r1, c);
   // clear the invalid bit sets for the next call (the lists are kept for meerkat_tree_invalidated)
   FOR_TREES(k, A)
     for (uint64_t i = tid; i < n_inv[k]; i += nt) {

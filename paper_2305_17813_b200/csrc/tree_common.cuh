@@ -49,6 +49,10 @@ constexpr int PREFETCH = MEERKAT_PREFETCH;
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" :: "l"(p));
 }
+#ifndef MEERKAT_DEC_FILTER
+#define MEERKAT_DEC_FILTER 1
+#endif
+constexpr bool DEC_FILTER = MEERKAT_DEC_FILTER != 0;   // decremental relax rounds probe only x in V_invalid
 #ifndef MEERKAT_STAT_SLOTS
 #define MEERKAT_STAT_SLOTS 1
 #endif
