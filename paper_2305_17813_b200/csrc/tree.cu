@@ -376,11 +376,7 @@ __device__ __forceinline__ uint32_t run_rounds(const TreeArgs& A, const uint32_t
       any |= n[k] != 0;
     }
     if (!any) break;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {   // diagnostics: this round's size beside its timeline entry
-      TreeCtrl* tc = A.T[0].ctrl;
-      const unsigned long long i = tc->nts;
-      if (i > 0 && i <= 48) tc->titems[i - 1] = n[0] + n[1];
-    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) timeline_items(A.T[0].ctrl, n[0] + n[1]);   // diagnostics
     if (n[0] + n[1] <= TAIL_ITEMS) {
       // Tail: a frontier this small is one chain per item for block 0's groups alone, so block 0
       // runs the rounds with block barriers (~0.1 us) instead of grid barriers (~2 us) while the
@@ -405,11 +401,7 @@ __device__ __forceinline__ uint32_t run_rounds(const TreeArgs& A, const uint32_t
           any = false;
 #pragma unroll
           for (int k = 0; k < MAX_TREES; k++) { n[k] = s_n[k]; any |= n[k] != 0; }
-          if (threadIdx.x == 0) {
-            TreeCtrl* tc = A.T[0].ctrl;
-            const unsigned long long i = tc->nts;
-            if (any && i > 0 && i <= 48) tc->titems[i - 1] = n[0] + n[1];
-          }
+          if (threadIdx.x == 0 && any) timeline_items(A.T[0].ctrl, n[0] + n[1]);
           __syncthreads();   // s_n is rewritten by the next iteration / the resumed loop
           if (!any || n[0] + n[1] > TAIL_ITEMS) break;
         }
@@ -494,7 +486,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, 2) k_tree_static(const __grid_cons
   const TreeDev& T = A.T[0];
   uint32_t epoch[MAX_TREES];
   load_epochs(A, epoch);
-  timeline(T.ctrl);
+  timeline_begin(T.ctrl);
   cg::grid_group grid = cg::this_grid();
   Counters c;
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
@@ -522,7 +514,7 @@ template <bool MAP>
 __global__ void __launch_bounds__(TREE_BLOCK, TREE_MINB) k_tree_inc(const __grid_constant__ TreeArgs A) {
   uint32_t epoch[MAX_TREES];
   load_epochs(A, epoch);
-  timeline(A.T[0].ctrl);
+  timeline_begin(A.T[0].ctrl);
   cg::grid_group grid = cg::this_grid();
   Counters c;
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
@@ -690,7 +682,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, TREE_MINB) k_tree_dec(const __grid
   extern __shared__ uint32_t filt[];
   uint32_t epoch[MAX_TREES];
   load_epochs(A, epoch);
-  timeline(A.T[0].ctrl);
+  timeline_begin(A.T[0].ctrl);
   cg::grid_group grid = cg::this_grid();
   Counters c;
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;

@@ -117,14 +117,31 @@ __device__ __forceinline__ bool bit_test(const uint32_t* bits, uint32_t x) {
   return (__ldcg(bits + (x >> 5)) >> (x & 31)) & 1u;
 }
 
-__device__ __forceinline__ void timeline(TreeCtrl* tc) {   // block 0 / thread 0 only
+// Device timeline (block 0 / thread 0): %globaltimer after the kernel start and every grid barrier.
+// The entry count lives in a register-like shared word of block 0 (timeline_nts) -- reading it back
+// from global memory put an L2 round trip on block 0's critical path after every barrier.
+__device__ __forceinline__ unsigned int& timeline_nts() {
+  __shared__ unsigned int s_nts;
+  return s_nts;
+}
+__device__ __forceinline__ void timeline_at(TreeCtrl* tc, bool begin) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    const unsigned long long i = tc->nts;
+    unsigned int& n = timeline_nts();
+    if (begin) n = 0;
+    const unsigned int i = n;
     if (i < 48) tc->tstamp[i] = t;
-    tc->nts = i + 1;
+    n = i + 1;
+    tc->nts = i + 1;   // store only (read back by meerkat_tree_timeline)
   }
+}
+__device__ __forceinline__ void timeline(TreeCtrl* tc) { timeline_at(tc, false); }
+__device__ __forceinline__ void timeline_begin(TreeCtrl* tc) { timeline_at(tc, true); }
+// this round's frontier size beside the timeline entry that opened it (block 0 / thread 0)
+__device__ __forceinline__ void timeline_items(TreeCtrl* tc, unsigned long long items) {
+  const unsigned int i = timeline_nts();
+  if (i > 0 && i <= 48) tc->titems[i - 1] = items;
 }
 
 // warpenqueuefrontier: all 32 lanes call; lanes with `has` append
