@@ -56,7 +56,11 @@ enum PartMode : uint32_t {
 };
 constexpr uint64_t HDR = 4;           // header messages (64 B) at the start of every exchange block
 constexpr uint32_t FLAG_RING = 64;    // per-unit mode words in mapped host memory
-constexpr uint32_t PIPE = 4;          // units in flight before the host reads one's mode word
+constexpr uint32_t MAX_PIPE = 8;      // event ring: units in flight before the host reads one's mode word
+#ifndef MEERKAT_PART_PIPE
+#define MEERKAT_PART_PIPE 2
+#endif
+constexpr uint32_t PIPE = MEERKAT_PART_PIPE;   // <= MAX_PIPE; PIPE - 1 no-op units run past the last
 constexpr uint64_t MAX_UNITS = 1ull << 22;
 constexpr uint64_t DEFAULT_CAP = 16384;
 constexpr int STATIC_CAP_MULT = 16;
@@ -964,7 +968,7 @@ struct PartState {
   uint32_t* dflags = nullptr;
   uint64_t units = 0;
   bool dirty = false;
-  cudaEvent_t ev[2 * PIPE] = {};
+  cudaEvent_t ev[2 * MAX_PIPE] = {};
   int bps = 0;
   // routing
   uint4* rsend = nullptr; uint64_t rsend_cap = 0;   // rows
@@ -1136,7 +1140,7 @@ meerkat_status part_init(meerkat_graph* g, const meerkat_config* cfg) {
   if (e == cudaSuccess) e = cudaMallocHost(&ps->hscr, SCR_WORDS * 8);
   if (e == cudaSuccess) { ps->dcoll_bytes = COLL_WORDS * 8 * 2; e = cudaMalloc(&ps->dcoll, ps->dcoll_bytes); }
   if (e == cudaSuccess) e = cudaMallocHost(&ps->hcoll, COLL_WORDS * 8);
-  for (uint32_t i = 0; i < 2 * PIPE && e == cudaSuccess; i++) e = cudaEventCreateWithFlags(&ps->ev[i], cudaEventDisableTiming);
+  for (uint32_t i = 0; i < 2 * MAX_PIPE && e == cudaSuccess; i++) e = cudaEventCreateWithFlags(&ps->ev[i], cudaEventDisableTiming);
   if (e == cudaSuccess) {
     std::memset(ps->hflags, 0, FLAG_RING * 4);
     auto fn = g->weighted ? (const void*)k_part_unit<true> : (const void*)k_part_unit<false>;
@@ -1170,7 +1174,7 @@ void part_free(meerkat_graph* g) {
   if (ps->hcoll) cudaFreeHost(ps->hcoll);
   if (ps->hsend) cudaFreeHost(ps->hsend);
   if (ps->hrecv) cudaFreeHost(ps->hrecv);
-  for (uint32_t i = 0; i < 2 * PIPE; i++) if (ps->ev[i]) cudaEventDestroy(ps->ev[i]);
+  for (uint32_t i = 0; i < 2 * MAX_PIPE; i++) if (ps->ev[i]) cudaEventDestroy(ps->ev[i]);
   delete ps;
   g->part = nullptr;
 }
@@ -1514,10 +1518,10 @@ static meerkat_status run_units(meerkat_graph* g, PArgs A, meerkat_tree* const* 
     }
     st = xchg(g, A.send, sb, so, A.recv, sb, so);
     if (st != MEERKAT_OK) return st;
-    if (cudaEventRecord(ps->ev[u % (2 * PIPE)], g->stream) != cudaSuccess) return MEERKAT_E_CUDA;
+    if (cudaEventRecord(ps->ev[u % (2 * MAX_PIPE)], g->stream) != cudaSuccess) return MEERKAT_E_CUDA;
     if (u + 1 < PIPE) continue;
     const uint64_t v = u + 1 - PIPE;   // the unit whose mode decides
-    cudaEvent_t ev = ps->ev[v % (2 * PIPE)];
+    cudaEvent_t ev = ps->ev[v % (2 * MAX_PIPE)];
     for (;;) {
       const cudaError_t q = cudaEventQuery(ev);
       if (q == cudaSuccess) break;
