@@ -85,3 +85,28 @@ def test_product_package_does_not_import_oracle():
     for f in os.listdir(os.path.join(ROOT, "paper_2305_17813_b200")):
         if f.endswith(".py"):
             assert "import oracle" not in open(os.path.join(ROOT, "paper_2305_17813_b200", f)).read()
+
+
+def test_ctypes_structs_match_the_header(tmp_path):
+    """Every ctypes Structure of the binding has the C layout of include/meerkat.h: a C program built
+    from the header prints sizeof / offsetof of each field, compared field by field."""
+    import subprocess
+    from paper_2305_17813_b200 import _lib
+    structs = {"meerkat_config": _lib.Config, "meerkat_stats": _lib.Stats, "meerkat_tree_stats": _lib.TreeStats,
+               "meerkat_pagerank_stats": _lib.PageRankStats, "meerkat_latency": _lib.Latency}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "meerkat.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'  printf("{cname} size %zu\\n", sizeof({cname}));')
+        for f, _t in py._fields_:
+            lines.append(f'  printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines) + "\n")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
+    got = {tuple(l.split()[:2]): int(l.split()[2]) for l in out if l.strip()}
+    for cname, py in structs.items():
+        assert got[(cname, "size")] == ctypes.sizeof(py), cname
+        for f, _t in py._fields_:
+            assert got[(cname, f)] == getattr(py, f).offset, (cname, f)
