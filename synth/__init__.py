@@ -147,6 +147,35 @@ def rmat_dynamic(scale: int, ef: int, batch: int, n_ins: int, n_del: int, seed_g
     return DynamicWorkload(1 << scale, base, inserts, deletes, src)
 
 
+def grid_dynamic(side: int, batch: int, n_ins: int, n_del: int, seed_w=SEED_W,
+                 seed_batch=SEED_BATCH) -> DynamicWorkload:
+    """The road-like stress case of SURVEY §8(d) ("not in BJ"): a side x side grid, vertex r*side + c,
+    directed edges to the 4 neighbours, w ~ U{1..64} (seeded), source 0 (a corner).  Diameter ~2*side,
+    so SSSP / BFS take thousands of rounds and decremental batches invalidate deep subtrees (the
+    paper's USAfull regime).  Held-out inserts / sampled deletes as rmat_dynamic."""
+    r, c = np.divmod(np.arange(side * side, dtype=np.int64), side)
+    v = r * side + c
+    srcs, dsts = [], []
+    for dr, dc in ((0, 1), (0, -1), (1, 0), (-1, 0)):
+        ok = (r + dr >= 0) & (r + dr < side) & (c + dc >= 0) & (c + dc < side)
+        srcs.append(v[ok])
+        dsts.append(((r + dr) * side + (c + dc))[ok])
+    s = np.concatenate(srcs).astype(np.uint32)
+    d = np.concatenate(dsts).astype(np.uint32)
+    o = np.lexsort((d, s))
+    s, d = s[o], d[o]
+    w = np.random.Generator(np.random.PCG64(seed_w)).integers(1, 65, s.size).astype(np.uint32)
+    m = s.size
+    pick = sample_distinct(m, batch * (n_ins + n_del), seed_batch)
+    held, dels = pick[: batch * n_ins], pick[batch * n_ins:]
+    keep = np.ones(m, bool)
+    keep[held] = False
+    cut = lambda idx, i: (s[idx[i * batch:(i + 1) * batch]], d[idx[i * batch:(i + 1) * batch]],
+                          w[idx[i * batch:(i + 1) * batch]])
+    return DynamicWorkload(side * side, (s[keep], d[keep], w[keep]), [cut(held, i) for i in range(n_ins)],
+                           [cut(dels, i) for i in range(n_del)], 0)
+
+
 def degrees(src: np.ndarray, vertex_n: int) -> np.ndarray:
     """Out-degree of each vertex in an edge list (degree hints for construction)."""
     return np.bincount(src, minlength=vertex_n).astype(np.uint32)

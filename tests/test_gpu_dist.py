@@ -36,7 +36,10 @@ def _worker(rank, ws, port, backend, scale, reverse, pairs, q, units=False):
         import oracle
         import synth
         from paper_2305_17813_b200.dist import DistGraph
-        W = synth.rmat_dynamic(scale, 16, batch=500, n_ins=2, n_del=2)
+        if isinstance(scale, str):   # "grid<side>": the road-like stress case (deep trees, many units)
+            W = synth.grid_dynamic(int(scale[4:]), 500, 2, 2)
+        else:
+            W = synth.rmat_dynamic(scale, 16, batch=500, n_ins=2, n_del=2)
         V, src = W.vertex_n, W.source
         bs, bd, bw = W.base
         # each rank brings a different slice of every batch (the library routes them)
@@ -130,7 +133,7 @@ def _worker(rank, ws, port, backend, scale, reverse, pairs, q, units=False):
 @pytest.mark.parametrize("ws,backend,scale,reverse,pairs", [
     (1, "nccl", 12, False, 0), (1, "nccl", 12, True, 0), (2, "gloo", 12, False, 0), (2, "gloo", 12, True, 0),
     (3, "gloo", 13, True, 0), (4, "gloo", 12, False, 0), (4, "gloo", 12, True, 64), (8, "gloo", 12, True, 0),
-    (8, "gloo", 12, False, 32)])
+    (8, "gloo", 12, False, 32), (3, "gloo", "grid64", True, 0), (2, "gloo", "grid64", False, 0)])
 def test_partitioned_dynamic_sssp_bfs(ws, backend, scale, reverse, pairs):
     _run(ws, backend, scale, reverse, pairs)
 

@@ -431,3 +431,46 @@ def test_seed_contract():
     g.delete_trees([t, b], s, d); o.delete(*W.inserts[2][:2])
     assert_nodes(t.nodes(), o.sssp(src)[1], "batch_trees after recompute")
     assert_nodes(b.nodes(), o.bfs(src)[1], "batch_trees after recompute (bfs)")
+
+
+@pytest.mark.parametrize("reverse", [True, False])
+def test_road_like_grid_deep_trees(reverse):
+    """SURVEY §8(d)'s road-like stress case (the paper's USAfull regime): a 192 x 192 grid,
+    diameter ~380, so the static and dynamic calls run hundreds of frontier rounds (rotating frontier
+    slots, stamp epochs, block-0 tail rounds) and deletions invalidate deep subtrees.  The bench's
+    sequence (seeded insert / delete + fused trees), then per-tree calls; every node vs the oracle, with
+    the invalidated sets, direct and frontier counts of the fused decremental calls."""
+    W = synth.grid_dynamic(192, 600, 2, 3)
+    V, src = W.vertex_n, W.source
+    bs, bd, bw = W.base
+    g = G(V, weighted=True, degree_hints=synth.degrees(bs, V), reverse=reverse,
+          in_degree_hints=synth.degrees(bd, V), load_factor=0.5)
+    o = oracle.OracleGraph(V)
+    g.insert(cuda(bs), cuda(bd), cuda(bw)); o.insert(bs, bd, bw)
+    t, b = g.sssp(src), g.bfs(src)
+    assert_nodes(t.nodes(), o.sssp(src)[1], "grid static sssp")
+    assert_nodes(b.nodes(), o.bfs(src)[1], "grid static bfs")
+    assert t.stats()["rounds"] > 200
+    for (s, d, w) in W.inserts:
+        o.insert(s, d, w)
+        g.insert_trees([t, b], cuda(s), cuda(d), cuda(w))
+        assert_nodes(t.nodes(), o.sssp(src)[1], "grid inc sssp")
+        assert_nodes(b.nodes(), o.bfs(src)[1], "grid inc bfs")
+    for i, (s, d, _w) in enumerate(W.deletes):
+        old_s, old_b = o.sssp(src)[1], o.bfs(src)[1]
+        o.delete(s, d)
+        if i < 2:
+            g.delete_trees([t, b], cuda(s), cuda(d))
+            for tree, old in ((t, old_s), (b, old_b)):
+                flag, nd = oracle.invalidated(V, src, old, s, d)
+                st = tree.stats()
+                assert tree.invalidated().tolist() == np.nonzero(flag)[0].tolist()
+                assert st["direct_invalid"] == nd
+                assert st["frontier_edges"] == o.dec_frontier_count(old, flag)
+        else:
+            g.delete(cuda(s), cuda(d))
+            t.decremental(cuda(s), cuda(d))
+            b.decremental(cuda(s), cuda(d))
+        assert_nodes(t.nodes(), o.sssp(src)[1], "grid dec sssp")
+        assert_nodes(b.nodes(), o.bfs(src)[1], "grid dec bfs")
+    assert t.stats()["invalidated"] > 0
