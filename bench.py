@@ -871,8 +871,13 @@ def run_ours(args, ws, rank, local):
         sp.recompute(); bf.recompute()
         g.sync()
         cs = torch.cuda.Stream(dev)
-        slots = [([torch.empty(n, dtype=torch.int32, device=dev) for _ in range(3)],
-                  [torch.empty(n, dtype=torch.int32, device=dev) for _ in range(2)]) for _ in range(2)]
+        # one pinned buffer per step holding the step's five arrays (insert src, dst, w; delete src, dst)
+        # and one device slot per parity: ONE copy per step (five separate copies cost more host time
+        # than the device spends on a step when the host is slow)
+        hb = [torch.cat([*hi[k], *hd[k]]).pin_memory() for k in range(K)]
+        dbuf = [torch.empty(5 * n, dtype=torch.int32, device=dev) for _ in range(2)]
+        slots = [([dbuf[i][j * n:(j + 1) * n] for j in range(3)], [dbuf[i][j * n:(j + 1) * n] for j in (3, 4)])
+                 for i in range(2)]
         ready = [torch.cuda.Event() for _ in range(2)]
         freed = [torch.cuda.Event() for _ in range(2)]
         ctr = torch.zeros((K, 3), dtype=torch.int64).pin_memory()
@@ -882,10 +887,7 @@ def run_ours(args, ws, rank, local):
             with torch.cuda.stream(cs):
                 if k >= 2:
                     cs.wait_event(freed[sl])   # step k - 2 is done with this slot
-                for dst, src in zip(slots[sl][0], hi[k]):
-                    dst.copy_(src, non_blocking=True)
-                for dst, src in zip(slots[sl][1], hd[k]):
-                    dst.copy_(src, non_blocking=True)
+                dbuf[sl].copy_(hb[k], non_blocking=True)
                 ready[sl].record(cs)
         torch.cuda.synchronize()
         barrier(ws)
@@ -922,8 +924,8 @@ def run_ours(args, ws, rank, local):
                "d2h_bytes_per_step": 3 * 8,             # the cumulative counters after the step
                "ms_per_step": p_ms / K,
                "how": "the K steps back to back through the public API (Graph on CUDA tensors): each step's "
-                      "batches copied from pinned host memory on a copy stream while the previous step "
-                      "computes (two device slots, events), each step's counters copied back with "
+                      "batches copied from pinned host memory (one buffer per step) on a copy stream while the "
+                      "previous step computes (two device slots, events), each step's counters copied back with "
                       "meerkat_counters_async; one synchronisation at the end; no L2 flush (store > L2)",
                "result_check": {"live_edges_after_last_step": live[-1], "stats_edges": st_end["edges"],
                                 "ok": live[-1] == st_end["edges"]},
