@@ -305,6 +305,10 @@ meerkat_status meerkat_tree_destroy(meerkat_tree* t);
  *   - meerkat_export_edges / meerkat_stats_get / meerkat_tree_stats_get: this rank's part (local).
  * PageRank, WCC, triangle counting, vanilla trees, seeded calls and distances are single-GPU only
  * (MEERKAT_E_STATE / MEERKAT_E_INVALID_ARG).  Results are bit-identical to world_size 1.
+ * Errors: argument / ordering-contract errors are detected identically on every rank (MEERKAT_E_STATE
+ * everywhere when any rank passed another batch; no tree is touched); data errors of a tree call
+ * (capacity, overflow) are OR-ed over ranks.  A MEERKAT_E_NCCL or MEERKAT_E_CUDA from a collective
+ * call can leave the ranks out of step: destroy the graph on every rank.
  * ------------------------------------------------------------------------------------------- */
 #define MEERKAT_MAX_RANKS 64
 

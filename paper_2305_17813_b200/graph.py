@@ -25,6 +25,24 @@ def _is_torch(x):
     return torch is not None and isinstance(x, torch.Tensor)
 
 
+_I32 = torch.int32 if torch is not None else None
+
+
+def _handles(trees):
+    """ctypes array of tree handles (cached per tuple of trees: the hot path passes the same list)."""
+    key = tuple(id(t) for t in trees)
+    arr = _HANDLES.get(key)
+    if arr is None or [a for a in arr] != [t._h.value for t in trees]:
+        arr = (ctypes.c_void_p * len(trees))(*[t._h.value for t in trees])
+        if len(_HANDLES) > 64:
+            _HANDLES.clear()
+        _HANDLES[key] = arr
+    return arr
+
+
+_HANDLES = {}
+
+
 def _u32(x, stream=None):
     """(pointer, keepalive, n) for a 32-bit id/weight array.  A CUDA tensor that has to be converted
     (dtype or layout) becomes a temporary allocated on torch's current stream; the library reads it
@@ -32,6 +50,8 @@ def _u32(x, stream=None):
     allocator does not hand its block out again before the library's work there is done."""
     if x is None:
         return None, None, 0
+    if _is_torch(x) and x.dtype is _I32 and x.is_contiguous():   # fast path: nothing to convert
+        return ctypes.c_void_p(x.data_ptr()), x, x.numel()
     if _is_torch(x):
         y = x
         if y.dtype not in (torch.int32, torch.uint32):
@@ -142,7 +162,7 @@ class Graph:
         out = ctypes.c_uint64(0)
         ob = ctypes.byref(out) if count else None
         if seed:
-            arr = (ctypes.c_void_p * len(seed))(*[t._h.value for t in seed])
+            arr = _handles(seed)
             st, fn = _lib.lib().meerkat_insert_batch_trees(self._h, sp, dp, wp, n, arr, len(seed), ob), \
                 "meerkat_insert_batch_trees"
         else:
@@ -160,7 +180,7 @@ class Graph:
         out = ctypes.c_uint64(0)
         ob = ctypes.byref(out) if count else None
         if seed:
-            arr = (ctypes.c_void_p * len(seed))(*[t._h.value for t in seed])
+            arr = _handles(seed)
             st, fn = _lib.lib().meerkat_delete_batch_trees(self._h, sp, dp, n, arr, len(seed), ob), \
                 "meerkat_delete_batch_trees"
         else:
@@ -228,7 +248,7 @@ class Graph:
         sp, ks, n = _u32(src, self._tstream)
         dp, kd, _ = _u32(dst, self._tstream)
         wp, kw, _ = _u32(w, self._tstream)
-        arr = (ctypes.c_void_p * len(trees))(*[t._h.value for t in trees])
+        arr = _handles(trees)
         check(_lib.lib().meerkat_trees_incremental(self._h, arr, len(trees), sp, dp, wp, n),
               "meerkat_trees_incremental")
 
@@ -236,7 +256,7 @@ class Graph:
         """Fused decremental update of several trees with the batch just deleted (one launch)."""
         sp, ks, n = _u32(src, self._tstream)
         dp, kd, _ = _u32(dst, self._tstream)
-        arr = (ctypes.c_void_p * len(trees))(*[t._h.value for t in trees])
+        arr = _handles(trees)
         check(_lib.lib().meerkat_trees_decremental(self._h, arr, len(trees), sp, dp, n), "meerkat_trees_decremental")
 
     def insert_trees(self, trees, src, dst, w=None, count: bool = True):
