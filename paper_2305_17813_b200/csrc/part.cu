@@ -102,6 +102,7 @@ struct PArgs {
   uint32_t fn_bad;               // the batch size differs from the mutation's
   uint32_t seed_mode;            // PM_SEED_INC / PM_SEED_DEC after a good verdict
   uint32_t chain;                // one rank: chain the phases in one launch (0: one unit per phase, as P > 1)
+  uint32_t self_send;            // the own block goes to send (exchanged through NCCL) instead of recv
 };
 
 // A message: x = target row at the destination, y = tag (kind << 1 | tree), z/w = payload lo/hi.
@@ -743,7 +744,7 @@ __global__ void __launch_bounds__(TREE_BLOCK, TREE_MINB) k_part_unit(const __gri
   for (uint32_t p = 0; p < ws; p++) {
     const unsigned long long t = __ldcg(&pc->tail[p]), h = s_head[p];
     const unsigned long long m = min((unsigned long long)A.cap, t - h);
-    uint4* dst = (p == G.rank ? A.recv : A.send) + (uint64_t)p * A.blk + HDR;
+    uint4* dst = (p == G.rank && !A.self_send ? A.recv : A.send) + (uint64_t)p * A.blk + HDR;
     const uint4* ring = A.q + (uint64_t)p * A.q_cap;
     for (uint64_t j = tid; j < m; j += nt) dst[j] = ring[(h + j) % A.q_cap];
   }
@@ -751,7 +752,8 @@ __global__ void __launch_bounds__(TREE_BLOCK, TREE_MINB) k_part_unit(const __gri
     for (uint32_t p = 0; p < ws; p++) {
       const unsigned long long t = __ldcg(&pc->tail[p]), h = s_head[p];
       const unsigned long long m = min((unsigned long long)A.cap, t - h);
-      unsigned long long* hd = reinterpret_cast<unsigned long long*>((p == G.rank ? A.recv : A.send) + (uint64_t)p * A.blk);
+      unsigned long long* hd =
+          reinterpret_cast<unsigned long long*>((p == G.rank && !A.self_send ? A.recv : A.send) + (uint64_t)p * A.blk);
       hd[0] = m; hd[1] = sent; hd[2] = pend; hd[3] = mode; hd[4] = verdict;
       pc->head[hpar ^ 1][p] = h + m;
     }
@@ -1027,6 +1029,14 @@ static cudaError_t ensure_host(PartState* ps, size_t bytes) {
 // All-to-all-v of device buffers: segment p of `send` (sb[p] bytes at offset so[p]) goes to rank p and
 // lands there as segment `rank`; recv segment q (rb[q] bytes at ro[q]) comes from rank q.  NCCL:
 // stream-ordered grouped send/recv.  Host transport: staged through pinned memory (synchronous).
+// MEERKAT_PART_NCCL_SELF=1 (tests): a rank's own segments and unit block also go through ncclSend /
+// ncclRecv to itself, so a one-GPU box drives every NCCL call of the P > 1 path with real data.
+static bool nccl_self() {
+  static int on = -1;
+  if (on < 0) on = std::getenv("MEERKAT_PART_NCCL_SELF") ? 1 : 0;
+  return on == 1;
+}
+
 static bool trace_on() {
   static int on = -1;
   if (on < 0) on = std::getenv("MEERKAT_PART_TRACE") ? 1 : 0;
@@ -1047,14 +1057,15 @@ static meerkat_status xchg(meerkat_graph* g, const void* send, const uint64_t* s
   const char* s8 = static_cast<const char*>(send);
   char* r8 = static_cast<char*>(recv);
   cudaError_t e = cudaSuccess;
-  if (sb[me]) e = cudaMemcpyAsync(r8 + ro[me], s8 + so[me], sb[me], cudaMemcpyDeviceToDevice, g->stream);
+  const bool self_nccl = ps->comm && nccl_self();
+  if (sb[me] && !self_nccl) e = cudaMemcpyAsync(r8 + ro[me], s8 + so[me], sb[me], cudaMemcpyDeviceToDevice, g->stream);
   if (e != cudaSuccess) return MEERKAT_E_CUDA;
-  if (ws == 1) return MEERKAT_OK;
+  if (ws == 1 && !self_nccl) return MEERKAT_OK;
   if (ps->comm) {
     NcclApi* api = nccl_api();
     bool ok = api->GroupStart() == ncclSuccess;
     for (uint32_t p = 0; p < ws && ok; p++) {
-      if (p == me) continue;
+      if (p == me && !self_nccl) continue;
       if (sb[p]) ok = api->Send(s8 + so[p], sb[p], ncclUint8, (int)p, ps->comm, g->stream) == ncclSuccess;
       if (ok && rb[p]) ok = api->Recv(r8 + ro[p], rb[p], ncclUint8, (int)p, ps->comm, g->stream) == ncclSuccess;
     }
@@ -1473,7 +1484,7 @@ static meerkat_status run_units(meerkat_graph* g, PArgs A, meerkat_tree* const* 
   const uint32_t ws = g->ws;
   uint64_t sb[MEERKAT_MAX_RANKS], so[MEERKAT_MAX_RANKS];
   const uint64_t bytes = A.blk * 16;
-  for (uint32_t p = 0; p < ws; p++) { sb[p] = p == g->rank ? 0 : bytes; so[p] = (uint64_t)p * bytes; }
+  for (uint32_t p = 0; p < ws; p++) { sb[p] = p == g->rank && !A.self_send ? 0 : bytes; so[p] = (uint64_t)p * bytes; }
   const uint64_t base = ps->units;
   uint64_t launched = 0;
   meerkat_status st = MEERKAT_OK;
@@ -1608,6 +1619,7 @@ meerkat_status part_trees(meerkat_graph* g, meerkat_tree* const* trees, uint32_t
   // protocol, host pipeline included) so a one-GPU box exercises it
   static const bool force_units = std::getenv("MEERKAT_PART_UNITS") != nullptr;
   A.chain = g->ws == 1 && !force_units ? 1u : 0u;
+  A.self_send = ps->comm && nccl_self() && !A.chain ? 1u : 0u;
   const uint64_t units0 = ps->units;
   meerkat_status st = run_units(g, A, trees, k);
   ps->dirty = st != MEERKAT_OK;

@@ -29,6 +29,8 @@ def _worker(rank, ws, port, backend, scale, reverse, pairs, q, units=False):
     import torch.distributed as dist
     if units:   # one exchange unit per phase at world size 1: the P > 1 protocol and host pipeline
         os.environ["MEERKAT_PART_UNITS"] = "1"
+    if units == "nccl_self":   # ... with the rank's own blocks and segments through ncclSend / ncclRecv
+        os.environ["MEERKAT_PART_NCCL_SELF"] = "1"
     try:
         torch.cuda.set_device(0)
         kw = {"device_id": torch.device("cuda", 0)} if backend == "nccl" else {}
@@ -138,12 +140,14 @@ def test_partitioned_dynamic_sssp_bfs(ws, backend, scale, reverse, pairs):
     _run(ws, backend, scale, reverse, pairs)
 
 
-@pytest.mark.parametrize("reverse", [True, False])
-def test_partitioned_nccl_unit_pipeline(reverse):
+@pytest.mark.parametrize("reverse,self_nccl", [(True, False), (False, False), (True, True)])
+def test_partitioned_nccl_unit_pipeline(reverse, self_nccl):
     """World size 1 through the library's NCCL communicator with one exchange unit per phase
     (MEERKAT_PART_UNITS=1): the pipelined host loop (units launched PIPE ahead, mode words read from
-    mapped memory) and the device-side phase changes of P > 1, on one GPU."""
-    _run(1, "nccl", 12, reverse, 0, units=True)
+    mapped memory) and the device-side phase changes of P > 1, on one GPU; with self_nccl
+    (MEERKAT_PART_NCCL_SELF=1) every own segment and unit block also moves through ncclSend / ncclRecv
+    to the rank itself, so the NCCL calls of the P > 1 path run with real data."""
+    _run(1, "nccl", 12, reverse, 0, units="nccl_self" if self_nccl else True)
 
 
 def _run(ws, backend, scale, reverse, pairs, units=False):
