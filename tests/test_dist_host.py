@@ -104,3 +104,22 @@ def test_owner_map_rejects_bad_args():
         owner_map(10, 2, [10])
     with pytest.raises(_lib.MeerkatError):
         owner_map(10, 0, [1])
+
+
+def test_tree_handle_arrays_cached_and_refreshed():
+    """graph._handles: the ctypes array of tree handles is reused for the same trees and rebuilt when
+    a tree's handle changes (no GPU: plain objects with a ctypes handle)."""
+    import ctypes as C
+    from paper_2305_17813_b200 import graph
+
+    class T:
+        def __init__(self, v):
+            self._h = C.c_void_p(v)
+
+    a, b = T(0x1000), T(0x2000)
+    arr1 = graph._handles([a, b])
+    assert [x for x in arr1] == [0x1000, 0x2000]
+    assert graph._handles([a, b]) is arr1
+    b._h = C.c_void_p(0x3000)   # e.g. the tree was destroyed and its slot reused
+    arr2 = graph._handles([a, b])
+    assert arr2 is not arr1 and [x for x in arr2] == [0x1000, 0x3000]
